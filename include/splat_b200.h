@@ -1,0 +1,154 @@
+/*
+ * splat_b200.h -- C ABI of the B200 (sm_100a) differentiable Gaussian
+ * splatting hot path (libsplat_b200.so).
+ *
+ * The reference (`splatgrad`, pure Python + numpy) exposes this path as
+ * Python functions; there is no reference FFI.  Each entry point below is
+ * the batched, device-side replacement of one reference function and cites
+ * it (paths under /root/reference/pkg/src/splatgrad, "sg/").  The Python
+ * package paper_2312_02121_b200 binds these with ctypes and re-exposes the
+ * reference's own API names on top.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless marked [host].  The library
+ *    never allocates device memory and never synchronizes the device; every
+ *    call is stream-ordered on `stream` and reentrant.
+ *  - Return value: 0 on success, -1 on a launch/argument error whose text is
+ *    available from gs_last_error() (thread-local).
+ *  - Per-element input errors of the reference (ValueError raised by
+ *    sg/core.py:160-163,189-191, sg/projection.py:54-55,108-109) do not abort
+ *    a kernel: they are folded into a device status word with atomicMin of
+ *    ((uint64)index << 8 | code), initialised by the caller to
+ *    GS_STATUS_OK (all ones).  The host wrapper raises ValueError naming the
+ *    first offending Gaussian, as the reference does.
+ *  - Float4 arrays must be 16-byte aligned.
+ */
+#ifndef SPLAT_B200_H
+#define SPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* gs_stream_t;
+
+#define GS_TILE_SIZE 16 /* sg/binning.py:8 TILE_SIZE */
+#define GS_STATUS_OK 0xFFFFFFFFFFFFFFFFull
+
+enum gs_error_code {
+    GS_OK = 0,
+    GS_ERR_SCALE = 1,   /* sg/core.py:189-191 "scale components must be positive" */
+    GS_ERR_QUAT = 2,    /* sg/core.py:160-163 "quaternion norm is too small ..." */
+    GS_ERR_HOMOG = 3,   /* sg/projection.py:54-55 "degenerate projection ..." */
+    GS_ERR_COV2D = 4,   /* sg/projection.py:108-109 "2d covariance must be positive definite" */
+};
+
+/* Pinhole camera, the fields of sg/core.py:59-129 Camera (view row-major,
+ * world->camera).  Passed by host pointer; copied into kernel parameters. */
+typedef struct gs_camera {
+    float view[16];
+    float fx, fy, cx, cy;
+    int32_t width, height;
+    float near_plane, far_plane;
+} gs_camera;
+
+const char* gs_last_error(void);
+int gs_version(void);
+/* Number of SMs of the current device (0 when no device). */
+int gs_device_sm_count(void);
+
+/* ---- Stage 1: projection ------------------------------------------------
+ * Replaces sg/projection.py:115-145 project_gaussian as batched by
+ * sg/raster_forward.py:246-252 _project_scene, plus the conic of
+ * sg/raster_forward.py:86-92 _cov2d_inverse_terms.
+ *   means3 (n,3), scales3 (n,3), quats4 (n,4) (w,x,y,z), opacities (n)
+ * Outputs (n rows, culled rows have tiles_touched = 0 and radius 0):
+ *   out_xydr4     (n,4): mean2d.x, mean2d.y, depth (camera z), radius (int bits)
+ *   out_conic4    (n,4): A, B, C (inverse of cov2d), opacity
+ *   out_tiles     (n)  : number of 16x16 tiles the bbox square touches
+ *   out_cov3      (n,3): cov2d a, b, c (optional, may be NULL)
+ *   status        (1)  : uint64 status word (see above)                     */
+int gs_project_fwd(const float* means3, const float* scales3, const float* quats4,
+                   const float* opacities, int64_t n, const gs_camera* cam /*[host]*/,
+                   float* out_xydr4, float* out_conic4, uint32_t* out_tiles, float* out_cov3,
+                   unsigned long long* status, gs_stream_t stream);
+
+/* ---- Stage 2: tile binning + depth sort ---------------------------------
+ * Together these replace sg/binning.py:27-47 assign_tiles and
+ * sg/binning.py:50-65 sort_bins.
+ * gs_scan_tiles: exclusive scan of tiles_touched -> offsets, total (uint64)
+ * (single-pass decoupled look-back).                                        */
+size_t gs_scan_workspace_bytes(int64_t n);
+int gs_scan_tiles(const uint32_t* tiles, uint32_t* offsets, int64_t n, void* ws, size_t ws_bytes,
+                  unsigned long long* total, gs_stream_t stream);
+
+/* gs_emit_keys: for every visible Gaussian i (in index order) and every tile
+ * (ty, tx) of its rectangle (row-major), writes
+ *   key = (uint64)(ty*tiles_x+tx) << 32 | float_bits(depth), value = i
+ * at offsets[i] + k.  Emission is in Gaussian-index order so a STABLE sort on
+ * the key reproduces the reference's (depth, source_index) tie-break. */
+int gs_emit_keys(const float* xydr4, const uint32_t* offsets, const uint32_t* tiles, int64_t n,
+                 int32_t width, int32_t height, unsigned long long* keys, uint32_t* vals,
+                 gs_stream_t stream);
+
+/* gs_sort_pairs: stable LSD radix sort (8-bit digits, onesweep: one upfront
+ * histogram + one chained-scan scatter per pass) of bits [0, end_bit).
+ * Result lands in (keys, vals) if *selector == 0 else in (keys_alt,
+ * vals_alt); *selector is written on the host, deterministically. */
+size_t gs_sort_workspace_bytes(int64_t n, int end_bit);
+int gs_sort_pairs(unsigned long long* keys, unsigned long long* keys_alt, uint32_t* vals,
+                  uint32_t* vals_alt, int64_t n, int end_bit, void* ws, size_t ws_bytes,
+                  int* selector /*[host]*/, gs_stream_t stream);
+
+/* gs_tile_ranges: per tile [start, end) into the sorted list (uint32 x 2,
+ * zero-filled by the call for empty tiles). */
+int gs_tile_ranges(const unsigned long long* sorted_keys, int64_t n, uint32_t* ranges2,
+                   int32_t n_tiles, gs_stream_t stream);
+
+/* ---- Stage 3: rasterize forward -----------------------------------------
+ * Replaces sg/raster_forward.py:116-154 _composite_tile over the tiles of
+ * sg/raster_forward.py:157-172,222-243.  Outputs HWC image (H,W,3), final_T
+ * (H,W) and n_contrib (H,W) int32 (sg/raster_forward.py:43-55).
+ * counts (optional, may be NULL; uint64[4], accumulated):
+ *   E_f, E_f_sigma, E_f_alpha, E_f_commit                    */
+int gs_raster_fwd(const uint32_t* ranges2, const uint32_t* sorted_vals, const float* xydr4,
+                  const float* conic4, const float* colors3, const float* background3 /*[host]*/,
+                  int32_t width, int32_t height, int early_termination, float* out_image,
+                  float* out_final_T, int32_t* out_n_contrib, unsigned long long* counts,
+                  gs_stream_t stream);
+
+/* ---- Stage 4: rasterize backward ----------------------------------------
+ * Replaces sg/raster_backward.py:47-108 _backward_tile summed as in
+ * sg/raster_backward.py:166-205 accumulate_image_backward.  Accumulates
+ * (atomically; buffers must be zeroed by the caller) per scene Gaussian:
+ *   d_rgbo4 (n,4): d_color r, g, b, d_opacity
+ *   d_geo4  (n,4): d_mean2d x, y, d_cov2d[0][0], d_cov2d[0][1] (= [1][0])
+ *   d_c11   (n)  : d_cov2d[1][1]
+ * counts (optional, uint64[3]): E_b, E_b_sigma, E_b_contrib.               */
+int gs_raster_bwd(const uint32_t* ranges2, const uint32_t* sorted_vals, const float* xydr4,
+                  const float* conic4, const float* colors3, const float* background3 /*[host]*/,
+                  int32_t width, int32_t height, const float* final_T, const int32_t* n_contrib,
+                  const float* d_image, float* d_rgbo4, float* d_geo4, float* d_c11,
+                  unsigned long long* counts, gs_stream_t stream);
+
+/* ---- Stage 5: projection backward ---------------------------------------
+ * Replaces the per-Gaussian loop of sg/proj_backward.py:178-223
+ * scene_backward (mean2d_backward :53-77, cov2d_backward :88-121,
+ * world_backward :124-136, covariance3d_backward :151-175, view rotation
+ * path :218-222).  Rows with tiles == 0 (culled) are written as exact 0.
+ * d_view16 (4x4 row-major) is fully written (not accumulated); the sum over
+ * Gaussians is deterministic (fixed-order block partials in ws).            */
+size_t gs_project_bwd_workspace_bytes(int64_t n);
+int gs_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n,
+                   const gs_camera* cam /*[host]*/, const uint32_t* tiles, const float* d_geo4,
+                   const float* d_c11, float* d_means3, float* d_scales3, float* d_quats4,
+                   float* d_view16, void* ws, size_t ws_bytes, gs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPLAT_B200_H */

@@ -1,0 +1,97 @@
+"""ctypes binding of libsplat_b200.so (the C ABI in include/splat_b200.h).
+
+There is no fallback: if the shared library is missing or cannot be loaded
+the import of the ops fails loudly with instructions to build it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsplat_b200.so")
+
+# Every symbol include/splat_b200.h declares (tests check the export table).
+EXPORTS = (
+    "gs_last_error", "gs_version", "gs_device_sm_count",
+    "gs_project_fwd",
+    "gs_scan_workspace_bytes", "gs_scan_tiles", "gs_emit_keys",
+    "gs_sort_workspace_bytes", "gs_sort_pairs", "gs_tile_ranges",
+    "gs_raster_fwd", "gs_raster_bwd",
+    "gs_project_bwd_workspace_bytes", "gs_project_bwd",
+)
+
+ERR_MESSAGES = {  # include/splat_b200.h gs_error_code -> the reference's ValueError text
+    1: "scale components must be positive",                      # sg/core.py:189-191
+    2: "quaternion norm is too small to define an orientation",  # sg/core.py:160-163
+    3: "degenerate projection: homogeneous component is ~0",     # sg/projection.py:54-55
+    4: "2d covariance must be positive definite",                # sg/projection.py:108-109
+}
+
+
+class GsCamera(C.Structure):
+    _fields_ = [("view", C.c_float * 16), ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float),
+                ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
+                ("near_plane", C.c_float), ("far_plane", C.c_float)]
+
+
+class SplatLibError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load():
+    """Load and type the library (raises if it is not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise SplatLibError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2312_02121_b200.build` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    P, i64, i32, sz = C.c_void_p, C.c_int64, C.c_int32, C.c_size_t
+    cam = C.POINTER(GsCamera)
+    sig = {
+        "gs_last_error": ([], C.c_char_p),
+        "gs_version": ([], C.c_int),
+        "gs_device_sm_count": ([], C.c_int),
+        "gs_project_fwd": ([P, P, P, P, i64, cam, P, P, P, P, P, P], C.c_int),
+        "gs_scan_workspace_bytes": ([i64], sz),
+        "gs_scan_tiles": ([P, P, i64, P, sz, P, P], C.c_int),
+        "gs_emit_keys": ([P, P, P, i64, i32, i32, P, P, P], C.c_int),
+        "gs_sort_workspace_bytes": ([i64, C.c_int], sz),
+        "gs_sort_pairs": ([P, P, P, P, i64, C.c_int, P, sz, C.POINTER(C.c_int), P], C.c_int),
+        "gs_tile_ranges": ([P, i64, P, i32, P], C.c_int),
+        "gs_raster_fwd": ([P, P, P, P, P, C.POINTER(C.c_float), i32, i32, C.c_int, P, P, P, P, P], C.c_int),
+        "gs_raster_bwd": ([P, P, P, P, P, C.POINTER(C.c_float), i32, i32, P, P, P, P, P, P, P, P], C.c_int),
+        "gs_project_bwd_workspace_bytes": ([i64], sz),
+        "gs_project_bwd": ([P, P, P, i64, cam, P, P, P, P, P, P, P, P, sz, P], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        msg = load().gs_last_error().decode(errors="replace")
+        raise SplatLibError(f"{what}: {msg}" if what else msg)
+
+
+def make_camera(view, fx, fy, cx, cy, width, height, near, far) -> GsCamera:
+    c = GsCamera()
+    flat = [float(v) for row in view for v in row] if hasattr(view[0], "__len__") else [float(v) for v in view]
+    if len(flat) != 16:
+        raise ValueError("view must have shape (4, 4)")
+    for k in range(16):
+        c.view[k] = flat[k]
+    c.fx, c.fy, c.cx, c.cy = float(fx), float(fy), float(cx), float(cy)
+    c.width, c.height = int(width), int(height)
+    c.near_plane, c.far_plane = float(near), float(far)
+    return c

@@ -1,0 +1,46 @@
+// abi.cu -- error plumbing and device queries of the C ABI.
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace gs {
+
+static thread_local char g_last_error[512] = "";
+
+int set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+    va_end(ap);
+    return -1;
+}
+
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error("%s: %s", what, cudaGetErrorString(e));
+    return 0;
+}
+
+}  // namespace gs
+
+extern "C" {
+
+const char* gs_last_error(void) { return gs::g_last_error; }
+
+int gs_version(void) { return 1; }
+
+int gs_device_sm_count(void) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return sms;
+}
+
+}  // extern "C"

@@ -1,0 +1,192 @@
+// binning.cu -- stage 2 around the sort: exclusive scan of the per-Gaussian
+// tile counts (single-pass decoupled look-back), key emission and per-tile
+// range detection.  Together with sort.cu these replace sg/binning.py:27-65
+// (assign_tiles + sort_bins).  All HBM-bound.
+#include "common.cuh"
+
+namespace gs {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 16;  // 4096 counts per CTA
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+constexpr unsigned long long FLAG_AGG = 1ull << 62;
+constexpr unsigned long long FLAG_PRE = 2ull << 62;
+constexpr unsigned long long VAL_MASK = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+    return *(const volatile unsigned long long*)p;
+}
+__device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long long v) {
+    *(volatile unsigned long long*)p = v;
+}
+
+// ws layout: [0] tile counter (u32, padded to 16 B), then u64 status[ctas].
+__global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(const uint32_t* __restrict__ in,
+                                                           uint32_t* __restrict__ out, int64_t n,
+                                                           unsigned int* __restrict__ tile_counter,
+                                                           unsigned long long* __restrict__ status,
+                                                           unsigned long long* __restrict__ total) {
+    __shared__ unsigned int s_tile;
+    __shared__ unsigned long long s_warp[SCAN_THREADS / 32];
+    __shared__ unsigned long long s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const unsigned int tile = s_tile;
+    const int64_t base = (int64_t)tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    uint32_t v[SCAN_ITEMS];
+    if (base + SCAN_ITEMS <= n && ((reinterpret_cast<uintptr_t>(in + base) & 15) == 0)) {
+        const uint4* p = reinterpret_cast<const uint4*>(in + base);
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS / 4; ++k) {
+            const uint4 q = p[k];
+            v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) v[k] = (base + k < n) ? in[base + k] : 0u;
+    }
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) sum += v[k];
+    // block exclusive scan of the per-thread sums
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    unsigned long long warp_off = 0, agg = 0;
+#pragma unroll
+    for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+        const unsigned long long s = s_warp[w];
+        if (w < warp) warp_off += s;
+        agg += s;
+    }
+    // decoupled look-back (one thread)
+    if (threadIdx.x == 0) {
+        unsigned long long prefix = 0;
+        if (tile == 0) {
+            st_volatile(&status[0], FLAG_PRE | agg);
+        } else {
+            st_volatile(&status[tile], FLAG_AGG | agg);
+            __threadfence();
+            int p = (int)tile - 1;
+            while (true) {
+                const unsigned long long s = ld_volatile(&status[p]);
+                const unsigned long long f = s & ~VAL_MASK;
+                if (f == 0) continue;
+                prefix += s & VAL_MASK;
+                if (f == FLAG_PRE) break;
+                --p;
+            }
+            st_volatile(&status[tile], FLAG_PRE | (prefix + agg));
+        }
+        s_prefix = prefix;
+        if ((int64_t)(tile + 1) * SCAN_TILE >= n) *total = prefix + agg;
+    }
+    __syncthreads();
+    unsigned long long run = s_prefix + warp_off + (incl - sum);
+    uint32_t o[SCAN_ITEMS];
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        o[k] = (uint32_t)run;
+        run += v[k];
+    }
+    if (base + SCAN_ITEMS <= n && ((reinterpret_cast<uintptr_t>(out + base) & 15) == 0)) {
+        uint4* p = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS / 4; ++k) p[k] = make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k)
+            if (base + k < n) out[base + k] = o[k];
+    }
+}
+
+// sg/binning.py:35-46: one (tile, gaussian) pair per tile of the rectangle,
+// row-major within a Gaussian, Gaussians in index order.
+__global__ void __launch_bounds__(256) emit_kernel(const float4* __restrict__ xydr,
+                                                   const uint32_t* __restrict__ offsets,
+                                                   const uint32_t* __restrict__ tiles, int n, int tiles_x,
+                                                   int tiles_y, unsigned long long* __restrict__ keys,
+                                                   uint32_t* __restrict__ vals) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (tiles[i] == 0u) return;
+    const float4 g = xydr[i];
+    const int r = __float_as_int(g.w);
+    int tx0, tx1, ty0, ty1;
+    tile_rect(g.x, g.y, r, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+    const unsigned long long dbits = (unsigned long long)__float_as_uint(g.z);
+    uint32_t off = offsets[i];
+    for (int ty = ty0; ty <= ty1; ++ty) {
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            keys[off] = ((unsigned long long)(ty * tiles_x + tx) << 32) | dbits;
+            vals[off] = (uint32_t)i;
+            ++off;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) ranges_kernel(const unsigned long long* __restrict__ keys, int64_t n,
+                                                     uint2* __restrict__ ranges) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = (uint32_t)(keys[i] >> 32);
+    if (i == 0 || (uint32_t)(keys[i - 1] >> 32) != t) ranges[t].x = (uint32_t)i;
+    if (i == n - 1 || (uint32_t)(keys[i + 1] >> 32) != t) ranges[t].y = (uint32_t)(i + 1);
+}
+
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" {
+
+size_t gs_scan_workspace_bytes(int64_t n) {
+    const int64_t ctas = (n + SCAN_TILE - 1) / SCAN_TILE;
+    return 16 + (size_t)(ctas > 0 ? ctas : 1) * sizeof(unsigned long long);
+}
+
+int gs_scan_tiles(const uint32_t* tiles, uint32_t* offsets, int64_t n, void* ws, size_t ws_bytes,
+                  unsigned long long* total, gs_stream_t stream) {
+    if (n < 0) return set_error("gs_scan_tiles: negative n");
+    if (ws_bytes < gs_scan_workspace_bytes(n)) return set_error("gs_scan_tiles: workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) {
+        if (cudaMemsetAsync(total, 0, sizeof(unsigned long long), s) != cudaSuccess)
+            return check_launch("gs_scan_tiles memset");
+        return 0;
+    }
+    const int64_t ctas = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (cudaMemsetAsync(ws, 0, gs_scan_workspace_bytes(n), s) != cudaSuccess) return check_launch("scan memset");
+    unsigned int* counter = (unsigned int*)ws;
+    unsigned long long* status = (unsigned long long*)((char*)ws + 16);
+    scan_kernel<<<(unsigned)ctas, SCAN_THREADS, 0, s>>>(tiles, offsets, n, counter, status, total);
+    return check_launch("scan_kernel");
+}
+
+int gs_emit_keys(const float* xydr4, const uint32_t* offsets, const uint32_t* tiles, int64_t n, int32_t width,
+                 int32_t height, unsigned long long* keys, uint32_t* vals, gs_stream_t stream) {
+    if (n < 0 || n > 0x7fffffff) return set_error("gs_emit_keys: n out of range");
+    if (n == 0) return 0;
+    const int tiles_x = (width + TILE - 1) / TILE, tiles_y = (height + TILE - 1) / TILE;
+    emit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        (const float4*)xydr4, offsets, tiles, (int)n, tiles_x, tiles_y, keys, vals);
+    return check_launch("emit_kernel");
+}
+
+int gs_tile_ranges(const unsigned long long* sorted_keys, int64_t n, uint32_t* ranges2, int32_t n_tiles,
+                   gs_stream_t stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(ranges2, 0, (size_t)n_tiles * 2 * sizeof(uint32_t), s) != cudaSuccess)
+        return check_launch("ranges memset");
+    if (n == 0) return 0;
+    ranges_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sorted_keys, n, (uint2*)ranges2);
+    return check_launch("ranges_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// common.cuh -- constants, camera parameters and the shared per-(pixel,
+// splat) evaluation used by BOTH the forward and backward rasterizers.
+//
+// The backward pass replays the forward's skip/clamp decisions
+// (sg/raster_backward.py:64-71 mirrors sg/raster_forward.py:130-137), so the
+// sigma/alpha arithmetic lives in exactly one function here, written with
+// explicit round-to-nearest intrinsics so nvcc cannot contract it
+// differently in the two kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/splat_b200.h"
+
+namespace gs {
+
+constexpr int TILE = GS_TILE_SIZE;             // sg/binning.py:8
+constexpr int TILE_PIX = TILE * TILE;
+constexpr float DILATION = 0.3f;               // sg/projection.py:17
+constexpr float ALPHA_MIN = 1.0f / 255.0f;     // sg/raster_forward.py:21
+constexpr float ALPHA_MAX = 0.999f;            // sg/raster_forward.py:22
+constexpr float T_MIN = 1e-4f;                 // sg/raster_forward.py:25
+constexpr float SIGMA_CUT = 4.5f;              // sg/raster_forward.py:30
+constexpr float QUAT_EPS = 1e-12f;             // sg/core.py:13
+constexpr float NEG_LOG2E = -1.4426950408889634f;
+constexpr int MAX_RADIUS = 1 << 24;            // clamp so int math cannot overflow
+
+// Kernel-side camera: rotation/translation split out of the 4x4 view.
+struct CamK {
+    float R[9];  // row-major R_cw
+    float t[3];
+    float fx, fy, cx, cy;
+    int W, H;
+    float near_plane, far_plane;
+    int tiles_x, tiles_y;
+};
+
+inline CamK make_camk(const gs_camera& c) {
+    CamK k;
+    for (int r = 0; r < 3; ++r) {
+        for (int q = 0; q < 3; ++q) k.R[3 * r + q] = c.view[4 * r + q];
+        k.t[r] = c.view[4 * r + 3];
+    }
+    k.fx = c.fx; k.fy = c.fy; k.cx = c.cx; k.cy = c.cy;
+    k.W = c.width; k.H = c.height;
+    k.near_plane = c.near_plane; k.far_plane = c.far_plane;
+    k.tiles_x = (c.width + TILE - 1) / TILE;
+    k.tiles_y = (c.height + TILE - 1) / TILE;
+    return k;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// sigma = 0.5*(A dx^2 + C dy^2) + B dx dy   (sg/raster_forward.py:132-135)
+// evaluated as dx*(hA*dx + B*dy) + (hC*dy)*dy with hA = A/2, hC = C/2
+// (exact halvings), every op rounded explicitly.
+__device__ __forceinline__ float splat_sigma(float dx, float dy, float hA, float B, float hC) {
+    const float t = __fmaf_rn(B, dy, __fmul_rn(hA, dx));
+    const float u = __fmul_rn(hC, dy);
+    return __fmaf_rn(dx, t, __fmul_rn(u, dy));
+}
+
+// exp(-sigma) shared by forward and backward (sg/raster_forward.py:136,
+// sg/raster_backward.py:68).
+__device__ __forceinline__ float splat_exp_neg(float sigma) {
+    return ex2_approx(__fmul_rn(sigma, NEG_LOG2E));
+}
+
+// Tile rectangle of a splat's closed bbox square, sg/binning.py:35-46.
+// floor((m -/+ r)/16) is computed exactly as floor_div(floor(m) -/+ r, 16):
+// m is fp32, r an integer, so no rounding can move a tile edge.
+__device__ __forceinline__ void tile_rect(float mx, float my, int r, int tiles_x, int tiles_y,
+                                          int& tx0, int& tx1, int& ty0, int& ty1) {
+    const int fx = (int)floorf(mx), fy = (int)floorf(my);
+    tx0 = max(0, (fx - r) >> 4);
+    tx1 = min(tiles_x - 1, (fx + r) >> 4);
+    ty0 = max(0, (fy - r) >> 4);
+    ty1 = min(tiles_y - 1, (fy + r) >> 4);
+}
+
+__device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+}  // namespace gs
+
+// error plumbing shared by the extern "C" entry points (defined in abi.cu)
+namespace gs {
+int set_error(const char* fmt, ...);
+int check_launch(const char* what);
+}  // namespace gs

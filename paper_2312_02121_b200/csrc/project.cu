@@ -1,0 +1,321 @@
+// project.cu -- stage 1 (projection forward) and stage 5 (projection
+// backward).  One thread per Gaussian; both kernels are HBM-bound
+// (80 B/Gaussian forward, 104 B/Gaussian backward).
+#include "common.cuh"
+
+namespace gs {
+
+// sg/core.py:146-171 quat_to_rotmat (normalised, (w,x,y,z) order).
+__device__ __forceinline__ void quat_rot(float w, float x, float y, float z, float R[9]) {
+    R[0] = 1.f - 2.f * (y * y + z * z); R[1] = 2.f * (x * y - w * z); R[2] = 2.f * (x * z + w * y);
+    R[3] = 2.f * (x * y + w * z); R[4] = 1.f - 2.f * (x * x + z * z); R[5] = 2.f * (y * z - w * x);
+    R[6] = 2.f * (x * z - w * y); R[7] = 2.f * (y * z + w * x); R[8] = 1.f - 2.f * (x * x + y * y);
+}
+
+__device__ __forceinline__ void report(unsigned long long* status, int i, int code) {
+    atomicMin(status, ((unsigned long long)(unsigned)i << 8) | (unsigned long long)code);
+}
+
+// sg/projection.py:115-145 project_gaussian for every Gaussian, in the
+// reference's order of checks: depth cull (:124-125) -> scale/quat errors
+// (sg/core.py:189-192) -> J (:64-82) -> Sigma' + 0.3 I (:85-96) -> pixel map
+// through P (:45-61; equals fx*tx/tz + 0.5 + cx) -> radius (:99-112) ->
+// off-screen cull (:131-137).  Plus the conic (sg/raster_forward.py:86-92)
+// and the tile count of the bbox square (sg/binning.py:35-46).
+__global__ void __launch_bounds__(256) project_fwd_kernel(
+    const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
+    const float* __restrict__ opac, int n, CamK cam, float4* __restrict__ xydr, float4* __restrict__ conic,
+    uint32_t* __restrict__ tiles, float* __restrict__ cov_out, unsigned long long* __restrict__ status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
+    const float* Rc = cam.R;
+    const float tx = Rc[0] * mx + Rc[1] * my + Rc[2] * mz + cam.t[0];
+    const float ty = Rc[3] * mx + Rc[4] * my + Rc[5] * mz + cam.t[1];
+    const float tz = Rc[6] * mx + Rc[7] * my + Rc[8] * mz + cam.t[2];
+    float4 o_xydr = make_float4(0.f, 0.f, tz, __int_as_float(0));
+    float4 o_con = make_float4(0.f, 0.f, 0.f, 0.f);
+    float ca = 0.f, cb = 0.f, cc = 0.f;
+    uint32_t nt = 0;
+    const bool depth_culled = (tz <= cam.near_plane) || (tz >= cam.far_plane);
+    if (!depth_culled) {
+        const float sx = scales[3 * i], sy = scales[3 * i + 1], sz = scales[3 * i + 2];
+        const float4 q = quats[i];
+        const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+        if (sx <= 0.f || sy <= 0.f || sz <= 0.f) {
+            report(status, i, GS_ERR_SCALE);
+        } else if (qn <= QUAT_EPS) {
+            report(status, i, GS_ERR_QUAT);
+        } else {
+            const float inv = 1.f / qn;
+            float R[9];
+            quat_rot(q.x * inv, q.y * inv, q.z * inv, q.w * inv, R);
+            // M = R diag(s)
+            const float M[9] = {R[0] * sx, R[1] * sy, R[2] * sz, R[3] * sx, R[4] * sy,
+                                R[5] * sz, R[6] * sx, R[7] * sy, R[8] * sz};
+            // T = J R_cw, J = [[fx/tz, 0, -fx tx/tz^2], [0, fy/tz, -fy ty/tz^2]]
+            const float iz = 1.f / tz;
+            const float j00 = cam.fx * iz, j02 = -cam.fx * tx * iz * iz;
+            const float j11 = cam.fy * iz, j12 = -cam.fy * ty * iz * iz;
+            float T0[3], T1[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                T0[k] = j00 * Rc[k] + j02 * Rc[6 + k];
+                T1[k] = j11 * Rc[3 + k] + j12 * Rc[6 + k];
+            }
+            // V = T M; Sigma' = V V^T + 0.3 I  (T Sigma T^T with Sigma = M M^T)
+            float V0[3], V1[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                V0[c] = T0[0] * M[c] + T0[1] * M[3 + c] + T0[2] * M[6 + c];
+                V1[c] = T1[0] * M[c] + T1[1] * M[3 + c] + T1[2] * M[6 + c];
+            }
+            ca = V0[0] * V0[0] + V0[1] * V0[1] + V0[2] * V0[2] + DILATION;
+            cb = V0[0] * V1[0] + V0[1] * V1[1] + V0[2] * V1[2];
+            cc = V1[0] * V1[0] + V1[1] * V1[1] + V1[2] * V1[2] + DILATION;
+            if (fabsf(tz) < 1e-12f) {
+                report(status, i, GS_ERR_HOMOG);
+            } else {
+                const float px = (cam.fx * (tx / tz) + 0.5f) + cam.cx;
+                const float py = (cam.fy * (ty / tz) + 0.5f) + cam.cy;
+                const float det = ca * cc - cb * cb;
+                if (!(det > 0.f && ca + cc > 0.f)) {
+                    report(status, i, GS_ERR_COV2D);
+                } else {
+                    const float mid = 0.5f * (ca + cc);
+                    const float lam = mid + sqrtf(0.25f * (ca - cc) * (ca - cc) + cb * cb);
+                    const float rf = ceilf(3.f * sqrtf(lam));
+                    const int r = rf < (float)MAX_RADIUS ? (int)rf : MAX_RADIUS;
+                    const float fr = (float)r;
+                    const bool off = (px + fr < 0.f) || (px - fr >= (float)cam.W) || (py + fr < 0.f) ||
+                                     (py - fr >= (float)cam.H);
+                    o_xydr = make_float4(px, py, tz, __int_as_float(off ? 0 : r));
+                    if (!off) {
+                        const float idet = 1.f / det;
+                        o_con = make_float4(cc * idet, -cb * idet, ca * idet, opac[i]);
+                        int tx0, tx1, ty0, ty1;
+                        tile_rect(px, py, r, cam.tiles_x, cam.tiles_y, tx0, tx1, ty0, ty1);
+                        nt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+                    }
+                }
+            }
+        }
+    }
+    xydr[i] = o_xydr;
+    conic[i] = o_con;
+    tiles[i] = nt;
+    if (cov_out) {
+        cov_out[3 * i] = ca;
+        cov_out[3 * i + 1] = cb;
+        cov_out[3 * i + 2] = cc;
+    }
+}
+
+constexpr int PBWD_THREADS = 256;
+
+// Per-Gaussian loop body of sg/proj_backward.py:200-222.
+__global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
+    const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
+    int n, CamK cam, const uint32_t* __restrict__ tiles, const float4* __restrict__ d_geo,
+    const float* __restrict__ d_c11, float* __restrict__ d_means, float* __restrict__ d_scales,
+    float4* __restrict__ d_quats, float* __restrict__ view_partials) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    float dv[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) dv[k] = 0.f;
+    if (i < n) {
+        float dmx = 0.f, dmy = 0.f, dmz = 0.f, dsx = 0.f, dsy = 0.f, dsz = 0.f;
+        float4 dq = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (tiles[i] != 0u) {
+            const float mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
+            const float s[3] = {scales[3 * i], scales[3 * i + 1], scales[3 * i + 2]};
+            const float4 q = quats[i];
+            const float* Rc = cam.R;
+            const float tx = Rc[0] * mx + Rc[1] * my + Rc[2] * mz + cam.t[0];
+            const float ty = Rc[3] * mx + Rc[4] * my + Rc[5] * mz + cam.t[1];
+            const float tz = Rc[6] * mx + Rc[7] * my + Rc[8] * mz + cam.t[2];
+            const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+            const float inv = 1.f / qn;
+            const float qw = q.x * inv, qx = q.y * inv, qy = q.z * inv, qz = q.w * inv;
+            float R[9];
+            quat_rot(qw, qx, qy, qz, R);
+            float M[9];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) M[3 * a + b] = R[3 * a + b] * s[b];
+            float Sg[9];  // Sigma = M M^T
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                    Sg[3 * a + b] = M[3 * a] * M[3 * b] + M[3 * a + 1] * M[3 * b + 1] + M[3 * a + 2] * M[3 * b + 2];
+            const float iz = 1.f / tz, iz2 = iz * iz;
+            const float j00 = cam.fx * iz, j02 = -cam.fx * tx * iz2;
+            const float j11 = cam.fy * iz, j12 = -cam.fy * ty * iz2;
+            float T0[3], T1[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                T0[k] = j00 * Rc[k] + j02 * Rc[6 + k];
+                T1[k] = j11 * Rc[3 + k] + j12 * Rc[6 + k];
+            }
+            const float4 gg = d_geo[i];
+            const float gx = gg.x, gy = gg.y, g00 = gg.z, g01 = gg.w, g11 = d_c11[i];
+            // mean2d_backward (:53-77) == J^T d_mean2d with dt_w = 0
+            float dt0 = cam.fx * gx * iz;
+            float dt1 = cam.fy * gy * iz;
+            float dt2 = -(cam.fx * gx * tx + cam.fy * gy * ty) * iz2;
+            // cov2d_backward (:88-121)
+            float GT0[3], GT1[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                GT0[k] = g00 * T0[k] + g01 * T1[k];
+                GT1[k] = g01 * T0[k] + g11 * T1[k];
+            }
+            float dS[9];  // T^T G T
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) dS[3 * a + b] = T0[a] * GT0[b] + T1[a] * GT1[b];
+            // _cov_transform_grad (:80-85): G T Sigma^T + G^T T Sigma = 2 (G T) Sigma
+            float dT0[3], dT1[3];
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                dT0[b] = 2.f * (GT0[0] * Sg[b] + GT0[1] * Sg[3 + b] + GT0[2] * Sg[6 + b]);
+                dT1[b] = 2.f * (GT1[0] * Sg[b] + GT1[1] * Sg[3 + b] + GT1[2] * Sg[6 + b]);
+            }
+            // dJ = dT R_cw^T (only the structurally non-zero entries of J matter)
+            const float dJ00 = dT0[0] * Rc[0] + dT0[1] * Rc[1] + dT0[2] * Rc[2];
+            const float dJ02 = dT0[0] * Rc[6] + dT0[1] * Rc[7] + dT0[2] * Rc[8];
+            const float dJ11 = dT1[0] * Rc[3] + dT1[1] * Rc[4] + dT1[2] * Rc[5];
+            const float dJ12 = dT1[0] * Rc[6] + dT1[1] * Rc[7] + dT1[2] * Rc[8];
+            const float iz3 = iz2 * iz;
+            dt0 += -cam.fx * iz2 * dJ02;
+            dt1 += -cam.fy * iz2 * dJ12;
+            dt2 += -cam.fx * iz2 * dJ00 + 2.f * cam.fx * tx * iz3 * dJ02 - cam.fy * iz2 * dJ11 +
+                   2.f * cam.fy * ty * iz3 * dJ12;
+            // world_backward (:124-136)
+            dmx = Rc[0] * dt0 + Rc[3] * dt1 + Rc[6] * dt2;
+            dmy = Rc[1] * dt0 + Rc[4] * dt1 + Rc[7] * dt2;
+            dmz = Rc[2] * dt0 + Rc[5] * dt1 + Rc[8] * dt2;
+            const float dtv[3] = {dt0, dt1, dt2};
+            const float hm[4] = {mx, my, mz, 1.f};
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dv[4 * a + b] = dtv[a] * hm[b];
+            // view rotation path (:218-222): d_view[:3,:3] += J^T dT
+            const float J0[3] = {j00, 0.f, j02}, J1[3] = {0.f, j11, j12};
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) dv[4 * a + b] += J0[a] * dT0[b] + J1[a] * dT1[b];
+            // covariance3d_backward (:151-175): dM = (dS + dS^T) M = 2 dS M
+            float dM[9];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                    dM[3 * a + b] = 2.f * (dS[3 * a] * M[b] + dS[3 * a + 1] * M[3 + b] + dS[3 * a + 2] * M[6 + b]);
+            float dR[9];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) dR[3 * a + b] = dM[3 * a + b] * s[b];
+            dsx = R[0] * dM[0] + R[3] * dM[3] + R[6] * dM[6];
+            dsy = R[1] * dM[1] + R[4] * dM[4] + R[7] * dM[7];
+            dsz = R[2] * dM[2] + R[5] * dM[5] + R[8] * dM[8];
+            // <dR, dR/dq_k> with the Jacobians of :139-148
+            const float gw = 2.f * (-qz * dR[1] + qy * dR[2] + qz * dR[3] - qx * dR[5] - qy * dR[6] + qx * dR[7]);
+            const float gxq = 2.f * (qy * dR[1] + qz * dR[2] + qy * dR[3] - 2.f * qx * dR[4] - qw * dR[5] +
+                                     qz * dR[6] + qw * dR[7] - 2.f * qx * dR[8]);
+            const float gyq = 2.f * (-2.f * qy * dR[0] + qx * dR[1] + qw * dR[2] + qx * dR[3] + qz * dR[5] -
+                                     qw * dR[6] + qz * dR[7] - 2.f * qy * dR[8]);
+            const float gzq = 2.f * (-2.f * qz * dR[0] - qw * dR[1] + qx * dR[2] + qw * dR[3] - 2.f * qz * dR[4] +
+                                     qy * dR[5] + qx * dR[6] + qy * dR[7]);
+            // normalisation chain: (dq_hat - q_hat (q_hat . dq_hat)) / |q|
+            const float dot = qw * gw + qx * gxq + qy * gyq + qz * gzq;
+            dq = make_float4((gw - qw * dot) * inv, (gxq - qx * dot) * inv, (gyq - qy * dot) * inv,
+                             (gzq - qz * dot) * inv);
+        }
+        d_means[3 * i] = dmx; d_means[3 * i + 1] = dmy; d_means[3 * i + 2] = dmz;
+        d_scales[3 * i] = dsx; d_scales[3 * i + 1] = dsy; d_scales[3 * i + 2] = dsz;
+        d_quats[i] = dq;
+    }
+    // block partial of d_view (deterministic: fixed shuffle tree + fixed warp order)
+    __shared__ float red[PBWD_THREADS / 32][12];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        float v = dv[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 12) {
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < PBWD_THREADS / 32; ++w) v += red[w][threadIdx.x];
+        view_partials[blockIdx.x * 12 + threadIdx.x] = v;
+    }
+}
+
+// Fixed-order sum of the per-block d_view partials -> 4x4 (bottom row 0,
+// sg/proj_backward.py:31-32).
+__global__ void __launch_bounds__(384) view_reduce_kernel(const float* __restrict__ partials, int nblocks,
+                                                          float* __restrict__ d_view16) {
+    const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float v = 0.f;
+    for (int b = lane; b < nblocks; b += 32) v += partials[b * 12 + k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) d_view16[k] = v;
+    if (threadIdx.x < 4) d_view16[12 + threadIdx.x] = 0.f;
+}
+
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" {
+
+int gs_project_fwd(const float* means3, const float* scales3, const float* quats4, const float* opacities,
+                   int64_t n, const gs_camera* cam, float* out_xydr4, float* out_conic4, uint32_t* out_tiles,
+                   float* out_cov3, unsigned long long* status, gs_stream_t stream) {
+    if (n < 0 || n > 0x7fffffff) return set_error("gs_project_fwd: n=%lld out of range", (long long)n);
+    if (!cam) return set_error("gs_project_fwd: null camera");
+    if (n == 0) return 0;
+    const CamK k = make_camk(*cam);
+    const int blocks = (int)((n + 255) / 256);
+    project_fwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        means3, scales3, (const float4*)quats4, opacities, (int)n, k, (float4*)out_xydr4, (float4*)out_conic4,
+        out_tiles, out_cov3, status);
+    return check_launch("project_fwd_kernel");
+}
+
+size_t gs_project_bwd_workspace_bytes(int64_t n) {
+    const int64_t blocks = (n + PBWD_THREADS - 1) / PBWD_THREADS;
+    return (size_t)(blocks > 0 ? blocks : 1) * 12 * sizeof(float);
+}
+
+int gs_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n,
+                   const gs_camera* cam, const uint32_t* tiles, const float* d_geo4, const float* d_c11,
+                   float* d_means3, float* d_scales3, float* d_quats4, float* d_view16, void* ws,
+                   size_t ws_bytes, gs_stream_t stream) {
+    if (n < 0 || n > 0x7fffffff) return set_error("gs_project_bwd: n=%lld out of range", (long long)n);
+    if (!cam) return set_error("gs_project_bwd: null camera");
+    if (ws_bytes < gs_project_bwd_workspace_bytes(n)) return set_error("gs_project_bwd: workspace too small");
+    const CamK k = make_camk(*cam);
+    const int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
+    if (blocks > 0) {
+        project_bwd_kernel<<<blocks, PBWD_THREADS, 0, (cudaStream_t)stream>>>(
+            means3, scales3, (const float4*)quats4, (int)n, k, tiles, (const float4*)d_geo4, d_c11, d_means3,
+            d_scales3, (float4*)d_quats4, (float*)ws);
+        if (check_launch("project_bwd_kernel")) return -1;
+    }
+    view_reduce_kernel<<<1, 384, 0, (cudaStream_t)stream>>>((const float*)ws, blocks, d_view16);
+    return check_launch("view_reduce_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,347 @@
+"""Device pipeline and autograd for the splatting hot path.
+
+Host code is Python/PyTorch: PyTorch owns every device buffer (caching
+allocator) and the stream; each stage is one call into libsplat_b200.so
+(``include/splat_b200.h``).  There is no CPU fallback: CPU tensors are
+rejected and a missing library raises.
+
+Stages (reference functions they replace, sg/ = /root/reference/pkg/src/splatgrad):
+  project        sg/projection.py:115-145 (+ sg/raster_forward.py:86-92,246-252)
+  bin_sort       sg/binning.py:27-65
+  raster_fwd     sg/raster_forward.py:116-172,222-243
+  raster_bwd     sg/raster_backward.py:47-108,166-205
+  project_bwd    sg/proj_backward.py:178-223
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+TILE = 16
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+@dataclass
+class CameraParams:
+    """Host-side pinhole camera (fields of sg/core.py:59-129 Camera)."""
+
+    view: list            # 4x4 nested list (row-major, world -> camera)
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+    near: float
+    far: float
+
+    @staticmethod
+    def of(cam) -> "CameraParams":
+        v = cam.view
+        if isinstance(v, torch.Tensor):
+            v = v.detach().to("cpu", torch.float64).tolist()
+        else:
+            v = [[float(x) for x in row] for row in v]
+        return CameraParams(v, float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy), int(cam.width),
+                            int(cam.height), float(cam.near), float(cam.far))
+
+    def c(self) -> _lib.GsCamera:
+        return _lib.make_camera(self.view, self.fx, self.fy, self.cx, self.cy, self.width, self.height,
+                                self.near, self.far)
+
+    @property
+    def tiles_x(self) -> int:
+        return (self.width + TILE - 1) // TILE
+
+    @property
+    def tiles_y(self) -> int:
+        return (self.height + TILE - 1) // TILE
+
+
+def _check_param(name, t, cols):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.dtype != torch.float32:
+        raise ValueError(f"{name} must be float32, got {t.dtype}")
+    if cols is None:
+        if t.dim() != 1:
+            raise ValueError(f"{name} must have shape (N,), got {tuple(t.shape)}")
+    elif t.dim() != 2 or t.shape[1] != cols:
+        raise ValueError(f"{name} must have shape (N, {cols}), got {tuple(t.shape)}")
+    return t.contiguous()
+
+
+def check_params(means, scales, quats, opacities, colors=None):
+    means = _check_param("means", means, 3)
+    n = means.shape[0]
+    scales = _check_param("scales", scales, 3)
+    quats = _check_param("quats", quats, 4)
+    opacities = _check_param("opacities", opacities, None)
+    out = [means, scales, quats, opacities]
+    if colors is not None:
+        out.append(_check_param("colors", colors, 3))
+    for name, t in zip(("scales", "quats", "opacities", "colors"), out[1:]):
+        if t.shape[0] != n:
+            raise ValueError(f"{name} has {t.shape[0]} rows, expected {n}")
+    return out
+
+
+# --------------------------------------------------------------------- stages
+
+@dataclass
+class Projection:
+    xydr: torch.Tensor      # (N,4) mean2d.x, mean2d.y, depth, radius bits
+    conic: torch.Tensor     # (N,4) A, B, C, opacity
+    tiles: torch.Tensor     # (N,) int32 (uint32 counts; 0 = culled)
+    cov2d: torch.Tensor | None  # (N,3) a, b, c (only when requested)
+
+    @property
+    def radius(self) -> torch.Tensor:
+        return self.xydr[:, 3].contiguous().view(torch.int32)
+
+
+def project(means, scales, quats, opacities, cam: CameraParams, *, want_cov=False,
+            status: torch.Tensor | None = None) -> Projection:
+    """Stage 1 (gs_project_fwd).  ``status`` (int64[1], init -1) collects errors."""
+    L = _lib.load()
+    n = means.shape[0]
+    dev = means.device
+    xydr = torch.empty((n, 4), device=dev, dtype=torch.float32)
+    conic = torch.empty((n, 4), device=dev, dtype=torch.float32)
+    tiles = torch.empty((n,), device=dev, dtype=torch.int32)
+    cov = torch.empty((n, 3), device=dev, dtype=torch.float32) if want_cov else None
+    if status is None:
+        status = torch.full((1,), -1, device=dev, dtype=torch.int64)
+    camc = cam.c()
+    check(L.gs_project_fwd(_ptr(means), _ptr(scales), _ptr(quats), _ptr(opacities), n, C.byref(camc),
+                           _ptr(xydr), _ptr(conic), _ptr(tiles), _ptr(cov), _ptr(status), _stream()),
+          "gs_project_fwd")
+    return Projection(xydr, conic, tiles, cov)
+
+
+def raise_status(status_value: int) -> None:
+    """Turn the device status word into the reference's ValueError."""
+    if status_value == -1:
+        return
+    s = status_value & 0xFFFFFFFFFFFFFFFF
+    idx, code = s >> 8, s & 0xFF
+    raise ValueError(f"gaussian {idx}: {_lib.ERR_MESSAGES.get(code, f'error {code}')}")
+
+
+def scan_tiles(tiles: torch.Tensor, total: torch.Tensor) -> torch.Tensor:
+    L = _lib.load()
+    n = tiles.shape[0]
+    offsets = torch.empty((n,), device=tiles.device, dtype=torch.int32)
+    wsb = L.gs_scan_workspace_bytes(n)
+    ws = torch.empty((wsb,), device=tiles.device, dtype=torch.uint8)
+    check(L.gs_scan_tiles(_ptr(tiles), _ptr(offsets), n, _ptr(ws), wsb, _ptr(total), _stream()), "gs_scan_tiles")
+    return offsets
+
+
+@dataclass
+class Bins:
+    ranges: torch.Tensor       # (tiles, 2) int32 [start, end)
+    sorted_keys: torch.Tensor  # (I,) int64 (tile << 32 | depth bits)
+    sorted_vals: torch.Tensor  # (I,) int32 Gaussian ids
+    n_isect: int
+
+
+def tile_bits(n_tiles: int) -> int:
+    return max(1, math.ceil(math.log2(n_tiles))) if n_tiles > 1 else 1
+
+
+def emit_and_sort(proj: Projection, offsets: torch.Tensor, n_isect: int, cam: CameraParams,
+                  sort: bool = True) -> Bins:
+    """Stage 2 after the scan: key emission, onesweep sort, tile ranges."""
+    L = _lib.load()
+    dev = proj.xydr.device
+    n = proj.xydr.shape[0]
+    n_tiles = cam.tiles_x * cam.tiles_y
+    keys = torch.empty((n_isect,), device=dev, dtype=torch.int64)
+    vals = torch.empty((n_isect,), device=dev, dtype=torch.int32)
+    st = _stream()
+    check(L.gs_emit_keys(_ptr(proj.xydr), _ptr(offsets), _ptr(proj.tiles), n, cam.width, cam.height,
+                         _ptr(keys), _ptr(vals), st), "gs_emit_keys")
+    if sort and n_isect > 0:
+        end_bit = 32 + tile_bits(n_tiles)
+        keys_alt = torch.empty_like(keys)
+        vals_alt = torch.empty_like(vals)
+        wsb = L.gs_sort_workspace_bytes(n_isect, end_bit)
+        ws = torch.empty((wsb,), device=dev, dtype=torch.uint8)
+        sel = C.c_int(0)
+        check(L.gs_sort_pairs(_ptr(keys), _ptr(keys_alt), _ptr(vals), _ptr(vals_alt), n_isect, end_bit,
+                              _ptr(ws), wsb, C.byref(sel), st), "gs_sort_pairs")
+        if sel.value:
+            keys, vals = keys_alt, vals_alt
+    ranges = torch.empty((n_tiles, 2), device=dev, dtype=torch.int32)
+    if sort:
+        check(L.gs_tile_ranges(_ptr(keys), n_isect, _ptr(ranges), n_tiles, st), "gs_tile_ranges")
+    return Bins(ranges, keys, vals, n_isect)
+
+
+def bin_sort(proj: Projection, cam: CameraParams, status: torch.Tensor | None = None) -> Bins:
+    """Scan + one 16-byte D2H read (status word and intersection count) +
+    emission + sort + ranges.  Raises the reference's ValueError on bad input."""
+    dev = proj.xydr.device
+    meta = torch.empty((2,), device=dev, dtype=torch.int64)
+    if status is not None:
+        meta[0:1].copy_(status)
+    else:
+        meta[0] = -1
+    offsets = scan_tiles(proj.tiles, meta[1:2])
+    host = meta.cpu()
+    raise_status(int(host[0]))
+    return emit_and_sort(proj, offsets, int(host[1]), cam)
+
+
+@dataclass
+class FrameState:
+    """What the backward pass needs (autograd ctx payload, cf. RenderResult
+    of sg/raster_forward.py:62-70)."""
+
+    cam: CameraParams
+    background: tuple
+    early_termination: bool
+    proj: Projection
+    bins: Bins
+    final_T: torch.Tensor
+    n_contrib: torch.Tensor
+    counts_fwd: torch.Tensor | None = None
+    extra: dict = field(default_factory=dict)
+
+
+def raster_fwd(proj: Projection, bins: Bins, colors, cam: CameraParams, background, early_termination=True,
+               counts: torch.Tensor | None = None):
+    L = _lib.load()
+    dev = proj.xydr.device
+    H, W = cam.height, cam.width
+    image = torch.empty((H, W, 3), device=dev, dtype=torch.float32)
+    final_T = torch.empty((H, W), device=dev, dtype=torch.float32)
+    n_contrib = torch.empty((H, W), device=dev, dtype=torch.int32)
+    bg = (C.c_float * 3)(*[float(b) for b in background])
+    check(L.gs_raster_fwd(_ptr(bins.ranges), _ptr(bins.sorted_vals), _ptr(proj.xydr), _ptr(proj.conic),
+                          _ptr(colors), bg, W, H, 1 if early_termination else 0, _ptr(image), _ptr(final_T),
+                          _ptr(n_contrib), _ptr(counts), _stream()), "gs_raster_fwd")
+    return image, final_T, n_contrib
+
+
+def raster_bwd(state: FrameState, colors, d_image, counts: torch.Tensor | None = None):
+    """Screen-space gradients per scene Gaussian (Splat2DGrads,
+    sg/raster_backward.py:24-44): returns (d_rgbo (N,4), d_geo (N,4), d_c11 (N,))."""
+    L = _lib.load()
+    cam = state.cam
+    n = state.proj.xydr.shape[0]
+    dev = state.proj.xydr.device
+    d_rgbo = torch.zeros((n, 4), device=dev, dtype=torch.float32)
+    d_geo = torch.zeros((n, 4), device=dev, dtype=torch.float32)
+    d_c11 = torch.zeros((n,), device=dev, dtype=torch.float32)
+    bg = (C.c_float * 3)(*[float(b) for b in state.background])
+    check(L.gs_raster_bwd(_ptr(state.bins.ranges), _ptr(state.bins.sorted_vals), _ptr(state.proj.xydr),
+                          _ptr(state.proj.conic), _ptr(colors), bg, cam.width, cam.height, _ptr(state.final_T),
+                          _ptr(state.n_contrib), _ptr(d_image), _ptr(d_rgbo), _ptr(d_geo), _ptr(d_c11),
+                          _ptr(counts), _stream()), "gs_raster_bwd")
+    return d_rgbo, d_geo, d_c11
+
+
+def project_bwd(means, scales, quats, cam: CameraParams, tiles, d_geo, d_c11):
+    L = _lib.load()
+    n = means.shape[0]
+    dev = means.device
+    d_means = torch.empty((n, 3), device=dev, dtype=torch.float32)
+    d_scales = torch.empty((n, 3), device=dev, dtype=torch.float32)
+    d_quats = torch.empty((n, 4), device=dev, dtype=torch.float32)
+    d_view = torch.empty((4, 4), device=dev, dtype=torch.float32)
+    wsb = L.gs_project_bwd_workspace_bytes(n)
+    ws = torch.empty((wsb,), device=dev, dtype=torch.uint8)
+    camc = cam.c()
+    check(L.gs_project_bwd(_ptr(means), _ptr(scales), _ptr(quats), n, C.byref(camc), _ptr(tiles), _ptr(d_geo),
+                           _ptr(d_c11), _ptr(d_means), _ptr(d_scales), _ptr(d_quats), _ptr(d_view), _ptr(ws), wsb,
+                           _stream()), "gs_project_bwd")
+    return d_means, d_scales, d_quats, d_view
+
+
+# ------------------------------------------------------------- whole frame
+
+def render_forward(means, scales, quats, opacities, colors, cam: CameraParams, background=(0.0, 0.0, 0.0),
+                   early_termination=True, *, want_cov=False, counts=False):
+    """project -> bin/sort -> raster fwd.  Returns (image (H,W,3), FrameState)."""
+    means, scales, quats, opacities, colors = check_params(means, scales, quats, opacities, colors)
+    status = torch.full((1,), -1, device=means.device, dtype=torch.int64)
+    proj = project(means, scales, quats, opacities, cam, want_cov=want_cov, status=status)
+    bins = bin_sort(proj, cam, status)
+    cnt = torch.zeros((4,), device=means.device, dtype=torch.int64) if counts else None
+    image, final_T, n_contrib = raster_fwd(proj, bins, colors, cam, background, early_termination, cnt)
+    state = FrameState(cam, tuple(float(b) for b in background), bool(early_termination), proj, bins, final_T,
+                       n_contrib, cnt)
+    return image, state
+
+
+def render_backward(state: FrameState, means, scales, quats, colors, d_image, *, counts=False):
+    """raster bwd -> projection bwd.  Returns dict of SceneGradients fields
+    (sg/proj_backward.py:25-50) as tensors plus the screen-space grads."""
+    H, W = state.cam.height, state.cam.width
+    if tuple(d_image.shape) != (H, W, 3):
+        raise ValueError(f"d_image must have shape {(H, W, 3)}, got {tuple(d_image.shape)}")  # sg/raster_backward.py:180-183
+    d_image = d_image.contiguous().to(torch.float32)
+    cnt = torch.zeros((3,), device=means.device, dtype=torch.int64) if counts else None
+    d_rgbo, d_geo, d_c11 = raster_bwd(state, colors, d_image, cnt)
+    d_means, d_scales, d_quats, d_view = project_bwd(means, scales, quats, state.cam, state.proj.tiles, d_geo, d_c11)
+    return dict(d_mean=d_means, d_scale=d_scales, d_quat=d_quats, d_opacity=d_rgbo[:, 3], d_color=d_rgbo[:, :3],
+                d_view=d_view, d_rgbo=d_rgbo, d_geo=d_geo, d_c11=d_c11, counts=cnt)
+
+
+class RasterizeGaussians(torch.autograd.Function):
+    """Differentiable render of one view.
+
+    forward(means (N,3), scales (N,3), quats (N,4) (w,x,y,z), opacities (N,),
+            colors (N,3), viewmat (4,4), camera (fx, fy, cx, cy, W, H, near, far),
+            background (3,), early_termination) -> image (H, W, 3)
+    backward returns d_means, d_scales, d_quats, d_opacities, d_colors,
+    d_viewmat -- field by field the reference's SceneGradients
+    (sg/proj_backward.py:34-39).
+    """
+
+    @staticmethod
+    def forward(ctx, means, scales, quats, opacities, colors, viewmat, intrinsics, background, early_termination):
+        fx, fy, cx, cy, W, H, near, far = intrinsics
+        cam = CameraParams(viewmat.detach().to("cpu", torch.float64).tolist(), fx, fy, cx, cy, W, H, near, far)
+        image, state = render_forward(means, scales, quats, opacities, colors, cam, background, early_termination)
+        ctx.state = state
+        ctx.view_device = viewmat.device
+        ctx.save_for_backward(means, scales, quats, colors)
+        ctx.mark_non_differentiable(state.final_T, state.n_contrib)
+        return image, state.final_T, state.n_contrib
+
+    @staticmethod
+    def backward(ctx, d_image, _d_T, _d_nc):
+        means, scales, quats, colors = ctx.saved_tensors
+        g = render_backward(ctx.state, means.contiguous(), scales.contiguous(), quats.contiguous(),
+                            colors.contiguous(), d_image)
+        return (g["d_mean"], g["d_scale"], g["d_quat"], g["d_opacity"], g["d_color"],
+                g["d_view"].to(ctx.view_device), None, None, None)
+
+
+def rasterize(means, scales, quats, opacities, colors, viewmat, fx, fy, cx, cy, width, height, near=0.01,
+              far=100.0, background=(0.0, 0.0, 0.0), early_termination=True):
+    """Autograd entry point: returns (image (H,W,3), final_T (H,W), n_contrib (H,W))."""
+    if not isinstance(viewmat, torch.Tensor):
+        viewmat = torch.as_tensor(viewmat, dtype=torch.float32)
+    return RasterizeGaussians.apply(means, scales, quats, opacities, colors, viewmat,
+                                    (fx, fy, cx, cy, int(width), int(height), near, far),
+                                    tuple(float(b) for b in background), bool(early_termination))

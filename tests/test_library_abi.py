@@ -1,0 +1,56 @@
+"""CPU: the C-ABI library builds, loads and exports every declared symbol."""
+
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "splat_b200.h")
+
+
+def header_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(gs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_lists_exports():
+    from paper_2312_02121_b200 import _lib
+    assert header_symbols() == sorted(_lib.EXPORTS)
+
+
+def test_library_exports_every_symbol():
+    from paper_2312_02121_b200 import _lib
+    L = _lib.load()
+    for name in header_symbols():
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for name in header_symbols():
+        assert re.search(rf"\bT {name}$", out, re.M), name
+
+
+def test_host_only_entry_points():
+    from paper_2312_02121_b200 import _lib
+    L = _lib.load()
+    assert L.gs_version() == 1
+    assert L.gs_scan_workspace_bytes(0) >= 16
+    assert L.gs_scan_workspace_bytes(10_000_000) > L.gs_scan_workspace_bytes(10)
+    assert L.gs_sort_workspace_bytes(1_000_000, 44) > 0
+    assert L.gs_project_bwd_workspace_bytes(1000) >= 4 * 12 * 4
+
+
+def test_kernels_are_sm100a():
+    from paper_2312_02121_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out, out
+
+
+def test_product_path_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2312_02121_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
+                assert "splat_oracle" not in txt, f
