@@ -1,0 +1,501 @@
+#!/usr/bin/env python
+"""Benchmark: differentiable Gaussian-splatting fwd+bwd on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One "step" = on every rank, the full hot path for that rank's view(s):
+project -> scan/emit/sort/ranges -> raster fwd -> raster bwd -> projection
+bwd, plus (N > 1) one NCCL sum-allreduce of the 14 fp32 gradients per
+Gaussian.  Inputs are seeded synthetic scenes with BASELINE.json's
+distributions (paper_2312_02121_b200/scenes.py).  Default workload: config 1
+(100k Gaussians, 800x800), one view per rank (weak scaling: rank r renders
+camera r of a ring; rank 0's camera is config 1's own).  --config 3 runs the
+32-view batch split across ranks (strong scaling).
+
+Rank 0 prints ONE JSON line (keys documented in DESIGN.md §Measurement).
+`--impl reference` times the CPU oracle port (oracle/, fp64, all host
+threads) on the same workload and prints the same line with "impl":
+"reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd frames/sec and Gaussian-pixel evals/s at 1/2/4/8 B200 (vs roofline)"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", type=int, default=1)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def views_for(cfg, spec, world, rank):
+    """(camera, d_image) pairs this rank renders each step."""
+    import numpy as np
+    from paper_2312_02121_b200.scenes import CameraSpec, look_at
+
+    if cfg == 3:
+        nv = len(spec.cameras)
+        idx = list(range(rank, nv, world))
+        return [(spec.cameras[i], spec.d_images[i]) for i in idx]
+    base = spec.cameras[0]
+    if rank == 0:
+        return [(base, spec.d_images[0])]
+    rng = np.random.default_rng(1000 + rank)
+    center = -base.view[:3, :3].T @ base.view[:3, 3]
+    dist = float(np.linalg.norm(center))
+    while True:
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        if abs(d[1]) <= 0.99:
+            break
+    cam = CameraSpec(look_at(dist * d), base.fx, base.fy, base.cx, base.cy, base.width, base.height,
+                     base.near, base.far)
+    dimg = rng.normal(size=(base.height, base.width, 3)).astype(np.float32)
+    return [(cam, dimg)]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=1)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def load_traffic():
+    """Per-launch DRAM bytes from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_02121_b200 import ops
+    from paper_2312_02121_b200.scenes import make_config
+
+    world, rank, local = dist_env()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = args.config
+    spec = make_config(cfg)
+    views = views_for(cfg, spec, world, rank)
+    n = spec.n
+    t = lambda a: torch.as_tensor(a, device=dev)
+    params = [t(spec.means), t(spec.scales), t(spec.quats), t(spec.opacities), t(spec.colors)]
+    cams = [ops.CameraParams.of(c) for c, _ in views]
+    d_imgs = [t(d) for _, d in views]
+    bg = (0.0, 0.0, 0.0)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, device=dev, dtype=torch.float32)
+    grad_flat = torch.empty((n, 14), device=dev, dtype=torch.float32)
+    stream = torch.cuda.current_stream()
+
+    stage_names = ("project", "bin_sort", "raster_fwd", "raster_bwd", "project_bwd", "allreduce")
+
+    def frame(cam, d_img, ev=None):
+        m, s, q, o, c = params
+        rec = (lambda k: ev[k].record(stream)) if ev is not None else (lambda k: None)
+        rec(0)
+        status = torch.full((1,), -1, device=dev, dtype=torch.int64)
+        proj = ops.project(m, s, q, o, cam, status=status)
+        rec(1)
+        bins = ops.bin_sort(proj, cam, status)
+        rec(2)
+        image, final_T, nc = ops.raster_fwd(proj, bins, c, cam, bg, True)
+        rec(3)
+        st = ops.FrameState(cam, bg, True, proj, bins, final_T, nc)
+        d_rgbo, d_geo, d_c11 = ops.raster_bwd(st, c, d_img)
+        rec(4)
+        dm, ds, dq, dv = ops.project_bwd(m, s, q, cam, proj.tiles, d_geo, d_c11)
+        rec(5)
+        return bins.n_isect, (dm, ds, dq, d_rgbo)
+
+    def step(ev_list=None):
+        acc = None
+        isect = 0
+        for vi, (cam, d_img) in enumerate(zip(cams, d_imgs)):
+            ev = ev_list[vi] if ev_list is not None else None
+            ni, (dm, ds, dq, d_rgbo) = frame(cam, d_img, ev)
+            isect += ni
+            if acc is None:
+                grad_flat[:, 0:3].copy_(dm)
+                grad_flat[:, 3:6].copy_(ds)
+                grad_flat[:, 6:10].copy_(dq)
+                grad_flat[:, 10:14].copy_(d_rgbo)
+                acc = True
+            else:
+                grad_flat[:, 0:3].add_(dm)
+                grad_flat[:, 3:6].add_(ds)
+                grad_flat[:, 6:10].add_(dq)
+                grad_flat[:, 10:14].add_(d_rgbo)
+        if world > 1:
+            dist.all_reduce(grad_flat)
+        return isect
+
+    # roofline numerators: evaluation-class counts (one counted pass, untimed)
+    counts_f = np.zeros(4, np.int64)
+    counts_b = np.zeros(3, np.int64)
+    for cam, d_img in zip(cams, d_imgs):
+        m, s, q, o, c = params
+        img, st = ops.render_forward(m, s, q, o, c, cam, bg, True, counts=True)
+        g = ops.render_backward(st, m, s, q, c, d_img, counts=True)
+        counts_f += st.counts_fwd.cpu().numpy()
+        counts_b += g["counts"].cpu().numpy()
+    n_isect_total = 0
+
+    for _ in range(max(args.warmup, 0)):
+        n_isect_total = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    step_ms = []
+    stage_ms = np.zeros(6)
+    for k in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (untimed)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev_list = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in cams]
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n_isect_total = step(ev_list)
+        e_ar = torch.cuda.Event(enable_timing=True)
+        e_ar.record(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        for ev in ev_list:
+            for j in range(5):
+                stage_ms[j] += ev[j].elapsed_time(ev[j + 1])
+        stage_ms[5] += ev_list[-1][5].elapsed_time(e_ar)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    stage_ms /= max(args.steps, 1)
+    frames_per_step = len(cams) * world if cfg != 3 else len(spec.cameras)
+    ms_per_step = total_ms / max(args.steps, 1)
+    fps = frames_per_step / (ms_per_step / 1e3)
+    evals_rank = float(counts_f[0] + counts_b[0])
+    evals_step = evals_rank
+    if world > 1:
+        ev_t = torch.tensor([evals_rank], device=dev, dtype=torch.float64)
+        dist.all_reduce(ev_t)
+        evals_step = float(ev_t.item())
+    evals_per_s = evals_step / (ms_per_step / 1e3)
+
+    # ---------------- e2e: public autograd API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, spec, views, dev, world)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_src = measured_peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 128.0 * sms * sm_max * 1e6  # lane-ops/s, FMA = 1 op
+    # algorithmic work per view (SURVEY.md §8d formulas)
+    nv = len(cams)
+    F_fwd = 8 * counts_f[0] + 4 * counts_f[1] + 3 * counts_f[2] + 4 * counts_f[3]
+    F_bwd = 8 * counts_b[0] + 4 * counts_b[1] + 42 * counts_b[2]
+    n_tiles = sum(c.tiles_x * c.tiles_y for c in cams)
+    I = n_isect_total
+    passes = math.ceil((32 + ops.tile_bits(cams[0].tiles_x * cams[0].tiles_y)) / 8)
+    bytes_proj = 80 * n * nv
+    bytes_sort = (8 * n + 24 * n) * nv + 12 * I + I * (8 + 24 * passes) + 8 * I + 8 * n_tiles
+    bytes_pbwd = 104 * n * nv
+    hbm = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
+    st = {}
+    for name, ms in zip(stage_names, stage_ms):
+        st[name] = {"ms": round(float(ms), 4)}
+    st["project"].update(bound="hbm", achieved_gbs=bytes_proj / (stage_ms[0] / 1e3) / 1e9)
+    st["bin_sort"].update(bound="hbm", achieved_gbs=bytes_sort / (stage_ms[1] / 1e3) / 1e9,
+                          note="includes the 16-byte D2H read of the intersection count")
+    st["raster_fwd"].update(bound="fp32", achieved_tops=F_fwd / (stage_ms[2] / 1e3) / 1e12)
+    st["raster_bwd"].update(bound="fp32", achieved_tops=F_bwd / (stage_ms[3] / 1e3) / 1e12)
+    st["project_bwd"].update(bound="hbm", achieved_gbs=bytes_pbwd / (stage_ms[4] / 1e3) / 1e9)
+    for k in ("project", "bin_sort", "project_bwd"):
+        st[k]["frac"] = st[k]["achieved_gbs"] * 1e9 / hbm
+    for k in ("raster_fwd", "raster_bwd"):
+        st[k]["frac"] = st[k]["achieved_tops"] * 1e12 / fp32_peak
+    dom = max(("raster_fwd", "raster_bwd", "project", "bin_sort", "project_bwd"), key=lambda k: stage_ms[
+        stage_names.index(k)])
+    traffic = load_traffic()
+    if st[dom]["bound"] == "fp32":
+        roof = {"bound": "fp32", "kernel": dom, "achieved": round(st[dom]["achieved_tops"], 3),
+                "peak": round(fp32_peak / 1e12, 3), "unit": "Tlane-op/s (FP32, FMA=1)",
+                "frac": round(st[dom]["frac"], 4),
+                "peak_at_measured_clock": round(128.0 * sms * (clocks["sm_mhz"] or sm_max) * 1e6 / 1e12, 3)
+                if clocks else None,
+                "peak_source": f"128 lanes x {sms} SMs x {sm_max:.0f} MHz ({peak_src} sm_max)"}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(st[dom]["achieved_gbs"], 1),
+                "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s", "frac": round(st[dom]["frac"], 4),
+                "peak_source": peak_src}
+    roof["traffic"] = traffic.get(dom)
+    roof["algorithmic_work_per_launch"] = {
+        "raster_fwd": int(F_fwd // nv), "raster_bwd": int(F_bwd // nv), "project": 80 * n,
+        "project_bwd": 104 * n}.get(dom)
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(spec, views[:1], sample_frames=1)
+
+    from paper_2312_02121_b200.scenes import config_sizes
+    sz = config_sizes(cfg)
+    out = {
+        "metric": METRIC, "value": round(fps, 3), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "strong" if cfg == 3 else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded, BASELINE.json distributions; scenes.py)",
+        "config": {"workload": f"config{cfg}", "gaussians": n, "image": f"{sz['width']}x{sz['height']}",
+                   "views_per_step": frames_per_step, "views_per_rank": len(cams),
+                   "early_termination": True, "background": "black",
+                   "parallelism": f"view-sharded x{world}" + (" + NCCL allreduce 14 fp32/Gaussian" if world > 1 else ""),
+                   "l2": "flushed between timed steps (256 MiB write, untimed)"},
+        "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
+        "intersections_per_step_rank0": int(I),
+        "e2e": e2e,
+        "gpu_launches": int(args.steps * len(cams) * (9 + passes)),
+        "roofline": roof,
+        "stages": st,
+        "counts": {"E_f": int(counts_f[0]), "E_f_sigma": int(counts_f[1]), "E_f_alpha": int(counts_f[2]),
+                   "E_f_commit": int(counts_f[3]), "E_b": int(counts_b[0]), "E_b_sigma": int(counts_b[1]),
+                   "E_b_contrib": int(counts_b[2]), "views": nv},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "impl": "ours",
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, spec, views, dev, world):
+    """Same metric through the public autograd API: pinned host params and
+    upstream gradient are copied H2D inside the timed region, the parameter
+    gradients are read back D2H; CUDA events + synchronize."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_02121_b200 import ops
+
+    host = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in
+            (spec.means, spec.scales, spec.quats, spec.opacities, spec.colors)]
+    dimgs = [torch.from_numpy(np.ascontiguousarray(d)).pin_memory() for _, d in views]
+    out_host = torch.empty((spec.n, 14), dtype=torch.float32).pin_memory()
+    cams = [c for c, _ in views]
+    h2d = sum(h.numel() * 4 for h in host) + sum(d.numel() * 4 for d in dimgs)
+    d2h = out_host.numel() * 4
+
+    def one():
+        dp = [h.to(dev, non_blocking=True).requires_grad_(True) for h in host]
+        acc = None
+        for cam, dh in zip(cams, dimgs):
+            d = dh.to(dev, non_blocking=True)
+            img, _, _ = ops.rasterize(*dp, torch.as_tensor(cam.view, dtype=torch.float32), cam.fx, cam.fy, cam.cx,
+                                      cam.cy, cam.width, cam.height, cam.near, cam.far)
+            img.backward(d)
+        g = torch.cat([dp[0].grad, dp[1].grad, dp[2].grad, dp[3].grad[:, None], dp[4].grad], dim=1)
+        if world > 1:
+            dist.all_reduce(g)
+        out_host.copy_(g, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(max(2, args.warmup // 2)):
+        one()
+    ms = []
+    steps = max(3, args.steps // 2)
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        one()
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    total = sum(ms)
+    if world > 1:
+        tt = torch.tensor([total], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total = float(tt.item())
+    frames = len(cams) * world if len(spec.cameras) == 1 else len(spec.cameras)
+    return {"value": round(frames / (total / steps / 1e3), 3), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "api": "paper_2312_02121_b200.ops.rasterize + backward"}
+
+
+def cpu_baseline(spec, views, sample_frames=1, nthreads=0):
+    """fp64 oracle port (oracle/) on the host cores: full fwd+bwd frames."""
+    import numpy as np
+
+    import oracle as O
+
+    nth = nthreads or (os.cpu_count() or 1)
+    f = lambda a: np.asarray(a, np.float64)
+    args = [f(spec.means), f(spec.scales), f(spec.quats), f(spec.opacities), f(spec.colors)]
+    t0 = time.perf_counter()
+    for cam, d in views[:sample_frames]:
+        oc = O.Camera.of(cam)
+        fw = O.render(*args, oc, np.zeros(3), True, nthreads=nth)
+        O.scene_backward(*args, oc, np.zeros(3), fw, f(d), nthreads=nth)
+    dt = time.perf_counter() - t0
+    nf = len(views[:sample_frames])
+    return {"value": round(nf / dt, 5), "unit": "frames/s", "cores": nth, "kind": "port",
+            "sample": f"{nf} full fwd+bwd frame(s) of the same workload (oracle/splat_oracle.c, fp64, OpenMP)",
+            "seconds": round(dt, 3)}
+
+
+# ------------------------------------------------------------ reference arm
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    from paper_2312_02121_b200.scenes import make_config
+
+    spec = make_config(args.config)
+    views = views_for(args.config, spec, 1, 0)
+    nth = os.cpu_count() or 1
+    # each step: one full fwd+bwd frame (bounded: ~1-3 s per frame at config 1)
+    for _ in range(min(args.warmup, 1)):
+        cpu_baseline(spec, views, 1, nth)
+    steps = max(1, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        cpu_baseline(spec, views, 1, nth)
+    dt = time.perf_counter() - t0
+    fps = steps / dt
+    out = {"metric": METRIC, "value": round(fps, 5), "unit": "frames/s", "n_gpus": args.gpus, "steps": steps,
+           "warmup": min(args.warmup, 1), "ms_per_step": round(dt / steps * 1e3, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; scenes.py)",
+           "config": {"workload": f"config{args.config}", "gaussians": spec.n},
+           "impl": "reference",
+           "cpu_baseline": {"value": round(fps, 5), "unit": "frames/s", "cores": nth, "kind": "port",
+                            "sample": "full fwd+bwd frame per step (oracle/splat_oracle.c, fp64, OpenMP)"},
+           "e2e": {"value": round(fps, 5), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

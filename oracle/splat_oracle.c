@@ -262,6 +262,7 @@ void orc_bin_fill(int64_t n, const int8_t* visible, const double* mean2d, const 
     free(fill);
     if (sort) {
         g_sort_depth = depth;
+#pragma omp parallel for schedule(dynamic, 16)
         for (int64_t t = 0; t < nt; ++t)
             qsort(bin_idx + bin_ptr[t], (size_t)(bin_ptr[t + 1] - bin_ptr[t]), sizeof(int64_t), cmp_depth_index);
     }

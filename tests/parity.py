@@ -188,3 +188,49 @@ def projection_diffs(gpu_out, pr):
     return dict(n_vis_gpu=int(vis_g.sum()), n_vis_oracle=int(vis_o.sum()), n_vis_diff=int((vis_g != vis_o).sum()),
                 n_radius_diff=int(len(rad_diff)), causes=causes, mean2d_max_abs=float(m2),
                 cov2d_max_rel=float(cov_rel))
+
+
+def classify_bins(g_ptr, g_idx, r_ptr, r_idx, gpu_depth, gpu_rect_fn=None, ref_rect_fn=None):
+    """Explain every tile whose GPU list differs from the reference's.
+
+    Causes: "depth-tie" (same members; the order differs only among splats
+    whose fp32 depths are equal, which the GPU orders by index while the
+    fp64 reference orders by the unrounded depth) and "rect" (membership
+    differs because the fp32 and fp64 tile rectangles differ, i.e. a radius
+    ceil / mean2d borderline case).  Anything else is "unexplained".
+    """
+    n_tiles = len(g_ptr) - 1
+    causes = {"depth-tie": 0, "rect": 0, "unexplained": 0}
+    details = []
+    for t in range(n_tiles):
+        a = g_idx[g_ptr[t]:g_ptr[t + 1]]
+        b = r_idx[r_ptr[t]:r_ptr[t + 1]]
+        if len(a) == len(b) and np.array_equal(a, b):
+            continue
+        if set(a.tolist()) == set(b.tolist()):
+            key = sorted(b.tolist(), key=lambda j: (np.float32(gpu_depth[j]), j))
+            if key == a.tolist():
+                causes["depth-tie"] += 1
+                details.append(("depth-tie", t))
+                continue
+            causes["unexplained"] += 1
+            details.append(("order", t))
+            continue
+        sym = set(a.tolist()) ^ set(b.tolist())
+        ok = gpu_rect_fn is not None and all(gpu_rect_fn(j, t) != ref_rect_fn(j, t) for j in sym)
+        causes["rect" if ok else "unexplained"] += 1
+        details.append(("rect" if ok else "membership", t, sorted(sym)[:5]))
+    return causes, details
+
+
+def rect_contains(mean2d, radius, width, height):
+    tx_n = (width + 15) // 16
+    ty_n = (height + 15) // 16
+
+    def fn(j, t):
+        tx, ty = t % tx_n, t // tx_n
+        x, y, r = float(mean2d[j][0]), float(mean2d[j][1]), int(radius[j])
+        x0 = max(0, int(np.floor((x - r) / 16))); x1 = min(tx_n - 1, int(np.floor((x + r) / 16)))
+        y0 = max(0, int(np.floor((y - r) / 16))); y1 = min(ty_n - 1, int(np.floor((y + r) / 16)))
+        return x0 <= tx <= x1 and y0 <= ty <= y1
+    return fn
