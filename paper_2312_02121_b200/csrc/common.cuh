@@ -65,6 +65,12 @@ __device__ __forceinline__ float splat_sigma(float dx, float dy, float hA, float
     return __fmaf_rn(dx, t, __fmul_rn(u, dy));
 }
 
+// Same expression with hA*dx hoisted (pixels sharing a column share dx):
+// bit-identical to splat_sigma(dx, dy, hA, B, hC) when hAdx == hA*dx.
+__device__ __forceinline__ float splat_sigma_h(float dx, float hAdx, float dy, float B, float hC) {
+    return __fmaf_rn(dx, __fmaf_rn(B, dy, hAdx), __fmul_rn(__fmul_rn(hC, dy), dy));
+}
+
 // exp(-sigma) shared by forward and backward (sg/raster_forward.py:136,
 // sg/raster_backward.py:68).
 __device__ __forceinline__ float splat_exp_neg(float sigma) {

@@ -76,7 +76,13 @@ def test_forward_matches_reference(case):
     t_err = np.abs(out["final_T"] - g["final_T"])
     safe = ref["margin"] >= FLIP_EPS
     assert t_err[safe].max(initial=0.0) <= 1e-4, name
-    assert np.array_equal(out["n_contrib"][safe], g["n_contrib"][safe]), name
+    # n_contrib is a bin POSITION: compare it stage-isolated (oracle on the
+    # GPU's bins), since fp32 depth ties may permute equal-depth entries
+    iso = O.raster_fwd(cam.width, cam.height, out["bin_ptr"], out["bin_idx"], out["mean2d"], out["cov2d"],
+                       g["inputs"][3], g["inputs"][4], g["background"], g["et"], margins=True)
+    safe_iso = iso["margin"] >= FLIP_EPS
+    assert np.array_equal(out["n_contrib"][safe_iso], iso["n_contrib"][safe_iso]), name
+    assert np.abs(out["image"] - iso["image"]).max(axis=-1)[safe_iso].max(initial=0.0) <= 1e-4, name
 
 
 def test_forward_counts_match_oracle(case):
