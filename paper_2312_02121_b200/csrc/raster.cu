@@ -1,23 +1,27 @@
 // raster.cu -- stage 3 (front-to-back compositing forward) and stage 4
 // (back-to-front replay backward).
 //
-// Layout: one CTA per 16x16 tile, 128 threads.  Warp w owns the 8x8 quadrant
-// (w&1, w>>1) of the tile; lane l owns the two pixels (l&7, l>>3) and
-// (l&7, (l>>3)+4) of that quadrant, so the two pixels share a column (and the
-// dx of every splat) and a warp covers a compact 8x8 block (good early-stop
-// coherence forward, dense contributions backward).  The tile's sorted splat
-// records are staged in shared memory 128 at a time.  Bound: FP32 issue.
+// Layout: one CTA per 16x16 tile, 256/PX threads, PX pixels per thread.
+// Lane l of warp w owns column (w&1)*8 + (l&7) and the PX rows
+// (w>>1)*4*PX + (l>>3) + 4k, k < PX, so a thread's pixels share a column
+// (hence dx and hA*dx of every splat) and a warp covers a compact 8 x 4*PX
+// block.  The tile's sorted splat records are staged in shared memory
+// RB = 128 at a time.  Bound: FP32 issue (DESIGN.md roofline).
+//
+// Retired pixels (forward: out of the image or early-terminated) get
+// py = +inf, so their sigma is inf/NaN and fails the cut: the hot loop needs
+// no per-pixel "done" test.
 #include "common.cuh"
 
 namespace gs {
 
-constexpr int RT = 128;  // threads per CTA == splats per staged batch
+constexpr int RB = 128;  // splats per staged batch
 
 struct SplatSmem {
-    float4 a[RT];  // x, y, hA = A/2, B
-    float4 b[RT];  // hC = C/2, opacity, r, g
-    float c[RT];   // blue
-    uint32_t id[RT];
+    float4 a[RB];  // x, y, hA = A/2, B
+    float4 b[RB];  // hC = C/2, opacity, r, g
+    float c[RB];   // blue
+    uint32_t id[RB];
 };
 
 __device__ __forceinline__ void stage_splat(SplatSmem& s, int k, uint32_t id, const float4* __restrict__ xydr,
@@ -31,119 +35,131 @@ __device__ __forceinline__ void stage_splat(SplatSmem& s, int k, uint32_t id, co
     s.id[k] = id;
 }
 
-struct PixMap {
-    int col, row0, row1;
-};
-
-__device__ __forceinline__ PixMap pixel_map(int tile, int tiles_x) {
-    const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    PixMap m;
-    m.col = tx * TILE + (warp & 1) * 8 + (lane & 7);
-    m.row0 = ty * TILE + (warp >> 1) * 8 + (lane >> 3);
-    m.row1 = m.row0 + 4;
-    return m;
+// Keep a loop-invariant value in a register (stops ptxas from
+// rematerialising it inside the hot loop).
+__device__ __forceinline__ float pin(float x) {
+    asm volatile("" : "+f"(x));
+    return x;
 }
 
-struct FwdPix {
-    float T, cr, cg, cb;
-    int nc;
-    bool done;
-};
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
-// One visible-candidate evaluation of sg/raster_forward.py:136-150 for one
-// pixel; sigma already passed the cut.
-template <bool ET>
-__device__ __forceinline__ void fwd_commit(FwdPix& p, float sigma, const float4& bq, float blue, int pos1,
-                                           unsigned long long& e_a, unsigned long long& e_c, bool count) {
-    const float e = splat_exp_neg(sigma);
-    const float alpha = fminf(__fmul_rn(bq.y, e), ALPHA_MAX);
-    if (alpha >= ALPHA_MIN) {
-        if (count) ++e_a;
-        const float nT = __fmul_rn(p.T, __fsub_rn(1.f, alpha));
-        if (ET && nT < T_MIN) {
-            p.done = true;  // the stopping splat is not composited (:141-144)
-            return;
-        }
-        if (count) ++e_c;
-        const float w = __fmul_rn(alpha, p.T);
-        p.cr = __fmaf_rn(w, bq.z, p.cr);
-        p.cg = __fmaf_rn(w, bq.w, p.cg);
-        p.cb = __fmaf_rn(w, blue, p.cb);
-        p.T = nT;
-        p.nc = pos1;
+template <int PX>
+struct TileGeom {
+    static constexpr int THREADS = TILE_PIX / PX;
+    int col;
+    int row[PX];
+    __device__ __forceinline__ TileGeom(int tile, int tiles_x) {
+        const int tx = tile % tiles_x, ty = tile / tiles_x;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        col = tx * TILE + (warp & 1) * 8 + (lane & 7);
+#pragma unroll
+        for (int k = 0; k < PX; ++k) row[k] = ty * TILE + (warp >> 1) * 4 * PX + (lane >> 3) + 4 * k;
     }
-}
+};
 
+// ============================================================ forward
 // sg/raster_forward.py:116-154 _composite_tile for one tile.
-template <bool ET, bool COUNT>
-__global__ void __launch_bounds__(RT) raster_fwd_kernel(const uint2* __restrict__ ranges,
-                                                        const uint32_t* __restrict__ sorted_vals,
-                                                        const float4* __restrict__ xydr,
-                                                        const float4* __restrict__ conic,
-                                                        const float* __restrict__ colors, float3 bg, int W, int H,
-                                                        int tiles_x, float* __restrict__ out_img,
-                                                        float* __restrict__ out_T, int* __restrict__ out_nc,
-                                                        unsigned long long* __restrict__ counts) {
+template <int PX, bool ET, bool COUNT>
+__global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_fwd_kernel(
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ sorted_vals, const float4* __restrict__ xydr,
+    const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg, int W, int H, int tiles_x,
+    float* __restrict__ out_img, float* __restrict__ out_T, int* __restrict__ out_nc,
+    unsigned long long* __restrict__ counts) {
+    constexpr int NT = TileGeom<PX>::THREADS;
+    constexpr int PER = RB / NT;  // splats staged per thread per batch
     __shared__ SplatSmem s;
     const int tile = blockIdx.x;
-    const PixMap pm = pixel_map(tile, tiles_x);
-    const bool in0 = pm.col < W && pm.row0 < H;
-    const bool in1 = pm.col < W && pm.row1 < H;
-    const float px = (float)pm.col + 0.5f;
-    const float py0 = (float)pm.row0 + 0.5f, py1 = (float)pm.row1 + 0.5f;
+    const TileGeom<PX> geo(tile, tiles_x);
+    const float INF = __int_as_float(0x7f800000);
+    const float px = pin((float)geo.col + 0.5f);
+    float py[PX], T[PX], cr[PX], cg[PX], cb[PX];
+    int nc[PX];
+    unsigned done = 0;
+#pragma unroll
+    for (int q = 0; q < PX; ++q) {
+        const bool in = geo.col < W && geo.row[q] < H;
+        py[q] = pin(in ? (float)geo.row[q] + 0.5f : INF);
+        done |= in ? 0u : (1u << q);
+        T[q] = 1.f; cr[q] = 0.f; cg[q] = 0.f; cb[q] = 0.f; nc[q] = 0;
+    }
+    constexpr unsigned ALL = (1u << PX) - 1u;
     const uint2 rg = ranges[tile];
     const int start = (int)rg.x, end = (int)rg.y;
-
-    FwdPix p0{1.f, 0.f, 0.f, 0.f, 0, !in0};
-    FwdPix p1{1.f, 0.f, 0.f, 0.f, 0, !in1};
     unsigned long long e_f = 0, e_s = 0, e_a = 0, e_c = 0;
-    for (int b0 = start; b0 < end; b0 += RT) {
-        if (__syncthreads_count(!(p0.done && p1.done)) == 0) break;
-        const int j = b0 + (int)threadIdx.x;
-        if (j < end) stage_splat(s, threadIdx.x, sorted_vals[j], xydr, conic, colors);
+
+    for (int b0 = start; b0 < end; b0 += RB) {
+        if (__syncthreads_count(done != ALL) == 0) break;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int k = u * NT + (int)threadIdx.x;
+            if (b0 + k < end) stage_splat(s, k, sorted_vals[b0 + k], xydr, conic, colors);
+        }
         __syncthreads();
-        const int cnt = min(RT, end - b0);
+        if (__all_sync(0xffffffffu, done == ALL)) continue;  // whole warp finished: only help staging
+        const int cnt = min(RB, end - b0);
         const int pos_base = b0 - start + 1;
+#pragma unroll 2
         for (int k = 0; k < cnt; ++k) {
-            if (p0.done && p1.done) break;
             const float4 a = s.a[k];
             const float hC = s.b[k].x;
             const float dx = __fsub_rn(px, a.x);
             const float hAdx = __fmul_rn(a.z, dx);
-            const float dy0 = __fsub_rn(py0, a.y);
-            const float dy1 = __fsub_rn(py1, a.y);
-            const float s0 = splat_sigma_h(dx, hAdx, dy0, a.w, hC);
-            const float s1 = splat_sigma_h(dx, hAdx, dy1, a.w, hC);
-            const bool v0 = !p0.done && s0 <= SIGMA_CUT;
-            const bool v1 = !p1.done && s1 <= SIGMA_CUT;
+            float sg[PX];
+            bool vis[PX];
+            bool any = false;
+#pragma unroll
+            for (int q = 0; q < PX; ++q) {
+                sg[q] = splat_sigma_h(dx, hAdx, __fsub_rn(py[q], a.y), a.w, hC);
+                vis[q] = sg[q] <= SIGMA_CUT;  // false for retired pixels (py = inf)
+                any |= vis[q];
+            }
             if (COUNT) {
-                e_f += (!p0.done) + (!p1.done);
-                e_s += v0 + v1;
+                e_f += PX - __popc(done);
+#pragma unroll
+                for (int q = 0; q < PX; ++q) e_s += vis[q];
             }
-            if (v0 || v1) {
-                const float4 bq = s.b[k];
-                const float blue = s.c[k];
-                if (v0) fwd_commit<ET>(p0, s0, bq, blue, pos_base + k, e_a, e_c, COUNT);
-                if (v1) fwd_commit<ET>(p1, s1, bq, blue, pos_base + k, e_a, e_c, COUNT);
+            if (!__any_sync(0xffffffffu, any)) continue;
+            const float4 bq = s.b[k];
+            const float blue = s.c[k];
+#pragma unroll
+            for (int q = 0; q < PX; ++q) {
+                if (!vis[q]) continue;
+                const float e = splat_exp_neg(sg[q]);
+                const float alpha = fminf(__fmul_rn(bq.y, e), ALPHA_MAX);
+                if (!(alpha >= ALPHA_MIN)) continue;
+                if (COUNT) ++e_a;
+                const float nT = __fmul_rn(T[q], __fsub_rn(1.f, alpha));
+                if (ET && nT < T_MIN) {  // stop WITHOUT compositing (:141-144)
+                    py[q] = INF;
+                    done |= 1u << q;
+                    continue;
+                }
+                if (COUNT) ++e_c;
+                const float w = __fmul_rn(alpha, T[q]);
+                cr[q] = __fmaf_rn(w, bq.z, cr[q]);
+                cg[q] = __fmaf_rn(w, bq.w, cg[q]);
+                cb[q] = __fmaf_rn(w, blue, cb[q]);
+                T[q] = nT;
+                nc[q] = pos_base + k;
             }
+            if (ET && __all_sync(0xffffffffu, done == ALL)) break;
         }
     }
-    if (in0) {
-        const int p = pm.row0 * W + pm.col;
-        out_img[3 * p] = __fmaf_rn(bg.x, p0.T, p0.cr);
-        out_img[3 * p + 1] = __fmaf_rn(bg.y, p0.T, p0.cg);
-        out_img[3 * p + 2] = __fmaf_rn(bg.z, p0.T, p0.cb);
-        out_T[p] = p0.T;
-        out_nc[p] = p0.nc;
-    }
-    if (in1) {
-        const int p = pm.row1 * W + pm.col;
-        out_img[3 * p] = __fmaf_rn(bg.x, p1.T, p1.cr);
-        out_img[3 * p + 1] = __fmaf_rn(bg.y, p1.T, p1.cg);
-        out_img[3 * p + 2] = __fmaf_rn(bg.z, p1.T, p1.cb);
-        out_T[p] = p1.T;
-        out_nc[p] = p1.nc;
+#pragma unroll
+    for (int q = 0; q < PX; ++q) {
+        if (geo.col < W && geo.row[q] < H) {
+            const int p = geo.row[q] * W + geo.col;
+            out_img[3 * p] = __fmaf_rn(bg.x, T[q], cr[q]);
+            out_img[3 * p + 1] = __fmaf_rn(bg.y, T[q], cg[q]);
+            out_img[3 * p + 2] = __fmaf_rn(bg.z, T[q], cb[q]);
+            out_T[p] = T[q];
+            out_nc[p] = nc[q];
+        }
     }
     if (COUNT) {
 #pragma unroll
@@ -162,53 +178,10 @@ __global__ void __launch_bounds__(RT) raster_fwd_kernel(const uint2* __restrict_
     }
 }
 
-struct BwdPix {
-    float T, S0, S1, S2, g0, g1, g2;
-    int nc;
-};
+// ============================================================ backward
 
-// Accumulators of the 9 per-splat gradient values of one lane.
-struct Acc9 {
-    float v[9];
-};
-
-// sg/raster_backward.py:62-108 for one pixel and one splat whose sigma passed
-// the cut and which is active (pos < n_contrib).
-__device__ __forceinline__ bool bwd_pixel(BwdPix& p, float sigma, float dx, float dy, const float4& a,
-                                          const float4& bq, float blue, Acc9& acc) {
-    const float e = splat_exp_neg(sigma);
-    const float araw = __fmul_rn(bq.y, e);
-    const float alpha = fminf(araw, ALPHA_MAX);
-    if (!(alpha >= ALPHA_MIN)) return false;
-    const float inv = __frcp_rn(1.f - alpha);
-    const float th = p.T * inv;  // T before this splat (:75)
-    const float w = alpha * th;
-    acc.v[0] = fmaf(w, p.g0, acc.v[0]);
-    acc.v[1] = fmaf(w, p.g1, acc.v[1]);
-    acc.v[2] = fmaf(w, p.g2, acc.v[2]);
-    // d alpha = sum_k (c_k T_here - S_k / (1 - alpha)) g_k  (:86-90)
-    const float da = th * (bq.z * p.g0 + bq.w * p.g1 + blue * p.g2) - inv * (p.S0 * p.g0 + p.S1 * p.g1 + p.S2 * p.g2);
-    if (araw < ALPHA_MAX) {  // live (:91)
-        acc.v[3] = fmaf(da, e, acc.v[3]);
-        const float m = araw * da;  // = -d_sigma
-        const float y0 = 2.f * a.z * dx + a.w * dy;
-        const float y1 = a.w * dx + 2.f * bq.x * dy;
-        acc.v[4] = fmaf(m, y0, acc.v[4]);   // d mean2d = -d_sigma * y  (:97-98)
-        acc.v[5] = fmaf(m, y1, acc.v[5]);
-        const float hm = 0.5f * m;           // d cov2d = -1/2 d_sigma y y^T (:99-105)
-        acc.v[6] = fmaf(hm * y0, y0, acc.v[6]);
-        acc.v[7] = fmaf(hm * y0, y1, acc.v[7]);
-        acc.v[8] = fmaf(hm * y1, y1, acc.v[8]);
-    }
-    p.S0 = fmaf(w, bq.z, p.S0);
-    p.S1 = fmaf(w, bq.w, p.S1);
-    p.S2 = fmaf(w, blue, p.S2);
-    p.T = th;
-    return true;
-}
-
-// Transposed warp reduction of 8 values: after it, lane L with (L & 3) == 0
-// holds the warp total of value index L >> 2.  9 shuffles instead of 40.
+// Transposed warp reduction of 8 values: afterwards lane L with (L & 3) == 0
+// holds the warp total of value index L >> 2 (9 shuffles instead of 40).
 __device__ __forceinline__ float warp_reduce8(const float* v, int lane) {
     float r4[4], r2[2];
     const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
@@ -232,58 +205,66 @@ __device__ __forceinline__ float warp_reduce8(const float* v, int lane) {
     return r;
 }
 
-// sg/raster_backward.py:47-108 _backward_tile for one tile.  Per splat the
-// 9 gradient values of the warp's 64 pixels are summed per lane, transposed-
-// reduced across the warp, and 8 lanes (+1 for d_cov11) issue one vector of
-// global reductions per warp per Gaussian.
-template <bool COUNT>
-__global__ void __launch_bounds__(RT) raster_bwd_kernel(
+// sg/raster_backward.py:47-108 _backward_tile for one tile: seed T = final_T,
+// S = bg * final_T; walk pos = max(n_contrib)-1 .. 0 replaying the forward's
+// decisions (same sigma/exp code); contrib -> T_here = T/(1-alpha),
+// w = alpha T_here, dc += w g, d_alpha = T_here c.g - S.g/(1-alpha);
+// live (alpha_raw < 0.999) -> d_opacity += d_alpha e^-sigma, d_sigma =
+// -alpha_raw d_alpha, d_mean2d += -d_sigma y, d_cov2d += -d_sigma/2 y y^T with
+// y = conic * delta (full-matrix convention, :99-105); S += w c; T = T_here.
+// Per splat the warp's 9 sums are transposed-reduced and 8 (+1) lanes issue
+// one global reduction each: one atomic per warp per Gaussian value.
+template <int PX, bool COUNT>
+__global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ sorted_vals, const float4* __restrict__ xydr,
     const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg, int W, int H, int tiles_x,
     const float* __restrict__ final_T, const int* __restrict__ n_contrib, const float* __restrict__ d_img,
     float4* __restrict__ d_rgbo, float4* __restrict__ d_geo, float* __restrict__ d_c11,
     unsigned long long* __restrict__ counts) {
+    constexpr int NT = TileGeom<PX>::THREADS;
+    constexpr int PER = RB / NT;
+    constexpr int NW = NT / 32;
     __shared__ SplatSmem s;
-    __shared__ int s_max[RT / 32];
+    __shared__ int s_max[NW];
     const int tile = blockIdx.x;
-    const PixMap pm = pixel_map(tile, tiles_x);
-    const bool in0 = pm.col < W && pm.row0 < H;
-    const bool in1 = pm.col < W && pm.row1 < H;
-    const float px = (float)pm.col + 0.5f;
-    const float py0 = (float)pm.row0 + 0.5f, py1 = (float)pm.row1 + 0.5f;
+    const TileGeom<PX> geo(tile, tiles_x);
+    const float px = pin((float)geo.col + 0.5f);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float py[PX], T[PX], S0[PX], S1[PX], S2[PX], g0[PX], g1[PX], g2[PX];
+    int nc[PX];
+    int my_max = 0;
+#pragma unroll
+    for (int q = 0; q < PX; ++q) {
+        const bool in = geo.col < W && geo.row[q] < H;
+        py[q] = pin((float)geo.row[q] + 0.5f);
+        T[q] = 1.f; nc[q] = 0; g0[q] = 0.f; g1[q] = 0.f; g2[q] = 0.f;
+        if (in) {
+            const int p = geo.row[q] * W + geo.col;
+            T[q] = final_T[p];
+            nc[q] = n_contrib[p];
+            g0[q] = d_img[3 * p]; g1[q] = d_img[3 * p + 1]; g2[q] = d_img[3 * p + 2];
+        }
+        S0[q] = bg.x * T[q]; S1[q] = bg.y * T[q]; S2[q] = bg.z * T[q];
+        my_max = max(my_max, nc[q]);
+    }
+    const int warp_max = __reduce_max_sync(0xffffffffu, my_max);
+    if (lane == 0) s_max[warp] = warp_max;
     const uint2 rg = ranges[tile];
     const int start = (int)rg.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-
-    BwdPix p0{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0};
-    BwdPix p1{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0};
-    if (in0) {
-        const int p = pm.row0 * W + pm.col;
-        p0.T = final_T[p];
-        p0.nc = n_contrib[p];
-        p0.g0 = d_img[3 * p]; p0.g1 = d_img[3 * p + 1]; p0.g2 = d_img[3 * p + 2];
-    }
-    if (in1) {
-        const int p = pm.row1 * W + pm.col;
-        p1.T = final_T[p];
-        p1.nc = n_contrib[p];
-        p1.g0 = d_img[3 * p]; p1.g1 = d_img[3 * p + 1]; p1.g2 = d_img[3 * p + 2];
-    }
-    p0.S0 = bg.x * p0.T; p0.S1 = bg.y * p0.T; p0.S2 = bg.z * p0.T;
-    p1.S0 = bg.x * p1.T; p1.S1 = bg.y * p1.T; p1.S2 = bg.z * p1.T;
-    const int warp_max = __reduce_max_sync(0xffffffffu, max(p0.nc, p1.nc));
-    if (lane == 0) s_max[warp] = warp_max;
     __syncthreads();
     int max_nc = 0;
 #pragma unroll
-    for (int w = 0; w < RT / 32; ++w) max_nc = max(max_nc, s_max[w]);
+    for (int w = 0; w < NW; ++w) max_nc = max(max_nc, s_max[w]);
     unsigned long long e_s = 0, e_c = 0;
 
-    for (int bend = max_nc; bend > 0; bend -= RT) {
-        const int bstart = max(0, bend - RT);
+    for (int bend = max_nc; bend > 0; bend -= RB) {
+        const int bstart = max(0, bend - RB);
         __syncthreads();
-        const int k0 = (int)threadIdx.x;
-        if (bstart + k0 < bend) stage_splat(s, k0, sorted_vals[start + bstart + k0], xydr, conic, colors);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int k = u * NT + (int)threadIdx.x;
+            if (bstart + k < bend) stage_splat(s, k, sorted_vals[start + bstart + k], xydr, conic, colors);
+        }
         __syncthreads();
         const int kmax = min(bend, warp_max) - bstart;  // positions >= warp_max are inactive for this warp
         for (int k = kmax - 1; k >= 0; --k) {
@@ -292,26 +273,66 @@ __global__ void __launch_bounds__(RT) raster_bwd_kernel(
             const float hC = s.b[k].x;
             const float dx = __fsub_rn(px, a.x);
             const float hAdx = __fmul_rn(a.z, dx);
-            const float dy0 = __fsub_rn(py0, a.y);
-            const float dy1 = __fsub_rn(py1, a.y);
-            const float s0 = splat_sigma_h(dx, hAdx, dy0, a.w, hC);
-            const float s1 = splat_sigma_h(dx, hAdx, dy1, a.w, hC);
-            const bool v0 = pos < p0.nc && s0 <= SIGMA_CUT;
-            const bool v1 = pos < p1.nc && s1 <= SIGMA_CUT;
-            if (COUNT) e_s += v0 + v1;
-            if (!__any_sync(0xffffffffu, v0 || v1)) continue;
+            float sg[PX], dy[PX];
+            bool v[PX];
+            bool any = false;
+#pragma unroll
+            for (int q = 0; q < PX; ++q) {
+                dy[q] = __fsub_rn(py[q], a.y);
+                sg[q] = splat_sigma_h(dx, hAdx, dy[q], a.w, hC);
+                v[q] = pos < nc[q] && sg[q] <= SIGMA_CUT;
+                any |= v[q];
+            }
+            if (COUNT) {
+#pragma unroll
+                for (int q = 0; q < PX; ++q) e_s += v[q];
+            }
+            if (!__any_sync(0xffffffffu, any)) continue;
             const float4 bq = s.b[k];
             const float blue = s.c[k];
-            Acc9 acc;
+            const float A2 = 2.f * a.z, C2 = 2.f * bq.x;
+            float acc[9];
 #pragma unroll
-            for (int q = 0; q < 9; ++q) acc.v[q] = 0.f;
-            bool c0 = false, c1 = false;
-            if (v0) c0 = bwd_pixel(p0, s0, dx, dy0, a, bq, blue, acc);
-            if (v1) c1 = bwd_pixel(p1, s1, dx, dy1, a, bq, blue, acc);
-            if (COUNT) e_c += c0 + c1;
-            if (!__any_sync(0xffffffffu, c0 || c1)) continue;
-            const float r = warp_reduce8(acc.v, lane);
-            float c11 = acc.v[8];
+            for (int j = 0; j < 9; ++j) acc[j] = 0.f;
+            bool anyc = false;
+#pragma unroll
+            for (int q = 0; q < PX; ++q) {
+                if (!v[q]) continue;
+                const float e = splat_exp_neg(sg[q]);
+                const float araw = __fmul_rn(bq.y, e);
+                const float alpha = fminf(araw, ALPHA_MAX);
+                if (!(alpha >= ALPHA_MIN)) continue;
+                anyc = true;
+                if (COUNT) ++e_c;
+                const float inv = rcp_approx(1.f - alpha);
+                const float th = T[q] * inv;  // T before this splat (:75)
+                const float w = alpha * th;
+                acc[0] = fmaf(w, g0[q], acc[0]);
+                acc[1] = fmaf(w, g1[q], acc[1]);
+                acc[2] = fmaf(w, g2[q], acc[2]);
+                const float cdot = bq.z * g0[q] + bq.w * g1[q] + blue * g2[q];
+                const float sdot = S0[q] * g0[q] + S1[q] * g1[q] + S2[q] * g2[q];
+                const float da = th * cdot - inv * sdot;
+                if (araw < ALPHA_MAX) {  // live (:91)
+                    acc[3] = fmaf(da, e, acc[3]);
+                    const float m = araw * da;  // = -d_sigma
+                    const float y0 = A2 * dx + a.w * dy[q];
+                    const float y1 = a.w * dx + C2 * dy[q];
+                    const float my0 = m * y0, hm = 0.5f * m;
+                    acc[4] += my0;
+                    acc[5] = fmaf(m, y1, acc[5]);
+                    acc[6] = fmaf(hm * y0, y0, acc[6]);
+                    acc[7] = fmaf(hm * y0, y1, acc[7]);
+                    acc[8] = fmaf(hm * y1, y1, acc[8]);
+                }
+                S0[q] = fmaf(w, bq.z, S0[q]);
+                S1[q] = fmaf(w, bq.w, S1[q]);
+                S2[q] = fmaf(w, blue, S2[q]);
+                T[q] = th;
+            }
+            if (!__any_sync(0xffffffffu, anyc)) continue;
+            const float r = warp_reduce8(acc, lane);
+            float c11 = acc[8];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) c11 += __shfl_xor_sync(0xffffffffu, c11, o);
             const uint32_t id = s.id[k];
@@ -325,7 +346,9 @@ __global__ void __launch_bounds__(RT) raster_bwd_kernel(
         }
     }
     if (COUNT) {
-        unsigned long long e_b = (unsigned long long)(p0.nc + p1.nc);
+        unsigned long long e_b = 0;
+#pragma unroll
+        for (int q = 0; q < PX; ++q) e_b += (unsigned long long)nc[q];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             e_b += __shfl_xor_sync(0xffffffffu, e_b, o);
@@ -338,6 +361,44 @@ __global__ void __launch_bounds__(RT) raster_bwd_kernel(
             atomicAdd(&counts[2], e_c);
         }
     }
+}
+
+// Pixels per thread (2 or 4); GS_RASTER_PX overrides for experiments.
+static int raster_px(const char* which) {
+    static int fwd = -1, bwd = -1;
+    int& v = which[0] == 'f' ? fwd : bwd;
+    if (v < 0) {
+        v = 4;
+        const char* e = getenv(which[0] == 'f' ? "GS_RASTER_PX_FWD" : "GS_RASTER_PX_BWD");
+        if (e && (atoi(e) == 2 || atoi(e) == 4)) v = atoi(e);
+    }
+    return v;
+}
+
+template <int PX>
+static void launch_fwd(bool et, bool cnt, unsigned nt, cudaStream_t s, const uint2* ranges, const uint32_t* vals,
+                       const float4* xydr, const float4* conic, const float* colors, float3 bg, int W, int H,
+                       int tiles_x, float* img, float* T, int* nc, unsigned long long* counts) {
+    constexpr int NT = TileGeom<PX>::THREADS;
+    if (et) {
+        if (cnt) raster_fwd_kernel<PX, true, true><<<nt, NT, 0, s>>>(ranges, vals, xydr, conic, colors, bg, W, H, tiles_x, img, T, nc, counts);
+        else raster_fwd_kernel<PX, true, false><<<nt, NT, 0, s>>>(ranges, vals, xydr, conic, colors, bg, W, H, tiles_x, img, T, nc, counts);
+    } else {
+        if (cnt) raster_fwd_kernel<PX, false, true><<<nt, NT, 0, s>>>(ranges, vals, xydr, conic, colors, bg, W, H, tiles_x, img, T, nc, counts);
+        else raster_fwd_kernel<PX, false, false><<<nt, NT, 0, s>>>(ranges, vals, xydr, conic, colors, bg, W, H, tiles_x, img, T, nc, counts);
+    }
+}
+
+template <int PX>
+static void launch_bwd(bool cnt, unsigned nt, cudaStream_t s, const uint2* ranges, const uint32_t* vals,
+                       const float4* xydr, const float4* conic, const float* colors, float3 bg, int W, int H,
+                       int tiles_x, const float* fT, const int* nc, const float* dimg, float4* d_rgbo,
+                       float4* d_geo, float* d_c11, unsigned long long* counts) {
+    constexpr int NT = TileGeom<PX>::THREADS;
+    if (cnt)
+        raster_bwd_kernel<PX, true><<<nt, NT, 0, s>>>(ranges, vals, xydr, conic, colors, bg, W, H, tiles_x, fT, nc, dimg, d_rgbo, d_geo, d_c11, counts);
+    else
+        raster_bwd_kernel<PX, false><<<nt, NT, 0, s>>>(ranges, vals, xydr, conic, colors, bg, W, H, tiles_x, fT, nc, dimg, d_rgbo, d_geo, d_c11, counts);
 }
 
 }  // namespace gs
@@ -355,16 +416,9 @@ int gs_raster_fwd(const uint32_t* ranges2, const uint32_t* sorted_vals, const fl
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     cudaStream_t s = (cudaStream_t)stream;
-#define GS_LAUNCH_FWD(ET, CNT)                                                                                 \
-    raster_fwd_kernel<ET, CNT><<<nt, RT, 0, s>>>((const uint2*)ranges2, sorted_vals, (const float4*)xydr4,    \
-                                                 (const float4*)conic4, colors3, bg, width, height, tiles_x, \
-                                                 out_image, out_final_T, out_n_contrib, counts)
-    if (early_termination) {
-        if (counts) GS_LAUNCH_FWD(true, true); else GS_LAUNCH_FWD(true, false);
-    } else {
-        if (counts) GS_LAUNCH_FWD(false, true); else GS_LAUNCH_FWD(false, false);
-    }
-#undef GS_LAUNCH_FWD
+    auto f = raster_px("fwd") == 2 ? launch_fwd<2> : launch_fwd<4>;
+    f(early_termination != 0, counts != nullptr, nt, s, (const uint2*)ranges2, sorted_vals, (const float4*)xydr4,
+      (const float4*)conic4, colors3, bg, width, height, tiles_x, out_image, out_final_T, out_n_contrib, counts);
     return check_launch("raster_fwd_kernel");
 }
 
@@ -377,16 +431,10 @@ int gs_raster_bwd(const uint32_t* ranges2, const uint32_t* sorted_vals, const fl
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     cudaStream_t s = (cudaStream_t)stream;
-    if (counts)
-        raster_bwd_kernel<true><<<nt, RT, 0, s>>>((const uint2*)ranges2, sorted_vals, (const float4*)xydr4,
-                                                  (const float4*)conic4, colors3, bg, width, height, tiles_x,
-                                                  final_T, n_contrib, d_image, (float4*)d_rgbo4, (float4*)d_geo4,
-                                                  d_c11, counts);
-    else
-        raster_bwd_kernel<false><<<nt, RT, 0, s>>>((const uint2*)ranges2, sorted_vals, (const float4*)xydr4,
-                                                   (const float4*)conic4, colors3, bg, width, height, tiles_x,
-                                                   final_T, n_contrib, d_image, (float4*)d_rgbo4,
-                                                   (float4*)d_geo4, d_c11, counts);
+    auto f = raster_px("bwd") == 2 ? launch_bwd<2> : launch_bwd<4>;
+    f(counts != nullptr, nt, s, (const uint2*)ranges2, sorted_vals, (const float4*)xydr4, (const float4*)conic4,
+      colors3, bg, width, height, tiles_x, final_T, n_contrib, d_image, (float4*)d_rgbo4, (float4*)d_geo4, d_c11,
+      counts);
     return check_launch("raster_bwd_kernel");
 }
 
