@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", action="store_true")
     return p.parse_args()
 
 
@@ -159,8 +160,8 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2312_02121_b200 import ops
-    from paper_2312_02121_b200.scenes import make_config
+    from paper_2312_02121_b200 import _lib, ops
+    from paper_2312_02121_b200.scenes import config_sizes, make_config
 
     world, rank, local = dist_env()
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
@@ -174,68 +175,80 @@ def run_ours(args):
     n = spec.n
     t = lambda a: torch.as_tensor(a, device=dev)
     params = [t(spec.means), t(spec.scales), t(spec.quats), t(spec.opacities), t(spec.colors)]
-    cams = [ops.CameraParams.of(c) for c, _ in views]
+    m, s, q, o, c = params
+    cams = [ops.CameraParams.of(cv) for cv, _ in views]
     d_imgs = [t(d) for _, d in views]
     bg = (0.0, 0.0, 0.0)
     flush = torch.empty(L2_FLUSH_BYTES // 4, device=dev, dtype=torch.float32)
-    grad_flat = torch.empty((n, 14), device=dev, dtype=torch.float32)
-    stream = torch.cuda.current_stream()
+    grad_flat = torch.zeros((n, 14), device=dev, dtype=torch.float32)
+    L = _lib.load()
 
-    stage_names = ("project", "bin_sort", "raster_fwd", "raster_bwd", "project_bwd", "allreduce")
-
-    def frame(cam, d_img, ev=None):
-        m, s, q, o, c = params
-        rec = (lambda k: ev[k].record(stream)) if ev is not None else (lambda k: None)
-        rec(0)
-        status = torch.full((1,), -1, device=dev, dtype=torch.int64)
-        proj = ops.project(m, s, q, o, cam, status=status)
-        rec(1)
-        bins = ops.bin_sort(proj, cam, status)
-        rec(2)
-        image, final_T, nc = ops.raster_fwd(proj, bins, c, cam, bg, True)
-        rec(3)
-        st = ops.FrameState(cam, bg, True, proj, bins, final_T, nc)
-        d_rgbo, d_geo, d_c11 = ops.raster_bwd(st, c, d_img)
-        rec(4)
-        dm, ds, dq, dv = ops.project_bwd(m, s, q, cam, proj.tiles, d_geo, d_c11)
-        rec(5)
-        return bins.n_isect, (dm, ds, dq, d_rgbo)
-
-    def step(ev_list=None):
-        acc = None
-        isect = 0
-        for vi, (cam, d_img) in enumerate(zip(cams, d_imgs)):
-            ev = ev_list[vi] if ev_list is not None else None
-            ni, (dm, ds, dq, d_rgbo) = frame(cam, d_img, ev)
-            isect += ni
-            if acc is None:
-                grad_flat[:, 0:3].copy_(dm)
-                grad_flat[:, 3:6].copy_(ds)
-                grad_flat[:, 6:10].copy_(dq)
-                grad_flat[:, 10:14].copy_(d_rgbo)
-                acc = True
-            else:
-                grad_flat[:, 0:3].add_(dm)
-                grad_flat[:, 3:6].add_(ds)
-                grad_flat[:, 6:10].add_(dq)
-                grad_flat[:, 10:14].add_(d_rgbo)
-        if world > 1:
-            dist.all_reduce(grad_flat)
-        return isect
-
-    # roofline numerators: evaluation-class counts (one counted pass, untimed)
+    # per-view static capacity + workspace (one checked run each), and the
+    # roofline numerators: evaluation-class counts of a counted pass (untimed)
     counts_f = np.zeros(4, np.int64)
     counts_b = np.zeros(3, np.int64)
+    caps, wss, isect = [], [], []
     for cam, d_img in zip(cams, d_imgs):
-        m, s, q, o, c = params
-        img, st = ops.render_forward(m, s, q, o, c, cam, bg, True, counts=True)
-        g = ops.render_backward(st, m, s, q, c, d_img, counts=True)
-        counts_f += st.counts_fwd.cpu().numpy()
+        fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, counts=True)
+        g = ops.frame_backward(fr, m, s, q, c, d_img, counts=True)
+        counts_f += fr.counts_fwd.cpu().numpy()
         counts_b += g["counts"].cpu().numpy()
-    n_isect_total = 0
+        isect.append(fr.n_isect)
+        cap = int(fr.n_isect * 1.05) + 4096
+        caps.append(cap)
+        wss.append(torch.empty((L.gs_frame_workspace_bytes(n, cap, cam.width, cam.height),), device=dev,
+                               dtype=torch.uint8))
+        del fr, g
+
+    def mk_events(k):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        for e in evs:
+            e.record()  # materialise the underlying cudaEvent_t
+        return evs
+
+    ev_f = [mk_events(6) for _ in cams]
+    ev_b = [mk_events(3) for _ in cams]
+    frames_out = [None] * len(cams)
+
+    def step():
+        for vi, (cam, d_img) in enumerate(zip(cams, d_imgs)):
+            fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, capacity=caps[vi], check_meta=False, ws=wss[vi],
+                                   events=ev_f[vi])
+            g = ops.frame_backward(fr, m, s, q, c, d_img, events=ev_b[vi])
+            frames_out[vi] = fr
+            if vi == 0:
+                grad_flat[:, 0:3].copy_(g["d_mean"])
+                grad_flat[:, 3:6].copy_(g["d_scale"])
+                grad_flat[:, 6:10].copy_(g["d_quat"])
+                grad_flat[:, 10:14].copy_(g["d_rgbo"])
+            else:
+                grad_flat[:, 0:3].add_(g["d_mean"])
+                grad_flat[:, 3:6].add_(g["d_scale"])
+                grad_flat[:, 6:10].add_(g["d_quat"])
+                grad_flat[:, 10:14].add_(g["d_rgbo"])
+
+    graph = None
+    if not args.no_graph:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                step()
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+
+    def run_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+        if world > 1:
+            dist.all_reduce(grad_flat)
 
     for _ in range(max(args.warmup, 0)):
-        n_isect_total = step()
+        run_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -244,29 +257,38 @@ def run_ours(args):
     if sampler:
         sampler.start()
     step_ms = []
-    stage_ms = np.zeros(6)
+    stage_names = ("project", "depth_sort", "scan_emit", "tile_sort_ranges", "raster_fwd", "raster_bwd",
+                   "project_bwd")
+    stage_ms = np.zeros(len(stage_names))
+    stream = torch.cuda.current_stream()
     for k in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (untimed)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        ev_list = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in cams]
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        n_isect_total = step(ev_list)
-        e_ar = torch.cuda.Event(enable_timing=True)
-        e_ar.record(stream)
+        run_step()
         e1.record(stream)
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
-        for ev in ev_list:
-            for j in range(5):
-                stage_ms[j] += ev[j].elapsed_time(ev[j + 1])
-        stage_ms[5] += ev_list[-1][5].elapsed_time(e_ar)
+        for vi in range(len(cams)):
+            f, b = ev_f[vi], ev_b[vi]
+            stage_ms[0] += f[0].elapsed_time(f[1])
+            stage_ms[1] += f[1].elapsed_time(f[2])
+            stage_ms[2] += f[2].elapsed_time(f[3])
+            stage_ms[3] += f[3].elapsed_time(f[4])
+            stage_ms[4] += f[4].elapsed_time(f[5])
+            stage_ms[5] += b[0].elapsed_time(b[1])
+            stage_ms[6] += b[1].elapsed_time(b[2])
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
+    # the capacity was sized from a checked run; confirm nothing overflowed
+    for vi, fr in enumerate(frames_out):
+        meta = fr.meta().cpu()
+        assert int(meta[0]) == -1 and int(meta[1]) <= caps[vi], "capacity overflow / status error in timed run"
     total_ms = float(sum(step_ms))
     if world > 1:
         tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -284,7 +306,6 @@ def run_ours(args):
         evals_step = float(ev_t.item())
     evals_per_s = evals_step / (ms_per_step / 1e3)
 
-    # ---------------- e2e: public autograd API with pinned host buffers
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, spec, views, dev, world)
@@ -298,54 +319,54 @@ def run_ours(args):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     fp32_peak = 128.0 * sms * sm_max * 1e6  # lane-ops/s, FMA = 1 op
-    # algorithmic work per view (SURVEY.md §8d formulas)
+    hbm = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
     nv = len(cams)
+    I = float(sum(isect))
+    n_tiles = sum(cm.tiles_x * cm.tiles_y for cm in cams)
+    tp = 1 if cams[0].tiles_x * cams[0].tiles_y <= 256 else 2
+    # algorithmic work; per rank-step, all views
     F_fwd = 8 * counts_f[0] + 4 * counts_f[1] + 3 * counts_f[2] + 4 * counts_f[3]
     F_bwd = 8 * counts_b[0] + 4 * counts_b[1] + 42 * counts_b[2]
-    n_tiles = sum(c.tiles_x * c.tiles_y for c in cams)
-    I = n_isect_total
-    passes = math.ceil((32 + ops.tile_bits(cams[0].tiles_x * cams[0].tiles_y)) / 8)
-    bytes_proj = 80 * n * nv
-    bytes_sort = (8 * n + 24 * n) * nv + 12 * I + I * (8 + 24 * passes) + 8 * I + 8 * n_tiles
-    bytes_pbwd = 104 * n * nv
-    hbm = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
+    work = {
+        "project": ("hbm", 84.0 * n * nv),                   # read 44 B, write xydr 16 + conic 16 + tiles 4 + depth key 4
+        "depth_sort": ("hbm", 4 * 16.0 * n * nv),            # 4 passes x (key+value) x (read+write)
+        "scan_emit": ("hbm", 12.0 * n * nv + 8.0 * I + 16.0 * n * nv),  # gather+scan, offsets, pairs out, xydr gather
+        "tile_sort_ranges": ("hbm", tp * 16.0 * I + 4.0 * I + 8.0 * n_tiles),
+        "raster_fwd": ("fp32", float(F_fwd)),
+        "raster_bwd": ("fp32", float(F_bwd)),
+        "project_bwd": ("hbm", 104.0 * n * nv),
+    }
     st = {}
     for name, ms in zip(stage_names, stage_ms):
-        st[name] = {"ms": round(float(ms), 4)}
-    st["project"].update(bound="hbm", achieved_gbs=bytes_proj / (stage_ms[0] / 1e3) / 1e9)
-    st["bin_sort"].update(bound="hbm", achieved_gbs=bytes_sort / (stage_ms[1] / 1e3) / 1e9,
-                          note="includes the 16-byte D2H read of the intersection count")
-    st["raster_fwd"].update(bound="fp32", achieved_tops=F_fwd / (stage_ms[2] / 1e3) / 1e12)
-    st["raster_bwd"].update(bound="fp32", achieved_tops=F_bwd / (stage_ms[3] / 1e3) / 1e12)
-    st["project_bwd"].update(bound="hbm", achieved_gbs=bytes_pbwd / (stage_ms[4] / 1e3) / 1e9)
-    for k in ("project", "bin_sort", "project_bwd"):
-        st[k]["frac"] = st[k]["achieved_gbs"] * 1e9 / hbm
-    for k in ("raster_fwd", "raster_bwd"):
-        st[k]["frac"] = st[k]["achieved_tops"] * 1e12 / fp32_peak
-    dom = max(("raster_fwd", "raster_bwd", "project", "bin_sort", "project_bwd"), key=lambda k: stage_ms[
-        stage_names.index(k)])
+        bound, w = work[name]
+        d = {"ms": round(float(ms), 4), "bound": bound}
+        if bound == "hbm":
+            d["achieved_gbs"] = round(w / (ms / 1e3) / 1e9, 1) if ms > 0 else None
+            d["frac"] = round(w / (ms / 1e3) / hbm, 4) if ms > 0 else None
+        else:
+            d["achieved_tops"] = round(w / (ms / 1e3) / 1e12, 3) if ms > 0 else None
+            d["frac"] = round(w / (ms / 1e3) / fp32_peak, 4) if ms > 0 else None
+        st[name] = d
+    dom = max(stage_names, key=lambda k: stage_ms[stage_names.index(k)])
     traffic = load_traffic()
     if st[dom]["bound"] == "fp32":
-        roof = {"bound": "fp32", "kernel": dom, "achieved": round(st[dom]["achieved_tops"], 3),
-                "peak": round(fp32_peak / 1e12, 3), "unit": "Tlane-op/s (FP32, FMA=1)",
-                "frac": round(st[dom]["frac"], 4),
+        roof = {"bound": "fp32", "kernel": dom, "achieved": st[dom]["achieved_tops"],
+                "peak": round(fp32_peak / 1e12, 3), "unit": "Tlane-op/s (FP32, FMA=1)", "frac": st[dom]["frac"],
                 "peak_at_measured_clock": round(128.0 * sms * (clocks["sm_mhz"] or sm_max) * 1e6 / 1e12, 3)
-                if clocks else None,
-                "peak_source": f"128 lanes x {sms} SMs x {sm_max:.0f} MHz ({peak_src} sm_max)"}
+                if clocks and clocks.get("sm_mhz") else None,
+                "peak_source": f"128 FP32 lanes x {sms} SMs x {sm_max:.0f} MHz ({peak_src} sm_max)"}
     else:
-        roof = {"bound": "hbm", "kernel": dom, "achieved": round(st[dom]["achieved_gbs"], 1),
-                "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s", "frac": round(st[dom]["frac"], 4),
+        roof = {"bound": "hbm", "kernel": dom, "achieved": st[dom]["achieved_gbs"],
+                "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s", "frac": st[dom]["frac"],
                 "peak_source": peak_src}
     roof["traffic"] = traffic.get(dom)
-    roof["algorithmic_work_per_launch"] = {
-        "raster_fwd": int(F_fwd // nv), "raster_bwd": int(F_bwd // nv), "project": 80 * n,
-        "project_bwd": 104 * n}.get(dom)
+    roof["algorithmic_work_per_launch"] = work[dom][1] / nv
+    roof["duration_ms_per_launch"] = round(float(stage_ms[stage_names.index(dom)]) / nv, 4)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(spec, views[:1], sample_frames=1)
 
-    from paper_2312_02121_b200.scenes import config_sizes
     sz = config_sizes(cfg)
     out = {
         "metric": METRIC, "value": round(fps, 3), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -356,11 +377,12 @@ def run_ours(args):
                    "views_per_step": frames_per_step, "views_per_rank": len(cams),
                    "early_termination": True, "background": "black",
                    "parallelism": f"view-sharded x{world}" + (" + NCCL allreduce 14 fp32/Gaussian" if world > 1 else ""),
+                   "cuda_graph": graph is not None,
                    "l2": "flushed between timed steps (256 MiB write, untimed)"},
         "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
-        "intersections_per_step_rank0": int(I),
+        "intersections_per_step_rank": int(I),
         "e2e": e2e,
-        "gpu_launches": int(args.steps * len(cams) * (9 + passes)),
+        "gpu_launches": int(args.steps * len(cams) * (12 + tp)),
         "roofline": roof,
         "stages": st,
         "counts": {"E_f": int(counts_f[0]), "E_f_sigma": int(counts_f[1]), "E_f_alpha": int(counts_f[2]),

@@ -147,6 +147,51 @@ int gs_project_bwd(const float* means3, const float* scales3, const float* quats
                    const float* d_c11, float* d_means3, float* d_scales3, float* d_quats4,
                    float* d_view16, void* ws, size_t ws_bytes, gs_stream_t stream);
 
+/* ---- Whole frame (sync-free orchestration of stages 1-5) ----------------
+ * The production path.  Stage 2 is "depth-first": the Gaussians are sorted
+ * once by depth (4 onesweep passes over N 32-bit keys), their tile pairs are
+ * emitted in that order and stably sorted by tile id (1-2 passes over I
+ * 32-bit keys) -- the same per-tile (depth, source_index) order as the
+ * 64-bit keys above, with ~3-4x less sort traffic.
+ * No host synchronisation, no allocation: intersections go into a caller-
+ * chosen capacity; meta[1] (device) reports the true total, meta[0] the
+ * status word.  If meta[1] > capacity the caller re-runs with a larger
+ * workspace (results are not valid until it does).
+ * forward  replaces sg/raster_forward.py:255-271 render;
+ * backward replaces sg/proj_backward.py:178-223 scene_backward.          */
+typedef struct gs_frame_view {
+    float* xydr4;               /* (n,4) as gs_project_fwd out_xydr4 */
+    float* conic4;              /* (n,4) as gs_project_fwd out_conic4 */
+    uint32_t* tiles;            /* (n)   tiles touched, 0 = culled */
+    uint32_t* depth_order;      /* (n)   Gaussian ids by (depth, index), culled last */
+    uint32_t* sorted_tile_keys; /* (capacity) tile id of each sorted pair */
+    uint32_t* sorted_vals;      /* (capacity) Gaussian id of each sorted pair */
+    uint32_t* ranges2;          /* (tiles,2) [start, end) */
+    unsigned long long* meta;   /* [0] status word, [1] total intersections */
+    float* d_geo4;              /* (n,4) d_mean2d x,y, d_cov00, d_cov01 (after backward) */
+    float* d_c11;               /* (n)   d_cov11 (after backward) */
+} gs_frame_view;
+
+size_t gs_frame_workspace_bytes(int64_t n, int64_t isect_capacity, int32_t width, int32_t height);
+int gs_frame_view_of(int64_t n, int64_t isect_capacity, int32_t width, int32_t height, void* ws,
+                     gs_frame_view* out /*[host]*/);
+int gs_frame_forward(const float* means3, const float* scales3, const float* quats4, const float* opacities,
+                     const float* colors3, int64_t n, const gs_camera* cam /*[host]*/,
+                     const float* background3 /*[host]*/, int early_termination, int64_t isect_capacity,
+                     void* ws, size_t ws_bytes, float* out_image, float* out_final_T, int32_t* out_n_contrib,
+                     unsigned long long* counts4, void* const* stage_events, gs_stream_t stream);
+/* stage_events (nullable; entries nullable): cudaEvent_t handles recorded
+ * on `stream` at stage boundaries, for live per-stage timing.
+ *   forward : [0] start [1] projected [2] depth-sorted [3] emitted [4] tile-sorted+ranges [5] rastered
+ *   backward: [0] start [1] raster backward done [2] projection backward done
+ * d_rgbo4 (n,4) = d_color r,g,b, d_opacity (overwritten); d_view16 4x4. */
+int gs_frame_backward(const float* means3, const float* scales3, const float* quats4, const float* colors3,
+                      int64_t n, const gs_camera* cam /*[host]*/, const float* background3 /*[host]*/,
+                      int64_t isect_capacity, void* ws, size_t ws_bytes, const float* final_T,
+                      const int32_t* n_contrib, const float* d_image, float* d_means3, float* d_scales3,
+                      float* d_quats4, float* d_rgbo4, float* d_view16, unsigned long long* counts3,
+                      void* const* stage_events, gs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,7 @@ EXPORTS = (
     "gs_sort_workspace_bytes", "gs_sort_pairs", "gs_tile_ranges",
     "gs_raster_fwd", "gs_raster_bwd",
     "gs_project_bwd_workspace_bytes", "gs_project_bwd",
+    "gs_frame_workspace_bytes", "gs_frame_view_of", "gs_frame_forward", "gs_frame_backward",
 )
 
 ERR_MESSAGES = {  # include/splat_b200.h gs_error_code -> the reference's ValueError text
@@ -33,6 +34,12 @@ class GsCamera(C.Structure):
     _fields_ = [("view", C.c_float * 16), ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float),
                 ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
                 ("near_plane", C.c_float), ("far_plane", C.c_float)]
+
+
+class GsFrameView(C.Structure):
+    _fields_ = [(name, C.c_void_p) for name in (
+        "xydr4", "conic4", "tiles", "depth_order", "sorted_tile_keys", "sorted_vals", "ranges2", "meta",
+        "d_geo4", "d_c11")]
 
 
 class SplatLibError(RuntimeError):
@@ -69,6 +76,12 @@ def load():
         "gs_raster_bwd": ([P, P, P, P, P, C.POINTER(C.c_float), i32, i32, P, P, P, P, P, P, P, P], C.c_int),
         "gs_project_bwd_workspace_bytes": ([i64], sz),
         "gs_project_bwd": ([P, P, P, i64, cam, P, P, P, P, P, P, P, P, sz, P], C.c_int),
+        "gs_frame_workspace_bytes": ([i64, i64, i32, i32], sz),
+        "gs_frame_view_of": ([i64, i64, i32, i32, P, C.POINTER(GsFrameView)], C.c_int),
+        "gs_frame_forward": ([P, P, P, P, P, i64, cam, C.POINTER(C.c_float), C.c_int, i64, P, sz, P, P, P, P, P,
+                              P], C.c_int),
+        "gs_frame_backward": ([P, P, P, P, i64, cam, C.POINTER(C.c_float), i64, P, sz, P, P, P, P, P, P, P, P, P,
+                               P, P], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -3,6 +3,7 @@
 // range detection.  Together with sort.cu these replace sg/binning.py:27-65
 // (assign_tiles + sort_bins).  All HBM-bound.
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace gs {
 
@@ -21,7 +22,9 @@ __device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long
 }
 
 // ws layout: [0] tile counter (u32, padded to 16 B), then u64 status[ctas].
+// gather != nullptr: scans in[gather[p]] (counts in depth-sorted order).
 __global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(const uint32_t* __restrict__ in,
+                                                           const uint32_t* __restrict__ gather,
                                                            uint32_t* __restrict__ out, int64_t n,
                                                            unsigned int* __restrict__ tile_counter,
                                                            unsigned long long* __restrict__ status,
@@ -34,7 +37,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(const uint32_t* __re
     const unsigned int tile = s_tile;
     const int64_t base = (int64_t)tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     uint32_t v[SCAN_ITEMS];
-    if (base + SCAN_ITEMS <= n && ((reinterpret_cast<uintptr_t>(in + base) & 15) == 0)) {
+    if (gather) {
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) v[k] = (base + k < n) ? in[gather[base + k]] : 0u;
+    } else if (base + SCAN_ITEMS <= n && ((reinterpret_cast<uintptr_t>(in + base) & 15) == 0)) {
         const uint4* p = reinterpret_cast<const uint4*>(in + base);
 #pragma unroll
         for (int k = 0; k < SCAN_ITEMS / 4; ++k) {
@@ -140,6 +146,98 @@ __global__ void __launch_bounds__(256) ranges_kernel(const unsigned long long* _
     if (i == n - 1 || (uint32_t)(keys[i + 1] >> 32) != t) ranges[t].y = (uint32_t)(i + 1);
 }
 
+// Depth-first emission: thread p handles the p-th Gaussian in (depth, index)
+// order (order[] from the depth sort) and writes one (tile id, gaussian id)
+// pair per tile of its rectangle, row-major, at offsets[p] + k.  A STABLE
+// sort on the tile id then yields per-tile lists in (depth, source_index)
+// order -- sg/binning.py:50-65 -- with 32-bit keys and 1-2 passes.  The
+// digit histograms of that sort are accumulated here (warp-aggregated).
+// Pairs at or beyond `capacity` are dropped (the caller re-runs with a
+// larger buffer when the reported total exceeds it).
+__global__ void __launch_bounds__(256) emit_sorted_kernel(const uint32_t* __restrict__ order,
+                                                          const float4* __restrict__ xydr,
+                                                          const uint32_t* __restrict__ offsets, int n, int tiles_x,
+                                                          int tiles_y, int64_t capacity,
+                                                          uint32_t* __restrict__ tile_keys,
+                                                          uint32_t* __restrict__ vals,
+                                                          uint32_t* __restrict__ tile_hist, int tile_passes) {
+    __shared__ uint32_t sh[2 * 256];
+    for (int k = threadIdx.x; k < 2 * 256; k += blockDim.x) sh[k] = 0;
+    __syncthreads();
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
+    uint32_t g = 0, off = 0;
+    if (p < n) {
+        g = order[p];
+        const float4 gx = xydr[g];
+        const int r = __float_as_int(gx.w);
+        if (r > 0) {
+            tile_rect(gx.x, gx.y, r, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+            off = offsets[p];
+        }
+    }
+    // warp-cooperative histogram update per emitted row of tiles
+    for (int ty = ty0; ty <= ty1; ++ty) {
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            const uint32_t t = (uint32_t)(ty * tiles_x + tx);
+            if ((int64_t)off < capacity) {
+                tile_keys[off] = t;
+                vals[off] = g;
+                atomicAdd(&sh[t & 255u], 1u);
+                if (tile_passes > 1) atomicAdd(&sh[256 + ((t >> 8) & 255u)], 1u);
+            }
+            ++off;
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < tile_passes * 256; k += blockDim.x) {
+        const uint32_t v = sh[k];
+        if (v) atomicAdd(&tile_hist[k], v);
+    }
+}
+
+__global__ void __launch_bounds__(256) ranges_u32_kernel(const uint32_t* __restrict__ keys, int64_t n_cap,
+                                                         const unsigned long long* __restrict__ n_dev,
+                                                         uint2* __restrict__ ranges) {
+    const int64_t n = n_dev ? min((int64_t)*n_dev, n_cap) : n_cap;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = keys[i];
+    if (i == 0 || keys[i - 1] != t) ranges[t].x = (uint32_t)i;
+    if (i == n - 1 || keys[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+}
+
+size_t scan_ws_bytes(int64_t n) {
+    const int64_t ctas = (n + SCAN_TILE - 1) / SCAN_TILE;
+    return 16 + (size_t)(ctas > 0 ? ctas : 1) * sizeof(unsigned long long);
+}
+
+int launch_scan(const uint32_t* in, const uint32_t* gather, uint32_t* out, int64_t n, void* ws,
+                unsigned long long* total, cudaStream_t s) {
+    if (n == 0) return 0;
+    const int64_t ctas = (n + SCAN_TILE - 1) / SCAN_TILE;
+    scan_kernel<<<(unsigned)ctas, SCAN_THREADS, 0, s>>>(in, gather, out, n, (unsigned int*)ws,
+                                                       (unsigned long long*)((char*)ws + 16), total);
+    return check_launch("scan_kernel");
+}
+
+int launch_emit_sorted(const uint32_t* order, const float* xydr4, const uint32_t* offsets, int64_t n, int tiles_x,
+                       int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals, uint32_t* tile_hist,
+                       int tile_passes, cudaStream_t s) {
+    if (n == 0) return 0;
+    emit_sorted_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(order, (const float4*)xydr4, offsets, (int)n,
+                                                                  tiles_x, tiles_y, capacity, tile_keys, vals,
+                                                                  tile_hist, tile_passes);
+    return check_launch("emit_sorted_kernel");
+}
+
+int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const unsigned long long* n_dev,
+                      uint2* ranges, cudaStream_t s) {
+    if (n_cap == 0) return 0;
+    ranges_u32_kernel<<<(unsigned)((n_cap + 255) / 256), 256, 0, s>>>(sorted_tile_keys, n_cap, n_dev, ranges);
+    return check_launch("ranges_u32_kernel");
+}
+
 }  // namespace gs
 
 using namespace gs;
@@ -165,7 +263,7 @@ int gs_scan_tiles(const uint32_t* tiles, uint32_t* offsets, int64_t n, void* ws,
     if (cudaMemsetAsync(ws, 0, gs_scan_workspace_bytes(n), s) != cudaSuccess) return check_launch("scan memset");
     unsigned int* counter = (unsigned int*)ws;
     unsigned long long* status = (unsigned long long*)((char*)ws + 16);
-    scan_kernel<<<(unsigned)ctas, SCAN_THREADS, 0, s>>>(tiles, offsets, n, counter, status, total);
+    scan_kernel<<<(unsigned)ctas, SCAN_THREADS, 0, s>>>(tiles, nullptr, offsets, n, counter, status, total);
     return check_launch("scan_kernel");
 }
 

@@ -1,0 +1,230 @@
+// frame.cu -- one differentiable render as two sync-free entry points.
+//
+// gs_frame_forward:  project (+ depth keys and their digit histograms)
+//   -> 4-pass onesweep sort of the Gaussians by depth (stable, index order)
+//   -> scan of tile counts in depth order -> emission of (tile, gaussian)
+//   pairs in depth order (+ tile-digit histograms) -> 1-2 pass stable sort by
+//   tile id -> per-tile ranges -> raster forward.
+// gs_frame_backward: raster backward (atomic per-warp accumulation of the
+//   screen-space gradients) -> projection backward (+ fixed-order d_view).
+//
+// Nothing here synchronizes with the host or allocates: intersections are
+// written into a caller-sized capacity and the true total is reported in
+// meta[1]; a caller that sees total > capacity re-runs with a larger
+// workspace.  That makes a whole training step capturable in a CUDA graph.
+//
+// The depth-first binning is equivalent to sorting (tile << 32 | depth bits)
+// keys emitted in Gaussian order (gs_emit_keys + gs_sort_pairs): both give
+// every tile's list in (depth, source_index) order -- sg/binning.py:50-65 --
+// but the 64-bit variant sorts I pairs over 5-6 passes while this sorts N
+// 32-bit keys over 4 passes plus I 32-bit keys over 1-2 passes.
+#include <cstring>
+
+#include "common.cuh"
+#include "internal.cuh"
+
+namespace gs {
+
+namespace {
+
+constexpr size_t ALIGN = 256;
+
+inline size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
+
+int tile_passes_for(int n_tiles) { return n_tiles <= 256 ? 1 : 2; }
+
+struct Layout {
+    // persistent (written each frame)
+    size_t xydr, conic, tiles, dkeys, dkeys_alt, order, order_alt, offsets;
+    size_t tkeys, tkeys_alt, tvals, tvals_alt, ranges;
+    // zeroed region
+    size_t zero_begin, meta, dhist, thist, counters, scan_ws, dstatus, tstatus, zero_end;
+    // backward
+    size_t d_geo, d_c11, partials;
+    size_t total;
+};
+
+Layout layout(int64_t n, int64_t cap, int W, int H) {
+    const int64_t nt = (int64_t)((W + TILE - 1) / TILE) * ((H + TILE - 1) / TILE);
+    const int tp = tile_passes_for((int)nt);
+    Layout L;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = o;
+        o += up(bytes > 0 ? bytes : 1);
+        return at;
+    };
+    L.xydr = take(16 * n);
+    L.conic = take(16 * n);
+    L.tiles = take(4 * n);
+    L.dkeys = take(4 * n);
+    L.dkeys_alt = take(4 * n);
+    L.order = take(4 * n);
+    L.order_alt = take(4 * n);
+    L.offsets = take(4 * n);
+    L.tkeys = take(4 * cap);
+    L.tkeys_alt = take(4 * cap);
+    L.tvals = take(4 * cap);
+    L.tvals_alt = take(4 * cap);
+    L.ranges = take(8 * nt);
+    L.zero_begin = o;
+    L.meta = take(16);
+    L.dhist = take(4 * 256 * 4);
+    L.thist = take(4 * 256 * 2);
+    L.counters = take(64);
+    L.scan_ws = take(scan_ws_bytes(n));
+    L.dstatus = take(onesweep_status_bytes<uint32_t>(n, 4));
+    L.tstatus = take(onesweep_status_bytes<uint32_t>(cap, tp));
+    L.zero_end = o;
+    L.d_geo = take(16 * n);
+    L.d_c11 = take(4 * n);
+    L.partials = take(12 * 4 * ((n + PBWD_BLOCK - 1) / PBWD_BLOCK + 1));
+    L.total = o;
+    return L;
+}
+
+void mark(void* const* ev, int k, cudaStream_t s) {
+    if (ev && ev[k]) cudaEventRecord((cudaEvent_t)ev[k], s);
+}
+
+template <typename T>
+T* at(void* ws, size_t off) {
+    return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+}  // namespace
+
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" {
+
+size_t gs_frame_workspace_bytes(int64_t n, int64_t isect_capacity, int32_t width, int32_t height) {
+    return layout(n, isect_capacity, width, height).total;
+}
+
+int gs_frame_view_of(int64_t n, int64_t isect_capacity, int32_t width, int32_t height, void* ws,
+                     gs_frame_view* out) {
+    const Layout L = layout(n, isect_capacity, width, height);
+    const int nt = ((width + TILE - 1) / TILE) * ((height + TILE - 1) / TILE);
+    const bool odd = tile_passes_for(nt) & 1;
+    out->xydr4 = at<float>(ws, L.xydr);
+    out->conic4 = at<float>(ws, L.conic);
+    out->tiles = at<uint32_t>(ws, L.tiles);
+    out->depth_order = at<uint32_t>(ws, L.order);
+    out->sorted_tile_keys = at<uint32_t>(ws, odd ? L.tkeys_alt : L.tkeys);
+    out->sorted_vals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
+    out->ranges2 = at<uint32_t>(ws, L.ranges);
+    out->meta = at<unsigned long long>(ws, L.meta);
+    out->d_geo4 = at<float>(ws, L.d_geo);
+    out->d_c11 = at<float>(ws, L.d_c11);
+    return 0;
+}
+
+int gs_frame_forward(const float* means3, const float* scales3, const float* quats4, const float* opacities,
+                     const float* colors3, int64_t n, const gs_camera* cam, const float* background3,
+                     int early_termination, int64_t isect_capacity, void* ws, size_t ws_bytes, float* out_image,
+                     float* out_final_T, int32_t* out_n_contrib, unsigned long long* counts4, void* const* stage_events,
+                     gs_stream_t stream) {
+    if (!cam || !background3) return set_error("gs_frame_forward: null camera/background");
+    if (n < 0 || n > 0x7fffffff) return set_error("gs_frame_forward: n=%lld out of range", (long long)n);
+    if (isect_capacity < 0 || isect_capacity >= (1ll << 30))
+        return set_error("gs_frame_forward: capacity %lld out of range", (long long)isect_capacity);
+    if (cam->width < 1 || cam->height < 1) return set_error("gs_frame_forward: bad image size");
+    const int W = cam->width, H = cam->height;
+    const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
+    if ((int64_t)tiles_x * tiles_y > 65536) return set_error("gs_frame_forward: more than 65536 tiles");
+    const Layout L = layout(n, isect_capacity, W, H);
+    if (ws_bytes < L.total) return set_error("gs_frame_forward: workspace %zu < %zu", ws_bytes, L.total);
+    cudaStream_t s = (cudaStream_t)stream;
+    const CamK k = make_camk(*cam);
+    const int tp = tile_passes_for(tiles_x * tiles_y);
+    unsigned long long* meta = at<unsigned long long>(ws, L.meta);
+    uint32_t* counters = at<uint32_t>(ws, L.counters);
+
+    mark(stage_events, 0, s);
+    if (cudaMemsetAsync(at<char>(ws, L.zero_begin), 0, L.zero_end - L.zero_begin, s) != cudaSuccess)
+        return check_launch("frame memset");
+    if (cudaMemsetAsync(meta, 0xFF, 8, s) != cudaSuccess) return check_launch("frame status memset");
+    if (cudaMemsetAsync(at<char>(ws, L.ranges), 0, 8 * (size_t)tiles_x * tiles_y, s) != cudaSuccess)
+        return check_launch("ranges memset");
+    // 1. projection + depth keys
+    if (launch_project_fwd_dkey(means3, scales3, quats4, opacities, n, k, at<float>(ws, L.xydr),
+                                at<float>(ws, L.conic), at<uint32_t>(ws, L.tiles), nullptr, meta,
+                                at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.dhist), s))
+        return -1;
+    mark(stage_events, 1, s);
+    // 2. stable depth sort of all Gaussians (culled ones last)
+    if (run_onesweep<uint32_t>(at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.order), at<uint32_t>(ws, L.dkeys_alt),
+                               at<uint32_t>(ws, L.order_alt), n, nullptr, 4, at<uint32_t>(ws, L.dhist),
+                               at<uint32_t>(ws, L.dstatus), counters, s, true))
+        return -1;
+    const uint32_t* order = at<uint32_t>(ws, L.order);  // 4 passes: back in the primary buffers
+    mark(stage_events, 2, s);
+    // 3. tile counts in depth order -> offsets, total -> meta[1]
+    if (launch_scan(at<uint32_t>(ws, L.tiles), order, at<uint32_t>(ws, L.offsets), n, at<char>(ws, L.scan_ws),
+                    meta + 1, s))
+        return -1;
+    // 4. emission in depth order (+ tile digit histograms)
+    if (launch_emit_sorted(order, at<float>(ws, L.xydr), at<uint32_t>(ws, L.offsets), n, tiles_x, tiles_y,
+                           isect_capacity, at<uint32_t>(ws, L.tkeys), at<uint32_t>(ws, L.tvals),
+                           at<uint32_t>(ws, L.thist), tp, s))
+        return -1;
+    mark(stage_events, 3, s);
+    // 5. stable sort by tile id (bits [0, 8*tp))
+    if (run_onesweep<uint32_t>(at<uint32_t>(ws, L.tkeys), at<uint32_t>(ws, L.tvals), at<uint32_t>(ws, L.tkeys_alt),
+                               at<uint32_t>(ws, L.tvals_alt), isect_capacity, meta + 1, tp,
+                               at<uint32_t>(ws, L.thist), at<uint32_t>(ws, L.tstatus), counters + 4, s, false))
+        return -1;
+    const bool odd = tp & 1;
+    const uint32_t* skeys = at<uint32_t>(ws, odd ? L.tkeys_alt : L.tkeys);
+    const uint32_t* svals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
+    // 6. per-tile ranges
+    if (launch_ranges_u32(skeys, isect_capacity, meta + 1, at<uint2>(ws, L.ranges), s)) return -1;
+    mark(stage_events, 4, s);
+    // 7. raster forward
+    const float3 bg = make_float3(background3[0], background3[1], background3[2]);
+    if (launch_raster_fwd(at<uint2>(ws, L.ranges), svals, at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3,
+                          bg, W, H, early_termination != 0, out_image, out_final_T, out_n_contrib, counts4, s))
+        return -1;
+    mark(stage_events, 5, s);
+    return 0;
+}
+
+int gs_frame_backward(const float* means3, const float* scales3, const float* quats4, const float* colors3,
+                      int64_t n, const gs_camera* cam, const float* background3, int64_t isect_capacity, void* ws,
+                      size_t ws_bytes, const float* final_T, const int32_t* n_contrib, const float* d_image,
+                      float* d_means3, float* d_scales3, float* d_quats4, float* d_rgbo4, float* d_view16,
+                      unsigned long long* counts3, void* const* stage_events, gs_stream_t stream) {
+    if (!cam || !background3) return set_error("gs_frame_backward: null camera/background");
+    const int W = cam->width, H = cam->height;
+    const Layout L = layout(n, isect_capacity, W, H);
+    if (ws_bytes < L.total) return set_error("gs_frame_backward: workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    const CamK k = make_camk(*cam);
+    const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
+    const int tp = tile_passes_for(tiles_x * tiles_y);
+    const bool odd = tp & 1;
+    const uint32_t* svals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
+    mark(stage_events, 0, s);
+    if (n > 0) {
+        if (cudaMemsetAsync(d_rgbo4, 0, 16 * (size_t)n, s) != cudaSuccess ||
+            cudaMemsetAsync(at<char>(ws, L.d_geo), 0, L.partials - L.d_geo, s) != cudaSuccess)
+            return check_launch("backward memset");
+    }
+    const float3 bg = make_float3(background3[0], background3[1], background3[2]);
+    if (launch_raster_bwd(at<uint2>(ws, L.ranges), svals, at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3,
+                          bg, W, H, final_T, n_contrib, d_image, d_rgbo4, at<float>(ws, L.d_geo),
+                          at<float>(ws, L.d_c11), counts3, s))
+        return -1;
+    mark(stage_events, 1, s);
+    if (launch_project_bwd(means3, scales3, quats4, n, k, at<uint32_t>(ws, L.tiles), at<float>(ws, L.d_geo),
+                           at<float>(ws, L.d_c11), d_means3, d_scales3, d_quats4, d_view16, at<float>(ws, L.partials),
+                           s))
+        return -1;
+    mark(stage_events, 2, s);
+    return 0;
+}
+
+}  // extern "C"

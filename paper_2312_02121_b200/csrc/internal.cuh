@@ -1,0 +1,52 @@
+// internal.cuh -- host-side launchers shared between translation units
+// (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace gs {
+
+// project.cu
+int launch_project_fwd_dkey(const float* means3, const float* scales3, const float* quats4, const float* opac,
+                            int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
+                            unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s);
+int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
+                       const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
+                       float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s);
+constexpr int PBWD_BLOCK = 256;
+
+// sort.cu
+int sort_sm_count();
+template <typename K>
+size_t onesweep_status_bytes(int64_t n_cap, int passes);
+template <typename K>
+int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
+                 int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
+                 bool identity_vals);
+template <typename K>
+int launch_sort_hist(const K* keys, int64_t n_cap, const unsigned long long* n_dev, int passes, uint32_t* hist,
+                     cudaStream_t s);
+
+// binning.cu
+size_t scan_ws_bytes(int64_t n);
+int launch_scan(const uint32_t* in, const uint32_t* gather, uint32_t* out, int64_t n, void* ws,
+                unsigned long long* total, cudaStream_t s);  // ws must be zeroed
+int launch_emit_sorted(const uint32_t* order, const float* xydr4, const uint32_t* offsets, int64_t n,
+                       int tiles_x, int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals,
+                       uint32_t* tile_hist, int tile_passes, cudaStream_t s);
+int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const unsigned long long* n_dev,
+                      uint2* ranges, cudaStream_t s);  // ranges must be zeroed
+
+// raster.cu
+int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
+                      const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
+                      unsigned long long* counts, cudaStream_t s);
+int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
+                      const float* colors3, float3 bg, int W, int H, const float* fT, const int* nc,
+                      const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11, unsigned long long* counts,
+                      cudaStream_t s);
+
+}  // namespace gs

@@ -22,12 +22,25 @@ __device__ __forceinline__ void report(unsigned long long* status, int i, int co
 // through P (:45-61; equals fx*tx/tz + 0.5 + cx) -> radius (:99-112) ->
 // off-screen cull (:131-137).  Plus the conic (sg/raster_forward.py:86-92)
 // and the tile count of the bbox square (sg/binning.py:35-46).
+// DKEY: also write the depth sort key of every Gaussian (float bits of the
+// camera depth for visible ones, 0xFFFFFFFF for culled ones so they sort
+// last) and accumulate the four 8-bit digit histograms of those keys for
+// the onesweep sort that follows (sort.cu), warp-aggregated with match_any.
+template <bool DKEY>
 __global__ void __launch_bounds__(256) project_fwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
     const float* __restrict__ opac, int n, CamK cam, float4* __restrict__ xydr, float4* __restrict__ conic,
-    uint32_t* __restrict__ tiles, float* __restrict__ cov_out, unsigned long long* __restrict__ status) {
+    uint32_t* __restrict__ tiles, float* __restrict__ cov_out, unsigned long long* __restrict__ status,
+    uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dhist) {
+    __shared__ uint32_t s_hist[DKEY ? 4 * 256 : 1];
+    if (DKEY) {
+        for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) s_hist[k] = 0;
+        __syncthreads();
+    }
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (!DKEY && i >= n) return;
+    uint32_t dkey = 0xFFFFFFFFu;
+    if (i < n) {
     const float mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
     const float* Rc = cam.R;
     const float tx = Rc[0] * mx + Rc[1] * my + Rc[2] * mz + cam.t[0];
@@ -108,6 +121,26 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
         cov_out[3 * i] = ca;
         cov_out[3 * i + 1] = cb;
         cov_out[3 * i + 2] = cc;
+    }
+    if (DKEY) {
+        dkey = nt ? __float_as_uint(tz) : 0xFFFFFFFFu;
+        dkeys[i] = dkey;
+    }
+    }  // i < n
+    if (DKEY) {
+        const bool valid = i < n;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const uint32_t d = valid ? (dkey >> (8 * p)) & 255u : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            if (valid && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1))
+                atomicAdd(&s_hist[p * 256 + d], (uint32_t)__popc(peers));
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) {
+            const uint32_t v = s_hist[k];
+            if (v) atomicAdd(&dhist[k], v);
+        }
     }
 }
 
@@ -274,6 +307,31 @@ __global__ void __launch_bounds__(384) view_reduce_kernel(const float* __restric
     if (threadIdx.x < 4) d_view16[12 + threadIdx.x] = 0.f;
 }
 
+int launch_project_fwd_dkey(const float* means3, const float* scales3, const float* quats4, const float* opac,
+                            int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
+                            unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s) {
+    if (n == 0) return 0;
+    const int blocks = (int)((n + 255) / 256);
+    project_fwd_kernel<true><<<blocks, 256, 0, s>>>(means3, scales3, (const float4*)quats4, opac, (int)n, k,
+                                                    (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
+                                                    dhist);
+    return check_launch("project_fwd_kernel<dkey>");
+}
+
+int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
+                       const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
+                       float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s) {
+    const int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
+    if (blocks > 0) {
+        project_bwd_kernel<<<blocks, PBWD_THREADS, 0, s>>>(means3, scales3, (const float4*)quats4, (int)n, k, tiles,
+                                                          (const float4*)d_geo4, d_c11, d_means3, d_scales3,
+                                                          (float4*)d_quats4, partials);
+        if (check_launch("project_bwd_kernel")) return -1;
+    }
+    view_reduce_kernel<<<1, 384, 0, s>>>(partials, blocks, d_view16);
+    return check_launch("view_reduce_kernel");
+}
+
 }  // namespace gs
 
 using namespace gs;
@@ -288,9 +346,9 @@ int gs_project_fwd(const float* means3, const float* scales3, const float* quats
     if (n == 0) return 0;
     const CamK k = make_camk(*cam);
     const int blocks = (int)((n + 255) / 256);
-    project_fwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+    project_fwd_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>(
         means3, scales3, (const float4*)quats4, opacities, (int)n, k, (float4*)out_xydr4, (float4*)out_conic4,
-        out_tiles, out_cov3, status);
+        out_tiles, out_cov3, status, nullptr, nullptr);
     return check_launch("project_fwd_kernel");
 }
 

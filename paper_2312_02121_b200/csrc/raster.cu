@@ -12,6 +12,7 @@
 // py = +inf, so their sigma is inf/NaN and fails the cut: the hot loop needs
 // no per-pixel "done" test.
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace gs {
 
@@ -399,6 +400,29 @@ static void launch_bwd(bool cnt, unsigned nt, cudaStream_t s, const uint2* range
         raster_bwd_kernel<PX, true><<<nt, NT, 0, s>>>(ranges, vals, xydr, conic, colors, bg, W, H, tiles_x, fT, nc, dimg, d_rgbo, d_geo, d_c11, counts);
     else
         raster_bwd_kernel<PX, false><<<nt, NT, 0, s>>>(ranges, vals, xydr, conic, colors, bg, W, H, tiles_x, fT, nc, dimg, d_rgbo, d_geo, d_c11, counts);
+}
+
+int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
+                      const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
+                      unsigned long long* counts, cudaStream_t s) {
+    const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
+    const unsigned nt = (unsigned)(tiles_x * tiles_y);
+    auto f = raster_px("fwd") == 2 ? launch_fwd<2> : launch_fwd<4>;
+    f(et, counts != nullptr, nt, s, ranges, vals, (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H,
+      tiles_x, img, T, nc, counts);
+    return check_launch("raster_fwd_kernel");
+}
+
+int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
+                      const float* colors3, float3 bg, int W, int H, const float* fT, const int* nc,
+                      const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11, unsigned long long* counts,
+                      cudaStream_t s) {
+    const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
+    const unsigned nt = (unsigned)(tiles_x * tiles_y);
+    auto f = raster_px("bwd") == 2 ? launch_bwd<2> : launch_bwd<4>;
+    f(counts != nullptr, nt, s, ranges, vals, (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H,
+      tiles_x, fT, nc, dimg, (float4*)d_rgbo4, (float4*)d_geo4, d_c11, counts);
+    return check_launch("raster_bwd_kernel");
 }
 
 }  // namespace gs

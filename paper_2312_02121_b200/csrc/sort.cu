@@ -1,37 +1,75 @@
-// sort.cu -- hand-written stable LSD radix sort of (uint64 key, uint32 value)
-// pairs in the "onesweep" style (one upfront histogram of every digit pass,
-// then one kernel per 8-bit pass that ranks a tile of keys, obtains its
-// global digit offsets through a decoupled look-back chained scan and
-// scatters).  Stability is what makes (tile << 32 | depth bits) keys emitted
-// in Gaussian-index order reproduce sg/binning.py:50-65's
-// (depth, source_index) order.
+// sort.cu -- hand-written stable LSD radix sort of (key, uint32 value) pairs
+// in the "onesweep" style: the digit histograms of every pass are produced
+// up front (by sort_hist_kernel, or fused into the producer kernel), then
+// one kernel per 8-bit pass ranks a tile of keys with warp match_any,
+// obtains the tile's global digit offsets through a decoupled look-back
+// chained scan, and scatters through shared memory so the global writes are
+// runs of consecutive addresses.
+//
+// Stability is what reproduces sg/binning.py:50-65's (depth, source_index)
+// order: keys are emitted in Gaussian-index order, equal keys keep it.
+// Keys: uint32 (depth-first binning, frame.cu) or uint64 (the general
+// (tile << 32 | depth bits) C-ABI sort, gs_sort_pairs).
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace gs {
 
 constexpr int SORT_THREADS = 256;
 constexpr int SORT_WARPS = SORT_THREADS / 32;
-constexpr int SORT_ITEMS = 15;
-constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;  // 3840 pairs per CTA
 constexpr int RADIX = 256;
 constexpr int MAX_PASSES = 8;
 constexpr uint32_t ST_AGG = 1u << 30;
 constexpr uint32_t ST_PRE = 2u << 30;
 constexpr uint32_t ST_MASK = (1u << 30) - 1;
-constexpr size_t SORT_SMEM = (size_t)SORT_TILE * 8 + (size_t)SORT_TILE * 4 + (size_t)SORT_WARPS * RADIX * 4 +
-                             2 * RADIX * 4;
+
+template <typename K>
+struct SortCfg;
+template <>
+struct SortCfg<uint32_t> {
+    static constexpr int ITEMS = 16;
+};
+template <>
+struct SortCfg<unsigned long long> {
+    static constexpr int ITEMS = 15;
+};
+
+template <typename K>
+constexpr int sort_tile() { return SORT_THREADS * SortCfg<K>::ITEMS; }
+
+template <typename K>
+constexpr size_t sort_smem() {
+    return (size_t)sort_tile<K>() * (sizeof(K) + 4) + (size_t)SORT_WARPS * RADIX * 4 + 2 * RADIX * 4;
+}
 
 __device__ __forceinline__ uint32_t ldv(const uint32_t* p) { return *(const volatile uint32_t*)p; }
 __device__ __forceinline__ void stv(uint32_t* p, uint32_t v) { *(volatile uint32_t*)p = v; }
 
-__global__ void __launch_bounds__(256) sort_hist_kernel(const unsigned long long* __restrict__ keys, int64_t n,
-                                                        int passes, uint32_t* __restrict__ hist) {
+__device__ __forceinline__ int64_t resolve_n(const unsigned long long* n_dev, int64_t n_cap) {
+    if (!n_dev) return n_cap;
+    const int64_t v = (int64_t)*n_dev;
+    return v < n_cap ? v : n_cap;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) sort_hist_kernel(const K* __restrict__ keys, int64_t n_cap,
+                                                        const unsigned long long* __restrict__ n_dev, int passes,
+                                                        uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[MAX_PASSES * RADIX];
     for (int k = threadIdx.x; k < passes * RADIX; k += blockDim.x) sh[k] = 0;
     __syncthreads();
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long key = keys[i];
-        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * RADIX + (int)((key >> (8 * p)) & 255ull)], 1u);
+    const int64_t n = resolve_n(n_dev, n_cap);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_round = (n + 31) / 32 * 32;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+        const bool valid = i < n;
+        const K key = valid ? keys[i] : (K)0;
+        for (int p = 0; p < passes; ++p) {
+            const uint32_t d = valid ? (uint32_t)((key >> (8 * p)) & (K)255) : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            if (valid && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1))
+                atomicAdd(&sh[p * RADIX + d], (uint32_t)__popc(peers));
+        }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < passes * RADIX; k += blockDim.x) {
@@ -40,7 +78,7 @@ __global__ void __launch_bounds__(256) sort_hist_kernel(const unsigned long long
     }
 }
 
-// Inclusive block scan over 256 threads (one value per thread).
+// Inclusive scan over the 256 threads of the CTA (one value per thread).
 __device__ __forceinline__ uint32_t block_incl_scan256(uint32_t v, uint32_t* s_tmp /*8*/) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -58,53 +96,55 @@ __device__ __forceinline__ uint32_t block_incl_scan256(uint32_t v, uint32_t* s_t
     return v + off;
 }
 
+// One 8-bit pass.  vin == nullptr means value = input index (identity).
+template <typename K>
 __global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
-    const unsigned long long* __restrict__ kin, const uint32_t* __restrict__ vin,
-    unsigned long long* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift,
+    const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
+    uint32_t* __restrict__ vout, int64_t n_cap, const unsigned long long* __restrict__ n_dev, int shift,
     const uint32_t* __restrict__ hist, uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
+    constexpr int ITEMS = SortCfg<K>::ITEMS;
+    constexpr int TILE_N = sort_tile<K>();
     extern __shared__ __align__(16) unsigned char smem[];
-    unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem);
-    uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + SORT_TILE);
-    uint32_t* s_whist = s_vals + SORT_TILE;       // [warp][digit]
+    K* s_keys = reinterpret_cast<K*>(smem);
+    uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + TILE_N);
+    uint32_t* s_whist = s_vals + TILE_N;               // [warp][digit]
     uint32_t* s_gbase = s_whist + SORT_WARPS * RADIX;  // global dst of local slot 0 per digit
-    uint32_t* s_lstart = s_gbase + RADIX;         // local start of each digit in the tile
+    uint32_t* s_lstart = s_gbase + RADIX;              // local start of each digit in the tile
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_tmp[SORT_WARPS];
 
+    const int64_t n = resolve_n(n_dev, n_cap);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(counter, 1u);
 #pragma unroll
     for (int k = 0; k < SORT_WARPS; ++k) s_whist[k * RADIX + tid] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
-    const int64_t wbase = (int64_t)tile * SORT_TILE + (int64_t)warp * (SORT_ITEMS * 32);
+    if ((int64_t)tile * TILE_N >= n) return;  // capacity-sized grid, fewer items this frame
+    const int64_t wbase = (int64_t)tile * TILE_N + (int64_t)warp * (ITEMS * 32);
 
-    unsigned long long key[SORT_ITEMS];
-    uint32_t val[SORT_ITEMS];
-    uint32_t rank[SORT_ITEMS];
+    K key[ITEMS];
+    uint32_t val[ITEMS];
+    uint32_t rank[ITEMS];
 #pragma unroll
-    for (int i = 0; i < SORT_ITEMS; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
         const int64_t idx = wbase + i * 32 + lane;
-        key[i] = idx < n ? kin[idx] : ~0ull;
-        val[i] = idx < n ? vin[idx] : 0u;
+        key[i] = idx < n ? kin[idx] : (K)0;
+        val[i] = idx < n ? (vin ? vin[idx] : (uint32_t)idx) : 0u;
     }
     // warp-local stable ranking: items in (i, lane) order = input order
     const uint32_t lt = lanemask_lt();
 #pragma unroll
-    for (int i = 0; i < SORT_ITEMS; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
         const int64_t idx = wbase + i * 32 + lane;
         const bool valid = idx < n;
-        const uint32_t d = (uint32_t)(key[i] >> shift) & 255u;
-        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-        rank[i] = 0;
-        if (valid) {
-            const uint32_t peers = __match_any_sync(vmask, d);
-            const int leader = __ffs(peers) - 1;
-            uint32_t old = 0;
-            if (lane == leader) old = atomicAdd(&s_whist[warp * RADIX + d], (uint32_t)__popc(peers));
-            old = __shfl_sync(peers, old, leader);
-            rank[i] = old + (uint32_t)__popc(peers & lt);
-        }
+        const uint32_t d = valid ? (uint32_t)(key[i] >> shift) & 255u : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (valid && lane == leader) old = atomicAdd(&s_whist[warp * RADIX + d], (uint32_t)__popc(peers));
+        old = __shfl_sync(0xffffffffu, old, leader);
+        rank[i] = old + (uint32_t)__popc(peers & lt);
     }
     __syncthreads();
     // per digit: exclusive prefix over warps, tile total, chained scan
@@ -141,7 +181,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
     s_gbase[d] = (hincl - h) + excl - lstart;  // mod 2^32; dst = gbase + local slot
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < SORT_ITEMS; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
         const int64_t idx = wbase + i * 32 + lane;
         if (idx < n) {
             const uint32_t dd = (uint32_t)(key[i] >> shift) & 255u;
@@ -151,10 +191,10 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
         }
     }
     __syncthreads();
-    const int64_t rem = n - (int64_t)tile * SORT_TILE;
-    const int cnt = rem < SORT_TILE ? (int)rem : SORT_TILE;
+    const int64_t rem = n - (int64_t)tile * TILE_N;
+    const int cnt = rem < TILE_N ? (int)rem : TILE_N;
     for (int j = tid; j < cnt; j += SORT_THREADS) {
-        const unsigned long long k = s_keys[j];
+        const K k = s_keys[j];
         const uint32_t dd = (uint32_t)(k >> shift) & 255u;
         const uint32_t dst = s_gbase[dd] + (uint32_t)j;
         kout[dst] = k;
@@ -162,7 +202,83 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
     }
 }
 
-static bool g_sort_attr_set = false;
+template <typename K>
+static int set_sort_attr() {
+    static bool done = false;
+    if (!done) {
+        if (cudaFuncSetAttribute(onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sort_smem<K>()) != cudaSuccess)
+            return check_launch("onesweep smem attribute");
+        done = true;
+    }
+    return 0;
+}
+
+int sort_sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <typename K>
+size_t onesweep_status_bytes(int64_t n_cap, int passes) {
+    const int64_t tiles = (n_cap + sort_tile<K>() - 1) / sort_tile<K>();
+    return (size_t)passes * (size_t)(tiles > 0 ? tiles : 1) * RADIX * 4;
+}
+template size_t onesweep_status_bytes<uint32_t>(int64_t, int);
+template size_t onesweep_status_bytes<unsigned long long>(int64_t, int);
+
+// Runs `passes` onesweep passes from bit 0.  hist: passes x 256 digit counts
+// (already accumulated), status: zeroed onesweep_status_bytes, counters:
+// `passes` zeroed uint32.  identity_vals: the first pass ignores v0's
+// contents and uses the input index as value (v0 is still the ping-pong
+// scratch).  Result lands in (k1, v1) when passes is odd, else (k0, v0).
+template <typename K>
+int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
+                 int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
+                 bool identity_vals) {
+    if (n_cap <= 0) return 0;
+    if (set_sort_attr<K>()) return -1;
+    const int64_t tiles = (n_cap + sort_tile<K>() - 1) / sort_tile<K>();
+    K* kin = k0;
+    K* kout = k1;
+    uint32_t* vin = v0;
+    uint32_t* vout = v1;
+    for (int p = 0; p < passes; ++p) {
+        onesweep_kernel<K><<<(unsigned)tiles, SORT_THREADS, sort_smem<K>(), s>>>(
+            kin, (p == 0 && identity_vals) ? nullptr : vin, kout, vout, n_cap, n_dev, 8 * p, hist + p * RADIX,
+            status + (size_t)p * tiles * RADIX, counters + p);
+        if (check_launch("onesweep_kernel")) return -1;
+        K* tk = kin; kin = kout; kout = tk;
+        uint32_t* tv = vin; vin = vout; vout = tv;
+    }
+    return 0;
+}
+template int run_onesweep<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, int64_t,
+                                    const unsigned long long*, int, const uint32_t*, uint32_t*, uint32_t*,
+                                    cudaStream_t, bool);
+template int run_onesweep<unsigned long long>(unsigned long long*, uint32_t*, unsigned long long*, uint32_t*,
+                                              int64_t, const unsigned long long*, int, const uint32_t*,
+                                              uint32_t*, uint32_t*, cudaStream_t, bool);
+
+template <typename K>
+int launch_sort_hist(const K* keys, int64_t n_cap, const unsigned long long* n_dev, int passes, uint32_t* hist,
+                     cudaStream_t s) {
+    int64_t hb = (n_cap + 255) / 256;
+    const int64_t lim = (int64_t)sort_sm_count() * 4;
+    if (hb > lim) hb = lim;
+    if (hb < 1) hb = 1;
+    sort_hist_kernel<K><<<(unsigned)hb, 256, 0, s>>>(keys, n_cap, n_dev, passes, hist);
+    return check_launch("sort_hist_kernel");
+}
+template int launch_sort_hist<uint32_t>(const uint32_t*, int64_t, const unsigned long long*, int, uint32_t*,
+                                        cudaStream_t);
+template int launch_sort_hist<unsigned long long>(const unsigned long long*, int64_t, const unsigned long long*,
+                                                  int, uint32_t*, cudaStream_t);
 
 }  // namespace gs
 
@@ -172,8 +288,7 @@ extern "C" {
 
 size_t gs_sort_workspace_bytes(int64_t n, int end_bit) {
     const int passes = (end_bit + 7) / 8;
-    const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
-    return (size_t)MAX_PASSES * RADIX * 4 + 64 + (size_t)passes * (size_t)(tiles > 0 ? tiles : 1) * RADIX * 4;
+    return (size_t)MAX_PASSES * RADIX * 4 + 64 + onesweep_status_bytes<unsigned long long>(n, passes);
 }
 
 int gs_sort_pairs(unsigned long long* keys, unsigned long long* keys_alt, uint32_t* vals, uint32_t* vals_alt,
@@ -185,40 +300,15 @@ int gs_sort_pairs(unsigned long long* keys, unsigned long long* keys_alt, uint32
     *selector = 0;
     if (n == 0) return 0;
     cudaStream_t s = (cudaStream_t)stream;
-    if (!g_sort_attr_set) {
-        if (cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SORT_SMEM) !=
-            cudaSuccess)
-            return check_launch("onesweep smem attribute");
-        g_sort_attr_set = true;
-    }
-    const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
     uint32_t* hist = (uint32_t*)ws;
     uint32_t* counters = hist + MAX_PASSES * RADIX;
     uint32_t* status = counters + 16;
-    const size_t status_bytes = (size_t)passes * (size_t)tiles * RADIX * 4;
-    if (cudaMemsetAsync(ws, 0, (size_t)MAX_PASSES * RADIX * 4 + 64 + status_bytes, s) != cudaSuccess)
+    if (cudaMemsetAsync(ws, 0, gs_sort_workspace_bytes(n, end_bit), s) != cudaSuccess)
         return check_launch("sort memset");
-    int sms = 148;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    int64_t hb = (n + 255) / 256;
-    if (hb > (int64_t)sms * 4) hb = (int64_t)sms * 4;
-    sort_hist_kernel<<<(unsigned)hb, 256, 0, s>>>(keys, n, passes, hist);
-    if (check_launch("sort_hist_kernel")) return -1;
-    unsigned long long* kin = keys;
-    unsigned long long* kout = keys_alt;
-    uint32_t* vin = vals;
-    uint32_t* vout = vals_alt;
-    for (int p = 0; p < passes; ++p) {
-        onesweep_kernel<<<(unsigned)tiles, SORT_THREADS, SORT_SMEM, s>>>(
-            kin, vin, kout, vout, n, 8 * p, hist + p * RADIX, status + (size_t)p * tiles * RADIX, counters + p);
-        if (check_launch("onesweep_kernel")) return -1;
-        unsigned long long* tk = kin; kin = kout; kout = tk;
-        uint32_t* tv = vin; vin = vout; vout = tv;
-    }
+    if (launch_sort_hist<unsigned long long>(keys, n, nullptr, passes, hist, s)) return -1;
+    if (run_onesweep<unsigned long long>(keys, vals, keys_alt, vals_alt, n, nullptr, passes, hist, status, counters,
+                                         s, false))
+        return -1;
     *selector = passes & 1;
     return 0;
 }

@@ -277,6 +277,158 @@ def project_bwd(means, scales, quats, cam: CameraParams, tiles, d_geo, d_c11):
 
 
 # ------------------------------------------------------------- whole frame
+#
+# Production path: two C-ABI calls per view (gs_frame_forward /
+# gs_frame_backward, csrc/frame.cu), no host synchronisation inside, the
+# intersection buffers sized by a capacity.  `check=True` (default) reads
+# the 16-byte meta word after the forward to raise the reference's
+# ValueError on bad input and to re-run when the capacity was too small.
+
+_capacity_hint: dict = {}
+
+
+def _default_capacity(n: int, key) -> int:
+    hint = _capacity_hint.get(key)
+    if hint is not None:
+        return hint
+    return max(1 << 16, 8 * n)
+
+
+@dataclass
+class Frame:
+    """One rendered view kept alive for its backward (cf. RenderResult,
+    sg/raster_forward.py:62-70).  Owns its workspace."""
+
+    cam: CameraParams
+    background: tuple
+    early_termination: bool
+    n: int
+    capacity: int
+    ws: torch.Tensor
+    image: torch.Tensor
+    final_T: torch.Tensor
+    n_contrib: torch.Tensor
+    counts_fwd: torch.Tensor | None = None
+    meta_host: tuple | None = None
+
+    def view(self) -> _lib.GsFrameView:
+        v = _lib.GsFrameView()
+        check(_lib.load().gs_frame_view_of(self.n, self.capacity, self.cam.width, self.cam.height,
+                                           self.ws.data_ptr(), C.byref(v)), "gs_frame_view_of")
+        return v
+
+    def meta(self) -> torch.Tensor:
+        v = self.view()
+        off = v.meta - self.ws.data_ptr()
+        return self.ws[off:off + 16].view(torch.int64)
+
+    @property
+    def n_isect(self) -> int:
+        if self.meta_host is None:
+            m = self.meta().cpu()
+            self.meta_host = (int(m[0]), int(m[1]))
+        return self.meta_host[1]
+
+    def tensors(self) -> dict:
+        """Device views of the frame's intermediates (for tests/adapters)."""
+        v = self.view()
+        base = self.ws.data_ptr()
+        n, W, H = self.n, self.cam.width, self.cam.height
+        nt = self.cam.tiles_x * self.cam.tiles_y
+
+        def sl(ptr, count, dtype, shape):
+            off = ptr - base
+            esz = torch.tensor([], dtype=dtype).element_size()
+            return self.ws[off:off + count * esz].view(dtype).view(shape)
+
+        m = min(self.n_isect, self.capacity)
+        return dict(xydr=sl(v.xydr4, 4 * n, torch.float32, (n, 4)), conic=sl(v.conic4, 4 * n, torch.float32, (n, 4)),
+                    tiles=sl(v.tiles, n, torch.int32, (n,)), depth_order=sl(v.depth_order, n, torch.int32, (n,)),
+                    sorted_tile_keys=sl(v.sorted_tile_keys, m, torch.int32, (m,)),
+                    sorted_vals=sl(v.sorted_vals, m, torch.int32, (m,)),
+                    ranges=sl(v.ranges2, 2 * nt, torch.int32, (nt, 2)),
+                    d_geo=sl(v.d_geo4, 4 * n, torch.float32, (n, 4)), d_c11=sl(v.d_c11, n, torch.float32, (n,)))
+
+
+def frame_forward(means, scales, quats, opacities, colors, cam: CameraParams, background=(0.0, 0.0, 0.0),
+                  early_termination=True, *, capacity: int | None = None, counts=False, check_meta=True,
+                  ws: torch.Tensor | None = None, events=None) -> Frame:
+    """gs_frame_forward: image, final_T, n_contrib of one view."""
+    L = _lib.load()
+    means, scales, quats, opacities, colors = check_params(means, scales, quats, opacities, colors)
+    n = means.shape[0]
+    dev = means.device
+    key = (n, cam.width, cam.height)
+    cap = int(capacity) if capacity is not None else _default_capacity(n, key)
+    H, W = cam.height, cam.width
+    camc = cam.c()
+    bg = (C.c_float * 3)(*[float(b) for b in background])
+    while True:
+        wsb = L.gs_frame_workspace_bytes(n, cap, W, H)
+        if ws is None or ws.numel() < wsb:
+            ws = torch.empty((wsb,), device=dev, dtype=torch.uint8)
+        image = torch.empty((H, W, 3), device=dev, dtype=torch.float32)
+        final_T = torch.empty((H, W), device=dev, dtype=torch.float32)
+        n_contrib = torch.empty((H, W), device=dev, dtype=torch.int32)
+        cnt = torch.zeros((4,), device=dev, dtype=torch.int64) if counts else None
+        check(L.gs_frame_forward(_ptr(means), _ptr(scales), _ptr(quats), _ptr(opacities), _ptr(colors), n,
+                                 C.byref(camc), bg, 1 if early_termination else 0, cap, _ptr(ws), ws.numel(),
+                                 _ptr(image), _ptr(final_T), _ptr(n_contrib), _ptr(cnt), _event_array(events),
+                                 _stream()), "gs_frame_forward")
+        fr = Frame(cam, tuple(float(b) for b in background), bool(early_termination), n, cap, ws, image, final_T,
+                   n_contrib, cnt)
+        if not check_meta:
+            return fr
+        m = fr.meta().cpu()
+        fr.meta_host = (int(m[0]), int(m[1]))
+        raise_status(fr.meta_host[0])
+        total = fr.meta_host[1]
+        _capacity_hint[key] = max(1 << 16, int(total * 1.25) + 1024)
+        if total <= cap:
+            return fr
+        cap = _capacity_hint[key]
+        ws = None
+
+
+def _event_array(events):
+    """torch.cuda.Event list -> void*[] of raw cudaEvent_t handles (None -> NULL)."""
+    if not events:
+        return None
+    arr = (C.c_void_p * len(events))()
+    for i, e in enumerate(events):
+        arr[i] = None if e is None else int(e.cuda_event)
+    return arr
+
+
+def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=False, events=None):
+    """gs_frame_backward: the SceneGradients fields (sg/proj_backward.py:25-50)."""
+    L = _lib.load()
+    H, W = fr.cam.height, fr.cam.width
+    if tuple(d_image.shape) != (H, W, 3):
+        raise ValueError(f"d_image must have shape {(H, W, 3)}, got {tuple(d_image.shape)}")  # sg/raster_backward.py:180-183
+    d_image = d_image.contiguous().to(torch.float32)
+    n = fr.n
+    dev = means.device
+    d_means = torch.empty((n, 3), device=dev, dtype=torch.float32)
+    d_scales = torch.empty((n, 3), device=dev, dtype=torch.float32)
+    d_quats = torch.empty((n, 4), device=dev, dtype=torch.float32)
+    d_rgbo = torch.empty((n, 4), device=dev, dtype=torch.float32)
+    d_view = torch.empty((4, 4), device=dev, dtype=torch.float32)
+    cnt = torch.zeros((3,), device=dev, dtype=torch.int64) if counts else None
+    camc = fr.cam.c()
+    bg = (C.c_float * 3)(*fr.background)
+    check(L.gs_frame_backward(_ptr(means), _ptr(scales), _ptr(quats), _ptr(colors), n, C.byref(camc), bg,
+                              fr.capacity, _ptr(fr.ws), fr.ws.numel(), _ptr(fr.final_T), _ptr(fr.n_contrib),
+                              _ptr(d_image), _ptr(d_means), _ptr(d_scales), _ptr(d_quats), _ptr(d_rgbo),
+                              _ptr(d_view), _ptr(cnt), _event_array(events), _stream()), "gs_frame_backward")
+    return dict(d_mean=d_means, d_scale=d_scales, d_quat=d_quats, d_opacity=d_rgbo[:, 3], d_color=d_rgbo[:, :3],
+                d_view=d_view, d_rgbo=d_rgbo, counts=cnt)
+
+
+# ------------------------------------------------------ staged (per-stage) path
+# The same frame through the individual stage entry points and the 64-bit
+# (tile << 32 | depth) key sort; used by the parity harness (it exposes every
+# intermediate, including cov2d) and checked equal to the frame path.
 
 def render_forward(means, scales, quats, opacities, colors, cam: CameraParams, background=(0.0, 0.0, 0.0),
                    early_termination=True, *, want_cov=False, counts=False):
@@ -307,11 +459,11 @@ def render_backward(state: FrameState, means, scales, quats, colors, d_image, *,
 
 
 class RasterizeGaussians(torch.autograd.Function):
-    """Differentiable render of one view.
+    """Differentiable render of one view (production frame path).
 
     forward(means (N,3), scales (N,3), quats (N,4) (w,x,y,z), opacities (N,),
             colors (N,3), viewmat (4,4), camera (fx, fy, cx, cy, W, H, near, far),
-            background (3,), early_termination) -> image (H, W, 3)
+            background (3,), early_termination) -> image (H, W, 3), final_T, n_contrib
     backward returns d_means, d_scales, d_quats, d_opacities, d_colors,
     d_viewmat -- field by field the reference's SceneGradients
     (sg/proj_backward.py:34-39).
@@ -321,18 +473,19 @@ class RasterizeGaussians(torch.autograd.Function):
     def forward(ctx, means, scales, quats, opacities, colors, viewmat, intrinsics, background, early_termination):
         fx, fy, cx, cy, W, H, near, far = intrinsics
         cam = CameraParams(viewmat.detach().to("cpu", torch.float64).tolist(), fx, fy, cx, cy, W, H, near, far)
-        image, state = render_forward(means, scales, quats, opacities, colors, cam, background, early_termination)
-        ctx.state = state
+        fr = frame_forward(means, scales, quats, opacities, colors, cam, background, early_termination)
+        ctx.frame = fr
         ctx.view_device = viewmat.device
         ctx.save_for_backward(means, scales, quats, colors)
-        ctx.mark_non_differentiable(state.final_T, state.n_contrib)
-        return image, state.final_T, state.n_contrib
+        ctx.mark_non_differentiable(fr.final_T, fr.n_contrib)
+        return fr.image, fr.final_T, fr.n_contrib
 
     @staticmethod
     def backward(ctx, d_image, _d_T, _d_nc):
         means, scales, quats, colors = ctx.saved_tensors
-        g = render_backward(ctx.state, means.contiguous(), scales.contiguous(), quats.contiguous(),
-                            colors.contiguous(), d_image)
+        g = frame_backward(ctx.frame, means.contiguous(), scales.contiguous(), quats.contiguous(),
+                           colors.contiguous(), d_image)
+        ctx.frame = None  # release the workspace
         return (g["d_mean"], g["d_scale"], g["d_quat"], g["d_opacity"], g["d_color"],
                 g["d_view"].to(ctx.view_device), None, None, None)
 
