@@ -84,7 +84,14 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
 }
 
 void mark(void* const* ev, int k, cudaStream_t s) {
-    if (ev && ev[k]) cudaEventRecord((cudaEvent_t)ev[k], s);
+    if (!ev || !ev[k]) return;
+    // inside stream capture an External record becomes a real event-record node
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags((cudaEvent_t)ev[k], s, cudaEventRecordExternal);
+    else
+        cudaEventRecord((cudaEvent_t)ev[k], s);
 }
 
 template <typename T>
