@@ -49,17 +49,24 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+// PX = 2: 4 warps, each an 8x8 quadrant; PX = 4: 2 warps, each 8 columns x
+// 16 rows; PX = 8: 1 warp for the whole 16x16 tile (lane = column, two row
+// groups).  A thread's PX pixels always share one column.
 template <int PX>
 struct TileGeom {
     static constexpr int THREADS = TILE_PIX / PX;
+    static constexpr int NW = THREADS / 32;
+    static constexpr int LC = NW >= 2 ? 8 : 16;  // columns covered by one warp
+    static constexpr int RS = 32 / LC;           // row stride between a thread's pixels
     int col;
     int row[PX];
     __device__ __forceinline__ TileGeom(int tile, int tiles_x) {
         const int tx = tile % tiles_x, ty = tile / tiles_x;
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        col = tx * TILE + (warp & 1) * 8 + (lane & 7);
+        col = tx * TILE + (NW >= 2 ? (warp & 1) * 8 : 0) + (lane % LC);
+        const int base = NW == 4 ? (warp >> 1) * 8 : 0;
 #pragma unroll
-        for (int k = 0; k < PX; ++k) row[k] = ty * TILE + (warp >> 1) * 4 * PX + (lane >> 3) + 4 * k;
+        for (int k = 0; k < PX; ++k) row[k] = ty * TILE + base + (lane / LC) + RS * k;
     }
 };
 
@@ -371,7 +378,7 @@ static int raster_px(const char* which) {
     if (v < 0) {
         v = 4;
         const char* e = getenv(which[0] == 'f' ? "GS_RASTER_PX_FWD" : "GS_RASTER_PX_BWD");
-        if (e && (atoi(e) == 2 || atoi(e) == 4)) v = atoi(e);
+        if (e && (atoi(e) == 2 || atoi(e) == 4 || atoi(e) == 8)) v = atoi(e);
     }
     return v;
 }
@@ -407,7 +414,8 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
                       unsigned long long* counts, cudaStream_t s) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
-    auto f = raster_px("fwd") == 2 ? launch_fwd<2> : launch_fwd<4>;
+    const int pxf = raster_px("fwd");
+    auto f = pxf == 2 ? launch_fwd<2> : pxf == 8 ? launch_fwd<8> : launch_fwd<4>;
     f(et, counts != nullptr, nt, s, ranges, vals, (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H,
       tiles_x, img, T, nc, counts);
     return check_launch("raster_fwd_kernel");
@@ -419,7 +427,8 @@ int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xy
                       cudaStream_t s) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
-    auto f = raster_px("bwd") == 2 ? launch_bwd<2> : launch_bwd<4>;
+    const int pxb = raster_px("bwd");
+    auto f = pxb == 2 ? launch_bwd<2> : pxb == 8 ? launch_bwd<8> : launch_bwd<4>;
     f(counts != nullptr, nt, s, ranges, vals, (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H,
       tiles_x, fT, nc, dimg, (float4*)d_rgbo4, (float4*)d_geo4, d_c11, counts);
     return check_launch("raster_bwd_kernel");
@@ -440,7 +449,8 @@ int gs_raster_fwd(const uint32_t* ranges2, const uint32_t* sorted_vals, const fl
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     cudaStream_t s = (cudaStream_t)stream;
-    auto f = raster_px("fwd") == 2 ? launch_fwd<2> : launch_fwd<4>;
+    const int pxf = raster_px("fwd");
+    auto f = pxf == 2 ? launch_fwd<2> : pxf == 8 ? launch_fwd<8> : launch_fwd<4>;
     f(early_termination != 0, counts != nullptr, nt, s, (const uint2*)ranges2, sorted_vals, (const float4*)xydr4,
       (const float4*)conic4, colors3, bg, width, height, tiles_x, out_image, out_final_T, out_n_contrib, counts);
     return check_launch("raster_fwd_kernel");
@@ -455,7 +465,8 @@ int gs_raster_bwd(const uint32_t* ranges2, const uint32_t* sorted_vals, const fl
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     cudaStream_t s = (cudaStream_t)stream;
-    auto f = raster_px("bwd") == 2 ? launch_bwd<2> : launch_bwd<4>;
+    const int pxb = raster_px("bwd");
+    auto f = pxb == 2 ? launch_bwd<2> : pxb == 8 ? launch_bwd<8> : launch_bwd<4>;
     f(counts != nullptr, nt, s, (const uint2*)ranges2, sorted_vals, (const float4*)xydr4, (const float4*)conic4,
       colors3, bg, width, height, tiles_x, final_T, n_contrib, d_image, (float4*)d_rgbo4, (float4*)d_geo4, d_c11,
       counts);
