@@ -2,21 +2,33 @@
 // (back-to-front replay backward).
 //
 // Layout: one CTA per 16x16 tile, 256/PX threads, PX pixels per thread.
-// Lane l of warp w owns column (w&1)*8 + (l&7) and the PX rows
-// (w>>1)*4*PX + (l>>3) + 4k, k < PX, so a thread's pixels share a column
-// (hence dx and hA*dx of every splat) and a warp covers a compact 8 x 4*PX
-// block.  The tile's sorted splat records are staged in shared memory
-// RB = 128 at a time.  Bound: FP32 issue (DESIGN.md roofline).
+//   PX = 2: 4 warps, each an 8x8 quadrant of the tile;
+//   PX = 4: 2 warps, each 8 columns x 16 rows;
+//   PX = 8: 1 warp for the whole tile.
+// A thread's PX pixels share one column (hence dx and hA*dx of every splat).
+// The tile's sorted splat records are staged in shared memory RB = 128 at a
+// time.  Bound: FP32 issue (DESIGN.md roofline).
+//
+// Region masks: while staging, every splat's bounding square (radius r, the
+// square sg/binning.py:35-46 bins by), grown by one pixel, is tested against
+// each warp's pixel region; a warp then walks only the set bits of its own
+// mask.  A skipped (pixel, splat) pair lies more than one pixel outside the
+// 3-sigma square, so sigma > 4.5 there with a wide margin: the skip never
+// changes a decision, and forward and backward (same PX, same test) replay
+// identical evaluation sequences.
 //
 // Retired pixels (forward: out of the image or early-terminated) get
 // py = +inf, so their sigma is inf/NaN and fails the cut: the hot loop needs
 // no per-pixel "done" test.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.cuh"
 
 namespace gs {
 
-constexpr int RB = 128;  // splats per staged batch
+constexpr int RB = 128;       // splats per staged batch
+constexpr int MW = RB / 32;   // mask words per warp region
 
 struct SplatSmem {
     float4 a[RB];  // x, y, hA = A/2, B
@@ -24,17 +36,6 @@ struct SplatSmem {
     float c[RB];   // blue
     uint32_t id[RB];
 };
-
-__device__ __forceinline__ void stage_splat(SplatSmem& s, int k, uint32_t id, const float4* __restrict__ xydr,
-                                            const float4* __restrict__ conic, const float* __restrict__ colors) {
-    const float4 g = xydr[id];
-    const float4 q = conic[id];
-    const float r = colors[3 * id], gg = colors[3 * id + 1], bb = colors[3 * id + 2];
-    s.a[k] = make_float4(g.x, g.y, 0.5f * q.x, q.y);
-    s.b[k] = make_float4(0.5f * q.z, q.w, r, gg);
-    s.c[k] = bb;
-    s.id[k] = id;
-}
 
 // Keep a loop-invariant value in a register (stops ptxas from
 // rematerialising it inside the hot loop).
@@ -49,15 +50,13 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
-// PX = 2: 4 warps, each an 8x8 quadrant; PX = 4: 2 warps, each 8 columns x
-// 16 rows; PX = 8: 1 warp for the whole 16x16 tile (lane = column, two row
-// groups).  A thread's PX pixels always share one column.
 template <int PX>
 struct TileGeom {
     static constexpr int THREADS = TILE_PIX / PX;
     static constexpr int NW = THREADS / 32;
-    static constexpr int LC = NW >= 2 ? 8 : 16;  // columns covered by one warp
-    static constexpr int RS = 32 / LC;           // row stride between a thread's pixels
+    static constexpr int LC = NW >= 2 ? 8 : 16;    // columns covered by one warp
+    static constexpr int RS = 32 / LC;             // row stride between a thread's pixels
+    static constexpr int WROWS = NW == 4 ? 8 : 16;  // rows covered by one warp
     int col;
     int row[PX];
     __device__ __forceinline__ TileGeom(int tile, int tiles_x) {
@@ -68,7 +67,56 @@ struct TileGeom {
 #pragma unroll
         for (int k = 0; k < PX; ++k) row[k] = ty * TILE + base + (lane / LC) + RS * k;
     }
+    // pixel-centre bounds of warp w's region
+    __device__ __forceinline__ static void region(int tile, int tiles_x, int w, float& x0, float& x1, float& y0,
+                                                  float& y1) {
+        const int tx = tile % tiles_x, ty = tile / tiles_x;
+        const int c0 = tx * TILE + (NW >= 2 ? (w & 1) * 8 : 0);
+        const int r0 = ty * TILE + (NW == 4 ? (w >> 1) * 8 : 0);
+        x0 = (float)c0 + 0.5f;
+        x1 = (float)(c0 + LC - 1) + 0.5f;
+        y0 = (float)r0 + 0.5f;
+        y1 = (float)(r0 + WROWS - 1) + 0.5f;
+    }
 };
+
+// Stage splat k of the batch and publish, per warp region, whether its
+// (grown) bounding square reaches that region.
+template <int PX>
+__device__ __forceinline__ void stage_batch(SplatSmem& s, uint32_t (*s_mask)[MW], int tile, int tiles_x,
+                                            const uint32_t* __restrict__ ids, int first, int count,
+                                            const float4* __restrict__ xydr, const float4* __restrict__ conic,
+                                            const float* __restrict__ colors) {
+    using G = TileGeom<PX>;
+    constexpr int NT = G::THREADS, PER = RB / NT;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int k = u * NT + (int)threadIdx.x;
+        const bool valid = k < count;
+        float x = 0.f, y = 0.f, r = -1e30f;
+        if (valid) {
+            const uint32_t id = ids[first + k];
+            const float4 g = xydr[id];
+            const float4 q = conic[id];
+            s.a[k] = make_float4(g.x, g.y, 0.5f * q.x, q.y);
+            s.b[k] = make_float4(0.5f * q.z, q.w, colors[3 * id], colors[3 * id + 1]);
+            s.c[k] = colors[3 * id + 2];
+            s.id[k] = id;
+            x = g.x;
+            y = g.y;
+            r = (float)__float_as_int(g.w) + 1.f;
+        }
+#pragma unroll
+        for (int w = 0; w < G::NW; ++w) {
+            float x0, x1, y0, y1;
+            G::region(tile, tiles_x, w, x0, x1, y0, y1);
+            const bool ov = valid && x + r >= x0 && x - r <= x1 && y + r >= y0 && y - r <= y1;
+            const uint32_t m = __ballot_sync(0xffffffffu, ov);
+            if (lane == 0) s_mask[w][u * G::NW + warp] = m;
+        }
+    }
+}
 
 // ============================================================ forward
 // sg/raster_forward.py:116-154 _composite_tile for one tile.
@@ -78,84 +126,89 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_fwd_kernel(
     const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg, int W, int H, int tiles_x,
     float* __restrict__ out_img, float* __restrict__ out_T, int* __restrict__ out_nc,
     unsigned long long* __restrict__ counts) {
-    constexpr int NT = TileGeom<PX>::THREADS;
-    constexpr int PER = RB / NT;  // splats staged per thread per batch
+    using G = TileGeom<PX>;
     __shared__ SplatSmem s;
+    __shared__ uint32_t s_mask[G::NW][MW];
     const int tile = blockIdx.x;
-    const TileGeom<PX> geo(tile, tiles_x);
+    const int warp = threadIdx.x >> 5;
+    const G geo(tile, tiles_x);
     const float INF = __int_as_float(0x7f800000);
     const float px = pin((float)geo.col + 0.5f);
     float py[PX], T[PX], cr[PX], cg[PX], cb[PX];
-    int nc[PX];
+    int nc[PX], stop[PX];
     unsigned done = 0;
 #pragma unroll
     for (int q = 0; q < PX; ++q) {
         const bool in = geo.col < W && geo.row[q] < H;
         py[q] = pin(in ? (float)geo.row[q] + 0.5f : INF);
         done |= in ? 0u : (1u << q);
-        T[q] = 1.f; cr[q] = 0.f; cg[q] = 0.f; cb[q] = 0.f; nc[q] = 0;
+        T[q] = 1.f; cr[q] = 0.f; cg[q] = 0.f; cb[q] = 0.f; nc[q] = 0; stop[q] = -1;
     }
     constexpr unsigned ALL = (1u << PX) - 1u;
     const uint2 rg = ranges[tile];
     const int start = (int)rg.x, end = (int)rg.y;
-    unsigned long long e_f = 0, e_s = 0, e_a = 0, e_c = 0;
+    unsigned long long e_s = 0, e_a = 0, e_c = 0;
 
     for (int b0 = start; b0 < end; b0 += RB) {
         if (__syncthreads_count(done != ALL) == 0) break;
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const int k = u * NT + (int)threadIdx.x;
-            if (b0 + k < end) stage_splat(s, k, sorted_vals[b0 + k], xydr, conic, colors);
-        }
+        stage_batch<PX>(s, s_mask, tile, tiles_x, sorted_vals, b0, min(RB, end - b0), xydr, conic, colors);
         __syncthreads();
         if (__all_sync(0xffffffffu, done == ALL)) continue;  // whole warp finished: only help staging
-        const int cnt = min(RB, end - b0);
         const int pos_base = b0 - start + 1;
-#pragma unroll 2
-        for (int k = 0; k < cnt; ++k) {
-            const float4 a = s.a[k];
-            const float hC = s.b[k].x;
-            const float dx = __fsub_rn(px, a.x);
-            const float hAdx = __fmul_rn(a.z, dx);
-            float sg[PX];
-            bool vis[PX];
-            bool any = false;
+        bool warp_done = false;
+#pragma unroll 1
+        for (int j = 0; j < MW && !warp_done; ++j) {
+            uint32_t m = s_mask[warp][j];
+            while (m) {
+                const int k = j * 32 + (__ffs(m) - 1);
+                m &= m - 1;
+                const float4 a = s.a[k];
+                const float hC = s.b[k].x;
+                const float dx = __fsub_rn(px, a.x);
+                const float hAdx = __fmul_rn(a.z, dx);
+                float sg[PX];
+                bool vis[PX];
+                bool any = false;
 #pragma unroll
-            for (int q = 0; q < PX; ++q) {
-                sg[q] = splat_sigma_h(dx, hAdx, __fsub_rn(py[q], a.y), a.w, hC);
-                vis[q] = sg[q] <= SIGMA_CUT;  // false for retired pixels (py = inf)
-                any |= vis[q];
-            }
-            if (COUNT) {
-                e_f += PX - __popc(done);
-#pragma unroll
-                for (int q = 0; q < PX; ++q) e_s += vis[q];
-            }
-            if (!__any_sync(0xffffffffu, any)) continue;
-            const float4 bq = s.b[k];
-            const float blue = s.c[k];
-#pragma unroll
-            for (int q = 0; q < PX; ++q) {
-                if (!vis[q]) continue;
-                const float e = splat_exp_neg(sg[q]);
-                const float alpha = fminf(__fmul_rn(bq.y, e), ALPHA_MAX);
-                if (!(alpha >= ALPHA_MIN)) continue;
-                if (COUNT) ++e_a;
-                const float nT = __fmul_rn(T[q], __fsub_rn(1.f, alpha));
-                if (ET && nT < T_MIN) {  // stop WITHOUT compositing (:141-144)
-                    py[q] = INF;
-                    done |= 1u << q;
-                    continue;
+                for (int q = 0; q < PX; ++q) {
+                    sg[q] = splat_sigma_h(dx, hAdx, __fsub_rn(py[q], a.y), a.w, hC);
+                    vis[q] = sg[q] <= SIGMA_CUT;  // false for retired pixels (py = inf)
+                    any |= vis[q];
                 }
-                if (COUNT) ++e_c;
-                const float w = __fmul_rn(alpha, T[q]);
-                cr[q] = __fmaf_rn(w, bq.z, cr[q]);
-                cg[q] = __fmaf_rn(w, bq.w, cg[q]);
-                cb[q] = __fmaf_rn(w, blue, cb[q]);
-                T[q] = nT;
-                nc[q] = pos_base + k;
+                if (COUNT) {
+#pragma unroll
+                    for (int q = 0; q < PX; ++q) e_s += vis[q];
+                }
+                if (!__any_sync(0xffffffffu, any)) continue;
+                const float4 bq = s.b[k];
+                const float blue = s.c[k];
+#pragma unroll
+                for (int q = 0; q < PX; ++q) {
+                    if (!vis[q]) continue;
+                    const float e = splat_exp_neg(sg[q]);
+                    const float alpha = fminf(__fmul_rn(bq.y, e), ALPHA_MAX);
+                    if (!(alpha >= ALPHA_MIN)) continue;
+                    if (COUNT) ++e_a;
+                    const float nT = __fmul_rn(T[q], __fsub_rn(1.f, alpha));
+                    if (ET && nT < T_MIN) {  // stop WITHOUT compositing (:141-144)
+                        py[q] = INF;
+                        done |= 1u << q;
+                        stop[q] = pos_base + k;
+                        continue;
+                    }
+                    if (COUNT) ++e_c;
+                    const float w = __fmul_rn(alpha, T[q]);
+                    cr[q] = __fmaf_rn(w, bq.z, cr[q]);
+                    cg[q] = __fmaf_rn(w, bq.w, cg[q]);
+                    cb[q] = __fmaf_rn(w, blue, cb[q]);
+                    T[q] = nT;
+                    nc[q] = pos_base + k;
+                }
+                if (ET && __all_sync(0xffffffffu, done == ALL)) {
+                    warp_done = true;
+                    break;
+                }
             }
-            if (ET && __all_sync(0xffffffffu, done == ALL)) break;
         }
     }
 #pragma unroll
@@ -170,6 +223,12 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_fwd_kernel(
         }
     }
     if (COUNT) {
+        // E_f: (pixel, entry) pairs the reference visits while not done =
+        // entries up to and including the stopping one, else the whole list
+        unsigned long long e_f = 0;
+#pragma unroll
+        for (int q = 0; q < PX; ++q)
+            if (geo.col < W && geo.row[q] < H) e_f += (unsigned long long)(stop[q] >= 0 ? stop[q] : end - start);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             e_f += __shfl_xor_sync(0xffffffffu, e_f, o);
@@ -215,13 +274,14 @@ __device__ __forceinline__ float warp_reduce8(const float* v, int lane) {
 
 // sg/raster_backward.py:47-108 _backward_tile for one tile: seed T = final_T,
 // S = bg * final_T; walk pos = max(n_contrib)-1 .. 0 replaying the forward's
-// decisions (same sigma/exp code); contrib -> T_here = T/(1-alpha),
-// w = alpha T_here, dc += w g, d_alpha = T_here c.g - S.g/(1-alpha);
-// live (alpha_raw < 0.999) -> d_opacity += d_alpha e^-sigma, d_sigma =
-// -alpha_raw d_alpha, d_mean2d += -d_sigma y, d_cov2d += -d_sigma/2 y y^T with
-// y = conic * delta (full-matrix convention, :99-105); S += w c; T = T_here.
-// Per splat the warp's 9 sums are transposed-reduced and 8 (+1) lanes issue
-// one global reduction each: one atomic per warp per Gaussian value.
+// decisions (same sigma/exp code, same region masks); contrib ->
+// T_here = T/(1-alpha), w = alpha T_here, dc += w g,
+// d_alpha = T_here c.g - S.g/(1-alpha); live (alpha_raw < 0.999) ->
+// d_opacity += d_alpha e^-sigma, d_sigma = -alpha_raw d_alpha,
+// d_mean2d += -d_sigma y, d_cov2d += -d_sigma/2 y y^T with y = conic * delta
+// (full-matrix convention, :99-105); S += w c; T = T_here.  Per splat the
+// warp's 9 sums are transposed-reduced and 8 (+1) lanes issue one global
+// reduction each: one atomic per warp per Gaussian value.
 template <int PX, bool COUNT>
 __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ sorted_vals, const float4* __restrict__ xydr,
@@ -229,13 +289,13 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_bwd_kernel(
     const float* __restrict__ final_T, const int* __restrict__ n_contrib, const float* __restrict__ d_img,
     float4* __restrict__ d_rgbo, float4* __restrict__ d_geo, float* __restrict__ d_c11,
     unsigned long long* __restrict__ counts) {
-    constexpr int NT = TileGeom<PX>::THREADS;
-    constexpr int PER = RB / NT;
-    constexpr int NW = NT / 32;
+    using G = TileGeom<PX>;
+    constexpr int NW = G::NW;
     __shared__ SplatSmem s;
+    __shared__ uint32_t s_mask[NW][MW];
     __shared__ int s_max[NW];
     const int tile = blockIdx.x;
-    const TileGeom<PX> geo(tile, tiles_x);
+    const G geo(tile, tiles_x);
     const float px = pin((float)geo.col + 0.5f);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float py[PX], T[PX], S0[PX], S1[PX], S2[PX], g0[PX], g1[PX], g2[PX];
@@ -268,89 +328,94 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_bwd_kernel(
     for (int bend = max_nc; bend > 0; bend -= RB) {
         const int bstart = max(0, bend - RB);
         __syncthreads();
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const int k = u * NT + (int)threadIdx.x;
-            if (bstart + k < bend) stage_splat(s, k, sorted_vals[start + bstart + k], xydr, conic, colors);
-        }
+        stage_batch<PX>(s, s_mask, tile, tiles_x, sorted_vals, start + bstart, bend - bstart, xydr, conic, colors);
         __syncthreads();
         const int kmax = min(bend, warp_max) - bstart;  // positions >= warp_max are inactive for this warp
-        for (int k = kmax - 1; k >= 0; --k) {
-            const int pos = bstart + k;
-            const float4 a = s.a[k];
-            const float hC = s.b[k].x;
-            const float dx = __fsub_rn(px, a.x);
-            const float hAdx = __fmul_rn(a.z, dx);
-            float sg[PX], dy[PX];
-            bool v[PX];
-            bool any = false;
+#pragma unroll 1
+        for (int j = MW - 1; j >= 0; --j) {
+            const int lim = kmax - 32 * j;
+            if (lim <= 0) continue;
+            uint32_t m = s_mask[warp][j] & (lim >= 32 ? 0xffffffffu : ((1u << lim) - 1u));
+            while (m) {
+                const int b = 31 - __clz(m);
+                m &= ~(1u << b);
+                const int k = 32 * j + b;
+                const int pos = bstart + k;
+                const float4 a = s.a[k];
+                const float hC = s.b[k].x;
+                const float dx = __fsub_rn(px, a.x);
+                const float hAdx = __fmul_rn(a.z, dx);
+                float sg[PX], dy[PX];
+                bool v[PX];
+                bool any = false;
 #pragma unroll
-            for (int q = 0; q < PX; ++q) {
-                dy[q] = __fsub_rn(py[q], a.y);
-                sg[q] = splat_sigma_h(dx, hAdx, dy[q], a.w, hC);
-                v[q] = pos < nc[q] && sg[q] <= SIGMA_CUT;
-                any |= v[q];
-            }
-            if (COUNT) {
-#pragma unroll
-                for (int q = 0; q < PX; ++q) e_s += v[q];
-            }
-            if (!__any_sync(0xffffffffu, any)) continue;
-            const float4 bq = s.b[k];
-            const float blue = s.c[k];
-            const float A2 = 2.f * a.z, C2 = 2.f * bq.x;
-            float acc[9];
-#pragma unroll
-            for (int j = 0; j < 9; ++j) acc[j] = 0.f;
-            bool anyc = false;
-#pragma unroll
-            for (int q = 0; q < PX; ++q) {
-                if (!v[q]) continue;
-                const float e = splat_exp_neg(sg[q]);
-                const float araw = __fmul_rn(bq.y, e);
-                const float alpha = fminf(araw, ALPHA_MAX);
-                if (!(alpha >= ALPHA_MIN)) continue;
-                anyc = true;
-                if (COUNT) ++e_c;
-                const float inv = rcp_approx(1.f - alpha);
-                const float th = T[q] * inv;  // T before this splat (:75)
-                const float w = alpha * th;
-                acc[0] = fmaf(w, g0[q], acc[0]);
-                acc[1] = fmaf(w, g1[q], acc[1]);
-                acc[2] = fmaf(w, g2[q], acc[2]);
-                const float cdot = bq.z * g0[q] + bq.w * g1[q] + blue * g2[q];
-                const float sdot = S0[q] * g0[q] + S1[q] * g1[q] + S2[q] * g2[q];
-                const float da = th * cdot - inv * sdot;
-                if (araw < ALPHA_MAX) {  // live (:91)
-                    acc[3] = fmaf(da, e, acc[3]);
-                    const float m = araw * da;  // = -d_sigma
-                    const float y0 = A2 * dx + a.w * dy[q];
-                    const float y1 = a.w * dx + C2 * dy[q];
-                    const float my0 = m * y0, hm = 0.5f * m;
-                    acc[4] += my0;
-                    acc[5] = fmaf(m, y1, acc[5]);
-                    acc[6] = fmaf(hm * y0, y0, acc[6]);
-                    acc[7] = fmaf(hm * y0, y1, acc[7]);
-                    acc[8] = fmaf(hm * y1, y1, acc[8]);
+                for (int q = 0; q < PX; ++q) {
+                    dy[q] = __fsub_rn(py[q], a.y);
+                    sg[q] = splat_sigma_h(dx, hAdx, dy[q], a.w, hC);
+                    v[q] = pos < nc[q] && sg[q] <= SIGMA_CUT;
+                    any |= v[q];
                 }
-                S0[q] = fmaf(w, bq.z, S0[q]);
-                S1[q] = fmaf(w, bq.w, S1[q]);
-                S2[q] = fmaf(w, blue, S2[q]);
-                T[q] = th;
-            }
-            if (!__any_sync(0xffffffffu, anyc)) continue;
-            const float r = warp_reduce8(acc, lane);
-            float c11 = acc[8];
+                if (COUNT) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) c11 += __shfl_xor_sync(0xffffffffu, c11, o);
-            const uint32_t id = s.id[k];
-            if ((lane & 3) == 0) {
-                const int idx = lane >> 2;
-                float* dst = idx < 4 ? reinterpret_cast<float*>(&d_rgbo[id]) + idx
-                                     : reinterpret_cast<float*>(&d_geo[id]) + (idx - 4);
-                atomicAdd(dst, r);
+                    for (int q = 0; q < PX; ++q) e_s += v[q];
+                }
+                if (!__any_sync(0xffffffffu, any)) continue;
+                const float4 bq = s.b[k];
+                const float blue = s.c[k];
+                const float A2 = 2.f * a.z, C2 = 2.f * bq.x;
+                float acc[9];
+#pragma unroll
+                for (int t = 0; t < 9; ++t) acc[t] = 0.f;
+                bool anyc = false;
+#pragma unroll
+                for (int q = 0; q < PX; ++q) {
+                    if (!v[q]) continue;
+                    const float e = splat_exp_neg(sg[q]);
+                    const float araw = __fmul_rn(bq.y, e);
+                    const float alpha = fminf(araw, ALPHA_MAX);
+                    if (!(alpha >= ALPHA_MIN)) continue;
+                    anyc = true;
+                    if (COUNT) ++e_c;
+                    const float inv = rcp_approx(1.f - alpha);
+                    const float th = T[q] * inv;  // T before this splat (:75)
+                    const float w = alpha * th;
+                    acc[0] = fmaf(w, g0[q], acc[0]);
+                    acc[1] = fmaf(w, g1[q], acc[1]);
+                    acc[2] = fmaf(w, g2[q], acc[2]);
+                    const float cdot = bq.z * g0[q] + bq.w * g1[q] + blue * g2[q];
+                    const float sdot = S0[q] * g0[q] + S1[q] * g1[q] + S2[q] * g2[q];
+                    const float da = th * cdot - inv * sdot;
+                    if (araw < ALPHA_MAX) {  // live (:91)
+                        acc[3] = fmaf(da, e, acc[3]);
+                        const float mm = araw * da;  // = -d_sigma
+                        const float y0 = A2 * dx + a.w * dy[q];
+                        const float y1 = a.w * dx + C2 * dy[q];
+                        const float hm = 0.5f * mm;
+                        acc[4] = fmaf(mm, y0, acc[4]);
+                        acc[5] = fmaf(mm, y1, acc[5]);
+                        acc[6] = fmaf(hm * y0, y0, acc[6]);
+                        acc[7] = fmaf(hm * y0, y1, acc[7]);
+                        acc[8] = fmaf(hm * y1, y1, acc[8]);
+                    }
+                    S0[q] = fmaf(w, bq.z, S0[q]);
+                    S1[q] = fmaf(w, bq.w, S1[q]);
+                    S2[q] = fmaf(w, blue, S2[q]);
+                    T[q] = th;
+                }
+                if (!__any_sync(0xffffffffu, anyc)) continue;
+                const float r = warp_reduce8(acc, lane);
+                float c11 = acc[8];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c11 += __shfl_xor_sync(0xffffffffu, c11, o);
+                const uint32_t id = s.id[k];
+                if ((lane & 3) == 0) {
+                    const int idx = lane >> 2;
+                    float* dst = idx < 4 ? reinterpret_cast<float*>(&d_rgbo[id]) + idx
+                                         : reinterpret_cast<float*>(&d_geo[id]) + (idx - 4);
+                    atomicAdd(dst, r);
+                }
+                if (lane == 0) atomicAdd(&d_c11[id], c11);
             }
-            if (lane == 0) atomicAdd(&d_c11[id], c11);
         }
     }
     if (COUNT) {
@@ -371,13 +436,13 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_bwd_kernel(
     }
 }
 
-// Pixels per thread (2 or 4); GS_RASTER_PX overrides for experiments.
-static int raster_px(const char* which) {
-    static int fwd = -1, bwd = -1;
-    int& v = which[0] == 'f' ? fwd : bwd;
+// Pixels per thread, shared by forward and backward (they must replay the
+// same evaluation sequence).  GS_RASTER_PX=2|4|8 overrides for experiments.
+static int raster_px() {
+    static int v = -1;
     if (v < 0) {
-        v = 4;
-        const char* e = getenv(which[0] == 'f' ? "GS_RASTER_PX_FWD" : "GS_RASTER_PX_BWD");
+        v = 2;
+        const char* e = getenv("GS_RASTER_PX");
         if (e && (atoi(e) == 2 || atoi(e) == 4 || atoi(e) == 8)) v = atoi(e);
     }
     return v;
@@ -414,8 +479,8 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
                       unsigned long long* counts, cudaStream_t s) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
-    const int pxf = raster_px("fwd");
-    auto f = pxf == 2 ? launch_fwd<2> : pxf == 8 ? launch_fwd<8> : launch_fwd<4>;
+    const int px = raster_px();
+    auto f = px == 2 ? launch_fwd<2> : px == 8 ? launch_fwd<8> : launch_fwd<4>;
     f(et, counts != nullptr, nt, s, ranges, vals, (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H,
       tiles_x, img, T, nc, counts);
     return check_launch("raster_fwd_kernel");
@@ -427,8 +492,8 @@ int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xy
                       cudaStream_t s) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
-    const int pxb = raster_px("bwd");
-    auto f = pxb == 2 ? launch_bwd<2> : pxb == 8 ? launch_bwd<8> : launch_bwd<4>;
+    const int px = raster_px();
+    auto f = px == 2 ? launch_bwd<2> : px == 8 ? launch_bwd<8> : launch_bwd<4>;
     f(counts != nullptr, nt, s, ranges, vals, (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H,
       tiles_x, fT, nc, dimg, (float4*)d_rgbo4, (float4*)d_geo4, d_c11, counts);
     return check_launch("raster_bwd_kernel");
@@ -445,15 +510,10 @@ int gs_raster_fwd(const uint32_t* ranges2, const uint32_t* sorted_vals, const fl
                   int early_termination, float* out_image, float* out_final_T, int32_t* out_n_contrib,
                   unsigned long long* counts, gs_stream_t stream) {
     if (width < 1 || height < 1) return set_error("gs_raster_fwd: bad image size %dx%d", width, height);
-    const int tiles_x = (width + TILE - 1) / TILE, tiles_y = (height + TILE - 1) / TILE;
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
-    const unsigned nt = (unsigned)(tiles_x * tiles_y);
-    cudaStream_t s = (cudaStream_t)stream;
-    const int pxf = raster_px("fwd");
-    auto f = pxf == 2 ? launch_fwd<2> : pxf == 8 ? launch_fwd<8> : launch_fwd<4>;
-    f(early_termination != 0, counts != nullptr, nt, s, (const uint2*)ranges2, sorted_vals, (const float4*)xydr4,
-      (const float4*)conic4, colors3, bg, width, height, tiles_x, out_image, out_final_T, out_n_contrib, counts);
-    return check_launch("raster_fwd_kernel");
+    return launch_raster_fwd((const uint2*)ranges2, sorted_vals, xydr4, conic4, colors3, bg, width, height,
+                             early_termination != 0, out_image, out_final_T, out_n_contrib, counts,
+                             (cudaStream_t)stream);
 }
 
 int gs_raster_bwd(const uint32_t* ranges2, const uint32_t* sorted_vals, const float* xydr4, const float* conic4,
@@ -461,16 +521,9 @@ int gs_raster_bwd(const uint32_t* ranges2, const uint32_t* sorted_vals, const fl
                   const float* final_T, const int32_t* n_contrib, const float* d_image, float* d_rgbo4,
                   float* d_geo4, float* d_c11, unsigned long long* counts, gs_stream_t stream) {
     if (width < 1 || height < 1) return set_error("gs_raster_bwd: bad image size %dx%d", width, height);
-    const int tiles_x = (width + TILE - 1) / TILE, tiles_y = (height + TILE - 1) / TILE;
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
-    const unsigned nt = (unsigned)(tiles_x * tiles_y);
-    cudaStream_t s = (cudaStream_t)stream;
-    const int pxb = raster_px("bwd");
-    auto f = pxb == 2 ? launch_bwd<2> : pxb == 8 ? launch_bwd<8> : launch_bwd<4>;
-    f(counts != nullptr, nt, s, (const uint2*)ranges2, sorted_vals, (const float4*)xydr4, (const float4*)conic4,
-      colors3, bg, width, height, tiles_x, final_T, n_contrib, d_image, (float4*)d_rgbo4, (float4*)d_geo4, d_c11,
-      counts);
-    return check_launch("raster_bwd_kernel");
+    return launch_raster_bwd((const uint2*)ranges2, sorted_vals, xydr4, conic4, colors3, bg, width, height, final_T,
+                             n_contrib, d_image, d_rgbo4, d_geo4, d_c11, counts, (cudaStream_t)stream);
 }
 
 }  // extern "C"
