@@ -71,6 +71,48 @@ __device__ __forceinline__ float splat_sigma_h(float dx, float hAdx, float dy, f
     return __fmaf_rn(dx, __fmaf_rn(B, dy, hAdx), __fmul_rn(__fmul_rn(hC, dy), dy));
 }
 
+// ---- packed fp32 pairs (sm_100a FFMA2/FMUL2/FADD2) ----------------------
+// Two pixels of one column are evaluated with one f32x2 instruction per op;
+// a scalar operand is broadcast for free.  Per lane the rounding is that of
+// the scalar op, so splat_sigma2 == (splat_sigma_h(lo), splat_sigma_h(hi))
+// bit for bit.
+typedef unsigned long long f32x2;
+
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk2(f32x2 v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f32x2 pin2(f32x2 x) {
+    asm volatile("" : "+l"(x));
+    return x;
+}
+
+// sigma for the pixel pair dy = (dy_lo, dy_hi) sharing dx (and hA*dx).
+__device__ __forceinline__ f32x2 splat_sigma2(float dx, float hAdx, f32x2 dy, float B, float hC) {
+    const f32x2 t = fma2(pk2(B, B), dy, pk2(hAdx, hAdx));
+    const f32x2 u = mul2(mul2(pk2(hC, hC), dy), dy);
+    return fma2(pk2(dx, dx), t, u);
+}
+
 // exp(-sigma) shared by forward and backward (sg/raster_forward.py:136,
 // sg/raster_backward.py:68).
 __device__ __forceinline__ float splat_exp_neg(float sigma) {

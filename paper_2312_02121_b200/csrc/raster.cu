@@ -133,17 +133,22 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_fwd_kernel(
     const int warp = threadIdx.x >> 5;
     const G geo(tile, tiles_x);
     const float INF = __int_as_float(0x7f800000);
+    static_assert(PX % 2 == 0, "pixels are evaluated in f32x2 pairs");
+    constexpr int NP = PX / 2;
     const float px = pin((float)geo.col + 0.5f);
     float py[PX], T[PX], cr[PX], cg[PX], cb[PX];
     int nc[PX], stop[PX];
+    f32x2 PY[NP];
     unsigned done = 0;
 #pragma unroll
     for (int q = 0; q < PX; ++q) {
         const bool in = geo.col < W && geo.row[q] < H;
-        py[q] = pin(in ? (float)geo.row[q] + 0.5f : INF);
+        py[q] = in ? (float)geo.row[q] + 0.5f : INF;
         done |= in ? 0u : (1u << q);
         T[q] = 1.f; cr[q] = 0.f; cg[q] = 0.f; cb[q] = 0.f; nc[q] = 0; stop[q] = -1;
     }
+#pragma unroll
+    for (int j = 0; j < NP; ++j) PY[j] = pin2(pk2(py[2 * j], py[2 * j + 1]));
     constexpr unsigned ALL = (1u << PX) - 1u;
     const uint2 rg = ranges[tile];
     const int start = (int)rg.x, end = (int)rg.y;
@@ -170,8 +175,10 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_fwd_kernel(
                 bool vis[PX];
                 bool any = false;
 #pragma unroll
+                for (int j = 0; j < NP; ++j)
+                    upk2(splat_sigma2(dx, hAdx, sub2(PY[j], pk2(a.y, a.y)), a.w, hC), sg[2 * j], sg[2 * j + 1]);
+#pragma unroll
                 for (int q = 0; q < PX; ++q) {
-                    sg[q] = splat_sigma_h(dx, hAdx, __fsub_rn(py[q], a.y), a.w, hC);
                     vis[q] = sg[q] <= SIGMA_CUT;  // false for retired pixels (py = inf)
                     any |= vis[q];
                 }
@@ -192,6 +199,7 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_fwd_kernel(
                     const float nT = __fmul_rn(T[q], __fsub_rn(1.f, alpha));
                     if (ET && nT < T_MIN) {  // stop WITHOUT compositing (:141-144)
                         py[q] = INF;
+                        PY[q / 2] = pk2(py[q & ~1], py[q | 1]);
                         done |= 1u << q;
                         stop[q] = pos_base + k;
                         continue;
@@ -296,6 +304,8 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_bwd_kernel(
     __shared__ int s_max[NW];
     const int tile = blockIdx.x;
     const G geo(tile, tiles_x);
+    static_assert(PX % 2 == 0, "pixels are evaluated in f32x2 pairs");
+    constexpr int NP = PX / 2;
     const float px = pin((float)geo.col + 0.5f);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float py[PX], T[PX], S0[PX], S1[PX], S2[PX], g0[PX], g1[PX], g2[PX];
@@ -304,7 +314,7 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_bwd_kernel(
 #pragma unroll
     for (int q = 0; q < PX; ++q) {
         const bool in = geo.col < W && geo.row[q] < H;
-        py[q] = pin((float)geo.row[q] + 0.5f);
+        py[q] = (float)geo.row[q] + 0.5f;
         T[q] = 1.f; nc[q] = 0; g0[q] = 0.f; g1[q] = 0.f; g2[q] = 0.f;
         if (in) {
             const int p = geo.row[q] * W + geo.col;
@@ -315,6 +325,9 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_bwd_kernel(
         S0[q] = bg.x * T[q]; S1[q] = bg.y * T[q]; S2[q] = bg.z * T[q];
         my_max = max(my_max, nc[q]);
     }
+    f32x2 PY[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) PY[j] = pin2(pk2(py[2 * j], py[2 * j + 1]));
     const int warp_max = __reduce_max_sync(0xffffffffu, my_max);
     if (lane == 0) s_max[warp] = warp_max;
     const uint2 rg = ranges[tile];
@@ -349,9 +362,13 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_bwd_kernel(
                 bool v[PX];
                 bool any = false;
 #pragma unroll
+                for (int j = 0; j < NP; ++j) {
+                    const f32x2 DY = sub2(PY[j], pk2(a.y, a.y));
+                    upk2(DY, dy[2 * j], dy[2 * j + 1]);
+                    upk2(splat_sigma2(dx, hAdx, DY, a.w, hC), sg[2 * j], sg[2 * j + 1]);
+                }
+#pragma unroll
                 for (int q = 0; q < PX; ++q) {
-                    dy[q] = __fsub_rn(py[q], a.y);
-                    sg[q] = splat_sigma_h(dx, hAdx, dy[q], a.w, hC);
                     v[q] = pos < nc[q] && sg[q] <= SIGMA_CUT;
                     any |= v[q];
                 }

@@ -23,6 +23,9 @@ constexpr uint32_t ST_AGG = 1u << 30;
 constexpr uint32_t ST_PRE = 2u << 30;
 constexpr uint32_t ST_MASK = (1u << 30) - 1;
 
+// Items per thread: the large tile amortises the look-back for big inputs;
+// the small one (4 items) gives 4x more CTAs when the input would otherwise
+// fill less than two waves (latency-bound passes at N ~ 1e5).
 template <typename K>
 struct SortCfg;
 template <>
@@ -33,13 +36,14 @@ template <>
 struct SortCfg<unsigned long long> {
     static constexpr int ITEMS = 15;
 };
+constexpr int SMALL_ITEMS = 4;
 
-template <typename K>
-constexpr int sort_tile() { return SORT_THREADS * SortCfg<K>::ITEMS; }
+template <typename K, int ITEMS>
+constexpr int sort_tile() { return SORT_THREADS * ITEMS; }
 
-template <typename K>
+template <typename K, int ITEMS>
 constexpr size_t sort_smem() {
-    return (size_t)sort_tile<K>() * (sizeof(K) + 4) + (size_t)SORT_WARPS * RADIX * 4 + 2 * RADIX * 4;
+    return (size_t)sort_tile<K, ITEMS>() * (sizeof(K) + 4) + (size_t)SORT_WARPS * RADIX * 4 + 2 * RADIX * 4;
 }
 
 __device__ __forceinline__ uint32_t ldv(const uint32_t* p) { return *(const volatile uint32_t*)p; }
@@ -97,13 +101,12 @@ __device__ __forceinline__ uint32_t block_incl_scan256(uint32_t v, uint32_t* s_t
 }
 
 // One 8-bit pass.  vin == nullptr means value = input index (identity).
-template <typename K>
+template <typename K, int ITEMS>
 __global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_cap, const unsigned long long* __restrict__ n_dev, int shift,
     const uint32_t* __restrict__ hist, uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
-    constexpr int ITEMS = SortCfg<K>::ITEMS;
-    constexpr int TILE_N = sort_tile<K>();
+    constexpr int TILE_N = sort_tile<K, ITEMS>();
     extern __shared__ __align__(16) unsigned char smem[];
     K* s_keys = reinterpret_cast<K*>(smem);
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + TILE_N);
@@ -202,12 +205,12 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
     }
 }
 
-template <typename K>
+template <typename K, int ITEMS>
 static int set_sort_attr() {
     static bool done = false;
     if (!done) {
-        if (cudaFuncSetAttribute(onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sort_smem<K>()) != cudaSuccess)
+        if (cudaFuncSetAttribute(onesweep_kernel<K, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sort_smem<K, ITEMS>()) != cudaSuccess)
             return check_launch("onesweep smem attribute");
         done = true;
     }
@@ -224,9 +227,10 @@ int sort_sm_count() {
     return sms;
 }
 
+// Sized for the small tile (the most CTAs either variant can launch).
 template <typename K>
 size_t onesweep_status_bytes(int64_t n_cap, int passes) {
-    const int64_t tiles = (n_cap + sort_tile<K>() - 1) / sort_tile<K>();
+    const int64_t tiles = (n_cap + sort_tile<K, SMALL_ITEMS>() - 1) / sort_tile<K, SMALL_ITEMS>();
     return (size_t)passes * (size_t)(tiles > 0 ? tiles : 1) * RADIX * 4;
 }
 template size_t onesweep_status_bytes<uint32_t>(int64_t, int);
@@ -237,19 +241,18 @@ template size_t onesweep_status_bytes<unsigned long long>(int64_t, int);
 // `passes` zeroed uint32.  identity_vals: the first pass ignores v0's
 // contents and uses the input index as value (v0 is still the ping-pong
 // scratch).  Result lands in (k1, v1) when passes is odd, else (k0, v0).
-template <typename K>
-int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
-                 int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
-                 bool identity_vals) {
-    if (n_cap <= 0) return 0;
-    if (set_sort_attr<K>()) return -1;
-    const int64_t tiles = (n_cap + sort_tile<K>() - 1) / sort_tile<K>();
+template <typename K, int ITEMS>
+static int run_passes(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
+                      int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
+                      bool identity_vals) {
+    if (set_sort_attr<K, ITEMS>()) return -1;
+    const int64_t tiles = (n_cap + sort_tile<K, ITEMS>() - 1) / sort_tile<K, ITEMS>();
     K* kin = k0;
     K* kout = k1;
     uint32_t* vin = v0;
     uint32_t* vout = v1;
     for (int p = 0; p < passes; ++p) {
-        onesweep_kernel<K><<<(unsigned)tiles, SORT_THREADS, sort_smem<K>(), s>>>(
+        onesweep_kernel<K, ITEMS><<<(unsigned)tiles, SORT_THREADS, sort_smem<K, ITEMS>(), s>>>(
             kin, (p == 0 && identity_vals) ? nullptr : vin, kout, vout, n_cap, n_dev, 8 * p, hist + p * RADIX,
             status + (size_t)p * tiles * RADIX, counters + p);
         if (check_launch("onesweep_kernel")) return -1;
@@ -257,6 +260,19 @@ int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const 
         uint32_t* tv = vin; vin = vout; vout = tv;
     }
     return 0;
+}
+
+template <typename K>
+int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
+                 int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
+                 bool identity_vals) {
+    if (n_cap <= 0) return 0;
+    constexpr int BIG = SortCfg<K>::ITEMS;
+    const int64_t big_tiles = (n_cap + sort_tile<K, BIG>() - 1) / sort_tile<K, BIG>();
+    if (big_tiles < 2 * (int64_t)sort_sm_count())
+        return run_passes<K, SMALL_ITEMS>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s,
+                                          identity_vals);
+    return run_passes<K, BIG>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
 }
 template int run_onesweep<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, int64_t,
                                     const unsigned long long*, int, const uint32_t*, uint32_t*, uint32_t*,
