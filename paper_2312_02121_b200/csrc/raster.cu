@@ -161,58 +161,86 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_fwd_kernel(
         if (__all_sync(0xffffffffu, done == ALL)) continue;  // whole warp finished: only help staging
         const int pos_base = b0 - start + 1;
         bool warp_done = false;
+        // composite splat k (sigma already evaluated) into the visible pixels
+        auto slow = [&](int k, const float* sg, const bool* vis) {
+            const float4 bq = s.b[k];
+            const float blue = s.c[k];
+#pragma unroll
+            for (int q = 0; q < PX; ++q) {
+                if (!vis[q]) continue;
+                const float e = splat_exp_neg(sg[q]);
+                const float alpha = fminf(__fmul_rn(bq.y, e), ALPHA_MAX);
+                if (!(alpha >= ALPHA_MIN)) continue;
+                if (COUNT) ++e_a;
+                const float nT = __fmul_rn(T[q], __fsub_rn(1.f, alpha));
+                if (ET && nT < T_MIN) {  // stop WITHOUT compositing (:141-144)
+                    py[q] = INF;
+                    PY[q / 2] = pk2(py[q & ~1], py[q | 1]);
+                    done |= 1u << q;
+                    stop[q] = pos_base + k;
+                    continue;
+                }
+                if (COUNT) ++e_c;
+                const float w = __fmul_rn(alpha, T[q]);
+                cr[q] = __fmaf_rn(w, bq.z, cr[q]);
+                cg[q] = __fmaf_rn(w, bq.w, cg[q]);
+                cb[q] = __fmaf_rn(w, blue, cb[q]);
+                T[q] = nT;
+                nc[q] = pos_base + k;
+            }
+        };
 #pragma unroll 1
         for (int j = 0; j < MW && !warp_done; ++j) {
             uint32_t m = s_mask[warp][j];
             while (m) {
-                const int k = j * 32 + (__ffs(m) - 1);
+                // two splats per iteration: independent sigma chains (ILP),
+                // compositing still strictly in list order
+                const int k0 = j * 32 + (__ffs(m) - 1);
                 m &= m - 1;
-                const float4 a = s.a[k];
-                const float hC = s.b[k].x;
-                const float dx = __fsub_rn(px, a.x);
-                const float hAdx = __fmul_rn(a.z, dx);
-                float sg[PX];
-                bool vis[PX];
-                bool any = false;
+                const bool has1 = m != 0;
+                const int k1 = has1 ? j * 32 + (__ffs(m) - 1) : k0;
+                m &= m - 1;
+                const float4 a0 = s.a[k0], a1 = s.a[k1];
+                const float hC0 = s.b[k0].x, hC1 = s.b[k1].x;
+                const float dx0 = __fsub_rn(px, a0.x), dx1 = __fsub_rn(px, a1.x);
+                const float hAdx0 = __fmul_rn(a0.z, dx0), hAdx1 = __fmul_rn(a1.z, dx1);
+                float sg0[PX], sg1[PX];
+                bool vis0[PX], vis1[PX];
+                bool any0 = false, any1 = false;
 #pragma unroll
-                for (int j = 0; j < NP; ++j)
-                    upk2(splat_sigma2(dx, hAdx, sub2(PY[j], pk2(a.y, a.y)), a.w, hC), sg[2 * j], sg[2 * j + 1]);
+                for (int t = 0; t < NP; ++t) {
+                    upk2(splat_sigma2(dx0, hAdx0, sub2(PY[t], pk2(a0.y, a0.y)), a0.w, hC0), sg0[2 * t],
+                         sg0[2 * t + 1]);
+                    upk2(splat_sigma2(dx1, hAdx1, sub2(PY[t], pk2(a1.y, a1.y)), a1.w, hC1), sg1[2 * t],
+                         sg1[2 * t + 1]);
+                }
 #pragma unroll
                 for (int q = 0; q < PX; ++q) {
-                    vis[q] = sg[q] <= SIGMA_CUT;  // false for retired pixels (py = inf)
-                    any |= vis[q];
+                    vis0[q] = sg0[q] <= SIGMA_CUT;  // false for retired pixels (py = inf)
+                    vis1[q] = has1 && sg1[q] <= SIGMA_CUT;
+                    any0 |= vis0[q];
+                    any1 |= vis1[q];
                 }
+                const uint32_t v0 = __ballot_sync(0xffffffffu, any0);
+                const uint32_t v1 = __ballot_sync(0xffffffffu, any1);
                 if (COUNT) {
 #pragma unroll
-                    for (int q = 0; q < PX; ++q) e_s += vis[q];
+                    for (int q = 0; q < PX; ++q) e_s += vis0[q];
                 }
-                if (!__any_sync(0xffffffffu, any)) continue;
-                const float4 bq = s.b[k];
-                const float blue = s.c[k];
+                if (v0) slow(k0, sg0, vis0);
+                if (v1) {
 #pragma unroll
-                for (int q = 0; q < PX; ++q) {
-                    if (!vis[q]) continue;
-                    const float e = splat_exp_neg(sg[q]);
-                    const float alpha = fminf(__fmul_rn(bq.y, e), ALPHA_MAX);
-                    if (!(alpha >= ALPHA_MIN)) continue;
-                    if (COUNT) ++e_a;
-                    const float nT = __fmul_rn(T[q], __fsub_rn(1.f, alpha));
-                    if (ET && nT < T_MIN) {  // stop WITHOUT compositing (:141-144)
-                        py[q] = INF;
-                        PY[q / 2] = pk2(py[q & ~1], py[q | 1]);
-                        done |= 1u << q;
-                        stop[q] = pos_base + k;
-                        continue;
+                    for (int q = 0; q < PX; ++q) vis1[q] = vis1[q] && !((done >> q) & 1u);  // retired at k0
+                    if (COUNT) {
+#pragma unroll
+                        for (int q = 0; q < PX; ++q) e_s += vis1[q];
                     }
-                    if (COUNT) ++e_c;
-                    const float w = __fmul_rn(alpha, T[q]);
-                    cr[q] = __fmaf_rn(w, bq.z, cr[q]);
-                    cg[q] = __fmaf_rn(w, bq.w, cg[q]);
-                    cb[q] = __fmaf_rn(w, blue, cb[q]);
-                    T[q] = nT;
-                    nc[q] = pos_base + k;
+                    slow(k1, sg1, vis1);
+                } else if (COUNT && has1) {
+#pragma unroll
+                    for (int q = 0; q < PX; ++q) e_s += vis1[q] && !((done >> q) & 1u);
                 }
-                if (ET && __all_sync(0xffffffffu, done == ALL)) {
+                if (ET && (v0 | v1) && __all_sync(0xffffffffu, done == ALL)) {
                     warp_done = true;
                     break;
                 }
@@ -419,12 +447,24 @@ __global__ void __launch_bounds__(TileGeom<PX>::THREADS) raster_bwd_kernel(
                     S2[q] = fmaf(w, blue, S2[q]);
                     T[q] = th;
                 }
-                if (!__any_sync(0xffffffffu, anyc)) continue;
+                const uint32_t cmask = __ballot_sync(0xffffffffu, anyc);
+                if (!cmask) continue;
+                const uint32_t id = s.id[k];
+                if (__popc(cmask) <= 3) {
+                    // few contributing lanes: their own vector reductions are
+                    // cheaper than a 9-value warp reduction (same or fewer
+                    // atomic lane-ops, ~45 fewer instructions)
+                    if (anyc) {
+                        red_add_v4(&d_rgbo[id], acc[0], acc[1], acc[2], acc[3]);
+                        red_add_v4(&d_geo[id], acc[4], acc[5], acc[6], acc[7]);
+                        atomicAdd(&d_c11[id], acc[8]);
+                    }
+                    continue;
+                }
                 const float r = warp_reduce8(acc, lane);
                 float c11 = acc[8];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) c11 += __shfl_xor_sync(0xffffffffu, c11, o);
-                const uint32_t id = s.id[k];
                 if ((lane & 3) == 0) {
                     const int idx = lane >> 2;
                     float* dst = idx < 4 ? reinterpret_cast<float*>(&d_rgbo[id]) + idx

@@ -269,7 +269,7 @@ int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const 
     if (n_cap <= 0) return 0;
     constexpr int BIG = SortCfg<K>::ITEMS;
     const int64_t big_tiles = (n_cap + sort_tile<K, BIG>() - 1) / sort_tile<K, BIG>();
-    if (big_tiles < 2 * (int64_t)sort_sm_count())
+    if (big_tiles < 64)
         return run_passes<K, SMALL_ITEMS>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s,
                                           identity_vals);
     return run_passes<K, BIG>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
