@@ -101,6 +101,28 @@ __device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
 }
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f32x2 bc2(float v) { return pk2(v, v); }
+__device__ __forceinline__ float lo2(f32x2 v) {
+    float a, b;
+    upk2(v, a, b);
+    return a;
+}
+__device__ __forceinline__ float hi2(f32x2 v) {
+    float a, b;
+    upk2(v, a, b);
+    return b;
+}
+__device__ __forceinline__ f32x2 sel2(bool plo, bool phi, f32x2 a, f32x2 b) {  // per lane: p ? a : b
+    float alo, ahi, blo, bhi;
+    upk2(a, alo, ahi);
+    upk2(b, blo, bhi);
+    return pk2(plo ? alo : blo, phi ? ahi : bhi);
+}
 __device__ __forceinline__ f32x2 pin2(f32x2 x) {
     asm volatile("" : "+l"(x));
     return x;
