@@ -103,6 +103,12 @@ int gs_sort_pairs(unsigned long long* keys, unsigned long long* keys_alt, uint32
                   uint32_t* vals_alt, int64_t n, int end_bit, void* ws, size_t ws_bytes,
                   int* selector /*[host]*/, gs_stream_t stream);
 
+/* gs_tile_counts: tiles touched by arbitrary (mean2d, radius) squares given
+ * as xydr4 rows (the input of sg/binning.py:27-47 assign_tiles when the
+ * projected list comes from the caller rather than gs_project_fwd). */
+int gs_tile_counts(const float* xydr4, int64_t n, int32_t width, int32_t height, uint32_t* out_tiles,
+                   gs_stream_t stream);
+
 /* gs_tile_ranges: per tile [start, end) into the sorted list (uint32 x 2,
  * zero-filled by the call for empty tiles). */
 int gs_tile_ranges(const unsigned long long* sorted_keys, int64_t n, uint32_t* ranges2,

@@ -16,7 +16,7 @@ EXPORTS = (
     "gs_last_error", "gs_version", "gs_device_sm_count",
     "gs_project_fwd",
     "gs_scan_workspace_bytes", "gs_scan_tiles", "gs_emit_keys",
-    "gs_sort_workspace_bytes", "gs_sort_pairs", "gs_tile_ranges",
+    "gs_sort_workspace_bytes", "gs_sort_pairs", "gs_tile_counts", "gs_tile_ranges",
     "gs_raster_fwd", "gs_raster_bwd",
     "gs_project_bwd_workspace_bytes", "gs_project_bwd",
     "gs_frame_workspace_bytes", "gs_frame_view_of", "gs_frame_forward", "gs_frame_backward",
@@ -71,6 +71,7 @@ def load():
         "gs_emit_keys": ([P, P, P, i64, i32, i32, P, P, P], C.c_int),
         "gs_sort_workspace_bytes": ([i64, C.c_int], sz),
         "gs_sort_pairs": ([P, P, P, P, i64, C.c_int, P, sz, C.POINTER(C.c_int), P], C.c_int),
+        "gs_tile_counts": ([P, i64, i32, i32, P, P], C.c_int),
         "gs_tile_ranges": ([P, i64, P, i32, P], C.c_int),
         "gs_raster_fwd": ([P, P, P, P, P, C.POINTER(C.c_float), i32, i32, C.c_int, P, P, P, P, P], C.c_int),
         "gs_raster_bwd": ([P, P, P, P, P, C.POINTER(C.c_float), i32, i32, P, P, P, P, P, P, P, P], C.c_int),

@@ -137,6 +137,24 @@ __global__ void __launch_bounds__(256) emit_kernel(const float4* __restrict__ xy
     }
 }
 
+// Tiles touched by an arbitrary (mean2d, radius) square (radius < 0 counts
+// 0), clamped to the grid like sg/binning.py:38-43 -- an off-image square
+// yields an empty rectangle.
+__global__ void __launch_bounds__(256) tile_counts_kernel(const float4* __restrict__ xydr, int n, int tiles_x,
+                                                          int tiles_y, uint32_t* __restrict__ tiles) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 g = xydr[i];
+    const int r = __float_as_int(g.w);
+    uint32_t c = 0;
+    if (r >= 0 && fabsf(g.x) < 1.6e7f && fabsf(g.y) < 1.6e7f) {
+        int tx0, tx1, ty0, ty1;
+        tile_rect(g.x, g.y, min(r, MAX_RADIUS), tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+        c = (uint32_t)(max(0, tx1 - tx0 + 1) * max(0, ty1 - ty0 + 1));
+    }
+    tiles[i] = c;
+}
+
 __global__ void __launch_bounds__(256) ranges_kernel(const unsigned long long* __restrict__ keys, int64_t n,
                                                      uint2* __restrict__ ranges) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -275,6 +293,16 @@ int gs_emit_keys(const float* xydr4, const uint32_t* offsets, const uint32_t* ti
     emit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         (const float4*)xydr4, offsets, tiles, (int)n, tiles_x, tiles_y, keys, vals);
     return check_launch("emit_kernel");
+}
+
+int gs_tile_counts(const float* xydr4, int64_t n, int32_t width, int32_t height, uint32_t* out_tiles,
+                   gs_stream_t stream) {
+    if (n < 0 || n > 0x7fffffff) return set_error("gs_tile_counts: n out of range");
+    if (n == 0) return 0;
+    const int tiles_x = (width + TILE - 1) / TILE, tiles_y = (height + TILE - 1) / TILE;
+    tile_counts_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        (const float4*)xydr4, (int)n, tiles_x, tiles_y, out_tiles);
+    return check_launch("tile_counts_kernel");
 }
 
 int gs_tile_ranges(const unsigned long long* sorted_keys, int64_t n, uint32_t* ranges2, int32_t n_tiles,

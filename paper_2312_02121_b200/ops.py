@@ -166,9 +166,29 @@ def tile_bits(n_tiles: int) -> int:
     return max(1, math.ceil(math.log2(n_tiles))) if n_tiles > 1 else 1
 
 
+def sort_pairs_(keys: torch.Tensor, vals: torch.Tensor, end_bit: int):
+    """gs_sort_pairs (stable onesweep radix sort of bits [0, end_bit)) on
+    int64 keys / int32 values; returns the sorted (keys, vals)."""
+    L = _lib.load()
+    n = keys.shape[0]
+    if n == 0:
+        return keys, vals
+    keys_alt = torch.empty_like(keys)
+    vals_alt = torch.empty_like(vals)
+    wsb = L.gs_sort_workspace_bytes(n, end_bit)
+    ws = torch.empty((wsb,), device=keys.device, dtype=torch.uint8)
+    sel = C.c_int(0)
+    check(L.gs_sort_pairs(_ptr(keys), _ptr(keys_alt), _ptr(vals), _ptr(vals_alt), n, end_bit, _ptr(ws), wsb,
+                          C.byref(sel), _stream()), "gs_sort_pairs")
+    return (keys_alt, vals_alt) if sel.value else (keys, vals)
+
+
 def emit_and_sort(proj: Projection, offsets: torch.Tensor, n_isect: int, cam: CameraParams,
-                  sort: bool = True) -> Bins:
-    """Stage 2 after the scan: key emission, onesweep sort, tile ranges."""
+                  sort: bool = True, key_bits: str = "tile_depth") -> Bins:
+    """Stage 2 after the scan: key emission, onesweep sort, tile ranges.
+    key_bits="tile" sorts on the tile id only (stable: index order per bin,
+    sg/binning.py:27-47 assign_tiles); "tile_depth" on (tile, depth)
+    (sg/binning.py:50-65 sort_bins)."""
     L = _lib.load()
     dev = proj.xydr.device
     n = proj.xydr.shape[0]
@@ -179,20 +199,50 @@ def emit_and_sort(proj: Projection, offsets: torch.Tensor, n_isect: int, cam: Ca
     check(L.gs_emit_keys(_ptr(proj.xydr), _ptr(offsets), _ptr(proj.tiles), n, cam.width, cam.height,
                          _ptr(keys), _ptr(vals), st), "gs_emit_keys")
     if sort and n_isect > 0:
-        end_bit = 32 + tile_bits(n_tiles)
-        keys_alt = torch.empty_like(keys)
-        vals_alt = torch.empty_like(vals)
-        wsb = L.gs_sort_workspace_bytes(n_isect, end_bit)
-        ws = torch.empty((wsb,), device=dev, dtype=torch.uint8)
-        sel = C.c_int(0)
-        check(L.gs_sort_pairs(_ptr(keys), _ptr(keys_alt), _ptr(vals), _ptr(vals_alt), n_isect, end_bit,
-                              _ptr(ws), wsb, C.byref(sel), st), "gs_sort_pairs")
-        if sel.value:
-            keys, vals = keys_alt, vals_alt
+        if key_bits == "tile":
+            keys, vals = sort_pairs_((keys >> 32).contiguous(), vals, tile_bits(n_tiles))
+            keys = (keys << 32).contiguous()
+        else:
+            keys, vals = sort_pairs_(keys, vals, 32 + tile_bits(n_tiles))
     ranges = torch.empty((n_tiles, 2), device=dev, dtype=torch.int32)
     if sort:
         check(L.gs_tile_ranges(_ptr(keys), n_isect, _ptr(ranges), n_tiles, st), "gs_tile_ranges")
     return Bins(ranges, keys, vals, n_isect)
+
+
+def tile_counts(xydr: torch.Tensor, cam: CameraParams) -> torch.Tensor:
+    """Tiles touched by each (mean2d, radius) square (gs_tile_counts)."""
+    L = _lib.load()
+    n = xydr.shape[0]
+    tiles = torch.empty((n,), device=xydr.device, dtype=torch.int32)
+    check(L.gs_tile_counts(_ptr(xydr), n, cam.width, cam.height, _ptr(tiles), _stream()), "gs_tile_counts")
+    return tiles
+
+
+def depth_rank(depths, dev) -> "np.ndarray":
+    """Rank of each float64 depth under a STABLE ascending sort (ties keep the
+    given order), computed with the device radix sort on order-preserving
+    transforms of the IEEE-754 bits."""
+    import numpy as np
+    d = torch.as_tensor(np.ascontiguousarray(depths, np.float64), device=dev)
+    bits = d.view(torch.int64)
+    neg = bits < 0
+    # order-preserving map to unsigned: flip all bits of negatives, set the sign bit of positives
+    key = torch.where(neg, ~bits, bits ^ torch.tensor(-(1 << 63), device=dev, dtype=torch.int64))
+    idx = torch.arange(d.shape[0], device=dev, dtype=torch.int32)
+    _, perm = sort_pairs_(key.contiguous(), idx, 64)
+    rank = torch.empty_like(perm)
+    rank[perm.long()] = torch.arange(d.shape[0], device=dev, dtype=torch.int32)
+    return rank.cpu().numpy().astype(np.int64)
+
+
+def stable_sort_pairs(keys, vals, dev, end_bit: int):
+    """Host convenience: stable device sort of int64 keys carrying int values."""
+    import numpy as np
+    k = torch.as_tensor(np.ascontiguousarray(keys, np.int64), device=dev)
+    v = torch.as_tensor(np.ascontiguousarray(vals, np.int32), device=dev)
+    _, sv = sort_pairs_(k, v, end_bit)
+    return sv.cpu().numpy().astype(np.int64)
 
 
 def bin_sort(proj: Projection, cam: CameraParams, status: torch.Tensor | None = None) -> Bins:
