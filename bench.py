@@ -67,6 +67,8 @@ def views_for(cfg, spec, world, rank):
         nv = len(spec.cameras)
         idx = list(range(rank, nv, world))
         return [(spec.cameras[i], spec.d_images[i]) for i in idx]
+    if cfg == 4:  # one frame; the band split is applied in run_ours
+        return [(spec.cameras[0], spec.d_images[0])]
     base = spec.cameras[0]
     if rank == 0:
         return [(base, spec.d_images[0])]
@@ -178,6 +180,18 @@ def run_ours(args):
     m, s, q, o, c = params
     cams = [ops.CameraParams.of(cv) for cv, _ in views]
     d_imgs = [t(d) for _, d in views]
+    band = None
+    if cfg == 4 and world > 1:
+        # tile-row bands balanced by intersections (every rank computes the same split)
+        from paper_2312_02121_b200 import dist as D
+        full = cams[0]
+        proj = ops.project(m, s, q, o, full)
+        work = D.tile_row_work_from_projection(proj.xydr, full.height, full.width)
+        band = D.band_rows(work, world, full.height)[rank]
+        cams = [D.band_camera(full, *band)]
+        d_imgs = [d_imgs[0][band[0]:band[1]].contiguous()]
+        views = [(cams[0], views[0][1][band[0]:band[1]])]
+        del proj
     bg = (0.0, 0.0, 0.0)
     flush = torch.empty(L2_FLUSH_BYTES // 4, device=dev, dtype=torch.float32)
     grad_flat = torch.zeros((n, 14), device=dev, dtype=torch.float32)
@@ -295,7 +309,7 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
     stage_ms /= max(args.steps, 1)
-    frames_per_step = len(cams) * world if cfg != 3 else len(spec.cameras)
+    frames_per_step = len(spec.cameras) if cfg in (3, 4) else len(cams) * world
     ms_per_step = total_ms / max(args.steps, 1)
     fps = frames_per_step / (ms_per_step / 1e3)
     evals_rank = float(counts_f[0] + counts_b[0])
@@ -308,7 +322,7 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, spec, views, dev, world)
+        e2e = run_e2e(args, spec, views, dev, world, frames_per_step)
 
     if rank != 0:
         if world > 1:
@@ -371,12 +385,12 @@ def run_ours(args):
     out = {
         "metric": METRIC, "value": round(fps, 3), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "strong" if cfg == 3 else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if cfg in (3, 4) else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded, BASELINE.json distributions; scenes.py)",
         "config": {"workload": f"config{cfg}", "gaussians": n, "image": f"{sz['width']}x{sz['height']}",
                    "views_per_step": frames_per_step, "views_per_rank": len(cams),
                    "early_termination": True, "background": "black",
-                   "parallelism": f"view-sharded x{world}" + (" + NCCL allreduce 14 fp32/Gaussian" if world > 1 else ""),
+                   "parallelism": (f"tile-row bands x{world} (rows {band})" if band else f"view-sharded x{world}") + (" + NCCL allreduce 14 fp32/Gaussian" if world > 1 else ""),
                    "cuda_graph": graph is not None,
                    "l2": "flushed between timed steps (256 MiB write, untimed)"},
         "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
@@ -397,7 +411,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, spec, views, dev, world):
+def run_e2e(args, spec, views, dev, world, frames):
     """Same metric through the public autograd API: pinned host params and
     upstream gradient are copied H2D inside the timed region, the parameter
     gradients are read back D2H; CUDA events + synchronize."""
@@ -448,7 +462,6 @@ def run_e2e(args, spec, views, dev, world):
         tt = torch.tensor([total], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total = float(tt.item())
-    frames = len(cams) * world if len(spec.cameras) == 1 else len(spec.cameras)
     return {"value": round(frames / (total / steps / 1e3), 3), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps, "api": "paper_2312_02121_b200.ops.rasterize + backward"}
 
