@@ -23,23 +23,29 @@
 //
 // Retired pixels (forward: out of the image or early-terminated) get
 // py = +inf, so sigma is inf/NaN and fails the cut.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.cuh"
 
 namespace gs {
 
-constexpr int NT = 128;  // threads per CTA
-constexpr int NW = 4;    // warps (quadrants)
-constexpr int RB = 128;  // splats per staged batch (one per thread)
+constexpr int NT = 128;  // threads per CTA (forward)
+constexpr int NW = 4;    // warps (quadrants, forward)
+constexpr int RB = 128;  // splats per staged batch
 
-struct Batch {
+// Warp regions: NWR = 4 -> four 8x8 quadrants (one pixel pair per lane);
+// NWR = 2 -> two 8-column x 16-row halves (two pixel pairs per lane).
+template <int NWR>
+struct BatchT {
     float4 a[RB];  // x, y, hA = A/2, B
     float4 b[RB];  // hC = C/2, opacity, r, g
     float c[RB];   // blue
     uint32_t id[RB];
-    uint32_t mask[NW][RB / 32];  // quadrant reach bits per group of 32 entries
-    uint8_t list[NW][RB];        // compacted entry indices per quadrant
+    uint32_t mask[NWR][RB / 32];  // region reach bits per group of 32 entries
+    uint8_t list[NWR][RB];        // compacted entry indices per region
 };
+using Batch = BatchT<NW>;
 
 __device__ __forceinline__ float pin(float x) {
     asm volatile("" : "+f"(x));
@@ -62,34 +68,41 @@ struct Quad {
     }
 };
 
-// Stage `count` entries starting at ids[first] and build the four quadrant
+// Stage `count` entries starting at ids[first] and build the warp-region
 // lists.  Returns this warp's list length.  Ends with the CTA synchronized.
-__device__ __forceinline__ int stage_batch(Batch& s, int tile, int tiles_x, const uint32_t* __restrict__ ids,
+template <int NWR>
+__device__ __forceinline__ int stage_batch(BatchT<NWR>& s, int tile, int tiles_x, const uint32_t* __restrict__ ids,
                                            int first, int count, const float4* __restrict__ xydr,
                                            const float4* __restrict__ conic, const float* __restrict__ colors) {
+    constexpr int NTR = 32 * NWR;
+    constexpr float RH = NWR == 4 ? 7.f : 15.f;  // region height - 1 (pixel rows)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int k = threadIdx.x;
-    const bool valid = k < count;
-    float x = 0.f, y = 0.f, r = -1e30f;
-    if (valid) {
-        const uint32_t id = ids[first + k];
-        const float4 g = xydr[id];
-        const float4 q = conic[id];
-        s.a[k] = make_float4(g.x, g.y, 0.5f * q.x, q.y);
-        s.b[k] = make_float4(0.5f * q.z, q.w, colors[3 * id], colors[3 * id + 1]);
-        s.c[k] = colors[3 * id + 2];
-        s.id[k] = id;
-        x = g.x;
-        y = g.y;
-        r = (float)__float_as_int(g.w) + 1.f;
-    }
     const int tx = tile % tiles_x, ty = tile / tiles_x;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        const float x0 = (float)(tx * TILE + (w & 1) * 8) + 0.5f, y0 = (float)(ty * TILE + (w >> 1) * 8) + 0.5f;
-        const bool ov = valid && x + r >= x0 && x - r <= x0 + 7.f && y + r >= y0 && y - r <= y0 + 7.f;
-        const uint32_t m = __ballot_sync(0xffffffffu, ov);
-        if (lane == 0) s.mask[w][warp] = m;
+    for (int u = 0; u < RB / NTR; ++u) {
+        const int k = u * NTR + (int)threadIdx.x;
+        const bool valid = k < count;
+        float x = 0.f, y = 0.f, r = -1e30f;
+        if (valid) {
+            const uint32_t id = ids[first + k];
+            const float4 g = xydr[id];
+            const float4 q = conic[id];
+            s.a[k] = make_float4(g.x, g.y, 0.5f * q.x, q.y);
+            s.b[k] = make_float4(0.5f * q.z, q.w, colors[3 * id], colors[3 * id + 1]);
+            s.c[k] = colors[3 * id + 2];
+            s.id[k] = id;
+            x = g.x;
+            y = g.y;
+            r = (float)__float_as_int(g.w) + 1.f;
+        }
+#pragma unroll
+        for (int w = 0; w < NWR; ++w) {
+            const float x0 = (float)(tx * TILE + (w & 1) * 8) + 0.5f;
+            const float y0 = (float)(ty * TILE + (NWR == 4 ? (w >> 1) * 8 : 0)) + 0.5f;
+            const bool ov = valid && x + r >= x0 && x - r <= x0 + 7.f && y + r >= y0 && y - r <= y0 + RH;
+            const uint32_t m = __ballot_sync(0xffffffffu, ov);
+            if (lane == 0) s.mask[w][u * NWR + warp] = m;
+        }
     }
     __syncthreads();
     // each warp compacts its own quadrant list (order preserved)
@@ -287,52 +300,59 @@ __device__ __forceinline__ float warp_reduce8(const float* v, int lane) {
 // warp's 9 sums are transposed-reduced and 8 (+1) lanes issue one global
 // reduction each (one atomic per warp per Gaussian value); when at most 3
 // lanes contribute they add their own sums directly instead.
-template <bool COUNT>
-__global__ void __launch_bounds__(NT) raster_bwd_kernel(
+template <int NWR, bool COUNT>
+__global__ void __launch_bounds__(32 * NWR) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ sorted_vals, const float4* __restrict__ xydr,
     const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg, int W, int H, int tiles_x,
     const float* __restrict__ final_T, const int* __restrict__ n_contrib, const float* __restrict__ d_img,
     float4* __restrict__ d_rgbo, float4* __restrict__ d_geo, float* __restrict__ d_c11,
     unsigned long long* __restrict__ counts) {
-    __shared__ Batch s;
-    __shared__ int s_max[NW];
+    constexpr int NPR = 4 / NWR;  // pixel pairs per lane
+    __shared__ BatchT<NWR> s;
+    __shared__ int s_max[NWR];
     const int tile = blockIdx.x;
-    const Quad qd(tile, tiles_x);
-    const float px = pin((float)qd.col + 0.5f);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool in0 = qd.col < W && qd.row0 < H, in1 = qd.col < W && qd.row0 + 4 < H;
-    float t0 = 1.f, t1 = 1.f, ga0 = 0.f, ga1 = 0.f, gb0 = 0.f, gb1 = 0.f, gc0 = 0.f, gc1 = 0.f;
-    int nc0 = 0, nc1 = 0;
-    if (in0) {
-        const int q = qd.row0 * W + qd.col;
-        t0 = final_T[q];
-        nc0 = n_contrib[q];
-        ga0 = d_img[3 * q]; gb0 = d_img[3 * q + 1]; gc0 = d_img[3 * q + 2];
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int col = tx * TILE + (warp & 1) * 8 + (lane & 7);
+    const int rbase = ty * TILE + (NWR == 4 ? (warp >> 1) * 8 : 0) + (lane >> 3);
+    const float px = pin((float)col + 0.5f);
+    f32x2 T[NPR], G0[NPR], G1[NPR], G2[NPR], S0[NPR], S1[NPR], S2[NPR], PY[NPR];
+    int nc[2 * NPR];
+    int my_max = 0;
+#pragma unroll
+    for (int j = 0; j < NPR; ++j) {
+        float t[2] = {1.f, 1.f}, ga[2] = {0.f, 0.f}, gb[2] = {0.f, 0.f}, gc[2] = {0.f, 0.f};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int row = rbase + 8 * j + 4 * h;
+            nc[2 * j + h] = 0;
+            if (col < W && row < H) {
+                const int q = row * W + col;
+                t[h] = final_T[q];
+                nc[2 * j + h] = n_contrib[q];
+                ga[h] = d_img[3 * q]; gb[h] = d_img[3 * q + 1]; gc[h] = d_img[3 * q + 2];
+            }
+            my_max = max(my_max, nc[2 * j + h]);
+        }
+        T[j] = pk2(t[0], t[1]);
+        G0[j] = pk2(ga[0], ga[1]); G1[j] = pk2(gb[0], gb[1]); G2[j] = pk2(gc[0], gc[1]);
+        S0[j] = mul2(bc2(bg.x), T[j]); S1[j] = mul2(bc2(bg.y), T[j]); S2[j] = mul2(bc2(bg.z), T[j]);
+        PY[j] = pin2(pk2((float)(rbase + 8 * j) + 0.5f, (float)(rbase + 8 * j) + 4.5f));
     }
-    if (in1) {
-        const int q = (qd.row0 + 4) * W + qd.col;
-        t1 = final_T[q];
-        nc1 = n_contrib[q];
-        ga1 = d_img[3 * q]; gb1 = d_img[3 * q + 1]; gc1 = d_img[3 * q + 2];
-    }
-    f32x2 T = pk2(t0, t1);
-    const f32x2 G0 = pk2(ga0, ga1), G1 = pk2(gb0, gb1), G2 = pk2(gc0, gc1);
-    f32x2 S0 = mul2(bc2(bg.x), T), S1 = mul2(bc2(bg.y), T), S2 = mul2(bc2(bg.z), T);
-    const f32x2 PY = pin2(pk2((float)qd.row0 + 0.5f, (float)qd.row0 + 4.5f));
-    const int warp_max = __reduce_max_sync(0xffffffffu, max(nc0, nc1));
+    const int warp_max = __reduce_max_sync(0xffffffffu, my_max);
     if (lane == 0) s_max[warp] = warp_max;
     const uint2 rg = ranges[tile];
     const int start = (int)rg.x;
     __syncthreads();
     int max_nc = 0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) max_nc = max(max_nc, s_max[w]);
+    for (int w = 0; w < NWR; ++w) max_nc = max(max_nc, s_max[w]);
     unsigned long long e_s = 0, e_c = 0;
 
     for (int bend = max_nc; bend > 0; bend -= RB) {
         const int bstart = max(0, bend - RB);
         __syncthreads();
-        int n = stage_batch(s, tile, tiles_x, sorted_vals, start + bstart, bend - bstart, xydr, conic, colors);
+        int n = stage_batch<NWR>(s, tile, tiles_x, sorted_vals, start + bstart, bend - bstart, xydr, conic, colors);
         const uint8_t* lst = s.list[warp];
         const int kmax = min(bend, warp_max) - bstart;  // positions >= warp_max are inactive for this warp
         while (n > 0 && (int)lst[n - 1] >= kmax) --n;
@@ -343,61 +363,81 @@ __global__ void __launch_bounds__(NT) raster_bwd_kernel(
             const float4 a = s.a[k];
             const float hC = s.b[k].x;
             const float dx = __fsub_rn(px, a.x);
-            const f32x2 DY = sub2(PY, bc2(a.y));
-            const f32x2 SG = splat_sigma2(dx, __fmul_rn(a.z, dx), DY, a.w, hC);
-            const bool v0 = pos < nc0 && lo2(SG) <= SIGMA_CUT, v1 = pos < nc1 && hi2(SG) <= SIGMA_CUT;
-            if (COUNT) e_s += (unsigned)v0 + (unsigned)v1;
-            if (!__any_sync(0xffffffffu, v0 || v1)) continue;
+            const float hAdx = __fmul_rn(a.z, dx);
+            f32x2 DY[NPR], SG[NPR];
+            bool v[2 * NPR];
+            bool any = false;
+#pragma unroll
+            for (int j = 0; j < NPR; ++j) {
+                DY[j] = sub2(PY[j], bc2(a.y));
+                SG[j] = splat_sigma2(dx, hAdx, DY[j], a.w, hC);
+                v[2 * j] = pos < nc[2 * j] && lo2(SG[j]) <= SIGMA_CUT;
+                v[2 * j + 1] = pos < nc[2 * j + 1] && hi2(SG[j]) <= SIGMA_CUT;
+                any = any || v[2 * j] || v[2 * j + 1];
+            }
+            if (COUNT) {
+#pragma unroll
+                for (int q = 0; q < 2 * NPR; ++q) e_s += (unsigned)v[q];
+            }
+            if (!__any_sync(0xffffffffu, any)) continue;
             const float4 bq = s.b[k];
             const float blue = s.c[k];
-            // replay of the forward decisions on the pair
-            const f32x2 SL = mul2(SG, bc2(NEG_LOG2E));
-            const f32x2 E = pk2(ex2_approx(lo2(SL)), ex2_approx(hi2(SL)));
-            const f32x2 ARAW = mul2(bc2(bq.y), E);
-            const float al0 = fminf(lo2(ARAW), ALPHA_MAX), al1 = fminf(hi2(ARAW), ALPHA_MAX);
-            const bool c0 = v0 && al0 >= ALPHA_MIN, c1 = v1 && al1 >= ALPHA_MIN;
-            const uint32_t cmask = __ballot_sync(0xffffffffu, c0 || c1);
-            if (COUNT) e_c += (unsigned)c0 + (unsigned)c1;
-            if (!cmask) continue;
-            const f32x2 AL = pk2(al0, al1);
-            const f32x2 OM = sub2(bc2(1.f), AL);
-            const f32x2 INV = pk2(rcp_approx(lo2(OM)), rcp_approx(hi2(OM)));
-            const f32x2 TH = mul2(T, INV);  // T before this splat (:75)
-            const f32x2 Wt = mul2(AL, TH);
-            const f32x2 WC = pk2(c0 ? lo2(Wt) : 0.f, c1 ? hi2(Wt) : 0.f);
-            const f32x2 CDOT = fma2(bc2(blue), G2, fma2(bc2(bq.w), G1, mul2(bc2(bq.z), G0)));
-            const f32x2 SDOT = fma2(S2, G2, fma2(S1, G1, mul2(S0, G0)));
-            const f32x2 DA = sub2(mul2(TH, CDOT), mul2(INV, SDOT));
-            // live (:91): contributing and not clamped
-            const bool l0 = c0 && lo2(ARAW) < ALPHA_MAX, l1 = c1 && hi2(ARAW) < ALPHA_MAX;
-            const f32x2 DAL = pk2(l0 ? lo2(DA) : 0.f, l1 ? hi2(DA) : 0.f);
-            const f32x2 M = mul2(ARAW, DAL);  // = -d_sigma
-            const f32x2 Y0 = fma2(bc2(a.w), DY, bc2(2.f * a.z * dx));
-            const f32x2 Y1 = fma2(bc2(2.f * hC), DY, bc2(a.w * dx));
-            const f32x2 HY0 = mul2(mul2(bc2(0.5f), M), Y0);
-            const f32x2 D0 = mul2(WC, G0), D1 = mul2(WC, G1), D2 = mul2(WC, G2), D3 = mul2(DAL, E);
-            const f32x2 D4 = mul2(M, Y0), D5 = mul2(M, Y1);
-            const f32x2 D6 = mul2(HY0, Y0), D7 = mul2(HY0, Y1);
-            const f32x2 D8 = mul2(mul2(mul2(bc2(0.5f), M), Y1), Y1);
             float acc[9];
-            acc[0] = lo2(D0) + hi2(D0);
-            acc[1] = lo2(D1) + hi2(D1);
-            acc[2] = lo2(D2) + hi2(D2);
-            acc[3] = lo2(D3) + hi2(D3);
-            acc[4] = lo2(D4) + hi2(D4);
-            acc[5] = lo2(D5) + hi2(D5);
-            acc[6] = lo2(D6) + hi2(D6);
-            acc[7] = lo2(D7) + hi2(D7);
-            acc[8] = lo2(D8) + hi2(D8);
-            S0 = fma2(WC, bc2(bq.z), S0);
-            S1 = fma2(WC, bc2(bq.w), S1);
-            S2 = fma2(WC, bc2(blue), S2);
-            T = sel2(c0, c1, TH, T);
+#pragma unroll
+            for (int t = 0; t < 9; ++t) acc[t] = 0.f;
+            bool anyc = false;
+#pragma unroll
+            for (int j = 0; j < NPR; ++j) {
+                // replay of the forward decisions on the pair
+                const f32x2 SL = mul2(SG[j], bc2(NEG_LOG2E));
+                const f32x2 E = pk2(ex2_approx(lo2(SL)), ex2_approx(hi2(SL)));
+                const f32x2 ARAW = mul2(bc2(bq.y), E);
+                const float al0 = fminf(lo2(ARAW), ALPHA_MAX), al1 = fminf(hi2(ARAW), ALPHA_MAX);
+                const bool c0 = v[2 * j] && al0 >= ALPHA_MIN, c1 = v[2 * j + 1] && al1 >= ALPHA_MIN;
+                if (COUNT) e_c += (unsigned)c0 + (unsigned)c1;
+                if (NPR > 1 && !__any_sync(0xffffffffu, c0 || c1)) continue;
+                anyc = anyc || c0 || c1;
+                const f32x2 AL = pk2(al0, al1);
+                const f32x2 OM = sub2(bc2(1.f), AL);
+                const f32x2 INV = pk2(rcp_approx(lo2(OM)), rcp_approx(hi2(OM)));
+                const f32x2 TH = mul2(T[j], INV);  // T before this splat (:75)
+                const f32x2 Wt = mul2(AL, TH);
+                const f32x2 WC = pk2(c0 ? lo2(Wt) : 0.f, c1 ? hi2(Wt) : 0.f);
+                const f32x2 CDOT = fma2(bc2(blue), G2[j], fma2(bc2(bq.w), G1[j], mul2(bc2(bq.z), G0[j])));
+                const f32x2 SDOT = fma2(S2[j], G2[j], fma2(S1[j], G1[j], mul2(S0[j], G0[j])));
+                const f32x2 DA = sub2(mul2(TH, CDOT), mul2(INV, SDOT));
+                // live (:91): contributing and not clamped
+                const bool l0 = c0 && lo2(ARAW) < ALPHA_MAX, l1 = c1 && hi2(ARAW) < ALPHA_MAX;
+                const f32x2 DAL = pk2(l0 ? lo2(DA) : 0.f, l1 ? hi2(DA) : 0.f);
+                const f32x2 M = mul2(ARAW, DAL);  // = -d_sigma
+                const f32x2 Y0 = fma2(bc2(a.w), DY[j], bc2(2.f * a.z * dx));
+                const f32x2 Y1 = fma2(bc2(2.f * hC), DY[j], bc2(a.w * dx));
+                const f32x2 HM = mul2(bc2(0.5f), M);
+                const f32x2 HY0 = mul2(HM, Y0), HY1 = mul2(HM, Y1);
+                const f32x2 D0 = mul2(WC, G0[j]), D1 = mul2(WC, G1[j]), D2 = mul2(WC, G2[j]);
+                const f32x2 D3 = mul2(DAL, E), D4 = mul2(M, Y0), D5 = mul2(M, Y1);
+                const f32x2 D6 = mul2(HY0, Y0), D7 = mul2(HY0, Y1), D8 = mul2(HY1, Y1);
+                acc[0] += lo2(D0) + hi2(D0);
+                acc[1] += lo2(D1) + hi2(D1);
+                acc[2] += lo2(D2) + hi2(D2);
+                acc[3] += lo2(D3) + hi2(D3);
+                acc[4] += lo2(D4) + hi2(D4);
+                acc[5] += lo2(D5) + hi2(D5);
+                acc[6] += lo2(D6) + hi2(D6);
+                acc[7] += lo2(D7) + hi2(D7);
+                acc[8] += lo2(D8) + hi2(D8);
+                S0[j] = fma2(WC, bc2(bq.z), S0[j]);
+                S1[j] = fma2(WC, bc2(bq.w), S1[j]);
+                S2[j] = fma2(WC, bc2(blue), S2[j]);
+                T[j] = sel2(c0, c1, TH, T[j]);
+            }
+            const uint32_t cmask = __ballot_sync(0xffffffffu, anyc);
+            if (!cmask) continue;
             const uint32_t id = s.id[k];
             if (__popc(cmask) <= 3) {
                 // few contributing lanes: their own vector reductions are
                 // cheaper than a 9-value warp reduction
-                if (c0 || c1) {
+                if (anyc) {
                     red_add_v4(&d_rgbo[id], acc[0], acc[1], acc[2], acc[3]);
                     red_add_v4(&d_geo[id], acc[4], acc[5], acc[6], acc[7]);
                     atomicAdd(&d_c11[id], acc[8]);
@@ -418,7 +458,9 @@ __global__ void __launch_bounds__(NT) raster_bwd_kernel(
         }
     }
     if (COUNT) {
-        unsigned long long e_b = (unsigned long long)nc0 + (unsigned long long)nc1;
+        unsigned long long e_b = 0;
+#pragma unroll
+        for (int q = 0; q < 2 * NPR; ++q) e_b += (unsigned long long)nc[q];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             e_b += __shfl_xor_sync(0xffffffffu, e_b, o);
@@ -431,6 +473,18 @@ __global__ void __launch_bounds__(NT) raster_bwd_kernel(
             atomicAdd(&counts[2], e_c);
         }
     }
+}
+
+// Warp regions of the backward: 2 (8x16 halves) or 4 (8x8 quadrants).  The
+// region geometry never changes a decision (skipped pairs are far outside
+// the 3-sigma square), so it is free to differ from the forward's.
+static int bwd_regions() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GS_BWD_REGIONS");
+        v = (e && atoi(e) == 4) ? 4 : 2;
+    }
+    return v;
 }
 
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
@@ -458,12 +512,15 @@ int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xy
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     const float4* g = (const float4*)xydr4;
     const float4* q = (const float4*)conic4;
-    if (counts)
-        raster_bwd_kernel<true><<<nt, NT, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, fT, nc, dimg,
-                                                 (float4*)d_rgbo4, (float4*)d_geo4, d_c11, counts);
-    else
-        raster_bwd_kernel<false><<<nt, NT, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, fT, nc, dimg,
-                                                  (float4*)d_rgbo4, (float4*)d_geo4, d_c11, counts);
+#define GS_BWD(NWR, CNT)                                                                                 \
+    raster_bwd_kernel<NWR, CNT><<<nt, 32 * NWR, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, fT, nc, \
+                                                        dimg, (float4*)d_rgbo4, (float4*)d_geo4, d_c11, counts)
+    if (bwd_regions() == 4) {
+        if (counts) GS_BWD(4, true); else GS_BWD(4, false);
+    } else {
+        if (counts) GS_BWD(2, true); else GS_BWD(2, false);
+    }
+#undef GS_BWD
     return check_launch("raster_bwd_kernel");
 }
 
