@@ -38,12 +38,12 @@ constexpr int RB = 128;  // splats per staged batch
 // NWR = 2 -> two 8-column x 16-row halves (two pixel pairs per lane).
 template <int NWR>
 struct BatchT {
-    float4 a[RB];  // x, y, hA = A/2, B
-    float4 b[RB];  // hC = C/2, opacity, r, g
-    float c[RB];   // blue
+    float4 a[RB + 1];  // x, y, hA = A/2, B   ([RB] = sentinel: x = +inf, never visible)
+    float4 b[RB + 1];  // hC = C/2, opacity, r, g
+    float c[RB + 1];   // blue
     uint32_t id[RB];
     uint32_t mask[NWR][RB / 32];  // region reach bits per group of 32 entries
-    uint8_t list[NWR][RB];        // compacted entry indices per region
+    __align__(4) uint8_t list[NWR][RB + 2];  // compacted entry indices per region (+ sentinel pad)
 };
 using Batch = BatchT<NW>;
 
@@ -114,6 +114,7 @@ __device__ __forceinline__ int stage_batch(BatchT<NWR>& s, int tile, int tiles_x
         if ((m >> lane) & 1u) s.list[warp][n + __popc(m & lt)] = (uint8_t)(32 * j + lane);
         n += __popc(m);
     }
+    if (lane == 0) s.list[warp][n] = (uint8_t)RB;  // pad odd lists with the sentinel
     __syncwarp();
     return n;
 }
@@ -188,26 +189,30 @@ __global__ void __launch_bounds__(NT) raster_fwd_kernel(const uint2* __restrict_
     const uint2 rg = ranges[tile];
     const int start = (int)rg.x, end = (int)rg.y;
     unsigned long long e_s = 0, e_a = 0, e_c = 0;
+    if (threadIdx.x == 0) {  // sentinel entry: dx = -inf -> sigma NaN -> never visible
+        s.a[RB] = make_float4(INF, 0.f, 0.f, 0.f);
+        s.b[RB] = make_float4(0.f, 0.f, 0.f, 0.f);
+        s.c[RB] = 0.f;
+    }
 
     for (int b0 = start; b0 < end; b0 += RB) {
         if (__syncthreads_count(p.done != 3u) == 0) break;
         const int n = stage_batch(s, tile, tiles_x, sorted_vals, b0, min(RB, end - b0), xydr, conic, colors);
         if (__all_sync(0xffffffffu, p.done == 3u)) continue;  // whole warp finished: only help staging
         const int pos_base = b0 - start + 1;
-        const uint8_t* lst = s.list[warp];
+        const uint16_t* lst2 = reinterpret_cast<const uint16_t*>(s.list[warp]);
 #pragma unroll 1
         for (int i = 0; i < n; i += 2) {
             // two entries per iteration: independent sigma chains, compositing in order
-            const int k0 = lst[i];
-            const bool has1 = i + 1 < n;
-            const int k1 = lst[has1 ? i + 1 : i];
+            const uint32_t kk = lst2[i >> 1];
+            const int k0 = kk & 0xffu, k1 = kk >> 8;  // k1 may be the sentinel
             const float4 a0 = s.a[k0], a1 = s.a[k1];
             const float hC0 = s.b[k0].x, hC1 = s.b[k1].x;
             const float dx0 = __fsub_rn(px, a0.x), dx1 = __fsub_rn(px, a1.x);
             const f32x2 SG0 = splat_sigma2(dx0, __fmul_rn(a0.z, dx0), sub2(p.PY, bc2(a0.y)), a0.w, hC0);
             const f32x2 SG1 = splat_sigma2(dx1, __fmul_rn(a1.z, dx1), sub2(p.PY, bc2(a1.y)), a1.w, hC1);
             const bool v00 = lo2(SG0) <= SIGMA_CUT, v01 = hi2(SG0) <= SIGMA_CUT;  // false when retired
-            bool v10 = has1 && lo2(SG1) <= SIGMA_CUT, v11 = has1 && hi2(SG1) <= SIGMA_CUT;
+            bool v10 = lo2(SG1) <= SIGMA_CUT, v11 = hi2(SG1) <= SIGMA_CUT;
             const uint32_t b0m = __ballot_sync(0xffffffffu, v00 || v01);
             const uint32_t b1m = __ballot_sync(0xffffffffu, v10 || v11);
             if (COUNT) e_s += (unsigned)v00 + (unsigned)v01;
@@ -482,7 +487,7 @@ static int bwd_regions() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("GS_BWD_REGIONS");
-        v = (e && atoi(e) == 4) ? 4 : 2;
+        v = (e && atoi(e) == 2) ? 2 : 4;
     }
     return v;
 }
