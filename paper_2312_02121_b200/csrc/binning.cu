@@ -183,28 +183,59 @@ __global__ void __launch_bounds__(256) emit_sorted_kernel(const uint32_t* __rest
     for (int k = threadIdx.x; k < 2 * 256; k += blockDim.x) sh[k] = 0;
     __syncthreads();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
     int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
     uint32_t g = 0, off = 0;
     if (p < n) {
         g = order[p];
+        off = offsets[p];
         const float4 gx = xydr[g];
         const int r = __float_as_int(gx.w);
-        if (r > 0) {
-            tile_rect(gx.x, gx.y, r, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
-            off = offsets[p];
-        }
+        if (r > 0) tile_rect(gx.x, gx.y, r, tiles_x, tiles_y, tx0, tx1, ty0, ty1);
     }
-    // warp-cooperative histogram update per emitted row of tiles
-    for (int ty = ty0; ty <= ty1; ++ty) {
-        for (int tx = tx0; tx <= tx1; ++tx) {
-            const uint32_t t = (uint32_t)(ty * tiles_x + tx);
-            if ((int64_t)off < capacity) {
-                tile_keys[off] = t;
-                vals[off] = g;
-                atomicAdd(&sh[t & 255u], 1u);
-                if (tile_passes > 1) atomicAdd(&sh[256 + ((t >> 8) & 255u)], 1u);
-            }
-            ++off;
+    // The warp's 32 Gaussians own the contiguous output range
+    // [off(lane 0), off(lane 0) + total): the warp walks it 32 entries at a
+    // time (coalesced stores); each entry finds its owner lane by a binary
+    // search over the lanes' exclusive prefix and decodes its tile row-major.
+    const int w = tx1 - tx0 + 1;
+    const uint32_t cnt = (uint32_t)(w * (ty1 - ty0 + 1));
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t base = __shfl_sync(0xffffffffu, off, 0);
+    const float rw = w > 0 ? 1.f / (float)w : 0.f;
+    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        int L = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t e = __shfl_sync(0xffffffffu, excl, L + step);
+            if (e <= t) L += step;
+        }
+        const uint32_t j = t - __shfl_sync(0xffffffffu, excl, L);
+        const int ow = __shfl_sync(0xffffffffu, w, L);
+        const float orw = __shfl_sync(0xffffffffu, rw, L);
+        const int otx0 = __shfl_sync(0xffffffffu, tx0, L), oty0 = __shfl_sync(0xffffffffu, ty0, L);
+        const uint32_t og = __shfl_sync(0xffffffffu, g, L);
+        int row = (int)((float)j * orw);
+        if (row * ow > (int)j) --row;
+        if ((row + 1) * ow <= (int)j) ++row;
+        const uint32_t tile = (uint32_t)((oty0 + row) * tiles_x + otx0 + ((int)j - row * ow));
+        const bool valid = t < total && (int64_t)(base + t) < capacity;
+        if (valid) {
+            tile_keys[base + t] = tile;
+            vals[base + t] = og;
+            atomicAdd(&sh[tile & 255u], 1u);
+        }
+        if (tile_passes > 1) {  // high digit: few distinct values per warp -> aggregate
+            const uint32_t d = valid ? (tile >> 8) & 255u : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            if (valid && lane == __ffs(peers) - 1) atomicAdd(&sh[256 + d], (uint32_t)__popc(peers));
         }
     }
     __syncthreads();
@@ -217,12 +248,29 @@ __global__ void __launch_bounds__(256) emit_sorted_kernel(const uint32_t* __rest
 __global__ void __launch_bounds__(256) ranges_u32_kernel(const uint32_t* __restrict__ keys, int64_t n_cap,
                                                          const unsigned long long* __restrict__ n_dev,
                                                          uint2* __restrict__ ranges) {
+    // 4 sorted keys per thread (one 16-byte load when aligned and in range)
     const int64_t n = n_dev ? min((int64_t)*n_dev, n_cap) : n_cap;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t t = keys[i];
-    if (i == 0 || keys[i - 1] != t) ranges[t].x = (uint32_t)i;
-    if (i == n - 1 || keys[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+    const int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (i0 >= n) return;
+    uint32_t k[4];
+    if (i0 + 4 <= n) {
+        const uint4 v = *reinterpret_cast<const uint4*>(keys + i0);
+        k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) k[j] = i0 + j < n ? keys[i0 + j] : 0xFFFFFFFFu;
+    }
+    uint32_t prev = i0 > 0 ? keys[i0 - 1] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t i = i0 + j;
+        if (i >= n) break;
+        const uint32_t t = k[j];
+        if (i == 0 || prev != t) ranges[t].x = (uint32_t)i;
+        const uint32_t next = j < 3 ? (i + 1 < n ? k[j + 1] : 0xFFFFFFFFu) : (i + 1 < n ? keys[i + 1] : 0xFFFFFFFFu);
+        if (i == n - 1 || next != t) ranges[t].y = (uint32_t)(i + 1);
+        prev = t;
+    }
 }
 
 size_t scan_ws_bytes(int64_t n) {
@@ -252,7 +300,7 @@ int launch_emit_sorted(const uint32_t* order, const float* xydr4, const uint32_t
 int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const unsigned long long* n_dev,
                       uint2* ranges, cudaStream_t s) {
     if (n_cap == 0) return 0;
-    ranges_u32_kernel<<<(unsigned)((n_cap + 255) / 256), 256, 0, s>>>(sorted_tile_keys, n_cap, n_dev, ranges);
+    ranges_u32_kernel<<<(unsigned)((n_cap + 1023) / 1024), 256, 0, s>>>(sorted_tile_keys, n_cap, n_dev, ranges);
     return check_launch("ranges_u32_kernel");
 }
 

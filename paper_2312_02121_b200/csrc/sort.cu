@@ -102,7 +102,7 @@ __device__ __forceinline__ uint32_t block_incl_scan256(uint32_t v, uint32_t* s_t
 
 // One 8-bit pass.  vin == nullptr means value = input index (identity).
 template <typename K, int ITEMS>
-__global__ void __launch_bounds__(SORT_THREADS, 2) onesweep_kernel(
+__global__ void __launch_bounds__(SORT_THREADS, sizeof(K) == 4 ? 3 : 2) onesweep_kernel(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_cap, const unsigned long long* __restrict__ n_dev, int shift,
     const uint32_t* __restrict__ hist, uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
