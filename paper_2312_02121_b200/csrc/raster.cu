@@ -163,29 +163,47 @@ __device__ __forceinline__ void fwd_commit(FwdPair& p, f32x2 SG, bool vis0, bool
 }
 
 // sg/raster_forward.py:116-154 _composite_tile for one tile.
-template <bool ET, bool COUNT>
-__global__ void __launch_bounds__(NT) raster_fwd_kernel(const uint2* __restrict__ ranges,
-                                                        const uint32_t* __restrict__ sorted_vals,
-                                                        const float4* __restrict__ xydr,
-                                                        const float4* __restrict__ conic,
-                                                        const float* __restrict__ colors, float3 bg, int W, int H,
-                                                        int tiles_x, float* __restrict__ out_img,
-                                                        float* __restrict__ out_T, int* __restrict__ out_nc,
-                                                        unsigned long long* __restrict__ counts) {
-    __shared__ Batch s;
+// NWR = 4: 128 threads, one pixel pair per lane, two list entries per
+// iteration (independent sigma chains); NWR = 2: 64 threads, two pixel pairs
+// per lane (8x16 halves), one entry per iteration.
+template <int NWR, bool ET, bool COUNT>
+__global__ void __launch_bounds__(32 * NWR) raster_fwd_kernel(const uint2* __restrict__ ranges,
+                                                              const uint32_t* __restrict__ sorted_vals,
+                                                              const float4* __restrict__ xydr,
+                                                              const float4* __restrict__ conic,
+                                                              const float* __restrict__ colors, float3 bg, int W,
+                                                              int H, int tiles_x, float* __restrict__ out_img,
+                                                              float* __restrict__ out_T, int* __restrict__ out_nc,
+                                                              unsigned long long* __restrict__ counts) {
+    constexpr int NPR = 4 / NWR;
+    __shared__ BatchT<NWR> s;
     const int tile = blockIdx.x;
-    const int warp = threadIdx.x >> 5;
-    const Quad qd(tile, tiles_x);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int col = tx * TILE + (warp & 1) * 8 + (lane & 7);
+    const int rbase = ty * TILE + (NWR == 4 ? (warp >> 1) * 8 : 0) + (lane >> 3);
     const float INF = __int_as_float(0x7f800000);
-    const bool in0 = qd.col < W && qd.row0 < H, in1 = qd.col < W && qd.row0 + 4 < H;
-    const float px = pin((float)qd.col + 0.5f);
-    FwdPair p;
-    p.T = bc2(1.f);
-    p.CR = p.CG = p.CB = bc2(0.f);
-    p.PY = pk2(in0 ? (float)qd.row0 + 0.5f : INF, in1 ? (float)qd.row0 + 4.5f : INF);
-    p.nc0 = p.nc1 = 0;
-    p.stop0 = p.stop1 = -1;
-    p.done = (in0 ? 0u : 1u) | (in1 ? 0u : 2u);
+    const float px = pin((float)col + 0.5f);
+    FwdPair p[NPR];
+    bool inb[2 * NPR];
+#pragma unroll
+    for (int j = 0; j < NPR; ++j) {
+        const int r0 = rbase + 8 * j;
+        inb[2 * j] = col < W && r0 < H;
+        inb[2 * j + 1] = col < W && r0 + 4 < H;
+        p[j].T = bc2(1.f);
+        p[j].CR = p[j].CG = p[j].CB = bc2(0.f);
+        p[j].PY = pk2(inb[2 * j] ? (float)r0 + 0.5f : INF, inb[2 * j + 1] ? (float)r0 + 4.5f : INF);
+        p[j].nc0 = p[j].nc1 = 0;
+        p[j].stop0 = p[j].stop1 = -1;
+        p[j].done = (inb[2 * j] ? 0u : 1u) | (inb[2 * j + 1] ? 0u : 2u);
+    }
+    auto all_done = [&]() {
+        bool d = true;
+#pragma unroll
+        for (int j = 0; j < NPR; ++j) d = d && p[j].done == 3u;
+        return d;
+    };
     const uint2 rg = ranges[tile];
     const int start = (int)rg.x, end = (int)rg.y;
     unsigned long long e_s = 0, e_a = 0, e_c = 0;
@@ -196,61 +214,101 @@ __global__ void __launch_bounds__(NT) raster_fwd_kernel(const uint2* __restrict_
     }
 
     for (int b0 = start; b0 < end; b0 += RB) {
-        if (__syncthreads_count(p.done != 3u) == 0) break;
-        const int n = stage_batch(s, tile, tiles_x, sorted_vals, b0, min(RB, end - b0), xydr, conic, colors);
-        if (__all_sync(0xffffffffu, p.done == 3u)) continue;  // whole warp finished: only help staging
+        if (__syncthreads_count(!all_done()) == 0) break;
+        const int n = stage_batch<NWR>(s, tile, tiles_x, sorted_vals, b0, min(RB, end - b0), xydr, conic, colors);
+        if (__all_sync(0xffffffffu, all_done())) continue;  // whole warp finished: only help staging
         const int pos_base = b0 - start + 1;
-        const uint16_t* lst2 = reinterpret_cast<const uint16_t*>(s.list[warp]);
+        if constexpr (NPR == 1) {
+            const uint16_t* lst2 = reinterpret_cast<const uint16_t*>(s.list[warp]);
 #pragma unroll 1
-        for (int i = 0; i < n; i += 2) {
-            // two entries per iteration: independent sigma chains, compositing in order
-            const uint32_t kk = lst2[i >> 1];
-            const int k0 = kk & 0xffu, k1 = kk >> 8;  // k1 may be the sentinel
-            const float4 a0 = s.a[k0], a1 = s.a[k1];
-            const float hC0 = s.b[k0].x, hC1 = s.b[k1].x;
-            const float dx0 = __fsub_rn(px, a0.x), dx1 = __fsub_rn(px, a1.x);
-            const f32x2 SG0 = splat_sigma2(dx0, __fmul_rn(a0.z, dx0), sub2(p.PY, bc2(a0.y)), a0.w, hC0);
-            const f32x2 SG1 = splat_sigma2(dx1, __fmul_rn(a1.z, dx1), sub2(p.PY, bc2(a1.y)), a1.w, hC1);
-            const bool v00 = lo2(SG0) <= SIGMA_CUT, v01 = hi2(SG0) <= SIGMA_CUT;  // false when retired
-            bool v10 = lo2(SG1) <= SIGMA_CUT, v11 = hi2(SG1) <= SIGMA_CUT;
-            const uint32_t b0m = __ballot_sync(0xffffffffu, v00 || v01);
-            const uint32_t b1m = __ballot_sync(0xffffffffu, v10 || v11);
-            if (COUNT) e_s += (unsigned)v00 + (unsigned)v01;
-            if (b0m) fwd_commit<ET, COUNT>(p, SG0, v00, v01, s.b[k0], s.c[k0], pos_base + k0, e_a, e_c);
-            v10 = v10 && !(p.done & 1u);  // retired at k0
-            v11 = v11 && !(p.done & 2u);
-            if (COUNT) e_s += (unsigned)v10 + (unsigned)v11;
-            if (b1m) fwd_commit<ET, COUNT>(p, SG1, v10, v11, s.b[k1], s.c[k1], pos_base + k1, e_a, e_c);
-            if (ET && (b0m | b1m) && __all_sync(0xffffffffu, p.done == 3u)) break;
+            for (int i = 0; i < n; i += 2) {
+                const uint32_t kk = lst2[i >> 1];
+                const int k0 = kk & 0xffu, k1 = kk >> 8;  // k1 may be the sentinel
+                const float4 a0 = s.a[k0], a1 = s.a[k1];
+                const float hC0 = s.b[k0].x, hC1 = s.b[k1].x;
+                const float dx0 = __fsub_rn(px, a0.x), dx1 = __fsub_rn(px, a1.x);
+                const f32x2 SG0 = splat_sigma2(dx0, __fmul_rn(a0.z, dx0), sub2(p[0].PY, bc2(a0.y)), a0.w, hC0);
+                const f32x2 SG1 = splat_sigma2(dx1, __fmul_rn(a1.z, dx1), sub2(p[0].PY, bc2(a1.y)), a1.w, hC1);
+                const bool v00 = lo2(SG0) <= SIGMA_CUT, v01 = hi2(SG0) <= SIGMA_CUT;  // false when retired
+                bool v10 = lo2(SG1) <= SIGMA_CUT, v11 = hi2(SG1) <= SIGMA_CUT;
+                const uint32_t b0m = __ballot_sync(0xffffffffu, v00 || v01);
+                const uint32_t b1m = __ballot_sync(0xffffffffu, v10 || v11);
+                if (COUNT) e_s += (unsigned)v00 + (unsigned)v01;
+                if (b0m) fwd_commit<ET, COUNT>(p[0], SG0, v00, v01, s.b[k0], s.c[k0], pos_base + k0, e_a, e_c);
+                v10 = v10 && !(p[0].done & 1u);  // retired at k0
+                v11 = v11 && !(p[0].done & 2u);
+                if (COUNT) e_s += (unsigned)v10 + (unsigned)v11;
+                if (b1m) fwd_commit<ET, COUNT>(p[0], SG1, v10, v11, s.b[k1], s.c[k1], pos_base + k1, e_a, e_c);
+                if (ET && (b0m | b1m) && __all_sync(0xffffffffu, p[0].done == 3u)) break;
+            }
+        } else {
+            const uint8_t* lst = s.list[warp];
+#pragma unroll 1
+            for (int i = 0; i < n; ++i) {
+                const int k = lst[i];
+                const float4 a = s.a[k];
+                const float hC = s.b[k].x;
+                const float dx = __fsub_rn(px, a.x);
+                const float hAdx = __fmul_rn(a.z, dx);
+                f32x2 SG[NPR];
+                bool v[2 * NPR];
+                bool any = false;
+#pragma unroll
+                for (int j = 0; j < NPR; ++j) {
+                    SG[j] = splat_sigma2(dx, hAdx, sub2(p[j].PY, bc2(a.y)), a.w, hC);
+                    v[2 * j] = lo2(SG[j]) <= SIGMA_CUT;
+                    v[2 * j + 1] = hi2(SG[j]) <= SIGMA_CUT;
+                    any = any || v[2 * j] || v[2 * j + 1];
+                }
+                if (COUNT) {
+#pragma unroll
+                    for (int q = 0; q < 2 * NPR; ++q) e_s += (unsigned)v[q];
+                }
+                if (!__any_sync(0xffffffffu, any)) continue;
+                const float4 bq = s.b[k];
+                const float blue = s.c[k];
+#pragma unroll
+                for (int j = 0; j < NPR; ++j)
+                    if (__any_sync(0xffffffffu, v[2 * j] || v[2 * j + 1]))
+                        fwd_commit<ET, COUNT>(p[j], SG[j], v[2 * j], v[2 * j + 1], bq, blue, pos_base + k, e_a, e_c);
+                if (ET && __all_sync(0xffffffffu, all_done())) break;
+            }
         }
     }
-    float T0, T1, r0, r1, g0, g1, bb0, bb1;
-    upk2(p.T, T0, T1);
-    upk2(p.CR, r0, r1);
-    upk2(p.CG, g0, g1);
-    upk2(p.CB, bb0, bb1);
-    if (in0) {
-        const int q = qd.row0 * W + qd.col;
-        out_img[3 * q] = __fmaf_rn(bg.x, T0, r0);
-        out_img[3 * q + 1] = __fmaf_rn(bg.y, T0, g0);
-        out_img[3 * q + 2] = __fmaf_rn(bg.z, T0, bb0);
-        out_T[q] = T0;
-        out_nc[q] = p.nc0;
-    }
-    if (in1) {
-        const int q = (qd.row0 + 4) * W + qd.col;
-        out_img[3 * q] = __fmaf_rn(bg.x, T1, r1);
-        out_img[3 * q + 1] = __fmaf_rn(bg.y, T1, g1);
-        out_img[3 * q + 2] = __fmaf_rn(bg.z, T1, bb1);
-        out_T[q] = T1;
-        out_nc[q] = p.nc1;
+#pragma unroll
+    for (int j = 0; j < NPR; ++j) {
+        float T0, T1, r0, r1, g0, g1, bb0, bb1;
+        upk2(p[j].T, T0, T1);
+        upk2(p[j].CR, r0, r1);
+        upk2(p[j].CG, g0, g1);
+        upk2(p[j].CB, bb0, bb1);
+        const int row0 = rbase + 8 * j;
+        if (inb[2 * j]) {
+            const int q = row0 * W + col;
+            out_img[3 * q] = __fmaf_rn(bg.x, T0, r0);
+            out_img[3 * q + 1] = __fmaf_rn(bg.y, T0, g0);
+            out_img[3 * q + 2] = __fmaf_rn(bg.z, T0, bb0);
+            out_T[q] = T0;
+            out_nc[q] = p[j].nc0;
+        }
+        if (inb[2 * j + 1]) {
+            const int q = (row0 + 4) * W + col;
+            out_img[3 * q] = __fmaf_rn(bg.x, T1, r1);
+            out_img[3 * q + 1] = __fmaf_rn(bg.y, T1, g1);
+            out_img[3 * q + 2] = __fmaf_rn(bg.z, T1, bb1);
+            out_T[q] = T1;
+            out_nc[q] = p[j].nc1;
+        }
     }
     if (COUNT) {
         // E_f: (pixel, entry) pairs the reference visits while not done =
         // entries up to and including the stopping one, else the whole list
         unsigned long long e_f = 0;
-        if (in0) e_f += (unsigned long long)(p.stop0 >= 0 ? p.stop0 : end - start);
-        if (in1) e_f += (unsigned long long)(p.stop1 >= 0 ? p.stop1 : end - start);
+#pragma unroll
+        for (int j = 0; j < NPR; ++j) {
+            if (inb[2 * j]) e_f += (unsigned long long)(p[j].stop0 >= 0 ? p[j].stop0 : end - start);
+            if (inb[2 * j + 1]) e_f += (unsigned long long)(p[j].stop1 >= 0 ? p[j].stop1 : end - start);
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             e_f += __shfl_xor_sync(0xffffffffu, e_f, o);
@@ -258,7 +316,7 @@ __global__ void __launch_bounds__(NT) raster_fwd_kernel(const uint2* __restrict_
             e_a += __shfl_xor_sync(0xffffffffu, e_a, o);
             e_c += __shfl_xor_sync(0xffffffffu, e_c, o);
         }
-        if ((threadIdx.x & 31) == 0) {
+        if (lane == 0) {
             atomicAdd(&counts[0], e_f);
             atomicAdd(&counts[1], e_s);
             atomicAdd(&counts[2], e_a);
@@ -492,6 +550,15 @@ static int bwd_regions() {
     return v;
 }
 
+static int fwd_regions() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GS_FWD_REGIONS");
+        v = (e && atoi(e) == 2) ? 2 : 4;
+    }
+    return v;
+}
+
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
                       unsigned long long* counts, cudaStream_t s) {
@@ -499,13 +566,18 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     const float4* g = (const float4*)xydr4;
     const float4* q = (const float4*)conic4;
-    if (et) {
-        if (counts) raster_fwd_kernel<true, true><<<nt, NT, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, img, T, nc, counts);
-        else raster_fwd_kernel<true, false><<<nt, NT, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, img, T, nc, counts);
+#define GS_FWD(NWR, ET, CNT)                                                                                  \
+    raster_fwd_kernel<NWR, ET, CNT><<<nt, 32 * NWR, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, img, \
+                                                            T, nc, counts)
+    const bool cnt = counts != nullptr;
+    if (fwd_regions() == 2) {
+        if (et) { if (cnt) GS_FWD(2, true, true); else GS_FWD(2, true, false); }
+        else { if (cnt) GS_FWD(2, false, true); else GS_FWD(2, false, false); }
     } else {
-        if (counts) raster_fwd_kernel<false, true><<<nt, NT, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, img, T, nc, counts);
-        else raster_fwd_kernel<false, false><<<nt, NT, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, img, T, nc, counts);
+        if (et) { if (cnt) GS_FWD(4, true, true); else GS_FWD(4, true, false); }
+        else { if (cnt) GS_FWD(4, false, true); else GS_FWD(4, false, false); }
     }
+#undef GS_FWD
     return check_launch("raster_fwd_kernel");
 }
 
