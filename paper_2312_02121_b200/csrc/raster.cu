@@ -167,7 +167,7 @@ __device__ __forceinline__ void fwd_commit(FwdPair& p, f32x2 SG, bool vis0, bool
 // iteration (independent sigma chains); NWR = 2: 64 threads, two pixel pairs
 // per lane (8x16 halves), one entry per iteration.
 template <int NWR, bool ET, bool COUNT>
-__global__ void __launch_bounds__(32 * NWR) raster_fwd_kernel(const uint2* __restrict__ ranges,
+__global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 10 : 16) raster_fwd_kernel(const uint2* __restrict__ ranges,
                                                               const uint32_t* __restrict__ sorted_vals,
                                                               const float4* __restrict__ xydr,
                                                               const float4* __restrict__ conic,
