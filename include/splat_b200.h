@@ -198,6 +198,24 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
                       float* d_quats4, float* d_rgbo4, float* d_view16, unsigned long long* counts3,
                       void* const* stage_events, gs_stream_t stream);
 
+/* ---- Training step around the path (sg/optimize.py:96-190 fit) ----------
+ * gs_activate : scales = exp(log_scales), opacities = sigmoid(logits)  (:144-145)
+ * gs_loss_l2  : d_image = 2 (image - target); *loss += sum (image - target)^2
+ *               (fp64 accumulation; :157-158,163)
+ * gs_adam_step: chain rule to log/logit space (:167,172), Adam per class
+ *               (:84-89) with lrs5 = {mean, scale, quat, opacity, color},
+ *               colour clip (:176), and the activated scales/opacities for
+ *               the next render.  adam_m14/adam_v14: (n,14) moments, column
+ *               order mean 3 | log_scale 3 | quat 4 | logit 1 | color 3.    */
+int gs_activate(const float* log_scales3, const float* logits, float* scales3, float* opacities, int64_t n,
+                gs_stream_t stream);
+int gs_loss_l2(const float* image, const float* target, int64_t n, float* d_image, double* loss,
+               gs_stream_t stream);
+int gs_adam_step(float* means3, float* log_scales3, float* quats4, float* logits, float* colors3, float* scales3,
+                 float* opacities, const float* d_means3, const float* d_scales3, const float* d_quats4,
+                 const float* d_rgbo4, float* adam_m14, float* adam_v14, int64_t n, int step,
+                 const float* lrs5 /*[host]*/, float beta1, float beta2, float eps, gs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,6 +20,7 @@ EXPORTS = (
     "gs_raster_fwd", "gs_raster_bwd",
     "gs_project_bwd_workspace_bytes", "gs_project_bwd",
     "gs_frame_workspace_bytes", "gs_frame_view_of", "gs_frame_forward", "gs_frame_backward",
+    "gs_activate", "gs_loss_l2", "gs_adam_step",
 )
 
 ERR_MESSAGES = {  # include/splat_b200.h gs_error_code -> the reference's ValueError text
@@ -84,6 +85,13 @@ def load():
         "gs_frame_backward": ([P, P, P, P, i64, cam, C.POINTER(C.c_float), i64, P, sz, P, P, P, P, P, P, P, P, P,
                                P, P], C.c_int),
     }
+    f32 = C.c_float
+    sig.update({
+        "gs_activate": ([P, P, P, P, i64, P], C.c_int),
+        "gs_loss_l2": ([P, P, i64, P, P, P], C.c_int),
+        "gs_adam_step": ([P, P, P, P, P, P, P, P, P, P, P, P, P, i64, C.c_int, C.POINTER(f32), f32, f32, f32, P],
+                         C.c_int),
+    })
     for name, (args, res) in sig.items():
         f = getattr(L, name)
         f.argtypes = args
