@@ -216,6 +216,44 @@ int gs_adam_step(float* means3, float* log_scales3, float* quats4, float* logits
                  const float* d_rgbo4, float* adam_m14, float* adam_v14, int64_t n, int step,
                  const float* lrs5 /*[host]*/, float beta1, float beta2, float eps, gs_stream_t stream);
 
+/* ---- Per-pixel API -------------------------------
+ * Splat arrays are the projection's layout: xydr4 (m,4) (x, y, depth,
+ * radius bits; only x, y are read), conic4 (m,4) (A, B, C, opacity),
+ * colors3 (m,3).  A query is a pixel centre pix2[q] and, for compositing,
+ * its own depth-ordered bin bin_idx[bin_ptr[q] .. bin_ptr[q+1]) of splat
+ * indices.  The arithmetic is the tile rasterizers' (bit-identical image /
+ * final_T / n_contrib for a rendered pixel's centre and tile bin).
+ *
+ * gs_conic_from_cov      replaces sg/raster_forward.py:86-92
+ *                        _cov2d_inverse_terms: cov3 (m,3) = (a, b, c) of
+ *                        the 2d covariance; det <= 0 reports GS_ERR_COV2D
+ *                        for the first such row into *status (atomicMin of
+ *                        index<<8 | code; initialise to all ones).
+ * gs_eval_alpha          replaces sg/raster_forward.py:175-196 eval_alpha
+ *                        for n (splat[q], pix2[q]) pairs.
+ * gs_composite_pixels    replaces sg/raster_forward.py:199-219
+ *                        composite_pixel for n queries.
+ * gs_composite_pixels_bwd replaces sg/raster_backward.py:111-135
+ *                        composite_pixel_backward (gradients accumulate into
+ *                        zeroed d_rgbo4 / d_geo4 / d_c11 rows per splat, the
+ *                        gs_raster_bwd layout) and, with t_log != NULL
+ *                        (sized like bin_idx), :138-163 transmittance_replay:
+ *                        the replayed T before every contributing entry, NaN
+ *                        at the others.                                      */
+int gs_conic_from_cov(const float* cov3, const float* opacities, int64_t n, float* out_conic4,
+                      unsigned long long* status, gs_stream_t stream);
+int gs_eval_alpha(const float* xydr4, const float* conic4, const int32_t* splat, const float* pix2, int64_t n,
+                  float* out_alpha, float* out_delta2, float* out_sigma, gs_stream_t stream);
+int gs_composite_pixels(const float* xydr4, const float* conic4, const float* colors3, const int64_t* bin_ptr,
+                        const int32_t* bin_idx, const float* pix2, int64_t n, const float* background3 /*[host]*/,
+                        int early_termination, float* out_color3, float* out_final_T, int32_t* out_n_contrib,
+                        gs_stream_t stream);
+int gs_composite_pixels_bwd(const float* xydr4, const float* conic4, const float* colors3, const int64_t* bin_ptr,
+                            const int32_t* bin_idx, const float* pix2, int64_t n,
+                            const float* background3 /*[host]*/, const float* final_T, const int32_t* n_contrib,
+                            const float* d_pixels3, float* d_rgbo4, float* d_geo4, float* d_c11, float* t_log,
+                            gs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,6 +70,12 @@ def lib():
         L.orc_raster_bwd.restype = None
         L.orc_project_bwd.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, P, P, C.c_int]
         L.orc_project_bwd.restype = C.c_int
+        L.orc_eval_alpha.argtypes = [i64, P, P, P, P, P, P]
+        L.orc_eval_alpha.restype = None
+        L.orc_composite_pixels.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, P, P, P, P]
+        L.orc_composite_pixels.restype = None
+        L.orc_composite_pixels_bwd.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, P, P, P]
+        L.orc_composite_pixels_bwd.restype = None
         L.orc_max_threads.argtypes = []
         L.orc_max_threads.restype = C.c_int
         _lib = L
@@ -242,3 +248,48 @@ def scene_backward(means, scales, quats, opacities, colors, cam: Camera, backgro
     return dict(d_mean=pb["d_mean"], d_scale=pb["d_scale"], d_quat=pb["d_quat"],
                 d_opacity=rb["d_opacity"], d_color=rb["d_color"], d_view=pb["d_view"],
                 d_mean2d=rb["d_mean2d"], d_cov2d=rb["d_cov2d"], counts=rb["counts"])
+
+
+# ------------------------------------------------------------------ per-pixel API
+
+def eval_alpha(splat, pix, mean2d, cov2d, opac) -> np.ndarray:
+    """sg/raster_forward.py:175-196 for q pairs -> (q,4) alpha, dx, dy, sigma."""
+    splat = np.ascontiguousarray(splat, np.int64)
+    pix, mean2d, cov2d, opac = _d(pix, (-1, 2)), _d(mean2d, (-1, 2)), _d(cov2d, (-1, 3)), _d(opac)
+    out = np.zeros((len(splat), 4))
+    lib().orc_eval_alpha(len(splat), _p(splat), _p(pix), _p(mean2d), _p(cov2d), _p(opac), _p(out))
+    return out
+
+
+def composite_pixels(bin_ptr, bin_idx, pix, et, mean2d, cov2d, opac, colors, bg) -> dict:
+    """sg/raster_forward.py:199-219 for q queries (own bin + et flag each)."""
+    bin_ptr = np.ascontiguousarray(bin_ptr, np.int64)
+    bin_idx = np.ascontiguousarray(bin_idx, np.int64)
+    q = len(bin_ptr) - 1
+    et = np.ascontiguousarray(np.broadcast_to(np.asarray(et, np.int8), (q,)))
+    pix, mean2d, cov2d = _d(pix, (-1, 2)), _d(mean2d, (-1, 2)), _d(cov2d, (-1, 3))
+    opac, colors, bg = _d(opac), _d(colors, (-1, 3)), _d(bg)
+    out = dict(color=np.zeros((q, 3)), final_T=np.zeros(q), n_contrib=np.zeros(q, np.int64), margin=np.zeros(q),
+               margin_kind=np.zeros(q, np.int8))
+    lib().orc_composite_pixels(q, _p(bin_ptr), _p(bin_idx), _p(pix), _p(et), _p(mean2d), _p(cov2d), _p(opac),
+                               _p(colors), _p(bg), _p(out["color"]), _p(out["final_T"]), _p(out["n_contrib"]),
+                               _p(out["margin"]), _p(out["margin_kind"]))
+    return out
+
+
+def composite_pixels_bwd(bin_ptr, bin_idx, pix, mean2d, cov2d, opac, colors, bg, final_T, n_contrib, d_pix,
+                         t_log=False) -> dict:
+    """sg/raster_backward.py:111-163 for q queries -> per-splat d9 rows
+    (d_color 3, d_opacity, d_mean2d 2, d_cov 00, 01, 11) and the replay log."""
+    bin_ptr = np.ascontiguousarray(bin_ptr, np.int64)
+    bin_idx = np.ascontiguousarray(bin_idx, np.int64)
+    q = len(bin_ptr) - 1
+    pix, mean2d, cov2d = _d(pix, (-1, 2)), _d(mean2d, (-1, 2)), _d(cov2d, (-1, 3))
+    opac, colors, bg, final_T, d_pix = _d(opac), _d(colors, (-1, 3)), _d(bg), _d(final_T), _d(d_pix, (-1, 3))
+    n_contrib = np.ascontiguousarray(n_contrib, np.int64)
+    d9 = np.zeros((mean2d.shape[0], 9))
+    log = np.zeros(len(bin_idx)) if t_log else None
+    lib().orc_composite_pixels_bwd(q, _p(bin_ptr), _p(bin_idx), _p(pix), _p(mean2d), _p(cov2d), _p(opac),
+                                   _p(colors), _p(bg), _p(final_T), _p(n_contrib), _p(d_pix), _p(d9),
+                                   _p(log) if t_log else C.c_void_p(0))
+    return dict(d9=d9, t_log=log)

@@ -473,6 +473,130 @@ void orc_raster_bwd(int64_t width, int64_t height, const int64_t* bin_ptr, const
     if (counts) { counts[0] = c_b; counts[1] = c_s; counts[2] = c_c; }
 }
 
+/*
+ * Per-pixel API.  Splat arrays are indexed by the
+ * query bins' own indices (the reference's `projected` list order);
+ * opac/colors are per splat (the scene rows already gathered).
+ *
+ * sg/raster_forward.py:86-92,175-196 eval_alpha for n (splat, pixel) pairs:
+ * out4[q] = (alpha, dx, dy, sigma), alpha 0 when skipped.
+ */
+void orc_eval_alpha(int64_t n, const int64_t* splat, const double* pix, const double* mean2d, const double* cov2d,
+                    const double* opac, double* out4) {
+    for (int64_t q = 0; q < n; ++q) {
+        int64_t j = splat[q];
+        double A, B, C;
+        conic_of(cov2d + 3 * j, &A, &B, &C);
+        double dx = pix[2 * q] - mean2d[2 * j], dy = pix[2 * q + 1] - mean2d[2 * j + 1];
+        double sigma = 0.5 * (A * dx * dx + C * dy * dy) + B * dx * dy;
+        double alpha = opac[j] * exp(-sigma);
+        if (alpha > ORC_ALPHA_MAX) alpha = ORC_ALPHA_MAX;
+        if (sigma > ORC_SIGMA_CUT || alpha < ORC_ALPHA_MIN) alpha = 0.0;
+        out4[4 * q] = alpha; out4[4 * q + 1] = dx; out4[4 * q + 2] = dy; out4[4 * q + 3] = sigma;
+    }
+}
+
+/*
+ * sg/raster_forward.py:199-219 composite_pixel (the :116-154 loop for one
+ * pixel) for n queries, each with its own bin and early-termination flag.
+ * margin/margin_kind as orc_raster_fwd (optional).
+ */
+void orc_composite_pixels(int64_t n, const int64_t* bin_ptr, const int64_t* bin_idx, const double* pix,
+                          const int8_t* et, const double* mean2d, const double* cov2d, const double* opac,
+                          const double* colors, const double* bg, double* color, double* final_T, int64_t* n_contrib,
+                          double* margin, int8_t* margin_kind) {
+    for (int64_t q = 0; q < n; ++q) {
+        double px = pix[2 * q], py = pix[2 * q + 1];
+        double cr = 0, cg = 0, cb = 0, T = 1.0, mg = INFINITY;
+        int64_t nc = 0;
+        int8_t mkind = 0;
+        for (int64_t pos = 0; pos < bin_ptr[q + 1] - bin_ptr[q]; ++pos) {
+            int64_t j = bin_idx[bin_ptr[q] + pos];
+            double A, B, C;
+            conic_of(cov2d + 3 * j, &A, &B, &C);
+            double dx = px - mean2d[2 * j], dy = py - mean2d[2 * j + 1];
+            double sigma = 0.5 * (A * dx * dx + C * dy * dy) + B * dx * dy;
+            double araw = opac[j] * exp(-sigma);
+            double alpha = araw < ORC_ALPHA_MAX ? araw : ORC_ALPHA_MAX;
+            double m = rel_margin(sigma, ORC_SIGMA_CUT);
+            if (m < mg) { mg = m; mkind = 1; }
+            if (!(sigma <= ORC_SIGMA_CUT)) continue;
+            m = rel_margin(alpha, ORC_ALPHA_MIN);
+            if (m < mg) { mg = m; mkind = 2; }
+            m = rel_margin(araw, ORC_ALPHA_MAX);
+            if (m < mg) { mg = m; mkind = 3; }
+            if (!(alpha >= ORC_ALPHA_MIN)) continue;
+            double nT = T * (1.0 - alpha);
+            if (et[q]) {
+                m = rel_margin(nT, ORC_T_MIN);
+                if (m < mg) { mg = m; mkind = 4; }
+                if (nT < ORC_T_MIN) break;
+            }
+            double w = alpha * T;
+            cr += w * colors[3 * j]; cg += w * colors[3 * j + 1]; cb += w * colors[3 * j + 2];
+            T = nT;
+            nc = pos + 1;
+        }
+        color[3 * q] = cr + bg[0] * T;
+        color[3 * q + 1] = cg + bg[1] * T;
+        color[3 * q + 2] = cb + bg[2] * T;
+        final_T[q] = T;
+        n_contrib[q] = nc;
+        if (margin) margin[q] = mg;
+        if (margin_kind) margin_kind[q] = mkind;
+    }
+}
+
+/*
+ * sg/raster_backward.py:111-163 composite_pixel_backward /
+ * transmittance_replay (the :47-108 walk for one pixel) for n queries.
+ * Gradients accumulate into per-splat rows: d9[j] = d_color 3, d_opacity,
+ * d_mean2d 2, d_cov2d 00, 01 (= 10), 11.  t_log (optional, sized like
+ * bin_idx): replayed T before each contributing entry, NaN elsewhere.
+ */
+void orc_composite_pixels_bwd(int64_t n, const int64_t* bin_ptr, const int64_t* bin_idx, const double* pix,
+                              const double* mean2d, const double* cov2d, const double* opac, const double* colors,
+                              const double* bg, const double* final_T, const int64_t* n_contrib,
+                              const double* d_pix, double* d9, double* t_log) {
+    for (int64_t q = 0; q < n; ++q) {
+        const int64_t b0 = bin_ptr[q], len = bin_ptr[q + 1] - b0;
+        if (t_log)
+            for (int64_t pos = 0; pos < len; ++pos) t_log[b0 + pos] = NAN;
+        double px = pix[2 * q], py = pix[2 * q + 1];
+        double T = final_T[q];
+        double S[3] = {bg[0] * T, bg[1] * T, bg[2] * T};
+        const double* g = d_pix + 3 * q;
+        int64_t nc = n_contrib[q] < len ? n_contrib[q] : len;
+        for (int64_t pos = nc - 1; pos >= 0; --pos) {
+            int64_t j = bin_idx[b0 + pos];
+            double A, B, C;
+            conic_of(cov2d + 3 * j, &A, &B, &C);
+            double dx = px - mean2d[2 * j], dy = py - mean2d[2 * j + 1];
+            double sigma = 0.5 * (A * dx * dx + C * dy * dy) + B * dx * dy;
+            double e = exp(-sigma);
+            double araw = opac[j] * e;
+            double alpha = araw < ORC_ALPHA_MAX ? araw : ORC_ALPHA_MAX;
+            if (!(sigma <= ORC_SIGMA_CUT) || !(alpha >= ORC_ALPHA_MIN)) continue;
+            double om = 1.0 - alpha, th = T / om, w = alpha * th;
+            if (t_log) t_log[b0 + pos] = th;
+            const double* col3 = colors + 3 * j;
+            double* a = d9 + 9 * j;
+            a[0] += w * g[0]; a[1] += w * g[1]; a[2] += w * g[2];
+            double da = (col3[0] * th - S[0] / om) * g[0] + (col3[1] * th - S[1] / om) * g[1] +
+                        (col3[2] * th - S[2] / om) * g[2];
+            if (araw < ORC_ALPHA_MAX) {
+                a[3] += da * e;
+                double dsig = -araw * da;
+                double y0 = A * dx + B * dy, y1 = B * dx + C * dy;
+                a[4] += -dsig * y0; a[5] += -dsig * y1;
+                a[6] += -0.5 * dsig * y0 * y0; a[7] += -0.5 * dsig * y0 * y1; a[8] += -0.5 * dsig * y1 * y1;
+            }
+            for (int c = 0; c < 3; ++c) S[c] += w * col3[c];
+            T = th;
+        }
+    }
+}
+
 /* sg/proj_backward.py:139-148 dR/d(w,x,y,z) for a unit quaternion. */
 static void rotmat_quat_jacobians(double w, double x, double y, double z, double Jq[4][9]) {
     double t[4][9] = {

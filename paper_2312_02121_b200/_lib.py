@@ -21,6 +21,7 @@ EXPORTS = (
     "gs_project_bwd_workspace_bytes", "gs_project_bwd",
     "gs_frame_workspace_bytes", "gs_frame_view_of", "gs_frame_forward", "gs_frame_backward",
     "gs_activate", "gs_loss_l2", "gs_adam_step",
+    "gs_conic_from_cov", "gs_eval_alpha", "gs_composite_pixels", "gs_composite_pixels_bwd",
 )
 
 ERR_MESSAGES = {  # include/splat_b200.h gs_error_code -> the reference's ValueError text
@@ -91,6 +92,10 @@ def load():
         "gs_loss_l2": ([P, P, i64, P, P, P], C.c_int),
         "gs_adam_step": ([P, P, P, P, P, P, P, P, P, P, P, P, P, i64, C.c_int, C.POINTER(f32), f32, f32, f32, P],
                          C.c_int),
+        "gs_conic_from_cov": ([P, P, i64, P, P, P], C.c_int),
+        "gs_eval_alpha": ([P, P, P, P, i64, P, P, P, P], C.c_int),
+        "gs_composite_pixels": ([P, P, P, P, P, P, i64, C.POINTER(f32), C.c_int, P, P, P, P], C.c_int),
+        "gs_composite_pixels_bwd": ([P, P, P, P, P, P, i64, C.POINTER(f32), P, P, P, P, P, P, P, P], C.c_int),
     })
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -9,6 +9,9 @@ splatgrad) for the hot path:
   accumulate_image_backward         sg/raster_backward.py:166-205
   project_gaussian                  sg/projection.py:115-145
   assign_tiles, sort_bins           sg/binning.py:27-65
+  eval_alpha, composite_pixel       sg/raster_forward.py:175-219
+  composite_pixel_backward,
+  transmittance_replay              sg/raster_backward.py:111-163
 
 plus the value types they exchange (Gaussian3D, Camera, ProjectedGaussian,
 TileGrid, RenderResult, RenderAux, ImageBuffer, Splat2DGrads,
@@ -22,11 +25,12 @@ reference work unchanged.  Requires a CUDA device (no CPU fallback).
 from __future__ import annotations
 
 from dataclasses import dataclass, field
+from typing import NamedTuple
 
 import numpy as np
 import torch
 
-from . import ops
+from . import ops, pixels
 
 # constants (sg/binning.py:8, sg/projection.py:17, sg/raster_forward.py:21-30, sg/core.py:13)
 TILE_SIZE = 16
@@ -167,6 +171,13 @@ class ImageBuffer:
 class RenderAux:
     final_T: np.ndarray
     n_contrib: np.ndarray
+
+
+class PixelAux(NamedTuple):
+    """sg/raster_forward.py:57-59."""
+
+    final_T: float
+    n_contrib: int
 
 
 @dataclass
@@ -426,3 +437,95 @@ def sort_bins(grid: TileGrid, projected) -> TileGrid:
         out.append(sorted_idx[pos:pos + sz].tolist())
         pos += sz
     return TileGrid(grid.tile_size, grid.tiles_x, grid.tiles_y, out)
+
+
+# ------------------------------------------------------------------ per-pixel API
+
+def _splat_arrays(projected, scene, dev):
+    """Device splat records of `projected` (sg/raster_forward.py:95-113
+    _pack_splats): xydr (m,4), conic (m,4) (A, B, C, opacity), colors (m,3),
+    and the source indices."""
+    m = len(projected)
+    xydr = np.zeros((m, 4), np.float32)
+    cov = np.zeros((m, 3), np.float32)
+    opac = np.zeros(m, np.float32)
+    colors = np.zeros((m, 3), np.float32)
+    src = np.zeros(m, np.int64)
+    for j, p in enumerate(projected):
+        c = np.asarray(p.cov2d, np.float64)
+        xydr[j, :2] = np.asarray(p.mean2d, np.float64)
+        cov[j] = c[0, 0], c[0, 1], c[1, 1]
+        if scene is not None:
+            g = scene[p.source_index]
+            opac[j], colors[j] = g.opacity, g.color
+        src[j] = p.source_index
+    t = lambda a: torch.as_tensor(a, device=dev)
+    conic = pixels.conic_from_cov(t(cov), t(opac))
+    return t(xydr), conic, t(colors), src
+
+
+def eval_alpha(g, opacity, pixel_center):
+    """sg/raster_forward.py:175-196 on the GPU: (alpha, delta, sigma)."""
+    dev = _device()
+    c = np.asarray(g.cov2d, np.float64)
+    xydr = torch.as_tensor(np.array([[g.mean2d[0], g.mean2d[1], 0.0, 0.0]], np.float32), device=dev)
+    conic = pixels.conic_from_cov(torch.as_tensor(np.array([[c[0, 0], c[0, 1], c[1, 1]]], np.float32), device=dev),
+                                  torch.as_tensor(np.array([opacity], np.float32), device=dev))
+    pix = torch.as_tensor(np.asarray(pixel_center, np.float64).reshape(1, 2).astype(np.float32), device=dev)
+    alpha, delta, sigma = pixels.eval_alpha(xydr, conic, torch.zeros(1, dtype=torch.int32, device=dev), pix)
+    return float(alpha.item()), _np(delta)[0].astype(np.float64), float(sigma.item())
+
+
+def _one_query(sorted_bin, pixel_center, dev):
+    idx = np.asarray(list(sorted_bin), np.int64)
+    bin_ptr = torch.as_tensor(np.array([0, len(idx)], np.int64), device=dev)
+    bin_idx = torch.as_tensor(idx.astype(np.int32), device=dev)
+    pix = torch.as_tensor(np.asarray(pixel_center, np.float64).reshape(1, 2).astype(np.float32), device=dev)
+    return bin_ptr, bin_idx, pix
+
+
+def composite_pixel(sorted_bin, projected, scene, pixel_center, background, early_termination=True):
+    """sg/raster_forward.py:199-219 on the GPU: (color 3-vector,
+    PixelAux(final_T, n_contrib))."""
+    dev = _device()
+    xydr, conic, colors, _ = _splat_arrays(projected, scene, dev)
+    bin_ptr, bin_idx, pix = _one_query(sorted_bin, pixel_center, dev)
+    color, T, nc = pixels.composite_pixels(xydr, conic, colors, bin_ptr, bin_idx, pix,
+                                           np.asarray(background, np.float64), early_termination)
+    return _np(color)[0].astype(np.float64), PixelAux(float(T.item()), int(nc.item()))
+
+
+def _pixel_backward(sorted_bin, projected, scene, pixel_center, background, aux_entry, d_pixel, want_t_log):
+    dev = _device()
+    xydr, conic, colors, src = _splat_arrays(projected, scene, dev)
+    bin_ptr, bin_idx, pix = _one_query(sorted_bin, pixel_center, dev)
+    fT = torch.as_tensor(np.array([aux_entry.final_T], np.float32), device=dev)
+    nc = torch.as_tensor(np.array([aux_entry.n_contrib], np.int32), device=dev)
+    d = torch.as_tensor(np.asarray(d_pixel, np.float64).reshape(1, 3).astype(np.float32), device=dev)
+    return src, pixels.composite_pixels_backward(xydr, conic, colors, bin_ptr, bin_idx, pix,
+                                                 np.asarray(background, np.float64), fT, nc, d,
+                                                 want_t_log=want_t_log)
+
+
+def composite_pixel_backward(sorted_bin, projected, scene, pixel_center, background, aux_entry,
+                             d_pixel) -> Splat2DGrads:
+    """sg/raster_backward.py:111-135 on the GPU: one row per scene Gaussian."""
+    src, (d_rgbo, d_geo, d_c11, _) = _pixel_backward(sorted_bin, projected, scene, pixel_center, background,
+                                                     aux_entry, d_pixel, False)
+    rgbo, geo, c11 = (_np(x).astype(np.float64) for x in (d_rgbo, d_geo, d_c11))
+    grads = Splat2DGrads.zeros(len(scene))
+    np.add.at(grads.d_color, src, rgbo[:, :3])
+    np.add.at(grads.d_opacity, src, rgbo[:, 3])
+    np.add.at(grads.d_mean2d, src, geo[:, :2])
+    cov = np.stack([geo[:, 2], geo[:, 3], geo[:, 3], c11], axis=1).reshape(-1, 2, 2)
+    np.add.at(grads.d_cov2d, src, cov)
+    return grads
+
+
+def transmittance_replay(sorted_bin, projected, scene, pixel_center, background, aux_entry):
+    """sg/raster_backward.py:138-163 on the GPU: (bin position, T) pairs in
+    back-to-front order, one per splat that contributed in the forward."""
+    _, (_, _, _, t_log) = _pixel_backward(sorted_bin, projected, scene, pixel_center, background, aux_entry,
+                                          np.zeros(3), True)
+    t = _np(t_log).astype(np.float64)
+    return [(pos, float(t[pos])) for pos in range(len(t) - 1, -1, -1) if np.isfinite(t[pos])]

@@ -56,6 +56,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // sigma = 0.5*(A dx^2 + C dy^2) + B dx dy   (sg/raster_forward.py:132-135)
 // evaluated as dx*(hA*dx + B*dy) + (hC*dy)*dy with hA = A/2, hC = C/2
 // (exact halvings), every op rounded explicitly.
@@ -133,6 +139,17 @@ __device__ __forceinline__ f32x2 splat_sigma2(float dx, float hAdx, f32x2 dy, fl
     const f32x2 t = fma2(pk2(B, B), dy, pk2(hAdx, hAdx));
     const f32x2 u = mul2(mul2(pk2(hC, hC), dy), dy);
     return fma2(pk2(dx, dx), t, u);
+}
+
+// det of the 2d covariance and its inverse terms (A, B, C)
+// (sg/raster_forward.py:86-92), shared by the projection kernel and the
+// per-pixel API so both produce the same conic bit for bit.
+__device__ __forceinline__ float cov2d_det(float ca, float cb, float cc) {
+    return __fmaf_rn(ca, cc, -__fmul_rn(cb, cb));
+}
+__device__ __forceinline__ float4 conic_of(float ca, float cb, float cc, float det, float opacity) {
+    const float idet = __fdiv_rn(1.f, det);
+    return make_float4(__fmul_rn(cc, idet), -__fmul_rn(cb, idet), __fmul_rn(ca, idet), opacity);
 }
 
 // exp(-sigma) shared by forward and backward (sg/raster_forward.py:136,

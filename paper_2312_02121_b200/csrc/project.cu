@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
             } else {
                 const float px = (cam.fx * (tx / tz) + 0.5f) + cam.cx;
                 const float py = (cam.fy * (ty / tz) + 0.5f) + cam.cy;
-                const float det = ca * cc - cb * cb;
+                const float det = cov2d_det(ca, cb, cc);
                 if (!(det > 0.f && ca + cc > 0.f)) {
                     report(status, i, GS_ERR_COV2D);
                 } else {
@@ -104,8 +104,7 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
                                      (py - fr >= (float)cam.H);
                     o_xydr = make_float4(px, py, tz, __int_as_float(off ? 0 : r));
                     if (!off) {
-                        const float idet = 1.f / det;
-                        o_con = make_float4(cc * idet, -cb * idet, ca * idet, opac[i]);
+                        o_con = conic_of(ca, cb, cc, det, opac[i]);
                         int tx0, tx1, ty0, ty1;
                         tile_rect(px, py, r, cam.tiles_x, cam.tiles_y, tx0, tx1, ty0, ty1);
                         nt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));

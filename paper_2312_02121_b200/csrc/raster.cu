@@ -52,12 +52,6 @@ __device__ __forceinline__ float pin(float x) {
     return x;
 }
 
-__device__ __forceinline__ float rcp_approx(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
 struct Quad {
     int col, row0;  // this thread's pixel column and first row (second = row0 + 4)
     __device__ __forceinline__ Quad(int tile, int tiles_x) {

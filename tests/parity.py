@@ -28,7 +28,22 @@ GRAD_CLASSES = ("d_mean", "d_scale", "d_quat", "d_opacity", "d_color", "d_view")
 
 
 def golden_names():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+    # frame fixtures (make_golden.py); pixel.npz is the per-pixel API's own
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if os.path.basename(p) != "pixel.npz")
+
+
+def load_pixel_golden():
+    """tests/golden/pixel.npz (make_golden_pixel.py) with per-splat arrays in
+    the oracle's layout: cov3 (a, b, c) and the scene rows gathered per
+    projected splat."""
+    z = dict(np.load(os.path.join(GOLDEN, "pixel.npz")))
+    src = z["source_index"]
+    z["cov3"] = z["cov2d"].reshape(-1, 4)[:, [0, 1, 3]]
+    z["ea_cov3"] = z["ea_cov2d"].reshape(-1, 4)[:, [0, 1, 3]]
+    z["p_opacity"] = z["s_opacity"][src]
+    z["p_color"] = z["s_color"][src]
+    return z
 
 
 def load_golden(name):
