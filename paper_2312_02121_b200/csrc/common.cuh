@@ -62,6 +62,12 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // sigma = 0.5*(A dx^2 + C dy^2) + B dx dy   (sg/raster_forward.py:132-135)
 // evaluated as dx*(hA*dx + B*dy) + (hC*dy)*dy with hA = A/2, hC = C/2
 // (exact halvings), every op rounded explicitly.

@@ -76,7 +76,7 @@ __device__ __forceinline__ int stage_batch(BatchT<NWR>& s, int tile, int tiles_x
     for (int u = 0; u < RB / NTR; ++u) {
         const int k = u * NTR + (int)threadIdx.x;
         const bool valid = k < count;
-        float x = 0.f, y = 0.f, r = -1e30f;
+        float x = 0.f, y = 0.f, rx = -1e30f, ry = -1e30f;
         if (valid) {
             const uint32_t id = ids[first + k];
             const float4 g = xydr[id];
@@ -87,13 +87,21 @@ __device__ __forceinline__ int stage_batch(BatchT<NWR>& s, int tile, int tiles_x
             s.id[k] = id;
             x = g.x;
             y = g.y;
-            r = (float)__float_as_int(g.w) + 1.f;
+            // Reach of the sigma <= 4.5 ellipse {d : d^T Q d <= 9} of this
+            // conic Q: |dx| <= 3 sqrt(Q_yy / det Q), |dy| <= 3 sqrt(Q_xx /
+            // det Q) (tighter than the circle radius the tiles are binned
+            // by), grown by 0.1% and one pixel so fp32 rounding cannot
+            // un-skip a pair; never more than the circle.
+            const float r = (float)__float_as_int(g.w) + 1.f;
+            const float idq = rcp_approx(__fmaf_rn(q.x, q.z, -__fmul_rn(q.y, q.y)));
+            rx = fminf(r, __fmaf_rn(3.003f, sqrt_approx(q.z * idq), 1.f));
+            ry = fminf(r, __fmaf_rn(3.003f, sqrt_approx(q.x * idq), 1.f));
         }
 #pragma unroll
         for (int w = 0; w < NWR; ++w) {
             const float x0 = (float)(tx * TILE + (w & 1) * 8) + 0.5f;
             const float y0 = (float)(ty * TILE + (NWR == 4 ? (w >> 1) * 8 : 0)) + 0.5f;
-            const bool ov = valid && x + r >= x0 && x - r <= x0 + 7.f && y + r >= y0 && y - r <= y0 + RH;
+            const bool ov = valid && x + rx >= x0 && x - rx <= x0 + 7.f && y + ry >= y0 && y - ry <= y0 + RH;
             const uint32_t m = __ballot_sync(0xffffffffu, ov);
             if (lane == 0) s.mask[w][u * NWR + warp] = m;
         }
@@ -346,6 +354,118 @@ __device__ __forceinline__ float warp_reduce8(const float* v, int lane) {
     return r;
 }
 
+// sigma of one list entry for this lane's pixel pairs (backward replay)
+template <int NPR>
+struct BwdEvalT {
+    float dx;
+    f32x2 DY[NPR], SG[NPR];
+    bool v[2 * NPR];
+    bool any;
+    unsigned n_vis;
+};
+template <int NPR, int NWR>
+__device__ __forceinline__ void bwd_eval(const BatchT<NWR>& s, int k, int pos, float px, const f32x2 (&PY)[NPR],
+                                         const int (&nc)[2 * NPR], BwdEvalT<NPR>& e) {
+    const float4 a = s.a[k];
+    const float hC = s.b[k].x;
+    e.dx = __fsub_rn(px, a.x);
+    const float hAdx = __fmul_rn(a.z, e.dx);
+    e.any = false;
+    e.n_vis = 0;
+#pragma unroll
+    for (int j = 0; j < NPR; ++j) {
+        e.DY[j] = sub2(PY[j], bc2(a.y));
+        e.SG[j] = splat_sigma2(e.dx, hAdx, e.DY[j], a.w, hC);
+        e.v[2 * j] = pos < nc[2 * j] && lo2(e.SG[j]) <= SIGMA_CUT;
+        e.v[2 * j + 1] = pos < nc[2 * j + 1] && hi2(e.SG[j]) <= SIGMA_CUT;
+        e.any = e.any || e.v[2 * j] || e.v[2 * j + 1];
+        e.n_vis += (unsigned)e.v[2 * j] + (unsigned)e.v[2 * j + 1];
+    }
+}
+
+// Replay + gradient of one entry on the lane's pairs (sg/raster_backward.py
+// :64-107), then the per-warp accumulation into the splat's gradient rows.
+template <int NPR, bool COUNT, int NWR>
+__device__ __forceinline__ void bwd_commit(const BatchT<NWR>& s, int k, const BwdEvalT<NPR>& e, int lane, f32x2 (&T)[NPR],
+                                           const f32x2 (&G0)[NPR], const f32x2 (&G1)[NPR], const f32x2 (&G2)[NPR],
+                                           f32x2 (&S0)[NPR], f32x2 (&S1)[NPR], f32x2 (&S2)[NPR],
+                                           float4* __restrict__ d_rgbo, float4* __restrict__ d_geo,
+                                           float* __restrict__ d_c11, unsigned long long& e_c) {
+    const float4 a = s.a[k];
+    const float4 bq = s.b[k];
+    const float blue = s.c[k];
+    const float hC = bq.x;
+    const float dx = e.dx;
+    float acc[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) acc[t] = 0.f;  // dead for NPR == 1 (first pair assigns)
+    bool anyc = false;
+#pragma unroll
+    for (int j = 0; j < NPR; ++j) {
+        // replay of the forward decisions on the pair
+        const f32x2 SL = mul2(e.SG[j], bc2(NEG_LOG2E));
+        const f32x2 E = pk2(ex2_approx(lo2(SL)), ex2_approx(hi2(SL)));
+        const f32x2 ARAW = mul2(bc2(bq.y), E);
+        const float al0 = fminf(lo2(ARAW), ALPHA_MAX), al1 = fminf(hi2(ARAW), ALPHA_MAX);
+        const bool c0 = e.v[2 * j] && al0 >= ALPHA_MIN, c1 = e.v[2 * j + 1] && al1 >= ALPHA_MIN;
+        if (COUNT) e_c += (unsigned)c0 + (unsigned)c1;
+        if (NPR > 1 && !__any_sync(0xffffffffu, c0 || c1)) continue;
+        anyc = anyc || c0 || c1;
+        const f32x2 AL = pk2(al0, al1);
+        const f32x2 OM = sub2(bc2(1.f), AL);
+        const f32x2 INV = pk2(rcp_approx(lo2(OM)), rcp_approx(hi2(OM)));
+        const f32x2 TH = mul2(T[j], INV);  // T before this splat (:75)
+        const f32x2 Wt = mul2(AL, TH);
+        const f32x2 WC = pk2(c0 ? lo2(Wt) : 0.f, c1 ? hi2(Wt) : 0.f);
+        const f32x2 CDOT = fma2(bc2(blue), G2[j], fma2(bc2(bq.w), G1[j], mul2(bc2(bq.z), G0[j])));
+        const f32x2 SDOT = fma2(S2[j], G2[j], fma2(S1[j], G1[j], mul2(S0[j], G0[j])));
+        const f32x2 DA = sub2(mul2(TH, CDOT), mul2(INV, SDOT));
+        // live (:91): contributing and not clamped
+        const bool l0 = c0 && lo2(ARAW) < ALPHA_MAX, l1 = c1 && hi2(ARAW) < ALPHA_MAX;
+        const f32x2 DAL = pk2(l0 ? lo2(DA) : 0.f, l1 ? hi2(DA) : 0.f);
+        const f32x2 M = mul2(ARAW, DAL);  // = -d_sigma
+        const f32x2 Y0 = fma2(bc2(a.w), e.DY[j], bc2(2.f * a.z * dx));
+        const f32x2 Y1 = fma2(bc2(2.f * hC), e.DY[j], bc2(a.w * dx));
+        const f32x2 HM = mul2(bc2(0.5f), M);
+        const f32x2 HY0 = mul2(HM, Y0), HY1 = mul2(HM, Y1);
+        const f32x2 D[9] = {mul2(WC, G0[j]), mul2(WC, G1[j]), mul2(WC, G2[j]), mul2(DAL, E), mul2(M, Y0),
+                            mul2(M, Y1),     mul2(HY0, Y0),   mul2(HY0, Y1),   mul2(HY1, Y1)};
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const float v = lo2(D[t]) + hi2(D[t]);
+            acc[t] = NPR == 1 ? v : acc[t] + v;
+        }
+        S0[j] = fma2(WC, bc2(bq.z), S0[j]);
+        S1[j] = fma2(WC, bc2(bq.w), S1[j]);
+        S2[j] = fma2(WC, bc2(blue), S2[j]);
+        T[j] = sel2(c0, c1, TH, T[j]);
+    }
+    const uint32_t cmask = __ballot_sync(0xffffffffu, anyc);
+    if (!cmask) return;
+    const uint32_t id = s.id[k];
+    if (__popc(cmask) <= 3) {
+        // few contributing lanes: their own vector reductions are cheaper
+        // than a 9-value warp reduction
+        if (anyc) {
+            red_add_v4(&d_rgbo[id], acc[0], acc[1], acc[2], acc[3]);
+            red_add_v4(&d_geo[id], acc[4], acc[5], acc[6], acc[7]);
+            atomicAdd(&d_c11[id], acc[8]);
+        }
+        return;
+    }
+    const float r = warp_reduce8(acc, lane);
+    float c11 = acc[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c11 += __shfl_xor_sync(0xffffffffu, c11, o);
+    if ((lane & 3) == 0) {
+        const int idx = lane >> 2;
+        float* dst = idx < 4 ? reinterpret_cast<float*>(&d_rgbo[id]) + idx
+                             : reinterpret_cast<float*>(&d_geo[id]) + (idx - 4);
+        atomicAdd(dst, r);
+    }
+    if (lane == 0) atomicAdd(&d_c11[id], c11);
+}
+
 // sg/raster_backward.py:47-108 _backward_tile for one tile: seed T = final_T,
 // S = bg * final_T; walk pos = max(n_contrib)-1 .. 0 replaying the forward's
 // decisions (same sigma/exp code, same quadrant lists); contrib ->
@@ -405,6 +525,11 @@ __global__ void __launch_bounds__(32 * NWR) raster_bwd_kernel(
 #pragma unroll
     for (int w = 0; w < NWR; ++w) max_nc = max(max_nc, s_max[w]);
     unsigned long long e_s = 0, e_c = 0;
+    if (threadIdx.x == 0) {  // sentinel entry: dx = -inf -> sigma NaN -> never visible
+        s.a[RB] = make_float4(__int_as_float(0x7f800000), 0.f, 0.f, 0.f);
+        s.b[RB] = make_float4(0.f, 0.f, 0.f, 0.f);
+        s.c[RB] = 0.f;
+    }
 
     for (int bend = max_nc; bend > 0; bend -= RB) {
         const int bstart = max(0, bend - RB);
@@ -413,105 +538,19 @@ __global__ void __launch_bounds__(32 * NWR) raster_bwd_kernel(
         const uint8_t* lst = s.list[warp];
         const int kmax = min(bend, warp_max) - bstart;  // positions >= warp_max are inactive for this warp
         while (n > 0 && (int)lst[n - 1] >= kmax) --n;
+        // two entries per iteration (independent sigma chains), committed
+        // strictly back to front; an odd list's last pair uses the sentinel
 #pragma unroll 1
-        for (int i = n - 1; i >= 0; --i) {
-            const int k = lst[i];
-            const int pos = bstart + k;
-            const float4 a = s.a[k];
-            const float hC = s.b[k].x;
-            const float dx = __fsub_rn(px, a.x);
-            const float hAdx = __fmul_rn(a.z, dx);
-            f32x2 DY[NPR], SG[NPR];
-            bool v[2 * NPR];
-            bool any = false;
-#pragma unroll
-            for (int j = 0; j < NPR; ++j) {
-                DY[j] = sub2(PY[j], bc2(a.y));
-                SG[j] = splat_sigma2(dx, hAdx, DY[j], a.w, hC);
-                v[2 * j] = pos < nc[2 * j] && lo2(SG[j]) <= SIGMA_CUT;
-                v[2 * j + 1] = pos < nc[2 * j + 1] && hi2(SG[j]) <= SIGMA_CUT;
-                any = any || v[2 * j] || v[2 * j + 1];
-            }
-            if (COUNT) {
-#pragma unroll
-                for (int q = 0; q < 2 * NPR; ++q) e_s += (unsigned)v[q];
-            }
-            if (!__any_sync(0xffffffffu, any)) continue;
-            const float4 bq = s.b[k];
-            const float blue = s.c[k];
-            float acc[9];
-#pragma unroll
-            for (int t = 0; t < 9; ++t) acc[t] = 0.f;
-            bool anyc = false;
-#pragma unroll
-            for (int j = 0; j < NPR; ++j) {
-                // replay of the forward decisions on the pair
-                const f32x2 SL = mul2(SG[j], bc2(NEG_LOG2E));
-                const f32x2 E = pk2(ex2_approx(lo2(SL)), ex2_approx(hi2(SL)));
-                const f32x2 ARAW = mul2(bc2(bq.y), E);
-                const float al0 = fminf(lo2(ARAW), ALPHA_MAX), al1 = fminf(hi2(ARAW), ALPHA_MAX);
-                const bool c0 = v[2 * j] && al0 >= ALPHA_MIN, c1 = v[2 * j + 1] && al1 >= ALPHA_MIN;
-                if (COUNT) e_c += (unsigned)c0 + (unsigned)c1;
-                if (NPR > 1 && !__any_sync(0xffffffffu, c0 || c1)) continue;
-                anyc = anyc || c0 || c1;
-                const f32x2 AL = pk2(al0, al1);
-                const f32x2 OM = sub2(bc2(1.f), AL);
-                const f32x2 INV = pk2(rcp_approx(lo2(OM)), rcp_approx(hi2(OM)));
-                const f32x2 TH = mul2(T[j], INV);  // T before this splat (:75)
-                const f32x2 Wt = mul2(AL, TH);
-                const f32x2 WC = pk2(c0 ? lo2(Wt) : 0.f, c1 ? hi2(Wt) : 0.f);
-                const f32x2 CDOT = fma2(bc2(blue), G2[j], fma2(bc2(bq.w), G1[j], mul2(bc2(bq.z), G0[j])));
-                const f32x2 SDOT = fma2(S2[j], G2[j], fma2(S1[j], G1[j], mul2(S0[j], G0[j])));
-                const f32x2 DA = sub2(mul2(TH, CDOT), mul2(INV, SDOT));
-                // live (:91): contributing and not clamped
-                const bool l0 = c0 && lo2(ARAW) < ALPHA_MAX, l1 = c1 && hi2(ARAW) < ALPHA_MAX;
-                const f32x2 DAL = pk2(l0 ? lo2(DA) : 0.f, l1 ? hi2(DA) : 0.f);
-                const f32x2 M = mul2(ARAW, DAL);  // = -d_sigma
-                const f32x2 Y0 = fma2(bc2(a.w), DY[j], bc2(2.f * a.z * dx));
-                const f32x2 Y1 = fma2(bc2(2.f * hC), DY[j], bc2(a.w * dx));
-                const f32x2 HM = mul2(bc2(0.5f), M);
-                const f32x2 HY0 = mul2(HM, Y0), HY1 = mul2(HM, Y1);
-                const f32x2 D0 = mul2(WC, G0[j]), D1 = mul2(WC, G1[j]), D2 = mul2(WC, G2[j]);
-                const f32x2 D3 = mul2(DAL, E), D4 = mul2(M, Y0), D5 = mul2(M, Y1);
-                const f32x2 D6 = mul2(HY0, Y0), D7 = mul2(HY0, Y1), D8 = mul2(HY1, Y1);
-                acc[0] += lo2(D0) + hi2(D0);
-                acc[1] += lo2(D1) + hi2(D1);
-                acc[2] += lo2(D2) + hi2(D2);
-                acc[3] += lo2(D3) + hi2(D3);
-                acc[4] += lo2(D4) + hi2(D4);
-                acc[5] += lo2(D5) + hi2(D5);
-                acc[6] += lo2(D6) + hi2(D6);
-                acc[7] += lo2(D7) + hi2(D7);
-                acc[8] += lo2(D8) + hi2(D8);
-                S0[j] = fma2(WC, bc2(bq.z), S0[j]);
-                S1[j] = fma2(WC, bc2(bq.w), S1[j]);
-                S2[j] = fma2(WC, bc2(blue), S2[j]);
-                T[j] = sel2(c0, c1, TH, T[j]);
-            }
-            const uint32_t cmask = __ballot_sync(0xffffffffu, anyc);
-            if (!cmask) continue;
-            const uint32_t id = s.id[k];
-            if (__popc(cmask) <= 3) {
-                // few contributing lanes: their own vector reductions are
-                // cheaper than a 9-value warp reduction
-                if (anyc) {
-                    red_add_v4(&d_rgbo[id], acc[0], acc[1], acc[2], acc[3]);
-                    red_add_v4(&d_geo[id], acc[4], acc[5], acc[6], acc[7]);
-                    atomicAdd(&d_c11[id], acc[8]);
-                }
-                continue;
-            }
-            const float r = warp_reduce8(acc, lane);
-            float c11 = acc[8];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) c11 += __shfl_xor_sync(0xffffffffu, c11, o);
-            if ((lane & 3) == 0) {
-                const int idx = lane >> 2;
-                float* dst = idx < 4 ? reinterpret_cast<float*>(&d_rgbo[id]) + idx
-                                     : reinterpret_cast<float*>(&d_geo[id]) + (idx - 4);
-                atomicAdd(dst, r);
-            }
-            if (lane == 0) atomicAdd(&d_c11[id], c11);
+        for (int i = n - 1; i >= 0; i -= 2) {
+            const int k0 = lst[i];
+            const int k1 = i > 0 ? (int)lst[i - 1] : RB;
+            BwdEvalT<NPR> e0, e1;
+            bwd_eval<NPR>(s, k0, bstart + k0, px, PY, nc, e0);
+            bwd_eval<NPR>(s, k1, bstart + k1, px, PY, nc, e1);
+            const bool a0 = __any_sync(0xffffffffu, e0.any), a1 = __any_sync(0xffffffffu, e1.any);
+            if (COUNT) e_s += e0.n_vis + e1.n_vis;
+            if (a0) bwd_commit<NPR, COUNT>(s, k0, e0, lane, T, G0, G1, G2, S0, S1, S2, d_rgbo, d_geo, d_c11, e_c);
+            if (a1) bwd_commit<NPR, COUNT>(s, k1, e1, lane, T, G0, G1, G2, S0, S1, S2, d_rgbo, d_geo, d_c11, e_c);
         }
     }
     if (COUNT) {
