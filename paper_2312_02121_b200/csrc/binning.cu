@@ -232,11 +232,7 @@ __global__ void __launch_bounds__(256) emit_sorted_kernel(const uint32_t* __rest
             vals[base + t] = og;
             atomicAdd(&sh[tile & 255u], 1u);
         }
-        if (tile_passes > 1) {  // high digit: few distinct values per warp -> aggregate
-            const uint32_t d = valid ? (tile >> 8) & 255u : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            if (valid && lane == __ffs(peers) - 1) atomicAdd(&sh[256 + d], (uint32_t)__popc(peers));
-        }
+        if (tile_passes > 1) warp_hist_add(sh + 256, (tile >> 8) & 255u, valid);  // high digit: few distinct values
     }
     __syncthreads();
     for (int k = threadIdx.x; k < tile_passes * 256; k += blockDim.x) {

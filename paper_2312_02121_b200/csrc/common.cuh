@@ -182,6 +182,22 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float
                  : "memory");
 }
 
+// Shared-memory histogram update for one digit per lane: when every valid
+// lane of the warp holds the same digit (typical for high key bytes) one
+// lane adds the count, otherwise each valid lane adds 1 (cheaper than
+// match_any aggregation on sm_100a).
+__device__ __forceinline__ void warp_hist_add(uint32_t* h, uint32_t d, bool valid) {
+    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+    if (!vm) return;
+    const int leader = __ffs(vm) - 1;
+    const uint32_t d0 = __shfl_sync(0xffffffffu, d, leader);
+    if (__all_sync(0xffffffffu, !valid || d == d0)) {
+        if ((int)(threadIdx.x & 31) == leader) atomicAdd(&h[d0], (uint32_t)__popc(vm));
+    } else if (valid) {
+        atomicAdd(&h[d], 1u);
+    }
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

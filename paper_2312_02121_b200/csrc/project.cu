@@ -25,7 +25,7 @@ __device__ __forceinline__ void report(unsigned long long* status, int i, int co
 // DKEY: also write the depth sort key of every Gaussian (float bits of the
 // camera depth for visible ones, 0xFFFFFFFF for culled ones so they sort
 // last) and accumulate the four 8-bit digit histograms of those keys for
-// the onesweep sort that follows (sort.cu), warp-aggregated with match_any.
+// the onesweep sort that follows (sort.cu), accumulated in shared memory.
 template <bool DKEY>
 __global__ void __launch_bounds__(256) project_fwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
@@ -128,13 +128,10 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
     }  // i < n
     if (DKEY) {
         const bool valid = i < n;
+        // low bytes of the depth bits are spread (per-lane atomics), high
+        // bytes and culled keys concentrated (warp-uniform fast path)
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const uint32_t d = valid ? (dkey >> (8 * p)) & 255u : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            if (valid && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1))
-                atomicAdd(&s_hist[p * 256 + d], (uint32_t)__popc(peers));
-        }
+        for (int p = 0; p < 4; ++p) warp_hist_add(s_hist + 256 * p, (dkey >> (8 * p)) & 255u, valid);
         __syncthreads();
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) {
             const uint32_t v = s_hist[k];

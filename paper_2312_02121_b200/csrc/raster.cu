@@ -478,7 +478,7 @@ __device__ __forceinline__ void bwd_commit(const BatchT<NWR>& s, int k, const Bw
 // reduction each (one atomic per warp per Gaussian value); when at most 3
 // lanes contribute they add their own sums directly instead.
 template <int NWR, bool COUNT>
-__global__ void __launch_bounds__(32 * NWR) raster_bwd_kernel(
+__global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ sorted_vals, const float4* __restrict__ xydr,
     const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg, int W, int H, int tiles_x,
     const float* __restrict__ final_T, const int* __restrict__ n_contrib, const float* __restrict__ d_img,

@@ -1,7 +1,7 @@
 // sort.cu -- hand-written stable LSD radix sort of (key, uint32 value) pairs
 // in the "onesweep" style: the digit histograms of every pass are produced
 // up front (by sort_hist_kernel, or fused into the producer kernel), then
-// one kernel per 8-bit pass ranks a tile of keys with warp match_any,
+// one kernel per 8-bit pass ranks a tile of keys with per-warp peer masks,
 // obtains the tile's global digit offsets through a decoupled look-back
 // chained scan, and scatters through shared memory so the global writes are
 // runs of consecutive addresses.
@@ -10,6 +10,8 @@
 // order: keys are emitted in Gaussian-index order, equal keys keep it.
 // Keys: uint32 (depth-first binning, frame.cu) or uint64 (the general
 // (tile << 32 | depth bits) C-ABI sort, gs_sort_pairs).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.cuh"
 
@@ -43,7 +45,8 @@ constexpr int sort_tile() { return SORT_THREADS * ITEMS; }
 
 template <typename K, int ITEMS>
 constexpr size_t sort_smem() {
-    return (size_t)sort_tile<K, ITEMS>() * (sizeof(K) + 4) + (size_t)SORT_WARPS * RADIX * 4 + 2 * RADIX * 4;
+    return (size_t)sort_tile<K, ITEMS>() * (sizeof(K) + 4) + (size_t)SORT_WARPS * RADIX * 4 + 2 * RADIX * 4 +
+           (size_t)SORT_WARPS * 2 * RADIX * 4;  // peer-mask banks (RANK_OR)
 }
 
 __device__ __forceinline__ uint32_t ldv(const uint32_t* p) { return *(const volatile uint32_t*)p; }
@@ -68,12 +71,8 @@ __global__ void __launch_bounds__(256) sort_hist_kernel(const K* __restrict__ ke
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
         const bool valid = i < n;
         const K key = valid ? keys[i] : (K)0;
-        for (int p = 0; p < passes; ++p) {
-            const uint32_t d = valid ? (uint32_t)((key >> (8 * p)) & (K)255) : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            if (valid && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1))
-                atomicAdd(&sh[p * RADIX + d], (uint32_t)__popc(peers));
-        }
+        for (int p = 0; p < passes; ++p)
+            warp_hist_add(sh + p * RADIX, (uint32_t)((key >> (8 * p)) & (K)255), valid);
     }
     __syncthreads();
     for (int k = threadIdx.x; k < passes * RADIX; k += blockDim.x) {
@@ -101,7 +100,7 @@ __device__ __forceinline__ uint32_t block_incl_scan256(uint32_t v, uint32_t* s_t
 }
 
 // One 8-bit pass.  vin == nullptr means value = input index (identity).
-template <typename K, int ITEMS>
+template <typename K, int ITEMS, bool RANK_OR>
 __global__ void __launch_bounds__(SORT_THREADS, sizeof(K) == 4 ? 3 : 2) onesweep_kernel(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_cap, const unsigned long long* __restrict__ n_dev, int shift,
@@ -113,6 +112,7 @@ __global__ void __launch_bounds__(SORT_THREADS, sizeof(K) == 4 ? 3 : 2) onesweep
     uint32_t* s_whist = s_vals + TILE_N;               // [warp][digit]
     uint32_t* s_gbase = s_whist + SORT_WARPS * RADIX;  // global dst of local slot 0 per digit
     uint32_t* s_lstart = s_gbase + RADIX;              // local start of each digit in the tile
+    uint32_t* s_peers = s_lstart + RADIX;              // [warp][2][digit] peer masks (RANK_OR)
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_tmp[SORT_WARPS];
 
@@ -121,6 +121,10 @@ __global__ void __launch_bounds__(SORT_THREADS, sizeof(K) == 4 ? 3 : 2) onesweep
     if (tid == 0) s_tile = atomicAdd(counter, 1u);
 #pragma unroll
     for (int k = 0; k < SORT_WARPS; ++k) s_whist[k * RADIX + tid] = 0;
+    if (RANK_OR) {
+#pragma unroll
+        for (int k = 0; k < 2 * SORT_WARPS; ++k) s_peers[k * RADIX + tid] = 0;
+    }
     __syncthreads();
     const uint32_t tile = s_tile;
     if ((int64_t)tile * TILE_N >= n) return;  // capacity-sized grid, fewer items this frame
@@ -137,17 +141,40 @@ __global__ void __launch_bounds__(SORT_THREADS, sizeof(K) == 4 ? 3 : 2) onesweep
     }
     // warp-local stable ranking: items in (i, lane) order = input order
     const uint32_t lt = lanemask_lt();
+    if (RANK_OR) {
+        // peer masks built with shared atomic OR (two alternating mask
+        // banks, so a bank is cleared while the other is being filled)
+        uint32_t* s_peer = s_peers + warp * 2 * RADIX;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const int64_t idx = wbase + i * 32 + lane;
-        const bool valid = idx < n;
-        const uint32_t d = valid ? (uint32_t)(key[i] >> shift) & 255u : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const int leader = __ffs(peers) - 1;
-        uint32_t old = 0;
-        if (valid && lane == leader) old = atomicAdd(&s_whist[warp * RADIX + d], (uint32_t)__popc(peers));
-        old = __shfl_sync(0xffffffffu, old, leader);
-        rank[i] = old + (uint32_t)__popc(peers & lt);
+        for (int i = 0; i < ITEMS; ++i) {
+            const int64_t idx = wbase + i * 32 + lane;
+            const bool valid = idx < n;
+            const uint32_t d = (uint32_t)(key[i] >> shift) & 255u;
+            uint32_t* pm = s_peer + (i & 1) * RADIX + d;
+            if (valid) atomicOr(pm, 1u << lane);
+            __syncwarp();
+            const uint32_t peers = valid ? *pm : 0u;
+            const uint32_t old = valid ? s_whist[warp * RADIX + d] : 0u;
+            __syncwarp();
+            if (valid && (peers & lt) == 0) {  // lowest peer: bump the count, clear the mask
+                s_whist[warp * RADIX + d] = old + (uint32_t)__popc(peers);
+                *pm = 0u;
+            }
+            rank[i] = old + (uint32_t)__popc(peers & lt);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int64_t idx = wbase + i * 32 + lane;
+            const bool valid = idx < n;
+            const uint32_t d = valid ? (uint32_t)(key[i] >> shift) & 255u : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const int leader = __ffs(peers) - 1;
+            uint32_t old = 0;
+            if (valid && lane == leader) old = atomicAdd(&s_whist[warp * RADIX + d], (uint32_t)__popc(peers));
+            old = __shfl_sync(0xffffffffu, old, leader);
+            rank[i] = old + (uint32_t)__popc(peers & lt);
+        }
     }
     __syncthreads();
     // per digit: exclusive prefix over warps, tile total, chained scan
@@ -205,11 +232,11 @@ __global__ void __launch_bounds__(SORT_THREADS, sizeof(K) == 4 ? 3 : 2) onesweep
     }
 }
 
-template <typename K, int ITEMS>
+template <typename K, int ITEMS, bool RANK_OR>
 static int set_sort_attr() {
     static bool done = false;
     if (!done) {
-        if (cudaFuncSetAttribute(onesweep_kernel<K, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(onesweep_kernel<K, ITEMS, RANK_OR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sort_smem<K, ITEMS>()) != cudaSuccess)
             return check_launch("onesweep smem attribute");
         done = true;
@@ -241,18 +268,29 @@ template size_t onesweep_status_bytes<unsigned long long>(int64_t, int);
 // `passes` zeroed uint32.  identity_vals: the first pass ignores v0's
 // contents and uses the input index as value (v0 is still the ping-pong
 // scratch).  Result lands in (k1, v1) when passes is odd, else (k0, v0).
-template <typename K, int ITEMS>
-static int run_passes(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
-                      int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
-                      bool identity_vals) {
-    if (set_sort_attr<K, ITEMS>()) return -1;
+// Warp ranking flavour: shared atomic-OR peer masks (default) or match_any
+// (GS_SORT_RANK=match).
+static bool rank_or() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GS_SORT_RANK");
+        v = (e && e[0] == 'm') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+template <typename K, int ITEMS, bool RANK_OR>
+static int run_passes_t(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
+                        int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
+                        bool identity_vals) {
+    if (set_sort_attr<K, ITEMS, RANK_OR>()) return -1;
     const int64_t tiles = (n_cap + sort_tile<K, ITEMS>() - 1) / sort_tile<K, ITEMS>();
     K* kin = k0;
     K* kout = k1;
     uint32_t* vin = v0;
     uint32_t* vout = v1;
     for (int p = 0; p < passes; ++p) {
-        onesweep_kernel<K, ITEMS><<<(unsigned)tiles, SORT_THREADS, sort_smem<K, ITEMS>(), s>>>(
+        onesweep_kernel<K, ITEMS, RANK_OR><<<(unsigned)tiles, SORT_THREADS, sort_smem<K, ITEMS>(), s>>>(
             kin, (p == 0 && identity_vals) ? nullptr : vin, kout, vout, n_cap, n_dev, 8 * p, hist + p * RADIX,
             status + (size_t)p * tiles * RADIX, counters + p);
         if (check_launch("onesweep_kernel")) return -1;
@@ -260,6 +298,17 @@ static int run_passes(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, c
         uint32_t* tv = vin; vin = vout; vout = tv;
     }
     return 0;
+}
+
+template <typename K, int ITEMS>
+static int run_passes(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
+                      int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
+                      bool identity_vals) {
+    if (rank_or())
+        return run_passes_t<K, ITEMS, true>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s,
+                                            identity_vals);
+    return run_passes_t<K, ITEMS, false>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s,
+                                         identity_vals);
 }
 
 template <typename K>
