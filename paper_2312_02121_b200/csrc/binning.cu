@@ -182,8 +182,11 @@ __global__ void __launch_bounds__(256) emit_sorted_kernel(const uint32_t* __rest
     __shared__ uint32_t sh[2 * 256];
     for (int k = threadIdx.x; k < 2 * 256; k += blockDim.x) sh[k] = 0;
     __syncthreads();
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
+    // grid-stride over Gaussians (whole warps per trip); the shared tile-digit
+    // histograms are flushed once per CTA
+    const int n_round = (n + 31) & ~31;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n_round; p += gridDim.x * blockDim.x) {
     int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
     uint32_t g = 0, off = 0;
     if (p < n) {
@@ -234,6 +237,7 @@ __global__ void __launch_bounds__(256) emit_sorted_kernel(const uint32_t* __rest
         }
         if (tile_passes > 1) warp_hist_add(sh + 256, (tile >> 8) & 255u, valid);  // high digit: few distinct values
     }
+    }  // grid-stride
     __syncthreads();
     for (int k = threadIdx.x; k < tile_passes * 256; k += blockDim.x) {
         const uint32_t v = sh[k];
@@ -287,7 +291,10 @@ int launch_emit_sorted(const uint32_t* order, const float* xydr4, const uint32_t
                        int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals, uint32_t* tile_hist,
                        int tile_passes, cudaStream_t s) {
     if (n == 0) return 0;
-    emit_sorted_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(order, (const float4*)xydr4, offsets, (int)n,
+    int64_t blocks = (n + 255) / 256;
+    const int64_t cap = (int64_t)sort_sm_count() * 8;  // resident CTAs
+    if (blocks > cap) blocks = cap;
+    emit_sorted_kernel<<<(unsigned)blocks, 256, 0, s>>>(order, (const float4*)xydr4, offsets, (int)n,
                                                                   tiles_x, tiles_y, capacity, tile_keys, vals,
                                                                   tile_hist, tile_passes);
     return check_launch("emit_sorted_kernel");

@@ -2,6 +2,7 @@
 // backward).  One thread per Gaussian; both kernels are HBM-bound
 // (80 B/Gaussian forward, 104 B/Gaussian backward).
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace gs {
 
@@ -37,8 +38,10 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) s_hist[k] = 0;
         __syncthreads();
     }
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (!DKEY && i >= n) return;
+    // grid-stride over Gaussians (warps stay converged for the histogram
+    // vote); the shared histograms are flushed once per CTA
+    const int n_round = (n + 31) & ~31;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += gridDim.x * blockDim.x) {
     uint32_t dkey = 0xFFFFFFFFu;
     if (i < n) {
     const float mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
@@ -132,6 +135,9 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
         // bytes and culled keys concentrated (warp-uniform fast path)
 #pragma unroll
         for (int p = 0; p < 4; ++p) warp_hist_add(s_hist + 256 * p, (dkey >> (8 * p)) & 255u, valid);
+    }
+    }  // grid-stride
+    if (DKEY) {
         __syncthreads();
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) {
             const uint32_t v = s_hist[k];
@@ -307,8 +313,10 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
                             int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
                             unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s) {
     if (n == 0) return 0;
-    const int blocks = (int)((n + 255) / 256);
-    project_fwd_kernel<true><<<blocks, 256, 0, s>>>(means3, scales3, (const float4*)quats4, opac, (int)n, k,
+    int64_t blocks = (n + 255) / 256;
+    const int64_t cap = (int64_t)sort_sm_count() * 6;  // resident CTAs (40 regs, 256 threads)
+    if (blocks > cap) blocks = cap;
+    project_fwd_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(means3, scales3, (const float4*)quats4, opac, (int)n, k,
                                                     (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
                                                     dhist);
     return check_launch("project_fwd_kernel<dkey>");
