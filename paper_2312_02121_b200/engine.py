@@ -1,0 +1,180 @@
+"""Repeated forward+backward renders through captured CUDA graphs.
+
+The per-call API (ops.rasterize, api.render/scene_backward) pays Python,
+allocation and a host sync for the intersection count on every frame.  A
+training or serving loop renders the same view sizes over and over; for it,
+``RenderStep`` captures the whole sync-free frame (gs_frame_forward +
+gs_frame_backward for every view, gradients summed over views) once per
+buffer set and replays it:
+
+  * static device buffers for the parameters, the upstream image gradients
+    and the 14 gradients per Gaussian (mean 3 | scale 3 | quat 4 | colour 3
+    | opacity 1 -- the SceneGradients fields, sg/proj_backward.py:25-50);
+  * two buffer sets, so the host<->device copies of one step overlap the
+    replay of the other (``pipeline``);
+  * the per-view intersection capacity comes from one checked frame; every
+    replay's status word and intersection count travel back with the
+    gradients and ``result()`` raises (status) or re-runs the step with a
+    larger capacity (overflow) exactly like the per-call path.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib, ops
+
+
+class RenderStep:
+    def __init__(self, n: int, cams, background=(0.0, 0.0, 0.0), early_termination=True, device=None,
+                 headroom: float = 1.05, buffers: int = 2):
+        self.dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.n = int(n)
+        self.cams = [c if isinstance(c, ops.CameraParams) else ops.CameraParams.of(c) for c in cams]
+        self.bg = tuple(float(b) for b in background)
+        self.et = bool(early_termination)
+        self.headroom = headroom
+        self.nbuf = buffers
+        z = lambda *shape: torch.zeros(shape, device=self.dev, dtype=torch.float32)
+        self.sets = []
+        for _ in range(buffers):
+            self.sets.append(dict(
+                params=[z(n, 3), z(n, 3), z(n, 4), z(n), z(n, 3)],
+                d_images=[z(c.height, c.width, 3) for c in self.cams],
+                grads=z(n, 14),
+                meta=torch.zeros((len(self.cams), 2), device=self.dev, dtype=torch.int64),
+                graph=None))
+        self.caps = None
+        self.wss = None
+
+    # -------------------------------------------------------------- set-up
+    def _size(self, k: int):
+        """One checked frame per view: the static intersection capacities."""
+        s = self.sets[k]
+        m, sc, q, o, c = s["params"]
+        L = _lib.load()
+        self.caps, self.wss = [], []
+        for cam, d in zip(self.cams, s["d_images"]):
+            fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et)
+            cap = int(fr.n_isect * self.headroom) + 4096
+            self.caps.append(cap)
+            self.wss.append(torch.empty((L.gs_frame_workspace_bytes(self.n, cap, cam.width, cam.height),),
+                                        device=self.dev, dtype=torch.uint8))
+
+    def _body(self, k: int):
+        s = self.sets[k]
+        m, sc, q, o, c = s["params"]
+        g14 = s["grads"]
+        for vi, (cam, d) in enumerate(zip(self.cams, s["d_images"])):
+            fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et, capacity=self.caps[vi], check_meta=False,
+                                   ws=self.wss[vi])
+            g = ops.frame_backward(fr, m, sc, q, c, d)
+            s["meta"][vi].copy_(fr.meta())
+            parts = ((0, 3, g["d_mean"]), (3, 6, g["d_scale"]), (6, 10, g["d_quat"]), (10, 13, g["d_color"]),
+                     (13, 14, g["d_opacity"][:, None]))
+            for a, b, t in parts:
+                if vi == 0:
+                    g14[:, a:b].copy_(t)
+                else:
+                    g14[:, a:b].add_(t)
+
+    def _capture(self):
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            for k in range(self.nbuf):
+                self._body(k)  # warm-up (allocations) outside capture
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        for k in range(self.nbuf):
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self._body(k)
+            self.sets[k]["graph"] = graph
+
+    def prime(self, params, d_images):
+        """Load one step's inputs, size the capacities and capture."""
+        for k in range(self.nbuf):
+            self.load(k, params, d_images)
+        self._size(0)
+        self._capture()
+
+    # ------------------------------------------------------------- stepping
+    def load(self, k: int, params, d_images, stream=None):
+        """Copy (non-blocking from pinned host, or device) into buffer set k."""
+        s = self.sets[k]
+        with torch.cuda.stream(stream or torch.cuda.current_stream(self.dev)):
+            for dst, src in zip(s["params"], params):
+                dst.copy_(src.reshape(dst.shape), non_blocking=True)
+            for dst, src in zip(s["d_images"], d_images):
+                dst.copy_(src, non_blocking=True)
+
+    def replay(self, k: int):
+        self.sets[k]["graph"].replay()
+
+    def grads(self, k: int) -> torch.Tensor:
+        return self.sets[k]["grads"]
+
+    def meta(self, k: int) -> torch.Tensor:
+        return self.sets[k]["meta"]
+
+    def result(self, k: int, meta_host=None):
+        """Check buffer set k's last replay: raise on a status error; on a
+        capacity overflow grow the capacities, re-capture and re-run it.
+        Returns the device gradient tensor (n, 14)."""
+        m = (meta_host if meta_host is not None else self.meta(k).cpu()).tolist()
+        for status, _ in m:
+            ops.raise_status(int(status))
+        if any(total > cap for (_, total), cap in zip(m, self.caps)):
+            self._size(k)
+            self._capture()
+            self.replay(k)
+            return self.result(k)
+        return self.grads(k)
+
+    def step(self, params, d_images) -> torch.Tensor:
+        """One synchronous step (load, replay, check); returns gradients."""
+        self.load(0, params, d_images)
+        self.replay(0)
+        return self.result(0)
+
+
+def pipeline(engine: RenderStep, host_params, host_d_images, out_host, steps: int, allreduce=None, flush=None):
+    """`steps` end-to-end steps with double buffering: the H2D copies of step
+    k+1 and the D2H read of step k-1 overlap the replay of step k (copy
+    engines vs SMs).  Every step copies its inputs from pinned host memory
+    and reads its gradients (and frame metadata) back.  out_host: one pinned
+    (n, 14) tensor per buffer set.  Returns the pinned meta tensors (status,
+    intersection count per view) of the last step of each buffer set, for
+    RenderStep.result().  The caller synchronizes."""
+    dev = engine.dev
+    comp = torch.cuda.current_stream(dev)
+    h2d = torch.cuda.Stream(dev)
+    d2h = torch.cuda.Stream(dev)
+    nb = engine.nbuf
+    loaded = [torch.cuda.Event() for _ in range(nb)]
+    done = [torch.cuda.Event() for _ in range(nb)]
+    read = [torch.cuda.Event() for _ in range(nb)]
+    metas = [torch.empty((len(engine.cams), 2), dtype=torch.int64).pin_memory() for _ in range(nb)]
+    for e in read + done:
+        e.record(comp)
+    for k in range(steps):
+        b = k % nb
+        h2d.wait_event(done[b])  # the replay that last read set b finished
+        engine.load(b, host_params, host_d_images, stream=h2d)
+        loaded[b].record(h2d)
+        comp.wait_event(loaded[b])
+        comp.wait_event(read[b])  # set b's previous gradients were read back
+        if flush is not None:
+            flush.zero_()  # benchmarking: evict L2 (inputs and workspace come from HBM)
+        engine.replay(b)
+        if allreduce is not None:
+            allreduce(engine.grads(b))  # data-parallel views: sum over ranks
+        done[b].record(comp)
+        d2h.wait_event(done[b])
+        with torch.cuda.stream(d2h):
+            out_host[b].copy_(engine.grads(b), non_blocking=True)
+            metas[b].copy_(engine.meta(b), non_blocking=True)
+        read[b].record(d2h)
+    for e in read:
+        comp.wait_event(e)
+    return metas
