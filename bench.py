@@ -163,6 +163,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2312_02121_b200 import _lib, ops
+    from paper_2312_02121_b200 import engine as E
     from paper_2312_02121_b200.scenes import config_sizes, make_config
 
     world, rank, local = dist_env()
@@ -194,7 +195,7 @@ def run_ours(args):
         del proj
     bg = (0.0, 0.0, 0.0)
     flush = torch.empty(L2_FLUSH_BYTES // 4, device=dev, dtype=torch.float32)
-    grad_flat = torch.zeros((n, 14), device=dev, dtype=torch.float32)
+    grad_flat = torch.zeros((14 * n,), device=dev, dtype=torch.float32)
     L = _lib.load()
 
     # per-view static capacity + workspace (one checked run each), and the
@@ -224,22 +225,16 @@ def run_ours(args):
     ev_b = [mk_events(3) for _ in cams]
     frames_out = [None] * len(cams)
 
+    grad_out = E.unpack(grad_flat, n)
+
     def step():
+        # every view writes (first) or accumulates (others) straight into
+        # the flat gradient buffer that the multi-GPU all-reduce sums
         for vi, (cam, d_img) in enumerate(zip(cams, d_imgs)):
             fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, capacity=caps[vi], check_meta=False, ws=wss[vi],
                                    events=ev_f[vi])
-            g = ops.frame_backward(fr, m, s, q, c, d_img, events=ev_b[vi])
+            ops.frame_backward(fr, m, s, q, c, d_img, events=ev_b[vi], out=grad_out, accumulate=vi > 0)
             frames_out[vi] = fr
-            if vi == 0:
-                grad_flat[:, 0:3].copy_(g["d_mean"])
-                grad_flat[:, 3:6].copy_(g["d_scale"])
-                grad_flat[:, 6:10].copy_(g["d_quat"])
-                grad_flat[:, 10:14].copy_(g["d_rgbo"])
-            else:
-                grad_flat[:, 0:3].add_(g["d_mean"])
-                grad_flat[:, 3:6].add_(g["d_scale"])
-                grad_flat[:, 6:10].add_(g["d_quat"])
-                grad_flat[:, 10:14].add_(g["d_rgbo"])
 
     graph = None
     if not args.no_graph:
@@ -431,7 +426,7 @@ def run_e2e(args, spec, views, dev, world, frames):
     cams = [c for c, _ in views]
     eng = E.RenderStep(spec.n, cams, device=dev)
     eng.prime(host, dimgs)
-    out_host = [torch.empty((spec.n, 14), dtype=torch.float32).pin_memory() for _ in range(eng.nbuf)]
+    out_host = [torch.empty((14 * spec.n,), dtype=torch.float32).pin_memory() for _ in range(eng.nbuf)]
     h2d = sum(h.numel() * 4 for h in host) + sum(d.numel() * 4 for d in dimgs)
     d2h = out_host[0].numel() * 4 + len(cams) * 16
     allreduce = (lambda g: dist.all_reduce(g)) if world > 1 else None

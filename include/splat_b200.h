@@ -190,13 +190,17 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
  * on `stream` at stage boundaries, for live per-stage timing.
  *   forward : [0] start [1] projected [2] depth-sorted [3] emitted [4] tile-sorted+ranges [5] rastered
  *   backward: [0] start [1] raster backward done [2] projection backward done
- * d_rgbo4 (n,4) = d_color r,g,b, d_opacity (overwritten); d_view16 4x4. */
+ * d_rgbo4 (n,4) = d_color r,g,b, d_opacity; d_view16 4x4 (always written).
+ * accumulate == 0: d_means3 / d_scales3 / d_quats4 / d_rgbo4 are
+ * overwritten; != 0: this view's gradients are ADDED to them (sum over the
+ * views of a step without extra kernels, sg/proj_backward.py:178-223 summed
+ * per camera). */
 int gs_frame_backward(const float* means3, const float* scales3, const float* quats4, const float* colors3,
                       int64_t n, const gs_camera* cam /*[host]*/, const float* background3 /*[host]*/,
                       int64_t isect_capacity, void* ws, size_t ws_bytes, const float* final_T,
                       const int32_t* n_contrib, const float* d_image, float* d_means3, float* d_scales3,
-                      float* d_quats4, float* d_rgbo4, float* d_view16, unsigned long long* counts3,
-                      void* const* stage_events, gs_stream_t stream);
+                      float* d_quats4, float* d_rgbo4, float* d_view16, int accumulate,
+                      unsigned long long* counts3, void* const* stage_events, gs_stream_t stream);
 
 /* ---- Training step around the path (sg/optimize.py:96-190 fit) ----------
  * gs_activate : scales = exp(log_scales), opacities = sigmoid(logits)  (:144-145)

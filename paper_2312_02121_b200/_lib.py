@@ -83,8 +83,8 @@ def load():
         "gs_frame_view_of": ([i64, i64, i32, i32, P, C.POINTER(GsFrameView)], C.c_int),
         "gs_frame_forward": ([P, P, P, P, P, i64, cam, C.POINTER(C.c_float), C.c_int, i64, P, sz, P, P, P, P, P,
                               P], C.c_int),
-        "gs_frame_backward": ([P, P, P, P, i64, cam, C.POINTER(C.c_float), i64, P, sz, P, P, P, P, P, P, P, P, P,
-                               P, P], C.c_int),
+        "gs_frame_backward": ([P, P, P, P, i64, cam, C.POINTER(C.c_float), i64, P, sz, P, P, P, P, P, P, P, P,
+                               C.c_int, P, P, P], C.c_int),
     }
     f32 = C.c_float
     sig.update({

@@ -203,7 +203,7 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
                       int64_t n, const gs_camera* cam, const float* background3, int64_t isect_capacity, void* ws,
                       size_t ws_bytes, const float* final_T, const int32_t* n_contrib, const float* d_image,
                       float* d_means3, float* d_scales3, float* d_quats4, float* d_rgbo4, float* d_view16,
-                      unsigned long long* counts3, void* const* stage_events, gs_stream_t stream) {
+                      int accumulate, unsigned long long* counts3, void* const* stage_events, gs_stream_t stream) {
     if (!cam || !background3) return set_error("gs_frame_backward: null camera/background");
     const int W = cam->width, H = cam->height;
     const Layout L = layout(n, isect_capacity, W, H);
@@ -216,7 +216,7 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
     const uint32_t* svals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
     mark(stage_events, 0, s);
     if (n > 0) {
-        if (cudaMemsetAsync(d_rgbo4, 0, 16 * (size_t)n, s) != cudaSuccess ||
+        if ((!accumulate && cudaMemsetAsync(d_rgbo4, 0, 16 * (size_t)n, s) != cudaSuccess) ||
             cudaMemsetAsync(at<char>(ws, L.d_geo), 0, L.partials - L.d_geo, s) != cudaSuccess)
             return check_launch("backward memset");
     }
@@ -228,7 +228,7 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
     mark(stage_events, 1, s);
     if (launch_project_bwd(means3, scales3, quats4, n, k, at<uint32_t>(ws, L.tiles), at<float>(ws, L.d_geo),
                            at<float>(ws, L.d_c11), d_means3, d_scales3, d_quats4, d_view16, at<float>(ws, L.partials),
-                           s))
+                           s, accumulate != 0))
         return -1;
     mark(stage_events, 2, s);
     return 0;

@@ -15,7 +15,8 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
                             unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s);
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
-                       float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s);
+                       float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
+                       bool accumulate = false);
 constexpr int PBWD_BLOCK = 256;
 
 // sort.cu

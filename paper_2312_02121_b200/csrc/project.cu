@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
     int n, CamK cam, const uint32_t* __restrict__ tiles, const float4* __restrict__ d_geo,
     const float* __restrict__ d_c11, float* __restrict__ d_means, float* __restrict__ d_scales,
-    float4* __restrict__ d_quats, float* __restrict__ view_partials) {
+    float4* __restrict__ d_quats, float* __restrict__ view_partials, bool accumulate) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     float dv[12];
 #pragma unroll
@@ -273,9 +273,16 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
             dq = make_float4((gw - qw * dot) * inv, (gxq - qx * dot) * inv, (gyq - qy * dot) * inv,
                              (gzq - qz * dot) * inv);
         }
-        d_means[3 * i] = dmx; d_means[3 * i + 1] = dmy; d_means[3 * i + 2] = dmz;
-        d_scales[3 * i] = dsx; d_scales[3 * i + 1] = dsy; d_scales[3 * i + 2] = dsz;
-        d_quats[i] = dq;
+        if (accumulate) {  // sum over views into the caller's gradient
+            d_means[3 * i] += dmx; d_means[3 * i + 1] += dmy; d_means[3 * i + 2] += dmz;
+            d_scales[3 * i] += dsx; d_scales[3 * i + 1] += dsy; d_scales[3 * i + 2] += dsz;
+            const float4 o = d_quats[i];
+            d_quats[i] = make_float4(o.x + dq.x, o.y + dq.y, o.z + dq.z, o.w + dq.w);
+        } else {
+            d_means[3 * i] = dmx; d_means[3 * i + 1] = dmy; d_means[3 * i + 2] = dmz;
+            d_scales[3 * i] = dsx; d_scales[3 * i + 1] = dsy; d_scales[3 * i + 2] = dsz;
+            d_quats[i] = dq;
+        }
     }
     // block partial of d_view (deterministic: fixed shuffle tree + fixed warp order)
     __shared__ float red[PBWD_THREADS / 32][12];
@@ -324,12 +331,13 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
 
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
-                       float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s) {
+                       float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
+                       bool accumulate) {
     const int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
     if (blocks > 0) {
         project_bwd_kernel<<<blocks, PBWD_THREADS, 0, s>>>(means3, scales3, (const float4*)quats4, (int)n, k, tiles,
                                                           (const float4*)d_geo4, d_c11, d_means3, d_scales3,
-                                                          (float4*)d_quats4, partials);
+                                                          (float4*)d_quats4, partials, accumulate);
         if (check_launch("project_bwd_kernel")) return -1;
     }
     view_reduce_kernel<<<1, 384, 0, s>>>(partials, blocks, d_view16);
@@ -373,7 +381,7 @@ int gs_project_bwd(const float* means3, const float* scales3, const float* quats
     if (blocks > 0) {
         project_bwd_kernel<<<blocks, PBWD_THREADS, 0, (cudaStream_t)stream>>>(
             means3, scales3, (const float4*)quats4, (int)n, k, tiles, (const float4*)d_geo4, d_c11, d_means3,
-            d_scales3, (float4*)d_quats4, (float*)ws);
+            d_scales3, (float4*)d_quats4, (float*)ws, false);
         if (check_launch("project_bwd_kernel")) return -1;
     }
     view_reduce_kernel<<<1, 384, 0, (cudaStream_t)stream>>>((const float*)ws, blocks, d_view16);

@@ -8,8 +8,11 @@ gs_frame_backward for every view, gradients summed over views) once per
 buffer set and replays it:
 
   * static device buffers for the parameters, the upstream image gradients
-    and the 14 gradients per Gaussian (mean 3 | scale 3 | quat 4 | colour 3
-    | opacity 1 -- the SceneGradients fields, sg/proj_backward.py:25-50);
+    and the 14 gradients per Gaussian, one flat buffer of contiguous blocks
+    d_mean (n,3) | d_scale (n,3) | d_quat (n,4) | d_rgbo (n,4) (colour 3,
+    opacity 1) -- the SceneGradients fields, sg/proj_backward.py:25-50 --
+    that gs_frame_backward writes (first view) or accumulates into (the
+    others) directly;
   * two buffer sets, so the host<->device copies of one step overlap the
     replay of the other (``pipeline``);
   * the per-view intersection capacity comes from one checked frame; every
@@ -23,6 +26,17 @@ from __future__ import annotations
 import torch
 
 from . import _lib, ops
+
+
+def unpack(flat: torch.Tensor, n: int) -> dict:
+    """Views of a flat (14 n) gradient buffer: d_mean (n,3), d_scale (n,3),
+    d_quat (n,4), d_rgbo (n,4), d_color (n,3), d_opacity (n)."""
+    d_mean = flat[0:3 * n].view(n, 3)
+    d_scale = flat[3 * n:6 * n].view(n, 3)
+    d_quat = flat[6 * n:10 * n].view(n, 4)
+    d_rgbo = flat[10 * n:14 * n].view(n, 4)
+    return dict(d_mean=d_mean, d_scale=d_scale, d_quat=d_quat, d_rgbo=d_rgbo, d_color=d_rgbo[:, :3],
+                d_opacity=d_rgbo[:, 3])
 
 
 class RenderStep:
@@ -41,7 +55,7 @@ class RenderStep:
             self.sets.append(dict(
                 params=[z(n, 3), z(n, 3), z(n, 4), z(n), z(n, 3)],
                 d_images=[z(c.height, c.width, 3) for c in self.cams],
-                grads=z(n, 14),
+                grads=z(14 * n),
                 meta=torch.zeros((len(self.cams), 2), device=self.dev, dtype=torch.int64),
                 graph=None))
         self.caps = None
@@ -64,19 +78,12 @@ class RenderStep:
     def _body(self, k: int):
         s = self.sets[k]
         m, sc, q, o, c = s["params"]
-        g14 = s["grads"]
+        out = unpack(s["grads"], self.n)
         for vi, (cam, d) in enumerate(zip(self.cams, s["d_images"])):
             fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et, capacity=self.caps[vi], check_meta=False,
                                    ws=self.wss[vi])
-            g = ops.frame_backward(fr, m, sc, q, c, d)
+            ops.frame_backward(fr, m, sc, q, c, d, out=out, accumulate=vi > 0)
             s["meta"][vi].copy_(fr.meta())
-            parts = ((0, 3, g["d_mean"]), (3, 6, g["d_scale"]), (6, 10, g["d_quat"]), (10, 13, g["d_color"]),
-                     (13, 14, g["d_opacity"][:, None]))
-            for a, b, t in parts:
-                if vi == 0:
-                    g14[:, a:b].copy_(t)
-                else:
-                    g14[:, a:b].add_(t)
 
     def _capture(self):
         side = torch.cuda.Stream(self.dev)
@@ -120,7 +127,7 @@ class RenderStep:
     def result(self, k: int, meta_host=None):
         """Check buffer set k's last replay: raise on a status error; on a
         capacity overflow grow the capacities, re-capture and re-run it.
-        Returns the device gradient tensor (n, 14)."""
+        Returns the flat device gradient buffer (see unpack)."""
         m = (meta_host if meta_host is not None else self.meta(k).cpu()).tolist()
         for status, _ in m:
             ops.raise_status(int(status))
@@ -143,7 +150,7 @@ def pipeline(engine: RenderStep, host_params, host_d_images, out_host, steps: in
     k+1 and the D2H read of step k-1 overlap the replay of step k (copy
     engines vs SMs).  Every step copies its inputs from pinned host memory
     and reads its gradients (and frame metadata) back.  out_host: one pinned
-    (n, 14) tensor per buffer set.  Returns the pinned meta tensors (status,
+    (14 n) tensor per buffer set.  Returns the pinned meta tensors (status,
     intersection count per view) of the last step of each buffer set, for
     RenderStep.result().  The caller synchronizes."""
     dev = engine.dev

@@ -450,8 +450,12 @@ def _event_array(events):
     return arr
 
 
-def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=False, events=None):
-    """gs_frame_backward: the SceneGradients fields (sg/proj_backward.py:25-50)."""
+def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=False, events=None, out=None,
+                   accumulate=False):
+    """gs_frame_backward: the SceneGradients fields (sg/proj_backward.py:25-50).
+    out: optional dict of contiguous output tensors d_mean (n,3), d_scale
+    (n,3), d_quat (n,4), d_rgbo (n,4) to write (accumulate=False) or add
+    this view's gradients into (accumulate=True)."""
     L = _lib.load()
     H, W = fr.cam.height, fr.cam.width
     if tuple(d_image.shape) != (H, W, 3):
@@ -459,10 +463,18 @@ def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=F
     d_image = d_image.contiguous().to(torch.float32)
     n = fr.n
     dev = means.device
-    d_means = torch.empty((n, 3), device=dev, dtype=torch.float32)
-    d_scales = torch.empty((n, 3), device=dev, dtype=torch.float32)
-    d_quats = torch.empty((n, 4), device=dev, dtype=torch.float32)
-    d_rgbo = torch.empty((n, 4), device=dev, dtype=torch.float32)
+    if out is not None:
+        d_means, d_scales, d_quats, d_rgbo = out["d_mean"], out["d_scale"], out["d_quat"], out["d_rgbo"]
+        for t, cols in ((d_means, 3), (d_scales, 3), (d_quats, 4), (d_rgbo, 4)):
+            if t.shape != (n, cols) or not t.is_contiguous() or t.dtype != torch.float32:
+                raise ValueError("frame_backward: out tensors must be contiguous float32 (n, 3|3|4|4)")
+    else:
+        if accumulate:
+            raise ValueError("frame_backward: accumulate needs out tensors")
+        d_means = torch.empty((n, 3), device=dev, dtype=torch.float32)
+        d_scales = torch.empty((n, 3), device=dev, dtype=torch.float32)
+        d_quats = torch.empty((n, 4), device=dev, dtype=torch.float32)
+        d_rgbo = torch.empty((n, 4), device=dev, dtype=torch.float32)
     d_view = torch.empty((4, 4), device=dev, dtype=torch.float32)
     cnt = torch.zeros((3,), device=dev, dtype=torch.int64) if counts else None
     camc = fr.cam.c()
@@ -470,7 +482,8 @@ def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=F
     check(L.gs_frame_backward(_ptr(means), _ptr(scales), _ptr(quats), _ptr(colors), n, C.byref(camc), bg,
                               fr.capacity, _ptr(fr.ws), fr.ws.numel(), _ptr(fr.final_T), _ptr(fr.n_contrib),
                               _ptr(d_image), _ptr(d_means), _ptr(d_scales), _ptr(d_quats), _ptr(d_rgbo),
-                              _ptr(d_view), _ptr(cnt), _event_array(events), _stream()), "gs_frame_backward")
+                              _ptr(d_view), 1 if accumulate else 0, _ptr(cnt), _event_array(events), _stream()),
+          "gs_frame_backward")
     return dict(d_mean=d_means, d_scale=d_scales, d_quat=d_quats, d_opacity=d_rgbo[:, 3], d_color=d_rgbo[:, :3],
                 d_view=d_view, d_rgbo=d_rgbo, counts=cnt)
 

@@ -14,13 +14,16 @@ pytestmark = pytest.mark.gpu
 def _per_call(ops, params, cam, d_image):
     fr = ops.frame_forward(*params, cam, (0.0, 0.0, 0.0), True)
     g = ops.frame_backward(fr, params[0], params[1], params[2], params[4], d_image)
-    return torch.cat([g["d_mean"], g["d_scale"], g["d_quat"], g["d_color"], g["d_opacity"][:, None]], 1)
+    return torch.cat([g["d_mean"].reshape(-1), g["d_scale"].reshape(-1), g["d_quat"].reshape(-1),
+                      g["d_rgbo"].reshape(-1)])
 
 
 def _close(a, b):
     a, b = a.cpu().numpy().astype(np.float64), b.cpu().numpy().astype(np.float64)
-    scale = np.abs(b).max(axis=0) + 1e-30
-    assert np.max(np.abs(a - b) / scale) < 1e-4  # atomic summation order only
+    n = len(a) // 14
+    for lo, hi in ((0, 3 * n), (3 * n, 6 * n), (6 * n, 10 * n), (10 * n, 14 * n)):  # per gradient class
+        scale = np.abs(b[lo:hi]).max() + 1e-30
+        assert np.max(np.abs(a[lo:hi] - b[lo:hi])) / scale < 1e-4  # atomic summation order only
 
 
 def test_step_and_pipeline_match_per_call(cuda):
@@ -38,7 +41,7 @@ def test_step_and_pipeline_match_per_call(cuda):
 
     host = [p.cpu().pin_memory() for p in params]
     dh = [d_image.cpu().pin_memory()]
-    out = [torch.empty((len(params[0]), 14)).pin_memory() for _ in range(eng.nbuf)]
+    out = [torch.empty((14 * len(params[0]),)).pin_memory() for _ in range(eng.nbuf)]
     metas = E.pipeline(eng, host, dh, out, 5)
     torch.cuda.synchronize()
     for b, mh in enumerate(metas):
@@ -74,3 +77,21 @@ def test_step_raises_reference_errors(cuda):
     bad[1].neg_()  # non-positive scales (sg/core.py:189-191)
     with pytest.raises(ValueError, match="scale"):
         eng.step(bad, [d_image])
+
+
+def test_multi_view_accumulation(cuda):
+    """Two views in one step: the accumulate path equals the sum of the
+    per-call gradients of each view."""
+    from paper_2312_02121_b200 import engine as E, ops
+    g = load_golden("config0")
+    params = [torch.as_tensor(np.asarray(a, np.float32), device=cuda) for a in g["inputs"]]
+    cam = ops.CameraParams.of(g["camera"])
+    cam2 = ops.CameraParams(cam.view, cam.fx * 1.1, cam.fy * 1.1, cam.cx, cam.cy, cam.width, cam.height, cam.near,
+                            cam.far)
+    rng = np.random.default_rng(1)
+    d1 = torch.as_tensor(rng.normal(size=(cam.height, cam.width, 3)).astype(np.float32), device=cuda)
+    d2 = torch.as_tensor(rng.normal(size=(cam.height, cam.width, 3)).astype(np.float32), device=cuda)
+    ref = _per_call(ops, params, cam, d1) + _per_call(ops, params, cam2, d2)
+    eng = E.RenderStep(len(params[0]), [cam, cam2], device=cuda)
+    eng.prime(params, [d1, d2])
+    _close(eng.step(params, [d1, d2]), ref)
