@@ -192,14 +192,27 @@ __global__ void __launch_bounds__(SORT_THREADS, sizeof(K) == 4 ? 3 : 2) onesweep
         stv(st, ST_PRE | run);
     } else {
         stv(st, ST_AGG | run);
+        // decoupled look-back over windows of LB predecessors: the LB status
+        // loads of a window are in flight together (one L2 round trip per
+        // window instead of per predecessor); a not-yet-posted entry is
+        // re-polled in place
+        constexpr int LB = 8;
         int p = (int)tile - 1;
-        while (true) {
-            const uint32_t s = ldv(status + (size_t)p * RADIX + d);
-            const uint32_t f = s & ~ST_MASK;
-            if (f == 0) continue;
-            excl += s & ST_MASK;
-            if (f == ST_PRE) break;
-            --p;
+        bool found = false;
+        while (!found) {
+            uint32_t w[LB];
+#pragma unroll
+            for (int j = 0; j < LB; ++j) w[j] = p - j >= 0 ? ldv(status + (size_t)(p - j) * RADIX + d) : ST_PRE;
+#pragma unroll
+            for (int j = 0; j < LB; ++j) {
+                if (!found) {
+                    uint32_t v = w[j];
+                    while ((v & ~ST_MASK) == 0) v = ldv(status + (size_t)(p - j) * RADIX + d);
+                    excl += v & ST_MASK;
+                    found = (v & ~ST_MASK) == ST_PRE;
+                }
+            }
+            p -= LB;
         }
         stv(st, ST_PRE | (excl + run));
     }
@@ -318,7 +331,13 @@ int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const 
     if (n_cap <= 0) return 0;
     constexpr int BIG = SortCfg<K>::ITEMS;
     const int64_t big_tiles = (n_cap + sort_tile<K, BIG>() - 1) / sort_tile<K, BIG>();
-    if (big_tiles < 64)
+    static int small_env = -2;
+    if (small_env == -2) {
+        const char* e = getenv("GS_SORT_SMALL");
+        small_env = e ? atoi(e) : -1;
+    }
+    const bool small = small_env >= 0 ? small_env != 0 : big_tiles < 64;
+    if (small)
         return run_passes<K, SMALL_ITEMS>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s,
                                           identity_vals);
     return run_passes<K, BIG>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
