@@ -258,6 +258,58 @@ int gs_composite_pixels_bwd(const float* xydr4, const float* conic4, const float
                             const float* d_pixels3, float* d_rgbo4, float* d_geo4, float* d_c11, float* t_log,
                             gs_stream_t stream);
 
+/* ---- The path in float64 --------------------------
+ * For the reference's finite-difference audit (sg/gradcheck.py) and fp64
+ * parity: the same stages with every value in double, each following the
+ * reference's expression order.  Host-synchronous in one place (the caller
+ * reads the intersection total after gs_bin64_count).
+ *
+ * gs_project64     sg/projection.py:115-145 per Gaussian: mean2d (n,2),
+ *                  cov3 (n,3) = (a, b, c), depth, radius, tiles touched
+ *                  (0 = culled), depth sort key; errors into *status as
+ *                  gs_project_fwd.
+ * gs_bin64_count   exclusive scan of tiles -> *out_total (device uint64).
+ * gs_bin64_sort    sg/binning.py:27-65: (depth, source_index) order, then
+ *                  per-tile lists (ranges2 (n_tiles,2) + *out_vals pointing
+ *                  into ws) -- same ws as gs_bin64_count, sized by
+ *                  gs_bin64_workspace_bytes(n, n_isect, n_tiles).
+ * gs_raster64_fwd  sg/raster_forward.py:116-172 (thread per pixel).
+ * gs_raster64_bwd  sg/raster_backward.py:47-108,166-205: d9 (n,9) zeroed,
+ *                  accumulates d_color 3, d_opacity, d_mean2d 2, d_cov2d
+ *                  00, 01 (= 10), 11 per Gaussian.
+ * gs_project64_bwd sg/proj_backward.py:178-223 (d_view16 fixed order).     */
+typedef struct gs_camera64 {
+    double view[16];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double near_plane, far_plane;
+} gs_camera64;
+
+int gs_project64(const double* means3, const double* scales3, const double* quats4, int64_t n,
+                 const gs_camera64* cam /*[host]*/, double* out_mean2d, double* out_cov3, double* out_depth,
+                 int32_t* out_radius, uint32_t* out_tiles, unsigned long long* out_dkeys,
+                 unsigned long long* status, gs_stream_t stream);
+size_t gs_bin64_workspace_bytes(int64_t n, int64_t n_isect, int32_t n_tiles);
+int gs_bin64_count(const uint32_t* tiles, int64_t n, void* ws, size_t ws_bytes, unsigned long long* out_total,
+                   gs_stream_t stream);
+int gs_bin64_sort(const double* mean2d, const int32_t* radius, const uint32_t* tiles,
+                  const unsigned long long* dkeys, int64_t n, int64_t n_isect, int32_t width, int32_t height,
+                  void* ws, size_t ws_bytes, uint32_t* out_ranges2, const uint32_t** out_vals /*[host]*/,
+                  gs_stream_t stream);
+int gs_raster64_fwd(const uint32_t* ranges2, const uint32_t* vals, const double* mean2d, const double* cov3,
+                    const double* opacities, const double* colors3, const double* background3 /*[host]*/,
+                    int32_t width, int32_t height, int early_termination, double* out_image, double* out_final_T,
+                    int32_t* out_n_contrib, gs_stream_t stream);
+int gs_raster64_bwd(const uint32_t* ranges2, const uint32_t* vals, const double* mean2d, const double* cov3,
+                    const double* opacities, const double* colors3, const double* background3 /*[host]*/,
+                    int32_t width, int32_t height, const double* final_T, const int32_t* n_contrib,
+                    const double* d_image, double* d9, gs_stream_t stream);
+size_t gs_project64_bwd_workspace_bytes(int64_t n);
+int gs_project64_bwd(const double* means3, const double* scales3, const double* quats4, int64_t n,
+                     const gs_camera64* cam /*[host]*/, const uint32_t* tiles, const double* d9, double* d_means3,
+                     double* d_scales3, double* d_quats4, double* d_view16, void* ws, size_t ws_bytes,
+                     gs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,8 @@ EXPORTS = (
     "gs_frame_workspace_bytes", "gs_frame_view_of", "gs_frame_forward", "gs_frame_backward",
     "gs_activate", "gs_loss_l2", "gs_adam_step",
     "gs_conic_from_cov", "gs_eval_alpha", "gs_composite_pixels", "gs_composite_pixels_bwd",
+    "gs_project64", "gs_bin64_workspace_bytes", "gs_bin64_count", "gs_bin64_sort", "gs_raster64_fwd",
+    "gs_raster64_bwd", "gs_project64_bwd_workspace_bytes", "gs_project64_bwd",
 )
 
 ERR_MESSAGES = {  # include/splat_b200.h gs_error_code -> the reference's ValueError text
@@ -36,6 +38,12 @@ class GsCamera(C.Structure):
     _fields_ = [("view", C.c_float * 16), ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float),
                 ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
                 ("near_plane", C.c_float), ("far_plane", C.c_float)]
+
+
+class GsCamera64(C.Structure):
+    _fields_ = [("view", C.c_double * 16), ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double),
+                ("cy", C.c_double), ("width", C.c_int32), ("height", C.c_int32),
+                ("near_plane", C.c_double), ("far_plane", C.c_double)]
 
 
 class GsFrameView(C.Structure):
@@ -97,6 +105,19 @@ def load():
         "gs_composite_pixels": ([P, P, P, P, P, P, i64, C.POINTER(f32), C.c_int, P, P, P, P], C.c_int),
         "gs_composite_pixels_bwd": ([P, P, P, P, P, P, i64, C.POINTER(f32), P, P, P, P, P, P, P, P], C.c_int),
     })
+    cam64 = C.POINTER(GsCamera64)
+    f64p = C.POINTER(C.c_double)
+    sig.update({
+        "gs_project64": ([P, P, P, i64, cam64, P, P, P, P, P, P, P, P], C.c_int),
+        "gs_bin64_workspace_bytes": ([i64, i64, C.c_int32], C.c_size_t),
+        "gs_bin64_count": ([P, i64, P, C.c_size_t, P, P], C.c_int),
+        "gs_bin64_sort": ([P, P, P, P, i64, i64, C.c_int32, C.c_int32, P, C.c_size_t, P,
+                           C.POINTER(C.c_void_p), P], C.c_int),
+        "gs_raster64_fwd": ([P, P, P, P, P, P, f64p, C.c_int32, C.c_int32, C.c_int, P, P, P, P], C.c_int),
+        "gs_raster64_bwd": ([P, P, P, P, P, P, f64p, C.c_int32, C.c_int32, P, P, P, P, P], C.c_int),
+        "gs_project64_bwd_workspace_bytes": ([i64], C.c_size_t),
+        "gs_project64_bwd": ([P, P, P, i64, cam64, P, P, P, P, P, P, P, C.c_size_t, P], C.c_int),
+    })
     for name, (args, res) in sig.items():
         f = getattr(L, name)
         f.argtypes = args
@@ -109,6 +130,19 @@ def check(rc: int, what: str = "") -> None:
     if rc != 0:
         msg = load().gs_last_error().decode(errors="replace")
         raise SplatLibError(f"{what}: {msg}" if what else msg)
+
+
+def make_camera64(view, fx, fy, cx, cy, width, height, near, far) -> GsCamera64:
+    c = GsCamera64()
+    flat = [float(v) for row in view for v in row] if hasattr(view[0], "__len__") else [float(v) for v in view]
+    if len(flat) != 16:
+        raise ValueError("view must have shape (4, 4)")
+    for k in range(16):
+        c.view[k] = flat[k]
+    c.fx, c.fy, c.cx, c.cy = float(fx), float(fy), float(cx), float(cy)
+    c.width, c.height = int(width), int(height)
+    c.near_plane, c.far_plane = float(near), float(far)
+    return c
 
 
 def make_camera(view, fx, fy, cx, cy, width, height, near, far) -> GsCamera:

@@ -300,6 +300,12 @@ int launch_emit_sorted(const uint32_t* order, const float* xydr4, const uint32_t
     return check_launch("emit_sorted_kernel");
 }
 
+int launch_ranges_u64(const unsigned long long* sorted_keys, int64_t n, uint2* ranges, cudaStream_t s) {
+    if (n == 0) return 0;
+    ranges_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sorted_keys, n, ranges);
+    return check_launch("ranges_kernel");
+}
+
 int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const unsigned long long* n_dev,
                       uint2* ranges, cudaStream_t s) {
     if (n_cap == 0) return 0;

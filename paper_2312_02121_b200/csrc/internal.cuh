@@ -38,6 +38,8 @@ int launch_scan(const uint32_t* in, const uint32_t* gather, uint32_t* out, int64
 int launch_emit_sorted(const uint32_t* order, const float* xydr4, const uint32_t* offsets, int64_t n,
                        int tiles_x, int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals,
                        uint32_t* tile_hist, int tile_passes, cudaStream_t s);
+int launch_ranges_u64(const unsigned long long* sorted_keys, int64_t n, uint2* ranges,
+                      cudaStream_t s);  // ranges must be zeroed
 int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const unsigned long long* n_dev,
                       uint2* ranges, cudaStream_t s);  // ranges must be zeroed
 
