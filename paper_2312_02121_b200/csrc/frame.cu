@@ -36,7 +36,7 @@ int tile_passes_for(int n_tiles) { return n_tiles <= 256 ? 1 : 2; }
 struct Layout {
     // persistent (written each frame)
     size_t xydr, conic, tiles, dkeys, dkeys_alt, order, order_alt, offsets;
-    size_t tkeys, tkeys_alt, tvals, tvals_alt, ranges;
+    size_t tkeys, tkeys_alt, tvals, tvals_alt, ranges, rec, rec_count;
     // zeroed region
     size_t zero_begin, meta, dhist, thist, counters, scan_ws, dstatus, tstatus, zero_end;
     // backward
@@ -67,6 +67,8 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.tvals = take(4 * cap);
     L.tvals_alt = take(4 * cap);
     L.ranges = take(8 * nt);
+    L.rec = take(8 * 4 * cap);    // forward commit records, 4 warp regions per tile list
+    L.rec_count = take(16 * nt);  // records per (tile, warp)
     L.zero_begin = o;
     L.meta = take(16);
     L.dhist = take(4 * 256 * 4);
@@ -193,7 +195,8 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     // 7. raster forward
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
     if (launch_raster_fwd(at<uint2>(ws, L.ranges), svals, at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3,
-                          bg, W, H, early_termination != 0, out_image, out_final_T, out_n_contrib, counts4, s))
+                          bg, W, H, early_termination != 0, out_image, out_final_T, out_n_contrib, counts4, s,
+                          at<uint2>(ws, L.rec), at<uint32_t>(ws, L.rec_count)))
         return -1;
     mark(stage_events, 5, s);
     return 0;
@@ -221,10 +224,17 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
             return check_launch("backward memset");
     }
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
-    if (launch_raster_bwd(at<uint2>(ws, L.ranges), svals, at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3,
-                          bg, W, H, final_T, n_contrib, d_image, d_rgbo4, at<float>(ws, L.d_geo),
-                          at<float>(ws, L.d_c11), counts3, s))
+    if (counts3) {  // counted pass (roofline numerators): the list-walking backward counts evaluations
+        if (launch_raster_bwd(at<uint2>(ws, L.ranges), svals, at<float>(ws, L.xydr), at<float>(ws, L.conic),
+                              colors3, bg, W, H, final_T, n_contrib, d_image, d_rgbo4, at<float>(ws, L.d_geo),
+                              at<float>(ws, L.d_c11), counts3, s))
+            return -1;
+    } else if (launch_raster_bwd_rec(at<uint2>(ws, L.ranges), at<uint2>(ws, L.rec), at<uint32_t>(ws, L.rec_count),
+                                     at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3, bg, W, H, final_T,
+                                     n_contrib, d_image, d_rgbo4, at<float>(ws, L.d_geo), at<float>(ws, L.d_c11),
+                                     s)) {
         return -1;
+    }
     mark(stage_events, 1, s);
     if (launch_project_bwd(means3, scales3, quats4, n, k, at<uint32_t>(ws, L.tiles), at<float>(ws, L.d_geo),
                            at<float>(ws, L.d_c11), d_means3, d_scales3, d_quats4, d_view16, at<float>(ws, L.partials),

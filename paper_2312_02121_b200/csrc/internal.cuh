@@ -46,7 +46,13 @@ int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const uns
 // raster.cu
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
-                      unsigned long long* counts, cudaStream_t s);
+                      unsigned long long* counts, cudaStream_t s, uint2* rec = nullptr,
+                      uint32_t* rec_count = nullptr);
+// record-driven backward of the frame path (records written by the forward)
+int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
+                          const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
+                          const int* nc, const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11,
+                          cudaStream_t s);
 int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, const float* fT, const int* nc,
                       const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11, unsigned long long* counts,

@@ -164,20 +164,33 @@ __device__ __forceinline__ void fwd_commit(FwdPair& p, f32x2 SG, bool vis0, bool
     }
 }
 
+// Record of one (warp, list entry) for the backward: the splat id and its
+// 0-based position in the tile list, written for every entry whose commit
+// step this warp ran (some pixel of the quadrant passed the sigma cut) --
+// a warp-uniform condition the forward already has, so recording costs no
+// extra vote.  The backward replays exactly these entries, back to front.
+__device__ __forceinline__ void fwd_record(uint2*& rp, uint32_t id, int pos0) {
+    if ((threadIdx.x & 31) == 0) *rp = make_uint2(id, (uint32_t)pos0);
+    ++rp;
+}
+
 // sg/raster_forward.py:116-154 _composite_tile for one tile.
 // NWR = 4: 128 threads, one pixel pair per lane, two list entries per
 // iteration (independent sigma chains); NWR = 2: 64 threads, two pixel pairs
 // per lane (8x16 halves), one entry per iteration.
-template <int NWR, bool ET, bool COUNT>
-__global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 10 : 16) raster_fwd_kernel(const uint2* __restrict__ ranges,
+template <int NWR, bool ET, bool COUNT, bool REC, int MINB = (NWR == 4 ? 10 : 16)>
+__global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2* __restrict__ ranges,
                                                               const uint32_t* __restrict__ sorted_vals,
                                                               const float4* __restrict__ xydr,
                                                               const float4* __restrict__ conic,
                                                               const float* __restrict__ colors, float3 bg, int W,
                                                               int H, int tiles_x, float* __restrict__ out_img,
                                                               float* __restrict__ out_T, int* __restrict__ out_nc,
-                                                              unsigned long long* __restrict__ counts) {
+                                                              unsigned long long* __restrict__ counts,
+                                                              uint2* __restrict__ rec,
+                                                              uint32_t* __restrict__ rec_count) {
     constexpr int NPR = 4 / NWR;
+    static_assert(!REC || NWR == 4, "records are per 8x8 quadrant");
     __shared__ BatchT<NWR> s;
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -209,6 +222,8 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 10 : 16) raster_fwd_kerne
     const uint2 rg = ranges[tile];
     const int start = (int)rg.x, end = (int)rg.y;
     unsigned long long e_s = 0, e_a = 0, e_c = 0;
+    // this warp's record region: 4 * start + warp * len (no atomics)
+    uint2* rp = REC ? rec + 4 * (int64_t)start + (int64_t)warp * (end - start) : nullptr;
     if (threadIdx.x == 0) {  // sentinel entry: dx = -inf -> sigma NaN -> never visible
         s.a[RB] = make_float4(INF, 0.f, 0.f, 0.f);
         s.b[RB] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -236,11 +251,17 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 10 : 16) raster_fwd_kerne
                 const uint32_t b0m = __ballot_sync(0xffffffffu, v00 || v01);
                 const uint32_t b1m = __ballot_sync(0xffffffffu, v10 || v11);
                 if (COUNT) e_s += (unsigned)v00 + (unsigned)v01;
-                if (b0m) fwd_commit<ET, COUNT>(p[0], SG0, v00, v01, s.b[k0], s.c[k0], pos_base + k0, e_a, e_c);
+                if (b0m) {
+                    fwd_commit<ET, COUNT>(p[0], SG0, v00, v01, s.b[k0], s.c[k0], pos_base + k0, e_a, e_c);
+                    if (REC) fwd_record(rp, s.id[k0], pos_base + k0 - 1);
+                }
                 v10 = v10 && !(p[0].done & 1u);  // retired at k0
                 v11 = v11 && !(p[0].done & 2u);
                 if (COUNT) e_s += (unsigned)v10 + (unsigned)v11;
-                if (b1m) fwd_commit<ET, COUNT>(p[0], SG1, v10, v11, s.b[k1], s.c[k1], pos_base + k1, e_a, e_c);
+                if (b1m) {  // never the sentinel (its sigma is NaN)
+                    fwd_commit<ET, COUNT>(p[0], SG1, v10, v11, s.b[k1], s.c[k1], pos_base + k1, e_a, e_c);
+                    if (REC) fwd_record(rp, s.id[k1], pos_base + k1 - 1);
+                }
                 if (ET && (b0m | b1m) && __all_sync(0xffffffffu, p[0].done == 3u)) break;
             }
         } else {
@@ -276,6 +297,11 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 10 : 16) raster_fwd_kerne
                 if (ET && __all_sync(0xffffffffu, all_done())) break;
             }
         }
+    }
+    if (REC && lane == 0) {
+        const uint2 r2 = ranges[tile];
+        rec_count[(size_t)tile * 4 + warp] =
+            (uint32_t)(rp - (rec + 4 * (int64_t)r2.x + (int64_t)warp * (r2.y - r2.x)));
     }
 #pragma unroll
     for (int j = 0; j < NPR; ++j) {
@@ -571,6 +597,132 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
     }
 }
 
+// Record-driven backward (frame path): each warp replays, back to front,
+// only the list entries its forward ran the commit step for (records of
+// (splat id, list position)) -- no list staging, no sigma vote over entries
+// the warp never composited, no CTA barriers.  Decisions are replayed with
+// the forward's arithmetic (sigma cut, alpha >= 1/255, position < n_contrib)
+// and the per-warp accumulation is bwd_commit's (sg/raster_backward.py:64-107).
+__global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
+    const uint2* __restrict__ ranges, const uint2* __restrict__ rec, const uint32_t* __restrict__ rec_count,
+    const float4* __restrict__ xydr, const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg,
+    int W, int H, int tiles_x, const float* __restrict__ final_T, const int* __restrict__ n_contrib,
+    const float* __restrict__ d_img, float4* __restrict__ d_rgbo, float4* __restrict__ d_geo,
+    float* __restrict__ d_c11) {
+    __shared__ float4 s_a[4][32], s_b[4][32];
+    __shared__ float s_c[4][32];
+    __shared__ uint32_t s_id[4][32], s_pos[4][32];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int col = tx * TILE + (warp & 1) * 8 + (lane & 7);
+    const int rbase = ty * TILE + (warp >> 1) * 8 + (lane >> 3);
+    const float px = pin((float)col + 0.5f);
+    float t[2] = {1.f, 1.f}, ga[2] = {0.f, 0.f}, gb[2] = {0.f, 0.f}, gc[2] = {0.f, 0.f};
+    int nc[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int row = rbase + 4 * h;
+        if (col < W && row < H) {
+            const int q = row * W + col;
+            t[h] = final_T[q];
+            nc[h] = n_contrib[q];
+            ga[h] = d_img[3 * q]; gb[h] = d_img[3 * q + 1]; gc[h] = d_img[3 * q + 2];
+        }
+    }
+    f32x2 T = pk2(t[0], t[1]);
+    const f32x2 G0 = pk2(ga[0], ga[1]), G1 = pk2(gb[0], gb[1]), G2 = pk2(gc[0], gc[1]);
+    f32x2 S0 = mul2(bc2(bg.x), T), S1 = mul2(bc2(bg.y), T), S2 = mul2(bc2(bg.z), T);
+    const f32x2 PY = pin2(pk2((float)rbase + 0.5f, (float)rbase + 4.5f));
+    const uint2 rg = ranges[tile];
+    const int64_t rb = 4 * (int64_t)rg.x + (int64_t)warp * (rg.y - rg.x);
+    const int count = (int)rec_count[(size_t)tile * 4 + warp];
+    const int warp_nc = __reduce_max_sync(0xffffffffu, max(nc[0], nc[1]));
+    for (int hi = count; hi > 0; hi -= 32) {
+        const int lo = hi > 32 ? hi - 32 : 0;
+        const int nb = hi - lo;
+        if (lane < nb) {  // stage up to 32 records and their splats (independent gathers)
+            const uint2 r = rec[rb + lo + lane];
+            const float4 g = xydr[r.x];
+            const float4 q = conic[r.x];
+            s_a[warp][lane] = make_float4(g.x, g.y, 0.5f * q.x, q.y);
+            s_b[warp][lane] = make_float4(0.5f * q.z, q.w, colors[3 * r.x], colors[3 * r.x + 1]);
+            s_c[warp][lane] = colors[3 * r.x + 2];
+            s_id[warp][lane] = r.x;
+            s_pos[warp][lane] = r.y;
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int k = nb - 1; k >= 0; --k) {
+            const int pos = (int)s_pos[warp][k];
+            if (pos >= warp_nc) continue;  // beyond every pixel's last contribution (warp-uniform)
+            const float4 a = s_a[warp][k];
+            const float4 bq = s_b[warp][k];
+            const float blue = s_c[warp][k];
+            const float hC = bq.x;
+            const float dx = __fsub_rn(px, a.x);
+            const float hAdx = __fmul_rn(a.z, dx);
+            const f32x2 DY = sub2(PY, bc2(a.y));
+            const f32x2 SG = splat_sigma2(dx, hAdx, DY, a.w, hC);
+            const f32x2 SL = mul2(SG, bc2(NEG_LOG2E));
+            const f32x2 E = pk2(ex2_approx(lo2(SL)), ex2_approx(hi2(SL)));
+            const f32x2 ARAW = mul2(bc2(bq.y), E);
+            const float al0 = fminf(lo2(ARAW), ALPHA_MAX), al1 = fminf(hi2(ARAW), ALPHA_MAX);
+            const bool c0 = pos < nc[0] && lo2(SG) <= SIGMA_CUT && al0 >= ALPHA_MIN;
+            const bool c1 = pos < nc[1] && hi2(SG) <= SIGMA_CUT && al1 >= ALPHA_MIN;
+            const bool anyc = c0 || c1;
+            const uint32_t cmask = __ballot_sync(0xffffffffu, anyc);
+            if (!cmask) continue;
+            const f32x2 AL = pk2(al0, al1);
+            const f32x2 OM = sub2(bc2(1.f), AL);
+            const f32x2 INV = pk2(rcp_approx(lo2(OM)), rcp_approx(hi2(OM)));
+            const f32x2 TH = mul2(T, INV);
+            const f32x2 Wt = mul2(AL, TH);
+            const f32x2 WC = pk2(c0 ? lo2(Wt) : 0.f, c1 ? hi2(Wt) : 0.f);
+            const f32x2 CDOT = fma2(bc2(blue), G2, fma2(bc2(bq.w), G1, mul2(bc2(bq.z), G0)));
+            const f32x2 SDOT = fma2(S2, G2, fma2(S1, G1, mul2(S0, G0)));
+            const f32x2 DA = sub2(mul2(TH, CDOT), mul2(INV, SDOT));
+            const bool l0 = c0 && lo2(ARAW) < ALPHA_MAX, l1 = c1 && hi2(ARAW) < ALPHA_MAX;
+            const f32x2 DAL = pk2(l0 ? lo2(DA) : 0.f, l1 ? hi2(DA) : 0.f);
+            const f32x2 M = mul2(ARAW, DAL);
+            const f32x2 Y0 = fma2(bc2(a.w), DY, bc2(2.f * a.z * dx));
+            const f32x2 Y1 = fma2(bc2(2.f * hC), DY, bc2(a.w * dx));
+            const f32x2 HM = mul2(bc2(0.5f), M);
+            const f32x2 HY0 = mul2(HM, Y0), HY1 = mul2(HM, Y1);
+            const f32x2 D[9] = {mul2(WC, G0), mul2(WC, G1), mul2(WC, G2), mul2(DAL, E), mul2(M, Y0),
+                                mul2(M, Y1),  mul2(HY0, Y0), mul2(HY0, Y1), mul2(HY1, Y1)};
+            float acc[9];
+#pragma unroll
+            for (int u = 0; u < 9; ++u) acc[u] = lo2(D[u]) + hi2(D[u]);
+            S0 = fma2(WC, bc2(bq.z), S0);
+            S1 = fma2(WC, bc2(bq.w), S1);
+            S2 = fma2(WC, bc2(blue), S2);
+            T = sel2(c0, c1, TH, T);
+            const uint32_t id = s_id[warp][k];
+            if (__popc(cmask) <= 3) {
+                if (anyc) {
+                    red_add_v4(&d_rgbo[id], acc[0], acc[1], acc[2], acc[3]);
+                    red_add_v4(&d_geo[id], acc[4], acc[5], acc[6], acc[7]);
+                    atomicAdd(&d_c11[id], acc[8]);
+                }
+                continue;
+            }
+            const float r = warp_reduce8(acc, lane);
+            float c11 = acc[8];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c11 += __shfl_xor_sync(0xffffffffu, c11, o);
+            if ((lane & 3) == 0) {
+                const int idx = lane >> 2;
+                float* dst = idx < 4 ? reinterpret_cast<float*>(&d_rgbo[id]) + idx
+                                     : reinterpret_cast<float*>(&d_geo[id]) + (idx - 4);
+                atomicAdd(dst, r);
+            }
+            if (lane == 0) atomicAdd(&d_c11[id], c11);
+        }
+        __syncwarp();
+    }
+}
+
 // Warp regions of the backward: 2 (8x16 halves) or 4 (8x8 quadrants).  The
 // region geometry never changes a decision (skipped pairs are far outside
 // the 3-sigma square), so it is free to differ from the forward's.
@@ -594,16 +746,33 @@ static int fwd_regions() {
 
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
-                      unsigned long long* counts, cudaStream_t s) {
+                      unsigned long long* counts, cudaStream_t s, uint2* rec, uint32_t* rec_count) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     const float4* g = (const float4*)xydr4;
     const float4* q = (const float4*)conic4;
-#define GS_FWD(NWR, ET, CNT)                                                                                  \
-    raster_fwd_kernel<NWR, ET, CNT><<<nt, 32 * NWR, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, img, \
-                                                            T, nc, counts)
+#define GS_FWD_R(NWR, ET, CNT, REC)                                                                          \
+    raster_fwd_kernel<NWR, ET, CNT, REC><<<nt, 32 * NWR, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, \
+                                                                 img, T, nc, counts, rec, rec_count)
+#define GS_FWD(NWR, ET, CNT) GS_FWD_R(NWR, ET, CNT, false)
     const bool cnt = counts != nullptr;
-    if (fwd_regions() == 2) {
+    static int minb = -1;
+    if (minb < 0) {
+        const char* e = getenv("GS_FWD_MINB");
+        minb = e ? atoi(e) : 9;
+    }
+#define GS_FWD_M(ET, M)                                                                                        \
+    raster_fwd_kernel<4, ET, false, true, M><<<nt, 128, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, \
+                                                                 img, T, nc, counts, rec, rec_count)
+    if (rec && !cnt) {  // frame path: 8x8 quadrants with commit records
+        if (et) {
+            if (minb == 8) GS_FWD_M(true, 8); else if (minb == 9) GS_FWD_M(true, 9); else GS_FWD_M(true, 10);
+        } else {
+            if (minb == 8) GS_FWD_M(false, 8); else if (minb == 9) GS_FWD_M(false, 9); else GS_FWD_M(false, 10);
+        }
+    } else if (rec) {
+        if (et) GS_FWD_R(4, true, true, true); else GS_FWD_R(4, false, true, true);
+    } else if (fwd_regions() == 2) {
         if (et) { if (cnt) GS_FWD(2, true, true); else GS_FWD(2, true, false); }
         else { if (cnt) GS_FWD(2, false, true); else GS_FWD(2, false, false); }
     } else {
@@ -611,6 +780,8 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
         else { if (cnt) GS_FWD(4, false, true); else GS_FWD(4, false, false); }
     }
 #undef GS_FWD
+#undef GS_FWD_R
+#undef GS_FWD_M
     return check_launch("raster_fwd_kernel");
 }
 
@@ -632,6 +803,17 @@ int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xy
     }
 #undef GS_BWD
     return check_launch("raster_bwd_kernel");
+}
+
+int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
+                          const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
+                          const int* nc, const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11,
+                          cudaStream_t s) {
+    const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
+    raster_bwd_rec_kernel<<<(unsigned)(tiles_x * tiles_y), 128, 0, s>>>(
+        ranges, rec, rec_count, (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H, tiles_x, fT, nc,
+        dimg, (float4*)d_rgbo4, (float4*)d_geo4, d_c11);
+    return check_launch("raster_bwd_rec_kernel");
 }
 
 }  // namespace gs
