@@ -174,7 +174,8 @@ typedef struct gs_frame_view {
     uint32_t* sorted_vals;      /* (capacity) Gaussian id of each sorted pair */
     uint32_t* ranges2;          /* (tiles,2) [start, end) */
     unsigned long long* meta;   /* [0] status word, [1] total intersections */
-    float* d_geo4;              /* (n,4) d_mean2d x,y, d_cov00, d_cov01 (after backward) */
+    float* d_geo4;              /* (n,4) d_mean2d x,y, d_cov00, d_cov01 (after backward),
+                                   row stride 8 floats (interleaved with d_rgbo) */
     float* d_c11;               /* (n)   d_cov11 (after backward) */
 } gs_frame_view;
 

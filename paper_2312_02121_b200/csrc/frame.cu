@@ -78,7 +78,7 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.dstatus = take(onesweep_status_bytes<uint32_t>(n, 4));
     L.tstatus = take(onesweep_status_bytes<uint32_t>(cap, tp));
     L.zero_end = o;
-    L.d_geo = take(16 * n);
+    L.d_geo = take(32 * n);  // interleaved screen-space gradients: [d_rgbo 4 | d_geo 4] per Gaussian
     L.d_c11 = take(4 * n);
     L.partials = take(12 * 4 * ((n + PBWD_BLOCK - 1) / PBWD_BLOCK + 1));
     L.total = o;
@@ -126,7 +126,7 @@ int gs_frame_view_of(int64_t n, int64_t isect_capacity, int32_t width, int32_t h
     out->sorted_vals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
     out->ranges2 = at<uint32_t>(ws, L.ranges);
     out->meta = at<unsigned long long>(ws, L.meta);
-    out->d_geo4 = at<float>(ws, L.d_geo);
+    out->d_geo4 = at<float>(ws, L.d_geo) + 4;  // rows of 8 floats: [d_rgbo 4 | d_geo 4]
     out->d_c11 = at<float>(ws, L.d_c11);
     return 0;
 }
@@ -219,26 +219,25 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
     const uint32_t* svals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
     mark(stage_events, 0, s);
     if (n > 0) {
-        if ((!accumulate && cudaMemsetAsync(d_rgbo4, 0, 16 * (size_t)n, s) != cudaSuccess) ||
-            cudaMemsetAsync(at<char>(ws, L.d_geo), 0, L.partials - L.d_geo, s) != cudaSuccess)
+        if (cudaMemsetAsync(at<char>(ws, L.d_geo), 0, L.partials - L.d_geo, s) != cudaSuccess)
             return check_launch("backward memset");
     }
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
+    float* g8 = at<float>(ws, L.d_geo);
     if (counts3) {  // counted pass (roofline numerators): the list-walking backward counts evaluations
         if (launch_raster_bwd(at<uint2>(ws, L.ranges), svals, at<float>(ws, L.xydr), at<float>(ws, L.conic),
-                              colors3, bg, W, H, final_T, n_contrib, d_image, d_rgbo4, at<float>(ws, L.d_geo),
-                              at<float>(ws, L.d_c11), counts3, s))
+                              colors3, bg, W, H, final_T, n_contrib, d_image, g8, g8 + 4, at<float>(ws, L.d_c11),
+                              counts3, s, 2))
             return -1;
     } else if (launch_raster_bwd_rec(at<uint2>(ws, L.ranges), at<uint2>(ws, L.rec), at<uint32_t>(ws, L.rec_count),
                                      at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3, bg, W, H, final_T,
-                                     n_contrib, d_image, d_rgbo4, at<float>(ws, L.d_geo), at<float>(ws, L.d_c11),
-                                     s)) {
+                                     n_contrib, d_image, g8, at<float>(ws, L.d_c11), s)) {
         return -1;
     }
     mark(stage_events, 1, s);
-    if (launch_project_bwd(means3, scales3, quats4, n, k, at<uint32_t>(ws, L.tiles), at<float>(ws, L.d_geo),
+    if (launch_project_bwd(means3, scales3, quats4, n, k, at<uint32_t>(ws, L.tiles), g8 + 4,
                            at<float>(ws, L.d_c11), d_means3, d_scales3, d_quats4, d_view16, at<float>(ws, L.partials),
-                           s, accumulate != 0))
+                           s, accumulate != 0, 2, g8, d_rgbo4))
         return -1;
     mark(stage_events, 2, s);
     return 0;

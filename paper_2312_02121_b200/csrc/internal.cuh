@@ -16,7 +16,10 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
                        float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
-                       bool accumulate = false);
+                       bool accumulate = false, int gstride = 1, const float* rgbo_in = nullptr,
+                       float* rgbo_out = nullptr);
+// gstride 2: d_geo4 rows interleaved with d_rgbo rows (g8 layout); with
+// rgbo_in, each Gaussian's d_rgbo row is copied (or added) to rgbo_out.
 constexpr int PBWD_BLOCK = 256;
 
 // sort.cu
@@ -51,11 +54,10 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
 // record-driven backward of the frame path (records written by the forward)
 int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
-                          const int* nc, const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11,
-                          cudaStream_t s);
+                          const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s);
 int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, const float* fT, const int* nc,
                       const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11, unsigned long long* counts,
-                      cudaStream_t s);
+                      cudaStream_t s, int gstride);  // gstride: float4 rows between splats (1, or 2 interleaved)
 
 }  // namespace gs

@@ -153,8 +153,18 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
     int n, CamK cam, const uint32_t* __restrict__ tiles, const float4* __restrict__ d_geo,
     const float* __restrict__ d_c11, float* __restrict__ d_means, float* __restrict__ d_scales,
-    float4* __restrict__ d_quats, float* __restrict__ view_partials, bool accumulate) {
+    float4* __restrict__ d_quats, float* __restrict__ view_partials, bool accumulate, int gstride,
+    const float4* __restrict__ rgbo_in, float4* __restrict__ rgbo_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (rgbo_in && i < n) {  // frame path: d_color / d_opacity rows out of the interleaved buffer
+        const float4 v = rgbo_in[(size_t)i * gstride];
+        if (accumulate) {
+            const float4 o = rgbo_out[i];
+            rgbo_out[i] = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
+        } else {
+            rgbo_out[i] = v;
+        }
+    }
     float dv[12];
 #pragma unroll
     for (int k = 0; k < 12; ++k) dv[k] = 0.f;
@@ -194,7 +204,7 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
                 T0[k] = j00 * Rc[k] + j02 * Rc[6 + k];
                 T1[k] = j11 * Rc[3 + k] + j12 * Rc[6 + k];
             }
-            const float4 gg = d_geo[i];
+            const float4 gg = d_geo[(size_t)i * gstride];
             const float gx = gg.x, gy = gg.y, g00 = gg.z, g01 = gg.w, g11 = d_c11[i];
             // mean2d_backward (:53-77) == J^T d_mean2d with dt_w = 0
             float dt0 = cam.fx * gx * iz;
@@ -332,12 +342,13 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
                        float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
-                       bool accumulate) {
+                       bool accumulate, int gstride, const float* rgbo_in, float* rgbo_out) {
     const int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
     if (blocks > 0) {
         project_bwd_kernel<<<blocks, PBWD_THREADS, 0, s>>>(means3, scales3, (const float4*)quats4, (int)n, k, tiles,
                                                           (const float4*)d_geo4, d_c11, d_means3, d_scales3,
-                                                          (float4*)d_quats4, partials, accumulate);
+                                                          (float4*)d_quats4, partials, accumulate, gstride,
+                                                          (const float4*)rgbo_in, (float4*)rgbo_out);
         if (check_launch("project_bwd_kernel")) return -1;
     }
     view_reduce_kernel<<<1, 384, 0, s>>>(partials, blocks, d_view16);
@@ -381,7 +392,7 @@ int gs_project_bwd(const float* means3, const float* scales3, const float* quats
     if (blocks > 0) {
         project_bwd_kernel<<<blocks, PBWD_THREADS, 0, (cudaStream_t)stream>>>(
             means3, scales3, (const float4*)quats4, (int)n, k, tiles, (const float4*)d_geo4, d_c11, d_means3,
-            d_scales3, (float4*)d_quats4, (float*)ws, false);
+            d_scales3, (float4*)d_quats4, (float*)ws, false, 1, nullptr, nullptr);
         if (check_launch("project_bwd_kernel")) return -1;
     }
     view_reduce_kernel<<<1, 384, 0, (cudaStream_t)stream>>>((const float*)ws, blocks, d_view16);

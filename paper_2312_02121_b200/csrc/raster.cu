@@ -416,7 +416,7 @@ __device__ __forceinline__ void bwd_commit(const BatchT<NWR>& s, int k, const Bw
                                            const f32x2 (&G0)[NPR], const f32x2 (&G1)[NPR], const f32x2 (&G2)[NPR],
                                            f32x2 (&S0)[NPR], f32x2 (&S1)[NPR], f32x2 (&S2)[NPR],
                                            float4* __restrict__ d_rgbo, float4* __restrict__ d_geo,
-                                           float* __restrict__ d_c11, unsigned long long& e_c) {
+                                           float* __restrict__ d_c11, int gstride, unsigned long long& e_c) {
     const float4 a = s.a[k];
     const float4 bq = s.b[k];
     const float blue = s.c[k];
@@ -473,8 +473,8 @@ __device__ __forceinline__ void bwd_commit(const BatchT<NWR>& s, int k, const Bw
         // few contributing lanes: their own vector reductions are cheaper
         // than a 9-value warp reduction
         if (anyc) {
-            red_add_v4(&d_rgbo[id], acc[0], acc[1], acc[2], acc[3]);
-            red_add_v4(&d_geo[id], acc[4], acc[5], acc[6], acc[7]);
+            red_add_v4(&d_rgbo[(size_t)id * gstride], acc[0], acc[1], acc[2], acc[3]);
+            red_add_v4(&d_geo[(size_t)id * gstride], acc[4], acc[5], acc[6], acc[7]);
             atomicAdd(&d_c11[id], acc[8]);
         }
         return;
@@ -485,8 +485,8 @@ __device__ __forceinline__ void bwd_commit(const BatchT<NWR>& s, int k, const Bw
     for (int o = 16; o > 0; o >>= 1) c11 += __shfl_xor_sync(0xffffffffu, c11, o);
     if ((lane & 3) == 0) {
         const int idx = lane >> 2;
-        float* dst = idx < 4 ? reinterpret_cast<float*>(&d_rgbo[id]) + idx
-                             : reinterpret_cast<float*>(&d_geo[id]) + (idx - 4);
+        float* dst = idx < 4 ? reinterpret_cast<float*>(&d_rgbo[(size_t)id * gstride]) + idx
+                             : reinterpret_cast<float*>(&d_geo[(size_t)id * gstride]) + (idx - 4);
         atomicAdd(dst, r);
     }
     if (lane == 0) atomicAdd(&d_c11[id], c11);
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ sorted_vals, const float4* __restrict__ xydr,
     const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg, int W, int H, int tiles_x,
     const float* __restrict__ final_T, const int* __restrict__ n_contrib, const float* __restrict__ d_img,
-    float4* __restrict__ d_rgbo, float4* __restrict__ d_geo, float* __restrict__ d_c11,
+    float4* __restrict__ d_rgbo, float4* __restrict__ d_geo, float* __restrict__ d_c11, int gstride,
     unsigned long long* __restrict__ counts) {
     constexpr int NPR = 4 / NWR;  // pixel pairs per lane
     __shared__ BatchT<NWR> s;
@@ -575,8 +575,12 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
             bwd_eval<NPR>(s, k1, bstart + k1, px, PY, nc, e1);
             const bool a0 = __any_sync(0xffffffffu, e0.any), a1 = __any_sync(0xffffffffu, e1.any);
             if (COUNT) e_s += e0.n_vis + e1.n_vis;
-            if (a0) bwd_commit<NPR, COUNT>(s, k0, e0, lane, T, G0, G1, G2, S0, S1, S2, d_rgbo, d_geo, d_c11, e_c);
-            if (a1) bwd_commit<NPR, COUNT>(s, k1, e1, lane, T, G0, G1, G2, S0, S1, S2, d_rgbo, d_geo, d_c11, e_c);
+            if (a0)
+                bwd_commit<NPR, COUNT>(s, k0, e0, lane, T, G0, G1, G2, S0, S1, S2, d_rgbo, d_geo, d_c11, gstride,
+                                       e_c);
+            if (a1)
+                bwd_commit<NPR, COUNT>(s, k1, e1, lane, T, G0, G1, G2, S0, S1, S2, d_rgbo, d_geo, d_c11, gstride,
+                                       e_c);
         }
     }
     if (COUNT) {
@@ -607,8 +611,7 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     const uint2* __restrict__ ranges, const uint2* __restrict__ rec, const uint32_t* __restrict__ rec_count,
     const float4* __restrict__ xydr, const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg,
     int W, int H, int tiles_x, const float* __restrict__ final_T, const int* __restrict__ n_contrib,
-    const float* __restrict__ d_img, float4* __restrict__ d_rgbo, float4* __restrict__ d_geo,
-    float* __restrict__ d_c11) {
+    const float* __restrict__ d_img, float* __restrict__ g8, float* __restrict__ d_c11) {
     __shared__ float4 s_a[4][32], s_b[4][32];
     __shared__ float s_c[4][32];
     __shared__ uint32_t s_id[4][32], s_pos[4][32];
@@ -699,10 +702,11 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             S2 = fma2(WC, bc2(blue), S2);
             T = sel2(c0, c1, TH, T);
             const uint32_t id = s_id[warp][k];
+            float* row = g8 + 8 * (size_t)id;  // [d_rgbo 4 | d_geo 4] of this splat
             if (__popc(cmask) <= 3) {
                 if (anyc) {
-                    red_add_v4(&d_rgbo[id], acc[0], acc[1], acc[2], acc[3]);
-                    red_add_v4(&d_geo[id], acc[4], acc[5], acc[6], acc[7]);
+                    red_add_v4(reinterpret_cast<float4*>(row), acc[0], acc[1], acc[2], acc[3]);
+                    red_add_v4(reinterpret_cast<float4*>(row) + 1, acc[4], acc[5], acc[6], acc[7]);
                     atomicAdd(&d_c11[id], acc[8]);
                 }
                 continue;
@@ -711,12 +715,7 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             float c11 = acc[8];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) c11 += __shfl_xor_sync(0xffffffffu, c11, o);
-            if ((lane & 3) == 0) {
-                const int idx = lane >> 2;
-                float* dst = idx < 4 ? reinterpret_cast<float*>(&d_rgbo[id]) + idx
-                                     : reinterpret_cast<float*>(&d_geo[id]) + (idx - 4);
-                atomicAdd(dst, r);
-            }
+            if ((lane & 3) == 0) atomicAdd(row + (lane >> 2), r);
             if (lane == 0) atomicAdd(&d_c11[id], c11);
         }
         __syncwarp();
@@ -788,14 +787,15 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
 int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, const float* fT, const int* nc,
                       const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11, unsigned long long* counts,
-                      cudaStream_t s) {
+                      cudaStream_t s, int gstride) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     const float4* g = (const float4*)xydr4;
     const float4* q = (const float4*)conic4;
 #define GS_BWD(NWR, CNT)                                                                                 \
     raster_bwd_kernel<NWR, CNT><<<nt, 32 * NWR, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, fT, nc, \
-                                                        dimg, (float4*)d_rgbo4, (float4*)d_geo4, d_c11, counts)
+                                                        dimg, (float4*)d_rgbo4, (float4*)d_geo4, d_c11, gstride, \
+                                                        counts)
     if (bwd_regions() == 4) {
         if (counts) GS_BWD(4, true); else GS_BWD(4, false);
     } else {
@@ -807,12 +807,11 @@ int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xy
 
 int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
-                          const int* nc, const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11,
-                          cudaStream_t s) {
+                          const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     raster_bwd_rec_kernel<<<(unsigned)(tiles_x * tiles_y), 128, 0, s>>>(
         ranges, rec, rec_count, (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H, tiles_x, fT, nc,
-        dimg, (float4*)d_rgbo4, (float4*)d_geo4, d_c11);
+        dimg, g8, d_c11);
     return check_launch("raster_bwd_rec_kernel");
 }
 
@@ -840,7 +839,7 @@ int gs_raster_bwd(const uint32_t* ranges2, const uint32_t* sorted_vals, const fl
     if (width < 1 || height < 1) return set_error("gs_raster_bwd: bad image size %dx%d", width, height);
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
     return launch_raster_bwd((const uint2*)ranges2, sorted_vals, xydr4, conic4, colors3, bg, width, height, final_T,
-                             n_contrib, d_image, d_rgbo4, d_geo4, d_c11, counts, (cudaStream_t)stream);
+                             n_contrib, d_image, d_rgbo4, d_geo4, d_c11, counts, (cudaStream_t)stream, 1);
 }
 
 }  // extern "C"

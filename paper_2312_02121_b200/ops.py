@@ -397,7 +397,8 @@ class Frame:
                     sorted_tile_keys=sl(v.sorted_tile_keys, m, torch.int32, (m,)),
                     sorted_vals=sl(v.sorted_vals, m, torch.int32, (m,)),
                     ranges=sl(v.ranges2, 2 * nt, torch.int32, (nt, 2)),
-                    d_geo=sl(v.d_geo4, 4 * n, torch.float32, (n, 4)), d_c11=sl(v.d_c11, n, torch.float32, (n,)))
+                    d_geo=sl(v.d_geo4 - 16, 8 * n, torch.float32, (n, 8))[:, 4:8],  # rows of [d_rgbo | d_geo]
+                    d_c11=sl(v.d_c11, n, torch.float32, (n,)))
 
 
 def frame_forward(means, scales, quats, opacities, colors, cam: CameraParams, background=(0.0, 0.0, 0.0),
