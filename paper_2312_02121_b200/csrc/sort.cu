@@ -100,8 +100,13 @@ __device__ __forceinline__ uint32_t block_incl_scan256(uint32_t v, uint32_t* s_t
 }
 
 // One 8-bit pass.  vin == nullptr means value = input index (identity).
+template <typename K, int ITEMS>
+constexpr int sort_minb() {
+    return sizeof(K) == 4 ? (ITEMS <= 8 ? 5 : (ITEMS <= 12 ? 4 : (ITEMS <= 16 ? 3 : 2))) : 2;
+}
+
 template <typename K, int ITEMS, bool RANK_OR>
-__global__ void __launch_bounds__(SORT_THREADS, sizeof(K) == 4 ? 3 : 2) onesweep_kernel(
+__global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) onesweep_kernel(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_cap, const unsigned long long* __restrict__ n_dev, int shift,
     const uint32_t* __restrict__ hist, uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
@@ -340,6 +345,19 @@ int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const 
     if (small)
         return run_passes<K, SMALL_ITEMS>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s,
                                           identity_vals);
+    if (sizeof(K) == 4) {
+        static int items_env = -2;
+        if (items_env == -2) {
+            const char* e = getenv("GS_SORT_ITEMS");
+            items_env = e ? atoi(e) : -1;
+        }
+        if (items_env == 8)
+            return run_passes<K, 8>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
+        if (items_env == 12)
+            return run_passes<K, 12>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
+        if (items_env == 20)
+            return run_passes<K, 20>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
+    }
     return run_passes<K, BIG>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
 }
 template int run_onesweep<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, int64_t,
