@@ -1,5 +1,6 @@
 // abi.cu -- error plumbing and device queries of the C ABI.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 
 #include "common.cuh"
@@ -14,6 +15,15 @@ int set_error(const char* fmt, ...) {
     vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
     va_end(ap);
     return -1;
+}
+
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("GS_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
 }
 
 int check_launch(const char* what) {

@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(const uint32_t* __re
                                                            unsigned int* __restrict__ tile_counter,
                                                            unsigned long long* __restrict__ status,
                                                            unsigned long long* __restrict__ total) {
+    griddep_wait();
     __shared__ unsigned int s_tile;
     __shared__ unsigned long long s_warp[SCAN_THREADS / 32];
     __shared__ unsigned long long s_prefix;
@@ -179,6 +180,7 @@ __global__ void __launch_bounds__(256) emit_sorted_kernel(const uint32_t* __rest
                                                           uint32_t* __restrict__ tile_keys,
                                                           uint32_t* __restrict__ vals,
                                                           uint32_t* __restrict__ tile_hist, int tile_passes) {
+    griddep_wait();
     __shared__ uint32_t sh[2 * 256];
     for (int k = threadIdx.x; k < 2 * 256; k += blockDim.x) sh[k] = 0;
     __syncthreads();
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(256) emit_sorted_kernel(const uint32_t* __rest
 __global__ void __launch_bounds__(256) ranges_u32_kernel(const uint32_t* __restrict__ keys, int64_t n_cap,
                                                          const unsigned long long* __restrict__ n_dev,
                                                          uint2* __restrict__ ranges) {
+    griddep_wait();
     // 4 sorted keys per thread (one 16-byte load when aligned and in range)
     const int64_t n = n_dev ? min((int64_t)*n_dev, n_cap) : n_cap;
     const int64_t i0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
@@ -282,7 +285,7 @@ int launch_scan(const uint32_t* in, const uint32_t* gather, uint32_t* out, int64
                 unsigned long long* total, cudaStream_t s) {
     if (n == 0) return 0;
     const int64_t ctas = (n + SCAN_TILE - 1) / SCAN_TILE;
-    scan_kernel<<<(unsigned)ctas, SCAN_THREADS, 0, s>>>(in, gather, out, n, (unsigned int*)ws,
+    launch_k(scan_kernel, dim3((unsigned)ctas), dim3(SCAN_THREADS), 0, s, in, gather, out, n, (unsigned int*)ws,
                                                        (unsigned long long*)((char*)ws + 16), total);
     return check_launch("scan_kernel");
 }
@@ -294,7 +297,7 @@ int launch_emit_sorted(const uint32_t* order, const float* xydr4, const uint32_t
     int64_t blocks = (n + 255) / 256;
     const int64_t cap = (int64_t)sort_sm_count() * 8;  // resident CTAs
     if (blocks > cap) blocks = cap;
-    emit_sorted_kernel<<<(unsigned)blocks, 256, 0, s>>>(order, (const float4*)xydr4, offsets, (int)n,
+    launch_k(emit_sorted_kernel, dim3((unsigned)blocks), dim3(256), 0, s, order, (const float4*)xydr4, offsets, (int)n,
                                                                   tiles_x, tiles_y, capacity, tile_keys, vals,
                                                                   tile_hist, tile_passes);
     return check_launch("emit_sorted_kernel");
@@ -309,7 +312,8 @@ int launch_ranges_u64(const unsigned long long* sorted_keys, int64_t n, uint2* r
 int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const unsigned long long* n_dev,
                       uint2* ranges, cudaStream_t s) {
     if (n_cap == 0) return 0;
-    ranges_u32_kernel<<<(unsigned)((n_cap + 1023) / 1024), 256, 0, s>>>(sorted_tile_keys, n_cap, n_dev, ranges);
+    launch_k(ranges_u32_kernel, dim3((unsigned)((n_cap + 1023) / 1024)), dim3(256), 0, s, sorted_tile_keys, n_cap,
+             n_dev, ranges);
     return check_launch("ranges_u32_kernel");
 }
 

@@ -210,4 +210,29 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 namespace gs {
 int set_error(const char* fmt, ...);
 int check_launch(const char* what);
+
+// Programmatic dependent launch: the frame path's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization so a kernel's CTAs can
+// be scheduled while its predecessor drains; each such kernel starts with
+// griddep_wait() (griddepcontrol.wait: returns once the predecessor grid
+// has completed and its memory is visible; a no-op for a normal launch).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();  // GS_PDL=0 disables (abi.cu)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 }  // namespace gs

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
     const float* __restrict__ opac, int n, CamK cam, float4* __restrict__ xydr, float4* __restrict__ conic,
     uint32_t* __restrict__ tiles, float* __restrict__ cov_out, unsigned long long* __restrict__ status,
     uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dhist) {
+    griddep_wait();
     __shared__ uint32_t s_hist[DKEY ? 4 * 256 : 1];
     if (DKEY) {
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) s_hist[k] = 0;
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
     const float* __restrict__ d_c11, float* __restrict__ d_means, float* __restrict__ d_scales,
     float4* __restrict__ d_quats, float* __restrict__ view_partials, bool accumulate, int gstride,
     const float4* __restrict__ rgbo_in, float4* __restrict__ rgbo_out) {
+    griddep_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (rgbo_in && i < n) {  // frame path: d_color / d_opacity rows out of the interleaved buffer
         const float4 v = rgbo_in[(size_t)i * gstride];
@@ -317,6 +319,7 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
 // sg/proj_backward.py:31-32).
 __global__ void __launch_bounds__(384) view_reduce_kernel(const float* __restrict__ partials, int nblocks,
                                                           float* __restrict__ d_view16) {
+    griddep_wait();
     const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float v = 0.f;
     for (int b = lane; b < nblocks; b += 32) v += partials[b * 12 + k];
@@ -333,9 +336,9 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
     int64_t blocks = (n + 255) / 256;
     const int64_t cap = (int64_t)sort_sm_count() * 6;  // resident CTAs (40 regs, 256 threads)
     if (blocks > cap) blocks = cap;
-    project_fwd_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(means3, scales3, (const float4*)quats4, opac, (int)n, k,
-                                                    (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
-                                                    dhist);
+    launch_k(project_fwd_kernel<true>, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
+             (const float4*)quats4, opac, (int)n, k, (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
+             dhist);
     return check_launch("project_fwd_kernel<dkey>");
 }
 
@@ -345,13 +348,13 @@ int launch_project_bwd(const float* means3, const float* scales3, const float* q
                        bool accumulate, int gstride, const float* rgbo_in, float* rgbo_out) {
     const int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
     if (blocks > 0) {
-        project_bwd_kernel<<<blocks, PBWD_THREADS, 0, s>>>(means3, scales3, (const float4*)quats4, (int)n, k, tiles,
+        launch_k(project_bwd_kernel, dim3(blocks), dim3(PBWD_THREADS), 0, s, means3, scales3, (const float4*)quats4, (int)n, k, tiles,
                                                           (const float4*)d_geo4, d_c11, d_means3, d_scales3,
                                                           (float4*)d_quats4, partials, accumulate, gstride,
                                                           (const float4*)rgbo_in, (float4*)rgbo_out);
         if (check_launch("project_bwd_kernel")) return -1;
     }
-    view_reduce_kernel<<<1, 384, 0, s>>>(partials, blocks, d_view16);
+    launch_k(view_reduce_kernel, dim3(1), dim3(384), 0, s, (const float*)partials, blocks, d_view16);
     return check_launch("view_reduce_kernel");
 }
 

@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
                                                               unsigned long long* __restrict__ counts,
                                                               uint2* __restrict__ rec,
                                                               uint32_t* __restrict__ rec_count) {
+    griddep_wait();
     constexpr int NPR = 4 / NWR;
     static_assert(!REC || NWR == 4, "records are per 8x8 quadrant");
     __shared__ BatchT<NWR> s;
@@ -612,6 +613,7 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     const float4* __restrict__ xydr, const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg,
     int W, int H, int tiles_x, const float* __restrict__ final_T, const int* __restrict__ n_contrib,
     const float* __restrict__ d_img, float* __restrict__ g8, float* __restrict__ d_c11) {
+    griddep_wait();
     __shared__ float4 s_a[4][32], s_b[4][32];
     __shared__ float s_c[4][32];
     __shared__ uint32_t s_id[4][32], s_pos[4][32];
@@ -761,8 +763,8 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
         minb = e ? atoi(e) : 9;
     }
 #define GS_FWD_M(ET, M)                                                                                        \
-    raster_fwd_kernel<4, ET, false, true, M><<<nt, 128, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, \
-                                                                 img, T, nc, counts, rec, rec_count)
+    launch_k(raster_fwd_kernel<4, ET, false, true, M>, dim3(nt), dim3(128), 0, s, ranges, vals, g, q, colors3, bg, \
+             W, H, tiles_x, img, T, nc, counts, rec, rec_count)
     if (rec && !cnt) {  // frame path: 8x8 quadrants with commit records
         if (et) {
             if (minb == 8) GS_FWD_M(true, 8); else if (minb == 9) GS_FWD_M(true, 9); else GS_FWD_M(true, 10);
@@ -809,9 +811,8 @@ int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t*
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
                           const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
-    raster_bwd_rec_kernel<<<(unsigned)(tiles_x * tiles_y), 128, 0, s>>>(
-        ranges, rec, rec_count, (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H, tiles_x, fT, nc,
-        dimg, g8, d_c11);
+    launch_k(raster_bwd_rec_kernel, dim3((unsigned)(tiles_x * tiles_y)), dim3(128), 0, s, ranges, rec, rec_count,
+             (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H, tiles_x, fT, nc, dimg, g8, d_c11);
     return check_launch("raster_bwd_rec_kernel");
 }
 

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_cap, const unsigned long long* __restrict__ n_dev, int shift,
     const uint32_t* __restrict__ hist, uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
+    griddep_wait();
     constexpr int TILE_N = sort_tile<K, ITEMS>();
     extern __shared__ __align__(16) unsigned char smem[];
     K* s_keys = reinterpret_cast<K*>(smem);
@@ -308,9 +309,10 @@ static int run_passes_t(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap,
     uint32_t* vin = v0;
     uint32_t* vout = v1;
     for (int p = 0; p < passes; ++p) {
-        onesweep_kernel<K, ITEMS, RANK_OR><<<(unsigned)tiles, SORT_THREADS, sort_smem<K, ITEMS>(), s>>>(
-            kin, (p == 0 && identity_vals) ? nullptr : vin, kout, vout, n_cap, n_dev, 8 * p, hist + p * RADIX,
-            status + (size_t)p * tiles * RADIX, counters + p);
+        launch_k(onesweep_kernel<K, ITEMS, RANK_OR>, dim3((unsigned)tiles), dim3(SORT_THREADS),
+                 sort_smem<K, ITEMS>(), s, (const K*)kin, (const uint32_t*)((p == 0 && identity_vals) ? nullptr : vin),
+                 kout, vout, n_cap, n_dev, 8 * p, (const uint32_t*)(hist + p * RADIX),
+                 status + (size_t)p * tiles * RADIX, counters + p);
         if (check_launch("onesweep_kernel")) return -1;
         K* tk = kin; kin = kout; kout = tk;
         uint32_t* tv = vin; vin = vout; vout = tv;
