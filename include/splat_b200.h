@@ -177,6 +177,10 @@ typedef struct gs_frame_view {
     float* d_geo4;              /* (n,4) d_mean2d x,y, d_cov00, d_cov01 (after backward),
                                    row stride 8 floats (interleaved with d_rgbo) */
     float* d_c11;               /* (n)   d_cov11 (after backward) */
+    void* bwd_accum;            /* the backward's atomic accumulators (d_rgbo/d_geo rows, d_c11): zeroed by
+                                   gs_frame_forward; zero bwd_accum_bytes here before a SECOND
+                                   gs_frame_backward of the same forward */
+    size_t bwd_accum_bytes;
 } gs_frame_view;
 
 size_t gs_frame_workspace_bytes(int64_t n, int64_t isect_capacity, int32_t width, int32_t height);

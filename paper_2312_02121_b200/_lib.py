@@ -49,7 +49,7 @@ class GsCamera64(C.Structure):
 class GsFrameView(C.Structure):
     _fields_ = [(name, C.c_void_p) for name in (
         "xydr4", "conic4", "tiles", "depth_order", "sorted_tile_keys", "sorted_vals", "ranges2", "meta",
-        "d_geo4", "d_c11")]
+        "d_geo4", "d_c11", "bwd_accum")] + [("bwd_accum_bytes", C.c_size_t)]
 
 
 class SplatLibError(RuntimeError):

@@ -220,6 +220,21 @@ __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wa
 
 bool pdl_enabled();  // GS_PDL=0 disables (abi.cu)
 
+// Buffers a kernel clears for the kernels after it (16-byte units), so a
+// frame needs no memset nodes (they would break the launch chain).
+struct ZeroJobs {
+    uint4* p[3];
+    unsigned long long n16[3];
+};
+
+__device__ __forceinline__ void run_zero_jobs(const ZeroJobs& zj) {
+    const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+        for (unsigned long long k = tid; k < zj.n16[j]; k += stride) zj.p[j][k] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                             Args... args) {

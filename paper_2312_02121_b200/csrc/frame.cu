@@ -128,6 +128,8 @@ int gs_frame_view_of(int64_t n, int64_t isect_capacity, int32_t width, int32_t h
     out->meta = at<unsigned long long>(ws, L.meta);
     out->d_geo4 = at<float>(ws, L.d_geo) + 4;  // rows of 8 floats: [d_rgbo 4 | d_geo 4]
     out->d_c11 = at<float>(ws, L.d_c11);
+    out->bwd_accum = at<char>(ws, L.d_geo);
+    out->bwd_accum_bytes = L.partials - L.d_geo;
     return 0;
 }
 
@@ -153,15 +155,20 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     uint32_t* counters = at<uint32_t>(ws, L.counters);
 
     mark(stage_events, 0, s);
-    if (cudaMemsetAsync(at<char>(ws, L.zero_begin), 0, L.zero_end - L.zero_begin, s) != cudaSuccess)
-        return check_launch("frame memset");
-    if (cudaMemsetAsync(meta, 0xFF, 8, s) != cudaSuccess) return check_launch("frame status memset");
-    if (cudaMemsetAsync(at<char>(ws, L.ranges), 0, 8 * (size_t)tiles_x * tiles_y, s) != cudaSuccess)
-        return check_launch("ranges memset");
-    // 1. projection + depth keys
+    // 1. projection + depth keys.  No memset nodes: a one-CTA init kernel
+    // resets meta and the depth histograms, and the projection kernel clears
+    // the later stages' counters / look-back status / tile ranges and the
+    // backward's screen-space accumulators (zeroed here, once per forward).
+    ZeroJobs zj;
+    zj.p[0] = at<uint4>(ws, L.thist);
+    zj.n16[0] = (L.zero_end - L.thist) / 16;
+    zj.p[1] = at<uint4>(ws, L.ranges);
+    zj.n16[1] = (8 * (size_t)tiles_x * tiles_y + 15) / 16;
+    zj.p[2] = at<uint4>(ws, L.d_geo);
+    zj.n16[2] = (L.partials - L.d_geo) / 16;
     if (launch_project_fwd_dkey(means3, scales3, quats4, opacities, n, k, at<float>(ws, L.xydr),
                                 at<float>(ws, L.conic), at<uint32_t>(ws, L.tiles), nullptr, meta,
-                                at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.dhist), s))
+                                at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.dhist), s, zj))
         return -1;
     mark(stage_events, 1, s);
     // 2. stable depth sort of all Gaussians (culled ones last)
@@ -218,10 +225,8 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
     const bool odd = tp & 1;
     const uint32_t* svals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
     mark(stage_events, 0, s);
-    if (n > 0) {
-        if (cudaMemsetAsync(at<char>(ws, L.d_geo), 0, L.partials - L.d_geo, s) != cudaSuccess)
-            return check_launch("backward memset");
-    }
+    // the screen-space accumulators were zeroed by gs_frame_forward (see
+    // gs_frame_view.bwd_accum to re-zero before a second backward)
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
     float* g8 = at<float>(ws, L.d_geo);
     if (counts3) {  // counted pass (roofline numerators): the list-walking backward counts evaluations

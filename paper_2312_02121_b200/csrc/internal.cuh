@@ -12,7 +12,8 @@ namespace gs {
 // project.cu
 int launch_project_fwd_dkey(const float* means3, const float* scales3, const float* quats4, const float* opac,
                             int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
-                            unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s);
+                            unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s,
+                            const ZeroJobs& zj);  // also resets meta (status, total) and dhist first
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
                        float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,

@@ -32,8 +32,9 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
     const float* __restrict__ opac, int n, CamK cam, float4* __restrict__ xydr, float4* __restrict__ conic,
     uint32_t* __restrict__ tiles, float* __restrict__ cov_out, unsigned long long* __restrict__ status,
-    uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dhist) {
+    uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dhist, ZeroJobs zj) {
     griddep_wait();
+    run_zero_jobs(zj);  // frame path: clear the later stages' counters / accumulators
     __shared__ uint32_t s_hist[DKEY ? 4 * 256 : 1];
     if (DKEY) {
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) s_hist[k] = 0;
@@ -329,16 +330,31 @@ __global__ void __launch_bounds__(384) view_reduce_kernel(const float* __restric
     if (threadIdx.x < 4) d_view16[12 + threadIdx.x] = 0.f;
 }
 
+// Frame start: status word = all ones (no error), intersection total and the
+// depth-digit histograms = 0 (the projection accumulates into them).
+__global__ void __launch_bounds__(256) frame_init_kernel(unsigned long long* __restrict__ meta,
+                                                         uint32_t* __restrict__ dhist) {
+    griddep_wait();
+    if (threadIdx.x == 0) {
+        meta[0] = ~0ull;
+        meta[1] = 0ull;
+    }
+    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) dhist[k] = 0u;
+}
+
 int launch_project_fwd_dkey(const float* means3, const float* scales3, const float* quats4, const float* opac,
                             int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
-                            unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s) {
-    if (n == 0) return 0;
+                            unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s,
+                            const ZeroJobs& zj) {
+    launch_k(frame_init_kernel, dim3(1), dim3(256), 0, s, status, dhist);
+    if (check_launch("frame_init_kernel")) return -1;
     int64_t blocks = (n + 255) / 256;
+    if (blocks < 1) blocks = 1;  // the zero jobs run even for an empty scene
     const int64_t cap = (int64_t)sort_sm_count() * 6;  // resident CTAs (40 regs, 256 threads)
     if (blocks > cap) blocks = cap;
     launch_k(project_fwd_kernel<true>, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
              (const float4*)quats4, opac, (int)n, k, (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
-             dhist);
+             dhist, zj);
     return check_launch("project_fwd_kernel<dkey>");
 }
 
@@ -374,7 +390,7 @@ int gs_project_fwd(const float* means3, const float* scales3, const float* quats
     const int blocks = (int)((n + 255) / 256);
     project_fwd_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>(
         means3, scales3, (const float4*)quats4, opacities, (int)n, k, (float4*)out_xydr4, (float4*)out_conic4,
-        out_tiles, out_cov3, status, nullptr, nullptr);
+        out_tiles, out_cov3, status, nullptr, nullptr, ZeroJobs{});
     return check_launch("project_fwd_kernel");
 }
 

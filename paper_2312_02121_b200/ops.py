@@ -360,6 +360,7 @@ class Frame:
     n_contrib: torch.Tensor
     counts_fwd: torch.Tensor | None = None
     meta_host: tuple | None = None
+    backward_runs: int = 0  # the forward zeroes the backward accumulators once
 
     def view(self) -> _lib.GsFrameView:
         v = _lib.GsFrameView()
@@ -480,6 +481,11 @@ def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=F
     cnt = torch.zeros((3,), device=dev, dtype=torch.int64) if counts else None
     camc = fr.cam.c()
     bg = (C.c_float * 3)(*fr.background)
+    if fr.backward_runs:  # a second backward of the same forward: re-zero the accumulators
+        v = fr.view()
+        off = v.bwd_accum - fr.ws.data_ptr()
+        fr.ws[off:off + v.bwd_accum_bytes].zero_()
+    fr.backward_runs += 1
     check(L.gs_frame_backward(_ptr(means), _ptr(scales), _ptr(quats), _ptr(colors), n, C.byref(camc), bg,
                               fr.capacity, _ptr(fr.ws), fr.ws.numel(), _ptr(fr.final_T), _ptr(fr.n_contrib),
                               _ptr(d_image), _ptr(d_means), _ptr(d_scales), _ptr(d_quats), _ptr(d_rgbo),
