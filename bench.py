@@ -417,7 +417,9 @@ def run_ours(args):
         "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
         "intersections_per_step_rank": int(I),
         "e2e": e2e,
-        "gpu_launches": int(args.steps * len(cams) * (12 + tp)),
+        # per view: init, project, 4 depth passes, scan, emit, tp tile passes, ranges, raster fwd |
+        # raster bwd, project bwd, view reduce
+        "gpu_launches": int(args.steps * len(cams) * (13 + tp)),
         "roofline": roof,
         "stages": st,
         "counts": {"E_f": int(counts_f[0]), "E_f_sigma": int(counts_f[1]), "E_f_alpha": int(counts_f[2]),
