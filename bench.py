@@ -418,8 +418,8 @@ def run_ours(args):
         "intersections_per_step_rank": int(I),
         "e2e": e2e,
         # per view: init, project, 4 depth passes, scan, emit, tp tile passes, ranges, raster fwd |
-        # raster bwd, project bwd, view reduce
-        "gpu_launches": int(args.steps * len(cams) * (13 + tp)),
+        # raster bwd, project bwd (its last block reduces d_view)
+        "gpu_launches": int(args.steps * len(cams) * (12 + tp)),
         "roofline": roof,
         "stages": st,
         "counts": {"E_f": int(counts_f[0]), "E_f_sigma": int(counts_f[1]), "E_f_alpha": int(counts_f[2]),

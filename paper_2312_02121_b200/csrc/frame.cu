@@ -40,7 +40,7 @@ struct Layout {
     // zeroed region
     size_t zero_begin, meta, dhist, thist, counters, scan_ws, dstatus, tstatus, zero_end;
     // backward
-    size_t d_geo, d_c11, partials;
+    size_t d_geo, d_c11, pbwd_done, partials;
     size_t total;
 };
 
@@ -80,6 +80,7 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.zero_end = o;
     L.d_geo = take(32 * n);  // interleaved screen-space gradients: [d_rgbo 4 | d_geo 4] per Gaussian
     L.d_c11 = take(4 * n);
+    L.pbwd_done = take(16);  // last-block counter of the projection backward (zeroed with the accumulators)
     L.partials = take(12 * 4 * ((n + PBWD_BLOCK - 1) / PBWD_BLOCK + 1));
     L.total = o;
     return L;
@@ -242,7 +243,7 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
     mark(stage_events, 1, s);
     if (launch_project_bwd(means3, scales3, quats4, n, k, at<uint32_t>(ws, L.tiles), g8 + 4,
                            at<float>(ws, L.d_c11), d_means3, d_scales3, d_quats4, d_view16, at<float>(ws, L.partials),
-                           s, accumulate != 0, 2, g8, d_rgbo4))
+                           s, accumulate != 0, 2, g8, d_rgbo4, at<unsigned int>(ws, L.pbwd_done)))
         return -1;
     mark(stage_events, 2, s);
     return 0;

@@ -18,7 +18,7 @@ int launch_project_bwd(const float* means3, const float* scales3, const float* q
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
                        float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
                        bool accumulate = false, int gstride = 1, const float* rgbo_in = nullptr,
-                       float* rgbo_out = nullptr);
+                       float* rgbo_out = nullptr, unsigned int* done_counter = nullptr);
 // gstride 2: d_geo4 rows interleaved with d_rgbo rows (g8 layout); with
 // rgbo_in, each Gaussian's d_rgbo row is copied (or added) to rgbo_out.
 constexpr int PBWD_BLOCK = 256;

@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
     int n, CamK cam, const uint32_t* __restrict__ tiles, const float4* __restrict__ d_geo,
     const float* __restrict__ d_c11, float* __restrict__ d_means, float* __restrict__ d_scales,
     float4* __restrict__ d_quats, float* __restrict__ view_partials, bool accumulate, int gstride,
-    const float4* __restrict__ rgbo_in, float4* __restrict__ rgbo_out) {
+    const float4* __restrict__ rgbo_in, float4* __restrict__ rgbo_out, unsigned int* __restrict__ done_counter,
+    float* __restrict__ d_view16) {
     griddep_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (rgbo_in && i < n) {  // frame path: d_color / d_opacity rows out of the interleaved buffer
@@ -314,6 +315,25 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
         for (int w = 0; w < PBWD_THREADS / 32; ++w) v += red[w][threadIdx.x];
         view_partials[blockIdx.x * 12 + threadIdx.x] = v;
     }
+    if (!done_counter) return;  // a separate view_reduce_kernel finishes d_view
+    // frame path: the last block to finish sums the partials (fixed order,
+    // same tree as view_reduce_kernel) -- no extra kernel launch
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(done_counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int k = warp; k < 12; k += PBWD_THREADS / 32) {
+        float v = 0.f;
+        for (int b = lane; b < (int)gridDim.x; b += 32) v += ((volatile float*)view_partials)[b * 12 + k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) d_view16[k] = v;
+    }
+    if (threadIdx.x < 4) d_view16[12 + threadIdx.x] = 0.f;
+    if (threadIdx.x == 0) *done_counter = 0u;
 }
 
 // Fixed-order sum of the per-block d_view partials -> 4x4 (bottom row 0,
@@ -361,14 +381,15 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
                        float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
-                       bool accumulate, int gstride, const float* rgbo_in, float* rgbo_out) {
+                       bool accumulate, int gstride, const float* rgbo_in, float* rgbo_out,
+                       unsigned int* done_counter) {
     const int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
     if (blocks > 0) {
-        launch_k(project_bwd_kernel, dim3(blocks), dim3(PBWD_THREADS), 0, s, means3, scales3, (const float4*)quats4, (int)n, k, tiles,
-                                                          (const float4*)d_geo4, d_c11, d_means3, d_scales3,
-                                                          (float4*)d_quats4, partials, accumulate, gstride,
-                                                          (const float4*)rgbo_in, (float4*)rgbo_out);
+        launch_k(project_bwd_kernel, dim3(blocks), dim3(PBWD_THREADS), 0, s, means3, scales3, (const float4*)quats4,
+                 (int)n, k, tiles, (const float4*)d_geo4, d_c11, d_means3, d_scales3, (float4*)d_quats4, partials,
+                 accumulate, gstride, (const float4*)rgbo_in, (float4*)rgbo_out, done_counter, d_view16);
         if (check_launch("project_bwd_kernel")) return -1;
+        if (done_counter) return 0;  // the last block wrote d_view
     }
     launch_k(view_reduce_kernel, dim3(1), dim3(384), 0, s, (const float*)partials, blocks, d_view16);
     return check_launch("view_reduce_kernel");
@@ -411,7 +432,7 @@ int gs_project_bwd(const float* means3, const float* scales3, const float* quats
     if (blocks > 0) {
         project_bwd_kernel<<<blocks, PBWD_THREADS, 0, (cudaStream_t)stream>>>(
             means3, scales3, (const float4*)quats4, (int)n, k, tiles, (const float4*)d_geo4, d_c11, d_means3,
-            d_scales3, (float4*)d_quats4, (float*)ws, false, 1, nullptr, nullptr);
+            d_scales3, (float4*)d_quats4, (float*)ws, false, 1, nullptr, nullptr, nullptr, d_view16);
         if (check_launch("project_bwd_kernel")) return -1;
     }
     view_reduce_kernel<<<1, 384, 0, (cudaStream_t)stream>>>((const float*)ws, blocks, d_view16);
