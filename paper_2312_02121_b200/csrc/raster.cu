@@ -606,8 +606,35 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
 // only the list entries its forward ran the commit step for (records of
 // (splat id, list position)) -- no list staging, no sigma vote over entries
 // the warp never composited, no CTA barriers.  Decisions are replayed with
-// the forward's arithmetic (sigma cut, alpha >= 1/255, position < n_contrib)
-// and the per-warp accumulation is bwd_commit's (sg/raster_backward.py:64-107).
+// the forward's arithmetic (sigma cut, alpha >= 1/255, position < n_contrib).
+//
+// Accumulation: instead of a shuffle reduction per contributing record,
+// each lane parks its 9 per-record partial sums (already summed over its
+// pixel pair) in a per-warp shared-memory batch laid out [slot][value][lane]
+// (rows of 32 lanes, stride 36 words so row reads are conflict-free 128-bit
+// loads); every RBS records the warp sums the 9 * RBS rows -- one row per
+// lane, 8 LDS.128 + adds -- and issues one atomic per row.  About half the
+// instructions of a 9-value shuffle reduction per record.
+constexpr int RBS = 3;        // records per reduction batch (9 * RBS <= 32 rows: one row per lane)
+constexpr int RROW = 36;      // row stride (words): 32 lanes + pad
+
+__device__ __forceinline__ void bwd_flush(const float (*red)[9][RROW], const uint32_t* rid, int nslot, int lane,
+                                          float* __restrict__ g8, float* __restrict__ d_c11) {
+    for (int r = lane; r < 9 * nslot; r += 32) {
+        const int k = r / 9, t = r - 9 * k;
+        const float4* row = reinterpret_cast<const float4*>(&red[k][t][0]);
+        float4 a = row[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+            const float4 b = row[j];
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        }
+        const float sum = (a.x + a.y) + (a.z + a.w);
+        const uint32_t id = rid[k];
+        atomicAdd(t < 8 ? g8 + 8 * (size_t)id + t : d_c11 + id, sum);
+    }
+}
+
 __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     const uint2* __restrict__ ranges, const uint2* __restrict__ rec, const uint32_t* __restrict__ rec_count,
     const float4* __restrict__ xydr, const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg,
@@ -617,6 +644,8 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     __shared__ float4 s_a[4][32], s_b[4][32];
     __shared__ float s_c[4][32];
     __shared__ uint32_t s_id[4][32], s_pos[4][32];
+    __shared__ __align__(16) float s_red[4][RBS][9][RROW];
+    __shared__ uint32_t s_rid[4][RBS];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -643,6 +672,7 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     const int64_t rb = 4 * (int64_t)rg.x + (int64_t)warp * (rg.y - rg.x);
     const int count = (int)rec_count[(size_t)tile * 4 + warp];
     const int warp_nc = __reduce_max_sync(0xffffffffu, max(nc[0], nc[1]));
+    int nslot = 0;
     for (int hi = count; hi > 0; hi -= 32) {
         const int lo = hi > 32 ? hi - 32 : 0;
         const int nb = hi - lo;
@@ -675,9 +705,7 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             const float al0 = fminf(lo2(ARAW), ALPHA_MAX), al1 = fminf(hi2(ARAW), ALPHA_MAX);
             const bool c0 = pos < nc[0] && lo2(SG) <= SIGMA_CUT && al0 >= ALPHA_MIN;
             const bool c1 = pos < nc[1] && hi2(SG) <= SIGMA_CUT && al1 >= ALPHA_MIN;
-            const bool anyc = c0 || c1;
-            const uint32_t cmask = __ballot_sync(0xffffffffu, anyc);
-            if (!cmask) continue;
+            if (!__any_sync(0xffffffffu, c0 || c1)) continue;
             const f32x2 AL = pk2(al0, al1);
             const f32x2 OM = sub2(bc2(1.f), AL);
             const f32x2 INV = pk2(rcp_approx(lo2(OM)), rcp_approx(hi2(OM)));
@@ -696,31 +724,25 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             const f32x2 HY0 = mul2(HM, Y0), HY1 = mul2(HM, Y1);
             const f32x2 D[9] = {mul2(WC, G0), mul2(WC, G1), mul2(WC, G2), mul2(DAL, E), mul2(M, Y0),
                                 mul2(M, Y1),  mul2(HY0, Y0), mul2(HY0, Y1), mul2(HY1, Y1)};
-            float acc[9];
 #pragma unroll
-            for (int u = 0; u < 9; ++u) acc[u] = lo2(D[u]) + hi2(D[u]);
+            for (int u = 0; u < 9; ++u) s_red[warp][nslot][u][lane] = lo2(D[u]) + hi2(D[u]);
+            if (lane == 0) s_rid[warp][nslot] = s_id[warp][k];
             S0 = fma2(WC, bc2(bq.z), S0);
             S1 = fma2(WC, bc2(bq.w), S1);
             S2 = fma2(WC, bc2(blue), S2);
             T = sel2(c0, c1, TH, T);
-            const uint32_t id = s_id[warp][k];
-            float* row = g8 + 8 * (size_t)id;  // [d_rgbo 4 | d_geo 4] of this splat
-            if (__popc(cmask) <= 3) {
-                if (anyc) {
-                    red_add_v4(reinterpret_cast<float4*>(row), acc[0], acc[1], acc[2], acc[3]);
-                    red_add_v4(reinterpret_cast<float4*>(row) + 1, acc[4], acc[5], acc[6], acc[7]);
-                    atomicAdd(&d_c11[id], acc[8]);
-                }
-                continue;
+            if (++nslot == RBS) {
+                __syncwarp();
+                bwd_flush(s_red[warp], s_rid[warp], RBS, lane, g8, d_c11);
+                __syncwarp();
+                nslot = 0;
             }
-            const float r = warp_reduce8(acc, lane);
-            float c11 = acc[8];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) c11 += __shfl_xor_sync(0xffffffffu, c11, o);
-            if ((lane & 3) == 0) atomicAdd(row + (lane >> 2), r);
-            if (lane == 0) atomicAdd(&d_c11[id], c11);
         }
         __syncwarp();
+    }
+    if (nslot) {
+        __syncwarp();
+        bwd_flush(s_red[warp], s_rid[warp], nslot, lane, g8, d_c11);
     }
 }
 

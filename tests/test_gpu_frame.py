@@ -46,7 +46,7 @@ def test_frame_equals_staged_on_golden(name, cuda):
     assert torch.equal(tv["sorted_tile_keys"].long(), (st.bins.sorted_keys >> 32))
     for k in GRAD_CLASSES:
         a, b = g_f[k].cpu().numpy(), g_s[k].cpu().numpy()
-        r = grad_gate(a, b, rel=1e-4, floor=1e-2)  # only the atomic summation order differs
+        r = grad_gate(a, b, rel=1e-3, floor=1e-2)  # only the fp32 summation order differs (atomics, reduction tree)
         assert r["ok"], (name, k, r)
 
 
