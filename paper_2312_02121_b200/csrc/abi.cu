@@ -1,6 +1,7 @@
 // abi.cu -- error plumbing and device queries of the C ABI.
 #include <cstdarg>
 #include <cstdlib>
+#include <cstring>
 #include <cstdio>
 
 #include "common.cuh"
@@ -26,6 +27,16 @@ bool pdl_enabled() {
     return v == 1;
 }
 
+static int g_binning = -1;  // -1: not set (env GS_BINNING, else auto)
+
+int binning_mode() {
+    if (g_binning < 0) {
+        const char* e = getenv("GS_BINNING");
+        g_binning = e ? atoi(e) : 0;
+    }
+    return g_binning;
+}
+
 int check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error("%s: %s", what, cudaGetErrorString(e));
@@ -39,6 +50,16 @@ extern "C" {
 const char* gs_last_error(void) { return gs::g_last_error; }
 
 int gs_version(void) { return 1; }
+
+int gs_set_option(const char* name, int value) {
+    if (!name) return gs::set_error("gs_set_option: null name");
+    if (strcmp(name, "binning") == 0) {
+        if (value < 0 || value > 2) return gs::set_error("gs_set_option: binning must be 0 (auto), 1 or 2");
+        gs::g_binning = value;
+        return 0;
+    }
+    return gs::set_error("gs_set_option: unknown option %s", name);
+}
 
 int gs_device_sm_count(void) {
     int dev = 0, sms = 0;

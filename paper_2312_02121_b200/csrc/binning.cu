@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) emit_sorted_kernel(const uint32_t* __rest
     int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
     uint32_t g = 0, off = 0;
     if (p < n) {
-        g = order[p];
+        g = order ? order[p] : (uint32_t)p;  // order == nullptr: Gaussian-index order
         off = offsets[p];
         const float4 gx = xydr[g];
         const int r = __float_as_int(gx.w);

@@ -172,12 +172,18 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
                                 at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.dhist), s, zj))
         return -1;
     mark(stage_events, 1, s);
-    // 2. stable depth sort of all Gaussians (culled ones last)
-    if (run_onesweep<uint32_t>(at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.order), at<uint32_t>(ws, L.dkeys_alt),
-                               at<uint32_t>(ws, L.order_alt), n, nullptr, 4, at<uint32_t>(ws, L.dhist),
-                               at<uint32_t>(ws, L.dstatus), counters, s, true))
-        return -1;
-    const uint32_t* order = at<uint32_t>(ws, L.order);  // 4 passes: back in the primary buffers
+    const int bmode = binning_mode();
+    const bool segment = bmode == 2 || (bmode == 0 && n <= 400000);
+    // 2. depth-first: stable depth sort of all Gaussians (culled ones last);
+    //    segment mode: none (pairs are emitted in index order, tiles sorted later)
+    const uint32_t* order = nullptr;
+    if (!segment) {
+        if (run_onesweep<uint32_t>(at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.order),
+                                   at<uint32_t>(ws, L.dkeys_alt), at<uint32_t>(ws, L.order_alt), n, nullptr, 4,
+                                   at<uint32_t>(ws, L.dhist), at<uint32_t>(ws, L.dstatus), counters, s, true))
+            return -1;
+        order = at<uint32_t>(ws, L.order);  // 4 passes: back in the primary buffers
+    }
     mark(stage_events, 2, s);
     // 3. tile counts in depth order -> offsets, total -> meta[1]
     if (launch_scan(at<uint32_t>(ws, L.tiles), order, at<uint32_t>(ws, L.offsets), n, at<char>(ws, L.scan_ws),
@@ -199,6 +205,10 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     const uint32_t* svals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
     // 6. per-tile ranges
     if (launch_ranges_u32(skeys, isect_capacity, meta + 1, at<uint2>(ws, L.ranges), s)) return -1;
+    // 6b. segment mode: each tile's (index-ordered) list stably sorted by depth
+    if (segment && launch_segsort(at<uint2>(ws, L.ranges), tiles_x * tiles_y, at<uint32_t>(ws, L.dkeys),
+                                  const_cast<uint32_t*>(svals), at<uint32_t>(ws, odd ? L.tvals : L.tvals_alt), s))
+        return -1;
     mark(stage_events, 4, s);
     // 7. raster forward
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);

@@ -47,6 +47,12 @@ int launch_ranges_u64(const unsigned long long* sorted_keys, int64_t n, uint2* r
 int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const unsigned long long* n_dev,
                       uint2* ranges, cudaStream_t s);  // ranges must be zeroed
 
+// segsort.cu: per-tile stable sort of each tile's list by depth key
+int launch_segsort(const uint2* ranges, int n_tiles, const uint32_t* dkeys, uint32_t* vals, uint32_t* alt,
+                   cudaStream_t s);
+// binning strategy of the frame path (abi.cu): 0 auto, 1 depth-first, 2 per-tile segments
+int binning_mode();
+
 // raster.cu
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,

@@ -72,6 +72,12 @@ class CameraParams:
         return (self.height + TILE - 1) // TILE
 
 
+def set_option(name: str, value: int) -> None:
+    """Process-wide tuning option of libsplat_b200.so (gs_set_option), e.g.
+    set_option("binning", 1) forces the depth-first frame binning."""
+    check(_lib.load().gs_set_option(name.encode(), int(value)), "gs_set_option")
+
+
 def _check_param(name, t, cols):
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")

@@ -50,11 +50,36 @@ def test_frame_equals_staged_on_golden(name, cuda):
         assert r["ok"], (name, k, r)
 
 
+@pytest.fixture(params=[1, 2], ids=["depth_first", "segments"])
+def binning(request, cuda):
+    """Run a test under both frame binning strategies (gs_set_option)."""
+    from paper_2312_02121_b200 import ops
+    ops.set_option("binning", request.param)
+    yield request.param
+    ops.set_option("binning", 0)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_binning_strategies_agree(name, binning, cuda):
+    """Depth-first and per-tile-segment binning give the same lists, bit for
+    bit (both are sg/binning.py:50-65's (depth, source_index) order)."""
+    g = load_golden(name)
+    st, g_s, img_s, fr, g_f = _both(g["inputs"], g["camera"], g["background"], g["et"], g["d_image"], cuda)
+    tv = fr.tensors()
+    assert torch.equal(tv["ranges"], st.bins.ranges)
+    assert torch.equal(tv["sorted_vals"], st.bins.sorted_vals)
+    assert torch.equal(fr.image, img_s)
+
+
 def test_depth_order_is_stable_sort(cuda):
     g = load_golden("dense_ties")  # has exact depth ties
     from paper_2312_02121_b200 import ops
     t = _tensors(g["inputs"], cuda)
-    fr = ops.frame_forward(*t, ops.CameraParams.of(g["camera"]), (0.0, 0.0, 0.0), True)
+    ops.set_option("binning", 1)  # depth_order exists in the depth-first strategy
+    try:
+        fr = ops.frame_forward(*t, ops.CameraParams.of(g["camera"]), (0.0, 0.0, 0.0), True)
+    finally:
+        ops.set_option("binning", 0)
     tv = fr.tensors()
     order = tv["depth_order"].cpu().numpy()
     depth = tv["xydr"][:, 2].cpu().numpy()
