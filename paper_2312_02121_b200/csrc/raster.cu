@@ -779,20 +779,11 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
                                                                  img, T, nc, counts, rec, rec_count)
 #define GS_FWD(NWR, ET, CNT) GS_FWD_R(NWR, ET, CNT, false)
     const bool cnt = counts != nullptr;
-    static int minb = -1;
-    if (minb < 0) {
-        const char* e = getenv("GS_FWD_MINB");
-        minb = e ? atoi(e) : 9;
-    }
 #define GS_FWD_M(ET, M)                                                                                        \
     launch_k(raster_fwd_kernel<4, ET, false, true, M>, dim3(nt), dim3(128), 0, s, ranges, vals, g, q, colors3, bg, \
              W, H, tiles_x, img, T, nc, counts, rec, rec_count)
-    if (rec && !cnt) {  // frame path: 8x8 quadrants with commit records
-        if (et) {
-            if (minb == 8) GS_FWD_M(true, 8); else if (minb == 9) GS_FWD_M(true, 9); else GS_FWD_M(true, 10);
-        } else {
-            if (minb == 8) GS_FWD_M(false, 8); else if (minb == 9) GS_FWD_M(false, 9); else GS_FWD_M(false, 10);
-        }
+    if (rec && !cnt) {  // frame path: 8x8 quadrants with commit records, 9 CTAs/SM (measured best)
+        if (et) GS_FWD_M(true, 9); else GS_FWD_M(false, 9);
     } else if (rec) {
         if (et) GS_FWD_R(4, true, true, true); else GS_FWD_R(4, false, true, true);
     } else if (fwd_regions() == 2) {
