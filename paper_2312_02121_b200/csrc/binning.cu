@@ -247,6 +247,204 @@ __global__ void __launch_bounds__(256) emit_sorted_kernel(const uint32_t* __rest
     }
 }
 
+// Warp-cooperative emission of 32 consecutive Gaussians' pairs (lane = one
+// Gaussian, off = its output offset, rect given): the warp owns the
+// contiguous range [off(lane 0), off(lane 0) + total) and walks it 32 entries
+// at a time (coalesced stores), each entry finding its owner lane by binary
+// search over the lanes' exclusive prefix and decoding its tile row-major.
+__device__ __forceinline__ void emit_warp(int lane, uint32_t g, uint32_t base, int tx0, int tx1, int ty0, int ty1,
+                                          int tiles_x, int64_t capacity, uint32_t* __restrict__ tile_keys,
+                                          uint32_t* __restrict__ vals, uint32_t* sh, int tile_passes) {
+    const int w = tx1 - tx0 + 1;
+    const uint32_t cnt = (uint32_t)(w * (ty1 - ty0 + 1));
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const float rw = w > 0 ? 1.f / (float)w : 0.f;
+    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        int L = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t e = __shfl_sync(0xffffffffu, excl, L + step);
+            if (e <= t) L += step;
+        }
+        const uint32_t j = t - __shfl_sync(0xffffffffu, excl, L);
+        const int ow = __shfl_sync(0xffffffffu, w, L);
+        const float orw = __shfl_sync(0xffffffffu, rw, L);
+        const int otx0 = __shfl_sync(0xffffffffu, tx0, L), oty0 = __shfl_sync(0xffffffffu, ty0, L);
+        const uint32_t og = __shfl_sync(0xffffffffu, g, L);
+        int row = (int)((float)j * orw);
+        if (row * ow > (int)j) --row;
+        if ((row + 1) * ow <= (int)j) ++row;
+        const uint32_t tile = (uint32_t)((oty0 + row) * tiles_x + otx0 + ((int)j - row * ow));
+        const bool valid = t < total && (int64_t)(base + t) < capacity;
+        if (valid) {
+            tile_keys[base + t] = tile;
+            vals[base + t] = og;
+            atomicAdd(&sh[tile & 255u], 1u);
+        }
+        if (tile_passes > 1) warp_hist_add(sh + 256, (tile >> 8) & 255u, valid);  // high digit: few distinct values
+    }
+}
+
+// Fused scan + emission (frame path): persistent CTAs take chunks of
+// ES_CHUNK consecutive Gaussians (in depth order, or index order when order
+// == nullptr) from a counter, scan their tile counts (the projection's
+// per-Gaussian counts), get the chunk's output base by decoupled look-back
+// and emit the pairs directly -- no offsets array, no separate scan kernel.
+// Chunk layout: round r, warp w, lane -> Gaussian r * 256 + w * 32 + lane,
+// so each warp emits 32 consecutive Gaussians per round.  The last chunk's
+// CTA writes the intersection total.
+constexpr int ES_THREADS = 256;
+
+size_t emit_scan_ws_bytes(int64_t n) {
+    const int64_t chunks = (n + ES_THREADS - 1) / ES_THREADS;  // sized for the 1-round variant
+    return 16 + (size_t)(chunks > 0 ? chunks : 1) * sizeof(unsigned long long);
+}
+
+template <int ES_ROUNDS>
+__global__ void __launch_bounds__(ES_THREADS) emit_scan_kernel(
+    const uint32_t* __restrict__ order, const float4* __restrict__ xydr, const uint32_t* __restrict__ counts, int n,
+    int tiles_x, int tiles_y, int64_t capacity, uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ vals,
+    uint32_t* __restrict__ tile_hist, int tile_passes, unsigned int* __restrict__ chunk_counter,
+    unsigned long long* __restrict__ status, unsigned long long* __restrict__ total) {
+    griddep_wait();
+    constexpr int ES_CHUNK = ES_THREADS * ES_ROUNDS;
+    __shared__ uint32_t sh[2 * 256];
+    __shared__ uint32_t s_wsum[ES_ROUNDS][ES_THREADS / 32];
+    __shared__ unsigned int s_chunk;
+    __shared__ unsigned long long s_prefix;
+    for (int k = threadIdx.x; k < 2 * 256; k += blockDim.x) sh[k] = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n_chunks = (n + ES_CHUNK - 1) / ES_CHUNK;
+    while (true) {
+        __syncthreads();  // s_chunk / s_wsum reuse
+        if (threadIdx.x == 0) s_chunk = atomicAdd(chunk_counter, 1u);
+        __syncthreads();
+        const int chunk = (int)s_chunk;
+        if (chunk >= n_chunks) break;
+        uint32_t g[ES_ROUNDS], cnt[ES_ROUNDS];
+#pragma unroll
+        for (int r = 0; r < ES_ROUNDS; ++r) {
+            const int p = chunk * ES_CHUNK + r * ES_THREADS + (int)threadIdx.x;
+            g[r] = p < n ? (order ? order[p] : (uint32_t)p) : 0u;
+            cnt[r] = p < n ? counts[g[r]] : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < ES_ROUNDS; ++r) {
+            uint32_t incl = cnt[r];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_wsum[r][warp] = incl;
+        }
+        __syncthreads();
+        // the chunk's aggregate and this warp's base in every round
+        unsigned long long agg = 0;
+        uint32_t wbase[ES_ROUNDS];
+#pragma unroll
+        for (int r = 0; r < ES_ROUNDS; ++r) {
+            uint32_t before = 0, rt = 0;
+#pragma unroll
+            for (int w = 0; w < ES_THREADS / 32; ++w) {
+                const uint32_t v = s_wsum[r][w];
+                if (w < warp) before += v;
+                rt += v;
+            }
+            wbase[r] = (uint32_t)agg + before;
+            agg += rt;
+        }
+        if (threadIdx.x == 0) {  // decoupled look-back
+            unsigned long long prefix = 0;
+            if (chunk == 0) {
+                st_volatile(&status[0], FLAG_PRE | agg);
+            } else {
+                st_volatile(&status[chunk], FLAG_AGG | agg);
+                __threadfence();
+                // look-back: the immediate predecessor first (usually already
+                // inclusive when chunks are processed in waves), then windows
+                // of LB predecessor statuses per round trip
+                constexpr int LB = 8;
+                int q = chunk - 1;
+                bool found = false;
+                {
+                    unsigned long long sv = ld_volatile(&status[q]);
+                    while ((sv & ~VAL_MASK) == 0) sv = ld_volatile(&status[q]);
+                    prefix += sv & VAL_MASK;
+                    found = (sv & ~VAL_MASK) == FLAG_PRE;
+                    --q;
+                }
+                while (!found) {
+                    unsigned long long wv[LB];
+#pragma unroll
+                    for (int j = 0; j < LB; ++j) wv[j] = q - j >= 0 ? ld_volatile(&status[q - j]) : FLAG_PRE;
+#pragma unroll
+                    for (int j = 0; j < LB; ++j) {
+                        if (!found) {
+                            unsigned long long sv = wv[j];
+                            while ((sv & ~VAL_MASK) == 0) sv = ld_volatile(&status[q - j]);
+                            prefix += sv & VAL_MASK;
+                            found = (sv & ~VAL_MASK) == FLAG_PRE;
+                        }
+                    }
+                    q -= LB;
+                }
+                st_volatile(&status[chunk], FLAG_PRE | (prefix + agg));
+            }
+            s_prefix = prefix;
+            if (chunk == n_chunks - 1) *total = prefix + agg;
+        }
+        __syncthreads();
+        const uint32_t prefix = (uint32_t)s_prefix;
+#pragma unroll
+        for (int r = 0; r < ES_ROUNDS; ++r) {
+            int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
+            if (cnt[r]) {
+                const float4 gx = xydr[g[r]];
+                tile_rect(gx.x, gx.y, __float_as_int(gx.w), tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+            }
+            emit_warp(lane, g[r], prefix + wbase[r], tx0, tx1, ty0, ty1, tiles_x, capacity, tile_keys, vals, sh,
+                      tile_passes);
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < tile_passes * 256; k += blockDim.x) {
+        const uint32_t v = sh[k];
+        if (v) atomicAdd(&tile_hist[k], v);
+    }
+}
+
+int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* counts, int64_t n, int tiles_x,
+                     int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals, uint32_t* tile_hist,
+                     int tile_passes, void* ws, unsigned long long* total, cudaStream_t s) {
+    // small scenes: one Gaussian per thread per chunk (more CTAs in flight);
+    // large: 4 rounds per chunk (fewer look-backs)
+    const int rounds = n <= (1 << 18) ? 1 : 4;
+    const int64_t chunks = (n + ES_THREADS * rounds - 1) / (ES_THREADS * rounds);
+    const int64_t resident = (int64_t)sort_sm_count() * 8;
+    int64_t grid = chunks < resident ? chunks : resident;
+    if (grid < 1) grid = 1;
+    unsigned int* counter = (unsigned int*)ws;
+    unsigned long long* status = (unsigned long long*)((char*)ws + 16);
+    if (rounds == 1)
+        launch_k(emit_scan_kernel<1>, dim3((unsigned)grid), dim3(ES_THREADS), 0, s, order, (const float4*)xydr4,
+                 counts, (int)n, tiles_x, tiles_y, capacity, tile_keys, vals, tile_hist, tile_passes, counter, status,
+                 total);
+    else
+        launch_k(emit_scan_kernel<4>, dim3((unsigned)grid), dim3(ES_THREADS), 0, s, order, (const float4*)xydr4,
+                 counts, (int)n, tiles_x, tiles_y, capacity, tile_keys, vals, tile_hist, tile_passes, counter, status,
+                 total);
+    return check_launch("emit_scan_kernel");
+}
+
 __global__ void __launch_bounds__(256) ranges_u32_kernel(const uint32_t* __restrict__ keys, int64_t n_cap,
                                                          const unsigned long long* __restrict__ n_dev,
                                                          uint2* __restrict__ ranges) {

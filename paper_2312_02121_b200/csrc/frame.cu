@@ -74,7 +74,7 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.dhist = take(4 * 256 * 4);
     L.thist = take(4 * 256 * 2);
     L.counters = take(64);
-    L.scan_ws = take(scan_ws_bytes(n));
+    L.scan_ws = take(emit_scan_ws_bytes(n));
     L.dstatus = take(onesweep_status_bytes<uint32_t>(n, 4));
     L.tstatus = take(onesweep_status_bytes<uint32_t>(cap, tp));
     L.zero_end = o;
@@ -185,14 +185,11 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
         order = at<uint32_t>(ws, L.order);  // 4 passes: back in the primary buffers
     }
     mark(stage_events, 2, s);
-    // 3. tile counts in depth order -> offsets, total -> meta[1]
-    if (launch_scan(at<uint32_t>(ws, L.tiles), order, at<uint32_t>(ws, L.offsets), n, at<char>(ws, L.scan_ws),
-                    meta + 1, s))
-        return -1;
-    // 4. emission in depth order (+ tile digit histograms)
-    if (launch_emit_sorted(order, at<float>(ws, L.xydr), at<uint32_t>(ws, L.offsets), n, tiles_x, tiles_y,
-                           isect_capacity, at<uint32_t>(ws, L.tkeys), at<uint32_t>(ws, L.tvals),
-                           at<uint32_t>(ws, L.thist), tp, s))
+    // 3+4. fused: scan of the tile counts (in depth or index order), total ->
+    //      meta[1], emission of the (tile, gaussian) pairs + tile-digit histograms
+    if (launch_emit_scan(order, at<float>(ws, L.xydr), at<uint32_t>(ws, L.tiles), n, tiles_x, tiles_y,
+                         isect_capacity, at<uint32_t>(ws, L.tkeys), at<uint32_t>(ws, L.tvals),
+                         at<uint32_t>(ws, L.thist), tp, at<char>(ws, L.scan_ws), meta + 1, s))
         return -1;
     mark(stage_events, 3, s);
     // 5. stable sort by tile id (bits [0, 8*tp))

@@ -42,6 +42,12 @@ int launch_scan(const uint32_t* in, const uint32_t* gather, uint32_t* out, int64
 int launch_emit_sorted(const uint32_t* order, const float* xydr4, const uint32_t* offsets, int64_t n,
                        int tiles_x, int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals,
                        uint32_t* tile_hist, int tile_passes, cudaStream_t s);
+// fused scan of the projection's tile counts + pair emission (frame path);
+// ws (emit_scan_ws_bytes(n), zeroed): chunk counter + look-back status
+size_t emit_scan_ws_bytes(int64_t n);
+int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* counts, int64_t n, int tiles_x,
+                     int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals, uint32_t* tile_hist,
+                     int tile_passes, void* ws, unsigned long long* total, cudaStream_t s);
 int launch_ranges_u64(const unsigned long long* sorted_keys, int64_t n, uint2* ranges,
                       cudaStream_t s);  // ranges must be zeroed
 int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const unsigned long long* n_dev,
