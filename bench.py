@@ -58,6 +58,12 @@ def dist_env():
     return world, rank, local
 
 
+def segment_binning(n):
+    """Which frame binning the library uses (csrc/frame.cu, gs_set_option)."""
+    mode = int(os.environ.get("GS_BINNING", "0"))
+    return mode == 2 or (mode == 0 and n <= 400000)
+
+
 def views_for(cfg, spec, world, rank):
     """(camera, d_image) pairs this rank renders each step."""
     import numpy as np
@@ -417,9 +423,10 @@ def run_ours(args):
         "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
         "intersections_per_step_rank": int(I),
         "e2e": e2e,
-        # per view: init, project, 4 depth passes, scan, emit, tp tile passes, ranges, raster fwd |
-        # raster bwd, project bwd (its last block reduces d_view)
-        "gpu_launches": int(args.steps * len(cams) * (12 + tp)),
+        # per view: init, project, [4 depth passes], fused scan+emit, tp tile passes, ranges,
+        # [2 per-tile depth-sort kernels], raster fwd | raster bwd, project bwd (its last block reduces
+        # d_view); the bracketed parts are the depth-first vs per-tile-segment binning (csrc/frame.cu)
+        "gpu_launches": int(args.steps * len(cams) * ((9 if segment_binning(n) else 11) + tp)),
         "roofline": roof,
         "stages": st,
         "counts": {"E_f": int(counts_f[0]), "E_f_sigma": int(counts_f[1]), "E_f_alpha": int(counts_f[2]),
