@@ -361,11 +361,16 @@ def run_ours(args):
     # algorithmic work; per rank-step, all views
     F_fwd = 8 * counts_f[0] + 4 * counts_f[1] + 3 * counts_f[2] + 4 * counts_f[3]
     F_bwd = 8 * counts_b[0] + 4 * counts_b[1] + 42 * counts_b[2]
+    seg = segment_binning(n)
     work = {
         "project": ("hbm", 84.0 * n * nv),                   # read 44 B, write xydr 16 + conic 16 + tiles 4 + depth key 4
-        "depth_sort": ("hbm", 4 * 16.0 * n * nv),            # 4 passes x (key+value) x (read+write)
-        "scan_emit": ("hbm", 12.0 * n * nv + 8.0 * I + 16.0 * n * nv),  # gather+scan, offsets, pairs out, xydr gather
-        "tile_sort_ranges": ("hbm", tp * 16.0 * I + 4.0 * I + 8.0 * n_tiles),
+        # depth-first: 4 passes x (key+value) x (read+write); segment binning: no global depth sort
+        "depth_sort": ("none", 0.0) if seg else ("hbm", 4 * 16.0 * n * nv),
+        # fused scan + emission: (order +) count + xydr gather per Gaussian, pairs out
+        "scan_emit": ("hbm", (4.0 if seg else 8.0) * n * nv + 16.0 * n * nv + 8.0 * I),
+        # tile passes (key+value, read+write) + ranges; segment binning adds the per-tile
+        # depth sort (value in, key gather, value out)
+        "tile_sort_ranges": ("hbm", tp * 16.0 * I + 4.0 * I + 8.0 * n_tiles + (12.0 * I if seg else 0.0)),
         "raster_fwd": ("fp32", float(F_fwd)),
         "raster_bwd": ("fp32", float(F_bwd)),
         "project_bwd": ("hbm", 104.0 * n * nv),
@@ -374,7 +379,9 @@ def run_ours(args):
     for name, ms in zip(stage_names, stage_ms):
         bound, w = work[name]
         d = {"ms": round(float(ms), 4), "bound": bound}
-        if bound == "hbm":
+        if bound == "none":
+            pass
+        elif bound == "hbm":
             d["achieved_gbs"] = round(w / (ms / 1e3) / 1e9, 1) if ms > 0 else None
             d["frac"] = round(w / (ms / 1e3) / hbm, 4) if ms > 0 else None
         else:
