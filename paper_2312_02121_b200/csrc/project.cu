@@ -160,7 +160,9 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
     float* __restrict__ d_view16) {
     griddep_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (rgbo_in && i < n) {  // frame path: d_color / d_opacity rows out of the interleaved buffer
+    const bool vis = i < n && tiles[i] != 0u;
+    // (accumulating: a culled Gaussian adds exact zeros -- skip its rows)
+    if (rgbo_in && i < n && (vis || !accumulate)) {  // frame path: d_color / d_opacity rows of the interleaved buffer
         const float4 v = rgbo_in[(size_t)i * gstride];
         if (accumulate) {
             const float4 o = rgbo_out[i];
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
     if (i < n) {
         float dmx = 0.f, dmy = 0.f, dmz = 0.f, dsx = 0.f, dsy = 0.f, dsz = 0.f;
         float4 dq = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (tiles[i] != 0u) {
+        if (vis) {
             const float mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
             const float s[3] = {scales[3 * i], scales[3 * i + 1], scales[3 * i + 2]};
             const float4 q = quats[i];
@@ -287,11 +289,13 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
             dq = make_float4((gw - qw * dot) * inv, (gxq - qx * dot) * inv, (gyq - qy * dot) * inv,
                              (gzq - qz * dot) * inv);
         }
-        if (accumulate) {  // sum over views into the caller's gradient
+        if (accumulate) {  // sum over views into the caller's gradient (culled: nothing to add)
+            if (vis) {
             d_means[3 * i] += dmx; d_means[3 * i + 1] += dmy; d_means[3 * i + 2] += dmz;
             d_scales[3 * i] += dsx; d_scales[3 * i + 1] += dsy; d_scales[3 * i + 2] += dsz;
             const float4 o = d_quats[i];
             d_quats[i] = make_float4(o.x + dq.x, o.y + dq.y, o.z + dq.z, o.w + dq.w);
+            }
         } else {
             d_means[3 * i] = dmx; d_means[3 * i + 1] = dmy; d_means[3 * i + 2] = dmz;
             d_scales[3 * i] = dsx; d_scales[3 * i + 1] = dsy; d_scales[3 * i + 2] = dsz;
