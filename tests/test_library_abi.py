@@ -40,6 +40,19 @@ def test_host_only_entry_points():
     assert L.gs_project_bwd_workspace_bytes(1000) >= 4 * 12 * 4
 
 
+def test_set_option():
+    from paper_2312_02121_b200 import _lib, ops
+    for v in (1, 2, 0):
+        ops.set_option("binning", v)
+    with pytest.raises(_lib.SplatLibError, match="binning"):
+        ops.set_option("binning", 7)
+    with pytest.raises(_lib.SplatLibError, match="unknown option"):
+        ops.set_option("no_such_option", 1)
+    L = _lib.load()
+    assert L.gs_bin64_workspace_bytes(1000, 5000, 256) > 0
+    assert L.gs_project64_bwd_workspace_bytes(1000) > 0
+
+
 def test_kernels_are_sm100a():
     from paper_2312_02121_b200 import _lib
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
