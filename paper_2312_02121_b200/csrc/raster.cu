@@ -618,19 +618,23 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
 constexpr int RBS = 3;        // records per reduction batch (9 * RBS <= 32 rows: one row per lane)
 constexpr int RROW = 36;      // row stride (words): 32 lanes + pad
 
-__device__ __forceinline__ void bwd_flush(const float (*red)[9][RROW], const uint32_t* rid, int nslot, int lane,
+// Sum the batch's 9 * nslot rows (one per lane) and add each to its
+// splat's gradient slot.  red: this warp's batch (32-bit shared address),
+// kslots: the batch's staged-record indices (8 bits each), ids: this warp's
+// staged splat ids.
+__device__ __forceinline__ void bwd_flush(uint32_t red, uint32_t kslots, const uint32_t* ids, int nslot, int lane,
                                           float* __restrict__ g8, float* __restrict__ d_c11) {
-    for (int r = lane; r < 9 * nslot; r += 32) {
-        const int k = r / 9, t = r - 9 * k;
-        const float4* row = reinterpret_cast<const float4*>(&red[k][t][0]);
-        float4 a = row[0];
+    if (lane < 9 * nslot) {
+        const int k = lane / 9, t = lane - 9 * k;
+        const uint32_t row = red + (uint32_t)lane * (RROW * 4);
+        float4 a = lds_f4(row);
 #pragma unroll
         for (int j = 1; j < 8; ++j) {
-            const float4 b = row[j];
+            const float4 b = lds_f4(row + 16 * j);
             a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
         }
         const float sum = (a.x + a.y) + (a.z + a.w);
-        const uint32_t id = rid[k];
+        const uint32_t id = ids[(kslots >> (8 * k)) & 255u];
         atomicAdd(t < 8 ? g8 + 8 * (size_t)id + t : d_c11 + id, sum);
     }
 }
@@ -645,7 +649,6 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     __shared__ float s_c[4][32];
     __shared__ uint32_t s_id[4][32], s_pos[4][32];
     __shared__ __align__(16) float s_red[4][RBS][9][RROW];
-    __shared__ uint32_t s_rid[4][RBS];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -672,7 +675,9 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     const int64_t rb = 4 * (int64_t)rg.x + (int64_t)warp * (rg.y - rg.x);
     const int count = (int)rec_count[(size_t)tile * 4 + warp];
     const int warp_nc = __reduce_max_sync(0xffffffffu, max(nc[0], nc[1]));
+    const uint32_t red_w = smem_addr(&s_red[warp][0][0][0]);
     int nslot = 0;
+    uint32_t kslots = 0;
     for (int hi = count; hi > 0; hi -= 32) {
         const int lo = hi > 32 ? hi - 32 : 0;
         const int nb = hi - lo;
@@ -724,25 +729,29 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             const f32x2 HY0 = mul2(HM, Y0), HY1 = mul2(HM, Y1);
             const f32x2 D[9] = {mul2(WC, G0), mul2(WC, G1), mul2(WC, G2), mul2(DAL, E), mul2(M, Y0),
                                 mul2(M, Y1),  mul2(HY0, Y0), mul2(HY0, Y1), mul2(HY1, Y1)};
+            const uint32_t slot = red_w + (uint32_t)nslot * (9 * RROW * 4) + 4 * lane;
 #pragma unroll
-            for (int u = 0; u < 9; ++u) s_red[warp][nslot][u][lane] = lo2(D[u]) + hi2(D[u]);
-            if (lane == 0) s_rid[warp][nslot] = s_id[warp][k];
+            for (int u = 0; u < 9; ++u) sts_f32(slot + u * (RROW * 4), lo2(D[u]) + hi2(D[u]));
+            kslots |= (uint32_t)k << (8 * nslot);
             S0 = fma2(WC, bc2(bq.z), S0);
             S1 = fma2(WC, bc2(bq.w), S1);
             S2 = fma2(WC, bc2(blue), S2);
             T = sel2(c0, c1, TH, T);
             if (++nslot == RBS) {
                 __syncwarp();
-                bwd_flush(s_red[warp], s_rid[warp], RBS, lane, g8, d_c11);
+                bwd_flush(red_w, kslots, s_id[warp], RBS, lane, g8, d_c11);
                 __syncwarp();
                 nslot = 0;
+                kslots = 0;
             }
         }
+        if (nslot) {  // the batch refers to this staging chunk's ids: flush before restaging
+            __syncwarp();
+            bwd_flush(red_w, kslots, s_id[warp], nslot, lane, g8, d_c11);
+            nslot = 0;
+            kslots = 0;
+        }
         __syncwarp();
-    }
-    if (nslot) {
-        __syncwarp();
-        bwd_flush(s_red[warp], s_rid[warp], nslot, lane, g8, d_c11);
     }
 }
 
