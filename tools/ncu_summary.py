@@ -20,14 +20,14 @@ import subprocess
 import sys
 from collections import defaultdict
 
-STAGE_OF = [  # kernel-name regex -> bench stage name
+STAGE_OF = [  # kernel-name regex -> bench stage name (first capture of each kernel wins)
     (r"project_fwd_kernel", "project"),
-    (r"onesweep_kernel<unsigned int, (16|4)>", "sort_u32"),
-    (r"scan_kernel", "scan_emit"),
-    (r"emit_sorted_kernel", "scan_emit"),
+    (r"onesweep_kernel<unsigned int, (16|4)", "sort_u32"),
+    (r"emit_scan_kernel", "scan_emit"),
+    (r"segsort_warp_kernel", "segsort"),
     (r"ranges_u32_kernel", "tile_sort_ranges"),
     (r"raster_fwd_kernel", "raster_fwd"),
-    (r"raster_bwd_kernel", "raster_bwd"),
+    (r"raster_bwd_rec_kernel", "raster_bwd"),
     (r"project_bwd_kernel", "project_bwd"),
 ]
 
@@ -121,14 +121,8 @@ def full(rep, out, traffic_out=None):
             lines.append(f"    {'top stall reasons':32s} {stalls[kid]}")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
-    if traffic_out:
-        old = {}
-        try:
-            old = json.load(open(traffic_out))
-        except Exception:
-            pass
-        old.update({k: int(v) for k, v in traffic.items()})
-        json.dump(old, open(traffic_out, "w"), indent=1)
+    if traffic_out:  # rewritten from this capture only (no stale entries)
+        json.dump({k: int(v) for k, v in traffic.items()}, open(traffic_out, "w"), indent=1)
 
 
 if __name__ == "__main__":
