@@ -302,15 +302,29 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
             d_quats[i] = dq;
         }
     }
-    // block partial of d_view (deterministic: fixed shuffle tree + fixed warp order)
+    // block partial of d_view (deterministic: fixed shuffle tree + fixed warp
+    // order).  Transposed warp reduction of the 12 values padded to 16: each
+    // level exchanges half of the values, so 16 shuffles instead of 60.
     __shared__ float red[PBWD_THREADS / 32][12];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    {
+        float v16[16];
 #pragma unroll
-    for (int k = 0; k < 12; ++k) {
-        float v = dv[k];
+        for (int k = 0; k < 16; ++k) v16[k] = k < 12 ? dv[k] : 0.f;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) red[warp][k] = v;
+        for (int h = 8, m = 16; h >= 1; h >>= 1, m >>= 1) {  // lane bit m selects the kept half
+            const bool up = lane & m;
+#pragma unroll
+            for (int j = 0; j < h; ++j) {
+                const float send = up ? v16[j] : v16[j + h];
+                const float keep = up ? v16[j + h] : v16[j];
+                v16[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+            }
+        }
+        // v16[0] of lane L: value index (L >> 1), summed over the 16 lanes sharing (L & 1)
+        const float tot = v16[0] + __shfl_xor_sync(0xffffffffu, v16[0], 1);
+        const int k = lane >> 1;
+        if ((lane & 1) == 0 && k < 12) red[warp][k] = tot;
     }
     __syncthreads();
     if (threadIdx.x < 12) {
@@ -318,12 +332,12 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
 #pragma unroll
         for (int w = 0; w < PBWD_THREADS / 32; ++w) v += red[w][threadIdx.x];
         view_partials[blockIdx.x * 12 + threadIdx.x] = v;
+        if (done_counter) __threadfence();  // the writers' fence, before the last-block vote
     }
     if (!done_counter) return;  // a separate view_reduce_kernel finishes d_view
     // frame path: the last block to finish sums the partials (fixed order,
     // same tree as view_reduce_kernel) -- no extra kernel launch
     __shared__ bool s_last;
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = atomicAdd(done_counter, 1u) == gridDim.x - 1;
     __syncthreads();
