@@ -156,3 +156,23 @@ def test_autograd_matches_frame(cuda):
     for k in GRAD_CLASSES:
         r = grad_gate(got[k].detach().cpu().numpy(), ref[k])
         assert r["ok"], (k, r)
+
+
+def test_forward_bitwise_deterministic(cuda):
+    """forward outputs and tile lists are bitwise identical run to
+    run (the backward may differ through atomic order, which the north star
+    allows); the analogue of tests/test_acceptance.py:265-284 for the GPU."""
+    from paper_2312_02121_b200 import ops
+    from paper_2312_02121_b200.scenes import make_config
+    spec = make_config(1)
+    t = _tensors((spec.means, spec.scales, spec.quats, spec.opacities, spec.colors), cuda)
+    cam = ops.CameraParams.of(spec.cameras[0])
+    outs = []
+    for _ in range(3):
+        fr = ops.frame_forward(*t, cam, (0.1, 0.2, 0.3), True)
+        tv = fr.tensors()
+        outs.append((fr.image.clone(), fr.final_T.clone(), fr.n_contrib.clone(), tv["ranges"].clone(),
+                     tv["sorted_vals"].clone()))
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert torch.equal(a, b)
