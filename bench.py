@@ -58,6 +58,13 @@ def dist_env():
     return world, rank, local
 
 
+def tile_order_launches(cam):
+    """1 when the frame launches the heaviest-first tile-order kernel
+    (csrc/frame.cu: more tiles than one raster wave)."""
+    on = os.environ.get("GS_TILE_ORDER", "1") != "0"
+    return 1 if on and cam.tiles_x * cam.tiles_y > 148 * 8 else 0
+
+
 def segment_binning(n):
     """Which frame binning the library uses (csrc/frame.cu, gs_set_option)."""
     mode = int(os.environ.get("GS_BINNING", "0"))
@@ -431,9 +438,11 @@ def run_ours(args):
         "intersections_per_step_rank": int(I),
         "e2e": e2e,
         # per view: init, project, [4 depth passes], fused scan+emit, tp tile passes, ranges,
-        # [2 per-tile depth-sort kernels], raster fwd | raster bwd, project bwd (its last block reduces
-        # d_view); the bracketed parts are the depth-first vs per-tile-segment binning (csrc/frame.cu)
-        "gpu_launches": int(args.steps * len(cams) * ((9 if segment_binning(n) else 11) + tp)),
+        # [2 per-tile depth-sort kernels], (tile order), raster fwd | raster bwd, project bwd (its last
+        # block reduces d_view); the bracketed parts are the depth-first vs per-tile-segment binning
+        # (csrc/frame.cu), the tile-order kernel runs for grids over one raster wave
+        "gpu_launches": int(args.steps * len(cams) * ((9 if segment_binning(n) else 11) + tp
+                                                      + tile_order_launches(cams[0]))),
         "roofline": roof,
         "stages": st,
         "counts": {"E_f": int(counts_f[0]), "E_f_sigma": int(counts_f[1]), "E_f_alpha": int(counts_f[2]),

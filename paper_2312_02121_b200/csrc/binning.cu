@@ -445,6 +445,43 @@ int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* 
     return check_launch("emit_scan_kernel");
 }
 
+// Raster launch order: heaviest tile lists first, so the rasterizers' last
+// CTAs are short ones (uneven scenes otherwise end on a few long tiles).
+// Tiles are bucketed by floor(log2(list length)), buckets descending; order
+// within a bucket is arbitrary.  One CTA (n_tiles <= 65536).
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restrict__ ranges, int n_tiles,
+                                                          uint32_t* __restrict__ order) {
+    griddep_wait();
+    __shared__ uint32_t s_cnt[34];
+    if (threadIdx.x < 34) s_cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        const uint32_t len = r.y - r.x;
+        atomicAdd(&s_cnt[__clz(len)], 1u);  // clz: 0 = longest bucket ... 32 = empty
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int b = 0; b < 33; ++b) {
+            const uint32_t c = s_cnt[b];
+            s_cnt[b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        order[atomicAdd(&s_cnt[__clz(r.y - r.x)], 1u)] = (uint32_t)t;
+    }
+}
+
+int launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* order, cudaStream_t s) {
+    if (n_tiles <= 0) return 0;
+    launch_k(tile_order_kernel, dim3(1), dim3(1024), 0, s, ranges, n_tiles, order);
+    return check_launch("tile_order_kernel");
+}
+
 __global__ void __launch_bounds__(256) ranges_u32_kernel(const uint32_t* __restrict__ keys, int64_t n_cap,
                                                          const unsigned long long* __restrict__ n_dev,
                                                          uint2* __restrict__ ranges) {

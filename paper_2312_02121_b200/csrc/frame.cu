@@ -33,10 +33,20 @@ inline size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 int tile_passes_for(int n_tiles) { return n_tiles <= 256 ? 1 : 2; }
 
+// Heaviest-first tile order pays only when the raster grid is more than one
+// wave (148 SMs x 8 resident CTAs); GS_TILE_ORDER=0 disables it (A/B switch).
+bool tile_order_enabled(int n_tiles) {
+    static const bool on = [] {
+        const char* e = getenv("GS_TILE_ORDER");
+        return !(e && e[0] == '0');
+    }();
+    return on && n_tiles > 148 * 8;
+}
+
 struct Layout {
     // persistent (written each frame)
     size_t xydr, conic, tiles, dkeys, dkeys_alt, order, order_alt, offsets;
-    size_t tkeys, tkeys_alt, tvals, tvals_alt, ranges, rec, rec_count;
+    size_t tkeys, tkeys_alt, tvals, tvals_alt, ranges, rec, rec_count, tile_order;
     // zeroed region
     size_t zero_begin, meta, dhist, thist, counters, scan_ws, dstatus, tstatus, zero_end;
     // backward
@@ -69,6 +79,7 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.ranges = take(8 * nt);
     L.rec = take(8 * 4 * cap);    // forward commit records, 4 warp regions per tile list
     L.rec_count = take(16 * nt);  // records per (tile, warp)
+    L.tile_order = take(4 * nt);  // raster launch order (heaviest lists first)
     L.zero_begin = o;
     L.meta = take(16);
     L.dhist = take(4 * 256 * 4);
@@ -206,12 +217,16 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     if (segment && launch_segsort(at<uint2>(ws, L.ranges), tiles_x * tiles_y, at<uint32_t>(ws, L.dkeys),
                                   const_cast<uint32_t*>(svals), at<uint32_t>(ws, odd ? L.tvals : L.tvals_alt), s))
         return -1;
+    // 6c. heaviest-first raster launch order
+    const uint32_t* t_order = tile_order_enabled(tiles_x * tiles_y) ? at<uint32_t>(ws, L.tile_order) : nullptr;
+    if (t_order && launch_tile_order(at<uint2>(ws, L.ranges), tiles_x * tiles_y, at<uint32_t>(ws, L.tile_order), s))
+        return -1;
     mark(stage_events, 4, s);
     // 7. raster forward
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
     if (launch_raster_fwd(at<uint2>(ws, L.ranges), svals, at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3,
                           bg, W, H, early_termination != 0, out_image, out_final_T, out_n_contrib, counts4, s,
-                          at<uint2>(ws, L.rec), at<uint32_t>(ws, L.rec_count)))
+                          at<uint2>(ws, L.rec), at<uint32_t>(ws, L.rec_count), t_order))
         return -1;
     mark(stage_events, 5, s);
     return 0;
@@ -244,7 +259,8 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
             return -1;
     } else if (launch_raster_bwd_rec(at<uint2>(ws, L.ranges), at<uint2>(ws, L.rec), at<uint32_t>(ws, L.rec_count),
                                      at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3, bg, W, H, final_T,
-                                     n_contrib, d_image, g8, at<float>(ws, L.d_c11), s)) {
+                                     n_contrib, d_image, g8, at<float>(ws, L.d_c11), s,
+                                     tile_order_enabled(tiles_x * tiles_y) ? at<uint32_t>(ws, L.tile_order) : nullptr)) {
         return -1;
     }
     mark(stage_events, 1, s);

@@ -48,6 +48,8 @@ size_t emit_scan_ws_bytes(int64_t n);
 int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* counts, int64_t n, int tiles_x,
                      int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals, uint32_t* tile_hist,
                      int tile_passes, void* ws, unsigned long long* total, cudaStream_t s);
+// heaviest-first raster launch order of the tiles (one CTA)
+int launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* order, cudaStream_t s);
 int launch_ranges_u64(const unsigned long long* sorted_keys, int64_t n, uint2* ranges,
                       cudaStream_t s);  // ranges must be zeroed
 int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const unsigned long long* n_dev,
@@ -63,11 +65,12 @@ int binning_mode();
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
                       unsigned long long* counts, cudaStream_t s, uint2* rec = nullptr,
-                      uint32_t* rec_count = nullptr);
+                      uint32_t* rec_count = nullptr, const uint32_t* tile_order = nullptr);
 // record-driven backward of the frame path (records written by the forward)
 int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
-                          const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s);
+                          const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s,
+                          const uint32_t* tile_order = nullptr);
 int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, const float* fT, const int* nc,
                       const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11, unsigned long long* counts,

@@ -188,12 +188,13 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
                                                               float* __restrict__ out_T, int* __restrict__ out_nc,
                                                               unsigned long long* __restrict__ counts,
                                                               uint2* __restrict__ rec,
-                                                              uint32_t* __restrict__ rec_count) {
+                                                              uint32_t* __restrict__ rec_count,
+                                                              const uint32_t* __restrict__ tile_order) {
     griddep_wait();
     constexpr int NPR = 4 / NWR;
     static_assert(!REC || NWR == 4, "records are per 8x8 quadrant");
     __shared__ BatchT<NWR> s;
-    const int tile = blockIdx.x;
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int col = tx * TILE + (warp & 1) * 8 + (lane & 7);
@@ -643,13 +644,14 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     const uint2* __restrict__ ranges, const uint2* __restrict__ rec, const uint32_t* __restrict__ rec_count,
     const float4* __restrict__ xydr, const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg,
     int W, int H, int tiles_x, const float* __restrict__ final_T, const int* __restrict__ n_contrib,
-    const float* __restrict__ d_img, float* __restrict__ g8, float* __restrict__ d_c11) {
+    const float* __restrict__ d_img, float* __restrict__ g8, float* __restrict__ d_c11,
+    const uint32_t* __restrict__ tile_order) {
     griddep_wait();
     __shared__ float4 s_a[4][32], s_b[4][32];
     __shared__ float s_c[4][32];
     __shared__ uint32_t s_id[4][32], s_pos[4][32];
     __shared__ __align__(16) float s_red[4][RBS][9][RROW];
-    const int tile = blockIdx.x;
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int col = tx * TILE + (warp & 1) * 8 + (lane & 7);
@@ -778,19 +780,20 @@ static int fwd_regions() {
 
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
-                      unsigned long long* counts, cudaStream_t s, uint2* rec, uint32_t* rec_count) {
+                      unsigned long long* counts, cudaStream_t s, uint2* rec, uint32_t* rec_count,
+                      const uint32_t* tile_order) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     const float4* g = (const float4*)xydr4;
     const float4* q = (const float4*)conic4;
 #define GS_FWD_R(NWR, ET, CNT, REC)                                                                          \
     raster_fwd_kernel<NWR, ET, CNT, REC><<<nt, 32 * NWR, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, \
-                                                                 img, T, nc, counts, rec, rec_count)
+                                                                 img, T, nc, counts, rec, rec_count, tile_order)
 #define GS_FWD(NWR, ET, CNT) GS_FWD_R(NWR, ET, CNT, false)
     const bool cnt = counts != nullptr;
 #define GS_FWD_M(ET, M)                                                                                        \
     launch_k(raster_fwd_kernel<4, ET, false, true, M>, dim3(nt), dim3(128), 0, s, ranges, vals, g, q, colors3, bg, \
-             W, H, tiles_x, img, T, nc, counts, rec, rec_count)
+             W, H, tiles_x, img, T, nc, counts, rec, rec_count, tile_order)
     if (rec && !cnt) {  // frame path: 8x8 quadrants with commit records, 9 CTAs/SM (measured best)
         if (et) GS_FWD_M(true, 9); else GS_FWD_M(false, 9);
     } else if (rec) {
@@ -831,10 +834,12 @@ int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xy
 
 int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
-                          const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s) {
+                          const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s,
+                          const uint32_t* tile_order) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     launch_k(raster_bwd_rec_kernel, dim3((unsigned)(tiles_x * tiles_y)), dim3(128), 0, s, ranges, rec, rec_count,
-             (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H, tiles_x, fT, nc, dimg, g8, d_c11);
+             (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H, tiles_x, fT, nc, dimg, g8, d_c11,
+             tile_order);
     return check_launch("raster_bwd_rec_kernel");
 }
 
