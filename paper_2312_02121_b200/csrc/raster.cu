@@ -9,13 +9,13 @@
 // Bound: FP32 issue (DESIGN.md roofline).
 //
 // Staging: the tile's sorted splat records are loaded RB = 128 at a time
-// into shared memory.  Each staged splat's bounding square (the radius-r
-// square sg/binning.py:35-46 bins by), grown by one pixel, is tested against
-// the four quadrants and every warp gets a compacted, order-preserving list
-// of the batch entries that can reach it.  A skipped (pixel, splat) pair lies
-// more than a pixel outside the 3-sigma square, so sigma > 4.5 there with a
-// wide margin: the skip never changes a decision, and forward and backward
-// (same lists) replay identical evaluation sequences.
+// into shared memory.  Each staged splat's sigma <= 4.5 ellipse (slightly
+// inflated, see stage_batch) is intersected exactly with the four quadrants
+// and every warp gets a compacted, order-preserving list of the batch
+// entries that can reach it (a third fewer than the ellipse's bounding box
+// admits).  A skipped (pixel, splat) pair has sigma > 4.5 with margin, so the
+// skip never changes a decision, and forward and backward (same lists) replay
+// identical evaluation sequences.
 //
 // The per-pixel work after the sigma cut is straight-line predicated code on
 // the pair (no per-pixel branches); the forward processes two list entries
@@ -69,14 +69,18 @@ __device__ __forceinline__ int stage_batch(BatchT<NWR>& s, int tile, int tiles_x
                                            int first, int count, const float4* __restrict__ xydr,
                                            const float4* __restrict__ conic, const float* __restrict__ colors) {
     constexpr int NTR = 32 * NWR;
-    constexpr float RH = NWR == 4 ? 7.f : 15.f;  // region height - 1 (pixel rows)
+    constexpr int NB = NWR == 4 ? 2 : 1;           // row bands of the tile (8 or 16 rows)
+    constexpr float RH = NWR == 4 ? 7.f : 15.f;  // band height - 1 (pixel rows)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
 #pragma unroll
     for (int u = 0; u < RB / NTR; ++u) {
         const int k = u * NTR + (int)threadIdx.x;
         const bool valid = k < count;
-        float x = 0.f, y = 0.f, rx = -1e30f, ry = -1e30f;
+        // per row band: the ellipse's x-interval [x + xl, x + xr] inside the band
+        float x = 0.f, xl[NB], xr[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) xl[j] = 1e30f, xr[j] = -1e30f;
         if (valid) {
             const uint32_t id = ids[first + k];
             const float4 g = xydr[id];
@@ -86,22 +90,58 @@ __device__ __forceinline__ int stage_batch(BatchT<NWR>& s, int tile, int tiles_x
             s.c[k] = colors[3 * id + 2];
             s.id[k] = id;
             x = g.x;
-            y = g.y;
-            // Reach of the sigma <= 4.5 ellipse {d : d^T Q d <= 9} of this
-            // conic Q: |dx| <= 3 sqrt(Q_yy / det Q), |dy| <= 3 sqrt(Q_xx /
-            // det Q) (tighter than the circle radius the tiles are binned
-            // by), grown by 0.1% and one pixel so fp32 rounding cannot
-            // un-skip a pair; never more than the circle.
+            // Exact reach of the sigma <= 4.5 ellipse {d : d^T Q d <= 9} of
+            // the conic Q = [A B; B C] in each band dy in [lo, hi]: x extends
+            // to (-B dy +- sqrt(K A - det dy^2)) / A, concave / convex in dy,
+            // so the extremes sit at dy = -+ B sqrt(K / (C det)) clamped to
+            // the band.  K = 9 (1 + 0.4%) absorbs the fp32 rounding of both
+            // this test and the pixels' sigma, which is bounded by ~8 eps 9
+            // / (1 - |rho|) for the conic's correlation rho: entries with
+            // 1 - rho^2 < 1e-3 (needle-thin) use the axis-aligned box grown
+            // by one pixel instead; the band extents get a 0.01 px + 0.2%
+            // pad for their own rounding.  Either way the skip never drops a pair
+            // the sigma cut would keep.  The circle radius (the binning
+            // bound, sg/binning.py:35-46) caps both.
+            const float A = q.x, B = q.y, Cq = q.z;
+            const float det = __fmaf_rn(A, Cq, -__fmul_rn(B, B));
             const float r = (float)__float_as_int(g.w) + 1.f;
-            const float idq = rcp_approx(__fmaf_rn(q.x, q.z, -__fmul_rn(q.y, q.y)));
-            rx = fminf(r, __fmaf_rn(3.003f, sqrt_approx(q.z * idq), 1.f));
-            ry = fminf(r, __fmaf_rn(3.003f, sqrt_approx(q.x * idq), 1.f));
+            const float idq = rcp_approx(det);
+            if (det > 1e-3f * A * Cq) {
+                constexpr float K = 9.036f;
+                const float rx = fminf(r, sqrt_approx(K * Cq * idq));
+                const float ry = fminf(r, sqrt_approx(K * A * idq));
+                const float iA = rcp_approx(A);
+                const float ds = -B * sqrt_approx(K * idq * rcp_approx(Cq));  // dy of the max-x point
+                // sqrt(K A - det dy^2) near the band's tangent rows loses up to
+                // sqrt(4 eps K A) / A <= 5e-4 rx (as 1/sqrt(A) <= rx/3)
+                const float pad = __fmaf_rn(2e-3f, rx, 0.01f);
+#pragma unroll
+                for (int j = 0; j < NB; ++j) {
+                    const float lo = fmaxf((float)(ty * TILE + 8 * j) + 0.5f - g.y, -ry);
+                    const float hi = fminf((float)(ty * TILE + 8 * j) + 0.5f + RH - g.y, ry);
+                    if (lo <= hi) {
+                        const float d1 = fminf(fmaxf(ds, lo), hi), d2 = fminf(fmaxf(-ds, lo), hi);
+                        const float s1 = sqrt_approx(fmaxf(__fmaf_rn(-det, d1 * d1, K * A), 0.f));
+                        const float s2 = sqrt_approx(fmaxf(__fmaf_rn(-det, d2 * d2, K * A), 0.f));
+                        xr[j] = fminf((s1 - B * d1) * iA, rx) + pad;
+                        xl[j] = fmaxf((-s2 - B * d2) * iA, -rx) - pad;
+                    }
+                }
+            } else {
+                const float rx = fminf(r, __fmaf_rn(3.003f, sqrt_approx(Cq * idq), 1.f));
+                const float ry = fminf(r, __fmaf_rn(3.003f, sqrt_approx(A * idq), 1.f));
+#pragma unroll
+                for (int j = 0; j < NB; ++j) {
+                    const float y0 = (float)(ty * TILE + 8 * j) + 0.5f;
+                    if (g.y + ry >= y0 && g.y - ry <= y0 + RH) xl[j] = -rx, xr[j] = rx;
+                }
+            }
         }
 #pragma unroll
         for (int w = 0; w < NWR; ++w) {
+            const int j = NB == 2 ? (w >> 1) : 0;
             const float x0 = (float)(tx * TILE + (w & 1) * 8) + 0.5f;
-            const float y0 = (float)(ty * TILE + (NWR == 4 ? (w >> 1) * 8 : 0)) + 0.5f;
-            const bool ov = valid && x + rx >= x0 && x - rx <= x0 + 7.f && y + ry >= y0 && y - ry <= y0 + RH;
+            const bool ov = x + xr[j] >= x0 && x + xl[j] <= x0 + 7.f;
             const uint32_t m = __ballot_sync(0xffffffffu, ov);
             if (lane == 0) s.mask[w][u * NWR + warp] = m;
         }
