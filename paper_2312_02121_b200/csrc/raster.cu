@@ -659,23 +659,41 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
 constexpr int RBS = 3;        // records per reduction batch (9 * RBS <= 32 rows: one row per lane)
 constexpr int RROW = 36;      // row stride (words): 32 lanes + pad
 
+// A staged record: the splat's (x, y, A/2, B), (C/2, opacity, r, g) and
+// (b, list position, splat id, -) -- one base address, three LDS.128.
+struct __align__(16) RecStage {
+    float4 a, b, c;
+};
+constexpr uint32_t REC_BYTES = sizeof(RecStage);
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+
 // Sum the batch's 9 * nslot rows (one per lane) and add each to its
 // splat's gradient slot.  red: this warp's batch (32-bit shared address),
-// kslots: the batch's staged-record indices (8 bits each), ids: this warp's
-// staged splat ids.
-__device__ __forceinline__ void bwd_flush(uint32_t red, uint32_t kslots, const uint32_t* ids, int nslot, int lane,
+// kslots: the batch's staged-record indices (8 bits each), stage: this
+// warp's staged records.  The conic rows (6..8) were accumulated without
+// their factor 1/2, applied here (exact).
+__device__ __forceinline__ void bwd_flush(uint32_t red, uint32_t kslots, uint32_t stage, int nslot, int lane,
                                           float* __restrict__ g8, float* __restrict__ d_c11) {
     if (lane < 9 * nslot) {
         const int k = lane / 9, t = lane - 9 * k;
         const uint32_t row = red + (uint32_t)lane * (RROW * 4);
-        float4 a = lds_f4(row);
+        const float4 a = lds_f4(row);
+        f32x2 s01 = pk2(a.x, a.y), s23 = pk2(a.z, a.w);
 #pragma unroll
         for (int j = 1; j < 8; ++j) {
             const float4 b = lds_f4(row + 16 * j);
-            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+            s01 = add2(s01, pk2(b.x, b.y));
+            s23 = add2(s23, pk2(b.z, b.w));
         }
-        const float sum = (a.x + a.y) + (a.z + a.w);
-        const uint32_t id = ids[(kslots >> (8 * k)) & 255u];
+        const f32x2 s2 = add2(s01, s23);
+        float sum = lo2(s2) + hi2(s2);
+        if (t >= 6) sum *= 0.5f;
+        const uint32_t id = lds_u32(stage + ((kslots >> (8 * k)) & 255u) * REC_BYTES + 40u);
         atomicAdd(t < 8 ? g8 + 8 * (size_t)id + t : d_c11 + id, sum);
     }
 }
@@ -687,9 +705,7 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     const float* __restrict__ d_img, float* __restrict__ g8, float* __restrict__ d_c11,
     const uint32_t* __restrict__ tile_order) {
     griddep_wait();
-    __shared__ float4 s_a[4][32], s_b[4][32];
-    __shared__ float s_c[4][32];
-    __shared__ uint32_t s_id[4][32], s_pos[4][32];
+    __shared__ RecStage s_rec[4][32];
     __shared__ __align__(16) float s_red[4][RBS][9][RROW];
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -718,6 +734,7 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     const int count = (int)rec_count[(size_t)tile * 4 + warp];
     const int warp_nc = __reduce_max_sync(0xffffffffu, max(nc[0], nc[1]));
     const uint32_t red_w = smem_addr(&s_red[warp][0][0][0]);
+    const uint32_t stage_w = smem_addr(&s_rec[warp][0]);
     int nslot = 0;
     uint32_t kslots = 0;
     for (int hi = count; hi > 0; hi -= 32) {
@@ -727,25 +744,30 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             const uint2 r = rec[rb + lo + lane];
             const float4 g = xydr[r.x];
             const float4 q = conic[r.x];
-            s_a[warp][lane] = make_float4(g.x, g.y, 0.5f * q.x, q.y);
-            s_b[warp][lane] = make_float4(0.5f * q.z, q.w, colors[3 * r.x], colors[3 * r.x + 1]);
-            s_c[warp][lane] = colors[3 * r.x + 2];
-            s_id[warp][lane] = r.x;
-            s_pos[warp][lane] = r.y;
+            RecStage& st = s_rec[warp][lane];
+            st.a = make_float4(g.x, g.y, 0.5f * q.x, q.y);
+            st.b = make_float4(0.5f * q.z, q.w, colors[3 * r.x], colors[3 * r.x + 1]);
+            st.c = make_float4(colors[3 * r.x + 2], __int_as_float((int)r.y), __int_as_float((int)r.x), 0.f);
         }
         __syncwarp();
 #pragma unroll 1
         for (int k = nb - 1; k >= 0; --k) {
-            const int pos = (int)s_pos[warp][k];
+            const uint32_t sk = stage_w + (uint32_t)k * REC_BYTES;
+            const float4 cq = lds_f4(sk + 32);
+            const int pos = __float_as_int(cq.y);
             if (pos >= warp_nc) continue;  // beyond every pixel's last contribution (warp-uniform)
-            const float4 a = s_a[warp][k];
-            const float4 bq = s_b[warp][k];
-            const float blue = s_c[warp][k];
+            const float4 a = lds_f4(sk);
+            const float4 bq = lds_f4(sk + 16);
+            const float blue = cq.x;
             const float hC = bq.x;
             const float dx = __fsub_rn(px, a.x);
             const float hAdx = __fmul_rn(a.z, dx);
             const f32x2 DY = sub2(PY, bc2(a.y));
-            const f32x2 SG = splat_sigma2(dx, hAdx, DY, a.w, hC);
+            // splat_sigma2 with its intermediates kept: P = A/2 dx + B dy,
+            // QC = C/2 dy; sigma = dx P + QC dy (same ops, same bits)
+            const f32x2 P = fma2(bc2(a.w), DY, bc2(hAdx));
+            const f32x2 QC = mul2(bc2(hC), DY);
+            const f32x2 SG = fma2(bc2(dx), P, mul2(QC, DY));
             const f32x2 SL = mul2(SG, bc2(NEG_LOG2E));
             const f32x2 E = pk2(ex2_approx(lo2(SL)), ex2_approx(hi2(SL)));
             const f32x2 ARAW = mul2(bc2(bq.y), E);
@@ -765,12 +787,12 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             const bool l0 = c0 && lo2(ARAW) < ALPHA_MAX, l1 = c1 && hi2(ARAW) < ALPHA_MAX;
             const f32x2 DAL = pk2(l0 ? lo2(DA) : 0.f, l1 ? hi2(DA) : 0.f);
             const f32x2 M = mul2(ARAW, DAL);
-            const f32x2 Y0 = fma2(bc2(a.w), DY, bc2(2.f * a.z * dx));
-            const f32x2 Y1 = fma2(bc2(2.f * hC), DY, bc2(a.w * dx));
-            const f32x2 HM = mul2(bc2(0.5f), M);
-            const f32x2 HY0 = mul2(HM, Y0), HY1 = mul2(HM, Y1);
-            const f32x2 D[9] = {mul2(WC, G0), mul2(WC, G1), mul2(WC, G2), mul2(DAL, E), mul2(M, Y0),
-                                mul2(M, Y1),  mul2(HY0, Y0), mul2(HY0, Y1), mul2(HY1, Y1)};
+            const f32x2 Y0 = add2(P, bc2(hAdx));                      // A dx + B dy
+            const f32x2 Y1 = fma2(bc2(2.f), QC, bc2(__fmul_rn(a.w, dx)));  // B dx + C dy
+            const f32x2 MY0 = mul2(M, Y0), MY1 = mul2(M, Y1);
+            // rows 6..8 are M Y Y without the 1/2 of d sigma / d conic (bwd_flush applies it)
+            const f32x2 D[9] = {mul2(WC, G0), mul2(WC, G1), mul2(WC, G2), mul2(DAL, E), MY0,
+                                MY1,          mul2(MY0, Y0), mul2(MY0, Y1), mul2(MY1, Y1)};
             const uint32_t slot = red_w + (uint32_t)nslot * (9 * RROW * 4) + 4 * lane;
 #pragma unroll
             for (int u = 0; u < 9; ++u) sts_f32(slot + u * (RROW * 4), lo2(D[u]) + hi2(D[u]));
@@ -781,7 +803,7 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             T = sel2(c0, c1, TH, T);
             if (++nslot == RBS) {
                 __syncwarp();
-                bwd_flush(red_w, kslots, s_id[warp], RBS, lane, g8, d_c11);
+                bwd_flush(red_w, kslots, stage_w, RBS, lane, g8, d_c11);
                 __syncwarp();
                 nslot = 0;
                 kslots = 0;
@@ -789,7 +811,7 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
         }
         if (nslot) {  // the batch refers to this staging chunk's ids: flush before restaging
             __syncwarp();
-            bwd_flush(red_w, kslots, s_id[warp], nslot, lane, g8, d_c11);
+            bwd_flush(red_w, kslots, stage_w, nslot, lane, g8, d_c11);
             nslot = 0;
             kslots = 0;
         }
