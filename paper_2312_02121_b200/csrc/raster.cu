@@ -44,6 +44,7 @@ struct BatchT {
     uint32_t id[RB];
     uint32_t mask[NWR][RB / 32];  // region reach bits per group of 32 entries
     __align__(4) uint8_t list[NWR][RB + 2];  // compacted entry indices per region (+ sentinel pad)
+    uint8_t rbuf[NWR][RB];                   // forward records of this batch (entry indices, per region)
 };
 using Batch = BatchT<NW>;
 
@@ -204,14 +205,28 @@ __device__ __forceinline__ void fwd_commit(FwdPair& p, f32x2 SG, bool vis0, bool
     }
 }
 
-// Record of one (warp, list entry) for the backward: the splat id and its
-// 0-based position in the tile list, written for every entry whose commit
-// step this warp ran (some pixel of the quadrant passed the sigma cut) --
-// a warp-uniform condition the forward already has, so recording costs no
+// Records of (warp, list entry) for the backward: the splat id and its
+// 0-based position in the tile list, for every entry whose commit step this
+// warp ran (some pixel of the quadrant passed the sigma cut) -- a
+// warp-uniform condition the forward already has, so recording costs no
 // extra vote.  The backward replays exactly these entries, back to front.
-__device__ __forceinline__ void fwd_record(uint2*& rp, uint32_t id, int pos0) {
-    if ((threadIdx.x & 31) == 0) *rp = make_uint2(id, (uint32_t)pos0);
-    ++rp;
+// Per entry one byte goes to the warp's shared buffer; the batch's records
+// are written out coalesced when the warp leaves the batch.
+template <int NWR>
+__device__ __forceinline__ void fwd_record(BatchT<NWR>& s, int warp, int lane, int& nrec, int k) {
+    if (lane == 0) s.rbuf[warp][nrec] = (uint8_t)k;
+    ++nrec;
+}
+template <int NWR>
+__device__ __forceinline__ void fwd_record_flush(const BatchT<NWR>& s, int warp, int lane, int& nrec, uint2*& rp,
+                                                 int pos0) {
+    __syncwarp();
+    for (int j = lane; j < nrec; j += 32) {
+        const int k = s.rbuf[warp][j];
+        rp[j] = make_uint2(s.id[k], (uint32_t)(pos0 + k));
+    }
+    rp += nrec;
+    nrec = 0;
 }
 
 // sg/raster_forward.py:116-154 _composite_tile for one tile.
@@ -266,6 +281,7 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
     unsigned long long e_s = 0, e_a = 0, e_c = 0;
     // this warp's record region: 4 * start + warp * len (no atomics)
     uint2* rp = REC ? rec + 4 * (int64_t)start + (int64_t)warp * (end - start) : nullptr;
+    int nrec = 0;
     if (threadIdx.x == 0) {  // sentinel entry: dx = -inf -> sigma NaN -> never visible
         s.a[RB] = make_float4(INF, 0.f, 0.f, 0.f);
         s.b[RB] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -295,17 +311,18 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
                 if (COUNT) e_s += (unsigned)v00 + (unsigned)v01;
                 if (b0m) {
                     fwd_commit<ET, COUNT>(p[0], SG0, v00, v01, s.b[k0], s.c[k0], pos_base + k0, e_a, e_c);
-                    if (REC) fwd_record(rp, s.id[k0], pos_base + k0 - 1);
+                    if (REC) fwd_record(s, warp, lane, nrec, k0);
                 }
                 v10 = v10 && !(p[0].done & 1u);  // retired at k0
                 v11 = v11 && !(p[0].done & 2u);
                 if (COUNT) e_s += (unsigned)v10 + (unsigned)v11;
                 if (b1m) {  // never the sentinel (its sigma is NaN)
                     fwd_commit<ET, COUNT>(p[0], SG1, v10, v11, s.b[k1], s.c[k1], pos_base + k1, e_a, e_c);
-                    if (REC) fwd_record(rp, s.id[k1], pos_base + k1 - 1);
+                    if (REC) fwd_record(s, warp, lane, nrec, k1);
                 }
                 if (ET && (b0m | b1m) && __all_sync(0xffffffffu, p[0].done == 3u)) break;
             }
+            if (REC) fwd_record_flush(s, warp, lane, nrec, rp, pos_base - 1);
         } else {
             const uint8_t* lst = s.list[warp];
 #pragma unroll 1
@@ -857,7 +874,13 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
     launch_k(raster_fwd_kernel<4, ET, false, true, M>, dim3(nt), dim3(128), 0, s, ranges, vals, g, q, colors3, bg, \
              W, H, tiles_x, img, T, nc, counts, rec, rec_count, tile_order)
     if (rec && !cnt) {  // frame path: 8x8 quadrants with commit records, 9 CTAs/SM (measured best)
-        if (et) GS_FWD_M(true, 9); else GS_FWD_M(false, 9);
+        static const int minb = [] {
+            const char* e = getenv("GS_FWD_MINB");
+            return e ? atoi(e) : 9;
+        }();
+        if (minb == 8) { if (et) GS_FWD_M(true, 8); else GS_FWD_M(false, 8); }
+        else if (minb == 10) { if (et) GS_FWD_M(true, 10); else GS_FWD_M(false, 10); }
+        else { if (et) GS_FWD_M(true, 9); else GS_FWD_M(false, 9); }
     } else if (rec) {
         if (et) GS_FWD_R(4, true, true, true); else GS_FWD_R(4, false, true, true);
     } else if (fwd_regions() == 2) {
