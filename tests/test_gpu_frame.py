@@ -176,3 +176,29 @@ def test_forward_bitwise_deterministic(cuda):
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("config", [1, 2])
+def test_binning_strategies_agree_on_configs(config, cuda):
+    """Both binnings on BASELINE configs: config 2's lists run to thousands of
+    entries, so the segment path's long-list CTA sort (len > 512) is covered
+    besides the one-warp sort."""
+    from paper_2312_02121_b200 import ops
+    from paper_2312_02121_b200.scenes import make_config
+    spec = make_config(config, n_views=1)
+    t = _tensors((spec.means, spec.scales, spec.quats, spec.opacities, spec.colors), cuda)
+    cam = ops.CameraParams.of(spec.cameras[0])
+    got = {}
+    try:
+        for mode in (1, 2):
+            ops.set_option("binning", mode)
+            fr = ops.frame_forward(*t, cam, (0.0, 0.0, 0.0), True)
+            tv = fr.tensors()
+            got[mode] = (tv["ranges"].clone(), tv["sorted_vals"].clone(), fr.image.clone())
+    finally:
+        ops.set_option("binning", 0)
+    lens = (got[1][0][:, 1] - got[1][0][:, 0])
+    if config == 2:
+        assert int(lens.max()) > 512
+    for a, b in zip(got[1], got[2]):
+        assert torch.equal(a, b)
