@@ -437,12 +437,13 @@ def run_ours(args):
         "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
         "intersections_per_step_rank": int(I),
         "e2e": e2e,
-        # per view: init, project, [4 depth passes], fused scan+emit, tp tile passes, ranges,
-        # [2 per-tile depth-sort kernels], (tile order), raster fwd | raster bwd, project bwd (its last
-        # block reduces d_view); the bracketed parts are the depth-first vs per-tile-segment binning
-        # (csrc/frame.cu), the tile-order kernel runs for grids over one raster wave
-        "gpu_launches": int(args.steps * len(cams) * ((9 if segment_binning(n) else 11) + tp
-                                                      + tile_order_launches(cams[0]))),
+        # per view (csrc/frame.cu): scatter binning: init, project (+ tile counts), tile scan
+        # (+ raster order), pair scatter, 2 per-tile sort kernels, raster fwd | raster bwd, project bwd
+        # (its last block reduces d_view); depth-first: init, project, 4 depth passes, fused
+        # scan+emit, tp tile passes, ranges, (tile order for grids over one raster wave), raster fwd |
+        # raster bwd, project bwd
+        "gpu_launches": int(args.steps * len(cams) * (9 if segment_binning(n) else
+                                                      11 + tp + tile_order_launches(cams[0]))),
         "roofline": roof,
         "stages": st,
         "counts": {"E_f": int(counts_f[0]), "E_f_sigma": int(counts_f[1]), "E_f_alpha": int(counts_f[2]),

@@ -445,6 +445,159 @@ int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* 
     return check_launch("emit_scan_kernel");
 }
 
+// ---------------------------------------------------------------- scatter binning
+// Small scenes (frame.cu): the projection counts every tile's intersections
+// (project_fwd_kernel<2>); one CTA scans those counts into the tile ranges
+// and per-tile write cursors; every pair is then written straight into its
+// tile's range through an atomic cursor -- no global sort by tile.  The
+// order inside a range is arbitrary; segsort.cu sorts each range by
+// (depth, source index) afterwards.
+
+// One CTA of 1024 threads (n_tiles <= 65536): exclusive scan of the tile
+// counts (TCOUNT_REPL replicas, summed) -> ranges and per-replica cursors
+// (tcount is overwritten in place), total -> *total.  Warp w owns a
+// contiguous chunk of tiles and walks it 32 tiles at a time (coalesced
+// replica reads): one sweep for the chunk total, a block scan over the 32
+// chunk totals, a second sweep that writes.  Over capacity: every range
+// empty and every cursor at capacity (the scatter then writes nothing; the
+// host reruns with more room).  order != nullptr: also the heaviest-first
+// raster launch order (tile_order_kernel's bucketing).
+__global__ void __launch_bounds__(1024) tile_scan_kernel(uint32_t* __restrict__ tcount, int n_tiles,
+                                                         int64_t capacity, uint2* __restrict__ ranges,
+                                                         unsigned long long* __restrict__ total,
+                                                         uint32_t* __restrict__ order) {
+    griddep_wait();
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_bucket[34];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int chunk = (((n_tiles + 31) >> 5) + 31) & ~31;  // tiles per warp, a multiple of 32
+    const int c0 = warp * chunk, c1 = min(n_tiles, c0 + chunk);
+    if (tid < 34) s_bucket[tid] = 0u;
+    auto tile_count = [&](int t) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int r = 0; r < TCOUNT_REPL; ++r) c += tcount[(size_t)r * n_tiles + t];
+        return c;
+    };
+    uint32_t sum = 0;
+    for (int t = c0 + lane; t < c1; t += 32) sum += tile_count(t);
+    sum = __reduce_add_sync(0xffffffffu, sum);
+    if (lane == 0) s_warp[warp] = sum;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = s_warp[lane];
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_warp[lane] = wi - w;  // exclusive chunk offsets
+        if (lane == 31) {
+            *total = (unsigned long long)wi;
+            s_bucket[33] = wi;
+        }
+    }
+    __syncthreads();
+    const bool over = (int64_t)s_bucket[33] > capacity;
+    uint32_t run = s_warp[warp];
+    for (int tb = c0; tb < c1; tb += 32) {
+        const int t = tb + lane;
+        const bool in = t < c1;
+        uint32_t cr[TCOUNT_REPL], c = 0;
+#pragma unroll
+        for (int r = 0; r < TCOUNT_REPL; ++r) {
+            cr[r] = in ? tcount[(size_t)r * n_tiles + t] : 0u;
+            c += cr[r];
+        }
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t start = run + incl - c;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+        if (in) {
+            uint32_t cur = start;
+#pragma unroll
+            for (int r = 0; r < TCOUNT_REPL; ++r) {  // replica r's cursor: the tile start + earlier replicas
+                tcount[(size_t)r * n_tiles + t] = over ? (uint32_t)capacity : cur;
+                cur += cr[r];
+            }
+            if (over) c = 0;
+            ranges[t] = c ? make_uint2(start, start + c) : make_uint2(0u, 0u);  // empty tiles: (0, 0)
+            if (order) atomicAdd(&s_bucket[__clz(c)], 1u);  // clz: 0 = longest bucket ... 32 = empty
+        }
+    }
+    if (!order) return;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t b_run = 0;
+        for (int b = 0; b < 33; ++b) {
+            const uint32_t c = s_bucket[b];
+            s_bucket[b] = b_run;
+            b_run += c;
+        }
+    }
+    __syncthreads();
+    for (int t = c0 + lane; t < c1; t += 32) {
+        const uint2 r = ranges[t];  // this thread's own writes
+        order[atomicAdd(&s_bucket[__clz(r.y - r.x)], 1u)] = (uint32_t)t;
+    }
+}
+
+int launch_tile_scan(uint32_t* tcount, int n_tiles, int64_t capacity, uint2* ranges, unsigned long long* total,
+                     uint32_t* order, cudaStream_t s) {
+    if (n_tiles <= 0 || n_tiles > 65536) return set_error("tile_scan: %d tiles out of range", n_tiles);
+    launch_k(tile_scan_kernel, dim3(1), dim3(1024), 0, s, tcount, n_tiles, capacity, ranges, total, order);
+    return check_launch("tile_scan_kernel");
+}
+
+// Every visible Gaussian's (tile, gaussian) pairs into the tiles' ranges
+// through the atomic cursors; warps walk 32 Gaussians' rects together.
+__global__ void __launch_bounds__(256) scatter_pairs_kernel(const float4* __restrict__ xydr,
+                                                            const uint32_t* __restrict__ counts, int n, int tiles_x,
+                                                            int tiles_y, uint32_t capacity,
+                                                            uint32_t* __restrict__ cursors,
+                                                            uint32_t* __restrict__ tile_keys,
+                                                            uint32_t* __restrict__ vals) {
+    griddep_wait();
+    const int n_round = (n + 31) & ~31;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += gridDim.x * blockDim.x) {
+        int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
+        if (i < n && counts[i]) {
+            const float4 g = xydr[i];
+            tile_rect(g.x, g.y, __float_as_int(g.w), tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+        }
+        uint32_t* cur = cursors + (size_t)tcount_replica((uint32_t)i) * (tiles_x * tiles_y);
+        walk_tile_rects<2>(threadIdx.x & 31, (uint32_t)i, tx0, tx1, ty0, ty1, tiles_x,
+                           [&](const uint32_t* tl, const uint32_t* gl) {
+                               uint32_t slot[2];
+#pragma unroll
+                               for (int u = 0; u < 2; ++u)
+                                   slot[u] = tl[u] != 0xFFFFFFFFu ? atomicAdd(&cur[tl[u]], 1u) : capacity;
+#pragma unroll
+                               for (int u = 0; u < 2; ++u)
+                                   if (slot[u] < capacity) {
+                                       tile_keys[slot[u]] = tl[u];
+                                       vals[slot[u]] = gl[u];
+                                   }
+                           });
+    }
+}
+
+int launch_scatter_pairs(const float* xydr4, const uint32_t* counts, int64_t n, int tiles_x, int tiles_y,
+                         int64_t capacity, uint32_t* cursors, uint32_t* tile_keys, uint32_t* vals, cudaStream_t s) {
+    int64_t blocks = (n + 255) / 256;
+    const int64_t cap = (int64_t)sort_sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) return 0;
+    launch_k(scatter_pairs_kernel, dim3((unsigned)blocks), dim3(256), 0, s, (const float4*)xydr4, counts, (int)n,
+             tiles_x, tiles_y, (uint32_t)capacity, cursors, tile_keys, vals);
+    return check_launch("scatter_pairs_kernel");
+}
+
 // Raster launch order: heaviest tile lists first, so the rasterizers' last
 // CTAs are short ones (uneven scenes otherwise end on a few long tiles).
 // Tiles are bucketed by floor(log2(list length)), buckets descending; order

@@ -176,6 +176,59 @@ __device__ __forceinline__ void tile_rect(float mx, float my, int r, int tiles_x
     ty1 = min(tiles_y - 1, (fy + r) >> 4);
 }
 
+// Warp-cooperative walk over 32 consecutive Gaussians' tile rects (lane =
+// one Gaussian, rect tx0..tx1 x ty0..ty1, empty when tx1 < tx0): the warp
+// takes the rects' tiles 32 at a time, each lane finding its entry's owner
+// by binary search over the lanes' exclusive prefix and decoding the tile
+// row-major; f(tiles[UNROLL], gaussians[UNROLL]) per step, tile 0xFFFFFFFF
+// for no entry.
+// TCOUNT_REPL replicas of the scatter binning's per-tile counters: Gaussian
+// g counts (and later takes its slots) in replica (g >> 5) % TCOUNT_REPL, so
+// the hot tiles' atomics spread over several L2 lines.
+constexpr int TCOUNT_REPL = 8;
+__device__ __forceinline__ uint32_t tcount_replica(uint32_t g) { return (g >> 5) & (TCOUNT_REPL - 1); }
+
+// Per entry f(tile, gaussian); UNROLL entries per lane per step (independent
+// atomics in flight).
+template <int UNROLL = 1, typename F>
+__device__ __forceinline__ void walk_tile_rects(int lane, uint32_t g, int tx0, int tx1, int ty0, int ty1,
+                                                int tiles_x, F&& f) {
+    const int w = tx1 - tx0 + 1;
+    const uint32_t cnt = (uint32_t)(w * (ty1 - ty0 + 1));
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const float rw = w > 0 ? 1.f / (float)w : 0.f;
+    for (uint32_t t0 = 0; t0 < total; t0 += 32 * UNROLL) {
+        uint32_t tl[UNROLL], gl[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const uint32_t t = t0 + 32 * u + lane;
+            int L = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t e = __shfl_sync(0xffffffffu, excl, L + step);
+                if (e <= t) L += step;
+            }
+            const uint32_t j = t - __shfl_sync(0xffffffffu, excl, L);
+            const int ow = __shfl_sync(0xffffffffu, w, L);
+            const float orw = __shfl_sync(0xffffffffu, rw, L);
+            const int otx0 = __shfl_sync(0xffffffffu, tx0, L), oty0 = __shfl_sync(0xffffffffu, ty0, L);
+            gl[u] = __shfl_sync(0xffffffffu, g, L);
+            int row = (int)((float)j * orw);
+            if (row * ow > (int)j) --row;
+            if ((row + 1) * ow <= (int)j) ++row;
+            tl[u] = t < total ? (uint32_t)((oty0 + row) * tiles_x + otx0 + ((int)j - row * ow)) : 0xFFFFFFFFu;
+        }
+        f(tl, gl);
+    }
+}
+
 __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
                  "f"(d)

@@ -43,10 +43,20 @@ bool tile_order_enabled(int n_tiles) {
     return on && n_tiles > 148 * 8;
 }
 
+// Scatter binning (segment mode) for small scenes, depth-first otherwise
+// (gs_set_option("binning"): 0 auto, 1 depth-first, 2 scatter).
+bool scatter_binning(int64_t n) {
+    const int bmode = binning_mode();
+    return bmode == 2 || (bmode == 0 && n <= 400000);
+}
+
+// where the tile-sorted (keys, vals) of a frame end up
+bool sorted_in_alt(int64_t n, int n_tiles) { return !scatter_binning(n) && (tile_passes_for(n_tiles) & 1); }
+
 struct Layout {
     // persistent (written each frame)
     size_t xydr, conic, tiles, dkeys, dkeys_alt, order, order_alt, offsets;
-    size_t tkeys, tkeys_alt, tvals, tvals_alt, ranges, rec, rec_count, tile_order;
+    size_t tkeys, tkeys_alt, tvals, tvals_alt, ranges, rec, rec_count, tile_order, tcount;
     // zeroed region
     size_t zero_begin, meta, dhist, thist, counters, scan_ws, dstatus, tstatus, zero_end;
     // backward
@@ -80,6 +90,7 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.rec = take(8 * 4 * cap);    // forward commit records, 4 warp regions per tile list
     L.rec_count = take(16 * nt);  // records per (tile, warp)
     L.tile_order = take(4 * nt);  // raster launch order (heaviest lists first)
+    L.tcount = take(4 * TCOUNT_REPL * nt);  // scatter binning: tile counts, then write cursors
     L.zero_begin = o;
     L.meta = take(16);
     L.dhist = take(4 * 256 * 4);
@@ -129,7 +140,7 @@ int gs_frame_view_of(int64_t n, int64_t isect_capacity, int32_t width, int32_t h
                      gs_frame_view* out) {
     const Layout L = layout(n, isect_capacity, width, height);
     const int nt = ((width + TILE - 1) / TILE) * ((height + TILE - 1) / TILE);
-    const bool odd = tile_passes_for(nt) & 1;
+    const bool odd = sorted_in_alt(n, nt);
     out->xydr4 = at<float>(ws, L.xydr);
     out->conic4 = at<float>(ws, L.conic);
     out->tiles = at<uint32_t>(ws, L.tiles);
@@ -178,17 +189,44 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     zj.n16[1] = (8 * (size_t)tiles_x * tiles_y + 15) / 16;
     zj.p[2] = at<uint4>(ws, L.d_geo);
     zj.n16[2] = (L.partials - L.d_geo) / 16;
+    const bool scatter = scatter_binning(n);
+    const int n_tiles = tiles_x * tiles_y;
+    const uint32_t* t_order = tile_order_enabled(n_tiles) ? at<uint32_t>(ws, L.tile_order) : nullptr;
     if (launch_project_fwd_dkey(means3, scales3, quats4, opacities, n, k, at<float>(ws, L.xydr),
                                 at<float>(ws, L.conic), at<uint32_t>(ws, L.tiles), nullptr, meta,
-                                at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.dhist), s, zj))
+                                at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.dhist), s, zj,
+                                scatter ? at<uint32_t>(ws, L.tcount) : nullptr))
         return -1;
     mark(stage_events, 1, s);
-    const int bmode = binning_mode();
-    const bool segment = bmode == 2 || (bmode == 0 && n <= 400000);
-    // 2. depth-first: stable depth sort of all Gaussians (culled ones last);
-    //    segment mode: none (pairs are emitted in index order, tiles sorted later)
+    const float3 bg = make_float3(background3[0], background3[1], background3[2]);
+    if (scatter) {
+        // 2-6. scatter binning: the projection counted every tile's pairs;
+        //      scan -> ranges + cursors (+ raster order), scatter the pairs
+        //      into their ranges, sort each range by (depth, index)
+        mark(stage_events, 2, s);
+        uint32_t* tcount = at<uint32_t>(ws, L.tcount);
+        if (launch_tile_scan(tcount, n_tiles, isect_capacity, at<uint2>(ws, L.ranges), meta + 1,
+                             const_cast<uint32_t*>(t_order), s))
+            return -1;
+        if (launch_scatter_pairs(at<float>(ws, L.xydr), at<uint32_t>(ws, L.tiles), n, tiles_x, tiles_y,
+                                 isect_capacity, tcount, at<uint32_t>(ws, L.tkeys), at<uint32_t>(ws, L.tvals), s))
+            return -1;
+        mark(stage_events, 3, s);
+        if (launch_segsort(at<uint2>(ws, L.ranges), n_tiles, at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.tvals),
+                           at<uint32_t>(ws, L.tvals_alt), s))
+            return -1;
+        mark(stage_events, 4, s);
+        if (launch_raster_fwd(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.tvals), at<float>(ws, L.xydr),
+                              at<float>(ws, L.conic), colors3, bg, W, H, early_termination != 0, out_image,
+                              out_final_T, out_n_contrib, counts4, s, at<uint2>(ws, L.rec),
+                              at<uint32_t>(ws, L.rec_count), t_order))
+            return -1;
+        mark(stage_events, 5, s);
+        return 0;
+    }
+    // 2. depth-first: stable depth sort of all Gaussians (culled ones last)
     const uint32_t* order = nullptr;
-    if (!segment) {
+    {
         if (run_onesweep<uint32_t>(at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.order),
                                    at<uint32_t>(ws, L.dkeys_alt), at<uint32_t>(ws, L.order_alt), n, nullptr, 4,
                                    at<uint32_t>(ws, L.dhist), at<uint32_t>(ws, L.dstatus), counters, s, true))
@@ -213,17 +251,11 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     const uint32_t* svals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
     // 6. per-tile ranges
     if (launch_ranges_u32(skeys, isect_capacity, meta + 1, at<uint2>(ws, L.ranges), s)) return -1;
-    // 6b. segment mode: each tile's (index-ordered) list stably sorted by depth
-    if (segment && launch_segsort(at<uint2>(ws, L.ranges), tiles_x * tiles_y, at<uint32_t>(ws, L.dkeys),
-                                  const_cast<uint32_t*>(svals), at<uint32_t>(ws, odd ? L.tvals : L.tvals_alt), s))
-        return -1;
-    // 6c. heaviest-first raster launch order
-    const uint32_t* t_order = tile_order_enabled(tiles_x * tiles_y) ? at<uint32_t>(ws, L.tile_order) : nullptr;
-    if (t_order && launch_tile_order(at<uint2>(ws, L.ranges), tiles_x * tiles_y, at<uint32_t>(ws, L.tile_order), s))
+    // 6b. heaviest-first raster launch order
+    if (t_order && launch_tile_order(at<uint2>(ws, L.ranges), n_tiles, at<uint32_t>(ws, L.tile_order), s))
         return -1;
     mark(stage_events, 4, s);
     // 7. raster forward
-    const float3 bg = make_float3(background3[0], background3[1], background3[2]);
     if (launch_raster_fwd(at<uint2>(ws, L.ranges), svals, at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3,
                           bg, W, H, early_termination != 0, out_image, out_final_T, out_n_contrib, counts4, s,
                           at<uint2>(ws, L.rec), at<uint32_t>(ws, L.rec_count), t_order))
@@ -244,9 +276,7 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
     cudaStream_t s = (cudaStream_t)stream;
     const CamK k = make_camk(*cam);
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
-    const int tp = tile_passes_for(tiles_x * tiles_y);
-    const bool odd = tp & 1;
-    const uint32_t* svals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
+    const uint32_t* svals = at<uint32_t>(ws, sorted_in_alt(n, tiles_x * tiles_y) ? L.tvals_alt : L.tvals);
     mark(stage_events, 0, s);
     // the screen-space accumulators were zeroed by gs_frame_forward (see
     // gs_frame_view.bwd_accum to re-zero before a second backward)

@@ -13,7 +13,8 @@ namespace gs {
 int launch_project_fwd_dkey(const float* means3, const float* scales3, const float* quats4, const float* opac,
                             int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
                             unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s,
-                            const ZeroJobs& zj);  // also resets meta (status, total) and dhist first
+                            const ZeroJobs& zj, uint32_t* tcount = nullptr);  // also resets meta (status,
+                            // total), dhist and (scatter binning: per-tile intersection counts) tcount first
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
                        float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
@@ -48,6 +49,12 @@ size_t emit_scan_ws_bytes(int64_t n);
 int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* counts, int64_t n, int tiles_x,
                      int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals, uint32_t* tile_hist,
                      int tile_passes, void* ws, unsigned long long* total, cudaStream_t s);
+// scatter binning: tile scan (ranges, cursors, total, optional raster order)
+// and the unordered scatter of the (tile, gaussian) pairs
+int launch_tile_scan(uint32_t* tcount, int n_tiles, int64_t capacity, uint2* ranges, unsigned long long* total,
+                     uint32_t* order, cudaStream_t s);
+int launch_scatter_pairs(const float* xydr4, const uint32_t* counts, int64_t n, int tiles_x, int tiles_y,
+                         int64_t capacity, uint32_t* cursors, uint32_t* tile_keys, uint32_t* vals, cudaStream_t s);
 // heaviest-first raster launch order of the tiles (one CTA)
 int launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* order, cudaStream_t s);
 int launch_ranges_u64(const unsigned long long* sorted_keys, int64_t n, uint2* ranges,

@@ -23,20 +23,23 @@ __device__ __forceinline__ void report(unsigned long long* status, int i, int co
 // through P (:45-61; equals fx*tx/tz + 0.5 + cx) -> radius (:99-112) ->
 // off-screen cull (:131-137).  Plus the conic (sg/raster_forward.py:86-92)
 // and the tile count of the bbox square (sg/binning.py:35-46).
-// DKEY: also write the depth sort key of every Gaussian (float bits of the
-// camera depth for visible ones, 0xFFFFFFFF for culled ones so they sort
-// last) and accumulate the four 8-bit digit histograms of those keys for
-// the onesweep sort that follows (sort.cu), accumulated in shared memory.
-template <bool DKEY>
+// MODE 1 / 2 (frame path): also write the depth sort key of every Gaussian
+// (float bits of the camera depth for visible ones, 0xFFFFFFFF for culled
+// ones so they sort last).  MODE 1 (depth-first binning) accumulates the
+// four 8-bit digit histograms of those keys for the onesweep depth sort
+// that follows (sort.cu), in shared memory; MODE 2 (scatter binning) counts
+// every tile's intersections instead (tcount, one red.add per pair).
+template <int MODE>
 __global__ void __launch_bounds__(256) project_fwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
     const float* __restrict__ opac, int n, CamK cam, float4* __restrict__ xydr, float4* __restrict__ conic,
     uint32_t* __restrict__ tiles, float* __restrict__ cov_out, unsigned long long* __restrict__ status,
-    uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dhist, ZeroJobs zj) {
+    uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dhist, ZeroJobs zj, uint32_t* __restrict__ tcount) {
+    constexpr bool DKEY = MODE != 0;
     griddep_wait();
     run_zero_jobs(zj);  // frame path: clear the later stages' counters / accumulators
-    __shared__ uint32_t s_hist[DKEY ? 4 * 256 : 1];
-    if (DKEY) {
+    __shared__ uint32_t s_hist[MODE == 1 ? 4 * 256 : 1];
+    if (MODE == 1) {
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) s_hist[k] = 0;
         __syncthreads();
     }
@@ -45,6 +48,7 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
     const int n_round = (n + 31) & ~31;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += gridDim.x * blockDim.x) {
     uint32_t dkey = 0xFFFFFFFFu;
+    int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;  // tile rect (MODE 2 walks it)
     if (i < n) {
     const float mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
     const float* Rc = cam.R;
@@ -110,7 +114,6 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
                     o_xydr = make_float4(px, py, tz, __int_as_float(off ? 0 : r));
                     if (!off) {
                         o_con = conic_of(ca, cb, cc, det, opac[i]);
-                        int tx0, tx1, ty0, ty1;
                         tile_rect(px, py, r, cam.tiles_x, cam.tiles_y, tx0, tx1, ty0, ty1);
                         nt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
                     }
@@ -131,7 +134,14 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
         dkeys[i] = dkey;
     }
     }  // i < n
-    if (DKEY) {
+    if (MODE == 2) {
+        uint32_t* tc = tcount + (size_t)tcount_replica((uint32_t)i) * (cam.tiles_x * cam.tiles_y);
+        walk_tile_rects(threadIdx.x & 31, 0u, tx0, tx1, ty0, ty1, cam.tiles_x,
+                        [&](const uint32_t* tl, const uint32_t*) {
+                            if (tl[0] != 0xFFFFFFFFu) atomicAdd(&tc[tl[0]], 1u);
+                        });
+    }
+    if (MODE == 1) {
         const bool valid = i < n;
         // low bytes of the depth bits are spread (per-lane atomics), high
         // bytes and culled keys concentrated (warp-uniform fast path)
@@ -139,7 +149,7 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
         for (int p = 0; p < 4; ++p) warp_hist_add(s_hist + 256 * p, (dkey >> (8 * p)) & 255u, valid);
     }
     }  // grid-stride
-    if (DKEY) {
+    if (MODE == 1) {
         __syncthreads();
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) {
             const uint32_t v = s_hist[k];
@@ -370,29 +380,44 @@ __global__ void __launch_bounds__(384) view_reduce_kernel(const float* __restric
 
 // Frame start: status word = all ones (no error), intersection total and the
 // depth-digit histograms = 0 (the projection accumulates into them).
+// Frame reset ahead of the projection: meta, the depth histograms and (scatter
+// binning) the per-tile intersection counts the projection accumulates.
 __global__ void __launch_bounds__(256) frame_init_kernel(unsigned long long* __restrict__ meta,
-                                                         uint32_t* __restrict__ dhist) {
+                                                         uint32_t* __restrict__ dhist, uint32_t* __restrict__ tcount,
+                                                         int n_counts) {
     griddep_wait();
-    if (threadIdx.x == 0) {
-        meta[0] = ~0ull;
-        meta[1] = 0ull;
+    if (blockIdx.x == 0) {
+        if (threadIdx.x == 0) {
+            meta[0] = ~0ull;
+            meta[1] = 0ull;
+        }
+        for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) dhist[k] = 0u;
     }
-    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) dhist[k] = 0u;
+    if (tcount)
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_counts; k += gridDim.x * blockDim.x) tcount[k] = 0u;
 }
 
 int launch_project_fwd_dkey(const float* means3, const float* scales3, const float* quats4, const float* opac,
                             int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
                             unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s,
-                            const ZeroJobs& zj) {
-    launch_k(frame_init_kernel, dim3(1), dim3(256), 0, s, status, dhist);
+                            const ZeroJobs& zj, uint32_t* tcount) {
+    const int n_tiles = k.tiles_x * k.tiles_y;
+    const int init_blocks = tcount ? (TCOUNT_REPL * n_tiles + 2047) / 2048 : 1;
+    launch_k(frame_init_kernel, dim3((unsigned)init_blocks), dim3(256), 0, s, status, dhist, tcount,
+             TCOUNT_REPL * n_tiles);
     if (check_launch("frame_init_kernel")) return -1;
     int64_t blocks = (n + 255) / 256;
     if (blocks < 1) blocks = 1;  // the zero jobs run even for an empty scene
     const int64_t cap = (int64_t)sort_sm_count() * 6;  // resident CTAs (40 regs, 256 threads)
     if (blocks > cap) blocks = cap;
-    launch_k(project_fwd_kernel<true>, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
-             (const float4*)quats4, opac, (int)n, k, (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
-             dhist, zj);
+    if (tcount)
+        launch_k(project_fwd_kernel<2>, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
+                 (const float4*)quats4, opac, (int)n, k, (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
+                 dhist, zj, tcount);
+    else
+        launch_k(project_fwd_kernel<1>, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
+                 (const float4*)quats4, opac, (int)n, k, (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
+                 dhist, zj, (uint32_t*)nullptr);
     return check_launch("project_fwd_kernel<dkey>");
 }
 
@@ -427,9 +452,9 @@ int gs_project_fwd(const float* means3, const float* scales3, const float* quats
     if (n == 0) return 0;
     const CamK k = make_camk(*cam);
     const int blocks = (int)((n + 255) / 256);
-    project_fwd_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+    project_fwd_kernel<0><<<blocks, 256, 0, (cudaStream_t)stream>>>(
         means3, scales3, (const float4*)quats4, opacities, (int)n, k, (float4*)out_xydr4, (float4*)out_conic4,
-        out_tiles, out_cov3, status, nullptr, nullptr, ZeroJobs{});
+        out_tiles, out_cov3, status, nullptr, nullptr, ZeroJobs{}, nullptr);
     return check_launch("project_fwd_kernel");
 }
 

@@ -1,21 +1,18 @@
-// segsort.cu -- per-tile depth sort (segment binning for small scenes).
+// segsort.cu -- per-tile sort of the scatter-binned lists (small scenes).
 //
 // sg/binning.py:27-65 wants every tile's list in (depth, source_index)
 // order.  The depth-first path (frame.cu) gets it from a global stable sort
 // of the N depth keys (4 onesweep passes) before emission.  For small scenes
-// those passes are latency-bound (~8 us each at N = 1e5), so the segment
-// path instead emits in Gaussian-index order, stably sorts by tile id, and
-// then sorts each tile's list here, stably by the depth key of its
-// Gaussians: stable on an index-ordered list = (depth, index) order.
+// those passes are latency-bound, so the scatter path writes every tile's
+// pairs straight into its range in arbitrary order (binning.cu) and sorts
+// each range here: a stable LSD radix sort by the Gaussians' depth keys,
+// then a check for equal depths next to each other.  Ties (rare: exactly
+// equal float depths) re-sort the range by source index first and by depth
+// second, which is the (depth, index) order whatever the input order was.
 //
-// One CTA per tile.  The list is processed in chunks of SEG_CHUNK entries
-// with the onesweep ranking (per-warp peer masks built with shared atomic
-// OR, input order = (warp, item, lane)); digit starts come from the
-// segment's own per-byte histograms (one read pass, which also finds the
-// key bytes that are constant over the segment -- those passes are
-// skipped; depths within a tile usually share their top byte).  Passes
-// ping-pong between the list and its alternate buffer through L2; keys are
-// re-gathered from the per-Gaussian key array every pass.
+// Key bytes that are constant over a range are skipped (depths within a
+// tile usually share their top byte); a range whose depths are all equal
+// is one tie run and gets the index passes only.
 #include "common.cuh"
 #include "internal.cuh"
 
@@ -27,14 +24,14 @@ constexpr int SEG_ITEMS = 4;
 constexpr int SEG_CHUNK = SEG_THREADS * SEG_ITEMS;
 
 // Short lists (the common case): one warp per tile, the whole list in
-// registers (WS_ITEMS per lane, input order = (item, lane)).  One read of
-// the list builds the warp's per-byte digit histograms (and finds the key
-// bytes that are constant over the list -- skipped); each varying byte is
-// then one stable peer-mask ranking pass that scatters every item to its
-// final slot as soon as it is ranked (digit starts known up front, so no
-// per-item rank registers), no CTA barriers.  Sized to stay at <= 96
-// registers so a frame's tiles fit one wave (5 CTAs of 4 warps per SM).
-// Longer lists are left to segsort_kernel below.
+// registers (WS_ITEMS per lane, input order = (item, lane)).  Each varying
+// key byte is one stable pass: a peer-mask ranking (per-warp shared atomic
+// OR; the lowest peer adds the group to the digit count, so no contended
+// counting) that parks every item's rank within its digit in shared
+// memory, a warp scan of the 256 digit counts, a scatter to the digit start
+// + rank and a gather back into registers -- no CTA barriers.  Sized to
+// stay under 96 registers so a frame's tiles fit one wave.  Longer lists
+// are left to segsort_kernel below.
 constexpr int WS_ITEMS = 16;
 constexpr int WS_MAX = 32 * WS_ITEMS;  // 512 entries
 constexpr int WS_WARPS = 4;
@@ -44,8 +41,9 @@ __global__ void __launch_bounds__(32 * WS_WARPS, 5) segsort_warp_kernel(const ui
                                                                        uint32_t* __restrict__ vals) {
     griddep_wait();
     __shared__ uint32_t s_peers[WS_WARPS][2][256];
-    __shared__ uint32_t s_hist[WS_WARPS][4][256];  // digit counts, then running digit slots
+    __shared__ uint32_t s_cnt[WS_WARPS][256];  // digit counts, then digit starts
     __shared__ uint32_t s_key[WS_WARPS][WS_MAX], s_val[WS_WARPS][WS_MAX];
+    __shared__ uint16_t s_rank[WS_WARPS][WS_MAX];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tile = blockIdx.x * WS_WARPS + warp;
     if (tile >= n_tiles) return;
@@ -54,7 +52,7 @@ __global__ void __launch_bounds__(32 * WS_WARPS, 5) segsort_warp_kernel(const ui
     if (len <= 1 || len > WS_MAX) return;
     uint32_t* gv = vals + rg.x;
     uint32_t k[WS_ITEMS], v[WS_ITEMS];
-    uint32_t o = 0u, a = ~0u;
+    uint32_t ko = 0u, ka = ~0u, vo = 0u, va = ~0u;
 #pragma unroll
     for (int i = 0; i < WS_ITEMS; ++i) {
         const int idx = i * 32 + lane;
@@ -65,33 +63,46 @@ __global__ void __launch_bounds__(32 * WS_WARPS, 5) segsort_warp_kernel(const ui
         const int idx = i * 32 + lane;
         k[i] = idx < len ? dkeys[v[i]] : 0u;
         if (idx < len) {
-            o |= k[i];
-            a &= k[i];
+            ko |= k[i];
+            ka &= k[i];
+            vo |= v[i];
+            va &= v[i];
         }
     }
-    const uint32_t vary = __reduce_or_sync(0xffffffffu, o) ^ __reduce_and_sync(0xffffffffu, a);
-    if (vary == 0u) return;  // all keys equal: the index order already is the answer
+    const uint32_t kvary = __reduce_or_sync(0xffffffffu, ko) ^ __reduce_and_sync(0xffffffffu, ka);
     {
         uint4* z = reinterpret_cast<uint4*>(&s_peers[warp][0][0]);
         for (int j = lane; j < 2 * 256 / 4; j += 32) z[j] = make_uint4(0u, 0u, 0u, 0u);
-        z = reinterpret_cast<uint4*>(&s_hist[warp][0][0]);
-        for (int j = lane; j < 4 * 256 / 4; j += 32) z[j] = make_uint4(0u, 0u, 0u, 0u);
     }
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < WS_ITEMS; ++i) {
-        if (i * 32 + lane < len) {
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if ((vary >> (8 * b)) & 255u) atomicAdd(&s_hist[warp][b][(k[i] >> (8 * b)) & 255u], 1u);
-        }
-    }
-    __syncwarp();
     const uint32_t lt = lanemask_lt();
-    for (int b = 0; b < 4; ++b) {
-        if (((vary >> (8 * b)) & 255u) == 0u) continue;
-        const int shift = 8 * b;
-        uint32_t* cnt = s_hist[warp][b];
+    uint32_t* cnt = s_cnt[warp];
+    // one stable pass over byte `shift` of the depth keys (by_id false) or
+    // of the source indices (by_id true)
+    auto pass = [&](bool by_id, int shift) {
+        {
+            uint4* z = reinterpret_cast<uint4*>(cnt);
+            for (int j = lane; j < 256 / 4; j += 32) z[j] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < WS_ITEMS; ++i) {
+            const bool valid = i * 32 + lane < len;
+            const uint32_t d = ((by_id ? v[i] : k[i]) >> shift) & 255u;
+            uint32_t* pm = &s_peers[warp][i & 1][d];
+            if (valid) atomicOr(pm, 1u << lane);
+            __syncwarp();
+            const uint32_t peers = valid ? *pm : 0u;
+            const uint32_t old = valid ? cnt[d] : 0u;
+            __syncwarp();
+            if (valid) {
+                if ((peers & lt) == 0u) {
+                    cnt[d] = old + (uint32_t)__popc(peers);
+                    *pm = 0u;
+                }
+                s_rank[warp][i * 32 + lane] = (uint16_t)(old + (uint32_t)__popc(peers & lt));
+            }
+        }
+        __syncwarp();
         {  // exclusive scan of the 256 digit counts: 8 per lane + warp scan
             uint32_t c8[8], run = 0;
 #pragma unroll
@@ -115,20 +126,9 @@ __global__ void __launch_bounds__(32 * WS_WARPS, 5) segsort_warp_kernel(const ui
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < WS_ITEMS; ++i) {
-            const bool valid = i * 32 + lane < len;
-            const uint32_t d = (k[i] >> shift) & 255u;
-            uint32_t* pm = &s_peers[warp][i & 1][d];
-            if (valid) atomicOr(pm, 1u << lane);
-            __syncwarp();
-            const uint32_t peers = valid ? *pm : 0u;
-            const uint32_t old = valid ? cnt[d] : 0u;
-            __syncwarp();
-            if (valid) {
-                if ((peers & lt) == 0u) {
-                    cnt[d] = old + (uint32_t)__popc(peers);
-                    *pm = 0u;
-                }
-                const uint32_t pos = old + (uint32_t)__popc(peers & lt);
+            const int idx = i * 32 + lane;
+            if (idx < len) {
+                const uint32_t pos = cnt[((by_id ? v[i] : k[i]) >> shift) & 255u] + s_rank[warp][idx];
                 s_key[warp][pos] = k[i];
                 s_val[warp][pos] = v[i];
             }
@@ -143,6 +143,26 @@ __global__ void __launch_bounds__(32 * WS_WARPS, 5) segsort_warp_kernel(const ui
             }
         }
         __syncwarp();
+    };
+    bool tie = kvary == 0u;  // all depths equal: one tie run
+    if (!tie) {
+        for (int b = 0; b < 4; ++b)
+            if ((kvary >> (8 * b)) & 255u) pass(false, 8 * b);
+        // s_key holds the depth-sorted keys: any equal neighbours?
+        bool t = false;
+#pragma unroll
+        for (int i = 0; i < WS_ITEMS; ++i) {
+            const int idx = i * 32 + lane;
+            if (idx > 0 && idx < len) t = t || s_key[warp][idx] == s_key[warp][idx - 1];
+        }
+        tie = __any_sync(0xffffffffu, t);
+    }
+    if (tie) {  // (depth, index) order: index bytes first, then depth bytes
+        const uint32_t vvary = __reduce_or_sync(0xffffffffu, vo) ^ __reduce_and_sync(0xffffffffu, va);
+        for (int b = 0; b < 4; ++b)
+            if ((vvary >> (8 * b)) & 255u) pass(true, 8 * b);
+        for (int b = 0; b < 4; ++b)
+            if ((kvary >> (8 * b)) & 255u) pass(false, 8 * b);
     }
 #pragma unroll
     for (int i = 0; i < WS_ITEMS; ++i) {
@@ -151,7 +171,132 @@ __global__ void __launch_bounds__(32 * WS_WARPS, 5) segsort_warp_kernel(const ui
     }
 }
 
-// Long lists (len > WS_MAX): one CTA per tile, chunked passes through L2.
+// Long lists (len > WS_MAX): a CTA sorts one range with chunked passes
+// through L2 (ping-pong between the range and its alternate buffer).  One
+// read pass builds the per-byte histograms of the key (depth key, or source
+// index when by_id) and finds its constant bytes; each varying byte is then
+// one stable pass: SEG_CHUNK entries at a time with the onesweep ranking
+// (per-warp peer masks built with shared atomic OR, input order = (warp,
+// item, lane)).  Ends with the sorted range back in `seg`.
+struct SegShared {
+    uint32_t hist[4][256];            // per byte, then running digit starts
+    uint32_t whist[SEG_WARPS][256];   // per-warp digit counts of the chunk
+    uint32_t peers[SEG_WARPS][2][256];  // peer-mask banks
+    uint32_t vor, vand, flag;
+    uint32_t tmp[SEG_WARPS];
+};
+
+__device__ __forceinline__ uint32_t seg_key(const uint32_t* __restrict__ dkeys, uint32_t v, bool by_id) {
+    return by_id ? v : dkeys[v];
+}
+
+__device__ void cta_radix(SegShared& sh, const uint32_t* __restrict__ dkeys, uint32_t* seg, uint32_t* alt, int len,
+                          bool by_id) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int k = tid; k < 4 * 256; k += SEG_THREADS) (&sh.hist[0][0])[k] = 0u;
+    for (int k = tid; k < SEG_WARPS * 2 * 256; k += SEG_THREADS) (&sh.peers[0][0][0])[k] = 0u;
+    if (tid == 0) {
+        sh.vor = 0u;
+        sh.vand = ~0u;
+    }
+    __syncthreads();
+    // 1. per-byte histograms + which bytes vary
+    uint32_t o = 0u, a = ~0u;
+    for (int i = tid; i < len; i += SEG_THREADS) {
+        const uint32_t key = seg_key(dkeys, seg[i], by_id);
+        o |= key;
+        a &= key;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) atomicAdd(&sh.hist[b][(key >> (8 * b)) & 255u], 1u);
+    }
+    o = __reduce_or_sync(0xffffffffu, o);
+    a = __reduce_and_sync(0xffffffffu, a);
+    if (lane == 0) {
+        atomicOr(&sh.vor, o);
+        atomicAnd(&sh.vand, a);
+    }
+    __syncthreads();
+    const uint32_t vary = sh.vor ^ sh.vand;
+    // exclusive digit starts per byte (thread = digit)
+#pragma unroll 1
+    for (int b = 0; b < 4; ++b) {
+        const uint32_t c = sh.hist[b][tid];
+        uint32_t incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        if (lane == 31) sh.tmp[warp] = incl;
+        __syncthreads();
+        uint32_t base = 0;
+        for (int w = 0; w < warp; ++w) base += sh.tmp[w];
+        __syncthreads();
+        sh.hist[b][tid] = base + incl - c;
+    }
+    __syncthreads();
+    // 2. one stable scatter pass per varying byte
+    uint32_t* src = seg;
+    uint32_t* dst = alt;
+    const uint32_t lt = lanemask_lt();
+    for (int b = 0; b < 4; ++b) {
+        if (((vary >> (8 * b)) & 255u) == 0u) continue;  // constant byte: identity pass
+        const int shift = 8 * b;
+        for (int c0 = 0; c0 < len; c0 += SEG_CHUNK) {
+            const int wbase = c0 + warp * (SEG_ITEMS * 32);
+            uint32_t v[SEG_ITEMS], d[SEG_ITEMS], rank[SEG_ITEMS];
+#pragma unroll
+            for (int i = 0; i < SEG_ITEMS; ++i) {
+                const int idx = wbase + i * 32 + lane;
+                v[i] = idx < len ? src[idx] : 0u;
+                d[i] = idx < len ? (seg_key(dkeys, v[i], by_id) >> shift) & 255u : 256u;
+            }
+#pragma unroll
+            for (int k = 0; k < SEG_WARPS; ++k) sh.whist[k][tid] = 0u;
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < SEG_ITEMS; ++i) {
+                const bool valid = d[i] < 256u;
+                uint32_t* pm = &sh.peers[warp][i & 1][valid ? d[i] : 0];
+                if (valid) atomicOr(pm, 1u << lane);
+                __syncwarp();
+                const uint32_t peers = valid ? *pm : 0u;
+                const uint32_t old = valid ? sh.whist[warp][d[i]] : 0u;
+                __syncwarp();
+                if (valid && (peers & lt) == 0u) {
+                    sh.whist[warp][d[i]] = old + (uint32_t)__popc(peers);
+                    *pm = 0u;
+                }
+                rank[i] = old + (uint32_t)__popc(peers & lt);
+            }
+            __syncthreads();
+            // per digit: warp offsets within the chunk, then advance the digit start
+            {
+                uint32_t run = sh.hist[b][tid];
+#pragma unroll
+                for (int w = 0; w < SEG_WARPS; ++w) {
+                    const uint32_t cnt = sh.whist[w][tid];
+                    sh.whist[w][tid] = run;
+                    run += cnt;
+                }
+                sh.hist[b][tid] = run;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < SEG_ITEMS; ++i)
+                if (d[i] < 256u) dst[sh.whist[warp][d[i]] + rank[i]] = v[i];
+            __syncthreads();
+        }
+        uint32_t* t = src;
+        src = dst;
+        dst = t;
+    }
+    if (src != seg) {  // odd number of passes: copy back
+        for (int i = tid; i < len; i += SEG_THREADS) seg[i] = src[i];
+    }
+    __syncthreads();
+}
+
 // A few CTAs stride over the tiles (long lists are rare) instead of one CTA
 // per tile that mostly exits at once.
 __global__ void __launch_bounds__(SEG_THREADS) segsort_kernel(const uint2* __restrict__ ranges, int n_tiles,
@@ -159,118 +304,25 @@ __global__ void __launch_bounds__(SEG_THREADS) segsort_kernel(const uint2* __res
                                                               uint32_t* __restrict__ vals,
                                                               uint32_t* __restrict__ alt) {
     griddep_wait();
-    __shared__ uint32_t s_hist[4][256];                 // per byte, then running digit starts
-    __shared__ uint32_t s_whist[SEG_WARPS][256];        // per-warp digit counts of the chunk
-    __shared__ uint32_t s_peers[SEG_WARPS][2][256];     // peer-mask banks
-    __shared__ uint32_t s_or, s_and;
-    __shared__ uint32_t s_tmp[SEG_WARPS];
+    __shared__ SegShared sh;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const uint2 rg = ranges[tile];
-        const int start = (int)rg.x, len = (int)(rg.y - rg.x);
+        const int len = (int)(rg.y - rg.x);
         if (len <= WS_MAX) continue;  // segsort_warp_kernel's
-        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-        for (int k = tid; k < 4 * 256; k += SEG_THREADS) (&s_hist[0][0])[k] = 0u;
-        for (int k = tid; k < SEG_WARPS * 2 * 256; k += SEG_THREADS) (&s_peers[0][0][0])[k] = 0u;
-        if (tid == 0) {
-            s_or = 0u;
-            s_and = ~0u;
-        }
+        uint32_t* seg = vals + rg.x;
+        cta_radix(sh, dkeys, seg, alt + rg.x, len, false);
+        // equal depths next to each other?  then (index, then depth) passes
+        if (threadIdx.x == 0) sh.flag = 0u;
         __syncthreads();
-        // 1. per-byte histograms + which bytes vary
-        uint32_t o = 0u, a = ~0u;
-        for (int i = tid; i < len; i += SEG_THREADS) {
-            const uint32_t key = dkeys[vals[start + i]];
-            o |= key;
-            a &= key;
-    #pragma unroll
-            for (int b = 0; b < 4; ++b) atomicAdd(&s_hist[b][(key >> (8 * b)) & 255u], 1u);
-        }
-        o = __reduce_or_sync(0xffffffffu, o);
-        a = __reduce_and_sync(0xffffffffu, a);
-        if (lane == 0) {
-            atomicOr(&s_or, o);
-            atomicAnd(&s_and, a);
-        }
+        bool t = false;
+        for (int i = 1 + (int)threadIdx.x; i < len; i += SEG_THREADS)
+            t = t || dkeys[seg[i]] == dkeys[seg[i - 1]];
+        if (__any_sync(0xffffffffu, t) && (threadIdx.x & 31) == 0) sh.flag = 1u;
         __syncthreads();
-        const uint32_t vary = s_or ^ s_and;
-        // exclusive digit starts per byte (thread = digit)
-    #pragma unroll 1
-        for (int b = 0; b < 4; ++b) {
-            const uint32_t c = s_hist[b][tid];
-            uint32_t incl = c;
-    #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += y;
-            }
-            if (lane == 31) s_tmp[warp] = incl;
-            __syncthreads();
-            uint32_t base = 0;
-            for (int w = 0; w < warp; ++w) base += s_tmp[w];
-            __syncthreads();
-            s_hist[b][tid] = base + incl - c;
+        if (sh.flag) {
+            cta_radix(sh, dkeys, seg, alt + rg.x, len, true);
+            cta_radix(sh, dkeys, seg, alt + rg.x, len, false);
         }
-        __syncthreads();
-        // 2. one stable scatter pass per varying byte
-        uint32_t* src = vals + start;
-        uint32_t* dst = alt + start;
-        const uint32_t lt = lanemask_lt();
-        for (int b = 0; b < 4; ++b) {
-            if (((vary >> (8 * b)) & 255u) == 0u) continue;  // constant byte: identity pass
-            const int shift = 8 * b;
-            for (int c0 = 0; c0 < len; c0 += SEG_CHUNK) {
-                const int wbase = c0 + warp * (SEG_ITEMS * 32);
-                uint32_t v[SEG_ITEMS], d[SEG_ITEMS], rank[SEG_ITEMS];
-    #pragma unroll
-                for (int i = 0; i < SEG_ITEMS; ++i) {
-                    const int idx = wbase + i * 32 + lane;
-                    v[i] = idx < len ? src[idx] : 0u;
-                    d[i] = idx < len ? (dkeys[v[i]] >> shift) & 255u : 256u;
-                }
-    #pragma unroll
-                for (int k = 0; k < SEG_WARPS; ++k) s_whist[k][tid] = 0u;
-                __syncthreads();
-    #pragma unroll
-                for (int i = 0; i < SEG_ITEMS; ++i) {
-                    const bool valid = d[i] < 256u;
-                    uint32_t* pm = &s_peers[warp][i & 1][valid ? d[i] : 0];
-                    if (valid) atomicOr(pm, 1u << lane);
-                    __syncwarp();
-                    const uint32_t peers = valid ? *pm : 0u;
-                    const uint32_t old = valid ? s_whist[warp][d[i]] : 0u;
-                    __syncwarp();
-                    if (valid && (peers & lt) == 0u) {
-                        s_whist[warp][d[i]] = old + (uint32_t)__popc(peers);
-                        *pm = 0u;
-                    }
-                    rank[i] = old + (uint32_t)__popc(peers & lt);
-                }
-                __syncthreads();
-                // per digit: warp offsets within the chunk, then advance the digit start
-                {
-                    uint32_t run = s_hist[b][tid];
-    #pragma unroll
-                    for (int w = 0; w < SEG_WARPS; ++w) {
-                        const uint32_t cnt = s_whist[w][tid];
-                        s_whist[w][tid] = run;
-                        run += cnt;
-                    }
-                    s_hist[b][tid] = run;
-                }
-                __syncthreads();
-    #pragma unroll
-                for (int i = 0; i < SEG_ITEMS; ++i)
-                    if (d[i] < 256u) dst[s_whist[warp][d[i]] + rank[i]] = v[i];
-                __syncthreads();
-            }
-            uint32_t* t = src;
-            src = dst;
-            dst = t;
-        }
-        if (src != vals + start) {  // odd number of passes: copy back
-            for (int i = tid; i < len; i += SEG_THREADS) vals[start + i] = src[i];
-        }
-        __syncthreads();  // shared state is reset for the next tile
     }
 }
 
