@@ -23,126 +23,142 @@ constexpr int SEG_WARPS = SEG_THREADS / 32;
 constexpr int SEG_ITEMS = 4;
 constexpr int SEG_CHUNK = SEG_THREADS * SEG_ITEMS;
 
-// Short lists (the common case): one warp per tile, the whole list in
-// registers (WS_ITEMS per lane, input order = (item, lane)).  Each varying
-// key byte is one stable pass: a peer-mask ranking (per-warp shared atomic
-// OR; the lowest peer adds the group to the digit count, so no contended
-// counting) that parks every item's rank within its digit in shared
-// memory, a warp scan of the 256 digit counts, a scatter to the digit start
-// + rank and a gather back into registers -- no CTA barriers.  Sized to
-// stay under 96 registers so a frame's tiles fit one wave.  Longer lists
-// are left to segsort_kernel below.
-constexpr int WS_ITEMS = 16;
-constexpr int WS_MAX = 32 * WS_ITEMS;  // 512 entries
+// Short lists (the common case, len <= WS_MAX): one CTA of 4 warps per
+// tile, 4 items per thread in registers (input order = (warp, item, lane)),
+// everything else in shared memory.  Each varying key byte is one stable
+// pass: per-warp peer-mask ranking (shared atomic OR; the lowest peer adds
+// the group to the warp's digit count), a CTA scan of the digits' per-warp
+// counts, a scatter to the digit start + warp offset + rank and a gather
+// back into registers.  Four items per lane keep the per-pass dependency
+// chain short (the ranking is the latency-bound part).
 constexpr int WS_WARPS = 4;
+constexpr int WS_THREADS = 32 * WS_WARPS;
+constexpr int WS_ITEMS = 4;
+constexpr int WS_MAX = WS_THREADS * WS_ITEMS;  // 512 entries
 
-__global__ void __launch_bounds__(32 * WS_WARPS, 5) segsort_warp_kernel(const uint2* __restrict__ ranges, int n_tiles,
-                                                                       const uint32_t* __restrict__ dkeys,
-                                                                       uint32_t* __restrict__ vals) {
+__global__ void __launch_bounds__(WS_THREADS) segsort_small_kernel(const uint2* __restrict__ ranges,
+                                                                   const uint32_t* __restrict__ dkeys,
+                                                                   uint32_t* __restrict__ vals) {
     griddep_wait();
     __shared__ uint32_t s_peers[WS_WARPS][2][256];
-    __shared__ uint32_t s_cnt[WS_WARPS][256];  // digit counts, then digit starts
-    __shared__ uint32_t s_key[WS_WARPS][WS_MAX], s_val[WS_WARPS][WS_MAX];
-    __shared__ uint16_t s_rank[WS_WARPS][WS_MAX];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = blockIdx.x * WS_WARPS + warp;
-    if (tile >= n_tiles) return;
-    const uint2 rg = ranges[tile];
+    __shared__ uint32_t s_whist[WS_WARPS][256];  // per-warp digit counts, then their output offsets
+    __shared__ uint32_t s_key[WS_MAX], s_val[WS_MAX];
+    __shared__ uint32_t s_tmp[WS_WARPS];
+    __shared__ uint32_t s_red[4];  // key or / and, index or / and
+    __shared__ uint32_t s_tie;
+    const uint2 rg = ranges[blockIdx.x];
     const int len = (int)(rg.y - rg.x);
     if (len <= 1 || len > WS_MAX) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t* gv = vals + rg.x;
+    const int ibase = warp * (32 * WS_ITEMS) + lane;  // item i at ibase + 32 i
     uint32_t k[WS_ITEMS], v[WS_ITEMS];
+    if (tid == 0) {
+        s_red[0] = 0u;
+        s_red[1] = ~0u;
+        s_red[2] = 0u;
+        s_red[3] = ~0u;
+        s_tie = 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < WS_ITEMS; ++i) v[i] = ibase + 32 * i < len ? gv[ibase + 32 * i] : 0u;
     uint32_t ko = 0u, ka = ~0u, vo = 0u, va = ~0u;
 #pragma unroll
     for (int i = 0; i < WS_ITEMS; ++i) {
-        const int idx = i * 32 + lane;
-        v[i] = idx < len ? gv[idx] : 0u;
-    }
-#pragma unroll
-    for (int i = 0; i < WS_ITEMS; ++i) {
-        const int idx = i * 32 + lane;
-        k[i] = idx < len ? dkeys[v[i]] : 0u;
-        if (idx < len) {
+        const bool in = ibase + 32 * i < len;
+        k[i] = in ? dkeys[v[i]] : 0u;
+        if (in) {
             ko |= k[i];
             ka &= k[i];
             vo |= v[i];
             va &= v[i];
         }
     }
-    const uint32_t kvary = __reduce_or_sync(0xffffffffu, ko) ^ __reduce_and_sync(0xffffffffu, ka);
-    {
-        uint4* z = reinterpret_cast<uint4*>(&s_peers[warp][0][0]);
-        for (int j = lane; j < 2 * 256 / 4; j += 32) z[j] = make_uint4(0u, 0u, 0u, 0u);
+    for (int j = lane; j < 2 * 256; j += 32) (&s_peers[warp][0][0])[j] = 0u;
+    __syncthreads();
+    ko = __reduce_or_sync(0xffffffffu, ko);
+    ka = __reduce_and_sync(0xffffffffu, ka);
+    vo = __reduce_or_sync(0xffffffffu, vo);
+    va = __reduce_and_sync(0xffffffffu, va);
+    if (lane == 0) {
+        atomicOr(&s_red[0], ko);
+        atomicAnd(&s_red[1], ka);
+        atomicOr(&s_red[2], vo);
+        atomicAnd(&s_red[3], va);
     }
+    __syncthreads();
+    const uint32_t kvary = s_red[0] ^ s_red[1], vvary = s_red[2] ^ s_red[3];
     const uint32_t lt = lanemask_lt();
-    uint32_t* cnt = s_cnt[warp];
     // one stable pass over byte `shift` of the depth keys (by_id false) or
     // of the source indices (by_id true)
     auto pass = [&](bool by_id, int shift) {
-        {
-            uint4* z = reinterpret_cast<uint4*>(cnt);
-            for (int j = lane; j < 256 / 4; j += 32) z[j] = make_uint4(0u, 0u, 0u, 0u);
-        }
+        for (int j = lane; j < 256; j += 32) s_whist[warp][j] = 0u;
         __syncwarp();
+        uint32_t rank[WS_ITEMS], dg[WS_ITEMS];
 #pragma unroll
         for (int i = 0; i < WS_ITEMS; ++i) {
-            const bool valid = i * 32 + lane < len;
+            const bool valid = ibase + 32 * i < len;
             const uint32_t d = ((by_id ? v[i] : k[i]) >> shift) & 255u;
+            dg[i] = d;
             uint32_t* pm = &s_peers[warp][i & 1][d];
             if (valid) atomicOr(pm, 1u << lane);
             __syncwarp();
             const uint32_t peers = valid ? *pm : 0u;
-            const uint32_t old = valid ? cnt[d] : 0u;
+            const uint32_t old = valid ? s_whist[warp][d] : 0u;
             __syncwarp();
-            if (valid) {
-                if ((peers & lt) == 0u) {
-                    cnt[d] = old + (uint32_t)__popc(peers);
-                    *pm = 0u;
+            if (valid && (peers & lt) == 0u) {
+                s_whist[warp][d] = old + (uint32_t)__popc(peers);
+                *pm = 0u;
+            }
+            rank[i] = old + (uint32_t)__popc(peers & lt);
+        }
+        __syncthreads();
+        {  // digits 2 tid, 2 tid + 1: CTA exclusive scan of the totals, then per-warp offsets
+            uint32_t c[2][WS_WARPS], tot[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                tot[h] = 0u;
+#pragma unroll
+                for (int w = 0; w < WS_WARPS; ++w) {
+                    c[h][w] = s_whist[w][2 * tid + h];
+                    tot[h] += c[h][w];
                 }
-                s_rank[warp][i * 32 + lane] = (uint16_t)(old + (uint32_t)__popc(peers & lt));
             }
+            const uint32_t mine = tot[0] + tot[1];
+            uint32_t incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_tmp[warp] = incl;
+            __syncthreads();
+            uint32_t run = incl - mine;
+            for (int w = 0; w < warp; ++w) run += s_tmp[w];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int w = 0; w < WS_WARPS; ++w) {
+                    s_whist[w][2 * tid + h] = run;
+                    run += c[h][w];
+                }
         }
-        __syncwarp();
-        {  // exclusive scan of the 256 digit counts: 8 per lane + warp scan
-            uint32_t c8[8], run = 0;
+        __syncthreads();
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                c8[j] = cnt[lane * 8 + j];
-                run += c8[j];
+        for (int i = 0; i < WS_ITEMS; ++i)
+            if (ibase + 32 * i < len) {
+                const uint32_t pos = s_whist[warp][dg[i]] + rank[i];
+                s_key[pos] = k[i];
+                s_val[pos] = v[i];
             }
-            uint32_t incl = run;
+        __syncthreads();
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += y;
+        for (int i = 0; i < WS_ITEMS; ++i)
+            if (ibase + 32 * i < len) {
+                k[i] = s_key[ibase + 32 * i];
+                v[i] = s_val[ibase + 32 * i];
             }
-            uint32_t base = incl - run;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                cnt[lane * 8 + j] = base;
-                base += c8[j];
-            }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < WS_ITEMS; ++i) {
-            const int idx = i * 32 + lane;
-            if (idx < len) {
-                const uint32_t pos = cnt[((by_id ? v[i] : k[i]) >> shift) & 255u] + s_rank[warp][idx];
-                s_key[warp][pos] = k[i];
-                s_val[warp][pos] = v[i];
-            }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < WS_ITEMS; ++i) {
-            const int idx = i * 32 + lane;
-            if (idx < len) {
-                k[i] = s_key[warp][idx];
-                v[i] = s_val[warp][idx];
-            }
-        }
-        __syncwarp();
+        __syncthreads();
     };
     bool tie = kvary == 0u;  // all depths equal: one tie run
     if (!tie) {
@@ -152,23 +168,22 @@ __global__ void __launch_bounds__(32 * WS_WARPS, 5) segsort_warp_kernel(const ui
         bool t = false;
 #pragma unroll
         for (int i = 0; i < WS_ITEMS; ++i) {
-            const int idx = i * 32 + lane;
-            if (idx > 0 && idx < len) t = t || s_key[warp][idx] == s_key[warp][idx - 1];
+            const int idx = ibase + 32 * i;
+            if (idx > 0 && idx < len) t = t || s_key[idx] == s_key[idx - 1];
         }
-        tie = __any_sync(0xffffffffu, t);
+        if (__any_sync(0xffffffffu, t) && lane == 0) s_tie = 1u;
+        __syncthreads();
+        tie = s_tie != 0u;
     }
     if (tie) {  // (depth, index) order: index bytes first, then depth bytes
-        const uint32_t vvary = __reduce_or_sync(0xffffffffu, vo) ^ __reduce_and_sync(0xffffffffu, va);
         for (int b = 0; b < 4; ++b)
             if ((vvary >> (8 * b)) & 255u) pass(true, 8 * b);
         for (int b = 0; b < 4; ++b)
             if ((kvary >> (8 * b)) & 255u) pass(false, 8 * b);
     }
 #pragma unroll
-    for (int i = 0; i < WS_ITEMS; ++i) {
-        const int idx = i * 32 + lane;
-        if (idx < len) gv[idx] = v[i];
-    }
+    for (int i = 0; i < WS_ITEMS; ++i)
+        if (ibase + 32 * i < len) gv[ibase + 32 * i] = v[i];
 }
 
 // Long lists (len > WS_MAX): a CTA sorts one range with chunked passes
@@ -308,7 +323,7 @@ __global__ void __launch_bounds__(SEG_THREADS) segsort_kernel(const uint2* __res
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const uint2 rg = ranges[tile];
         const int len = (int)(rg.y - rg.x);
-        if (len <= WS_MAX) continue;  // segsort_warp_kernel's
+        if (len <= WS_MAX) continue;  // segsort_small_kernel's
         uint32_t* seg = vals + rg.x;
         cta_radix(sh, dkeys, seg, alt + rg.x, len, false);
         // equal depths next to each other?  then (index, then depth) passes
@@ -329,14 +344,8 @@ __global__ void __launch_bounds__(SEG_THREADS) segsort_kernel(const uint2* __res
 int launch_segsort(const uint2* ranges, int n_tiles, const uint32_t* dkeys, uint32_t* vals, uint32_t* alt,
                    cudaStream_t s) {
     if (n_tiles <= 0) return 0;
-    static const bool carve = [] {  // 5 CTAs x 41 KB: ask for the full shared-memory carveout
-        return cudaFuncSetAttribute(segsort_warp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    (int)cudaSharedmemCarveoutMaxShared) == cudaSuccess;
-    }();
-    (void)carve;
-    launch_k(segsort_warp_kernel, dim3((unsigned)((n_tiles + WS_WARPS - 1) / WS_WARPS)), dim3(32 * WS_WARPS), 0, s,
-             ranges, n_tiles, dkeys, vals);
-    if (check_launch("segsort_warp_kernel")) return -1;
+    launch_k(segsort_small_kernel, dim3((unsigned)n_tiles), dim3(WS_THREADS), 0, s, ranges, dkeys, vals);
+    if (check_launch("segsort_small_kernel")) return -1;
     launch_k(segsort_kernel, dim3((unsigned)min(n_tiles, 2 * 148)), dim3(SEG_THREADS), 0, s, ranges, n_tiles, dkeys,
              vals, alt);
     return check_launch("segsort_kernel");

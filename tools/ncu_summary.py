@@ -24,7 +24,7 @@ STAGE_OF = [  # kernel-name regex -> bench stage name (first capture of each ker
     (r"project_fwd_kernel", "project"),
     (r"onesweep_kernel<unsigned int, (16|4)", "sort_u32"),
     (r"emit_scan_kernel", "scan_emit"),
-    (r"segsort_warp_kernel", "segsort"),
+    (r"segsort_small_kernel", "segsort"),
     (r"ranges_u32_kernel", "tile_sort_ranges"),
     (r"raster_fwd_kernel", "raster_fwd"),
     (r"raster_bwd_rec_kernel", "raster_bwd"),
