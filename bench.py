@@ -438,11 +438,11 @@ def run_ours(args):
         "intersections_per_step_rank": int(I),
         "e2e": e2e,
         # per view (csrc/frame.cu): scatter binning: init, project (+ tile counts), tile scan
-        # (+ raster order), pair scatter, 2 per-tile sort kernels, raster fwd | raster bwd, project bwd
+        # (+ raster order), pair scatter, per-tile sort, raster fwd | raster bwd, project bwd
         # (its last block reduces d_view); depth-first: init, project, 4 depth passes, fused
         # scan+emit, tp tile passes, ranges, (tile order for grids over one raster wave), raster fwd |
         # raster bwd, project bwd
-        "gpu_launches": int(args.steps * len(cams) * (9 if segment_binning(n) else
+        "gpu_launches": int(args.steps * len(cams) * (8 if segment_binning(n) else
                                                       11 + tp + tile_order_launches(cams[0]))),
         "roofline": roof,
         "stages": st,

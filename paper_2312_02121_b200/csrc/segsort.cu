@@ -18,7 +18,7 @@
 
 namespace gs {
 
-constexpr int SEG_THREADS = 256;
+constexpr int SEG_THREADS = 128;
 constexpr int SEG_WARPS = SEG_THREADS / 32;
 constexpr int SEG_ITEMS = 4;
 constexpr int SEG_CHUNK = SEG_THREADS * SEG_ITEMS;
@@ -36,21 +36,25 @@ constexpr int WS_THREADS = 32 * WS_WARPS;
 constexpr int WS_ITEMS = 4;
 constexpr int WS_MAX = WS_THREADS * WS_ITEMS;  // 512 entries
 
-__global__ void __launch_bounds__(WS_THREADS) segsort_small_kernel(const uint2* __restrict__ ranges,
-                                                                   const uint32_t* __restrict__ dkeys,
-                                                                   uint32_t* __restrict__ vals) {
-    griddep_wait();
-    __shared__ uint32_t s_peers[WS_WARPS][2][256];
-    __shared__ uint32_t s_whist[WS_WARPS][256];  // per-warp digit counts, then their output offsets
-    __shared__ uint32_t s_key[WS_MAX], s_val[WS_MAX];
-    __shared__ uint32_t s_tmp[WS_WARPS];
-    __shared__ uint32_t s_red[4];  // key or / and, index or / and
-    __shared__ uint32_t s_tie;
-    const uint2 rg = ranges[blockIdx.x];
-    const int len = (int)(rg.y - rg.x);
-    if (len <= 1 || len > WS_MAX) return;
+struct SmallShared {
+    uint32_t peers[WS_WARPS][2][256];
+    uint32_t whist[WS_WARPS][256];  // per-warp digit counts, then their output offsets
+    uint32_t key[WS_MAX], val[WS_MAX];
+    uint32_t tmp[WS_WARPS];
+    uint32_t red[4];  // key or / and, index or / and
+    uint32_t tie;
+};
+
+__device__ __forceinline__ void small_sort(SmallShared& sh, const uint32_t* __restrict__ dkeys, uint32_t* gv,
+                                           int len) {
+    auto& s_peers = sh.peers;
+    auto& s_whist = sh.whist;
+    auto& s_key = sh.key;
+    auto& s_val = sh.val;
+    auto& s_tmp = sh.tmp;
+    auto& s_red = sh.red;
+    auto& s_tie = sh.tie;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t* gv = vals + rg.x;
     const int ibase = warp * (32 * WS_ITEMS) + lane;  // item i at ibase + 32 i
     uint32_t k[WS_ITEMS], v[WS_ITEMS];
     if (tid == 0) {
@@ -113,18 +117,17 @@ __global__ void __launch_bounds__(WS_THREADS) segsort_small_kernel(const uint2* 
             rank[i] = old + (uint32_t)__popc(peers & lt);
         }
         __syncthreads();
-        {  // digits 2 tid, 2 tid + 1: CTA exclusive scan of the totals, then per-warp offsets
-            uint32_t c[2][WS_WARPS], tot[2];
+        {  // digits DPT tid ..: CTA exclusive scan of the totals, then per-warp offsets
+            constexpr int DPT = 256 / WS_THREADS;
+            uint32_t c[DPT][WS_WARPS], mine = 0u;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                tot[h] = 0u;
+            for (int h = 0; h < DPT; ++h) {
 #pragma unroll
                 for (int w = 0; w < WS_WARPS; ++w) {
-                    c[h][w] = s_whist[w][2 * tid + h];
-                    tot[h] += c[h][w];
+                    c[h][w] = s_whist[w][DPT * tid + h];
+                    mine += c[h][w];
                 }
             }
-            const uint32_t mine = tot[0] + tot[1];
             uint32_t incl = mine;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -136,10 +139,10 @@ __global__ void __launch_bounds__(WS_THREADS) segsort_small_kernel(const uint2* 
             uint32_t run = incl - mine;
             for (int w = 0; w < warp; ++w) run += s_tmp[w];
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < DPT; ++h)
 #pragma unroll
                 for (int w = 0; w < WS_WARPS; ++w) {
-                    s_whist[w][2 * tid + h] = run;
+                    s_whist[w][DPT * tid + h] = run;
                     run += c[h][w];
                 }
         }
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(WS_THREADS) segsort_small_kernel(const uint2* 
         if (ibase + 32 * i < len) gv[ibase + 32 * i] = v[i];
 }
 
-// Long lists (len > WS_MAX): a CTA sorts one range with chunked passes
+// Long lists (len > WS_MAX): the CTA sorts its range with chunked passes
 // through L2 (ping-pong between the range and its alternate buffer).  One
 // read pass builds the per-byte histograms of the key (depth key, or source
 // index when by_id) and finds its constant bytes; each varying byte is then
@@ -232,11 +235,17 @@ __device__ void cta_radix(SegShared& sh, const uint32_t* __restrict__ dkeys, uin
     }
     __syncthreads();
     const uint32_t vary = sh.vor ^ sh.vand;
-    // exclusive digit starts per byte (thread = digit)
+    // exclusive digit starts per byte (thread = DPT consecutive digits)
+    constexpr int DPT = 256 / SEG_THREADS;
 #pragma unroll 1
     for (int b = 0; b < 4; ++b) {
-        const uint32_t c = sh.hist[b][tid];
-        uint32_t incl = c;
+        uint32_t c[DPT], mine = 0u;
+#pragma unroll
+        for (int h = 0; h < DPT; ++h) {
+            c[h] = sh.hist[b][DPT * tid + h];
+            mine += c[h];
+        }
+        uint32_t incl = mine;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
@@ -244,10 +253,14 @@ __device__ void cta_radix(SegShared& sh, const uint32_t* __restrict__ dkeys, uin
         }
         if (lane == 31) sh.tmp[warp] = incl;
         __syncthreads();
-        uint32_t base = 0;
+        uint32_t base = incl - mine;
         for (int w = 0; w < warp; ++w) base += sh.tmp[w];
         __syncthreads();
-        sh.hist[b][tid] = base + incl - c;
+#pragma unroll
+        for (int h = 0; h < DPT; ++h) {
+            sh.hist[b][DPT * tid + h] = base;
+            base += c[h];
+        }
     }
     __syncthreads();
     // 2. one stable scatter pass per varying byte
@@ -266,8 +279,7 @@ __device__ void cta_radix(SegShared& sh, const uint32_t* __restrict__ dkeys, uin
                 v[i] = idx < len ? src[idx] : 0u;
                 d[i] = idx < len ? (seg_key(dkeys, v[i], by_id) >> shift) & 255u : 256u;
             }
-#pragma unroll
-            for (int k = 0; k < SEG_WARPS; ++k) sh.whist[k][tid] = 0u;
+            for (int k = tid; k < SEG_WARPS * 256; k += SEG_THREADS) (&sh.whist[0][0])[k] = 0u;
             __syncthreads();
 #pragma unroll
             for (int i = 0; i < SEG_ITEMS; ++i) {
@@ -286,15 +298,15 @@ __device__ void cta_radix(SegShared& sh, const uint32_t* __restrict__ dkeys, uin
             }
             __syncthreads();
             // per digit: warp offsets within the chunk, then advance the digit start
-            {
-                uint32_t run = sh.hist[b][tid];
+            for (int dd = tid; dd < 256; dd += SEG_THREADS) {
+                uint32_t run = sh.hist[b][dd];
 #pragma unroll
                 for (int w = 0; w < SEG_WARPS; ++w) {
-                    const uint32_t cnt = sh.whist[w][tid];
-                    sh.whist[w][tid] = run;
+                    const uint32_t cnt = sh.whist[w][dd];
+                    sh.whist[w][dd] = run;
                     run += cnt;
                 }
-                sh.hist[b][tid] = run;
+                sh.hist[b][dd] = run;
             }
             __syncthreads();
 #pragma unroll
@@ -312,42 +324,43 @@ __device__ void cta_radix(SegShared& sh, const uint32_t* __restrict__ dkeys, uin
     __syncthreads();
 }
 
-// A few CTAs stride over the tiles (long lists are rare) instead of one CTA
-// per tile that mostly exits at once.
-__global__ void __launch_bounds__(SEG_THREADS) segsort_kernel(const uint2* __restrict__ ranges, int n_tiles,
-                                                              const uint32_t* __restrict__ dkeys,
-                                                              uint32_t* __restrict__ vals,
-                                                              uint32_t* __restrict__ alt) {
+// One CTA per tile: short lists sorted in shared memory (small_sort), long
+// ones with chunked passes through L2 (cta_radix) plus the tie repair.
+__global__ void __launch_bounds__(WS_THREADS) segsort_kernel(const uint2* __restrict__ ranges,
+                                                             const uint32_t* __restrict__ dkeys,
+                                                             uint32_t* __restrict__ vals,
+                                                             uint32_t* __restrict__ alt) {
     griddep_wait();
-    __shared__ SegShared sh;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const uint2 rg = ranges[tile];
-        const int len = (int)(rg.y - rg.x);
-        if (len <= WS_MAX) continue;  // segsort_small_kernel's
-        uint32_t* seg = vals + rg.x;
-        cta_radix(sh, dkeys, seg, alt + rg.x, len, false);
-        // equal depths next to each other?  then (index, then depth) passes
-        if (threadIdx.x == 0) sh.flag = 0u;
-        __syncthreads();
-        bool t = false;
-        for (int i = 1 + (int)threadIdx.x; i < len; i += SEG_THREADS)
-            t = t || dkeys[seg[i]] == dkeys[seg[i - 1]];
-        if (__any_sync(0xffffffffu, t) && (threadIdx.x & 31) == 0) sh.flag = 1u;
-        __syncthreads();
-        if (sh.flag) {
-            cta_radix(sh, dkeys, seg, alt + rg.x, len, true);
-            cta_radix(sh, dkeys, seg, alt + rg.x, len, false);
-        }
+    __shared__ union {
+        SmallShared small;
+        SegShared large;
+    } sh;
+    const uint2 rg = ranges[blockIdx.x];
+    const int len = (int)(rg.y - rg.x);
+    if (len <= 1) return;
+    uint32_t* seg = vals + rg.x;
+    if (len <= WS_MAX) {
+        small_sort(sh.small, dkeys, seg, len);
+        return;
+    }
+    cta_radix(sh.large, dkeys, seg, alt + rg.x, len, false);
+    // equal depths next to each other?  then (index, then depth) passes
+    if (threadIdx.x == 0) sh.large.flag = 0u;
+    __syncthreads();
+    bool t = false;
+    for (int i = 1 + (int)threadIdx.x; i < len; i += SEG_THREADS) t = t || dkeys[seg[i]] == dkeys[seg[i - 1]];
+    if (__any_sync(0xffffffffu, t) && (threadIdx.x & 31) == 0) sh.large.flag = 1u;
+    __syncthreads();
+    if (sh.large.flag) {
+        cta_radix(sh.large, dkeys, seg, alt + rg.x, len, true);
+        cta_radix(sh.large, dkeys, seg, alt + rg.x, len, false);
     }
 }
 
 int launch_segsort(const uint2* ranges, int n_tiles, const uint32_t* dkeys, uint32_t* vals, uint32_t* alt,
                    cudaStream_t s) {
     if (n_tiles <= 0) return 0;
-    launch_k(segsort_small_kernel, dim3((unsigned)n_tiles), dim3(WS_THREADS), 0, s, ranges, dkeys, vals);
-    if (check_launch("segsort_small_kernel")) return -1;
-    launch_k(segsort_kernel, dim3((unsigned)min(n_tiles, 2 * 148)), dim3(SEG_THREADS), 0, s, ranges, n_tiles, dkeys,
-             vals, alt);
+    launch_k(segsort_kernel, dim3((unsigned)n_tiles), dim3(WS_THREADS), 0, s, ranges, dkeys, vals, alt);
     return check_launch("segsort_kernel");
 }
 
