@@ -33,7 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fwd+bwd frames/sec and Gaussian-pixel evals/s at 1/2/4/8 B200 (vs roofline)"
-L2_FLUSH_BYTES = 256 << 20
+L2_FLUSH_BYTES = 192 << 20  # > 1.5x the 126 MB L2
 
 
 def parse():
@@ -370,14 +370,18 @@ def run_ours(args):
     F_bwd = 8 * counts_b[0] + 4 * counts_b[1] + 42 * counts_b[2]
     seg = segment_binning(n)
     work = {
-        "project": ("hbm", 84.0 * n * nv),                   # read 44 B, write xydr 16 + conic 16 + tiles 4 + depth key 4
-        # depth-first: 4 passes x (key+value) x (read+write); segment binning: no global depth sort
+        # read 44 B, write xydr 16 + conic 16 + tiles 4 + depth key 4 (scatter binning: + tile-count atomics)
+        "project": ("hbm", 84.0 * n * nv),
+        # depth-first: 4 passes x (key+value) x (read+write); scatter binning: no global depth sort
         "depth_sort": ("none", 0.0) if seg else ("hbm", 4 * 16.0 * n * nv),
-        # fused scan + emission: (order +) count + xydr gather per Gaussian, pairs out
-        "scan_emit": ("hbm", (4.0 if seg else 8.0) * n * nv + 16.0 * n * nv + 8.0 * I),
-        # tile passes (key+value, read+write) + ranges; segment binning adds the per-tile
-        # depth sort (value in, key gather, value out)
-        "tile_sort_ranges": ("hbm", tp * 16.0 * I + 4.0 * I + 8.0 * n_tiles + (12.0 * I if seg else 0.0)),
+        # depth-first: fused scan + emission, (order +) count + xydr gather per Gaussian, pairs out;
+        # scatter: tile scan (8 counter replicas + ranges) + count + xydr per Gaussian, pairs out
+        "scan_emit": ("hbm", (40.0 * n_tiles + 20.0 * n * nv + 8.0 * I) if seg else
+                      (8.0 * n * nv + 16.0 * n * nv + 8.0 * I)),
+        # depth-first: tile passes (key+value, read+write) + ranges; scatter: per-tile sort
+        # (value in, key gather, value out) + ranges
+        "tile_sort_ranges": ("hbm", (12.0 * I + 8.0 * n_tiles) if seg else
+                             (tp * 16.0 * I + 4.0 * I + 8.0 * n_tiles)),
         "raster_fwd": ("fp32", float(F_fwd)),
         "raster_bwd": ("fp32", float(F_bwd)),
         "project_bwd": ("hbm", 104.0 * n * nv),
@@ -433,7 +437,7 @@ def run_ours(args):
                    "early_termination": True, "background": "black",
                    "parallelism": (f"tile-row bands x{world} (rows {band})" if band else f"view-sharded x{world}") + (" + NCCL allreduce 14 fp32/Gaussian" if world > 1 else ""),
                    "cuda_graph": graph is not None,
-                   "l2": "flushed between timed steps (256 MiB write, untimed)"},
+                   "l2": "flushed between timed steps (192 MiB write, untimed)"},
         "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
         "intersections_per_step_rank": int(I),
         "e2e": e2e,

@@ -169,10 +169,10 @@ def pipeline(engine: RenderStep, host_params, host_d_images, out_host, steps: in
         h2d.wait_event(done[b])  # the replay that last read set b finished
         engine.load(b, host_params, host_d_images, stream=h2d)
         loaded[b].record(h2d)
+        if flush is not None:
+            flush.zero_()  # benchmarking: evict L2 (workspace comes from HBM); overlaps this step's H2D
         comp.wait_event(loaded[b])
         comp.wait_event(read[b])  # set b's previous gradients were read back
-        if flush is not None:
-            flush.zero_()  # benchmarking: evict L2 (inputs and workspace come from HBM)
         engine.replay(b)
         if allreduce is not None:
             allreduce(engine.grads(b))  # data-parallel views: sum over ranks

@@ -7,5 +7,5 @@ $CMD > gpurun_out/plain.log 2>&1 || { echo "plain bench failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
     $CMD > gpurun_out/ncu_launch.log 2>&1; echo "launch list rc=$?"
 PYTHONPATH=. python tools/prof_frame.py 1 > gpurun_out/plain_frame.log 2>&1 || { echo "plain frame failed"; exit 1; }
-PYTHONPATH=. ncu --set full --clock-control none --import-source on -s 12 -c 16 -o gpurun_out/prof_c1 \
+PYTHONPATH=. ncu --set full --clock-control none --import-source on -s 0 -c 40 -o gpurun_out/prof_c1 \
     python tools/prof_frame.py 1 > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?"
