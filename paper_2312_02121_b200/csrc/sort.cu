@@ -347,6 +347,21 @@ int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const 
     if (small)
         return run_passes<K, SMALL_ITEMS>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s,
                                           identity_vals);
+    if constexpr (sizeof(K) == 4) {  // A/B switch: GS_SORT_ITEMS=8|12 (default SortCfg)
+        static int items_env = -2;
+        if (items_env == -2) {
+            const char* e = getenv("GS_SORT_ITEMS");
+            items_env = e ? atoi(e) : -1;
+        }
+        if (items_env == 8)
+            return run_passes<K, 8>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
+        if (items_env == 12)
+            return run_passes<K, 12>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
+        if (items_env == 20)
+            return run_passes<K, 20>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
+        if (items_env == 24)
+            return run_passes<K, 24>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
+    }
     return run_passes<K, BIG>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s, identity_vals);
 }
 template int run_onesweep<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, int64_t,

@@ -202,3 +202,43 @@ def test_binning_strategies_agree_on_configs(config, cuda):
         assert int(lens.max()) > 512
     for a, b in zip(got[1], got[2]):
         assert torch.equal(a, b)
+
+
+def test_scatter_binning_ties_in_long_lists(cuda):
+    """Scatter binning writes a tile's pairs in arbitrary order; exact depth
+    ties must still come out in source-index order, in the shared-memory
+    per-tile sort (<= 512 entries) and in the chunked long-list sort alike.
+    2400 splats over a 64x64 image (16 tiles, lists of 0 to ~1700 entries),
+    a third of them at one exact
+    depth and a third at another, checked against depth-first binning (a
+    stable global sort, sg/binning.py:50-65's (depth, index) order)."""
+    from paper_2312_02121_b200 import ops
+    rng = np.random.default_rng(7)
+    n = 2400
+    means = np.zeros((n, 3), np.float32)
+    means[:, 0] = rng.uniform(-0.5, 0.5, n)
+    means[:, 1] = rng.uniform(-0.5, 0.5, n)
+    means[:, 2] = rng.uniform(-0.5, 0.5, n)
+    means[0::3, 2] = 0.25   # exact ties
+    means[1::3, 2] = -0.125
+    scales = np.exp(rng.uniform(np.log(0.01), np.log(0.2), (n, 3))).astype(np.float32)
+    quats = rng.normal(size=(n, 4)).astype(np.float32)
+    quats /= np.linalg.norm(quats, axis=1, keepdims=True)
+    opac = rng.uniform(0.2, 0.9, n).astype(np.float32)
+    cols = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+    view = [[1.0, 0, 0, 0], [0, 1.0, 0, 0], [0, 0, 1.0, 4.0], [0, 0, 0, 1.0]]
+    cam = ops.CameraParams(view=view, fx=60.0, fy=60.0, cx=31.5, cy=31.5, width=64, height=64, near=0.1, far=100.0)
+    t = _tensors((means, scales, quats, opac, cols), cuda)
+    got = {}
+    try:
+        for mode in (1, 2):
+            ops.set_option("binning", mode)
+            fr = ops.frame_forward(*t, cam, (0.0, 0.0, 0.0), True)
+            tv = fr.tensors()
+            got[mode] = (tv["ranges"].clone(), tv["sorted_vals"].clone(), fr.image.clone())
+    finally:
+        ops.set_option("binning", 0)
+    lens = got[1][0][:, 1] - got[1][0][:, 0]
+    assert int(lens.max()) > 512 and bool(((lens > 1) & (lens <= 512)).any())
+    for a, b in zip(got[1], got[2]):
+        assert torch.equal(a, b)
