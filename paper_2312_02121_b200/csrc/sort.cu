@@ -15,6 +15,12 @@
 #include "common.cuh"
 #include "internal.cuh"
 
+// decoupled look-back window (status loads in flight per round trip; 4 beat
+// 1, 8 and 16 at configs 2 and 4)
+#ifndef GS_SORT_LB
+#define GS_SORT_LB 4
+#endif
+
 namespace gs {
 
 constexpr int SORT_THREADS = 256;
@@ -202,7 +208,7 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
         // loads of a window are in flight together (one L2 round trip per
         // window instead of per predecessor); a not-yet-posted entry is
         // re-polled in place
-        constexpr int LB = 8;
+        constexpr int LB = GS_SORT_LB;
         int p = (int)tile - 1;
         bool found = false;
         while (!found) {
