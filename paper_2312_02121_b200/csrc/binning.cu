@@ -14,11 +14,15 @@ constexpr unsigned long long FLAG_AGG = 1ull << 62;
 constexpr unsigned long long FLAG_PRE = 2ull << 62;
 constexpr unsigned long long VAL_MASK = (1ull << 62) - 1;
 
+// look-back status words (flag and value in one 64-bit word): GPU-scope
+// relaxed accesses (volatile would make them system-scope)
 __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
-    return *(const volatile unsigned long long*)p;
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 __device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long long v) {
-    *(volatile unsigned long long*)p = v;
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // ws layout: [0] tile counter (u32, padded to 16 B), then u64 status[ctas].

@@ -55,8 +55,17 @@ constexpr size_t sort_smem() {
            (size_t)SORT_WARPS * 2 * RADIX * 4;  // peer-mask banks (RANK_OR)
 }
 
-__device__ __forceinline__ uint32_t ldv(const uint32_t* p) { return *(const volatile uint32_t*)p; }
-__device__ __forceinline__ void stv(uint32_t* p, uint32_t v) { *(volatile uint32_t*)p = v; }
+// look-back status words: GPU-scope relaxed accesses (flag and value share
+// one 32-bit word, so no further ordering is needed); volatile would make
+// them system-scope
+__device__ __forceinline__ uint32_t ldv(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void stv(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ int64_t resolve_n(const unsigned long long* n_dev, int64_t n_cap) {
     if (!n_dev) return n_cap;
