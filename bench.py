@@ -65,7 +65,7 @@ def tile_order_launches(cam):
     return 1 if on and cam.tiles_x * cam.tiles_y > 148 * 8 else 0
 
 
-def segment_binning(n):
+def scatter_binning(n):
     """Which frame binning the library uses (csrc/frame.cu, gs_set_option)."""
     mode = int(os.environ.get("GS_BINNING", "0"))
     return mode == 2 or (mode == 0 and n <= 400000)
@@ -368,7 +368,7 @@ def run_ours(args):
     # algorithmic work; per rank-step, all views
     F_fwd = 8 * counts_f[0] + 4 * counts_f[1] + 3 * counts_f[2] + 4 * counts_f[3]
     F_bwd = 8 * counts_b[0] + 4 * counts_b[1] + 42 * counts_b[2]
-    seg = segment_binning(n)
+    seg = scatter_binning(n)
     work = {
         # read 44 B, write xydr 16 + conic 16 + tiles 4 + depth key 4 (scatter binning: + tile-count atomics)
         "project": ("hbm", 84.0 * n * nv),
@@ -446,7 +446,7 @@ def run_ours(args):
         # (its last block reduces d_view); depth-first: init, project, 4 depth passes, fused
         # scan+emit, tp tile passes, ranges, (tile order for grids over one raster wave), raster fwd |
         # raster bwd, project bwd
-        "gpu_launches": int(args.steps * len(cams) * (8 if segment_binning(n) else
+        "gpu_launches": int(args.steps * len(cams) * (8 if scatter_binning(n) else
                                                       11 + tp + tile_order_launches(cams[0]))),
         "roofline": roof,
         "stages": st,

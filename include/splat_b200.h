@@ -58,11 +58,12 @@ typedef struct gs_camera {
 const char* gs_last_error(void);
 int gs_version(void);
 /* Process-wide tuning options.  "binning": the frame path's tile binning,
- * 0 = auto (per-tile segments for n <= 400000 Gaussians, else depth-first),
+ * 0 = auto (scatter for n <= 400000 Gaussians, else depth-first),
  * 1 = depth-first (global stable depth sort, then tile sort of pairs emitted
- * in depth order), 2 = per-tile segments (pairs emitted in index order,
- * tile sort, then each tile's list stably sorted by depth).  Both give
- * sg/binning.py:50-65's (depth, source_index) lists bit for bit. */
+ * in depth order), 2 = scatter (per-tile counts from the projection, pairs
+ * written into their tile ranges through atomic cursors, each range sorted
+ * by (depth, index)).  Both give sg/binning.py:50-65's (depth,
+ * source_index) lists bit for bit. */
 int gs_set_option(const char* name, int value);
 /* Number of SMs of the current device (0 when no device). */
 int gs_device_sm_count(void);

@@ -1,10 +1,15 @@
 // frame.cu -- one differentiable render as two sync-free entry points.
 //
-// gs_frame_forward:  project (+ depth keys and their digit histograms)
+// gs_frame_forward, depth-first binning (large scenes):
+//   project (+ depth keys and their digit histograms)
 //   -> 4-pass onesweep sort of the Gaussians by depth (stable, index order)
 //   -> scan of tile counts in depth order -> emission of (tile, gaussian)
 //   pairs in depth order (+ tile-digit histograms) -> 1-2 pass stable sort by
-//   tile id -> per-tile ranges -> raster forward.
+//   tile id -> per-tile ranges (+ raster order) -> raster forward.
+// gs_frame_forward, scatter binning (N <= 400k):
+//   project (+ depth keys and per-tile intersection counts) -> tile scan
+//   (ranges, cursors, raster order) -> pair scatter -> per-tile (depth,
+//   index) sort (segsort.cu) -> raster forward.
 // gs_frame_backward: raster backward (atomic per-warp accumulation of the
 //   screen-space gradients) -> projection backward (+ fixed-order d_view).
 //
@@ -43,7 +48,7 @@ bool tile_order_enabled(int n_tiles) {
     return on && n_tiles > 148 * 8;
 }
 
-// Scatter binning (segment mode) for small scenes, depth-first otherwise
+// Scatter binning for small scenes, depth-first otherwise
 // (gs_set_option("binning"): 0 auto, 1 depth-first, 2 scatter).
 bool scatter_binning(int64_t n) {
     const int bmode = binning_mode();
@@ -234,7 +239,7 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
         order = at<uint32_t>(ws, L.order);  // 4 passes: back in the primary buffers
     }
     mark(stage_events, 2, s);
-    // 3+4. fused: scan of the tile counts (in depth or index order), total ->
+    // 3+4. fused: scan of the tile counts (in depth order), total ->
     //      meta[1], emission of the (tile, gaussian) pairs + tile-digit histograms
     if (launch_emit_scan(order, at<float>(ws, L.xydr), at<uint32_t>(ws, L.tiles), n, tiles_x, tiles_y,
                          isect_capacity, at<uint32_t>(ws, L.tkeys), at<uint32_t>(ws, L.tvals),

@@ -65,7 +65,7 @@ int launch_ranges_u32(const uint32_t* sorted_tile_keys, int64_t n_cap, const uns
 // segsort.cu: per-tile stable sort of each tile's list by depth key
 int launch_segsort(const uint2* ranges, int n_tiles, const uint32_t* dkeys, uint32_t* vals, uint32_t* alt,
                    cudaStream_t s);
-// binning strategy of the frame path (abi.cu): 0 auto, 1 depth-first, 2 per-tile segments
+// binning strategy of the frame path (abi.cu): 0 auto, 1 depth-first, 2 scatter
 int binning_mode();
 
 // raster.cu

@@ -50,7 +50,7 @@ def test_frame_equals_staged_on_golden(name, cuda):
         assert r["ok"], (name, k, r)
 
 
-@pytest.fixture(params=[1, 2], ids=["depth_first", "segments"])
+@pytest.fixture(params=[1, 2], ids=["depth_first", "scatter"])
 def binning(request, cuda):
     """Run a test under both frame binning strategies (gs_set_option)."""
     from paper_2312_02121_b200 import ops
@@ -61,7 +61,7 @@ def binning(request, cuda):
 
 @pytest.mark.parametrize("name", golden_names())
 def test_binning_strategies_agree(name, binning, cuda):
-    """Depth-first and per-tile-segment binning give the same lists, bit for
+    """Depth-first and scatter binning give the same lists, bit for
     bit (both are sg/binning.py:50-65's (depth, source_index) order)."""
     g = load_golden(name)
     st, g_s, img_s, fr, g_f = _both(g["inputs"], g["camera"], g["background"], g["et"], g["d_image"], cuda)
@@ -181,7 +181,7 @@ def test_forward_bitwise_deterministic(cuda):
 @pytest.mark.parametrize("config", [1, 2])
 def test_binning_strategies_agree_on_configs(config, cuda):
     """Both binnings on BASELINE configs: config 2's lists run to thousands of
-    entries, so the segment path's long-list CTA sort (len > 512) is covered
+    entries, so the scatter path's long-list CTA sort (len > 512) is covered
     besides the one-warp sort."""
     from paper_2312_02121_b200 import ops
     from paper_2312_02121_b200.scenes import make_config
