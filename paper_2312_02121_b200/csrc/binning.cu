@@ -559,7 +559,11 @@ int launch_tile_scan(uint32_t* tcount, int n_tiles, int64_t capacity, uint2* ran
 }
 
 // Every visible Gaussian's (tile, gaussian) pairs into the tiles' ranges
-// through the atomic cursors; warps walk 32 Gaussians' rects together.
+// through the atomic cursors; warps walk 32 Gaussians' rects together,
+// SCATTER_UNROLL cursor atomics in flight per lane.
+#ifndef SCATTER_UNROLL
+#define SCATTER_UNROLL 4
+#endif
 __global__ void __launch_bounds__(256) scatter_pairs_kernel(const float4* __restrict__ xydr,
                                                             const uint32_t* __restrict__ counts, int n, int tiles_x,
                                                             int tiles_y, uint32_t capacity,
@@ -575,14 +579,14 @@ __global__ void __launch_bounds__(256) scatter_pairs_kernel(const float4* __rest
             tile_rect(g.x, g.y, __float_as_int(g.w), tiles_x, tiles_y, tx0, tx1, ty0, ty1);
         }
         uint32_t* cur = cursors + (size_t)tcount_replica((uint32_t)i) * (tiles_x * tiles_y);
-        walk_tile_rects<2>(threadIdx.x & 31, (uint32_t)i, tx0, tx1, ty0, ty1, tiles_x,
+        walk_tile_rects<SCATTER_UNROLL>(threadIdx.x & 31, (uint32_t)i, tx0, tx1, ty0, ty1, tiles_x,
                            [&](const uint32_t* tl, const uint32_t* gl) {
-                               uint32_t slot[2];
+                               uint32_t slot[SCATTER_UNROLL];
 #pragma unroll
-                               for (int u = 0; u < 2; ++u)
+                               for (int u = 0; u < SCATTER_UNROLL; ++u)
                                    slot[u] = tl[u] != 0xFFFFFFFFu ? atomicAdd(&cur[tl[u]], 1u) : capacity;
 #pragma unroll
-                               for (int u = 0; u < 2; ++u)
+                               for (int u = 0; u < SCATTER_UNROLL; ++u)
                                    if (slot[u] < capacity) {
                                        tile_keys[slot[u]] = tl[u];
                                        vals[slot[u]] = gl[u];
