@@ -384,7 +384,9 @@ def run_ours(args):
                              (tp * 16.0 * I + 4.0 * I + 8.0 * n_tiles)),
         "raster_fwd": ("fp32", float(F_fwd)),
         "raster_bwd": ("fp32", float(F_bwd)),
-        "project_bwd": ("hbm", 104.0 * n * nv),
+        # read tiles 4 + gradient row 32 + d_c11 4 + mean 12 + scale 12 + quat 16, write d_mean 12 +
+        # d_scale 12 + d_quat 16 + d_rgbo 16; views after the first also read the running sums (56)
+        "project_bwd": ("hbm", 136.0 * n * nv + 56.0 * n * max(nv - 1, 0)),
     }
     st = {}
     for name, ms in zip(stage_names, stage_ms):

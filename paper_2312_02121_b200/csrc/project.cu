@@ -51,6 +51,11 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
     int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;  // tile rect (MODE 2 walks it)
     if (i < n) {
     const float mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
+    // every input load is issued up front (one memory round trip; the culled
+    // Gaussians' scale / quat / opacity reads are the price)
+    const float sx = scales[3 * i], sy = scales[3 * i + 1], sz = scales[3 * i + 2];
+    const float4 q = quats[i];
+    const float op = opac[i];
     const float* Rc = cam.R;
     const float tx = Rc[0] * mx + Rc[1] * my + Rc[2] * mz + cam.t[0];
     const float ty = Rc[3] * mx + Rc[4] * my + Rc[5] * mz + cam.t[1];
@@ -61,8 +66,6 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
     uint32_t nt = 0;
     const bool depth_culled = (tz <= cam.near_plane) || (tz >= cam.far_plane);
     if (!depth_culled) {
-        const float sx = scales[3 * i], sy = scales[3 * i + 1], sz = scales[3 * i + 2];
-        const float4 q = quats[i];
         const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
         if (sx <= 0.f || sy <= 0.f || sz <= 0.f) {
             report(status, i, GS_ERR_SCALE);
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
                                      (py - fr >= (float)cam.H);
                     o_xydr = make_float4(px, py, tz, __int_as_float(off ? 0 : r));
                     if (!off) {
-                        o_con = conic_of(ca, cb, cc, det, opac[i]);
+                        o_con = conic_of(ca, cb, cc, det, op);
                         tile_rect(px, py, r, cam.tiles_x, cam.tiles_y, tx0, tx1, ty0, ty1);
                         nt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
                     }
@@ -170,27 +173,44 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
     float* __restrict__ d_view16) {
     griddep_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool vis = i < n && tiles[i] != 0u;
+    // every load is issued up front, ahead of the visibility test (one memory
+    // round trip instead of two; culled Gaussians' reads are the price)
+    const bool in = i < n;
+    const uint32_t nt = in ? tiles[i] : 0u;
+    const float4 v_rgbo = in && rgbo_in ? rgbo_in[(size_t)i * gstride] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 gg = in ? d_geo[(size_t)i * gstride] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float g11 = in ? d_c11[i] : 0.f;
+    float mx = 0.f, my = 0.f, mz = 0.f, s[3] = {1.f, 1.f, 1.f};
+    float4 q = make_float4(1.f, 0.f, 0.f, 0.f);
+    if (in) {
+        mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
+        s[0] = scales[3 * i], s[1] = scales[3 * i + 1], s[2] = scales[3 * i + 2];
+        q = quats[i];
+    }
+    float om[3] = {0.f, 0.f, 0.f}, os[3] = {0.f, 0.f, 0.f};  // accumulate: the caller's running sums
+    float4 oq = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (accumulate && in) {
+        om[0] = d_means[3 * i], om[1] = d_means[3 * i + 1], om[2] = d_means[3 * i + 2];
+        os[0] = d_scales[3 * i], os[1] = d_scales[3 * i + 1], os[2] = d_scales[3 * i + 2];
+        oq = d_quats[i];
+    }
+    const bool vis = in && nt != 0u;
     // (accumulating: a culled Gaussian adds exact zeros -- skip its rows)
-    if (rgbo_in && i < n && (vis || !accumulate)) {  // frame path: d_color / d_opacity rows of the interleaved buffer
-        const float4 v = rgbo_in[(size_t)i * gstride];
+    if (rgbo_in && in && (vis || !accumulate)) {  // frame path: d_color / d_opacity rows of the interleaved buffer
         if (accumulate) {
             const float4 o = rgbo_out[i];
-            rgbo_out[i] = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
+            rgbo_out[i] = make_float4(o.x + v_rgbo.x, o.y + v_rgbo.y, o.z + v_rgbo.z, o.w + v_rgbo.w);
         } else {
-            rgbo_out[i] = v;
+            rgbo_out[i] = v_rgbo;
         }
     }
     float dv[12];
 #pragma unroll
     for (int k = 0; k < 12; ++k) dv[k] = 0.f;
-    if (i < n) {
+    if (in) {
         float dmx = 0.f, dmy = 0.f, dmz = 0.f, dsx = 0.f, dsy = 0.f, dsz = 0.f;
         float4 dq = make_float4(0.f, 0.f, 0.f, 0.f);
         if (vis) {
-            const float mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
-            const float s[3] = {scales[3 * i], scales[3 * i + 1], scales[3 * i + 2]};
-            const float4 q = quats[i];
             const float* Rc = cam.R;
             const float tx = Rc[0] * mx + Rc[1] * my + Rc[2] * mz + cam.t[0];
             const float ty = Rc[3] * mx + Rc[4] * my + Rc[5] * mz + cam.t[1];
@@ -220,8 +240,7 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
                 T0[k] = j00 * Rc[k] + j02 * Rc[6 + k];
                 T1[k] = j11 * Rc[3 + k] + j12 * Rc[6 + k];
             }
-            const float4 gg = d_geo[(size_t)i * gstride];
-            const float gx = gg.x, gy = gg.y, g00 = gg.z, g01 = gg.w, g11 = d_c11[i];
+            const float gx = gg.x, gy = gg.y, g00 = gg.z, g01 = gg.w;
             // mean2d_backward (:53-77) == J^T d_mean2d with dt_w = 0
             float dt0 = cam.fx * gx * iz;
             float dt1 = cam.fy * gy * iz;
@@ -301,10 +320,9 @@ __global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
         }
         if (accumulate) {  // sum over views into the caller's gradient (culled: nothing to add)
             if (vis) {
-            d_means[3 * i] += dmx; d_means[3 * i + 1] += dmy; d_means[3 * i + 2] += dmz;
-            d_scales[3 * i] += dsx; d_scales[3 * i + 1] += dsy; d_scales[3 * i + 2] += dsz;
-            const float4 o = d_quats[i];
-            d_quats[i] = make_float4(o.x + dq.x, o.y + dq.y, o.z + dq.z, o.w + dq.w);
+            d_means[3 * i] = om[0] + dmx; d_means[3 * i + 1] = om[1] + dmy; d_means[3 * i + 2] = om[2] + dmz;
+            d_scales[3 * i] = os[0] + dsx; d_scales[3 * i + 1] = os[1] + dsy; d_scales[3 * i + 2] = os[2] + dsz;
+            d_quats[i] = make_float4(oq.x + dq.x, oq.y + dq.y, oq.z + dq.z, oq.w + dq.w);
             }
         } else {
             d_means[3 * i] = dmx; d_means[3 * i + 1] = dmy; d_means[3 * i + 2] = dmz;
