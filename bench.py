@@ -542,11 +542,12 @@ def run_reference(args):
         return
     import numpy as np
 
-    from paper_2312_02121_b200.scenes import make_config
+    from paper_2312_02121_b200.scenes import config_sizes, make_config
 
     spec = make_config(args.config)
     views = views_for(args.config, spec, 1, 0)
     nth = os.cpu_count() or 1
+    sz = config_sizes(args.config)
     # each step: one full fwd+bwd frame (bounded: ~1-3 s per frame at config 1)
     for _ in range(min(args.warmup, 1)):
         cpu_baseline(spec, views, 1, nth)
@@ -559,7 +560,10 @@ def run_reference(args):
     out = {"metric": METRIC, "value": round(fps, 5), "unit": "frames/s", "n_gpus": args.gpus, "steps": steps,
            "warmup": min(args.warmup, 1), "ms_per_step": round(dt / steps * 1e3, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; scenes.py)",
-           "config": {"workload": f"config{args.config}", "gaussians": spec.n},
+           "config": {"workload": f"config{args.config}", "gaussians": spec.n,
+                      "image": f"{sz['width']}x{sz['height']}",
+                      "views_per_step": 1, "early_termination": True, "background": "black",
+                      "parallelism": f"host OpenMP x{nth} (fp64 oracle port)"},
            "impl": "reference",
            "cpu_baseline": {"value": round(fps, 5), "unit": "frames/s", "cores": nth, "kind": "port",
                             "sample": "full fwd+bwd frame per step (oracle/splat_oracle.c, fp64, OpenMP)"},
