@@ -672,7 +672,9 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
 // (rows of 32 lanes, stride 36 words so row reads are conflict-free 128-bit
 // loads); every RBS records the warp sums the 9 * RBS rows -- one row per
 // lane, 8 LDS.128 + adds -- and issues one atomic per row.  About half the
-// instructions of a 9-value shuffle reduction per record.
+// instructions of a 9-value shuffle reduction per record.  A slot's splat
+// id rides in the padding word of its first row, so a batch may span
+// staging chunks.
 constexpr int RBS = 3;        // records per reduction batch (9 * RBS <= 32 rows: one row per lane)
 constexpr int RROW = 36;      // row stride (words): 32 lanes + pad
 
@@ -690,12 +692,12 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
 }
 
 // Sum the batch's 9 * nslot rows (one per lane) and add each to its
-// splat's gradient slot.  red: this warp's batch (32-bit shared address),
-// kslots: the batch's staged-record indices (8 bits each), stage: this
-// warp's staged records.  The conic rows (6..8) were accumulated without
-// their factor 1/2, applied here (exact).
-__device__ __forceinline__ void bwd_flush(uint32_t red, uint32_t kslots, uint32_t stage, int nslot, int lane,
-                                          float* __restrict__ g8, float* __restrict__ d_c11) {
+// splat's gradient slot.  red: this warp's batch (32-bit shared address);
+// each slot's splat id sits in the padding word (lane 32) of its first row.
+// The conic rows (6..8) were accumulated without their factor 1/2, applied
+// here (exact).
+__device__ __forceinline__ void bwd_flush(uint32_t red, int nslot, int lane, float* __restrict__ g8,
+                                          float* __restrict__ d_c11) {
     if (lane < 9 * nslot) {
         const int k = lane / 9, t = lane - 9 * k;
         const uint32_t row = red + (uint32_t)lane * (RROW * 4);
@@ -710,7 +712,7 @@ __device__ __forceinline__ void bwd_flush(uint32_t red, uint32_t kslots, uint32_
         const f32x2 s2 = add2(s01, s23);
         float sum = lo2(s2) + hi2(s2);
         if (t >= 6) sum *= 0.5f;
-        const uint32_t id = lds_u32(stage + ((kslots >> (8 * k)) & 255u) * REC_BYTES + 40u);
+        const uint32_t id = lds_u32(red + (uint32_t)k * (9 * RROW * 4) + 32 * 4);
         atomicAdd(t < 8 ? g8 + 8 * (size_t)id + t : d_c11 + id, sum);
     }
 }
@@ -752,7 +754,6 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
     const uint32_t red_w = smem_addr(&s_red[warp][0][0][0]);
     const uint32_t stage_w = smem_addr(&s_rec[warp][0]);
     int nslot = 0;
-    uint32_t kslots = 0;
     for (int hi = count; hi > 0; hi -= 32) {
         const int lo = hi > 32 ? hi - 32 : 0;
         const int nb = hi - lo;
@@ -812,26 +813,23 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             const uint32_t slot = red_w + (uint32_t)nslot * (9 * RROW * 4) + 4 * lane;
 #pragma unroll
             for (int u = 0; u < 9; ++u) sts_f32(slot + u * (RROW * 4), lo2(D[u]) + hi2(D[u]));
-            kslots |= (uint32_t)k << (8 * nslot);
+            if (lane == 0) sts_u32(slot + 32 * 4, __float_as_uint(cq.z));  // splat id -> row padding
             S0 = fma2(WC, bc2(bq.z), S0);
             S1 = fma2(WC, bc2(bq.w), S1);
             S2 = fma2(WC, bc2(blue), S2);
             T = sel2(c0, c1, TH, T);
             if (++nslot == RBS) {
                 __syncwarp();
-                bwd_flush(red_w, kslots, stage_w, RBS, lane, g8, d_c11);
+                bwd_flush(red_w, RBS, lane, g8, d_c11);
                 __syncwarp();
                 nslot = 0;
-                kslots = 0;
             }
         }
-        if (nslot) {  // the batch refers to this staging chunk's ids: flush before restaging
-            __syncwarp();
-            bwd_flush(red_w, kslots, stage_w, nslot, lane, g8, d_c11);
-            nslot = 0;
-            kslots = 0;
-        }
+        __syncwarp();  // the next chunk restages s_rec (the batch keeps its own ids)
+    }
+    if (nslot) {
         __syncwarp();
+        bwd_flush(red_w, nslot, lane, g8, d_c11);
     }
 }
 
