@@ -38,10 +38,12 @@ constexpr int RB = 128;  // splats per staged batch
 // NWR = 2 -> two 8-column x 16-row halves (two pixel pairs per lane).
 template <int NWR>
 struct BatchT {
-    float4 a[RB + 1];  // x, y, hA = A/2, B   ([RB] = sentinel: x = +inf, never visible)
-    float4 b[RB + 1];  // hC = C/2, opacity, r, g
-    float c[RB + 1];   // blue
-    uint32_t id[RB];
+    // per staged entry, one 48-byte record (one base address for all of its
+    // loads): a = (x, y, hA = A/2, B), b = (hC = C/2, opacity, r, g),
+    // c = (blue, splat id bits, -, -); [RB] = sentinel: x = +inf, never visible
+    struct Ent {
+        float4 a, b, c;
+    } e[RB + 1];
     uint32_t mask[NWR][RB / 32];  // region reach bits per group of 32 entries
     __align__(4) uint8_t list[NWR][RB + 2];  // compacted entry indices per region (+ sentinel pad)
     uint8_t rbuf[NWR][RB];                   // forward records of this batch (entry indices, per region)
@@ -86,10 +88,9 @@ __device__ __forceinline__ int stage_batch(BatchT<NWR>& s, int tile, int tiles_x
             const uint32_t id = ids[first + k];
             const float4 g = xydr[id];
             const float4 q = conic[id];
-            s.a[k] = make_float4(g.x, g.y, 0.5f * q.x, q.y);
-            s.b[k] = make_float4(0.5f * q.z, q.w, colors[3 * id], colors[3 * id + 1]);
-            s.c[k] = colors[3 * id + 2];
-            s.id[k] = id;
+            s.e[k].a = make_float4(g.x, g.y, 0.5f * q.x, q.y);
+            s.e[k].b = make_float4(0.5f * q.z, q.w, colors[3 * id], colors[3 * id + 1]);
+            s.e[k].c = make_float4(colors[3 * id + 2], __uint_as_float(id), 0.f, 0.f);
             x = g.x;
             // Exact reach of the sigma <= 4.5 ellipse {d : d^T Q d <= 9} of
             // the conic Q = [A B; B C] in each band dy in [lo, hi]: x extends
@@ -223,7 +224,7 @@ __device__ __forceinline__ void fwd_record_flush(const BatchT<NWR>& s, int warp,
     __syncwarp();
     for (int j = lane; j < nrec; j += 32) {
         const int k = s.rbuf[warp][j];
-        rp[j] = make_uint2(s.id[k], (uint32_t)(pos0 + k));
+        rp[j] = make_uint2(__float_as_uint(s.e[k].c.y), (uint32_t)(pos0 + k));
     }
     rp += nrec;
     nrec = 0;
@@ -283,9 +284,9 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
     uint2* rp = REC ? rec + 4 * (int64_t)start + (int64_t)warp * (end - start) : nullptr;
     int nrec = 0;
     if (threadIdx.x == 0) {  // sentinel entry: dx = -inf -> sigma NaN -> never visible
-        s.a[RB] = make_float4(INF, 0.f, 0.f, 0.f);
-        s.b[RB] = make_float4(0.f, 0.f, 0.f, 0.f);
-        s.c[RB] = 0.f;
+        s.e[RB].a = make_float4(INF, 0.f, 0.f, 0.f);
+        s.e[RB].b = make_float4(0.f, 0.f, 0.f, 0.f);
+        s.e[RB].c = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
     for (int b0 = start; b0 < end; b0 += RB) {
@@ -299,8 +300,8 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
             for (int i = 0; i < n; i += 2) {
                 const uint32_t kk = lst2[i >> 1];
                 const int k0 = kk & 0xffu, k1 = kk >> 8;  // k1 may be the sentinel
-                const float4 a0 = s.a[k0], a1 = s.a[k1];
-                const float hC0 = s.b[k0].x, hC1 = s.b[k1].x;
+                const float4 a0 = s.e[k0].a, a1 = s.e[k1].a;
+                const float hC0 = s.e[k0].b.x, hC1 = s.e[k1].b.x;
                 const float dx0 = __fsub_rn(px, a0.x), dx1 = __fsub_rn(px, a1.x);
                 const f32x2 SG0 = splat_sigma2(dx0, __fmul_rn(a0.z, dx0), sub2(p[0].PY, bc2(a0.y)), a0.w, hC0);
                 const f32x2 SG1 = splat_sigma2(dx1, __fmul_rn(a1.z, dx1), sub2(p[0].PY, bc2(a1.y)), a1.w, hC1);
@@ -310,14 +311,14 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
                 const uint32_t b1m = __ballot_sync(0xffffffffu, v10 || v11);
                 if (COUNT) e_s += (unsigned)v00 + (unsigned)v01;
                 if (b0m) {
-                    fwd_commit<ET, COUNT>(p[0], SG0, v00, v01, s.b[k0], s.c[k0], pos_base + k0, e_a, e_c);
+                    fwd_commit<ET, COUNT>(p[0], SG0, v00, v01, s.e[k0].b, s.e[k0].c.x, pos_base + k0, e_a, e_c);
                     if (REC) fwd_record(s, warp, lane, nrec, k0);
                 }
                 v10 = v10 && !(p[0].done & 1u);  // retired at k0
                 v11 = v11 && !(p[0].done & 2u);
                 if (COUNT) e_s += (unsigned)v10 + (unsigned)v11;
                 if (b1m) {  // never the sentinel (its sigma is NaN)
-                    fwd_commit<ET, COUNT>(p[0], SG1, v10, v11, s.b[k1], s.c[k1], pos_base + k1, e_a, e_c);
+                    fwd_commit<ET, COUNT>(p[0], SG1, v10, v11, s.e[k1].b, s.e[k1].c.x, pos_base + k1, e_a, e_c);
                     if (REC) fwd_record(s, warp, lane, nrec, k1);
                 }
                 if (ET && (b0m | b1m) && __all_sync(0xffffffffu, p[0].done == 3u)) break;
@@ -328,8 +329,8 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
 #pragma unroll 1
             for (int i = 0; i < n; ++i) {
                 const int k = lst[i];
-                const float4 a = s.a[k];
-                const float hC = s.b[k].x;
+                const float4 a = s.e[k].a;
+                const float hC = s.e[k].b.x;
                 const float dx = __fsub_rn(px, a.x);
                 const float hAdx = __fmul_rn(a.z, dx);
                 f32x2 SG[NPR];
@@ -347,8 +348,8 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
                     for (int q = 0; q < 2 * NPR; ++q) e_s += (unsigned)v[q];
                 }
                 if (!__any_sync(0xffffffffu, any)) continue;
-                const float4 bq = s.b[k];
-                const float blue = s.c[k];
+                const float4 bq = s.e[k].b;
+                const float blue = s.e[k].c.x;
 #pragma unroll
                 for (int j = 0; j < NPR; ++j)
                     if (__any_sync(0xffffffffu, v[2 * j] || v[2 * j + 1]))
@@ -451,8 +452,8 @@ struct BwdEvalT {
 template <int NPR, int NWR>
 __device__ __forceinline__ void bwd_eval(const BatchT<NWR>& s, int k, int pos, float px, const f32x2 (&PY)[NPR],
                                          const int (&nc)[2 * NPR], BwdEvalT<NPR>& e) {
-    const float4 a = s.a[k];
-    const float hC = s.b[k].x;
+    const float4 a = s.e[k].a;
+    const float hC = s.e[k].b.x;
     e.dx = __fsub_rn(px, a.x);
     const float hAdx = __fmul_rn(a.z, e.dx);
     e.any = false;
@@ -476,9 +477,9 @@ __device__ __forceinline__ void bwd_commit(const BatchT<NWR>& s, int k, const Bw
                                            f32x2 (&S0)[NPR], f32x2 (&S1)[NPR], f32x2 (&S2)[NPR],
                                            float4* __restrict__ d_rgbo, float4* __restrict__ d_geo,
                                            float* __restrict__ d_c11, int gstride, unsigned long long& e_c) {
-    const float4 a = s.a[k];
-    const float4 bq = s.b[k];
-    const float blue = s.c[k];
+    const float4 a = s.e[k].a;
+    const float4 bq = s.e[k].b;
+    const float blue = s.e[k].c.x;
     const float hC = bq.x;
     const float dx = e.dx;
     float acc[9];
@@ -527,7 +528,7 @@ __device__ __forceinline__ void bwd_commit(const BatchT<NWR>& s, int k, const Bw
     }
     const uint32_t cmask = __ballot_sync(0xffffffffu, anyc);
     if (!cmask) return;
-    const uint32_t id = s.id[k];
+    const uint32_t id = __float_as_uint(s.e[k].c.y);
     if (__popc(cmask) <= 3) {
         // few contributing lanes: their own vector reductions are cheaper
         // than a 9-value warp reduction
@@ -611,9 +612,9 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
     for (int w = 0; w < NWR; ++w) max_nc = max(max_nc, s_max[w]);
     unsigned long long e_s = 0, e_c = 0;
     if (threadIdx.x == 0) {  // sentinel entry: dx = -inf -> sigma NaN -> never visible
-        s.a[RB] = make_float4(__int_as_float(0x7f800000), 0.f, 0.f, 0.f);
-        s.b[RB] = make_float4(0.f, 0.f, 0.f, 0.f);
-        s.c[RB] = 0.f;
+        s.e[RB].a = make_float4(__int_as_float(0x7f800000), 0.f, 0.f, 0.f);
+        s.e[RB].b = make_float4(0.f, 0.f, 0.f, 0.f);
+        s.e[RB].c = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
     for (int bend = max_nc; bend > 0; bend -= RB) {
