@@ -10,6 +10,8 @@ import ctypes as C
 import os
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsplat_b200.so")
+# A/B builds of one kernel variant (tools/build_variant.py) load through this
+LIB_PATH = os.environ.get("GS_LIB_PATH") or LIB_PATH
 
 # Every symbol include/splat_b200.h declares (tests check the export table).
 EXPORTS = (

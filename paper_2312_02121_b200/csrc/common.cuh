@@ -69,18 +69,18 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 }
 
 // sigma = 0.5*(A dx^2 + C dy^2) + B dx dy   (sg/raster_forward.py:132-135)
-// evaluated as dx*(hA*dx + B*dy) + (hC*dy)*dy with hA = A/2, hC = C/2
-// (exact halvings), every op rounded explicitly.
+// evaluated as (hC*dy + B*dx)*dy + (hA*dx)*dx with hA = A/2, hC = C/2
+// (exact halvings), every op rounded explicitly.  The packed form computes
+// (hA*dx, B*dx) with one FMUL2 from the staged (hA, B) pair.
 __device__ __forceinline__ float splat_sigma(float dx, float dy, float hA, float B, float hC) {
-    const float t = __fmaf_rn(B, dy, __fmul_rn(hA, dx));
-    const float u = __fmul_rn(hC, dy);
-    return __fmaf_rn(dx, t, __fmul_rn(u, dy));
+    const float t = __fmaf_rn(hC, dy, __fmul_rn(dx, B));
+    return __fmaf_rn(t, dy, __fmul_rn(__fmul_rn(dx, hA), dx));
 }
 
 // Same expression with hA*dx hoisted (pixels sharing a column share dx):
-// bit-identical to splat_sigma(dx, dy, hA, B, hC) when hAdx == hA*dx.
+// bit-identical to splat_sigma(dx, dy, hA, B, hC) when hAdx == dx*hA.
 __device__ __forceinline__ float splat_sigma_h(float dx, float hAdx, float dy, float B, float hC) {
-    return __fmaf_rn(dx, __fmaf_rn(B, dy, hAdx), __fmul_rn(__fmul_rn(hC, dy), dy));
+    return __fmaf_rn(__fmaf_rn(hC, dy, __fmul_rn(dx, B)), dy, __fmul_rn(hAdx, dx));
 }
 
 // ---- packed fp32 pairs (sm_100a FFMA2/FMUL2/FADD2) ----------------------
@@ -140,11 +140,16 @@ __device__ __forceinline__ f32x2 pin2(f32x2 x) {
     return x;
 }
 
-// sigma for the pixel pair dy = (dy_lo, dy_hi) sharing dx (and hA*dx).
-__device__ __forceinline__ f32x2 splat_sigma2(float dx, float hAdx, f32x2 dy, float B, float hC) {
-    const f32x2 t = fma2(pk2(B, B), dy, pk2(hAdx, hAdx));
-    const f32x2 u = mul2(mul2(pk2(hC, hC), dy), dy);
-    return fma2(pk2(dx, dx), t, u);
+// (hA*dx, B*dx) for a column: one FMUL2 from the staged (hA, B) pair.
+__device__ __forceinline__ f32x2 sigma_base(float dx, float hA, float B) { return mul2(pk2(dx, dx), pk2(hA, B)); }
+
+// sigma for the pixel pair dy = (dy_lo, dy_hi) sharing dx, from
+// base = sigma_base(dx, hA, B): per lane bit-identical to splat_sigma.
+__device__ __forceinline__ f32x2 splat_sigma2(float dx, f32x2 base, f32x2 dy, float hC, f32x2* t_out = nullptr) {
+    const f32x2 t = fma2(pk2(hC, hC), dy, pk2(hi2(base), hi2(base)));
+    if (t_out) *t_out = t;
+    const float c0 = __fmul_rn(lo2(base), dx);
+    return fma2(t, dy, pk2(c0, c0));
 }
 
 // det of the 2d covariance and its inverse terms (A, B, C)

@@ -213,21 +213,23 @@ __device__ __forceinline__ void fwd_commit(FwdPair& p, f32x2 SG, bool vis0, bool
 // extra vote.  The backward replays exactly these entries, back to front.
 // Per entry one byte goes to the warp's shared buffer; the batch's records
 // are written out coalesced when the warp leaves the batch.
-template <int NWR>
-__device__ __forceinline__ void fwd_record(BatchT<NWR>& s, int warp, int lane, int& nrec, int k) {
-    if (lane == 0) s.rbuf[warp][nrec] = (uint8_t)k;
-    ++nrec;
+// rcur: the warp's shared cursor (32-bit shared address of its next byte in
+// rbuf), so a record costs one predicated STS.U8 and one add.
+__device__ __forceinline__ void fwd_record(uint32_t& rcur, int lane, int k) {
+    if (lane == 0) asm volatile("st.shared.u8 [%0], %1;" ::"r"(rcur), "r"(k) : "memory");
+    ++rcur;
 }
 template <int NWR>
-__device__ __forceinline__ void fwd_record_flush(const BatchT<NWR>& s, int warp, int lane, int& nrec, uint2*& rp,
-                                                 int pos0) {
+__device__ __forceinline__ void fwd_record_flush(const BatchT<NWR>& s, int warp, int lane, uint32_t& rcur,
+                                                 uint32_t rbase_w, uint2*& rp, int pos0) {
     __syncwarp();
+    const int nrec = (int)(rcur - rbase_w);
     for (int j = lane; j < nrec; j += 32) {
         const int k = s.rbuf[warp][j];
         rp[j] = make_uint2(__float_as_uint(s.e[k].c.y), (uint32_t)(pos0 + k));
     }
     rp += nrec;
-    nrec = 0;
+    rcur = rbase_w;
 }
 
 // sg/raster_forward.py:116-154 _composite_tile for one tile.
@@ -282,7 +284,8 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
     unsigned long long e_s = 0, e_a = 0, e_c = 0;
     // this warp's record region: 4 * start + warp * len (no atomics)
     uint2* rp = REC ? rec + 4 * (int64_t)start + (int64_t)warp * (end - start) : nullptr;
-    int nrec = 0;
+    const uint32_t rbuf_w = smem_addr(&s.rbuf[warp][0]);
+    uint32_t rcur = rbuf_w;
     if (threadIdx.x == 0) {  // sentinel entry: dx = -inf -> sigma NaN -> never visible
         s.e[RB].a = make_float4(INF, 0.f, 0.f, 0.f);
         s.e[RB].b = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -303,8 +306,8 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
                 const float4 a0 = s.e[k0].a, a1 = s.e[k1].a;
                 const float hC0 = s.e[k0].b.x, hC1 = s.e[k1].b.x;
                 const float dx0 = __fsub_rn(px, a0.x), dx1 = __fsub_rn(px, a1.x);
-                const f32x2 SG0 = splat_sigma2(dx0, __fmul_rn(a0.z, dx0), sub2(p[0].PY, bc2(a0.y)), a0.w, hC0);
-                const f32x2 SG1 = splat_sigma2(dx1, __fmul_rn(a1.z, dx1), sub2(p[0].PY, bc2(a1.y)), a1.w, hC1);
+                const f32x2 SG0 = splat_sigma2(dx0, sigma_base(dx0, a0.z, a0.w), sub2(p[0].PY, bc2(a0.y)), hC0);
+                const f32x2 SG1 = splat_sigma2(dx1, sigma_base(dx1, a1.z, a1.w), sub2(p[0].PY, bc2(a1.y)), hC1);
                 const bool v00 = lo2(SG0) <= SIGMA_CUT, v01 = hi2(SG0) <= SIGMA_CUT;  // false when retired
                 bool v10 = lo2(SG1) <= SIGMA_CUT, v11 = hi2(SG1) <= SIGMA_CUT;
                 const uint32_t b0m = __ballot_sync(0xffffffffu, v00 || v01);
@@ -312,18 +315,18 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
                 if (COUNT) e_s += (unsigned)v00 + (unsigned)v01;
                 if (b0m) {
                     fwd_commit<ET, COUNT>(p[0], SG0, v00, v01, s.e[k0].b, s.e[k0].c.x, pos_base + k0, e_a, e_c);
-                    if (REC) fwd_record(s, warp, lane, nrec, k0);
+                    if (REC) fwd_record(rcur, lane, k0);
                 }
                 v10 = v10 && !(p[0].done & 1u);  // retired at k0
                 v11 = v11 && !(p[0].done & 2u);
                 if (COUNT) e_s += (unsigned)v10 + (unsigned)v11;
                 if (b1m) {  // never the sentinel (its sigma is NaN)
                     fwd_commit<ET, COUNT>(p[0], SG1, v10, v11, s.e[k1].b, s.e[k1].c.x, pos_base + k1, e_a, e_c);
-                    if (REC) fwd_record(s, warp, lane, nrec, k1);
+                    if (REC) fwd_record(rcur, lane, k1);
                 }
                 if (ET && (b0m | b1m) && __all_sync(0xffffffffu, p[0].done == 3u)) break;
             }
-            if (REC) fwd_record_flush(s, warp, lane, nrec, rp, pos_base - 1);
+            if (REC) fwd_record_flush(s, warp, lane, rcur, rbuf_w, rp, pos_base - 1);
         } else {
             const uint8_t* lst = s.list[warp];
 #pragma unroll 1
@@ -332,13 +335,13 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
                 const float4 a = s.e[k].a;
                 const float hC = s.e[k].b.x;
                 const float dx = __fsub_rn(px, a.x);
-                const float hAdx = __fmul_rn(a.z, dx);
+                const f32x2 base = sigma_base(dx, a.z, a.w);
                 f32x2 SG[NPR];
                 bool v[2 * NPR];
                 bool any = false;
 #pragma unroll
                 for (int j = 0; j < NPR; ++j) {
-                    SG[j] = splat_sigma2(dx, hAdx, sub2(p[j].PY, bc2(a.y)), a.w, hC);
+                    SG[j] = splat_sigma2(dx, base, sub2(p[j].PY, bc2(a.y)), hC);
                     v[2 * j] = lo2(SG[j]) <= SIGMA_CUT;
                     v[2 * j + 1] = hi2(SG[j]) <= SIGMA_CUT;
                     any = any || v[2 * j] || v[2 * j + 1];
@@ -455,13 +458,13 @@ __device__ __forceinline__ void bwd_eval(const BatchT<NWR>& s, int k, int pos, f
     const float4 a = s.e[k].a;
     const float hC = s.e[k].b.x;
     e.dx = __fsub_rn(px, a.x);
-    const float hAdx = __fmul_rn(a.z, e.dx);
+    const f32x2 base = sigma_base(e.dx, a.z, a.w);
     e.any = false;
     e.n_vis = 0;
 #pragma unroll
     for (int j = 0; j < NPR; ++j) {
         e.DY[j] = sub2(PY[j], bc2(a.y));
-        e.SG[j] = splat_sigma2(e.dx, hAdx, e.DY[j], a.w, hC);
+        e.SG[j] = splat_sigma2(e.dx, base, e.DY[j], hC);
         e.v[2 * j] = pos < nc[2 * j] && lo2(e.SG[j]) <= SIGMA_CUT;
         e.v[2 * j + 1] = pos < nc[2 * j + 1] && hi2(e.SG[j]) <= SIGMA_CUT;
         e.any = e.any || e.v[2 * j] || e.v[2 * j + 1];
@@ -679,7 +682,7 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
 constexpr int RBS = 3;        // records per reduction batch (9 * RBS <= 32 rows: one row per lane)
 constexpr int RROW = 36;      // row stride (words): 32 lanes + pad
 
-// A staged record: the splat's (x, y, A/2, B), (C/2, opacity, r, g) and
+// A staged record: the splat's (x, y, A/2, B), (C/2, opacity, r, g),
 // (b, list position, splat id, -) -- one base address, three LDS.128.
 struct __align__(16) RecStage {
     float4 a, b, c;
@@ -778,13 +781,10 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             const float blue = cq.x;
             const float hC = bq.x;
             const float dx = __fsub_rn(px, a.x);
-            const float hAdx = __fmul_rn(a.z, dx);
+            const f32x2 base = sigma_base(dx, a.z, a.w);  // (A/2 dx, B dx)
             const f32x2 DY = sub2(PY, bc2(a.y));
-            // splat_sigma2 with its intermediates kept: P = A/2 dx + B dy,
-            // QC = C/2 dy; sigma = dx P + QC dy (same ops, same bits)
-            const f32x2 P = fma2(bc2(a.w), DY, bc2(hAdx));
-            const f32x2 QC = mul2(bc2(hC), DY);
-            const f32x2 SG = fma2(bc2(dx), P, mul2(QC, DY));
+            f32x2 T1;  // C/2 dy + B dx
+            const f32x2 SG = splat_sigma2(dx, base, DY, hC, &T1);
             const f32x2 SL = mul2(SG, bc2(NEG_LOG2E));
             const f32x2 E = pk2(ex2_approx(lo2(SL)), ex2_approx(hi2(SL)));
             const f32x2 ARAW = mul2(bc2(bq.y), E);
@@ -805,8 +805,8 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             const bool l0 = c0 && lo2(ARAW) < ALPHA_MAX, l1 = c1 && hi2(ARAW) < ALPHA_MAX;
             const f32x2 DAL = pk2(l0 ? lo2(DA) : 0.f, l1 ? hi2(DA) : 0.f);
             const f32x2 M = mul2(ARAW, DAL);
-            const f32x2 Y0 = add2(P, bc2(hAdx));                      // A dx + B dy
-            const f32x2 Y1 = fma2(bc2(2.f), QC, bc2(__fmul_rn(a.w, dx)));  // B dx + C dy
+            const f32x2 Y0 = fma2(bc2(a.w), DY, bc2(lo2(base) + lo2(base)));  // A dx + B dy
+            const f32x2 Y1 = fma2(bc2(hC), DY, T1);                           // B dx + C dy
             const f32x2 MY0 = mul2(M, Y0), MY1 = mul2(M, Y1);
             // rows 6..8 are M Y Y without the 1/2 of d sigma / d conic (bwd_flush applies it)
             const f32x2 D[9] = {mul2(WC, G0), mul2(WC, G1), mul2(WC, G2), mul2(DAL, E), MY0,
