@@ -66,9 +66,16 @@ def tile_order_launches(cam):
 
 
 def scatter_binning(n):
-    """Which frame binning the library uses (csrc/frame.cu, gs_set_option)."""
-    mode = int(os.environ.get("GS_BINNING", "0"))
+    """Which frame binning the library uses (csrc/frame.cu, gs_get_option)."""
+    from paper_2312_02121_b200 import ops
+    mode = ops.get_option("binning")
     return mode == 2 or (mode == 0 and n <= 400000)
+
+
+def fused_sort(n):
+    """Scatter binning with its per-tile sort fused into the raster forward."""
+    from paper_2312_02121_b200 import ops
+    return scatter_binning(n) and ops.get_option("fuse_sort") == 1
 
 
 def views_for(cfg, spec, world, rank):
@@ -379,8 +386,9 @@ def run_ours(args):
         "scan_emit": ("hbm", (40.0 * n_tiles + 20.0 * n * nv + 8.0 * I) if seg else
                       (8.0 * n * nv + 16.0 * n * nv + 8.0 * I)),
         # depth-first: tile passes (key+value, read+write) + ranges; scatter: per-tile sort
-        # (value in, key gather, value out) + ranges
-        "tile_sort_ranges": ("hbm", (12.0 * I + 8.0 * n_tiles) if seg else
+        # (value in, key gather, value out) + ranges -- fused into the raster forward by default
+        "tile_sort_ranges": ("none", 0.0) if fused_sort(n) else
+                            ("hbm", (12.0 * I + 8.0 * n_tiles) if seg else
                              (tp * 16.0 * I + 4.0 * I + 8.0 * n_tiles)),
         "raster_fwd": ("fp32", float(F_fwd)),
         "raster_bwd": ("fp32", float(F_bwd)),
@@ -400,6 +408,8 @@ def run_ours(args):
         else:
             d["achieved_tops"] = round(w / (ms / 1e3) / 1e12, 3) if ms > 0 else None
             d["frac"] = round(w / (ms / 1e3) / fp32_peak, 4) if ms > 0 else None
+        if name == "raster_fwd" and fused_sort(n):
+            d["includes"] = "per-tile (depth, index) sort of the tile's list (fuse_sort)"
         st[name] = d
     dom = max(stage_names, key=lambda k: stage_ms[stage_names.index(k)])
     if dom == "raster_bwd" and timed_bwd_ms > 0:
@@ -444,11 +454,12 @@ def run_ours(args):
         "intersections_per_step_rank": int(I),
         "e2e": e2e,
         # per view (csrc/frame.cu): scatter binning: init, project (+ tile counts), tile scan
-        # (+ raster order), pair scatter, per-tile sort, raster fwd | raster bwd, project bwd
+        # (+ raster order), pair scatter, [per-tile sort,] raster fwd (+ the per-tile sort when
+        # fused) | raster bwd, project bwd
         # (its last block reduces d_view); depth-first: init, project, 4 depth passes, fused
         # scan+emit, tp tile passes, ranges, (tile order for grids over one raster wave), raster fwd |
         # raster bwd, project bwd
-        "gpu_launches": int(args.steps * len(cams) * (8 if scatter_binning(n) else
+        "gpu_launches": int(args.steps * len(cams) * ((7 if fused_sort(n) else 8) if scatter_binning(n) else
                                                       11 + tp + tile_order_launches(cams[0]))),
         "roofline": roof,
         "stages": st,

@@ -63,8 +63,13 @@ int gs_version(void);
  * in depth order), 2 = scatter (per-tile counts from the projection, pairs
  * written into their tile ranges through atomic cursors, each range sorted
  * by (depth, index)).  Both give sg/binning.py:50-65's (depth,
- * source_index) lists bit for bit. */
+ * source_index) lists bit for bit.  "fuse_sort" (scatter binning): 1
+ * (default) sorts each tile's range at the top of the raster forward CTA
+ * that composites it, 0 in a separate per-tile sort kernel; same lists. */
 int gs_set_option(const char* name, int value);
+/* Current value of an option of gs_set_option (-1 and gs_last_error for an
+ * unknown name). */
+int gs_get_option(const char* name);
 /* Number of SMs of the current device (0 when no device). */
 int gs_device_sm_count(void);
 

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("GS_LIB_PATH") or LIB_PATH
 
 # Every symbol include/splat_b200.h declares (tests check the export table).
 EXPORTS = (
-    "gs_last_error", "gs_version", "gs_device_sm_count", "gs_set_option",
+    "gs_last_error", "gs_version", "gs_device_sm_count", "gs_set_option", "gs_get_option",
     "gs_project_fwd",
     "gs_scan_workspace_bytes", "gs_scan_tiles", "gs_emit_keys",
     "gs_sort_workspace_bytes", "gs_sort_pairs", "gs_tile_counts", "gs_tile_ranges",
@@ -112,6 +112,7 @@ def load():
     sig.update({
         "gs_project64": ([P, P, P, i64, cam64, P, P, P, P, P, P, P, P], C.c_int),
         "gs_set_option": ([C.c_char_p, C.c_int], C.c_int),
+        "gs_get_option": ([C.c_char_p], C.c_int),
         "gs_bin64_workspace_bytes": ([i64, i64, C.c_int32], C.c_size_t),
         "gs_bin64_count": ([P, i64, P, C.c_size_t, P, P], C.c_int),
         "gs_bin64_sort": ([P, P, P, P, i64, i64, C.c_int32, C.c_int32, P, C.c_size_t, P,

@@ -37,6 +37,16 @@ int binning_mode() {
     return g_binning;
 }
 
+static int g_fuse_sort = -1;  // -1: not set (env GS_FUSE_SORT, else on)
+
+bool fuse_sort() {
+    if (g_fuse_sort < 0) {
+        const char* e = getenv("GS_FUSE_SORT");
+        g_fuse_sort = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_fuse_sort == 1;
+}
+
 int check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error("%s: %s", what, cudaGetErrorString(e));
@@ -58,7 +68,19 @@ int gs_set_option(const char* name, int value) {
         gs::g_binning = value;
         return 0;
     }
+    if (strcmp(name, "fuse_sort") == 0) {
+        if (value < 0 || value > 1) return gs::set_error("gs_set_option: fuse_sort must be 0 or 1");
+        gs::g_fuse_sort = value;
+        return 0;
+    }
     return gs::set_error("gs_set_option: unknown option %s", name);
+}
+
+int gs_get_option(const char* name) {
+    if (!name) return gs::set_error("gs_get_option: null name");
+    if (strcmp(name, "binning") == 0) return gs::binning_mode();
+    if (strcmp(name, "fuse_sort") == 0) return gs::fuse_sort() ? 1 : 0;
+    return gs::set_error("gs_get_option: unknown option %s", name);
 }
 
 int gs_device_sm_count(void) {

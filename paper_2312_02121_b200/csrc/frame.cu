@@ -217,14 +217,17 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
                                  isect_capacity, tcount, at<uint32_t>(ws, L.tkeys), at<uint32_t>(ws, L.tvals), s))
             return -1;
         mark(stage_events, 3, s);
-        if (launch_segsort(at<uint2>(ws, L.ranges), n_tiles, at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.tvals),
-                           at<uint32_t>(ws, L.tvals_alt), s))
+        // per-tile sort at the top of the raster forward (the counted pass keeps the separate kernel)
+        const bool fused = fuse_sort() && counts4 == nullptr;
+        if (!fused && launch_segsort(at<uint2>(ws, L.ranges), n_tiles, at<uint32_t>(ws, L.dkeys),
+                                     at<uint32_t>(ws, L.tvals), at<uint32_t>(ws, L.tvals_alt), s))
             return -1;
         mark(stage_events, 4, s);
         if (launch_raster_fwd(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.tvals), at<float>(ws, L.xydr),
                               at<float>(ws, L.conic), colors3, bg, W, H, early_termination != 0, out_image,
                               out_final_T, out_n_contrib, counts4, s, at<uint2>(ws, L.rec),
-                              at<uint32_t>(ws, L.rec_count), t_order))
+                              at<uint32_t>(ws, L.rec_count), t_order, fused ? at<uint32_t>(ws, L.dkeys) : nullptr,
+                              fused ? at<uint32_t>(ws, L.tvals_alt) : nullptr))
             return -1;
         mark(stage_events, 5, s);
         return 0;

@@ -67,12 +67,15 @@ int launch_segsort(const uint2* ranges, int n_tiles, const uint32_t* dkeys, uint
                    cudaStream_t s);
 // binning strategy of the frame path (abi.cu): 0 auto, 1 depth-first, 2 scatter
 int binning_mode();
+// frame path with scatter binning: tile sort fused into the raster forward (1) or its own kernel (0)
+bool fuse_sort();
 
 // raster.cu
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
                       unsigned long long* counts, cudaStream_t s, uint2* rec = nullptr,
-                      uint32_t* rec_count = nullptr, const uint32_t* tile_order = nullptr);
+                      uint32_t* rec_count = nullptr, const uint32_t* tile_order = nullptr,
+                      const uint32_t* dkeys = nullptr, uint32_t* sort_alt = nullptr);  // dkeys: fused tile sort
 // record-driven backward of the frame path (records written by the forward)
 int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,

@@ -27,10 +27,10 @@
 
 #include "common.cuh"
 #include "internal.cuh"
+#include "segsort.cuh"
 
 namespace gs {
 
-constexpr int NT = 128;  // threads per CTA (forward)
 constexpr int NW = 4;    // warps (quadrants, forward)
 constexpr int RB = 128;  // splats per staged batch
 
@@ -68,7 +68,7 @@ struct Quad {
 // Stage `count` entries starting at ids[first] and build the warp-region
 // lists.  Returns this warp's list length.  Ends with the CTA synchronized.
 template <int NWR>
-__device__ __forceinline__ int stage_batch(BatchT<NWR>& s, int tile, int tiles_x, const uint32_t* __restrict__ ids,
+__device__ __forceinline__ int stage_batch(BatchT<NWR>& s, int tile, int tiles_x, const uint32_t* ids,
                                            int first, int count, const float4* __restrict__ xydr,
                                            const float4* __restrict__ conic, const float* __restrict__ colors) {
     constexpr int NTR = 32 * NWR;
@@ -236,9 +236,34 @@ __device__ __forceinline__ void fwd_record_flush(const BatchT<NWR>& s, int warp,
 // NWR = 4: 128 threads, one pixel pair per lane, two list entries per
 // iteration (independent sigma chains); NWR = 2: 64 threads, two pixel pairs
 // per lane (8x16 halves), one entry per iteration.
-template <int NWR, bool ET, bool COUNT, bool REC, int MINB = (NWR == 4 ? 10 : 16)>
-__global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2* __restrict__ ranges,
-                                                              const uint32_t* __restrict__ sorted_vals,
+// Shared memory of the forward: the staged batch, or (SORT) its union with
+// the per-tile sort that runs first.
+template <int NWR, bool SORT>
+struct FwdShared {
+    BatchT<NWR> b;
+};
+template <int NWR>
+struct FwdShared<NWR, true> {
+    union {
+        BatchT<NWR> b;
+        SegsortShared srt;
+    };
+};
+
+// Out of line, so the sort's register allocation stays out of the raster loop's.
+static __device__ __noinline__ void fwd_sort_tile(SegsortShared& sh, uint2 rg, const uint32_t* __restrict__ dkeys,
+                                                  uint32_t* vals, uint32_t* __restrict__ alt) {
+    segsort_tile(sh, rg, dkeys, vals, alt);
+}
+
+// SORT (frame path, scatter binning): the CTA first sorts its tile's range
+// of sorted_vals in place by (depth, index) (segsort.cuh) -- the per-tile
+// sort fused into the raster, so a tile's sort overlaps other tiles'
+// compositing on the same SM instead of being a latency-bound kernel of its
+// own.
+template <int NWR, bool ET, bool COUNT, bool REC>
+__device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uint2* __restrict__ ranges,
+                                                              const uint32_t* sorted_vals,
                                                               const float4* __restrict__ xydr,
                                                               const float4* __restrict__ conic,
                                                               const float* __restrict__ colors, float3 bg, int W,
@@ -248,11 +273,8 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
                                                               uint2* __restrict__ rec,
                                                               uint32_t* __restrict__ rec_count,
                                                               const uint32_t* __restrict__ tile_order) {
-    griddep_wait();
     constexpr int NPR = 4 / NWR;
     static_assert(!REC || NWR == 4, "records are per 8x8 quadrant");
-    __shared__ BatchT<NWR> s;
-    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int col = tx * TILE + (warp & 1) * 8 + (lane & 7);
@@ -414,6 +436,21 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(const uint2*
             atomicAdd(&counts[3], e_c);
         }
     }
+}
+
+template <int NWR, bool ET, bool COUNT, bool REC, int MINB = (NWR == 4 ? 10 : 16), bool SORT = false>
+__global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(
+    const uint2* __restrict__ ranges, const uint32_t* sorted_vals, const float4* __restrict__ xydr,
+    const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg, int W, int H, int tiles_x,
+    float* __restrict__ out_img, float* __restrict__ out_T, int* __restrict__ out_nc,
+    unsigned long long* __restrict__ counts, uint2* __restrict__ rec, uint32_t* __restrict__ rec_count,
+    const uint32_t* __restrict__ tile_order, const uint32_t* __restrict__ dkeys, uint32_t* __restrict__ sort_alt) {
+    griddep_wait();
+    __shared__ FwdShared<NWR, SORT> sh;
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
+    if constexpr (SORT) fwd_sort_tile(sh.srt, ranges[tile], dkeys, const_cast<uint32_t*>(sorted_vals), sort_alt);
+    raster_fwd_body<NWR, ET, COUNT, REC>(sh.b, tile, ranges, sorted_vals, xydr, conic, colors, bg, W, H, tiles_x,
+                                         out_img, out_T, out_nc, counts, rec, rec_count, tile_order);
 }
 
 // ============================================================ backward
@@ -858,27 +895,27 @@ static int fwd_regions() {
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
                       unsigned long long* counts, cudaStream_t s, uint2* rec, uint32_t* rec_count,
-                      const uint32_t* tile_order) {
+                      const uint32_t* tile_order, const uint32_t* dkeys, uint32_t* sort_alt) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     const float4* g = (const float4*)xydr4;
     const float4* q = (const float4*)conic4;
+    uint32_t* dk = nullptr;
 #define GS_FWD_R(NWR, ET, CNT, REC)                                                                          \
     raster_fwd_kernel<NWR, ET, CNT, REC><<<nt, 32 * NWR, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, \
-                                                                 img, T, nc, counts, rec, rec_count, tile_order)
+                                                                 img, T, nc, counts, rec, rec_count, tile_order, \
+                                                                 dk, dk)
 #define GS_FWD(NWR, ET, CNT) GS_FWD_R(NWR, ET, CNT, false)
     const bool cnt = counts != nullptr;
-#define GS_FWD_M(ET, M)                                                                                        \
-    launch_k(raster_fwd_kernel<4, ET, false, true, M>, dim3(nt), dim3(128), 0, s, ranges, vals, g, q, colors3, bg, \
-             W, H, tiles_x, img, T, nc, counts, rec, rec_count, tile_order)
-    if (rec && !cnt) {  // frame path: 8x8 quadrants with commit records, 9 CTAs/SM (measured best)
-        static const int minb = [] {
-            const char* e = getenv("GS_FWD_MINB");
-            return e ? atoi(e) : 9;
-        }();
-        if (minb == 8) { if (et) GS_FWD_M(true, 8); else GS_FWD_M(false, 8); }
-        else if (minb == 10) { if (et) GS_FWD_M(true, 10); else GS_FWD_M(false, 10); }
-        else { if (et) GS_FWD_M(true, 9); else GS_FWD_M(false, 9); }
+    // frame path: 8x8 quadrants with commit records, 9 CTAs/SM (measured best
+    // against 8 and 10), optionally with the per-tile sort fused in front
+#define GS_FWD_M(ET, SORT)                                                                                     \
+    launch_k(raster_fwd_kernel<4, ET, false, true, 9, SORT>, dim3(nt), dim3(128), 0, s, ranges, vals, g, q,   \
+             colors3, bg, W, H, tiles_x, img, T, nc, counts, rec, rec_count, tile_order, dkeys, sort_alt)
+    if (dkeys && !(rec && !cnt)) return set_error("raster_fwd: the fused tile sort needs the frame path");
+    if (rec && !cnt) {
+        if (dkeys) { if (et) GS_FWD_M(true, true); else GS_FWD_M(false, true); }
+        else { if (et) GS_FWD_M(true, false); else GS_FWD_M(false, false); }
     } else if (rec) {
         if (et) GS_FWD_R(4, true, true, true); else GS_FWD_R(4, false, true, true);
     } else if (fwd_regions() == 2) {

@@ -78,6 +78,14 @@ def set_option(name: str, value: int) -> None:
     check(_lib.load().gs_set_option(name.encode(), int(value)), "gs_set_option")
 
 
+def get_option(name: str) -> int:
+    """Current value of a gs_set_option option (gs_get_option)."""
+    v = int(_lib.load().gs_get_option(name.encode()))
+    if v < 0:
+        check(v, "gs_get_option")
+    return v
+
+
 def _check_param(name, t, cols):
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")

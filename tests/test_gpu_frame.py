@@ -50,13 +50,17 @@ def test_frame_equals_staged_on_golden(name, cuda):
         assert r["ok"], (name, k, r)
 
 
-@pytest.fixture(params=[1, 2], ids=["depth_first", "scatter"])
+@pytest.fixture(params=[(1, 1), (2, 1), (2, 0)], ids=["depth_first", "scatter", "scatter_sort_kernel"])
 def binning(request, cuda):
-    """Run a test under both frame binning strategies (gs_set_option)."""
+    """Run a test under both frame binning strategies (gs_set_option), the
+    scatter one with its per-tile sort fused into the raster forward and as
+    its own kernel."""
     from paper_2312_02121_b200 import ops
-    ops.set_option("binning", request.param)
-    yield request.param
+    ops.set_option("binning", request.param[0])
+    ops.set_option("fuse_sort", request.param[1])
+    yield request.param[0]
     ops.set_option("binning", 0)
+    ops.set_option("fuse_sort", 1)
 
 
 @pytest.mark.parametrize("name", golden_names())

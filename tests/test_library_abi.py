@@ -44,10 +44,18 @@ def test_set_option():
     from paper_2312_02121_b200 import _lib, ops
     for v in (1, 2, 0):
         ops.set_option("binning", v)
+        assert ops.get_option("binning") == v
+    for v in (0, 1):
+        ops.set_option("fuse_sort", v)
+        assert ops.get_option("fuse_sort") == v
     with pytest.raises(_lib.SplatLibError, match="binning"):
         ops.set_option("binning", 7)
+    with pytest.raises(_lib.SplatLibError, match="fuse_sort"):
+        ops.set_option("fuse_sort", 2)
     with pytest.raises(_lib.SplatLibError, match="unknown option"):
         ops.set_option("no_such_option", 1)
+    with pytest.raises(_lib.SplatLibError, match="unknown option"):
+        ops.get_option("no_such_option")
     L = _lib.load()
     assert L.gs_bin64_workspace_bytes(1000, 5000, 256) > 0
     assert L.gs_project64_bwd_workspace_bytes(1000) > 0
