@@ -65,17 +65,19 @@ def tile_order_launches(cam):
     return 1 if on and cam.tiles_x * cam.tiles_y > 148 * 8 else 0
 
 
-def scatter_binning(n):
-    """Which frame binning the library uses (csrc/frame.cu, gs_get_option)."""
+def binning_of(n, cam):
+    """The frame binning the library uses for this view (gs_frame_binning):
+    "depth_first", "scatter" or "direct"."""
     from paper_2312_02121_b200 import ops
-    mode = ops.get_option("binning")
-    return mode == 2 or (mode == 0 and n <= 400000)
+    return ops.frame_binning(n, cam)
 
 
-def fused_sort(n):
-    """Scatter binning with its per-tile sort fused into the raster forward."""
+def fused_sort(n, cam):
+    """The per-tile sort runs inside the raster forward (direct binning, or
+    scatter binning with the fuse_sort option)."""
     from paper_2312_02121_b200 import ops
-    return scatter_binning(n) and ops.get_option("fuse_sort") == 1
+    b = binning_of(n, cam)
+    return b == "direct" or (b == "scatter" and ops.get_option("fuse_sort") == 1)
 
 
 def views_for(cfg, spec, world, rank):
@@ -229,11 +231,14 @@ def run_ours(args):
         counts_f += fr.counts_fwd.cpu().numpy()
         counts_b += g["counts"].cpu().numpy()
         isect.append(fr.n_isect)
-        cap = int(fr.n_isect * 1.05) + 4096
+        del fr, g
+        # the timed frames' capacity (the counted pass may bin differently: size from an uncounted frame)
+        fr = ops.frame_forward(m, s, q, o, c, cam, bg, True)
+        cap = int(fr.needed_capacity * 1.05) + 4096
         caps.append(cap)
         wss.append(torch.empty((L.gs_frame_workspace_bytes(n, cap, cam.width, cam.height),), device=dev,
                                dtype=torch.uint8))
-        del fr, g
+        del fr
 
     def mk_events(k):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
@@ -336,7 +341,7 @@ def run_ours(args):
     # the capacity was sized from a checked run; confirm nothing overflowed
     for vi, fr in enumerate(frames_out):
         meta = fr.meta().cpu()
-        assert int(meta[0]) == -1 and int(meta[1]) <= caps[vi], "capacity overflow / status error in timed run"
+        assert int(meta[0]) == -1 and ops.needed_capacity(meta) <= caps[vi], "capacity overflow / status error in timed run"
     total_ms = float(sum(step_ms))
     if world > 1:
         tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -375,19 +380,25 @@ def run_ours(args):
     # algorithmic work; per rank-step, all views
     F_fwd = 8 * counts_f[0] + 4 * counts_f[1] + 3 * counts_f[2] + 4 * counts_f[3]
     F_bwd = 8 * counts_b[0] + 4 * counts_b[1] + 42 * counts_b[2]
-    seg = scatter_binning(n)
+    binning = binning_of(n, cams[0])
+    seg = binning != "depth_first"
+    direct = binning == "direct"
+    fused = fused_sort(n, cams[0])
     work = {
-        # read 44 B, write xydr 16 + conic 16 + tiles 4 + depth key 4 (scatter binning: + tile-count atomics)
-        "project": ("hbm", 84.0 * n * nv),
-        # depth-first: 4 passes x (key+value) x (read+write); scatter binning: no global depth sort
+        # read 44 B, write xydr 16 + conic 16 + tiles 4 + depth key 4; direct binning: + a slot
+        # atomic and the Gaussian id per intersection (8 B)
+        "project": ("hbm", 84.0 * n * nv + (8.0 * I if direct else 0.0)),
+        # depth-first: 4 passes x (key+value) x (read+write); scatter / direct: no global depth sort
         "depth_sort": ("none", 0.0) if seg else ("hbm", 4 * 16.0 * n * nv),
         # depth-first: fused scan + emission, (order +) count + xydr gather per Gaussian, pairs out;
-        # scatter: tile scan (8 counter replicas + ranges) + count + xydr per Gaussian, pairs out
-        "scan_emit": ("hbm", (40.0 * n_tiles + 20.0 * n * nv + 8.0 * I) if seg else
+        # scatter: tile scan (8 counter replicas + ranges) + count + xydr per Gaussian, pairs out;
+        # direct: none (the projection placed the pairs)
+        "scan_emit": ("none", 0.0) if direct else
+                     ("hbm", (40.0 * n_tiles + 20.0 * n * nv + 8.0 * I) if seg else
                       (8.0 * n * nv + 16.0 * n * nv + 8.0 * I)),
         # depth-first: tile passes (key+value, read+write) + ranges; scatter: per-tile sort
-        # (value in, key gather, value out) + ranges -- fused into the raster forward by default
-        "tile_sort_ranges": ("none", 0.0) if fused_sort(n) else
+        # (value in, key gather, value out) + ranges -- inside the raster forward when fused
+        "tile_sort_ranges": ("none", 0.0) if fused else
                             ("hbm", (12.0 * I + 8.0 * n_tiles) if seg else
                              (tp * 16.0 * I + 4.0 * I + 8.0 * n_tiles)),
         "raster_fwd": ("fp32", float(F_fwd)),
@@ -408,8 +419,8 @@ def run_ours(args):
         else:
             d["achieved_tops"] = round(w / (ms / 1e3) / 1e12, 3) if ms > 0 else None
             d["frac"] = round(w / (ms / 1e3) / fp32_peak, 4) if ms > 0 else None
-        if name == "raster_fwd" and fused_sort(n):
-            d["includes"] = "per-tile (depth, index) sort of the tile's list (fuse_sort)"
+        if name == "raster_fwd" and fused:
+            d["includes"] = "per-tile (depth, index) sort of the tile's list"
         st[name] = d
     dom = max(stage_names, key=lambda k: stage_ms[stage_names.index(k)])
     if dom == "raster_bwd" and timed_bwd_ms > 0:
@@ -453,14 +464,15 @@ def run_ours(args):
         "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
         "intersections_per_step_rank": int(I),
         "e2e": e2e,
-        # per view (csrc/frame.cu): scatter binning: init, project (+ tile counts), tile scan
-        # (+ raster order), pair scatter, [per-tile sort,] raster fwd (+ the per-tile sort when
-        # fused) | raster bwd, project bwd
-        # (its last block reduces d_view); depth-first: init, project, 4 depth passes, fused
-        # scan+emit, tp tile passes, ranges, (tile order for grids over one raster wave), raster fwd |
-        # raster bwd, project bwd
-        "gpu_launches": int(args.steps * len(cams) * ((7 if fused_sort(n) else 8) if scatter_binning(n) else
+        # per view (csrc/frame.cu): direct binning: init, project (+ pairs into the tile bins),
+        # raster fwd (+ the per-tile sort) | raster bwd, project bwd; scatter binning: init, project
+        # (+ tile counts), tile scan (+ raster order), pair scatter, [per-tile sort,] raster fwd |
+        # raster bwd, project bwd; depth-first: init, project, 4 depth passes, fused scan+emit, tp
+        # tile passes, ranges, (tile order for grids over one raster wave), raster fwd | raster bwd,
+        # project bwd
+        "gpu_launches": int(args.steps * len(cams) * (5 if direct else (7 if fused else 8) if seg else
                                                       11 + tp + tile_order_launches(cams[0]))),
+        "binning": binning,
         "roofline": roof,
         "stages": st,
         "counts": {"E_f": int(counts_f[0]), "E_f_sigma": int(counts_f[1]), "E_f_alpha": int(counts_f[2]),

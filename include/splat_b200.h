@@ -58,11 +58,14 @@ typedef struct gs_camera {
 const char* gs_last_error(void);
 int gs_version(void);
 /* Process-wide tuning options.  "binning": the frame path's tile binning,
- * 0 = auto (scatter for n <= 400000 Gaussians, else depth-first),
+ * 0 = auto (direct for n <= 400000 Gaussians on <= 4096 tiles, scatter for
+ * other n <= 400000, else depth-first),
  * 1 = depth-first (global stable depth sort, then tile sort of pairs emitted
  * in depth order), 2 = scatter (per-tile counts from the projection, pairs
  * written into their tile ranges through atomic cursors, each range sorted
- * by (depth, index)).  Both give sg/binning.py:50-65's (depth,
+ * by (depth, index)), 3 = direct (the projection writes every pair into its
+ * tile's fixed-stride bin through an atomic slot counter; the raster
+ * forward sorts each bin).  Both give sg/binning.py:50-65's (depth,
  * source_index) lists bit for bit.  "fuse_sort" (scatter binning): 1
  * (default) sorts each tile's range at the top of the raster forward CTA
  * that composites it, 0 in a separate per-tile sort kernel; same lists. */
@@ -173,8 +176,11 @@ int gs_project_bwd(const float* means3, const float* scales3, const float* quats
  * 32-bit keys) -- the same per-tile (depth, source_index) order as the
  * 64-bit keys above, with ~3-4x less sort traffic.
  * No host synchronisation, no allocation: intersections go into a caller-
- * chosen capacity; meta[1] (device) reports the true total, meta[0] the
- * status word.  If meta[1] > capacity the caller re-runs with a larger
+ * chosen capacity; meta (device, 4 words) reports [0] the status word, [1]
+ * the true total, [2] the capacity needed when it exceeds the total (direct
+ * binning: every tile owns capacity / tiles slots, so tiles x the longest
+ * list) and [3] the direct-binning tile stride (0: compact bins).  If
+ * max(meta[1], meta[2]) > capacity the caller re-runs with a larger
  * workspace (results are not valid until it does).
  * forward  replaces sg/raster_forward.py:255-271 render;
  * backward replaces sg/proj_backward.py:178-223 scene_backward.          */
@@ -186,7 +192,8 @@ typedef struct gs_frame_view {
     uint32_t* sorted_tile_keys; /* (capacity) tile id of each sorted pair */
     uint32_t* sorted_vals;      /* (capacity) Gaussian id of each sorted pair */
     uint32_t* ranges2;          /* (tiles,2) [start, end) */
-    unsigned long long* meta;   /* [0] status word, [1] total intersections */
+    unsigned long long* meta;   /* [0] status word, [1] total intersections, [2] capacity needed,
+                                   [3] direct-binning tile stride (0: compact bins) */
     float* d_geo4;              /* (n,4) d_mean2d x,y, d_cov00, d_cov01 (after backward),
                                    row stride 8 floats (interleaved with d_rgbo) */
     float* d_c11;               /* (n)   d_cov11 (after backward) */
@@ -197,6 +204,9 @@ typedef struct gs_frame_view {
 } gs_frame_view;
 
 size_t gs_frame_workspace_bytes(int64_t n, int64_t isect_capacity, int32_t width, int32_t height);
+/* The binning gs_frame_forward uses for n Gaussians on a width x height
+ * view under the current options: 1 depth-first, 2 scatter, 3 direct. */
+int gs_frame_binning(int64_t n, int32_t width, int32_t height);
 int gs_frame_view_of(int64_t n, int64_t isect_capacity, int32_t width, int32_t height, void* ws,
                      gs_frame_view* out /*[host]*/);
 int gs_frame_forward(const float* means3, const float* scales3, const float* quats4, const float* opacities,

@@ -64,7 +64,7 @@ int gs_version(void) { return 1; }
 int gs_set_option(const char* name, int value) {
     if (!name) return gs::set_error("gs_set_option: null name");
     if (strcmp(name, "binning") == 0) {
-        if (value < 0 || value > 2) return gs::set_error("gs_set_option: binning must be 0 (auto), 1 or 2");
+        if (value < 0 || value > 3) return gs::set_error("gs_set_option: binning must be 0 (auto), 1, 2 or 3");
         gs::g_binning = value;
         return 0;
     }

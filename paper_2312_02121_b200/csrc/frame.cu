@@ -48,15 +48,25 @@ bool tile_order_enabled(int n_tiles) {
     return on && n_tiles > 148 * 8;
 }
 
-// Scatter binning for small scenes, depth-first otherwise
-// (gs_set_option("binning"): 0 auto, 1 depth-first, 2 scatter).
-bool scatter_binning(int64_t n) {
+// Binning strategy (gs_set_option("binning"): 0 auto, 1 depth-first,
+// 2 scatter, 3 direct).  Auto: direct for small scenes on up to 4096 tiles,
+// scatter for other small scenes, depth-first for N > 400k.
+enum Binning { DEPTH_FIRST = 1, SCATTER = 2, DIRECT = 3 };
+Binning binning_for(int64_t n, int n_tiles) {
     const int bmode = binning_mode();
-    return bmode == 2 || (bmode == 0 && n <= 400000);
+    if (bmode >= 1 && bmode <= 3) return (Binning)bmode;
+    if (n > 400000) return DEPTH_FIRST;
+    return n_tiles <= 4096 ? DIRECT : SCATTER;
 }
+bool scatter_binning(int64_t n, int n_tiles) { return binning_for(n, n_tiles) != DEPTH_FIRST; }
+
+// Direct binning: every tile owns kstride = capacity / tiles pair slots.
+int64_t direct_stride(int64_t cap, int n_tiles) { return n_tiles > 0 ? cap / n_tiles : 0; }
 
 // where the tile-sorted (keys, vals) of a frame end up
-bool sorted_in_alt(int64_t n, int n_tiles) { return !scatter_binning(n) && (tile_passes_for(n_tiles) & 1); }
+bool sorted_in_alt(int64_t n, int n_tiles) {
+    return !scatter_binning(n, n_tiles) && (tile_passes_for(n_tiles) & 1);
+}
 
 struct Layout {
     // persistent (written each frame)
@@ -97,7 +107,7 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.tile_order = take(4 * nt);  // raster launch order (heaviest lists first)
     L.tcount = take(4 * TCOUNT_REPL * nt);  // scatter binning: tile counts, then write cursors
     L.zero_begin = o;
-    L.meta = take(16);
+    L.meta = take(32);  // status, total intersections, capacity needed, direct-binning tile stride
     L.dhist = take(4 * 256 * 4);
     L.thist = take(4 * 256 * 2);
     L.counters = take(64);
@@ -136,6 +146,10 @@ T* at(void* ws, size_t off) {
 using namespace gs;
 
 extern "C" {
+
+int gs_frame_binning(int64_t n, int32_t width, int32_t height) {
+    return (int)binning_for(n, ((width + TILE - 1) / TILE) * ((height + TILE - 1) / TILE));
+}
 
 size_t gs_frame_workspace_bytes(int64_t n, int64_t isect_capacity, int32_t width, int32_t height) {
     return layout(n, isect_capacity, width, height).total;
@@ -194,17 +208,37 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     zj.n16[1] = (8 * (size_t)tiles_x * tiles_y + 15) / 16;
     zj.p[2] = at<uint4>(ws, L.d_geo);
     zj.n16[2] = (L.partials - L.d_geo) / 16;
-    const bool scatter = scatter_binning(n);
     const int n_tiles = tiles_x * tiles_y;
-    const uint32_t* t_order = tile_order_enabled(n_tiles) ? at<uint32_t>(ws, L.tile_order) : nullptr;
+    const Binning binning = binning_for(n, n_tiles);
+    const bool scatter = binning == SCATTER;
+    const bool direct = binning == DIRECT && counts4 == nullptr;  // the counted pass bins by scatter
+    const int64_t kstride = direct_stride(isect_capacity, n_tiles);
+    const uint32_t* t_order = !direct && tile_order_enabled(n_tiles) ? at<uint32_t>(ws, L.tile_order) : nullptr;
     if (launch_project_fwd_dkey(means3, scales3, quats4, opacities, n, k, at<float>(ws, L.xydr),
                                 at<float>(ws, L.conic), at<uint32_t>(ws, L.tiles), nullptr, meta,
                                 at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.dhist), s, zj,
-                                scatter ? at<uint32_t>(ws, L.tcount) : nullptr))
+                                binning != DEPTH_FIRST ? at<uint32_t>(ws, L.tcount) : nullptr,
+                                direct ? at<uint32_t>(ws, L.tvals) : nullptr, (uint32_t)kstride))
         return -1;
     mark(stage_events, 1, s);
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
-    if (scatter) {
+    if (direct) {
+        // 2-6. direct binning: the projection wrote every pair into its
+        //      tile's fixed-stride bin; the raster forward sorts each bin
+        //      by (depth, index) first and reports the counts
+        mark(stage_events, 2, s);
+        mark(stage_events, 3, s);
+        mark(stage_events, 4, s);
+        if (launch_raster_fwd(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.tvals), at<float>(ws, L.xydr),
+                              at<float>(ws, L.conic), colors3, bg, W, H, early_termination != 0, out_image,
+                              out_final_T, out_n_contrib, nullptr, s, at<uint2>(ws, L.rec),
+                              at<uint32_t>(ws, L.rec_count), nullptr, at<uint32_t>(ws, L.dkeys),
+                              at<uint32_t>(ws, L.tvals_alt), at<uint32_t>(ws, L.tcount), (uint32_t)kstride, meta))
+            return -1;
+        mark(stage_events, 5, s);
+        return 0;
+    }
+    if (binning != DEPTH_FIRST) {
         // 2-6. scatter binning: the projection counted every tile's pairs;
         //      scan -> ranges + cursors (+ raster order), scatter the pairs
         //      into their ranges, sort each range by (depth, index)
@@ -298,7 +332,9 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
     } else if (launch_raster_bwd_rec(at<uint2>(ws, L.ranges), at<uint2>(ws, L.rec), at<uint32_t>(ws, L.rec_count),
                                      at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3, bg, W, H, final_T,
                                      n_contrib, d_image, g8, at<float>(ws, L.d_c11), s,
-                                     tile_order_enabled(tiles_x * tiles_y) ? at<uint32_t>(ws, L.tile_order) : nullptr)) {
+                                     binning_for(n, tiles_x * tiles_y) != DIRECT && tile_order_enabled(tiles_x * tiles_y)
+                                         ? at<uint32_t>(ws, L.tile_order)
+                                         : nullptr)) {
         return -1;
     }
     mark(stage_events, 1, s);

@@ -13,8 +13,10 @@ namespace gs {
 int launch_project_fwd_dkey(const float* means3, const float* scales3, const float* quats4, const float* opac,
                             int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
                             unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s,
-                            const ZeroJobs& zj, uint32_t* tcount = nullptr);  // also resets meta (status,
-                            // total), dhist and (scatter binning: per-tile intersection counts) tcount first
+                            const ZeroJobs& zj, uint32_t* tcount = nullptr, uint32_t* bins = nullptr,
+                            uint32_t kstride = 0);  // also resets meta (status, total, need), dhist and
+                            // (scatter / direct binning: per-tile intersection counts) tcount first;
+                            // bins != nullptr: direct binning into bins[tile * kstride + slot]
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
                        float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
@@ -75,7 +77,9 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
                       unsigned long long* counts, cudaStream_t s, uint2* rec = nullptr,
                       uint32_t* rec_count = nullptr, const uint32_t* tile_order = nullptr,
-                      const uint32_t* dkeys = nullptr, uint32_t* sort_alt = nullptr);  // dkeys: fused tile sort
+                      const uint32_t* dkeys = nullptr, uint32_t* sort_alt = nullptr,  // dkeys: fused tile sort
+                      const uint32_t* direct_counts = nullptr, uint32_t kstride = 0,    // direct binning
+                      unsigned long long* meta = nullptr);
 // record-driven backward of the frame path (records written by the forward)
 int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,

@@ -28,13 +28,21 @@ __device__ __forceinline__ void report(unsigned long long* status, int i, int co
 // ones so they sort last).  MODE 1 (depth-first binning) accumulates the
 // four 8-bit digit histograms of those keys for the onesweep depth sort
 // that follows (sort.cu), in shared memory; MODE 2 (scatter binning) counts
-// every tile's intersections instead (tcount, one red.add per pair).
+// every tile's intersections instead (tcount, one red.add per pair); MODE 3
+// (direct binning) takes a slot in the tile's fixed-stride bin for every
+// pair (atomicAdd on tcount[tile] with return, 4 in flight per lane) and
+// writes the Gaussian id there: bins[tile * kstride + slot] (slots past
+// kstride are dropped; the raster forward reports the overflow).
+#ifndef DIRECT_UNROLL
+#define DIRECT_UNROLL 4  // slot atomics in flight per lane (direct binning)
+#endif
 template <int MODE>
 __global__ void __launch_bounds__(256) project_fwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
     const float* __restrict__ opac, int n, CamK cam, float4* __restrict__ xydr, float4* __restrict__ conic,
     uint32_t* __restrict__ tiles, float* __restrict__ cov_out, unsigned long long* __restrict__ status,
-    uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dhist, ZeroJobs zj, uint32_t* __restrict__ tcount) {
+    uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dhist, ZeroJobs zj, uint32_t* __restrict__ tcount,
+    uint32_t* __restrict__ bins, uint32_t kstride) {
     constexpr bool DKEY = MODE != 0;
     griddep_wait();
     run_zero_jobs(zj);  // frame path: clear the later stages' counters / accumulators
@@ -48,7 +56,7 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
     const int n_round = (n + 31) & ~31;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += gridDim.x * blockDim.x) {
     uint32_t dkey = 0xFFFFFFFFu;
-    int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;  // tile rect (MODE 2 walks it)
+    int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;  // tile rect (MODE 2 / 3 walk it)
     if (i < n) {
     const float mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
     // every input load is issued up front (one memory round trip; the culled
@@ -137,6 +145,18 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
         dkeys[i] = dkey;
     }
     }  // i < n
+    if (MODE == 3) {
+        walk_tile_rects<DIRECT_UNROLL>(threadIdx.x & 31, (uint32_t)i, tx0, tx1, ty0, ty1, cam.tiles_x,
+                           [&](const uint32_t* tl, const uint32_t* gl) {
+                               uint32_t slot[DIRECT_UNROLL];
+#pragma unroll
+                               for (int u = 0; u < DIRECT_UNROLL; ++u)
+                                   slot[u] = tl[u] != 0xFFFFFFFFu ? atomicAdd(&tcount[tl[u]], 1u) : kstride;
+#pragma unroll
+                               for (int u = 0; u < DIRECT_UNROLL; ++u)
+                                   if (slot[u] < kstride) bins[(size_t)tl[u] * kstride + slot[u]] = gl[u];
+                           });
+    }
     if (MODE == 2) {
         uint32_t* tc = tcount + (size_t)tcount_replica((uint32_t)i) * (cam.tiles_x * cam.tiles_y);
         walk_tile_rects(threadIdx.x & 31, 0u, tx0, tx1, ty0, ty1, cam.tiles_x,
@@ -408,6 +428,8 @@ __global__ void __launch_bounds__(256) frame_init_kernel(unsigned long long* __r
         if (threadIdx.x == 0) {
             meta[0] = ~0ull;
             meta[1] = 0ull;
+            meta[2] = 0ull;
+            meta[3] = 0ull;
         }
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) dhist[k] = 0u;
     }
@@ -418,7 +440,7 @@ __global__ void __launch_bounds__(256) frame_init_kernel(unsigned long long* __r
 int launch_project_fwd_dkey(const float* means3, const float* scales3, const float* quats4, const float* opac,
                             int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
                             unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s,
-                            const ZeroJobs& zj, uint32_t* tcount) {
+                            const ZeroJobs& zj, uint32_t* tcount, uint32_t* bins, uint32_t kstride) {
     const int n_tiles = k.tiles_x * k.tiles_y;
     const int init_blocks = tcount ? (TCOUNT_REPL * n_tiles + 2047) / 2048 : 1;
     launch_k(frame_init_kernel, dim3((unsigned)init_blocks), dim3(256), 0, s, status, dhist, tcount,
@@ -428,14 +450,18 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
     if (blocks < 1) blocks = 1;  // the zero jobs run even for an empty scene
     const int64_t cap = (int64_t)sort_sm_count() * 6;  // resident CTAs (40 regs, 256 threads)
     if (blocks > cap) blocks = cap;
-    if (tcount)
+    if (tcount && bins)
+        launch_k(project_fwd_kernel<3>, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
+                 (const float4*)quats4, opac, (int)n, k, (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
+                 dhist, zj, tcount, bins, kstride);
+    else if (tcount)
         launch_k(project_fwd_kernel<2>, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
                  (const float4*)quats4, opac, (int)n, k, (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
-                 dhist, zj, tcount);
+                 dhist, zj, tcount, (uint32_t*)nullptr, 0u);
     else
         launch_k(project_fwd_kernel<1>, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
                  (const float4*)quats4, opac, (int)n, k, (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
-                 dhist, zj, (uint32_t*)nullptr);
+                 dhist, zj, (uint32_t*)nullptr, (uint32_t*)nullptr, 0u);
     return check_launch("project_fwd_kernel<dkey>");
 }
 
@@ -472,7 +498,7 @@ int gs_project_fwd(const float* means3, const float* scales3, const float* quats
     const int blocks = (int)((n + 255) / 256);
     project_fwd_kernel<0><<<blocks, 256, 0, (cudaStream_t)stream>>>(
         means3, scales3, (const float4*)quats4, opacities, (int)n, k, (float4*)out_xydr4, (float4*)out_conic4,
-        out_tiles, out_cov3, status, nullptr, nullptr, ZeroJobs{}, nullptr);
+        out_tiles, out_cov3, status, nullptr, nullptr, ZeroJobs{}, nullptr, nullptr, 0u);
     return check_launch("project_fwd_kernel");
 }
 

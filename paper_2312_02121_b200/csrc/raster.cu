@@ -256,13 +256,8 @@ static __device__ __noinline__ void fwd_sort_tile(SegsortShared& sh, uint2 rg, c
     segsort_tile(sh, rg, dkeys, vals, alt);
 }
 
-// SORT (frame path, scatter binning): the CTA first sorts its tile's range
-// of sorted_vals in place by (depth, index) (segsort.cuh) -- the per-tile
-// sort fused into the raster, so a tile's sort overlaps other tiles'
-// compositing on the same SM instead of being a latency-bound kernel of its
-// own.
 template <int NWR, bool ET, bool COUNT, bool REC>
-__device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uint2* __restrict__ ranges,
+__device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uint2 rg,
                                                               const uint32_t* sorted_vals,
                                                               const float4* __restrict__ xydr,
                                                               const float4* __restrict__ conic,
@@ -301,7 +296,6 @@ __device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uin
         for (int j = 0; j < NPR; ++j) d = d && p[j].done == 3u;
         return d;
     };
-    const uint2 rg = ranges[tile];
     const int start = (int)rg.x, end = (int)rg.y;
     unsigned long long e_s = 0, e_a = 0, e_c = 0;
     // this warp's record region: 4 * start + warp * len (no atomics)
@@ -384,9 +378,8 @@ __device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uin
         }
     }
     if (REC && lane == 0) {
-        const uint2 r2 = ranges[tile];
         rec_count[(size_t)tile * 4 + warp] =
-            (uint32_t)(rp - (rec + 4 * (int64_t)r2.x + (int64_t)warp * (r2.y - r2.x)));
+            (uint32_t)(rp - (rec + 4 * (int64_t)rg.x + (int64_t)warp * (rg.y - rg.x)));
     }
 #pragma unroll
     for (int j = 0; j < NPR; ++j) {
@@ -438,18 +431,45 @@ __device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uin
     }
 }
 
+// SORT (frame path, scatter / direct binning): the CTA first sorts its
+// tile's range of sorted_vals in place by (depth, index) (segsort.cuh) --
+// the per-tile sort fused into the raster, so a tile's sort overlaps other
+// tiles' compositing on the same SM instead of being a latency-bound kernel
+// of its own.  Direct binning (direct_counts != nullptr): the tile's list is
+// bins[tile * kstride, + count) as the projection left it; the CTA writes
+// the tile's range, adds its count to meta[1] (total intersections) and
+// raises meta[2] (capacity needed = tiles * the longest list); a list over
+// kstride is not rastered (the caller re-runs with a larger capacity).
+// meta[3] = kstride tells readers of the bins that they are strided.
 template <int NWR, bool ET, bool COUNT, bool REC, int MINB = (NWR == 4 ? 10 : 16), bool SORT = false>
 __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(
-    const uint2* __restrict__ ranges, const uint32_t* sorted_vals, const float4* __restrict__ xydr,
+    const uint2* ranges, const uint32_t* sorted_vals, const float4* __restrict__ xydr,
     const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg, int W, int H, int tiles_x,
     float* __restrict__ out_img, float* __restrict__ out_T, int* __restrict__ out_nc,
     unsigned long long* __restrict__ counts, uint2* __restrict__ rec, uint32_t* __restrict__ rec_count,
-    const uint32_t* __restrict__ tile_order, const uint32_t* __restrict__ dkeys, uint32_t* __restrict__ sort_alt) {
+    const uint32_t* __restrict__ tile_order, const uint32_t* __restrict__ dkeys, uint32_t* __restrict__ sort_alt,
+    const uint32_t* __restrict__ direct_counts, uint32_t kstride, unsigned long long* __restrict__ meta) {
     griddep_wait();
     __shared__ FwdShared<NWR, SORT> sh;
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
-    if constexpr (SORT) fwd_sort_tile(sh.srt, ranges[tile], dkeys, const_cast<uint32_t*>(sorted_vals), sort_alt);
-    raster_fwd_body<NWR, ET, COUNT, REC>(sh.b, tile, ranges, sorted_vals, xydr, conic, colors, bg, W, H, tiles_x,
+    uint2 rg;
+    if (SORT && direct_counts) {
+        const uint32_t c = direct_counts[tile];
+        const uint32_t b = (uint32_t)tile * kstride;
+        rg = c <= kstride ? make_uint2(b, b + c) : make_uint2(b, b);
+        if (threadIdx.x == 0) {
+            if (blockIdx.x == 0) meta[3] = kstride;
+            const_cast<uint2*>(ranges)[tile] = rg;
+            if (c) {
+                atomicAdd(&meta[1], (unsigned long long)c);
+                atomicMax(&meta[2], (unsigned long long)c * (unsigned long long)(gridDim.x));
+            }
+        }
+    } else {
+        rg = ranges[tile];
+    }
+    if constexpr (SORT) fwd_sort_tile(sh.srt, rg, dkeys, const_cast<uint32_t*>(sorted_vals), sort_alt);
+    raster_fwd_body<NWR, ET, COUNT, REC>(sh.b, tile, rg, sorted_vals, xydr, conic, colors, bg, W, H, tiles_x,
                                          out_img, out_T, out_nc, counts, rec, rec_count, tile_order);
 }
 
@@ -895,7 +915,8 @@ static int fwd_regions() {
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
                       unsigned long long* counts, cudaStream_t s, uint2* rec, uint32_t* rec_count,
-                      const uint32_t* tile_order, const uint32_t* dkeys, uint32_t* sort_alt) {
+                      const uint32_t* tile_order, const uint32_t* dkeys, uint32_t* sort_alt,
+                      const uint32_t* direct_counts, uint32_t kstride, unsigned long long* meta) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     const unsigned nt = (unsigned)(tiles_x * tiles_y);
     const float4* g = (const float4*)xydr4;
@@ -904,15 +925,17 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
 #define GS_FWD_R(NWR, ET, CNT, REC)                                                                          \
     raster_fwd_kernel<NWR, ET, CNT, REC><<<nt, 32 * NWR, 0, s>>>(ranges, vals, g, q, colors3, bg, W, H, tiles_x, \
                                                                  img, T, nc, counts, rec, rec_count, tile_order, \
-                                                                 dk, dk)
+                                                                 dk, dk, dk, 0u, nullptr)
 #define GS_FWD(NWR, ET, CNT) GS_FWD_R(NWR, ET, CNT, false)
     const bool cnt = counts != nullptr;
     // frame path: 8x8 quadrants with commit records, 9 CTAs/SM (measured best
     // against 8 and 10), optionally with the per-tile sort fused in front
 #define GS_FWD_M(ET, SORT)                                                                                     \
     launch_k(raster_fwd_kernel<4, ET, false, true, 9, SORT>, dim3(nt), dim3(128), 0, s, ranges, vals, g, q,   \
-             colors3, bg, W, H, tiles_x, img, T, nc, counts, rec, rec_count, tile_order, dkeys, sort_alt)
+             colors3, bg, W, H, tiles_x, img, T, nc, counts, rec, rec_count, tile_order, dkeys, sort_alt,        \
+             direct_counts, kstride, meta)
     if (dkeys && !(rec && !cnt)) return set_error("raster_fwd: the fused tile sort needs the frame path");
+    if (direct_counts && (!dkeys || !meta)) return set_error("raster_fwd: direct binning needs the fused sort");
     if (rec && !cnt) {
         if (dkeys) { if (et) GS_FWD_M(true, true); else GS_FWD_M(false, true); }
         else { if (et) GS_FWD_M(true, false); else GS_FWD_M(false, false); }

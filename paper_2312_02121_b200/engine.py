@@ -56,7 +56,7 @@ class RenderStep:
                 params=[z(n, 3), z(n, 3), z(n, 4), z(n), z(n, 3)],
                 d_images=[z(c.height, c.width, 3) for c in self.cams],
                 grads=z(14 * n),
-                meta=torch.zeros((len(self.cams), 2), device=self.dev, dtype=torch.int64),
+                meta=torch.zeros((len(self.cams), 4), device=self.dev, dtype=torch.int64),
                 graph=None))
         self.caps = None
         self.wss = None
@@ -70,7 +70,7 @@ class RenderStep:
         self.caps, self.wss = [], []
         for cam, d in zip(self.cams, s["d_images"]):
             fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et)
-            cap = int(fr.n_isect * self.headroom) + 4096
+            cap = int(fr.needed_capacity * self.headroom) + 4096
             self.caps.append(cap)
             self.wss.append(torch.empty((L.gs_frame_workspace_bytes(self.n, cap, cam.width, cam.height),),
                                         device=self.dev, dtype=torch.uint8))
@@ -129,9 +129,9 @@ class RenderStep:
         capacity overflow grow the capacities, re-capture and re-run it.
         Returns the flat device gradient buffer (see unpack)."""
         m = (meta_host if meta_host is not None else self.meta(k).cpu()).tolist()
-        for status, _ in m:
-            ops.raise_status(int(status))
-        if any(total > cap for (_, total), cap in zip(m, self.caps)):
+        for row in m:
+            ops.raise_status(int(row[0]))
+        if any(ops.needed_capacity(row) > cap for row, cap in zip(m, self.caps)):
             self._size(k)
             self._capture()
             self.replay(k)
@@ -161,7 +161,7 @@ def pipeline(engine: RenderStep, host_params, host_d_images, out_host, steps: in
     loaded = [torch.cuda.Event() for _ in range(nb)]
     done = [torch.cuda.Event() for _ in range(nb)]
     read = [torch.cuda.Event() for _ in range(nb)]
-    metas = [torch.empty((len(engine.cams), 2), dtype=torch.int64).pin_memory() for _ in range(nb)]
+    metas = [torch.empty((len(engine.cams), 4), dtype=torch.int64).pin_memory() for _ in range(nb)]
     for e in read + done:
         e.record(comp)
     for k in range(steps):

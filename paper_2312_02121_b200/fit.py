@@ -111,15 +111,16 @@ class GpuFit:
             fr = ops.frame_forward(self.means, self.scales, self.quats, self.opac, self.colors, self.cam, self.bg,
                                    True, capacity=self.capacity, check_meta=self.capacity is None, ws=self.ws)
             if self.capacity is None:  # first frame sized the buffers
-                self.capacity = int(fr.n_isect * 1.5) + 4096
+                self.capacity = int(fr.needed_capacity * 1.5) + 4096
                 self.ws = None
                 continue
             meta = fr.meta().cpu()
             ops.raise_status(int(meta[0]))
-            if int(meta[1]) <= self.capacity:
+            need = ops.needed_capacity(meta)
+            if need <= self.capacity:
                 self.ws = fr.ws
                 break
-            self.capacity = int(int(meta[1]) * 1.5) + 4096
+            self.capacity = int(need * 1.5) + 4096
             self.ws = None
         loss_slot = self.losses[it:it + 1]
         check(L.gs_loss_l2(fr.image.data_ptr(), self.target.data_ptr(), self.target.numel(), self.d_image.data_ptr(),

@@ -78,6 +78,13 @@ def set_option(name: str, value: int) -> None:
     check(_lib.load().gs_set_option(name.encode(), int(value)), "gs_set_option")
 
 
+def frame_binning(n: int, cam) -> str:
+    """The tile binning gs_frame_forward uses for n Gaussians on this view
+    under the current options: "depth_first", "scatter" or "direct"."""
+    b = int(_lib.load().gs_frame_binning(int(n), int(cam.width), int(cam.height)))
+    return {1: "depth_first", 2: "scatter", 3: "direct"}[b]
+
+
 def get_option(name: str) -> int:
     """Current value of a gs_set_option option (gs_get_option)."""
     v = int(_lib.load().gs_get_option(name.encode()))
@@ -358,6 +365,12 @@ def _default_capacity(n: int, key) -> int:
     return max(1 << 16, 8 * n)
 
 
+def needed_capacity(meta) -> int:
+    """Intersection capacity a frame needs, from its meta words: the total,
+    or under direct binning tiles x the longest tile list if larger."""
+    return max(int(meta[1]), int(meta[2]))
+
+
 @dataclass
 class Frame:
     """One rendered view kept alive for its backward (cf. RenderResult,
@@ -383,16 +396,25 @@ class Frame:
         return v
 
     def meta(self) -> torch.Tensor:
+        """The device meta words: [0] status, [1] total intersections, [2]
+        capacity needed (direct binning: tiles x the longest list), [3] the
+        direct-binning tile stride (0: compact bins)."""
         v = self.view()
         off = v.meta - self.ws.data_ptr()
-        return self.ws[off:off + 16].view(torch.int64)
+        return self.ws[off:off + 32].view(torch.int64)
+
+    def _meta_host(self) -> tuple:
+        if self.meta_host is None:
+            self.meta_host = tuple(int(x) for x in self.meta().cpu())
+        return self.meta_host
 
     @property
     def n_isect(self) -> int:
-        if self.meta_host is None:
-            m = self.meta().cpu()
-            self.meta_host = (int(m[0]), int(m[1]))
-        return self.meta_host[1]
+        return self._meta_host()[1]
+
+    @property
+    def needed_capacity(self) -> int:
+        return needed_capacity(self._meta_host())
 
     def tensors(self) -> dict:
         """Device views of the frame's intermediates (for tests/adapters)."""
@@ -407,11 +429,24 @@ class Frame:
             return self.ws[off:off + count * esz].view(dtype).view(shape)
 
         m = min(self.n_isect, self.capacity)
+        ranges = sl(v.ranges2, 2 * nt, torch.int32, (nt, 2))
+        stride = self._meta_host()[3]
+        if stride > 0:  # direct binning: tile t's list at [t * stride, + count) -> compact (tile order)
+            cnt = (ranges[:, 1] - ranges[:, 0]).long()
+            src = torch.repeat_interleave(ranges[:, 0].long(), cnt)
+            pos = torch.arange(int(cnt.sum()), device=cnt.device) - torch.repeat_interleave(
+                torch.cumsum(cnt, 0) - cnt, cnt)
+            sorted_vals = sl(v.sorted_vals, self.capacity, torch.int32, (self.capacity,))[src + pos].contiguous()
+            sorted_tile_keys = torch.repeat_interleave(torch.arange(nt, device=cnt.device, dtype=torch.int32), cnt)
+            end = torch.cumsum(cnt, 0)
+            ranges = torch.stack([end - cnt, end], 1).to(torch.int32)
+            ranges[cnt == 0] = 0  # empty tiles: (0, 0), as the other binnings write them
+        else:
+            sorted_vals = sl(v.sorted_vals, m, torch.int32, (m,))
+            sorted_tile_keys = sl(v.sorted_tile_keys, m, torch.int32, (m,))
         return dict(xydr=sl(v.xydr4, 4 * n, torch.float32, (n, 4)), conic=sl(v.conic4, 4 * n, torch.float32, (n, 4)),
                     tiles=sl(v.tiles, n, torch.int32, (n,)), depth_order=sl(v.depth_order, n, torch.int32, (n,)),
-                    sorted_tile_keys=sl(v.sorted_tile_keys, m, torch.int32, (m,)),
-                    sorted_vals=sl(v.sorted_vals, m, torch.int32, (m,)),
-                    ranges=sl(v.ranges2, 2 * nt, torch.int32, (nt, 2)),
+                    sorted_tile_keys=sorted_tile_keys, sorted_vals=sorted_vals, ranges=ranges,
                     d_geo=sl(v.d_geo4 - 16, 8 * n, torch.float32, (n, 8))[:, 4:8],  # rows of [d_rgbo | d_geo]
                     d_c11=sl(v.d_c11, n, torch.float32, (n,)))
 
@@ -445,12 +480,11 @@ def frame_forward(means, scales, quats, opacities, colors, cam: CameraParams, ba
                    n_contrib, cnt)
         if not check_meta:
             return fr
-        m = fr.meta().cpu()
-        fr.meta_host = (int(m[0]), int(m[1]))
-        raise_status(fr.meta_host[0])
-        total = fr.meta_host[1]
-        _capacity_hint[key] = max(1 << 16, int(total * 1.25) + 1024)
-        if total <= cap:
+        m = fr._meta_host()
+        raise_status(m[0])
+        need = needed_capacity(m)
+        _capacity_hint[key] = max(1 << 16, int(need * 1.25) + 1024)
+        if need <= cap:
             return fr
         cap = _capacity_hint[key]
         ws = None

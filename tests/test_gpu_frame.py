@@ -50,9 +50,10 @@ def test_frame_equals_staged_on_golden(name, cuda):
         assert r["ok"], (name, k, r)
 
 
-@pytest.fixture(params=[(1, 1), (2, 1), (2, 0)], ids=["depth_first", "scatter", "scatter_sort_kernel"])
+@pytest.fixture(params=[(1, 1), (2, 1), (2, 0), (3, 1)],
+                ids=["depth_first", "scatter", "scatter_sort_kernel", "direct"])
 def binning(request, cuda):
-    """Run a test under both frame binning strategies (gs_set_option), the
+    """Run a test under every frame binning strategy (gs_set_option), the
     scatter one with its per-tile sort fused into the raster forward and as
     its own kernel."""
     from paper_2312_02121_b200 import ops
@@ -184,9 +185,9 @@ def test_forward_bitwise_deterministic(cuda):
 
 @pytest.mark.parametrize("config", [1, 2])
 def test_binning_strategies_agree_on_configs(config, cuda):
-    """Both binnings on BASELINE configs: config 2's lists run to thousands of
-    entries, so the scatter path's long-list CTA sort (len > 512) is covered
-    besides the one-warp sort."""
+    """All binnings on BASELINE configs: config 2's lists run to thousands of
+    entries, so the long-list CTA sort (len > 512) of the scatter and direct
+    paths is covered besides the shared-memory sort."""
     from paper_2312_02121_b200 import ops
     from paper_2312_02121_b200.scenes import make_config
     spec = make_config(config, n_views=1)
@@ -194,18 +195,20 @@ def test_binning_strategies_agree_on_configs(config, cuda):
     cam = ops.CameraParams.of(spec.cameras[0])
     got = {}
     try:
-        for mode in (1, 2):
+        for mode in (1, 2, 3):
             ops.set_option("binning", mode)
             fr = ops.frame_forward(*t, cam, (0.0, 0.0, 0.0), True)
             tv = fr.tensors()
             got[mode] = (tv["ranges"].clone(), tv["sorted_vals"].clone(), fr.image.clone())
+            del fr, tv
     finally:
         ops.set_option("binning", 0)
     lens = (got[1][0][:, 1] - got[1][0][:, 0])
     if config == 2:
         assert int(lens.max()) > 512
-    for a, b in zip(got[1], got[2]):
-        assert torch.equal(a, b)
+    for m in (2, 3):
+        for a, b in zip(got[1], got[m]):
+            assert torch.equal(a, b)
 
 
 def test_scatter_binning_ties_in_long_lists(cuda):
@@ -235,7 +238,7 @@ def test_scatter_binning_ties_in_long_lists(cuda):
     t = _tensors((means, scales, quats, opac, cols), cuda)
     got = {}
     try:
-        for mode in (1, 2):
+        for mode in (1, 2, 3):
             ops.set_option("binning", mode)
             fr = ops.frame_forward(*t, cam, (0.0, 0.0, 0.0), True)
             tv = fr.tensors()
@@ -244,5 +247,33 @@ def test_scatter_binning_ties_in_long_lists(cuda):
         ops.set_option("binning", 0)
     lens = got[1][0][:, 1] - got[1][0][:, 0]
     assert int(lens.max()) > 512 and bool(((lens > 1) & (lens <= 512)).any())
-    for a, b in zip(got[1], got[2]):
-        assert torch.equal(a, b)
+    for m in (2, 3):
+        for a, b in zip(got[1], got[m]):
+            assert torch.equal(a, b)
+
+
+def test_direct_binning_tile_overflow_reruns(cuda):
+    """Direct binning gives every tile capacity / tiles slots: a capacity
+    above the total but below tiles x the longest list must report the
+    capacity it needs (meta[2]) and re-run to the same frame."""
+    from paper_2312_02121_b200 import ops
+    g = load_golden("cfg0_mini")
+    t = _tensors(g["inputs"], cuda)
+    cp = ops.CameraParams.of(g["camera"])
+    ops.set_option("binning", 3)
+    try:
+        full = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True)
+        tv = full.tensors()
+        lens = tv["ranges"][:, 1] - tv["ranges"][:, 0]
+        nt = lens.numel()
+        need = nt * int(lens.max())
+        assert full.needed_capacity == need > full.n_isect  # uneven lists
+        raw = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True, capacity=need - 1, check_meta=False)
+        m = raw.meta().cpu()
+        assert int(m[0]) == -1 and int(m[1]) == full.n_isect and int(m[2]) == need
+        small = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True, capacity=full.n_isect + 1)  # re-runs
+        assert small.capacity >= need
+        assert torch.equal(small.image, full.image)
+        assert torch.equal(small.tensors()["sorted_vals"], tv["sorted_vals"])
+    finally:
+        ops.set_option("binning", 0)

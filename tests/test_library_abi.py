@@ -42,7 +42,7 @@ def test_host_only_entry_points():
 
 def test_set_option():
     from paper_2312_02121_b200 import _lib, ops
-    for v in (1, 2, 0):
+    for v in (1, 2, 3, 0):
         ops.set_option("binning", v)
         assert ops.get_option("binning") == v
     for v in (0, 1):
@@ -50,6 +50,10 @@ def test_set_option():
         assert ops.get_option("fuse_sort") == v
     with pytest.raises(_lib.SplatLibError, match="binning"):
         ops.set_option("binning", 7)
+    L = _lib.load()
+    assert L.gs_frame_binning(100000, 800, 800) == 3  # auto: direct (2500 tiles)
+    assert L.gs_frame_binning(100000, 1920, 1080) == 2  # 8160 tiles: scatter
+    assert L.gs_frame_binning(1000000, 800, 800) == 1  # large scene: depth-first
     with pytest.raises(_lib.SplatLibError, match="fuse_sort"):
         ops.set_option("fuse_sort", 2)
     with pytest.raises(_lib.SplatLibError, match="unknown option"):
