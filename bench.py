@@ -186,6 +186,7 @@ def run_ours(args):
 
     from paper_2312_02121_b200 import _lib, ops
     from paper_2312_02121_b200 import engine as E
+    from paper_2312_02121_b200 import ops
     from paper_2312_02121_b200.scenes import config_sizes, make_config
 
     world, rank, local = dist_env()
@@ -500,6 +501,7 @@ def run_e2e(args, spec, views, dev, world, frames):
     import torch.distributed as dist
 
     from paper_2312_02121_b200 import engine as E
+    from paper_2312_02121_b200 import ops
 
     host = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in
             (spec.means, spec.scales, spec.quats, spec.opacities, spec.colors)]
@@ -525,7 +527,8 @@ def run_e2e(args, spec, views, dev, world, frames):
     total = e0.elapsed_time(e1)
     for b, mh in enumerate(metas):
         eng.result(b, mh)  # raises on a status error; capacity was sized by a checked frame
-        assert all(int(t) <= c for (_, t), c in zip(mh.tolist(), eng.caps)), "capacity overflow in timed e2e run"
+        assert all(ops.needed_capacity(row) <= c for row, c in zip(mh.tolist(), eng.caps)), \
+            "capacity overflow in timed e2e run"
     if world > 1:
         tt = torch.tensor([total], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)

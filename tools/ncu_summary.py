@@ -20,7 +20,7 @@ import subprocess
 import sys
 from collections import defaultdict
 
-STAGE_OF = [  # kernel-name regex -> bench stage name (first capture of each kernel wins)
+STAGE_OF = [  # kernel-name regex -> bench stage name (the last capture of each kernel wins)
     (r"project_fwd_kernel", "project"),
     (r"onesweep_kernel<unsigned int, (16|4)", "sort_u32"),
     (r"emit_scan_kernel", "scan_emit"),
@@ -110,7 +110,7 @@ def full(rep, out, traffic_out=None):
         nm = names.get(kid, short(d.get("Kernel Name", "")))
         for pat, stage in STAGE_OF:
             if re.search(pat, d.get("Kernel Name", "")):
-                traffic.setdefault(stage, (rd + wr) * scale)
+                traffic[stage] = (rd + wr) * scale  # the last capture wins (warmed-up frame)
     lines = []
     for kid in sorted(per, key=lambda x: int(x)):
         lines.append(f"[{kid}] {names.get(kid, '?')}")

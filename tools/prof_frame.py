@@ -18,7 +18,7 @@ m, s, q, o, c = t(spec.means), t(spec.scales), t(spec.quats), t(spec.opacities),
 cam = ops.CameraParams.of(spec.cameras[0])
 d_image = torch.ones((cam.height, cam.width, 3), device=dev)
 fr = ops.frame_forward(m, s, q, o, c, cam, (0.0, 0.0, 0.0), True)
-cap = int(fr.n_isect * 1.05) + 4096
+cap = int(fr.needed_capacity * 1.05) + 4096
 for _ in range(reps):
     fr = ops.frame_forward(m, s, q, o, c, cam, (0.0, 0.0, 0.0), True, capacity=cap)
     g = ops.frame_backward(fr, m, s, q, c, d_image)
