@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--streams", type=int, default=2, help="streams the views of a multi-view step alternate on")
     return p.parse_args()
 
 
@@ -262,13 +263,35 @@ def run_ours(args):
         # only the pair bracketing the raster backward (the roofline
         # kernel); the per-stage breakdown comes from a second, fully
         # instrumented graph replayed after the timed region.
+        # Several views: the views go round-robin over args.streams streams, each with
+        # its own workspace; a view's backward waits for the previous view's
+        # (the gradient sums keep the sequential order), so one view's
+        # forward overlaps the previous view's backward.
+        ns = min(args.streams, len(cams)) if not staged else 1
+        two = ns > 1
+        main = torch.cuda.current_stream()
+        sts = [main] + aux[:ns - 1]
+        for a in sts[1:]:
+            a.wait_stream(main)
+        bwd_done = None
         for vi, (cam, d_img) in enumerate(zip(cams, d_imgs)):
-            fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, capacity=caps[vi], check_meta=False, ws=wss[vi],
-                                   events=ev_f[vi] if staged else None)
-            ops.frame_backward(fr, m, s, q, c, d_img, events=ev_b[vi] if staged else [ev_t[vi][0], ev_t[vi][1], None],
-                               out=grad_out, accumulate=vi > 0)
+            st = sts[vi % ns]
+            with torch.cuda.stream(st):
+                fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, capacity=caps[vi], check_meta=False,
+                                       ws=wss[vi], events=ev_f[vi] if staged else None)
+                if bwd_done is not None:
+                    st.wait_event(bwd_done)
+                ops.frame_backward(fr, m, s, q, c, d_img,
+                                   events=ev_b[vi] if staged else [ev_t[vi][0], ev_t[vi][1], None],
+                                   out=grad_out, accumulate=vi > 0)
+                if two:
+                    bwd_done = torch.cuda.Event()
+                    bwd_done.record(st)
             frames_out[vi] = fr
+        for a in sts[1:]:
+            main.wait_stream(a)
 
+    aux = [torch.cuda.Stream() for _ in range(max(args.streams - 1, 0))]
     graph = graph_staged = None
     if not args.no_graph:
         side = torch.cuda.Stream()
@@ -460,7 +483,7 @@ def run_ours(args):
                    "views_per_step": frames_per_step, "views_per_rank": len(cams),
                    "early_termination": True, "background": "black",
                    "parallelism": (f"tile-row bands x{world} (rows {band})" if band else f"view-sharded x{world}") + (" + NCCL allreduce 14 fp32/Gaussian" if world > 1 else ""),
-                   "cuda_graph": graph is not None,
+                   "cuda_graph": graph is not None, "view_streams": min(args.streams, len(cams)),
                    "l2": "flushed between timed steps (192 MiB write, untimed)"},
         "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
         "intersections_per_step_rank": int(I),

@@ -778,7 +778,14 @@ __device__ __forceinline__ void bwd_flush(uint32_t red, int nslot, int lane, flo
     }
 }
 
-__global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
+#ifndef GS_BWD_MINB
+#define GS_BWD_MINB 8
+#endif
+#ifndef GS_BWD_UNROLL
+#define GS_BWD_UNROLL 1
+#endif
+constexpr int BWD_UNROLL = GS_BWD_UNROLL;
+__global__ void __launch_bounds__(128, GS_BWD_MINB) raster_bwd_rec_kernel(
     const uint2* __restrict__ ranges, const uint2* __restrict__ rec, const uint32_t* __restrict__ rec_count,
     const float4* __restrict__ xydr, const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg,
     int W, int H, int tiles_x, const float* __restrict__ final_T, const int* __restrict__ n_contrib,
@@ -828,7 +835,7 @@ __global__ void __launch_bounds__(128, 8) raster_bwd_rec_kernel(
             st.c = make_float4(colors[3 * r.x + 2], __int_as_float((int)r.y), __int_as_float((int)r.x), 0.f);
         }
         __syncwarp();
-#pragma unroll 1
+#pragma unroll BWD_UNROLL
         for (int k = nb - 1; k >= 0; --k) {
             const uint32_t sk = stage_w + (uint32_t)k * REC_BYTES;
             const float4 cq = lds_f4(sk + 32);

@@ -60,6 +60,7 @@ class RenderStep:
                 graph=None))
         self.caps = None
         self.wss = None
+        self.aux = torch.cuda.Stream(self.dev)  # second view stream (multi-view steps)
 
     # -------------------------------------------------------------- set-up
     def _size(self, k: int):
@@ -76,14 +77,32 @@ class RenderStep:
                                         device=self.dev, dtype=torch.uint8))
 
     def _body(self, k: int):
+        """All views of one step.  Several views alternate between two
+        streams (each view has its own workspace); a view's backward waits
+        for the previous view's, so the gradient sums keep the sequential
+        order while one view's forward overlaps the previous backward."""
         s = self.sets[k]
         m, sc, q, o, c = s["params"]
         out = unpack(s["grads"], self.n)
+        main = torch.cuda.current_stream(self.dev)
+        sts = [main] + ([self.aux] if len(self.cams) > 1 else [])
+        for a in sts[1:]:
+            a.wait_stream(main)
+        bwd_done = None
         for vi, (cam, d) in enumerate(zip(self.cams, s["d_images"])):
-            fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et, capacity=self.caps[vi], check_meta=False,
-                                   ws=self.wss[vi])
-            ops.frame_backward(fr, m, sc, q, c, d, out=out, accumulate=vi > 0)
-            s["meta"][vi].copy_(fr.meta())
+            st = sts[vi % len(sts)]
+            with torch.cuda.stream(st):
+                fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et, capacity=self.caps[vi],
+                                       check_meta=False, ws=self.wss[vi])
+                if bwd_done is not None:
+                    st.wait_event(bwd_done)
+                ops.frame_backward(fr, m, sc, q, c, d, out=out, accumulate=vi > 0)
+                s["meta"][vi].copy_(fr.meta())
+                if len(sts) > 1:
+                    bwd_done = torch.cuda.Event()
+                    bwd_done.record(st)
+        for a in sts[1:]:
+            main.wait_stream(a)
 
     def _capture(self):
         side = torch.cuda.Stream(self.dev)

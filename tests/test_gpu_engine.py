@@ -95,3 +95,28 @@ def test_multi_view_accumulation(cuda):
     eng = E.RenderStep(len(params[0]), [cam, cam2], device=cuda)
     eng.prime(params, [d1, d2])
     _close(eng.step(params, [d1, d2]), ref)
+
+
+def test_multi_view_step_sums_views(cuda):
+    """Three views on two streams (engine._body): the step's gradients are
+    the sum of the per-call frames' gradients, every view's meta is read."""
+    from paper_2312_02121_b200 import engine as E, ops
+    g = load_golden("config0")
+    params = [torch.as_tensor(np.asarray(a, np.float32), device=cuda) for a in g["inputs"]]
+    cam0 = ops.CameraParams.of(g["camera"])
+    cams = []
+    for k, ang in enumerate((0.0, 0.15, -0.2)):
+        c, s_ = np.cos(ang), np.sin(ang)
+        view = np.array(cam0.view, np.float64)
+        view[:3, :3] = np.array([[c, 0.0, s_], [0.0, 1.0, 0.0], [-s_, 0.0, c]]) @ view[:3, :3]
+        cams.append(ops.CameraParams(view.tolist(), cam0.fx, cam0.fy, cam0.cx, cam0.cy, cam0.width, cam0.height,
+                                     cam0.near, cam0.far))
+    rng = np.random.default_rng(1)
+    d_imgs = [torch.as_tensor(rng.normal(size=(cam0.height, cam0.width, 3)).astype(np.float32), device=cuda)
+              for _ in cams]
+    ref = sum(_per_call(ops, params, c, d) for c, d in zip(cams, d_imgs))
+    eng = E.RenderStep(len(params[0]), cams, device=cuda)
+    eng.prime(params, d_imgs)
+    _close(eng.step(params, d_imgs), ref)
+    m = eng.meta(0).cpu()
+    assert m.shape == (3, 4) and bool((m[:, 0] == -1).all()) and bool((m[:, 1] > 0).all())
