@@ -23,6 +23,8 @@ buffer set and replays it:
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib, ops
@@ -126,12 +128,20 @@ class RenderStep:
 
     # ------------------------------------------------------------- stepping
     def load(self, k: int, params, d_images, stream=None):
-        """Copy (non-blocking from pinned host, or device) into buffer set k."""
+        """Copy (non-blocking from pinned host, or device) into buffer set k.
+        stream: one stream, or a list of streams the copies are split over
+        in chunks (several DMA streams in flight: on some hosts one stream
+        gets well under the link's host-to-device bandwidth)."""
         s = self.sets[k]
-        with torch.cuda.stream(stream or torch.cuda.current_stream(self.dev)):
-            for dst, src in zip(s["params"], params):
-                dst.copy_(src.reshape(dst.shape), non_blocking=True)
-            for dst, src in zip(s["d_images"], d_images):
+        streams = stream if isinstance(stream, (list, tuple)) else [stream or torch.cuda.current_stream(self.dev)]
+        pairs = [(dst.view(-1), src.reshape(-1)) for dst, src in zip(s["params"], params)]
+        pairs += [(dst.view(-1), src.reshape(-1)) for dst, src in zip(s["d_images"], d_images)]
+        chunks = []
+        for dst, src in pairs:
+            parts = max(1, min(len(streams), dst.numel() * 4 // (1 << 20)))  # >= 1 MiB per chunk
+            chunks += list(zip(dst.chunk(parts), src.chunk(parts)))
+        for i, (dst, src) in enumerate(chunks):
+            with torch.cuda.stream(streams[i % len(streams)]):
                 dst.copy_(src, non_blocking=True)
 
     def replay(self, k: int):
@@ -164,6 +174,13 @@ class RenderStep:
         return self.result(0)
 
 
+# host->device copy streams of pipeline.  A slow host measured 16.5 GB/s on one
+# stream and 28 GB/s over 8 in isolation (tools/pcie_bw.py), but the
+# pipelined e2e rate did not follow (noisy, 1.2-2.0 k frames/s either way), so
+# the default stays 1; GS_H2D_STREAMS=k splits the copies over k streams.
+H2D_STREAMS = int(os.environ.get("GS_H2D_STREAMS", "1"))
+
+
 def pipeline(engine: RenderStep, host_params, host_d_images, out_host, steps: int, allreduce=None, flush=None):
     """`steps` end-to-end steps with double buffering: the H2D copies of step
     k+1 and the D2H read of step k-1 overlap the replay of step k (copy
@@ -174,7 +191,7 @@ def pipeline(engine: RenderStep, host_params, host_d_images, out_host, steps: in
     RenderStep.result().  The caller synchronizes."""
     dev = engine.dev
     comp = torch.cuda.current_stream(dev)
-    h2d = torch.cuda.Stream(dev)
+    h2d = [torch.cuda.Stream(dev) for _ in range(H2D_STREAMS)]
     d2h = torch.cuda.Stream(dev)
     nb = engine.nbuf
     loaded = [torch.cuda.Event() for _ in range(nb)]
@@ -185,9 +202,12 @@ def pipeline(engine: RenderStep, host_params, host_d_images, out_host, steps: in
         e.record(comp)
     for k in range(steps):
         b = k % nb
-        h2d.wait_event(done[b])  # the replay that last read set b finished
+        for st in h2d:
+            st.wait_event(done[b])  # the replay that last read set b finished
         engine.load(b, host_params, host_d_images, stream=h2d)
-        loaded[b].record(h2d)
+        for st in h2d[1:]:
+            h2d[0].wait_stream(st)
+        loaded[b].record(h2d[0])
         if flush is not None:
             flush.zero_()  # benchmarking: evict L2 (workspace comes from HBM); overlaps this step's H2D
         comp.wait_event(loaded[b])
