@@ -214,9 +214,10 @@ __device__ __forceinline__ void fwd_commit(FwdPair& p, f32x2 SG, bool vis0, bool
 // Per entry one byte goes to the warp's shared buffer; the batch's records
 // are written out coalesced when the warp leaves the batch.
 // rcur: the warp's shared cursor (32-bit shared address of its next byte in
-// rbuf), so a record costs one predicated STS.U8 and one add.
-__device__ __forceinline__ void fwd_record(uint32_t& rcur, int lane, int k) {
-    if (lane == 0) asm volatile("st.shared.u8 [%0], %1;" ::"r"(rcur), "r"(k) : "memory");
+// rbuf), so a record costs one STS.U8 and one add (every lane stores the
+// same byte to the same address: no lane test).
+__device__ __forceinline__ void fwd_record(uint32_t& rcur, int k) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(rcur), "r"(k) : "memory");
     ++rcur;
 }
 template <int NWR>
@@ -331,14 +332,14 @@ __device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uin
                 if (COUNT) e_s += (unsigned)v00 + (unsigned)v01;
                 if (b0m) {
                     fwd_commit<ET, COUNT>(p[0], SG0, v00, v01, s.e[k0].b, s.e[k0].c.x, pos_base + k0, e_a, e_c);
-                    if (REC) fwd_record(rcur, lane, k0);
+                    if (REC) fwd_record(rcur, k0);
                 }
                 v10 = v10 && !(p[0].done & 1u);  // retired at k0
                 v11 = v11 && !(p[0].done & 2u);
                 if (COUNT) e_s += (unsigned)v10 + (unsigned)v11;
                 if (b1m) {  // never the sentinel (its sigma is NaN)
                     fwd_commit<ET, COUNT>(p[0], SG1, v10, v11, s.e[k1].b, s.e[k1].c.x, pos_base + k1, e_a, e_c);
-                    if (REC) fwd_record(rcur, lane, k1);
+                    if (REC) fwd_record(rcur, k1);
                 }
                 if (ET && (b0m | b1m) && __all_sync(0xffffffffu, p[0].done == 3u)) break;
             }
