@@ -409,9 +409,11 @@ def run_ours(args):
     direct = binning == "direct"
     fused = fused_sort(n, cams[0])
     work = {
-        # read 44 B, write xydr 16 + conic 16 + tiles 4 + depth key 4; direct binning: + a slot
-        # atomic and the Gaussian id per intersection (8 B)
-        "project": ("hbm", 84.0 * n * nv + (8.0 * I if direct else 0.0)),
+        # read 44 B, write xydr 16 + conic 16 + tiles 4 + depth key 4, and zero the backward's
+        # screen-space gradient accumulators (rows of 8 floats + d_c11: 36 B) the projection
+        # kernel clears for the frame; direct binning: + a slot atomic and the Gaussian id per
+        # intersection (8 B)
+        "project": ("hbm", 120.0 * n * nv + (8.0 * I if direct else 0.0)),
         # depth-first: 4 passes x (key+value) x (read+write); scatter / direct: no global depth sort
         "depth_sort": ("none", 0.0) if seg else ("hbm", 4 * 16.0 * n * nv),
         # depth-first: fused scan + emission, (order +) count + xydr gather per Gaussian, pairs out;

@@ -37,7 +37,10 @@ __device__ __forceinline__ void report(unsigned long long* status, int i, int co
 #define DIRECT_UNROLL 4  // slot atomics in flight per lane (direct binning)
 #endif
 template <int MODE>
-__global__ void __launch_bounds__(256) project_fwd_kernel(
+#ifndef PFWD_MINB
+#define PFWD_MINB 8  // 32 registers, 8 resident CTAs per SM (config 4 projection 165 -> 160 us)
+#endif
+__global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
     const float* __restrict__ opac, int n, CamK cam, float4* __restrict__ xydr, float4* __restrict__ conic,
     uint32_t* __restrict__ tiles, float* __restrict__ cov_out, unsigned long long* __restrict__ status,
@@ -184,7 +187,10 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
 constexpr int PBWD_THREADS = 256;
 
 // Per-Gaussian loop body of sg/proj_backward.py:200-222.
-__global__ void __launch_bounds__(PBWD_THREADS) project_bwd_kernel(
+#ifndef PBWD_MINB
+#define PBWD_MINB 4  // 64 registers: 4 CTAs per SM (config 4: 264 -> 239 us)
+#endif
+__global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
     int n, CamK cam, const uint32_t* __restrict__ tiles, const float4* __restrict__ d_geo,
     const float* __restrict__ d_c11, float* __restrict__ d_means, float* __restrict__ d_scales,
@@ -448,7 +454,7 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
     if (check_launch("frame_init_kernel")) return -1;
     int64_t blocks = (n + 255) / 256;
     if (blocks < 1) blocks = 1;  // the zero jobs run even for an empty scene
-    const int64_t cap = (int64_t)sort_sm_count() * 6;  // resident CTAs (40 regs, 256 threads)
+    const int64_t cap = (int64_t)sort_sm_count() * PFWD_MINB;  // resident CTAs of 256 threads
     if (blocks > cap) blocks = cap;
     if (tcount && bins)
         launch_k(project_fwd_kernel<3>, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
