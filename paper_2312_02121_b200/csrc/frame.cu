@@ -332,9 +332,8 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
     } else if (launch_raster_bwd_rec(at<uint2>(ws, L.ranges), at<uint2>(ws, L.rec), at<uint32_t>(ws, L.rec_count),
                                      at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3, bg, W, H, final_T,
                                      n_contrib, d_image, g8, at<float>(ws, L.d_c11), s,
-                                     binning_for(n, tiles_x * tiles_y) != DIRECT && tile_order_enabled(tiles_x * tiles_y)
-                                         ? at<uint32_t>(ws, L.tile_order)
-                                         : nullptr)) {
+                                     tile_order_enabled(tiles_x * tiles_y) ? at<uint32_t>(ws, L.tile_order) : nullptr,
+                                     at<unsigned long long>(ws, L.meta))) {
         return -1;
     }
     mark(stage_events, 1, s);

@@ -84,7 +84,7 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
 int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
                           const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s,
-                          const uint32_t* tile_order = nullptr);
+                          const uint32_t* tile_order = nullptr, const unsigned long long* meta = nullptr);
 int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, const float* fT, const int* nc,
                       const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11, unsigned long long* counts,

@@ -791,11 +791,12 @@ __global__ void __launch_bounds__(128, GS_BWD_MINB) raster_bwd_rec_kernel(
     const float4* __restrict__ xydr, const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg,
     int W, int H, int tiles_x, const float* __restrict__ final_T, const int* __restrict__ n_contrib,
     const float* __restrict__ d_img, float* __restrict__ g8, float* __restrict__ d_c11,
-    const uint32_t* __restrict__ tile_order) {
+    const uint32_t* __restrict__ tile_order, const unsigned long long* __restrict__ meta) {
     griddep_wait();
     __shared__ RecStage s_rec[4][32];
     __shared__ __align__(16) float s_red[4][RBS][9][RROW];
-    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
+    // the forward's raster order exists unless it binned directly (meta[3] = bin stride)
+    const int tile = tile_order && meta[3] == 0 ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int col = tx * TILE + (warp & 1) * 8 + (lane & 7);
@@ -986,11 +987,12 @@ int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xy
 int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
                           const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s,
-                          const uint32_t* tile_order) {
+                          const uint32_t* tile_order, const unsigned long long* meta) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
+    if (tile_order && !meta) return set_error("raster_bwd_rec: a raster order needs the frame meta");
     launch_k(raster_bwd_rec_kernel, dim3((unsigned)(tiles_x * tiles_y)), dim3(128), 0, s, ranges, rec, rec_count,
              (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H, tiles_x, fT, nc, dimg, g8, d_c11,
-             tile_order);
+             tile_order, meta);
     return check_launch("raster_bwd_rec_kernel");
 }
 

@@ -277,3 +277,26 @@ def test_direct_binning_tile_overflow_reruns(cuda):
         assert torch.equal(small.tensors()["sorted_vals"], tv["sorted_vals"])
     finally:
         ops.set_option("binning", 0)
+
+
+def test_option_change_between_forward_and_backward(cuda):
+    """The backward follows what its forward did (the raster order exists
+    only for compact bins: meta[3]), not the options at backward time."""
+    from paper_2312_02121_b200 import ops
+    from paper_2312_02121_b200.scenes import make_config
+    spec = make_config(1, n_views=1)  # 2500 tiles: more than one raster wave, so a raster order is used
+    t = _tensors((spec.means, spec.scales, spec.quats, spec.opacities, spec.colors), cuda)
+    cam = ops.CameraParams.of(spec.cameras[0])
+    d = torch.as_tensor(np.asarray(spec.d_images[0], np.float32), device=cuda)
+    ref = ops.frame_backward(ops.frame_forward(*t, cam, (0.0, 0.0, 0.0), True), t[0], t[1], t[2], t[4], d)
+    try:
+        for fwd_mode, bwd_mode in ((3, 2), (2, 3)):
+            ops.set_option("binning", fwd_mode)
+            fr = ops.frame_forward(*t, cam, (0.0, 0.0, 0.0), True)
+            ops.set_option("binning", bwd_mode)
+            g = ops.frame_backward(fr, t[0], t[1], t[2], t[4], d)
+            for k in GRAD_CLASSES:
+                r = grad_gate(g[k].cpu().numpy(), ref[k].cpu().numpy(), rel=1e-3, floor=1e-2)
+                assert r["ok"], (fwd_mode, bwd_mode, k, r)
+    finally:
+        ops.set_option("binning", 0)
