@@ -192,6 +192,12 @@ __device__ __forceinline__ void tile_rect(float mx, float my, int r, int tiles_x
 // the hot tiles' atomics spread over several L2 lines.
 constexpr int TCOUNT_REPL = 8;
 __device__ __forceinline__ uint32_t tcount_replica(uint32_t g) { return (g >> 5) & (TCOUNT_REPL - 1); }
+// direct binning: slot-counter replicas per tile (<= TCOUNT_REPL), chosen per warp of Gaussians
+#ifndef DIRECT_REPL
+#define DIRECT_REPL 8
+#endif
+constexpr int DREPL = DIRECT_REPL;
+__device__ __forceinline__ uint32_t direct_replica(uint32_t g) { return (g >> 5) & (DREPL - 1); }
 
 // Per entry f(tile, gaussian); UNROLL entries per lane per step (independent
 // atomics in flight).

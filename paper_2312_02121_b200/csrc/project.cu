@@ -30,9 +30,10 @@ __device__ __forceinline__ void report(unsigned long long* status, int i, int co
 // that follows (sort.cu), in shared memory; MODE 2 (scatter binning) counts
 // every tile's intersections instead (tcount, one red.add per pair); MODE 3
 // (direct binning) takes a slot in the tile's fixed-stride bin for every
-// pair (atomicAdd on tcount[tile] with return, 4 in flight per lane) and
-// writes the Gaussian id there: bins[tile * kstride + slot] (slots past
-// kstride are dropped; the raster forward reports the overflow).
+// pair (atomicAdd with return on one of the tile's DREPL counters, 4
+// in flight per lane) and writes the Gaussian id there:
+// bins[tile * kstride + replica * kr + slot], kr = kstride / DREPL
+// (slots past kr are dropped; the raster forward reports the overflow).
 #ifndef DIRECT_UNROLL
 #define DIRECT_UNROLL 4  // slot atomics in flight per lane (direct binning)
 #endif
@@ -149,15 +150,21 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
     }
     }  // i < n
     if (MODE == 3) {
+        // replica r of every tile: counter tcount[r * tiles + tile], slots
+        // [r * kr, (r + 1) * kr) of the tile's bin (a warp's Gaussians share
+        // r; spreading the slot atomics over DREPL addresses per tile
+        // cuts their same-address serialisation in L2)
+        const uint32_t r = direct_replica((uint32_t)i), kr = kstride / DREPL;
+        uint32_t* tc = tcount + (size_t)r * (cam.tiles_x * cam.tiles_y);
         walk_tile_rects<DIRECT_UNROLL>(threadIdx.x & 31, (uint32_t)i, tx0, tx1, ty0, ty1, cam.tiles_x,
                            [&](const uint32_t* tl, const uint32_t* gl) {
                                uint32_t slot[DIRECT_UNROLL];
 #pragma unroll
                                for (int u = 0; u < DIRECT_UNROLL; ++u)
-                                   slot[u] = tl[u] != 0xFFFFFFFFu ? atomicAdd(&tcount[tl[u]], 1u) : kstride;
+                                   slot[u] = tl[u] != 0xFFFFFFFFu ? atomicAdd(&tc[tl[u]], 1u) : kr;
 #pragma unroll
                                for (int u = 0; u < DIRECT_UNROLL; ++u)
-                                   if (slot[u] < kstride) bins[(size_t)tl[u] * kstride + slot[u]] = gl[u];
+                                   if (slot[u] < kr) bins[(size_t)tl[u] * kstride + r * kr + slot[u]] = gl[u];
                            });
     }
     if (MODE == 2) {

@@ -251,7 +251,13 @@ struct FwdShared<NWR, true> {
     };
 };
 
-// Out of line, so the sort's register allocation stays out of the raster loop's.
+// Out of line, so the sorts' register allocation stays out of the raster loop's.
+static __device__ __noinline__ void fwd_sort_segments(SegsortShared& sh, uint32_t base, uint32_t kr,
+                                                      const uint32_t (&cnt)[DREPL],
+                                                      const uint32_t* __restrict__ dkeys, uint32_t* vals,
+                                                      uint32_t* __restrict__ alt) {
+    segsort_tile_segments<DREPL>(sh, base, kr, cnt, dkeys, vals, alt);
+}
 static __device__ __noinline__ void fwd_sort_tile(SegsortShared& sh, uint2 rg, const uint32_t* __restrict__ dkeys,
                                                   uint32_t* vals, uint32_t* __restrict__ alt) {
     segsort_tile(sh, rg, dkeys, vals, alt);
@@ -439,8 +445,9 @@ __device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uin
 // of its own.  Direct binning (direct_counts != nullptr): the tile's list is
 // bins[tile * kstride, + count) as the projection left it; the CTA writes
 // the tile's range, adds its count to meta[1] (total intersections) and
-// raises meta[2] (capacity needed = tiles * the longest list); a list over
-// kstride is not rastered (the caller re-runs with a larger capacity).
+// raises meta[2] (capacity needed = tiles * DREPL * the longest replica
+// segment); a segment over kstride / DREPL leaves the tile
+// unrastered (the caller re-runs with a larger capacity).
 // meta[3] = kstride tells readers of the bins that they are strided.
 template <int NWR, bool ET, bool COUNT, bool REC, int MINB = (NWR == 4 ? 10 : 16), bool SORT = false>
 __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(
@@ -454,22 +461,34 @@ __global__ void __launch_bounds__(32 * NWR, MINB) raster_fwd_kernel(
     __shared__ FwdShared<NWR, SORT> sh;
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     uint2 rg;
-    if (SORT && direct_counts) {
-        const uint32_t c = direct_counts[tile];
-        const uint32_t b = (uint32_t)tile * kstride;
-        rg = c <= kstride ? make_uint2(b, b + c) : make_uint2(b, b);
+    if constexpr (SORT) {
+      if (direct_counts) {
+        // the tile's DREPL replica segments (project.cu MODE 3)
+        const uint32_t kr = kstride / DREPL, b = (uint32_t)tile * kstride;
+        uint32_t cnt[DREPL], c = 0, mx = 0;
+#pragma unroll
+        for (int r = 0; r < DREPL; ++r) {
+            cnt[r] = direct_counts[(size_t)r * gridDim.x + tile];
+            c += cnt[r];
+            mx = max(mx, cnt[r]);
+        }
+        rg = mx <= kr ? make_uint2(b, b + c) : make_uint2(b, b);
         if (threadIdx.x == 0) {
             if (blockIdx.x == 0) meta[3] = kstride;
             const_cast<uint2*>(ranges)[tile] = rg;
             if (c) {
                 atomicAdd(&meta[1], (unsigned long long)c);
-                atomicMax(&meta[2], (unsigned long long)c * (unsigned long long)(gridDim.x));
+                atomicMax(&meta[2], (unsigned long long)mx * DREPL * (unsigned long long)(gridDim.x));
             }
         }
+        if (mx <= kr) fwd_sort_segments(sh.srt, b, kr, cnt, dkeys, const_cast<uint32_t*>(sorted_vals), sort_alt);
+      } else {
+        rg = ranges[tile];
+        fwd_sort_tile(sh.srt, rg, dkeys, const_cast<uint32_t*>(sorted_vals), sort_alt);
+      }
     } else {
         rg = ranges[tile];
     }
-    if constexpr (SORT) fwd_sort_tile(sh.srt, rg, dkeys, const_cast<uint32_t*>(sorted_vals), sort_alt);
     raster_fwd_body<NWR, ET, COUNT, REC>(sh.b, tile, rg, sorted_vals, xydr, conic, colors, bg, W, H, tiles_x,
                                          out_img, out_T, out_nc, counts, rec, rec_count, tile_order);
 }

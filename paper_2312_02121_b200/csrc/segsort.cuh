@@ -48,8 +48,11 @@ struct SmallShared {
     uint32_t tie;
 };
 
+// load(idx): the input value at list position idx (all loads happen before
+// any write to gv, so the input may live inside gv's range).
+template <typename Load>
 __device__ __forceinline__ void small_sort(SmallShared& sh, const uint32_t* __restrict__ dkeys, uint32_t* gv,
-                                           int len) {
+                                           int len, Load load) {
     auto& s_peers = sh.peers;
     auto& s_whist = sh.whist;
     auto& s_key = sh.key;
@@ -68,7 +71,7 @@ __device__ __forceinline__ void small_sort(SmallShared& sh, const uint32_t* __re
         s_tie = 0u;
     }
 #pragma unroll
-    for (int i = 0; i < WS_ITEMS; ++i) v[i] = ibase + 32 * i < len ? gv[ibase + 32 * i] : 0u;
+    for (int i = 0; i < WS_ITEMS; ++i) v[i] = ibase + 32 * i < len ? load(ibase + 32 * i) : 0u;
     uint32_t ko = 0u, ka = ~0u, vo = 0u, va = ~0u;
 #pragma unroll
     for (int i = 0; i < WS_ITEMS; ++i) {
@@ -343,7 +346,7 @@ __device__ __forceinline__ void segsort_tile(SegsortShared& sh, uint2 rg, const 
     if (len <= 1) return;
     uint32_t* seg = vals + rg.x;
     if (len <= WS_MAX) {
-        small_sort(sh.small, dkeys, seg, len);
+        small_sort(sh.small, dkeys, seg, len, [&](int i) { return seg[i]; });
         __syncthreads();
         return;
     }
@@ -359,6 +362,47 @@ __device__ __forceinline__ void segsort_tile(SegsortShared& sh, uint2 rg, const 
         cta_radix(sh.large, dkeys, seg, alt + rg.x, len, true);
         cta_radix(sh.large, dkeys, seg, alt + rg.x, len, false);
     }
+}
+
+// Direct binning with replicated slot counters: the tile's list is NR
+// segments, segment j at vals[base + j * kr, + cnt[j]).  Sorted by
+// (depth, index) into vals[base, + sum cnt) (the NR segments are gathered
+// first; the first segment's data is already in place).
+template <int NR>
+__device__ __forceinline__ void segsort_tile_segments(SegsortShared& sh, uint32_t base, uint32_t kr,
+                                                      const uint32_t (&cnt)[NR],
+                                                      const uint32_t* __restrict__ dkeys,
+                                                      uint32_t* __restrict__ vals, uint32_t* __restrict__ alt) {
+    uint32_t pre[NR + 1];
+    pre[0] = 0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) pre[j + 1] = pre[j] + cnt[j];
+    const int len = (int)pre[NR];
+    uint32_t* seg = vals + base;
+    auto load = [&](int i) {  // list position -> segment value
+        int j = 0;
+#pragma unroll
+        for (int q = 1; q < NR; ++q) j += (uint32_t)i >= pre[q] ? 1 : 0;
+        return seg[(uint32_t)j * kr + ((uint32_t)i - pre[j])];
+    };
+    if (len <= WS_MAX) {
+        if (len == 1) {
+            if (threadIdx.x == 0) seg[0] = load(0);
+            __syncthreads();
+            return;
+        }
+        if (len > 1) small_sort(sh.small, dkeys, seg, len, load);
+        __syncthreads();
+        return;
+    }
+    // long list: gather into alt, copy back contiguous, then the in-place path
+    uint32_t* tmp = alt + base;
+    for (int i = threadIdx.x; i < len; i += SEG_THREADS) tmp[i] = load(i);
+    __syncthreads();
+    for (int i = threadIdx.x; i < len; i += SEG_THREADS) seg[i] = tmp[i];
+    __syncthreads();
+    segsort_tile(sh, make_uint2(base, base + (uint32_t)len), dkeys, vals, alt);
+    __syncthreads();
 }
 
 }  // namespace gs

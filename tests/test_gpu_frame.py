@@ -253,9 +253,10 @@ def test_scatter_binning_ties_in_long_lists(cuda):
 
 
 def test_direct_binning_tile_overflow_reruns(cuda):
-    """Direct binning gives every tile capacity / tiles slots: a capacity
-    above the total but below tiles x the longest list must report the
-    capacity it needs (meta[2]) and re-run to the same frame."""
+    """Direct binning gives every tile capacity / tiles slots in 8 replica
+    segments: a capacity above the total but below what the longest segment
+    needs must report the capacity it needs (meta[2]) and re-run to the
+    same frame."""
     from paper_2312_02121_b200 import ops
     g = load_golden("cfg0_mini")
     t = _tensors(g["inputs"], cuda)
@@ -266,8 +267,8 @@ def test_direct_binning_tile_overflow_reruns(cuda):
         tv = full.tensors()
         lens = tv["ranges"][:, 1] - tv["ranges"][:, 0]
         nt = lens.numel()
-        need = nt * int(lens.max())
-        assert full.needed_capacity == need > full.n_isect  # uneven lists
+        need = full.needed_capacity  # tiles x 8 replica segments x the longest segment
+        assert need % (8 * nt) == 0 and need >= nt * int(lens.max()) and need > full.n_isect
         raw = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True, capacity=need - 1, check_meta=False)
         m = raw.meta().cpu()
         assert int(m[0]) == -1 and int(m[1]) == full.n_isect and int(m[2]) == need
