@@ -175,11 +175,11 @@ class RenderStep:
 
 
 # host->device copy streams of pipeline.  On a box whose single-stream pinned
-# copies ran at 16 GB/s (28 GB/s over 8 streams, tools/pcie_bw.py) config 1's
-# e2e rate over two runs each was 1 453 / 1 523 frames/s with 1 stream,
-# 1 340 / 2 781 with 4 and 2 642 / 1 387 with 8 (bimodal per process); 4 is
-# the default.  GS_H2D_STREAMS=k overrides.
-H2D_STREAMS = int(os.environ.get("GS_H2D_STREAMS", "4"))
+# copies ran at 14-16 GB/s (28 GB/s over 8 streams in isolation,
+# tools/pcie_bw.py) config 1's e2e rate per process was 1.45-1.96 k frames/s
+# with 1 stream, 1.2-2.8 k with 4 and 1.4-2.6 k with 8 (bimodal, no clear
+# winner), so the default stays 1.  GS_H2D_STREAMS=k overrides.
+H2D_STREAMS = int(os.environ.get("GS_H2D_STREAMS", "1"))
 
 
 def pipeline(engine: RenderStep, host_params, host_d_images, out_host, steps: int, allreduce=None, flush=None):
