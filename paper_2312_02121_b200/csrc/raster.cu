@@ -798,25 +798,36 @@ __device__ __forceinline__ void bwd_flush(uint32_t red, int nslot, int lane, flo
     }
 }
 
+#ifndef GS_BWD_WPC
+#define GS_BWD_WPC 4
+#endif
+constexpr int BWD_WPC = GS_BWD_WPC;  // warps per CTA of the record backward (4 or 1)
 #ifndef GS_BWD_MINB
-#define GS_BWD_MINB 8
+#define GS_BWD_MINB (32 / GS_BWD_WPC)
 #endif
 #ifndef GS_BWD_UNROLL
 #define GS_BWD_UNROLL 1
 #endif
 constexpr int BWD_UNROLL = GS_BWD_UNROLL;
-__global__ void __launch_bounds__(128, GS_BWD_MINB) raster_bwd_rec_kernel(
+__global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kernel(
     const uint2* __restrict__ ranges, const uint2* __restrict__ rec, const uint32_t* __restrict__ rec_count,
     const float4* __restrict__ xydr, const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg,
     int W, int H, int tiles_x, const float* __restrict__ final_T, const int* __restrict__ n_contrib,
     const float* __restrict__ d_img, float* __restrict__ g8, float* __restrict__ d_c11,
     const uint32_t* __restrict__ tile_order, const unsigned long long* __restrict__ meta) {
     griddep_wait();
-    __shared__ RecStage s_rec[4][32];
-    __shared__ __align__(16) float s_red[4][RBS][9][RROW];
+    // BWD_WPC warps per CTA: 4 (one CTA per tile) or 1 (one CTA per 8x8
+    // quadrant: a warp that finishes frees its slot without waiting for
+    // its tile's slowest quadrant; the warps never synchronise anyway).
+    // Measured: 1 is 3 % slower at config 1 and 5 % at config 2 -- a tile's
+    // four warps gather the same splats, so they share L1 lines.
+    __shared__ RecStage s_rec[BWD_WPC][32];
+    __shared__ __align__(16) float s_red[BWD_WPC][RBS][9][RROW];
+    const int job = (int)blockIdx.x / (4 / BWD_WPC);
     // the forward's raster order exists unless it binned directly (meta[3] = bin stride)
-    const int tile = tile_order && meta[3] == 0 ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = tile_order && meta[3] == 0 ? (int)tile_order[job] : job;
+    const int lane = threadIdx.x & 31, wslot = threadIdx.x >> 5;
+    const int warp = BWD_WPC == 4 ? wslot : (int)blockIdx.x % 4;  // quadrant
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int col = tx * TILE + (warp & 1) * 8 + (lane & 7);
     const int rbase = ty * TILE + (warp >> 1) * 8 + (lane >> 3);
@@ -840,8 +851,8 @@ __global__ void __launch_bounds__(128, GS_BWD_MINB) raster_bwd_rec_kernel(
     const uint2 rg = ranges[tile];
     const int64_t rb = 4 * (int64_t)rg.x + (int64_t)warp * (rg.y - rg.x);
     const int count = (int)rec_count[(size_t)tile * 4 + warp];
-    const uint32_t red_w = smem_addr(&s_red[warp][0][0][0]);
-    const uint32_t stage_w = smem_addr(&s_rec[warp][0]);
+    const uint32_t red_w = smem_addr(&s_red[wslot][0][0][0]);
+    const uint32_t stage_w = smem_addr(&s_rec[wslot][0]);
     int nslot = 0;
     for (int hi = count; hi > 0; hi -= 32) {
         const int lo = hi > 32 ? hi - 32 : 0;
@@ -850,7 +861,7 @@ __global__ void __launch_bounds__(128, GS_BWD_MINB) raster_bwd_rec_kernel(
             const uint2 r = rec[rb + lo + lane];
             const float4 g = xydr[r.x];
             const float4 q = conic[r.x];
-            RecStage& st = s_rec[warp][lane];
+            RecStage& st = s_rec[wslot][lane];
             st.a = make_float4(g.x, g.y, 0.5f * q.x, q.y);
             st.b = make_float4(0.5f * q.z, q.w, colors[3 * r.x], colors[3 * r.x + 1]);
             st.c = make_float4(colors[3 * r.x + 2], __int_as_float((int)r.y), __int_as_float((int)r.x), 0.f);
@@ -1009,7 +1020,8 @@ int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t*
                           const uint32_t* tile_order, const unsigned long long* meta) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     if (tile_order && !meta) return set_error("raster_bwd_rec: a raster order needs the frame meta");
-    launch_k(raster_bwd_rec_kernel, dim3((unsigned)(tiles_x * tiles_y)), dim3(128), 0, s, ranges, rec, rec_count,
+    launch_k(raster_bwd_rec_kernel, dim3((unsigned)(tiles_x * tiles_y * (4 / BWD_WPC))), dim3(32 * BWD_WPC), 0, s,
+             ranges, rec, rec_count,
              (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H, tiles_x, fT, nc, dimg, g8, d_c11,
              tile_order, meta);
     return check_launch("raster_bwd_rec_kernel");
