@@ -120,3 +120,29 @@ def test_multi_view_step_sums_views(cuda):
     _close(eng.step(params, d_imgs), ref)
     m = eng.meta(0).cpu()
     assert m.shape == (3, 4) and bool((m[:, 0] == -1).all()) and bool((m[:, 1] > 0).all())
+
+
+def test_pipeline_from_write_combined_staging(cuda):
+    """Inputs staged in write-combined pinned memory (engine.host_staging)
+    give the same gradients as the per-call path."""
+    from paper_2312_02121_b200 import engine as E, ops
+    g = load_golden("config0")
+    params = [torch.as_tensor(np.asarray(a, np.float32), device=cuda) for a in g["inputs"]]
+    cam = ops.CameraParams.of(g["camera"])
+    rng = np.random.default_rng(3)
+    d_image = torch.as_tensor(rng.normal(size=(cam.height, cam.width, 3)).astype(np.float32), device=cuda)
+    ref = _per_call(ops, params, cam, d_image)
+    host = []
+    for p in params + [d_image]:
+        t = E.host_staging(tuple(p.shape))
+        assert t.is_pinned()
+        t.copy_(p.cpu())
+        host.append(t)
+    eng = E.RenderStep(len(params[0]), [cam], device=cuda)
+    eng.prime(params, [d_image])
+    out = [torch.empty((14 * len(params[0]),)).pin_memory() for _ in range(eng.nbuf)]
+    metas = E.pipeline(eng, host[:5], host[5:], out, 4)
+    torch.cuda.synchronize()
+    for b, mh in enumerate(metas):
+        eng.result(b, mh)
+        _close(out[b], ref)
