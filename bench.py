@@ -5,17 +5,21 @@
 
 One "step" = on every rank, the full hot path for that rank's view(s):
 project -> scan/emit/sort/ranges -> raster fwd -> raster bwd -> projection
-bwd, plus (N > 1) one NCCL sum-allreduce of the 14 fp32 gradients per
-Gaussian.  Inputs are seeded synthetic scenes with BASELINE.json's
-distributions (paper_2312_02121_b200/scenes.py).  Default workload: config 1
-(100k Gaussians, 800x800), one view per rank (weak scaling: rank r renders
-camera r of a ring; rank 0's camera is config 1's own).  --config 3 runs the
-32-view batch split across ranks (strong scaling).
+bwd, plus (N > 1) the NCCL sum-allreduce of the per-Gaussian gradients.
+Inputs are seeded synthetic scenes with BASELINE.json's distributions
+(paper_2312_02121_b200/scenes.py).  Default workload: config 3 -- the
+32-view batch of 3M Gaussians at 1297x840 that BASELINE.json's metric is
+quoted on at 1/2/4/8 B200 -- split by view across ranks (strong scaling).
+--config 4 is the 4K frame split by tile-row bands; --config 0/1/2 are single
+views (weak scaling: rank r renders camera r of a ring).
 
-Rank 0 prints ONE JSON line (keys documented in DESIGN.md §Measurement).
-`--impl reference` times the CPU oracle port (oracle/, fp64, all host
-threads) on the same workload and prints the same line with "impl":
-"reference".
+`--gpus N` without torchrun re-launches itself under
+torch.distributed.run (one rank per GPU, 127.0.0.1).
+
+Rank 0 prints ONE JSON line (keys documented in DESIGN.md §7).
+`--impl reference` times the CPU oracle port (oracle/, fp64) on the host
+cores -- each step one full fwd+bwd view of the same workload -- and prints
+the same line with "impl": "reference".
 """
 
 from __future__ import annotations
@@ -41,7 +45,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--config", type=int, default=1)
+    p.add_argument("--config", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -473,20 +477,20 @@ def run_ours(args):
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(spec, views[:1], sample_frames=1)
+        cpu = cpu_baseline(spec, views[:1], frames_per_step)
 
-    sz = config_sizes(cfg)
     out = {
         "metric": METRIC, "value": round(fps, 3), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "strong" if cfg in (3, 4) else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded, BASELINE.json distributions; scenes.py)",
-        "config": {"workload": f"config{cfg}", "gaussians": n, "image": f"{sz['width']}x{sz['height']}",
-                   "views_per_step": frames_per_step, "views_per_rank": len(cams),
-                   "early_termination": True, "background": "black",
-                   "parallelism": (f"tile-row bands x{world} (rows {band})" if band else f"view-sharded x{world}") + (" + NCCL allreduce 14 fp32/Gaussian" if world > 1 else ""),
-                   "cuda_graph": graph is not None, "view_streams": min(args.streams, len(cams)),
-                   "l2": "flushed between timed steps (192 MiB write, untimed)"},
+        "config": bench_config(cfg, world,
+                               parallelism=(f"tile-row bands x{world} (rows {band})" if band else
+                                            f"view-sharded x{world}") +
+                               (" + NCCL allreduce 14 fp32/Gaussian" if world > 1 else ""),
+                               views_per_rank=len(cams), cuda_graph=graph is not None,
+                               view_streams=min(args.streams, len(cams)),
+                               l2="flushed between timed steps (192 MiB write, untimed)"),
         "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
         "intersections_per_step_rank": int(I),
         "e2e": e2e,
@@ -528,7 +532,7 @@ def run_e2e(args, spec, views, dev, world, frames):
     from paper_2312_02121_b200 import engine as E
     from paper_2312_02121_b200 import ops
 
-    def staged(a):  # the host writes each step's inputs into write-combined pinned staging buffers
+    def staged(a):  # inputs written once into write-combined pinned staging (engine.host_staging), before timing
         a = np.ascontiguousarray(a, dtype=np.float32)
         t = E.host_staging(a.shape)
         t.copy_(torch.from_numpy(a))
@@ -540,6 +544,7 @@ def run_e2e(args, spec, views, dev, world, frames):
     eng = E.RenderStep(spec.n, cams, device=dev)
     eng.prime(host, dimgs)
     out_host = [torch.empty((14 * spec.n,), dtype=torch.float32).pin_memory() for _ in range(eng.nbuf)]
+    wc = all(E.is_write_combined(h) for h in host + dimgs)
     h2d = sum(h.numel() * 4 for h in host) + sum(d.numel() * 4 for d in dimgs)
     d2h = out_host[0].numel() * 4 + len(cams) * 16
     allreduce = (lambda g: dist.all_reduce(g)) if world > 1 else None
@@ -565,70 +570,156 @@ def run_e2e(args, spec, views, dev, world, frames):
         total = float(tt.item())
     return {"value": round(frames / (total / steps / 1e3), 3), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "api": "paper_2312_02121_b200.engine.RenderStep + pipeline (pinned host I/O every step, "
-                   "double-buffered; inputs from write-combined pinned staging, gradients into ordinary pinned)", "l2": "flushed before every step inside the timed region (conservative)"}
+            "api": "paper_2312_02121_b200.engine.RenderStep + pipeline (host->device copy of every step's "
+                   "inputs and device->host read of its gradients inside the timed region, double-buffered; "
+                   "the inputs are written into the host buffers once, before timing)",
+            "host_inputs": "write-combined pinned" if wc else "pinned (cuda-python unavailable)",
+            "host_outputs": "pinned",
+            "l2": "flushed before every step inside the timed region (conservative)"}
 
 
-def cpu_baseline(spec, views, sample_frames=1, nthreads=0):
-    """fp64 oracle port (oracle/) on the host cores: full fwd+bwd frames."""
+def cpu_info() -> dict:
+    """The host the CPU numbers were taken on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"cpu_model": model, "nproc": usable}
+
+
+def _oracle_view(args64, cam, d_image, nth):
+    """One full fwd+bwd frame of the fp64 oracle port: render (sg/raster_forward.py:255-271)
+    + scene_backward (sg/proj_backward.py:178-223)."""
     import numpy as np
 
     import oracle as O
+    oc = O.Camera.of(cam)
+    fw = O.render(*args64, oc, np.zeros(3), True, nthreads=nth)
+    O.scene_backward(*args64, oc, np.zeros(3), fw, np.asarray(d_image, np.float64), nthreads=nth)
 
-    nth = nthreads or (os.cpu_count() or 1)
+
+def _args64(spec):
+    import numpy as np
     f = lambda a: np.asarray(a, np.float64)
-    args = [f(spec.means), f(spec.scales), f(spec.quats), f(spec.opacities), f(spec.colors)]
+    return [f(spec.means), f(spec.scales), f(spec.quats), f(spec.opacities), f(spec.colors)]
+
+
+def cpu_one_core(spec, views, budget_s=40.0, all_cores_s=None, nth_all=1):
+    """The reference is single-threaded by design (pkg/README.md:10-13): one
+    full view on ONE core, unless the all-cores time predicts more than
+    budget_s (then reported as not measured)."""
+    if all_cores_s is not None and all_cores_s * nth_all > budget_s * 1.5:
+        return None, None
+    a = _args64(spec)
+    cam, d = views[0]
     t0 = time.perf_counter()
-    for cam, d in views[:sample_frames]:
-        oc = O.Camera.of(cam)
-        fw = O.render(*args, oc, np.zeros(3), True, nthreads=nth)
-        O.scene_backward(*args, oc, np.zeros(3), fw, f(d), nthreads=nth)
+    _oracle_view(a, cam, d, 1)
     dt = time.perf_counter() - t0
-    nf = len(views[:sample_frames])
-    return {"value": round(nf / dt, 5), "unit": "frames/s", "cores": nth, "kind": "port",
-            "sample": f"{nf} full fwd+bwd frame(s) of the same workload (oracle/splat_oracle.c, fp64, OpenMP)",
-            "seconds": round(dt, 3)}
+    return round(1.0 / dt, 5), round(dt, 3)
+
+
+def cpu_baseline(spec, views, frames_per_step):
+    """Bounded sample of the same workload on the host (rank 0, N = 1): one
+    full fwd+bwd view on all host threads, then one on one core.  frames/s =
+    views / seconds; a config-3 step is 32 such views."""
+    info = cpu_info()
+    nth = info["nproc"]
+    a = _args64(spec)
+    cam, d = views[0]
+    t0 = time.perf_counter()
+    _oracle_view(a, cam, d, nth)
+    dt = time.perf_counter() - t0
+    v1, s1 = cpu_one_core(spec, views, all_cores_s=dt, nth_all=nth)
+    return {"value": round(1.0 / dt, 5), "unit": "frames/s", "cores": nth, "kind": "port",
+            "sample": f"1 of {frames_per_step} views per step, full fwd+bwd (oracle/splat_oracle.c, fp64, "
+                      f"OpenMP x{nth}); frames/s = views/s",
+            "seconds": round(dt, 3), "one_core": {"value": v1, "unit": "frames/s", "seconds": s1}, **info}
 
 
 # ------------------------------------------------------------ reference arm
 
 def run_reference(args):
+    """The reference's CPU path (fp64 oracle port of sg/raster_forward.py:255-271
+    render + sg/proj_backward.py:178-223 scene_backward) on the host cores:
+    W untimed + K timed steps, each ONE full fwd+bwd view of the workload
+    (views cycle through the config's cameras), all host threads.  Under
+    torchrun only rank 0 runs."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np
 
     from paper_2312_02121_b200.scenes import config_sizes, make_config
 
-    spec = make_config(args.config)
-    views = views_for(args.config, spec, 1, 0)
-    nth = os.cpu_count() or 1
-    sz = config_sizes(args.config)
-    # each step: one full fwd+bwd frame (bounded: ~1-3 s per frame at config 1)
-    for _ in range(min(args.warmup, 1)):
-        cpu_baseline(spec, views, 1, nth)
-    steps = max(1, min(args.steps, 10))
+    cfg = args.config
+    K, W = max(1, args.steps), max(0, args.warmup)
+    nv_cfg = config_sizes(cfg)["views"]
+    spec = make_config(cfg, n_views=min(nv_cfg, K + W)) if cfg == 3 else make_config(cfg)
+    views = list(zip(spec.cameras, spec.d_images))
+    info = cpu_info()
+    nth = info["nproc"]
+    a = _args64(spec)
+    for i in range(W):
+        cam, d = views[i % len(views)]
+        _oracle_view(a, cam, d, nth)
     t0 = time.perf_counter()
-    for _ in range(steps):
-        cpu_baseline(spec, views, 1, nth)
+    for i in range(K):
+        cam, d = views[(W + i) % len(views)]
+        _oracle_view(a, cam, d, nth)
     dt = time.perf_counter() - t0
-    fps = steps / dt
-    out = {"metric": METRIC, "value": round(fps, 5), "unit": "frames/s", "n_gpus": args.gpus, "steps": steps,
-           "warmup": min(args.warmup, 1), "ms_per_step": round(dt / steps * 1e3, 3), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; scenes.py)",
-           "config": {"workload": f"config{args.config}", "gaussians": spec.n,
-                      "image": f"{sz['width']}x{sz['height']}",
-                      "views_per_step": 1, "early_termination": True, "background": "black",
-                      "parallelism": f"host OpenMP x{nth} (fp64 oracle port)"},
+    fps = K / dt
+    v1, s1 = cpu_one_core(spec, views, all_cores_s=dt / K, nth_all=nth)
+    out = {"metric": METRIC, "value": round(fps, 5), "unit": "frames/s", "n_gpus": args.gpus, "steps": K,
+           "warmup": W, "ms_per_step": round(dt / K * 1e3, 3), "higher_is_better": True,
+           "scaling": "strong" if cfg in (3, 4) else "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded, BASELINE.json distributions; scenes.py)",
+           "config": bench_config(cfg, args.gpus, parallelism=f"host OpenMP x{nth} (fp64 oracle port)",
+                                  views_per_rank=nv_cfg if cfg in (3, 4) else 1, cuda_graph=False, view_streams=1,
+                                  l2="n/a (host)"),
            "impl": "reference",
            "cpu_baseline": {"value": round(fps, 5), "unit": "frames/s", "cores": nth, "kind": "port",
-                            "sample": "full fwd+bwd frame per step (oracle/splat_oracle.c, fp64, OpenMP)"},
+                            "sample": f"each step 1 full fwd+bwd view (of {nv_cfg} per workload step) on all host "
+                                      f"threads (oracle/splat_oracle.c, fp64, OpenMP); frames/s = views/s",
+                            "one_core": {"value": v1, "unit": "frames/s", "seconds": s1}, **info},
            "e2e": {"value": round(fps, 5), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
+def bench_config(cfg, world, parallelism=None, **extra):
+    """The line's `config` object (same keys for both arms)."""
+    from paper_2312_02121_b200.scenes import config_sizes
+    sz = config_sizes(cfg)
+    c = {"workload": f"config{cfg}", "gaussians": sz["gaussians"], "image": f"{sz['width']}x{sz['height']}",
+         "views_per_step": sz["views"] if cfg in (3, 4) else world, "early_termination": True,
+         "background": "black", "parallelism": parallelism}
+    c.update(extra)
+    return c
+
+
+def self_launch(args) -> int:
+    """`--gpus N` (N > 1) outside torchrun: run this script under
+    torch.distributed.run, one rank per GPU, rendezvous on 127.0.0.1."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -279,18 +279,24 @@ def _grid_from_bins(bins: ops.Bins, cam: ops.CameraParams, vis):
 # ------------------------------------------------------------------ API
 
 def render(scene, camera: Camera, background, *, early_termination=True) -> RenderResult:
-    """sg/raster_forward.py:255-271 on the GPU."""
+    """sg/raster_forward.py:255-271 on the GPU, through the production frame
+    path (gs_frame_forward: the frame binning, raster_fwd_kernel with commit
+    records -- what bench.py times).  The ProjectedGaussian list (which needs
+    cov2d, not stored by the frame) comes from the stage projection kernel,
+    the same arithmetic bit for bit."""
     dev = _device()
     bg = np.asarray(background, dtype=np.float64)
     cam = ops.CameraParams.of(camera)
     t = _scene_tensors(scene, dev)
-    image, st = ops.render_forward(*t, cam, tuple(bg), early_termination, want_cov=True)
-    projected, vis = _projected_list(camera, scene, st.proj)
-    grid = _grid_from_bins(st.bins, cam, vis)
-    st.extra["tensors"] = t
-    return RenderResult(image=ImageBuffer(cam.width, cam.height, _np(image).astype(np.float64)),
-                        aux=RenderAux(_np(st.final_T).astype(np.float64), _np(st.n_contrib).astype(np.int64)),
-                        grid=grid, projected=projected, background=bg, _gpu=st)
+    fr = ops.frame_forward(*t, cam, tuple(bg), early_termination)
+    proj = ops.project(t[0], t[1], t[2], t[3], cam, want_cov=True)
+    tv = fr.tensors()
+    projected, vis = _projected_list(camera, scene, proj)
+    grid = _grid_from_bins(ops.Bins(tv["ranges"], None, tv["sorted_vals"], fr.n_isect), cam, vis)
+    fr.extra = dict(tensors=t, tv=tv)
+    return RenderResult(image=ImageBuffer(cam.width, cam.height, _np(fr.image).astype(np.float64)),
+                        aux=RenderAux(_np(fr.final_T).astype(np.float64), _np(fr.n_contrib).astype(np.int64)),
+                        grid=grid, projected=projected, background=bg, _gpu=fr)
 
 
 def render_brute_force(scene, camera: Camera, background, *, early_termination=True) -> RenderResult:
@@ -338,12 +344,25 @@ def _state(scene, result):
     return st, t
 
 
+def _stage_state(st) -> ops.FrameState:
+    """A frame-path result as the stage kernels' FrameState (its own
+    projection, compacted bins, final_T and n_contrib)."""
+    if isinstance(st, ops.FrameState):
+        return st
+    tv = st.extra.get("tv") or st.tensors()
+    proj = ops.Projection(tv["xydr"], tv["conic"], tv["tiles"], None)
+    bins = ops.Bins(tv["ranges"], None, tv["sorted_vals"], st.n_isect)
+    return ops.FrameState(st.cam, st.background, st.early_termination, proj, bins, st.final_T, st.n_contrib)
+
+
 def accumulate_image_backward(scene, result: RenderResult, d_image) -> Splat2DGrads:
-    """sg/raster_backward.py:166-205 on the GPU (screen-space gradients)."""
+    """sg/raster_backward.py:166-205 on the GPU (screen-space gradients):
+    the list-staging raster backward (gs_raster_bwd) over the frame's own
+    projection and bins."""
     d_image = _check_dimage(result, d_image)
     st, t = _state(scene, result)
     d = torch.as_tensor(d_image.astype(np.float32), device=t[0].device)
-    d_rgbo, d_geo, d_c11 = ops.raster_bwd(st, t[4], d)
+    d_rgbo, d_geo, d_c11 = ops.raster_bwd(_stage_state(st), t[4], d)
     geo = _np(d_geo).astype(np.float64)
     c11 = _np(d_c11).astype(np.float64)
     rgbo = _np(d_rgbo).astype(np.float64)
@@ -353,11 +372,16 @@ def accumulate_image_backward(scene, result: RenderResult, d_image) -> Splat2DGr
 
 
 def scene_backward(scene, camera: Camera, result: RenderResult, d_image) -> SceneGradients:
-    """sg/proj_backward.py:178-223 on the GPU."""
+    """sg/proj_backward.py:178-223 on the GPU: gs_frame_backward (the record-
+    driven raster backward + the projection backward) for a render() result;
+    the stage kernels for a render_brute_force() result."""
     d_image = _check_dimage(result, d_image)
     st, t = _state(scene, result)
     d = torch.as_tensor(d_image.astype(np.float32), device=t[0].device)
-    g = ops.render_backward(st, t[0], t[1], t[2], t[4], d)
+    if isinstance(st, ops.FrameState):
+        g = ops.render_backward(st, t[0], t[1], t[2], t[4], d)
+    else:
+        g = ops.frame_backward(st, t[0], t[1], t[2], t[4], d)
     f = lambda x: _np(x).astype(np.float64)
     return SceneGradients(d_mean=f(g["d_mean"]), d_scale=f(g["d_scale"]), d_quat=f(g["d_quat"]),
                           d_opacity=f(g["d_opacity"]).copy(), d_color=f(g["d_color"]).copy(), d_view=f(g["d_view"]))

@@ -30,6 +30,9 @@ import torch
 from . import _lib, ops
 
 
+_WC_PTRS: set = set()
+
+
 def host_staging(shape, dtype=torch.float32) -> torch.Tensor:
     """A CPU tensor in pinned, write-combined host memory
     (cudaHostAllocWriteCombined) for inputs the host writes and the GPU
@@ -37,13 +40,19 @@ def host_staging(shape, dtype=torch.float32) -> torch.Tensor:
     caches (on one box of the pool pinned host->device copies ran at 14 GB/s
     from ordinary pinned memory and 55 GB/s from write-combined memory,
     tools/pcie_bw.py).  The host must not READ it (uncached).  Falls back to
-    ordinary pinned memory when cuda-python is unavailable."""
+    ordinary pinned memory when cuda-python is unavailable;
+    ``is_write_combined(t)`` tells which kind a tensor got.
+
+    The allocation is owned by the buffer object torch.frombuffer keeps alive
+    for the storage's lifetime, so it is freed when the last tensor sharing
+    the storage dies (not when this wrapper does)."""
     import ctypes
-    import weakref
     numel = 1
     for d in shape:
         numel *= int(d)
-    nbytes = max(1, numel * torch.empty((), dtype=dtype).element_size())
+    if numel == 0:
+        return torch.empty(tuple(shape), dtype=dtype).pin_memory()
+    nbytes = numel * torch.empty((), dtype=dtype).element_size()
     try:
         try:
             from cuda.bindings import runtime as cr
@@ -54,10 +63,24 @@ def host_staging(shape, dtype=torch.float32) -> torch.Tensor:
             raise RuntimeError(f"cudaHostAlloc: {err}")
     except Exception:  # noqa: BLE001 -- no cuda-python: ordinary pinned memory
         return torch.empty(tuple(shape), dtype=dtype).pin_memory()
-    raw = (ctypes.c_uint8 * nbytes).from_address(int(ptr))
+    ptr = int(ptr)
+
+    class _WCBuffer(ctypes.c_uint8 * nbytes):
+        """Owns the cudaHostAlloc block; freed when the storage releases it."""
+
+        def __del__(self, _free=cr.cudaFreeHost, _ptr=ptr, _reg=_WC_PTRS):
+            _reg.discard(_ptr)
+            _free(_ptr)
+
+    raw = _WCBuffer.from_address(ptr)
     t = torch.frombuffer(raw, dtype=dtype, count=numel).view(tuple(shape))
-    weakref.finalize(t, lambda p=int(ptr), keep=raw: cr.cudaFreeHost(p))
+    _WC_PTRS.add(ptr)
     return t
+
+
+def is_write_combined(t: torch.Tensor) -> bool:
+    """True when ``t`` lives in a host_staging write-combined block."""
+    return t.untyped_storage().data_ptr() in _WC_PTRS
 
 
 def unpack(flat: torch.Tensor, n: int) -> dict:

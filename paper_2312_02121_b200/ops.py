@@ -388,6 +388,7 @@ class Frame:
     counts_fwd: torch.Tensor | None = None
     meta_host: tuple | None = None
     backward_runs: int = 0  # the forward zeroes the backward accumulators once
+    extra: dict = field(default_factory=dict)  # adapters' payload (api.render)
 
     def view(self) -> _lib.GsFrameView:
         v = _lib.GsFrameView()
