@@ -777,10 +777,19 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
 // each slot's splat id sits in the padding word (lane 32) of its first row.
 // The conic rows (6..8) were accumulated without their factor 1/2, applied
 // here (exact).
+// GS_BWD_V4=1: two red.global.add.v4.f32 + one scalar red per (warp, record)
+// instead of 9 scalar reds (3 L2 requests instead of 9).  Measured at config 3:
+// raster backward 9.03 -> 9.54 ms per 32 views (the 3 shuffles + the extra
+// predicated branch cost more issue slots than the L2 requests saved; the
+// kernel is issue-bound, not L2-atomic-bound: 19 G reds/s), so it is off.
+#ifndef GS_BWD_V4
+#define GS_BWD_V4 0
+#endif
 __device__ __forceinline__ void bwd_flush(uint32_t red, int nslot, int lane, float* __restrict__ g8,
                                           float* __restrict__ d_c11) {
+    const int k = lane / 9, t = lane - 9 * k;
+    float sum = 0.f;
     if (lane < 9 * nslot) {
-        const int k = lane / 9, t = lane - 9 * k;
         const uint32_t row = red + (uint32_t)lane * (RROW * 4);
         const float4 a = lds_f4(row);
         f32x2 s01 = pk2(a.x, a.y), s23 = pk2(a.z, a.w);
@@ -791,11 +800,30 @@ __device__ __forceinline__ void bwd_flush(uint32_t red, int nslot, int lane, flo
             s23 = add2(s23, pk2(b.z, b.w));
         }
         const f32x2 s2 = add2(s01, s23);
-        float sum = lo2(s2) + hi2(s2);
+        sum = lo2(s2) + hi2(s2);
         if (t >= 6) sum *= 0.5f;
+    }
+#if GS_BWD_V4
+    // rows 0-3 (d_rgbo) and 4-7 (d_geo) of a slot are one 16-byte gradient
+    // row each: lanes 9k and 9k+4 gather their 3 neighbours' sums and issue
+    // one red.global.add.v4.f32 each, lane 9k+8 adds d_c11 (3 L2 requests
+    // per (warp, record) instead of 9)
+    const float s1 = __shfl_down_sync(0xffffffffu, sum, 1);
+    const float s2v = __shfl_down_sync(0xffffffffu, sum, 2);
+    const float s3 = __shfl_down_sync(0xffffffffu, sum, 3);
+    if (lane < 9 * nslot && (t == 0 || t == 4 || t == 8)) {
+        const uint32_t id = lds_u32(red + (uint32_t)k * (9 * RROW * 4) + 32 * 4);
+        if (t == 8)
+            atomicAdd(d_c11 + id, sum);
+        else
+            red_add_v4(reinterpret_cast<float4*>(g8 + 8 * (size_t)id + t), sum, s1, s2v, s3);
+    }
+#else
+    if (lane < 9 * nslot) {
         const uint32_t id = lds_u32(red + (uint32_t)k * (9 * RROW * 4) + 32 * 4);
         atomicAdd(t < 8 ? g8 + 8 * (size_t)id + t : d_c11 + id, sum);
     }
+#endif
 }
 
 #ifndef GS_BWD_WPC
@@ -846,7 +874,11 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
     }
     f32x2 T = pk2(t[0], t[1]);
     const f32x2 G0 = pk2(ga[0], ga[1]), G1 = pk2(gb[0], gb[1]), G2 = pk2(gc[0], gc[1]);
-    f32x2 S0 = mul2(bc2(bg.x), T), S1 = mul2(bc2(bg.y), T), S2 = mul2(bc2(bg.z), T);
+    // the backward's running sum S (sg/raster_backward.py:58,107: S = bg T_final + sum w c over the
+    // entries behind) enters the gradient only through S . g, so the pixel keeps SDOT = S . g:
+    // seeded (bg . g) T_final, advanced by w (c . g) = w CDOT per contributing entry (1 FFMA2
+    // instead of 3 S updates + a 3-term dot per record)
+    f32x2 SDOT = mul2(fma2(bc2(bg.z), G2, fma2(bc2(bg.y), G1, mul2(bc2(bg.x), G0))), T);
     const f32x2 PY = pin2(pk2((float)rbase + 0.5f, (float)rbase + 4.5f));
     const uint2 rg = ranges[tile];
     const int64_t rb = 4 * (int64_t)rg.x + (int64_t)warp * (rg.y - rg.x);
@@ -896,7 +928,6 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
             const f32x2 Wt = mul2(AL, TH);
             const f32x2 WC = pk2(c0 ? lo2(Wt) : 0.f, c1 ? hi2(Wt) : 0.f);
             const f32x2 CDOT = fma2(bc2(blue), G2, fma2(bc2(bq.w), G1, mul2(bc2(bq.z), G0)));
-            const f32x2 SDOT = fma2(S2, G2, fma2(S1, G1, mul2(S0, G0)));
             const f32x2 DA = sub2(mul2(TH, CDOT), mul2(INV, SDOT));
             const bool l0 = c0 && lo2(ARAW) < ALPHA_MAX, l1 = c1 && hi2(ARAW) < ALPHA_MAX;
             const f32x2 DAL = pk2(l0 ? lo2(DA) : 0.f, l1 ? hi2(DA) : 0.f);
@@ -911,9 +942,7 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
 #pragma unroll
             for (int u = 0; u < 9; ++u) sts_f32(slot + u * (RROW * 4), lo2(D[u]) + hi2(D[u]));
             if (lane == 0) sts_u32(slot + 32 * 4, __float_as_uint(cq.z));  // splat id -> row padding
-            S0 = fma2(WC, bc2(bq.z), S0);
-            S1 = fma2(WC, bc2(bq.w), S1);
-            S2 = fma2(WC, bc2(blue), S2);
+            SDOT = fma2(WC, CDOT, SDOT);
             T = sel2(c0, c1, TH, T);
             if (++nslot == RBS) {
                 __syncwarp();
