@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true")
-    p.add_argument("--streams", type=int, default=2, help="streams the views of a multi-view step alternate on")
+    p.add_argument("--streams", type=int, default=3, help="streams the views of a multi-view step alternate on")
     return p.parse_args()
 
 
@@ -242,8 +242,7 @@ def run_ours(args):
         fr = ops.frame_forward(m, s, q, o, c, cam, bg, True)
         cap = int(fr.needed_capacity * 1.05) + 4096
         caps.append(cap)
-        wss.append(torch.empty((L.gs_frame_workspace_bytes(n, cap, cam.width, cam.height),), device=dev,
-                               dtype=torch.uint8))
+        wss.append(ops.frame_workspace(n, cap, cam.width, cam.height, dev))
         del fr
 
     def mk_events(k):
@@ -283,11 +282,11 @@ def run_ours(args):
             with torch.cuda.stream(st):
                 fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, capacity=caps[vi], check_meta=False,
                                        ws=wss[vi], events=ev_f[vi] if staged else None)
-                if bwd_done is not None:
-                    st.wait_event(bwd_done)
+                # only the views' accumulation into grad_out is ordered: this view's raster
+                # backward overlaps the previous view's projection backward
                 ops.frame_backward(fr, m, s, q, c, d_img,
                                    events=ev_b[vi] if staged else [ev_t[vi][0], ev_t[vi][1], None],
-                                   out=grad_out, accumulate=vi > 0)
+                                   out=grad_out, accumulate=vi > 0, wait_before_accumulate=bwd_done)
                 if two:
                     bwd_done = torch.cuda.Event()
                     bwd_done.record(st)
@@ -413,11 +412,12 @@ def run_ours(args):
     direct = binning == "direct"
     fused = fused_sort(n, cams[0])
     work = {
-        # read 44 B, write xydr 16 + conic 16 + tiles 4 + depth key 4, and zero the backward's
-        # screen-space gradient accumulators (rows of 8 floats + d_c11: 36 B) the projection
-        # kernel clears for the frame; direct binning: + a slot atomic and the Gaussian id per
-        # intersection (8 B)
-        "project": ("hbm", 120.0 * n * nv + (8.0 * I if direct else 0.0)),
+        # 72 B per Gaussian (read mean 12 + scale 12 + quat 16; write mean2d 8 +
+        # cov/conic 12 + depth 4 + radius 4 + tiles 4).  The kernel itself moves 84 B (+ opacity
+        # 4 in, the conic's 4th float and the depth sort key out); the backward accumulators are
+        # no longer zeroed here (the projection backward clears the rows it reads).  Direct
+        # binning: + a slot atomic and the Gaussian id per intersection (8 B)
+        "project": ("hbm", 72.0 * n * nv + (8.0 * I if direct else 0.0)),
         # depth-first: 4 passes x (key+value) x (read+write); scatter / direct: no global depth sort
         "depth_sort": ("none", 0.0) if seg else ("hbm", 4 * 16.0 * n * nv),
         # depth-first: fused scan + emission, (order +) count + xydr gather per Gaussian, pairs out;
@@ -433,9 +433,11 @@ def run_ours(args):
                              (tp * 16.0 * I + 4.0 * I + 8.0 * n_tiles)),
         "raster_fwd": ("fp32", float(F_fwd)),
         "raster_bwd": ("fp32", float(F_bwd)),
-        # read tiles 4 + gradient row 32 + d_c11 4 + mean 12 + scale 12 + quat 16, write d_mean 12 +
-        # d_scale 12 + d_quat 16 + d_rgbo 16; views after the first also read the running sums (56)
-        "project_bwd": ("hbm", 136.0 * n * nv + 56.0 * n * max(nv - 1, 0)),
+        # 104 B per Gaussian (read mean, scale, quat 40 + d_mean2d 8 + d_cov 12 +
+        # radius/visibility 4; write d_mean, d_scale, d_quat 40).  The kernel also copies the
+        # d_color/d_opacity row (16 + 16), clears the rows it read, and views after the first
+        # read-modify-write the running sums
+        "project_bwd": ("hbm", 104.0 * n * nv),
     }
     st = {}
     for name, ms in zip(stage_names, stage_ms):
@@ -454,8 +456,12 @@ def run_ours(args):
         st[name] = d
     dom = max(stage_names, key=lambda k: stage_ms[stage_names.index(k)])
     if dom == "raster_bwd" and timed_bwd_ms > 0:
-        # the roofline kernel's duration as measured inside the timed region
+        # the roofline kernel's duration as measured inside the timed region (with several view
+        # streams its event interval also covers the other views' kernels sharing the SMs); the
+        # instrumented single-stream replay gives the kernel alone
         bwd_ms = timed_bwd_ms / max(args.steps, 1)
+        st[dom]["ms_isolated"] = st[dom]["ms"]
+        st[dom]["frac_isolated"] = st[dom]["frac"]
         st[dom]["ms_timed_region"] = round(bwd_ms, 4)
         st[dom]["achieved_tops"] = round(work[dom][1] / (bwd_ms / 1e3) / 1e12, 3)
         st[dom]["frac"] = round(work[dom][1] / (bwd_ms / 1e3) / fp32_peak, 4)
@@ -471,6 +477,9 @@ def run_ours(args):
         roof = {"bound": "hbm", "kernel": dom, "achieved": st[dom]["achieved_gbs"],
                 "peak": float(peaks.get("hbm_gbs", 6650.0)), "unit": "GB/s", "frac": st[dom]["frac"],
                 "peak_source": peak_src}
+    if "frac_isolated" in st[dom]:
+        roof["frac_isolated"] = st[dom]["frac_isolated"]
+        roof["duration_ms_isolated_per_launch"] = round(st[dom]["ms_isolated"] / nv, 4)
     roof["traffic"] = traffic.get(dom)
     roof["algorithmic_work_per_launch"] = work[dom][1] / nv
     roof["duration_ms_per_launch"] = round(float(stage_ms[stage_names.index(dom)]) / nv, 4)

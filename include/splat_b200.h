@@ -194,16 +194,25 @@ typedef struct gs_frame_view {
     uint32_t* ranges2;          /* (tiles,2) [start, end) */
     unsigned long long* meta;   /* [0] status word, [1] total intersections, [2] capacity needed,
                                    [3] direct-binning tile stride (0: compact bins) */
-    float* d_geo4;              /* (n,4) d_mean2d x,y, d_cov00, d_cov01 (after backward),
-                                   row stride 8 floats (interleaved with d_rgbo) */
-    float* d_c11;               /* (n)   d_cov11 (after backward) */
-    void* bwd_accum;            /* the backward's atomic accumulators (d_rgbo/d_geo rows, d_c11): zeroed by
-                                   gs_frame_forward; zero bwd_accum_bytes here before a SECOND
-                                   gs_frame_backward of the same forward */
+    float* d_geo4;              /* (n,4) d_mean2d x,y, d_cov00, d_cov01 (after a backward run with
+                                   accumulate bit 1 set; zeros otherwise), row stride 8 floats
+                                   (interleaved with d_rgbo) */
+    float* d_c11;               /* (n)   d_cov11 (idem) */
+    void* bwd_accum;            /* the backward's atomic accumulators (d_rgbo/d_geo rows, d_c11).  Zero
+                                   between frames: the projection backward clears every row it
+                                   reads; gs_frame_forward zeroes them itself only when the
+                                   workspace is not stamped clean for this layout */
     size_t bwd_accum_bytes;
+    uint32_t* rec_count;        /* (tiles,4) forward commit records per (tile, 8x8 quadrant warp) */
 } gs_frame_view;
 
 size_t gs_frame_workspace_bytes(int64_t n, int64_t isect_capacity, int32_t width, int32_t height);
+/* Mark a freshly allocated (or re-purposed) workspace as not clean: the next
+ * gs_frame_forward then zeroes the backward accumulators itself.  Call it
+ * once per allocation; a workspace kept across frames of one layout needs
+ * nothing more (a stale layout is detected by its signature).              */
+int gs_frame_workspace_init(int64_t n, int64_t isect_capacity, int32_t width, int32_t height, void* ws,
+                            gs_stream_t stream);
 /* The binning gs_frame_forward uses for n Gaussians on a width x height
  * view under the current options: 1 depth-first, 2 scatter, 3 direct. */
 int gs_frame_binning(int64_t n, int32_t width, int32_t height);
@@ -219,10 +228,15 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
  *   forward : [0] start [1] projected [2] depth-sorted [3] emitted [4] tile-sorted+ranges [5] rastered
  *   backward: [0] start [1] raster backward done [2] projection backward done
  * d_rgbo4 (n,4) = d_color r,g,b, d_opacity; d_view16 4x4 (always written).
- * accumulate == 0: d_means3 / d_scales3 / d_quats4 / d_rgbo4 are
- * overwritten; != 0: this view's gradients are ADDED to them (sum over the
+ * accumulate bit 0 clear: d_means3 / d_scales3 / d_quats4 / d_rgbo4 are
+ * overwritten; set: this view's gradients are ADDED to them (sum over the
  * views of a step without extra kernels, sg/proj_backward.py:178-223 summed
- * per camera). */
+ * per camera).  Bit 1 set: leave the screen-space gradients readable in the
+ * workspace (gs_frame_view d_geo4 / d_c11; the next forward re-zeroes them);
+ * clear (default): the projection backward zeroes them as it reads them.
+ * Bit 2 set: stage_events has a 4th entry, an event `stream` waits on before
+ * the projection backward (a multi-view step serialises only the views'
+ * read-modify-write accumulation; their raster backwards may overlap). */
 int gs_frame_backward(const float* means3, const float* scales3, const float* quats4, const float* colors3,
                       int64_t n, const gs_camera* cam /*[host]*/, const float* background3 /*[host]*/,
                       int64_t isect_capacity, void* ws, size_t ws_bytes, const float* final_T,

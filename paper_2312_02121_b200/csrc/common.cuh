@@ -307,14 +307,19 @@ bool pdl_enabled();  // GS_PDL=0 disables (abi.cu)
 struct ZeroJobs {
     uint4* p[3];
     unsigned long long n16[3];
+    // job 2 runs only when *cond2 != 0 (null: always) -- the frame path's
+    // backward accumulators, zeroed only when the workspace is not known clean
+    const unsigned long long* cond2;
 };
 
 __device__ __forceinline__ void run_zero_jobs(const ZeroJobs& zj) {
     const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
+    for (int j = 0; j < 3; ++j) {
+        if (j == 2 && zj.cond2 && *zj.cond2 == 0ull) continue;
         for (unsigned long long k = tid; k < zj.n16[j]; k += stride) zj.p[j][k] = make_uint4(0u, 0u, 0u, 0u);
+    }
 }
 
 template <typename... KArgs, typename... Args>

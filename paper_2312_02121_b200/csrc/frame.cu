@@ -63,15 +63,14 @@ bool scatter_binning(int64_t n, int n_tiles) { return binning_for(n, n_tiles) !=
 // Direct binning: every tile owns kstride = capacity / tiles pair slots.
 int64_t direct_stride(int64_t cap, int n_tiles) { return n_tiles > 0 ? cap / n_tiles : 0; }
 
-// where the tile-sorted (keys, vals) of a frame end up
-bool sorted_in_alt(int64_t n, int n_tiles) {
-    return !scatter_binning(n, n_tiles) && (tile_passes_for(n_tiles) & 1);
-}
+// Every binning leaves the frame's tile-sorted (keys, vals) in the primary
+// buffers (the depth-first emission targets the alternates when it sorts an
+// odd number of tile passes), so readers never depend on the options.
 
 struct Layout {
     // persistent (written each frame)
     size_t xydr, conic, tiles, dkeys, dkeys_alt, order, order_alt, offsets;
-    size_t tkeys, tkeys_alt, tvals, tvals_alt, ranges, rec, rec_count, tile_order, tcount;
+    size_t tkeys, tkeys_alt, tvals, tvals_alt, ranges, rec, rec_count, tile_order, tcount, clean;
     // zeroed region
     size_t zero_begin, meta, dhist, thist, counters, scan_ws, dstatus, tstatus, zero_end;
     // backward
@@ -89,6 +88,9 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
         o += up(bytes > 0 ? bytes : 1);
         return at;
     };
+    // the clean word sits at offset 0 for every layout, so a frame of any
+    // other layout run on the same workspace always overwrites it
+    L.clean = take(16);  // layout signature while the backward accumulators are known zero
     L.xydr = take(16 * n);
     L.conic = take(16 * n);
     L.tiles = take(4 * n);
@@ -107,7 +109,8 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.tile_order = take(4 * nt);  // raster launch order (heaviest lists first)
     L.tcount = take(4 * TCOUNT_REPL * nt);  // scatter binning: tile counts, then write cursors
     L.zero_begin = o;
-    L.meta = take(32);  // status, total intersections, capacity needed, direct-binning tile stride
+    L.meta = take(64);  // status, total intersections, capacity needed, direct-binning tile stride,
+                        // accumulators-to-zero flag, reserved
     L.dhist = take(4 * 256 * 4);
     L.thist = take(4 * 256 * 2);
     L.counters = take(64);
@@ -139,6 +142,18 @@ T* at(void* ws, size_t off) {
     return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
 }
 
+// Signature of a workspace layout (stamped in the clean word while the
+// backward accumulators hold zeros).
+unsigned long long clean_sig(int64_t n, int64_t cap, int W, int H) {
+    unsigned long long h = 0x9e3779b97f4a7c15ull;
+    for (unsigned long long v : {(unsigned long long)n, (unsigned long long)cap, (unsigned long long)W,
+                                 (unsigned long long)H}) {
+        h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+        h *= 0xbf58476d1ce4e5b9ull;
+    }
+    return h | 1ull;  // never 0 (0 = "not clean")
+}
+
 }  // namespace
 
 }  // namespace gs
@@ -155,23 +170,30 @@ size_t gs_frame_workspace_bytes(int64_t n, int64_t isect_capacity, int32_t width
     return layout(n, isect_capacity, width, height).total;
 }
 
+int gs_frame_workspace_init(int64_t n, int64_t isect_capacity, int32_t width, int32_t height, void* ws,
+                            gs_stream_t stream) {
+    const Layout L = layout(n, isect_capacity, width, height);
+    if (cudaMemsetAsync(at<char>(ws, L.clean), 0, 16, (cudaStream_t)stream) != cudaSuccess)
+        return check_launch("gs_frame_workspace_init");
+    return 0;
+}
+
 int gs_frame_view_of(int64_t n, int64_t isect_capacity, int32_t width, int32_t height, void* ws,
                      gs_frame_view* out) {
     const Layout L = layout(n, isect_capacity, width, height);
-    const int nt = ((width + TILE - 1) / TILE) * ((height + TILE - 1) / TILE);
-    const bool odd = sorted_in_alt(n, nt);
     out->xydr4 = at<float>(ws, L.xydr);
     out->conic4 = at<float>(ws, L.conic);
     out->tiles = at<uint32_t>(ws, L.tiles);
     out->depth_order = at<uint32_t>(ws, L.order);
-    out->sorted_tile_keys = at<uint32_t>(ws, odd ? L.tkeys_alt : L.tkeys);
-    out->sorted_vals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
+    out->sorted_tile_keys = at<uint32_t>(ws, L.tkeys);
+    out->sorted_vals = at<uint32_t>(ws, L.tvals);
     out->ranges2 = at<uint32_t>(ws, L.ranges);
     out->meta = at<unsigned long long>(ws, L.meta);
     out->d_geo4 = at<float>(ws, L.d_geo) + 4;  // rows of 8 floats: [d_rgbo 4 | d_geo 4]
     out->d_c11 = at<float>(ws, L.d_c11);
     out->bwd_accum = at<char>(ws, L.d_geo);
     out->bwd_accum_bytes = L.partials - L.d_geo;
+    out->rec_count = at<uint32_t>(ws, L.rec_count);
     return 0;
 }
 
@@ -206,8 +228,9 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     zj.n16[0] = (L.zero_end - L.thist) / 16;
     zj.p[1] = at<uint4>(ws, L.ranges);
     zj.n16[1] = (8 * (size_t)tiles_x * tiles_y + 15) / 16;
-    zj.p[2] = at<uint4>(ws, L.d_geo);
+    zj.p[2] = at<uint4>(ws, L.d_geo);  // the backward accumulators: only when not known clean (meta[4])
     zj.n16[2] = (L.partials - L.d_geo) / 16;
+    zj.cond2 = meta + 4;
     const int n_tiles = tiles_x * tiles_y;
     const Binning binning = binning_for(n, n_tiles);
     const bool scatter = binning == SCATTER;
@@ -218,7 +241,8 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
                                 at<float>(ws, L.conic), at<uint32_t>(ws, L.tiles), nullptr, meta,
                                 at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.dhist), s, zj,
                                 binning != DEPTH_FIRST ? at<uint32_t>(ws, L.tcount) : nullptr,
-                                direct ? at<uint32_t>(ws, L.tvals) : nullptr, (uint32_t)kstride))
+                                direct ? at<uint32_t>(ws, L.tvals) : nullptr, (uint32_t)kstride,
+                                at<unsigned long long>(ws, L.clean), clean_sig(n, isect_capacity, W, H)))
         return -1;
     mark(stage_events, 1, s);
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
@@ -278,19 +302,23 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     mark(stage_events, 2, s);
     // 3+4. fused: scan of the tile counts (in depth order), total ->
     //      meta[1], emission of the (tile, gaussian) pairs + tile-digit histograms
+    // (an odd number of tile passes starts from the alternate buffers, so the
+    // sorted pairs always end in the primary ones)
+    const bool odd = tp & 1;
+    uint32_t* k0 = at<uint32_t>(ws, odd ? L.tkeys_alt : L.tkeys);
+    uint32_t* v0 = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
+    uint32_t* k1 = at<uint32_t>(ws, odd ? L.tkeys : L.tkeys_alt);
+    uint32_t* v1 = at<uint32_t>(ws, odd ? L.tvals : L.tvals_alt);
     if (launch_emit_scan(order, at<float>(ws, L.xydr), at<uint32_t>(ws, L.tiles), n, tiles_x, tiles_y,
-                         isect_capacity, at<uint32_t>(ws, L.tkeys), at<uint32_t>(ws, L.tvals),
-                         at<uint32_t>(ws, L.thist), tp, at<char>(ws, L.scan_ws), meta + 1, s))
+                         isect_capacity, k0, v0, at<uint32_t>(ws, L.thist), tp, at<char>(ws, L.scan_ws), meta + 1, s))
         return -1;
     mark(stage_events, 3, s);
     // 5. stable sort by tile id (bits [0, 8*tp))
-    if (run_onesweep<uint32_t>(at<uint32_t>(ws, L.tkeys), at<uint32_t>(ws, L.tvals), at<uint32_t>(ws, L.tkeys_alt),
-                               at<uint32_t>(ws, L.tvals_alt), isect_capacity, meta + 1, tp,
-                               at<uint32_t>(ws, L.thist), at<uint32_t>(ws, L.tstatus), counters + 4, s, false))
+    if (run_onesweep<uint32_t>(k0, v0, k1, v1, isect_capacity, meta + 1, tp, at<uint32_t>(ws, L.thist),
+                               at<uint32_t>(ws, L.tstatus), counters + 4, s, false))
         return -1;
-    const bool odd = tp & 1;
-    const uint32_t* skeys = at<uint32_t>(ws, odd ? L.tkeys_alt : L.tkeys);
-    const uint32_t* svals = at<uint32_t>(ws, odd ? L.tvals_alt : L.tvals);
+    const uint32_t* skeys = at<uint32_t>(ws, L.tkeys);
+    const uint32_t* svals = at<uint32_t>(ws, L.tvals);
     // 6. per-tile ranges
     if (launch_ranges_u32(skeys, isect_capacity, meta + 1, at<uint2>(ws, L.ranges), s)) return -1;
     // 6b. heaviest-first raster launch order
@@ -318,10 +346,11 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
     cudaStream_t s = (cudaStream_t)stream;
     const CamK k = make_camk(*cam);
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
-    const uint32_t* svals = at<uint32_t>(ws, sorted_in_alt(n, tiles_x * tiles_y) ? L.tvals_alt : L.tvals);
+    const uint32_t* svals = at<uint32_t>(ws, L.tvals);
     mark(stage_events, 0, s);
-    // the screen-space accumulators were zeroed by gs_frame_forward (see
-    // gs_frame_view.bwd_accum to re-zero before a second backward)
+    // the screen-space accumulators are zero here: the previous backward's
+    // projection backward cleared the rows it read, or gs_frame_forward zeroed
+    // them (meta[4]) when the workspace was not stamped clean for this layout
     const float3 bg = make_float3(background3[0], background3[1], background3[2]);
     float* g8 = at<float>(ws, L.d_geo);
     if (counts3) {  // counted pass (roofline numerators): the list-walking backward counts evaluations
@@ -337,9 +366,21 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
         return -1;
     }
     mark(stage_events, 1, s);
+    // accumulate bit 0: add into the outputs; bit 1: keep the screen-space
+    // gradients in the workspace (gs_frame_view.d_geo4 / d_c11) -- the next
+    // forward then re-zeroes them; bit 2: stage_events[3] is an event this
+    // stream waits on before the projection backward -- a multi-view step
+    // orders only the views' read-modify-write accumulation, so one view's
+    // raster backward (its own workspace) overlaps the previous view's
+    // projection backward
+    const bool keep = (accumulate & 2) != 0;
+    if ((accumulate & 4) && stage_events && stage_events[3] &&
+        cudaStreamWaitEvent(s, (cudaEvent_t)stage_events[3], 0) != cudaSuccess)
+        return check_launch("gs_frame_backward: wait event");
     if (launch_project_bwd(means3, scales3, quats4, n, k, at<uint32_t>(ws, L.tiles), g8 + 4,
                            at<float>(ws, L.d_c11), d_means3, d_scales3, d_quats4, d_view16, at<float>(ws, L.partials),
-                           s, accumulate != 0, 2, g8, d_rgbo4, at<unsigned int>(ws, L.pbwd_done)))
+                           s, (accumulate & 1) != 0, 2, g8, d_rgbo4, at<unsigned int>(ws, L.pbwd_done),
+                           at<unsigned long long>(ws, L.clean), clean_sig(n, isect_capacity, W, H), !keep))
         return -1;
     mark(stage_events, 2, s);
     return 0;

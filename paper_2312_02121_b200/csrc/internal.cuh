@@ -14,14 +14,21 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
                             int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
                             unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s,
                             const ZeroJobs& zj, uint32_t* tcount = nullptr, uint32_t* bins = nullptr,
-                            uint32_t kstride = 0);  // also resets meta (status, total, need), dhist and
+                            uint32_t kstride = 0, unsigned long long* clean_word = nullptr,
+                            unsigned long long clean_sig = 0);  // also resets meta (status, total, need), dhist and
                             // (scatter / direct binning: per-tile intersection counts) tcount first;
                             // bins != nullptr: direct binning into bins[tile * kstride + slot]
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
                        float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
                        bool accumulate = false, int gstride = 1, const float* rgbo_in = nullptr,
-                       float* rgbo_out = nullptr, unsigned int* done_counter = nullptr);
+                       float* rgbo_out = nullptr, unsigned int* done_counter = nullptr,
+                       unsigned long long* clean_word = nullptr, unsigned long long clean_sig = 0,
+                       bool clear_accum = false);
+// clear_accum (frame path): every visible Gaussian's screen-space accumulator
+// row (d_geo4 row + d_rgbo row + d_c11) is zeroed after it is read, and the
+// last block stamps *clean_word = clean_sig (0 when not clearing), which the
+// next gs_frame_forward checks instead of zeroing the accumulators itself.
 // gstride 2: d_geo4 rows interleaved with d_rgbo rows (g8 layout); with
 // rgbo_in, each Gaussian's d_rgbo row is copied (or added) to rgbo_out.
 constexpr int PBWD_BLOCK = 256;

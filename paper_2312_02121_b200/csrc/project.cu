@@ -194,42 +194,59 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
 constexpr int PBWD_THREADS = 256;
 
 // Per-Gaussian loop body of sg/proj_backward.py:200-222.
+#ifndef PBWD_RGBO_EARLY
+#define PBWD_RGBO_EARLY 1  // measured: config 3 1042 -> 1057 frames/s (project bwd itself 4.38 -> 4.54 ms)
+#endif
+#ifndef PBWD_TWO_PHASE
+#define PBWD_TWO_PHASE 0  // 1: read the visibility word first, the rest only for visible Gaussians
+#endif
+#ifndef PBWD_LASTBLOCK
+#define PBWD_LASTBLOCK 0  // 1: the last block to finish reduces d_view (else view_reduce_kernel)
+#endif
 #ifndef PBWD_MINB
 #define PBWD_MINB 4  // 64 registers: 4 CTAs per SM (config 4: 264 -> 239 us)
 #endif
 __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
-    int n, CamK cam, const uint32_t* __restrict__ tiles, const float4* __restrict__ d_geo,
-    const float* __restrict__ d_c11, float* __restrict__ d_means, float* __restrict__ d_scales,
+    int n, CamK cam, const uint32_t* __restrict__ tiles, float4* __restrict__ d_geo,
+    float* __restrict__ d_c11, float* __restrict__ d_means, float* __restrict__ d_scales,
     float4* __restrict__ d_quats, float* __restrict__ view_partials, bool accumulate, int gstride,
-    const float4* __restrict__ rgbo_in, float4* __restrict__ rgbo_out, unsigned int* __restrict__ done_counter,
-    float* __restrict__ d_view16) {
+    float4* __restrict__ rgbo_in, float4* __restrict__ rgbo_out, unsigned int* __restrict__ done_counter,
+    float* __restrict__ d_view16, unsigned long long* __restrict__ clean_word, unsigned long long clean_sig,
+    bool clear_accum) {
     griddep_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    // every load is issued up front, ahead of the visibility test (one memory
-    // round trip instead of two; culled Gaussians' reads are the price)
+    // the visibility word first: a culled Gaussian's gradient is exactly
+    // zero (sg/proj_backward.py:200-203 loops over `projected` only), so its
+    // parameters and (never touched) accumulator rows are not read at all
     const bool in = i < n;
     const uint32_t nt = in ? tiles[i] : 0u;
-    const float4 v_rgbo = in && rgbo_in ? rgbo_in[(size_t)i * gstride] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 gg = in ? d_geo[(size_t)i * gstride] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float g11 = in ? d_c11[i] : 0.f;
+    const bool vis = in && nt != 0u;
+    float4 v_rgbo = make_float4(0.f, 0.f, 0.f, 0.f), gg = make_float4(0.f, 0.f, 0.f, 0.f);
+    float g11 = 0.f;
     float mx = 0.f, my = 0.f, mz = 0.f, s[3] = {1.f, 1.f, 1.f};
     float4 q = make_float4(1.f, 0.f, 0.f, 0.f);
-    if (in) {
+    float om[3] = {0.f, 0.f, 0.f}, os[3] = {0.f, 0.f, 0.f};  // accumulate: the caller's running sums
+    float4 oq = make_float4(0.f, 0.f, 0.f, 0.f), orgbo = make_float4(0.f, 0.f, 0.f, 0.f);
+#if PBWD_TWO_PHASE
+    if (vis) {
+#else
+    if (in) {  // every load issued up front, ahead of the visibility test (one memory round trip)
+#endif
+        if (rgbo_in) v_rgbo = rgbo_in[(size_t)i * gstride];
+        gg = d_geo[(size_t)i * gstride];
+        g11 = d_c11[i];
         mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
         s[0] = scales[3 * i], s[1] = scales[3 * i + 1], s[2] = scales[3 * i + 2];
         q = quats[i];
+        if (accumulate) {
+            om[0] = d_means[3 * i], om[1] = d_means[3 * i + 1], om[2] = d_means[3 * i + 2];
+            os[0] = d_scales[3 * i], os[1] = d_scales[3 * i + 1], os[2] = d_scales[3 * i + 2];
+            oq = d_quats[i];
+            if (rgbo_in && !PBWD_RGBO_EARLY) orgbo = rgbo_out[i];
+        }
     }
-    float om[3] = {0.f, 0.f, 0.f}, os[3] = {0.f, 0.f, 0.f};  // accumulate: the caller's running sums
-    float4 oq = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (accumulate && in) {
-        om[0] = d_means[3 * i], om[1] = d_means[3 * i + 1], om[2] = d_means[3 * i + 2];
-        os[0] = d_scales[3 * i], os[1] = d_scales[3 * i + 1], os[2] = d_scales[3 * i + 2];
-        oq = d_quats[i];
-    }
-    const bool vis = in && nt != 0u;
-    // (accumulating: a culled Gaussian adds exact zeros -- skip its rows)
-    if (rgbo_in && in && (vis || !accumulate)) {  // frame path: d_color / d_opacity rows of the interleaved buffer
+    if (PBWD_RGBO_EARLY && rgbo_in && in && (vis || !accumulate)) {
         if (accumulate) {
             const float4 o = rgbo_out[i];
             rgbo_out[i] = make_float4(o.x + v_rgbo.x, o.y + v_rgbo.y, o.z + v_rgbo.z, o.w + v_rgbo.w);
@@ -363,6 +380,23 @@ __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
             d_quats[i] = dq;
         }
     }
+    // frame path: the d_color / d_opacity row of the interleaved buffer
+    // (accumulating: a culled Gaussian adds exact zeros -- skip its row); all
+    // read-modify-writes store at the end, well behind their loads
+    if (!PBWD_RGBO_EARLY && rgbo_in && in && (vis || !accumulate))
+        rgbo_out[i] = accumulate ? make_float4(orgbo.x + v_rgbo.x, orgbo.y + v_rgbo.y, orgbo.z + v_rgbo.z,
+                                               orgbo.w + v_rgbo.w)
+                                 : v_rgbo;
+    if (clear_accum && vis) {
+        // leave the accumulators zero for the next frame (culled rows were
+        // never touched).  After the outputs, with streaming stores: issued
+        // right behind the loads of the same rows, these stores made the
+        // kernel 2.2x slower at config 3 (the loads' sectors stall them)
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (rgbo_in) __stcs(rgbo_in + (size_t)i * gstride, z);
+        __stcs(d_geo + (size_t)i * gstride, z);
+        __stcs(d_c11 + i, 0.f);
+    }
     // block partial of d_view (deterministic: fixed shuffle tree + fixed warp
     // order).  Transposed warp reduction of the 12 values padded to 16: each
     // level exchanges half of the values, so 16 shuffles instead of 60.
@@ -412,14 +446,20 @@ __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
         if (lane == 0) d_view16[k] = v;
     }
     if (threadIdx.x < 4) d_view16[12 + threadIdx.x] = 0.f;
-    if (threadIdx.x == 0) *done_counter = 0u;
+    if (threadIdx.x == 0) {
+        *done_counter = 0u;
+        if (clean_word) *clean_word = clear_accum ? clean_sig : 0ull;
+    }
 }
 
 // Fixed-order sum of the per-block d_view partials -> 4x4 (bottom row 0,
 // sg/proj_backward.py:31-32).
 __global__ void __launch_bounds__(384) view_reduce_kernel(const float* __restrict__ partials, int nblocks,
-                                                          float* __restrict__ d_view16) {
+                                                          float* __restrict__ d_view16,
+                                                          unsigned long long* __restrict__ clean_word,
+                                                          unsigned long long clean_stamp) {
     griddep_wait();
+    if (clean_word && threadIdx.x == 0) *clean_word = clean_stamp;
     const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float v = 0.f;
     for (int b = lane; b < nblocks; b += 32) v += partials[b * 12 + k];
@@ -433,9 +473,14 @@ __global__ void __launch_bounds__(384) view_reduce_kernel(const float* __restric
 // depth-digit histograms = 0 (the projection accumulates into them).
 // Frame reset ahead of the projection: meta, the depth histograms and (scatter
 // binning) the per-tile intersection counts the projection accumulates.
+// meta[4] = 1 when the backward accumulators must be zeroed this frame: the
+// workspace's clean word does not carry this layout's signature (fresh or
+// re-laid-out workspace, or the last backward kept its screen-space
+// gradients); the word is then stamped (the projection zeroes them).
 __global__ void __launch_bounds__(256) frame_init_kernel(unsigned long long* __restrict__ meta,
                                                          uint32_t* __restrict__ dhist, uint32_t* __restrict__ tcount,
-                                                         int n_counts) {
+                                                         int n_counts, unsigned long long* __restrict__ clean_word,
+                                                         unsigned long long clean_sig) {
     griddep_wait();
     if (blockIdx.x == 0) {
         if (threadIdx.x == 0) {
@@ -443,6 +488,10 @@ __global__ void __launch_bounds__(256) frame_init_kernel(unsigned long long* __r
             meta[1] = 0ull;
             meta[2] = 0ull;
             meta[3] = 0ull;
+            if (clean_word) {
+                meta[4] = *clean_word != clean_sig ? 1ull : 0ull;
+                *clean_word = clean_sig;
+            }
         }
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) dhist[k] = 0u;
     }
@@ -453,11 +502,12 @@ __global__ void __launch_bounds__(256) frame_init_kernel(unsigned long long* __r
 int launch_project_fwd_dkey(const float* means3, const float* scales3, const float* quats4, const float* opac,
                             int64_t n, const CamK& k, float* xydr4, float* conic4, uint32_t* tiles, float* cov3,
                             unsigned long long* status, uint32_t* dkeys, uint32_t* dhist, cudaStream_t s,
-                            const ZeroJobs& zj, uint32_t* tcount, uint32_t* bins, uint32_t kstride) {
+                            const ZeroJobs& zj, uint32_t* tcount, uint32_t* bins, uint32_t kstride,
+                            unsigned long long* clean_word, unsigned long long clean_sig) {
     const int n_tiles = k.tiles_x * k.tiles_y;
     const int init_blocks = tcount ? (TCOUNT_REPL * n_tiles + 2047) / 2048 : 1;
     launch_k(frame_init_kernel, dim3((unsigned)init_blocks), dim3(256), 0, s, status, dhist, tcount,
-             TCOUNT_REPL * n_tiles);
+             TCOUNT_REPL * n_tiles, clean_word, clean_sig);
     if (check_launch("frame_init_kernel")) return -1;
     int64_t blocks = (n + 255) / 256;
     if (blocks < 1) blocks = 1;  // the zero jobs run even for an empty scene
@@ -482,16 +532,20 @@ int launch_project_bwd(const float* means3, const float* scales3, const float* q
                        const uint32_t* tiles, const float* d_geo4, const float* d_c11, float* d_means3,
                        float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
                        bool accumulate, int gstride, const float* rgbo_in, float* rgbo_out,
-                       unsigned int* done_counter) {
+                       unsigned int* done_counter, unsigned long long* clean_word, unsigned long long clean_sig,
+                       bool clear_accum) {
     const int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
     if (blocks > 0) {
         launch_k(project_bwd_kernel, dim3(blocks), dim3(PBWD_THREADS), 0, s, means3, scales3, (const float4*)quats4,
-                 (int)n, k, tiles, (const float4*)d_geo4, d_c11, d_means3, d_scales3, (float4*)d_quats4, partials,
-                 accumulate, gstride, (const float4*)rgbo_in, (float4*)rgbo_out, done_counter, d_view16);
+                 (int)n, k, tiles, (float4*)d_geo4, const_cast<float*>(d_c11), d_means3, d_scales3,
+                 (float4*)d_quats4, partials, accumulate, gstride, (float4*)rgbo_in, (float4*)rgbo_out,
+                 PBWD_LASTBLOCK ? done_counter : nullptr, d_view16, clean_word, clean_sig, clear_accum);
+        done_counter = PBWD_LASTBLOCK ? done_counter : nullptr;
         if (check_launch("project_bwd_kernel")) return -1;
         if (done_counter) return 0;  // the last block wrote d_view
     }
-    launch_k(view_reduce_kernel, dim3(1), dim3(384), 0, s, (const float*)partials, blocks, d_view16);
+    launch_k(view_reduce_kernel, dim3(1), dim3(384), 0, s, (const float*)partials, blocks, d_view16, clean_word,
+             clear_accum ? clean_sig : 0ull);
     return check_launch("view_reduce_kernel");
 }
 
@@ -531,11 +585,12 @@ int gs_project_bwd(const float* means3, const float* scales3, const float* quats
     const int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
     if (blocks > 0) {
         project_bwd_kernel<<<blocks, PBWD_THREADS, 0, (cudaStream_t)stream>>>(
-            means3, scales3, (const float4*)quats4, (int)n, k, tiles, (const float4*)d_geo4, d_c11, d_means3,
-            d_scales3, (float4*)d_quats4, (float*)ws, false, 1, nullptr, nullptr, nullptr, d_view16);
+            means3, scales3, (const float4*)quats4, (int)n, k, tiles, (float4*)d_geo4, const_cast<float*>(d_c11),
+            d_means3, d_scales3, (float4*)d_quats4, (float*)ws, false, 1, nullptr, nullptr, nullptr, d_view16,
+            nullptr, 0ull, false);
         if (check_launch("project_bwd_kernel")) return -1;
     }
-    view_reduce_kernel<<<1, 384, 0, (cudaStream_t)stream>>>((const float*)ws, blocks, d_view16);
+    view_reduce_kernel<<<1, 384, 0, (cudaStream_t)stream>>>((const float*)ws, blocks, d_view16, nullptr, 0ull);
     return check_launch("view_reduce_kernel");
 }
 

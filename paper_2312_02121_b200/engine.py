@@ -96,7 +96,7 @@ def unpack(flat: torch.Tensor, n: int) -> dict:
 
 class RenderStep:
     def __init__(self, n: int, cams, background=(0.0, 0.0, 0.0), early_termination=True, device=None,
-                 headroom: float = 1.05, buffers: int = 2):
+                 headroom: float = 1.05, buffers: int = 2, view_streams: int = 3):
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         self.n = int(n)
         self.cams = [c if isinstance(c, ops.CameraParams) else ops.CameraParams.of(c) for c in cams]
@@ -115,7 +115,9 @@ class RenderStep:
                 graph=None))
         self.caps = None
         self.wss = None
-        self.aux = torch.cuda.Stream(self.dev)  # second view stream (multi-view steps)
+        # further view streams (multi-view steps): 3 streams measured best at config 3
+        # (2: 1066, 3: 1077 frames/s, bench.py --streams)
+        self.aux = [torch.cuda.Stream(self.dev) for _ in range(max(0, min(view_streams, len(self.cams)) - 1))]
 
     # -------------------------------------------------------------- set-up
     def _size(self, k: int):
@@ -128,19 +130,21 @@ class RenderStep:
             fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et)
             cap = int(fr.needed_capacity * self.headroom) + 4096
             self.caps.append(cap)
-            self.wss.append(torch.empty((L.gs_frame_workspace_bytes(self.n, cap, cam.width, cam.height),),
-                                        device=self.dev, dtype=torch.uint8))
+            self.wss.append(ops.frame_workspace(self.n, cap, cam.width, cam.height, self.dev))
 
     def _body(self, k: int):
-        """All views of one step.  Several views alternate between two
-        streams (each view has its own workspace); a view's backward waits
-        for the previous view's, so the gradient sums keep the sequential
-        order while one view's forward overlaps the previous backward."""
+        """All views of one step.  Several views alternate between the view
+        streams (each view has its own workspace); a view's projection
+        backward -- the read-modify-write accumulation into the step's
+        gradients -- waits for the previous view's, so the views are summed
+        in order, while forwards and raster backwards of neighbouring views
+        overlap.  (Within a view the raster backward's fp32 atomics already
+        make the low bits order-dependent.)"""
         s = self.sets[k]
         m, sc, q, o, c = s["params"]
         out = unpack(s["grads"], self.n)
         main = torch.cuda.current_stream(self.dev)
-        sts = [main] + ([self.aux] if len(self.cams) > 1 else [])
+        sts = [main] + self.aux
         for a in sts[1:]:
             a.wait_stream(main)
         bwd_done = None
@@ -149,9 +153,7 @@ class RenderStep:
             with torch.cuda.stream(st):
                 fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et, capacity=self.caps[vi],
                                        check_meta=False, ws=self.wss[vi])
-                if bwd_done is not None:
-                    st.wait_event(bwd_done)
-                ops.frame_backward(fr, m, sc, q, c, d, out=out, accumulate=vi > 0)
+                ops.frame_backward(fr, m, sc, q, c, d, out=out, accumulate=vi > 0, wait_before_accumulate=bwd_done)
                 s["meta"][vi].copy_(fr.meta())
                 if len(sts) > 1:
                     bwd_done = torch.cuda.Event()

@@ -387,7 +387,6 @@ class Frame:
     n_contrib: torch.Tensor
     counts_fwd: torch.Tensor | None = None
     meta_host: tuple | None = None
-    backward_runs: int = 0  # the forward zeroes the backward accumulators once
     extra: dict = field(default_factory=dict)  # adapters' payload (api.render)
 
     def view(self) -> _lib.GsFrameView:
@@ -449,7 +448,18 @@ class Frame:
                     tiles=sl(v.tiles, n, torch.int32, (n,)), depth_order=sl(v.depth_order, n, torch.int32, (n,)),
                     sorted_tile_keys=sorted_tile_keys, sorted_vals=sorted_vals, ranges=ranges,
                     d_geo=sl(v.d_geo4 - 16, 8 * n, torch.float32, (n, 8))[:, 4:8],  # rows of [d_rgbo | d_geo]
-                    d_c11=sl(v.d_c11, n, torch.float32, (n,)))
+                    d_c11=sl(v.d_c11, n, torch.float32, (n,)),
+                    rec_count=sl(v.rec_count, 4 * nt, torch.int32, (nt, 4)))
+
+
+def frame_workspace(n: int, capacity: int, width: int, height: int, device) -> torch.Tensor:
+    """A frame workspace (gs_frame_workspace_bytes) marked not clean
+    (gs_frame_workspace_init), for callers that keep one across frames."""
+    L = _lib.load()
+    ws = torch.empty((L.gs_frame_workspace_bytes(n, capacity, width, height),), device=device, dtype=torch.uint8)
+    check(L.gs_frame_workspace_init(n, capacity, width, height, ws.data_ptr(), _stream()),
+          "gs_frame_workspace_init")
+    return ws
 
 
 def frame_forward(means, scales, quats, opacities, colors, cam: CameraParams, background=(0.0, 0.0, 0.0),
@@ -468,7 +478,7 @@ def frame_forward(means, scales, quats, opacities, colors, cam: CameraParams, ba
     while True:
         wsb = L.gs_frame_workspace_bytes(n, cap, W, H)
         if ws is None or ws.numel() < wsb:
-            ws = torch.empty((wsb,), device=dev, dtype=torch.uint8)
+            ws = frame_workspace(n, cap, W, H, dev)
         image = torch.empty((H, W, 3), device=dev, dtype=torch.float32)
         final_T = torch.empty((H, W), device=dev, dtype=torch.float32)
         n_contrib = torch.empty((H, W), device=dev, dtype=torch.int32)
@@ -502,11 +512,18 @@ def _event_array(events):
 
 
 def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=False, events=None, out=None,
-                   accumulate=False):
+                   accumulate=False, keep_screen=False, wait_before_accumulate=None):
     """gs_frame_backward: the SceneGradients fields (sg/proj_backward.py:25-50).
     out: optional dict of contiguous output tensors d_mean (n,3), d_scale
     (n,3), d_quat (n,4), d_rgbo (n,4) to write (accumulate=False) or add
-    this view's gradients into (accumulate=True)."""
+    this view's gradients into (accumulate=True).  keep_screen: leave the
+    screen-space gradients (Splat2DGrads) readable through fr.tensors()
+    (d_geo, d_c11); otherwise the projection backward clears them as it
+    reads them, so the next frame needs no zeroing pass.
+    wait_before_accumulate: a torch.cuda.Event the stream waits on between
+    the raster backward and the projection backward (which adds into `out`):
+    views of one step on several streams then overlap their raster backwards
+    and serialise only the accumulation."""
     L = _lib.load()
     H, W = fr.cam.height, fr.cam.width
     if tuple(d_image.shape) != (H, W, 3):
@@ -530,15 +547,15 @@ def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=F
     cnt = torch.zeros((3,), device=dev, dtype=torch.int64) if counts else None
     camc = fr.cam.c()
     bg = (C.c_float * 3)(*fr.background)
-    if fr.backward_runs:  # a second backward of the same forward: re-zero the accumulators
-        v = fr.view()
-        off = v.bwd_accum - fr.ws.data_ptr()
-        fr.ws[off:off + v.bwd_accum_bytes].zero_()
-    fr.backward_runs += 1
+    flags = (1 if accumulate else 0) | (2 if keep_screen else 0)
+    if wait_before_accumulate is not None:
+        flags |= 4
+        events = (list(events) + [None] * 3)[:3] if events else [None, None, None]
+        events.append(wait_before_accumulate)
     check(L.gs_frame_backward(_ptr(means), _ptr(scales), _ptr(quats), _ptr(colors), n, C.byref(camc), bg,
                               fr.capacity, _ptr(fr.ws), fr.ws.numel(), _ptr(fr.final_T), _ptr(fr.n_contrib),
                               _ptr(d_image), _ptr(d_means), _ptr(d_scales), _ptr(d_quats), _ptr(d_rgbo),
-                              _ptr(d_view), 1 if accumulate else 0, _ptr(cnt), _event_array(events), _stream()),
+                              _ptr(d_view), flags, _ptr(cnt), _event_array(events), _stream()),
           "gs_frame_backward")
     return dict(d_mean=d_means, d_scale=d_scales, d_quat=d_quats, d_opacity=d_rgbo[:, 3], d_color=d_rgbo[:, :3],
                 d_view=d_view, d_rgbo=d_rgbo, counts=cnt)

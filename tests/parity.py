@@ -405,7 +405,7 @@ def frame_parity(spec_arrays, cam_spec, d_image, dev, *, tile_frac=None, seed=0,
     rep["gaussians_checked"] = int(len(touched))
     if return_case:
         return rep, dict(d_masked=d_masked, ref=ref, touched=touched, frame=fr)
-    gf = ops.frame_backward(fr, t[0], t[1], t[2], t[4], torch.as_tensor(d_masked, device=dev))
+    gf = ops.frame_backward(fr, t[0], t[1], t[2], t[4], torch.as_tensor(d_masked, device=dev), keep_screen=True)
     torch.cuda.synchronize()
     got = {k: _np(gf[k]).astype(np.float64) for k in GRAD_CLASSES}
     rep["gradients"] = compare_grads(got, ref, touched)

@@ -301,3 +301,52 @@ def test_option_change_between_forward_and_backward(cuda):
                 assert r["ok"], (fwd_mode, bwd_mode, k, r)
     finally:
         ops.set_option("binning", 0)
+
+
+def test_backward_accumulators_stay_clean(cuda):
+    """The projection backward clears the screen-space accumulators as it
+    reads them, so the next forward skips its zeroing pass; a workspace that
+    is dirty (garbage, another layout, or a backward that kept its
+    screen-space gradients) is re-zeroed by the forward (clean-word
+    signature).  Every sequence must give the fresh-workspace gradients."""
+    from paper_2312_02121_b200 import ops
+    g = load_golden("config0")
+    t = _tensors(g["inputs"], cuda)
+    cp = ops.CameraParams.of(g["camera"])
+    rng = np.random.default_rng(5)
+    d = torch.as_tensor(rng.normal(size=(cp.height, cp.width, 3)).astype(np.float32), device=cuda)
+
+    def grads(fr, **kw):
+        out = ops.frame_backward(fr, t[0], t[1], t[2], t[4], d, **kw)
+        torch.cuda.synchronize()
+        return {k: out[k].clone() for k in ("d_mean", "d_scale", "d_quat", "d_rgbo")}
+
+    def same(a, b):
+        for k in a:
+            # only the fp32 atomic order differs (a dirty accumulator would be off by O(1))
+            r = grad_gate(a[k].cpu().numpy(), b[k].cpu().numpy(), rel=1e-4, floor=1e-2)
+            assert r["ok"], (k, r)
+
+    ref = grads(ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True))
+    fr = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True)
+    cap = fr.capacity
+    same(grads(fr), ref)
+    same(grads(fr), ref)  # a second backward of the same forward: the first left the rows zero
+    same(grads(fr, keep_screen=True), ref)
+    tv = fr.tensors()
+    assert float(tv["d_geo"].abs().sum()) > 0  # kept readable
+    fr2 = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True, capacity=cap, ws=fr.ws)  # forward re-zeroes
+    same(grads(fr2), ref)
+    assert float(fr2.tensors()["d_geo"].abs().sum()) == 0.0  # cleared by the projection backward
+    # garbage workspace, marked not clean
+    ws = ops.frame_workspace(t[0].shape[0], cap, cp.width, cp.height, cuda)
+    ws.random_(0, 255)
+    L = ops._lib.load()
+    L.gs_frame_workspace_init(t[0].shape[0], cap, cp.width, cp.height, ws.data_ptr(), ops._stream())
+    same(grads(ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True, capacity=cap, ws=ws)), ref)
+    # the same workspace used for a smaller scene (another layout) and back
+    m = t[0].shape[0] // 2
+    half = [x[:m].contiguous() for x in t]
+    frh = ops.frame_forward(*half, cp, (0.0, 0.0, 0.0), True, capacity=cap, ws=ws)
+    ops.frame_backward(frh, half[0], half[1], half[2], half[4], d, keep_screen=True)
+    same(grads(ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True, capacity=cap, ws=ws)), ref)

@@ -117,7 +117,7 @@ def test_full_frame_record_backward_equals_stage_backward(config, cuda):
     cp = ops.CameraParams.of(spec.cameras[0])
     d = torch.as_tensor(spec.d_images[0], device=cuda)
     fr = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True)
-    gf = ops.frame_backward(fr, t[0], t[1], t[2], t[4], d)
+    gf = ops.frame_backward(fr, t[0], t[1], t[2], t[4], d, keep_screen=True)
     tv = fr.tensors()
     img, st = ops.render_forward(*t, cp, (0.0, 0.0, 0.0), True)
     assert torch.equal(img, fr.image) and torch.equal(st.n_contrib, fr.n_contrib)

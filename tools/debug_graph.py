@@ -10,7 +10,7 @@ cam = ops.CameraParams.of(spec.cameras[0])
 fr = ops.frame_forward(m, s, q, o, c, cam)
 cap = fr.n_isect + 1000
 L = _lib.load()
-ws = torch.empty((L.gs_frame_workspace_bytes(spec.n, cap, cam.width, cam.height),), device=dev, dtype=torch.uint8)
+ws = ops.frame_workspace(spec.n, cap, cam.width, cam.height, dev)
 for use_ev in (False, True):
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     for e in evs: e.record()
