@@ -188,12 +188,14 @@ typedef struct gs_frame_view {
     float* xydr4;               /* (n,4) as gs_project_fwd out_xydr4 */
     float* conic4;              /* (n,4) as gs_project_fwd out_conic4 */
     uint32_t* tiles;            /* (n)   tiles touched, 0 = culled */
-    uint32_t* depth_order;      /* (n)   Gaussian ids by (depth, index), culled last */
+    uint32_t* depth_order;      /* (n)   Gaussian ids by (depth, index) (see depth_order_alt) */
     uint32_t* sorted_tile_keys; /* (capacity) tile id of each sorted pair */
     uint32_t* sorted_vals;      /* (capacity) Gaussian id of each sorted pair */
     uint32_t* ranges2;          /* (tiles,2) [start, end) */
     unsigned long long* meta;   /* [0] status word, [1] total intersections, [2] capacity needed,
-                                   [3] direct-binning tile stride (0: compact bins) */
+                                   [3] direct-binning tile stride (0: compact bins), [4] the forward
+                                   zeroed the backward accumulators, [5,6] visible depth-key bits
+                                   min / max, [7] visible Gaussians, [8] depth-sort passes */
     float* d_geo4;              /* (n,4) d_mean2d x,y, d_cov00, d_cov01 (after a backward run with
                                    accumulate bit 1 set; zeros otherwise), row stride 8 floats
                                    (interleaved with d_rgbo) */
@@ -204,6 +206,9 @@ typedef struct gs_frame_view {
                                    workspace is not stamped clean for this layout */
     size_t bwd_accum_bytes;
     uint32_t* rec_count;        /* (tiles,4) forward commit records per (tile, 8x8 quadrant warp) */
+    uint32_t* depth_order_alt;  /* depth-first binning: the visible Gaussians (meta[7] of them) by
+                                   (depth, index) are in depth_order_alt when meta[8] (the depth-sort
+                                   pass count) is odd, else in depth_order */
 } gs_frame_view;
 
 size_t gs_frame_workspace_bytes(int64_t n, int64_t isect_capacity, int32_t width, int32_t height);

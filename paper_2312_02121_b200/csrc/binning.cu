@@ -317,8 +317,13 @@ __global__ void __launch_bounds__(ES_THREADS) emit_scan_kernel(
     const uint32_t* __restrict__ order, const float4* __restrict__ xydr, const uint32_t* __restrict__ counts, int n,
     int tiles_x, int tiles_y, int64_t capacity, uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ vals,
     uint32_t* __restrict__ tile_hist, int tile_passes, unsigned int* __restrict__ chunk_counter,
-    unsigned long long* __restrict__ status, unsigned long long* __restrict__ total) {
+    unsigned long long* __restrict__ status, unsigned long long* __restrict__ total,
+    const uint32_t* __restrict__ order_alt, const unsigned long long* __restrict__ sort_meta) {
     griddep_wait();
+    if (sort_meta) {  // depth-first frame: meta[7] visible Gaussians sorted, in order_alt after an odd pass count
+        if (sort_meta[1] & 1ull) order = order_alt;
+        n = min(n, (int)sort_meta[0]);
+    }
     constexpr int ES_CHUNK = ES_THREADS * ES_ROUNDS;
     __shared__ uint32_t sh[2 * 256];
     __shared__ uint32_t s_wsum[ES_ROUNDS][ES_THREADS / 32];
@@ -428,7 +433,8 @@ __global__ void __launch_bounds__(ES_THREADS) emit_scan_kernel(
 
 int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* counts, int64_t n, int tiles_x,
                      int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals, uint32_t* tile_hist,
-                     int tile_passes, void* ws, unsigned long long* total, cudaStream_t s) {
+                     int tile_passes, void* ws, unsigned long long* total, cudaStream_t s, const uint32_t* order_alt,
+                     const unsigned long long* sort_meta) {
     // small scenes: one Gaussian per thread per chunk (more CTAs in flight);
     // large: 4 rounds per chunk (fewer look-backs)
     const int rounds = n <= (1 << 18) ? 1 : 4;
@@ -441,11 +447,11 @@ int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* 
     if (rounds == 1)
         launch_k(emit_scan_kernel<1>, dim3((unsigned)grid), dim3(ES_THREADS), 0, s, order, (const float4*)xydr4,
                  counts, (int)n, tiles_x, tiles_y, capacity, tile_keys, vals, tile_hist, tile_passes, counter, status,
-                 total);
+                 total, order_alt, sort_meta);
     else
         launch_k(emit_scan_kernel<4>, dim3((unsigned)grid), dim3(ES_THREADS), 0, s, order, (const float4*)xydr4,
                  counts, (int)n, tiles_x, tiles_y, capacity, tile_keys, vals, tile_hist, tile_passes, counter, status,
-                 total);
+                 total, order_alt, sort_meta);
     return check_launch("emit_scan_kernel");
 }
 

@@ -262,6 +262,14 @@ __device__ __forceinline__ void warp_hist_add(uint32_t* h, uint32_t d, bool vali
     }
 }
 
+// The same update aggregated with match_any: one atomic per distinct digit
+// of the warp (for concentrated digits, where per-lane atomics serialise on
+// a few addresses).
+__device__ __forceinline__ void warp_hist_add_match(uint32_t* h, uint32_t d, bool valid) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu);
+    if (valid && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0u) atomicAdd(&h[d], (uint32_t)__popc(peers));
+}
+
 // Shared-memory access through 32-bit shared-window addresses computed once
 // (keeps nvcc from re-deriving generic->shared conversions in hot loops).
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }

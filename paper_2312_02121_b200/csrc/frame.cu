@@ -109,8 +109,9 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.tile_order = take(4 * nt);  // raster launch order (heaviest lists first)
     L.tcount = take(4 * TCOUNT_REPL * nt);  // scatter binning: tile counts, then write cursors
     L.zero_begin = o;
-    L.meta = take(64);  // status, total intersections, capacity needed, direct-binning tile stride,
-                        // accumulators-to-zero flag, reserved
+    L.meta = take(128);  // [0] status [1] total intersections [2] capacity needed [3] direct-binning
+                         // tile stride [4] accumulators-to-zero flag [5,6] visible depth-key min / max
+                         // [7] visible Gaussians [8] depth-sort passes
     L.dhist = take(4 * 256 * 4);
     L.thist = take(4 * 256 * 2);
     L.counters = take(64);
@@ -185,6 +186,7 @@ int gs_frame_view_of(int64_t n, int64_t isect_capacity, int32_t width, int32_t h
     out->conic4 = at<float>(ws, L.conic);
     out->tiles = at<uint32_t>(ws, L.tiles);
     out->depth_order = at<uint32_t>(ws, L.order);
+    out->depth_order_alt = at<uint32_t>(ws, L.order_alt);
     out->sorted_tile_keys = at<uint32_t>(ws, L.tkeys);
     out->sorted_vals = at<uint32_t>(ws, L.tvals);
     out->ranges2 = at<uint32_t>(ws, L.ranges);
@@ -290,15 +292,15 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
         mark(stage_events, 5, s);
         return 0;
     }
-    // 2. depth-first: stable depth sort of all Gaussians (culled ones last)
-    const uint32_t* order = nullptr;
-    {
-        if (run_onesweep<uint32_t>(at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.order),
-                                   at<uint32_t>(ws, L.dkeys_alt), at<uint32_t>(ws, L.order_alt), n, nullptr, 4,
-                                   at<uint32_t>(ws, L.dhist), at<uint32_t>(ws, L.dstatus), counters, s, true))
-            return -1;
-        order = at<uint32_t>(ws, L.order);  // 4 passes: back in the primary buffers
-    }
+    // 2. depth-first: stable depth sort of the visible Gaussians (keys relative
+    //    to the visible minimum, culled ones dropped by the first pass, only the
+    //    passes the key width needs; the order ends in `order_alt` after an odd
+    //    pass count, meta[8])
+    if (run_depth_sort(at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.order), at<uint32_t>(ws, L.dkeys_alt),
+                       at<uint32_t>(ws, L.order_alt), n, meta, at<uint32_t>(ws, L.dhist), at<uint32_t>(ws, L.dstatus),
+                       counters, s))
+        return -1;
+    const uint32_t* order = at<uint32_t>(ws, L.order);
     mark(stage_events, 2, s);
     // 3+4. fused: scan of the tile counts (in depth order), total ->
     //      meta[1], emission of the (tile, gaussian) pairs + tile-digit histograms
@@ -310,7 +312,8 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     uint32_t* k1 = at<uint32_t>(ws, odd ? L.tkeys : L.tkeys_alt);
     uint32_t* v1 = at<uint32_t>(ws, odd ? L.tvals : L.tvals_alt);
     if (launch_emit_scan(order, at<float>(ws, L.xydr), at<uint32_t>(ws, L.tiles), n, tiles_x, tiles_y,
-                         isect_capacity, k0, v0, at<uint32_t>(ws, L.thist), tp, at<char>(ws, L.scan_ws), meta + 1, s))
+                         isect_capacity, k0, v0, at<uint32_t>(ws, L.thist), tp, at<char>(ws, L.scan_ws), meta + 1, s,
+                         at<uint32_t>(ws, L.order_alt), meta + 7))
         return -1;
     mark(stage_events, 3, s);
     // 5. stable sort by tile id (bits [0, 8*tp))

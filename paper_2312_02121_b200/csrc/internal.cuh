@@ -41,6 +41,12 @@ template <typename K>
 int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
                  int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
                  bool identity_vals);
+// Stable sort of the visible Gaussians by depth (frame.cu, depth-first
+// binning): keys relative to meta[5], culled (0xFFFFFFFF) ones dropped by the
+// first pass, later passes over meta[7] items, passes beyond meta[8] skipped.
+// The (keys, ids) end in (k1, v1) when meta[8] is odd, else in (k0, v0).
+int run_depth_sort(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t n_cap,
+                   unsigned long long* meta, uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s);
 template <typename K>
 int launch_sort_hist(const K* keys, int64_t n_cap, const unsigned long long* n_dev, int passes, uint32_t* hist,
                      cudaStream_t s);
@@ -57,7 +63,10 @@ int launch_emit_sorted(const uint32_t* order, const float* xydr4, const uint32_t
 size_t emit_scan_ws_bytes(int64_t n);
 int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* counts, int64_t n, int tiles_x,
                      int tiles_y, int64_t capacity, uint32_t* tile_keys, uint32_t* vals, uint32_t* tile_hist,
-                     int tile_passes, void* ws, unsigned long long* total, cudaStream_t s);
+                     int tile_passes, void* ws, unsigned long long* total, cudaStream_t s,
+                     const uint32_t* order_alt = nullptr, const unsigned long long* sort_meta = nullptr);
+// sort_meta (depth-first frame, = meta + 7): [0] the number of sorted (visible)
+// Gaussians, [1] the depth-sort pass count (odd: the order is in order_alt)
 // scatter binning: tile scan (ranges, cursors, total, optional raster order)
 // and the unordered scatter of the (tile, gaussian) pairs
 int launch_tile_scan(uint32_t* tcount, int n_tiles, int64_t capacity, uint2* ranges, unsigned long long* total,

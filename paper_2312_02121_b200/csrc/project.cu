@@ -25,9 +25,9 @@ __device__ __forceinline__ void report(unsigned long long* status, int i, int co
 // and the tile count of the bbox square (sg/binning.py:35-46).
 // MODE 1 / 2 (frame path): also write the depth sort key of every Gaussian
 // (float bits of the camera depth for visible ones, 0xFFFFFFFF for culled
-// ones so they sort last).  MODE 1 (depth-first binning) accumulates the
-// four 8-bit digit histograms of those keys for the onesweep depth sort
-// that follows (sort.cu), in shared memory; MODE 2 (scatter binning) counts
+// ones).  MODE 1 (depth-first binning) reduces the range [kmin, kmax] of the
+// visible keys into meta[5] / meta[6] for the depth sort that follows
+// (sort.cu: keys relative to kmin, culled ones dropped); MODE 2 (scatter binning) counts
 // every tile's intersections instead (tcount, one red.add per pair); MODE 3
 // (direct binning) takes a slot in the tile's fixed-stride bin for every
 // pair (atomicAdd with return on one of the tile's DREPL counters, 4
@@ -50,11 +50,9 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
     constexpr bool DKEY = MODE != 0;
     griddep_wait();
     run_zero_jobs(zj);  // frame path: clear the later stages' counters / accumulators
-    __shared__ uint32_t s_hist[MODE == 1 ? 4 * 256 : 1];
-    if (MODE == 1) {
-        for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) s_hist[k] = 0;
-        __syncthreads();
-    }
+    // MODE 1: the range [kmin, kmax] of the visible depth keys, so the depth
+    // sort ranks keys relative to kmin and skips the passes above its width
+    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
     // grid-stride over Gaussians (warps stay converged for the histogram
     // vote); the shared histograms are flushed once per CTA
     const int n_round = (n + 31) & ~31;
@@ -174,19 +172,17 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
                             if (tl[0] != 0xFFFFFFFFu) atomicAdd(&tc[tl[0]], 1u);
                         });
     }
-    if (MODE == 1) {
-        const bool valid = i < n;
-        // low bytes of the depth bits are spread (per-lane atomics), high
-        // bytes and culled keys concentrated (warp-uniform fast path)
-#pragma unroll
-        for (int p = 0; p < 4; ++p) warp_hist_add(s_hist + 256 * p, (dkey >> (8 * p)) & 255u, valid);
+    if (MODE == 1 && dkey != 0xFFFFFFFFu) {
+        kmin = min(kmin, dkey);
+        kmax = max(kmax, dkey);
     }
     }  // grid-stride
-    if (MODE == 1) {
-        __syncthreads();
-        for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) {
-            const uint32_t v = s_hist[k];
-            if (v) atomicAdd(&dhist[k], v);
+    if (MODE == 1) {  // one atomic pair per warp (meta[5] / meta[6], reset by frame_init_kernel)
+        kmin = __reduce_min_sync(0xffffffffu, kmin);
+        kmax = __reduce_max_sync(0xffffffffu, kmax);
+        if ((threadIdx.x & 31) == 0 && kmin <= kmax) {
+            atomicMin(reinterpret_cast<unsigned long long*>(status) + 5, (unsigned long long)kmin);
+            atomicMax(reinterpret_cast<unsigned long long*>(status) + 6, (unsigned long long)kmax);
         }
     }
 }
@@ -215,7 +211,13 @@ __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
     float* __restrict__ d_view16, unsigned long long* __restrict__ clean_word, unsigned long long clean_sig,
     bool clear_accum) {
     griddep_wait();
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    // grid-stride over Gaussians (resident blocks): d_view is accumulated per
+    // thread over its Gaussians and reduced once per block, so the fixed-order
+    // reduction of the block partials (view_reduce_kernel) stays short
+    float dva[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) dva[k] = 0.f;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     // the visibility word first: a culled Gaussian's gradient is exactly
     // zero (sg/proj_backward.py:200-203 loops over `projected` only), so its
     // parameters and (never touched) accumulator rows are not read at all
@@ -397,6 +399,9 @@ __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
         __stcs(d_geo + (size_t)i * gstride, z);
         __stcs(d_c11 + i, 0.f);
     }
+#pragma unroll
+    for (int k = 0; k < 12; ++k) dva[k] += dv[k];
+    }  // grid-stride
     // block partial of d_view (deterministic: fixed shuffle tree + fixed warp
     // order).  Transposed warp reduction of the 12 values padded to 16: each
     // level exchanges half of the values, so 16 shuffles instead of 60.
@@ -405,7 +410,7 @@ __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
     {
         float v16[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v16[k] = k < 12 ? dv[k] : 0.f;
+        for (int k = 0; k < 16; ++k) v16[k] = k < 12 ? dva[k] : 0.f;
 #pragma unroll
         for (int h = 8, m = 16; h >= 1; h >>= 1, m >>= 1) {  // lane bit m selects the kept half
             const bool up = lane & m;
@@ -492,6 +497,10 @@ __global__ void __launch_bounds__(256) frame_init_kernel(unsigned long long* __r
                 meta[4] = *clean_word != clean_sig ? 1ull : 0ull;
                 *clean_word = clean_sig;
             }
+            meta[5] = 0xFFFFFFFFull;  // visible depth-key range (depth-first binning)
+            meta[6] = 0ull;
+            meta[7] = 0ull;           // visible Gaussians (depth_hist_kernel)
+            meta[8] = 4ull;           // depth-sort passes
         }
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) dhist[k] = 0u;
     }
@@ -534,7 +543,9 @@ int launch_project_bwd(const float* means3, const float* scales3, const float* q
                        bool accumulate, int gstride, const float* rgbo_in, float* rgbo_out,
                        unsigned int* done_counter, unsigned long long* clean_word, unsigned long long clean_sig,
                        bool clear_accum) {
-    const int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
+    int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
+    const int resident = sort_sm_count() * PBWD_MINB;
+    if (blocks > resident) blocks = resident;
     if (blocks > 0) {
         launch_k(project_bwd_kernel, dim3(blocks), dim3(PBWD_THREADS), 0, s, means3, scales3, (const float4*)quats4,
                  (int)n, k, tiles, (float4*)d_geo4, const_cast<float*>(d_c11), d_means3, d_scales3,

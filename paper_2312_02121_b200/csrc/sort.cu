@@ -120,12 +120,18 @@ constexpr int sort_minb() {
     return sizeof(K) == 4 ? (ITEMS <= 8 ? 5 : (ITEMS <= 12 ? 4 : (ITEMS <= 16 ? 3 : 2))) : 2;
 }
 
+// rel_min (uint32 keys, depth sort pass 0): keys are taken relative to
+// *rel_min and 0xFFFFFFFF keys (culled Gaussians) are dropped -- the output
+// holds only the valid items, in order.  npass_dev: the pass is skipped
+// entirely when `pass` >= *npass_dev (the relative keys are narrower).
 template <typename K, int ITEMS, bool RANK_OR>
 __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) onesweep_kernel(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_cap, const unsigned long long* __restrict__ n_dev, int shift,
-    const uint32_t* __restrict__ hist, uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
+    const uint32_t* __restrict__ hist, uint32_t* __restrict__ status, uint32_t* __restrict__ counter,
+    const unsigned long long* __restrict__ rel_min, const unsigned long long* __restrict__ npass_dev, int pass) {
     griddep_wait();
+    if (npass_dev && pass >= (int)*npass_dev) return;
     constexpr int TILE_N = sort_tile<K, ITEMS>();
     extern __shared__ __align__(16) unsigned char smem[];
     K* s_keys = reinterpret_cast<K*>(smem);
@@ -136,6 +142,7 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
     uint32_t* s_peers = s_lstart + RADIX;              // [warp][2][digit] peer masks (RANK_OR)
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_tmp[SORT_WARPS];
+    __shared__ uint32_t s_total;
 
     const int64_t n = resolve_n(n_dev, n_cap);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -154,11 +161,19 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
     K key[ITEMS];
     uint32_t val[ITEMS];
     uint32_t rank[ITEMS];
+    uint32_t okm = 0;  // valid items (bit i)
+    const K kmin = rel_min ? (K)*rel_min : (K)0;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int64_t idx = wbase + i * 32 + lane;
         key[i] = idx < n ? kin[idx] : (K)0;
         val[i] = idx < n ? (vin ? vin[idx] : (uint32_t)idx) : 0u;
+        bool ok = idx < n;
+        if (rel_min) {
+            ok = ok && key[i] != (K)0xFFFFFFFFu;
+            key[i] -= kmin;
+        }
+        okm |= ok ? (1u << i) : 0u;
     }
     // warp-local stable ranking: items in (i, lane) order = input order
     const uint32_t lt = lanemask_lt();
@@ -168,8 +183,7 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
         uint32_t* s_peer = s_peers + warp * 2 * RADIX;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const int64_t idx = wbase + i * 32 + lane;
-            const bool valid = idx < n;
+            const bool valid = (okm >> i) & 1u;
             const uint32_t d = (uint32_t)(key[i] >> shift) & 255u;
             uint32_t* pm = s_peer + (i & 1) * RADIX + d;
             if (valid) atomicOr(pm, 1u << lane);
@@ -186,8 +200,7 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
     } else {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const int64_t idx = wbase + i * 32 + lane;
-            const bool valid = idx < n;
+            const bool valid = (okm >> i) & 1u;
             const uint32_t d = valid ? (uint32_t)(key[i] >> shift) & 255u : 256u;
             const uint32_t peers = __match_any_sync(0xffffffffu, d);
             const int leader = __ffs(peers) - 1;
@@ -241,13 +254,13 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
     const uint32_t lincl = block_incl_scan256(run, s_tmp);
     const uint32_t hincl = block_incl_scan256(h, s_tmp);
     const uint32_t lstart = lincl - run;
+    if (d == RADIX - 1) s_total = lincl;  // valid items of the tile
     s_lstart[d] = lstart;
     s_gbase[d] = (hincl - h) + excl - lstart;  // mod 2^32; dst = gbase + local slot
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const int64_t idx = wbase + i * 32 + lane;
-        if (idx < n) {
+        if ((okm >> i) & 1u) {
             const uint32_t dd = (uint32_t)(key[i] >> shift) & 255u;
             const uint32_t pos = s_lstart[dd] + s_whist[warp * RADIX + dd] + rank[i];
             s_keys[pos] = key[i];
@@ -255,8 +268,7 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
         }
     }
     __syncthreads();
-    const int64_t rem = n - (int64_t)tile * TILE_N;
-    const int cnt = rem < TILE_N ? (int)rem : TILE_N;
+    const int cnt = (int)s_total;
     for (int j = tid; j < cnt; j += SORT_THREADS) {
         const K k = s_keys[j];
         const uint32_t dd = (uint32_t)(k >> shift) & 255u;
@@ -313,10 +325,16 @@ static bool rank_or() {
     return v == 1;
 }
 
+struct PassOpts {  // depth sort: pass 0 relative + compacting, later passes on the compacted count
+    const unsigned long long* n_dev_rest = nullptr;
+    const unsigned long long* rel_min0 = nullptr;
+    const unsigned long long* npass_dev = nullptr;
+};
+
 template <typename K, int ITEMS, bool RANK_OR>
 static int run_passes_t(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
                         int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
-                        bool identity_vals) {
+                        bool identity_vals, const PassOpts& po = PassOpts()) {
     if (set_sort_attr<K, ITEMS, RANK_OR>()) return -1;
     const int64_t tiles = (n_cap + sort_tile<K, ITEMS>() - 1) / sort_tile<K, ITEMS>();
     K* kin = k0;
@@ -326,8 +344,9 @@ static int run_passes_t(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap,
     for (int p = 0; p < passes; ++p) {
         launch_k(onesweep_kernel<K, ITEMS, RANK_OR>, dim3((unsigned)tiles), dim3(SORT_THREADS),
                  sort_smem<K, ITEMS>(), s, (const K*)kin, (const uint32_t*)((p == 0 && identity_vals) ? nullptr : vin),
-                 kout, vout, n_cap, n_dev, 8 * p, (const uint32_t*)(hist + p * RADIX),
-                 status + (size_t)p * tiles * RADIX, counters + p);
+                 kout, vout, n_cap, (p > 0 && po.n_dev_rest) ? po.n_dev_rest : n_dev, 8 * p,
+                 (const uint32_t*)(hist + p * RADIX), status + (size_t)p * tiles * RADIX, counters + p,
+                 p == 0 ? po.rel_min0 : nullptr, po.npass_dev, p);
         if (check_launch("onesweep_kernel")) return -1;
         K* tk = kin; kin = kout; kout = tk;
         uint32_t* tv = vin; vin = vout; vout = tv;
@@ -338,12 +357,12 @@ static int run_passes_t(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap,
 template <typename K, int ITEMS>
 static int run_passes(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
                       int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,
-                      bool identity_vals) {
+                      bool identity_vals, const PassOpts& po = PassOpts()) {
     if (rank_or())
         return run_passes_t<K, ITEMS, true>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s,
-                                            identity_vals);
+                                            identity_vals, po);
     return run_passes_t<K, ITEMS, false>(k0, v0, k1, v1, n_cap, n_dev, passes, hist, status, counters, s,
-                                         identity_vals);
+                                         identity_vals, po);
 }
 
 template <typename K>
@@ -385,6 +404,83 @@ template int run_onesweep<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, 
 template int run_onesweep<unsigned long long>(unsigned long long*, uint32_t*, unsigned long long*, uint32_t*,
                                               int64_t, const unsigned long long*, int, const uint32_t*,
                                               uint32_t*, uint32_t*, cudaStream_t, bool);
+
+// Digit histograms of the visible Gaussians' depth keys relative to the
+// visible minimum (meta[5]; culled keys are 0xFFFFFFFF), their count V
+// (meta[7], reset by frame_init_kernel) and the number of 8-bit passes the
+// relative keys need (meta[8]: the width of meta[6] - meta[5]).
+__global__ void __launch_bounds__(256) depth_hist_kernel(const uint32_t* __restrict__ keys, int64_t n,
+                                                         unsigned long long* __restrict__ meta,
+                                                         uint32_t* __restrict__ hist) {
+    griddep_wait();
+    __shared__ uint32_t sh[4 * RADIX];
+    __shared__ uint32_t s_cnt;
+    for (int k = threadIdx.x; k < 4 * RADIX; k += blockDim.x) sh[k] = 0;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const uint32_t kmin = (uint32_t)meta[5], kmax = (uint32_t)meta[6];
+    const uint32_t range = kmin <= kmax ? kmax - kmin : 0u;
+    const int npass = range == 0u ? 1 : (32 - __clz((int)range) + 7) / 8;
+    // 8 keys per thread per round (two 16-byte loads in flight): the loop is
+    // latency-bound with one key per load (33 us at config 3 -> ~10 us)
+    constexpr int KPT = 8;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * KPT;
+    const int64_t n_round = (n + 32 * KPT - 1) / (32 * KPT) * (32 * KPT);
+    uint32_t cnt = 0;
+    for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * KPT; base < n_round; base += stride) {
+        uint32_t kk[KPT];
+        if (base + KPT <= n) {
+            const uint4 a = *reinterpret_cast<const uint4*>(keys + base);
+            const uint4 b = *reinterpret_cast<const uint4*>(keys + base + 4);
+            kk[0] = a.x; kk[1] = a.y; kk[2] = a.z; kk[3] = a.w; kk[4] = b.x; kk[5] = b.y; kk[6] = b.z; kk[7] = b.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) kk[j] = base + j < n ? keys[base + j] : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            const uint32_t key = kk[j];
+            const bool valid = key != 0xFFFFFFFFu;
+            const uint32_t rel = key - kmin;
+            cnt += valid;
+            warp_hist_add(sh, rel & 255u, valid);
+            warp_hist_add(sh + RADIX, (rel >> 8) & 255u, valid);
+            if (npass > 2) warp_hist_add(sh + 2 * RADIX, (rel >> 16) & 255u, valid);
+            if (npass > 3) warp_hist_add(sh + 3 * RADIX, rel >> 24, valid);
+        }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_cnt, cnt);
+    __syncthreads();
+    for (int k = threadIdx.x; k < 4 * RADIX; k += blockDim.x) {
+        const uint32_t v = sh[k];
+        if (v) atomicAdd(&hist[k], v);
+    }
+    if (threadIdx.x == 0) {
+        if (s_cnt) atomicAdd(&meta[7], (unsigned long long)s_cnt);
+        if (blockIdx.x == 0) meta[8] = (unsigned long long)npass;
+    }
+}
+
+int run_depth_sort(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t n_cap,
+                   unsigned long long* meta, uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s) {
+    if (n_cap <= 0) return 0;
+    int64_t hb = (n_cap + 256 * 8 - 1) / (256 * 8);
+    const int64_t lim = (int64_t)sort_sm_count() * 4;
+    if (hb > lim) hb = lim;
+    launch_k(depth_hist_kernel, dim3((unsigned)hb), dim3(256), 0, s, (const uint32_t*)k0, n_cap, meta, hist);
+    if (check_launch("depth_hist_kernel")) return -1;
+    PassOpts po;
+    po.n_dev_rest = meta + 7;
+    po.rel_min0 = meta + 5;
+    po.npass_dev = meta + 8;
+    constexpr int BIG = SortCfg<uint32_t>::ITEMS;
+    const int64_t big_tiles = (n_cap + sort_tile<uint32_t, BIG>() - 1) / sort_tile<uint32_t, BIG>();
+    if (big_tiles < 64)
+        return run_passes<uint32_t, SMALL_ITEMS>(k0, v0, k1, v1, n_cap, nullptr, 4, hist, status, counters, s, true,
+                                                 po);
+    return run_passes<uint32_t, BIG>(k0, v0, k1, v1, n_cap, nullptr, 4, hist, status, counters, s, true, po);
+}
 
 template <typename K>
 int launch_sort_hist(const K* keys, int64_t n_cap, const unsigned long long* n_dev, int passes, uint32_t* hist,

@@ -154,7 +154,7 @@ class RenderStep:
                 fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et, capacity=self.caps[vi],
                                        check_meta=False, ws=self.wss[vi])
                 ops.frame_backward(fr, m, sc, q, c, d, out=out, accumulate=vi > 0, wait_before_accumulate=bwd_done)
-                s["meta"][vi].copy_(fr.meta())
+                s["meta"][vi].copy_(fr.meta()[:4])
                 if len(sts) > 1:
                     bwd_done = torch.cuda.Event()
                     bwd_done.record(st)

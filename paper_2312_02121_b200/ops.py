@@ -398,10 +398,12 @@ class Frame:
     def meta(self) -> torch.Tensor:
         """The device meta words: [0] status, [1] total intersections, [2]
         capacity needed (direct binning: tiles x the longest list), [3] the
-        direct-binning tile stride (0: compact bins)."""
+        direct-binning tile stride (0: compact bins), [4] the forward zeroed
+        the backward accumulators, [5,6] the visible depth keys' min / max,
+        [7] visible Gaussians, [8] depth-sort passes (depth-first binning)."""
         v = self.view()
         off = v.meta - self.ws.data_ptr()
-        return self.ws[off:off + 32].view(torch.int64)
+        return self.ws[off:off + 72].view(torch.int64)
 
     def _meta_host(self) -> tuple:
         if self.meta_host is None:
@@ -444,8 +446,11 @@ class Frame:
         else:
             sorted_vals = sl(v.sorted_vals, m, torch.int32, (m,))
             sorted_tile_keys = sl(v.sorted_tile_keys, m, torch.int32, (m,))
+        mh = self._meta_host()
+        n_sorted = min(mh[7], n)  # depth-first binning: the visible Gaussians by (depth, index)
+        dptr = v.depth_order_alt if mh[8] & 1 else v.depth_order
         return dict(xydr=sl(v.xydr4, 4 * n, torch.float32, (n, 4)), conic=sl(v.conic4, 4 * n, torch.float32, (n, 4)),
-                    tiles=sl(v.tiles, n, torch.int32, (n,)), depth_order=sl(v.depth_order, n, torch.int32, (n,)),
+                    tiles=sl(v.tiles, n, torch.int32, (n,)), depth_order=sl(dptr, n_sorted, torch.int32, (n_sorted,)),
                     sorted_tile_keys=sorted_tile_keys, sorted_vals=sorted_vals, ranges=ranges,
                     d_geo=sl(v.d_geo4 - 16, 8 * n, torch.float32, (n, 8))[:, 4:8],  # rows of [d_rgbo | d_geo]
                     d_c11=sl(v.d_c11, n, torch.float32, (n,)),

@@ -90,8 +90,44 @@ def test_depth_order_is_stable_sort(cuda):
     depth = tv["xydr"][:, 2].cpu().numpy()
     vis = tv["tiles"].cpu().numpy() > 0
     key = np.where(vis, depth.view(np.uint32), np.uint32(0xFFFFFFFF)).astype(np.uint64)
-    ref = np.lexsort((np.arange(len(key)), key))
+    ref = np.lexsort((np.arange(len(key)), key))[:int(vis.sum())]  # culled ones are dropped
     assert np.array_equal(order, ref)
+
+
+@pytest.mark.parametrize("depth_lo,depth_hi,passes", [(3.0, 3.0, 1), (2.0, 7.9, 3), (0.02, 90.0, 4), (1.0, 1.0001, 2)])
+def test_depth_sort_relative_keys(depth_lo, depth_hi, passes, cuda):
+    """The depth sort ranks keys relative to the visible minimum and runs
+    only the 8-bit passes their width needs (meta[8]); culled Gaussians are
+    dropped by the first pass.  Order = stable (depth bits, index) of the
+    visible ones, whatever the width; bins equal the 64-bit staged sort."""
+    from paper_2312_02121_b200 import ops
+    rng = np.random.default_rng(int(depth_hi * 100))
+    n = 60000
+    z = rng.uniform(depth_lo, depth_hi, n) if depth_hi > depth_lo else np.full(n, depth_lo)
+    z[::7] = -1.0  # behind the camera: culled
+    means = np.stack([rng.uniform(-0.3, 0.3, n) * z, rng.uniform(-0.3, 0.3, n) * z, z], 1)
+    means[::11, 0] += 50.0 * np.abs(z[::11])  # off-screen: culled
+    scales = np.exp(rng.uniform(np.log(0.002), np.log(0.01), (n, 3))) * np.abs(z)[:, None]
+    quats = rng.normal(size=(n, 4))
+    opac = rng.uniform(0.05, 0.95, n)
+    colors = rng.uniform(0, 1, (n, 3))
+    t = _tensors((means, scales, quats, opac, colors), cuda)
+    cp = ops.CameraParams(np.eye(4).tolist(), 300.0, 300.0, 320.0, 240.0, 640, 480, 0.01, 100.0)
+    ops.set_option("binning", 1)
+    try:
+        fr = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True)
+    finally:
+        ops.set_option("binning", 0)
+    meta = fr.meta().cpu().numpy()
+    tv = fr.tensors()
+    vis = tv["tiles"].cpu().numpy() > 0
+    assert int(meta[7]) == int(vis.sum()) and int(meta[8]) == passes, (meta[5:9], passes)
+    depth = tv["xydr"][:, 2].cpu().numpy().view(np.uint32).astype(np.uint64)
+    key = np.where(vis, depth, np.uint64(0xFFFFFFFF))
+    ref = np.lexsort((np.arange(n), key))[:int(vis.sum())]
+    assert np.array_equal(tv["depth_order"].cpu().numpy(), ref)
+    img_s, st = ops.render_forward(*t, cp, (0.0, 0.0, 0.0), True)
+    assert torch.equal(tv["sorted_vals"], st.bins.sorted_vals) and torch.equal(fr.image, img_s)
 
 
 @pytest.mark.parametrize("config", [0, 1])
