@@ -283,10 +283,14 @@ def run_ours(args):
                 fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, capacity=caps[vi], check_meta=False,
                                        ws=wss[vi], events=ev_f[vi] if staged else None)
                 # only the views' accumulation into grad_out is ordered: this view's raster
-                # backward overlaps the previous view's projection backward
+                # backward overlaps the previous view's projection backward.  N > 1: the
+                # last view's projection backward runs after the graph, bucketed under the
+                # all-reduce (view shards), or after the screen-space all-reduce (bands)
+                tail = world > 1 and vi == len(cams) - 1
                 ops.frame_backward(fr, m, s, q, c, d_img,
                                    events=ev_b[vi] if staged else [ev_t[vi][0], ev_t[vi][1], None],
-                                   out=grad_out, accumulate=vi > 0, wait_before_accumulate=bwd_done)
+                                   out=grad_out, accumulate=vi > 0, wait_before_accumulate=bwd_done,
+                                   project=not tail)
                 if two:
                     bwd_done = torch.cuda.Event()
                     bwd_done.record(st)
@@ -311,13 +315,24 @@ def run_ours(args):
         with torch.cuda.graph(graph_staged):
             step(True)
 
+    from paper_2312_02121_b200 import dist as D
+    reducer = D.GradReducer(n, buckets=4) if world > 1 and band is None else None
+    d_view_tail = torch.zeros((4, 4), device=dev, dtype=torch.float32)
+
     def run_step(staged=False):
         if graph is not None:
             (graph_staged if staged else graph).replay()
         else:
             step(staged)
         if world > 1:
-            dist.all_reduce(grad_flat)
+            fr = frames_out[-1]
+            if band is None:  # view shards: 14 fp32 per Gaussian, all-reduced under the last projection bwd
+                reducer.wait(reducer.last_view(fr, params, grad_out, d_view_tail, accumulate=len(cams) > 1))
+            else:  # tile bands: 9 screen-space fp32 per Gaussian, then the projection bwd on every rank
+                rows, c11 = ops.frame_screen_grads(fr)
+                dist.all_reduce(rows)
+                dist.all_reduce(c11)
+                ops.frame_project_backward(fr, m, s, q, grad_out, d_view_tail, vis_from_grads=True)
 
     for _ in range(max(args.warmup, 0)):
         run_step()
@@ -496,7 +511,10 @@ def run_ours(args):
         "config": bench_config(cfg, world,
                                parallelism=(f"tile-row bands x{world} (rows {band})" if band else
                                             f"view-sharded x{world}") +
-                               (" + NCCL allreduce 14 fp32/Gaussian" if world > 1 else ""),
+                               ((" + NCCL all-reduce of 9 screen-space fp32/Gaussian, then the projection "
+                                 "backward on every rank") if band else
+                                (" + NCCL all-reduce 14 fp32/Gaussian in 4 buckets overlapped with the last "
+                                 "view's projection backward") if world > 1 else ""),
                                views_per_rank=len(cams), cuda_graph=graph is not None,
                                view_streams=min(args.streams, len(cams)),
                                l2="flushed between timed steps (192 MiB write, untimed)"),
@@ -504,13 +522,16 @@ def run_ours(args):
         "intersections_per_step_rank": int(I),
         "e2e": e2e,
         # per view (csrc/frame.cu): direct binning: init, project (+ pairs into the tile bins),
-        # raster fwd (+ the per-tile sort) | raster bwd, project bwd; scatter binning: init, project
-        # (+ tile counts), tile scan (+ raster order), pair scatter, [per-tile sort,] raster fwd |
-        # raster bwd, project bwd; depth-first: init, project, 4 depth passes, fused scan+emit, tp
-        # tile passes, ranges, (tile order for grids over one raster wave), raster fwd | raster bwd,
-        # project bwd
-        "gpu_launches": int(args.steps * len(cams) * (5 if direct else (7 if fused else 8) if seg else
-                                                      11 + tp + tile_order_launches(cams[0]))),
+        # raster fwd (+ the per-tile sort) | raster bwd, project bwd, view reduce; scatter binning:
+        # init, project (+ tile counts), tile scan (+ raster order), pair scatter, [per-tile sort,]
+        # raster fwd | raster bwd, project bwd, view reduce; depth-first: init, project, depth
+        # histogram, 4 depth passes, fused scan+emit, tp tile passes, ranges, (tile order for grids
+        # over one raster wave), raster fwd | raster bwd, project bwd, view reduce
+        # (depth-first: + the depth histogram, the view reduce; depth passes skipped on the
+        # device beyond the key width still launch)
+        "gpu_launches": int(args.steps * (len(cams) * (6 if direct else (8 if fused else 9) if seg else
+                                                       13 + tp + tile_order_launches(cams[0])) +
+                                          (0 if world == 1 else 2 if band else 2 * len(reducer.bounds)))),
         "binning": binning,
         "roofline": roof,
         "stages": st,

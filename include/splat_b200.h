@@ -241,13 +241,31 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
  * clear (default): the projection backward zeroes them as it reads them.
  * Bit 2 set: stage_events has a 4th entry, an event `stream` waits on before
  * the projection backward (a multi-view step serialises only the views'
- * read-modify-write accumulation; their raster backwards may overlap). */
+ * read-modify-write accumulation; their raster backwards may overlap).
+ * Bit 3 set: raster backward only -- the screen-space gradients stay in the
+ * workspace (gs_frame_view d_geo4 rows + d_c11, d_rgbo in the first half of
+ * each row) for a reduction across ranks, then gs_frame_project_backward. */
 int gs_frame_backward(const float* means3, const float* scales3, const float* quats4, const float* colors3,
                       int64_t n, const gs_camera* cam /*[host]*/, const float* background3 /*[host]*/,
                       int64_t isect_capacity, void* ws, size_t ws_bytes, const float* final_T,
                       const int32_t* n_contrib, const float* d_image, float* d_means3, float* d_scales3,
                       float* d_quats4, float* d_rgbo4, float* d_view16, int accumulate,
                       unsigned long long* counts3, void* const* stage_events, gs_stream_t stream);
+
+/* The projection backward of a frame (the second half of gs_frame_backward,
+ * sg/proj_backward.py:178-223) over the Gaussians [begin, end), from the
+ * screen-space gradients in the workspace (after gs_frame_backward with
+ * bit 3, possibly summed across ranks in place).  Outputs are indexed by
+ * scene Gaussian (rows begin..end-1 written).  flags: bit 0 add into the
+ * outputs, bit 1 keep the screen-space rows (else cleared as read), bit 4
+ * add this range's d_view into d_view16 (else overwrite), bit 5 treat a
+ * Gaussian as visible when its screen-space row is non-zero even if this
+ * frame culled it (rows summed over tile bands of one frame).  Ranges let a
+ * caller start reducing finished Gaussian buckets while later ones run.   */
+int gs_frame_project_backward(const float* means3, const float* scales3, const float* quats4, int64_t n,
+                              const gs_camera* cam /*[host]*/, int64_t isect_capacity, void* ws, size_t ws_bytes,
+                              int64_t begin, int64_t end, float* d_means3, float* d_scales3, float* d_quats4,
+                              float* d_rgbo4, float* d_view16, int flags, gs_stream_t stream);
 
 /* ---- Training step around the path (sg/optimize.py:96-190 fit) ----------
  * gs_activate : scales = exp(log_scales), opacities = sigmoid(logits)  (:144-145)

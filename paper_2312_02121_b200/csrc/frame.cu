@@ -377,6 +377,15 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
     // raster backward (its own workspace) overlaps the previous view's
     // projection backward
     const bool keep = (accumulate & 2) != 0;
+    if (accumulate & 8) {
+        // raster backward only: the screen-space gradients stay in the
+        // workspace for a reduction across ranks (tile bands) and
+        // gs_frame_project_backward; until then the accumulators are dirty
+        if (cudaMemsetAsync(at<char>(ws, L.clean), 0, 8, s) != cudaSuccess)
+            return check_launch("gs_frame_backward: clean word");
+        mark(stage_events, 2, s);
+        return 0;
+    }
     if ((accumulate & 4) && stage_events && stage_events[3] &&
         cudaStreamWaitEvent(s, (cudaEvent_t)stage_events[3], 0) != cudaSuccess)
         return check_launch("gs_frame_backward: wait event");
@@ -387,6 +396,29 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
         return -1;
     mark(stage_events, 2, s);
     return 0;
+}
+
+int gs_frame_project_backward(const float* means3, const float* scales3, const float* quats4, int64_t n,
+                              const gs_camera* cam, int64_t isect_capacity, void* ws, size_t ws_bytes, int64_t begin,
+                              int64_t end, float* d_means3, float* d_scales3, float* d_quats4, float* d_rgbo4,
+                              float* d_view16, int flags, gs_stream_t stream) {
+    if (!cam) return set_error("gs_frame_project_backward: null camera");
+    if (begin < 0 || end > n || begin > end)
+        return set_error("gs_frame_project_backward: range [%lld, %lld) outside [0, %lld)", (long long)begin,
+                         (long long)end, (long long)n);
+    const int W = cam->width, H = cam->height;
+    const Layout L = layout(n, isect_capacity, W, H);
+    if (ws_bytes < L.total) return set_error("gs_frame_project_backward: workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    const CamK k = make_camk(*cam);
+    float* g8 = at<float>(ws, L.d_geo) + 8 * begin;
+    const bool keep = (flags & 2) != 0;
+    return launch_project_bwd(means3 + 3 * begin, scales3 + 3 * begin, quats4 + 4 * begin, end - begin, k,
+                              at<uint32_t>(ws, L.tiles) + begin, g8 + 4, at<float>(ws, L.d_c11) + begin,
+                              d_means3 + 3 * begin, d_scales3 + 3 * begin, d_quats4 + 4 * begin, d_view16,
+                              at<float>(ws, L.partials), s, (flags & 1) != 0, 2, g8, d_rgbo4 + 4 * begin, nullptr,
+                              at<unsigned long long>(ws, L.clean), clean_sig(n, isect_capacity, W, H), !keep,
+                              (flags & 16) != 0, (flags & 32) != 0);
 }
 
 }  // extern "C"

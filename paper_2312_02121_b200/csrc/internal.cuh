@@ -24,7 +24,7 @@ int launch_project_bwd(const float* means3, const float* scales3, const float* q
                        bool accumulate = false, int gstride = 1, const float* rgbo_in = nullptr,
                        float* rgbo_out = nullptr, unsigned int* done_counter = nullptr,
                        unsigned long long* clean_word = nullptr, unsigned long long clean_sig = 0,
-                       bool clear_accum = false);
+                       bool clear_accum = false, bool add_view = false, bool vis_from_grads = false);
 // clear_accum (frame path): every visible Gaussian's screen-space accumulator
 // row (d_geo4 row + d_rgbo row + d_c11) is zeroed after it is read, and the
 // last block stamps *clean_word = clean_sig (0 when not clearing), which the

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
     float4* __restrict__ d_quats, float* __restrict__ view_partials, bool accumulate, int gstride,
     float4* __restrict__ rgbo_in, float4* __restrict__ rgbo_out, unsigned int* __restrict__ done_counter,
     float* __restrict__ d_view16, unsigned long long* __restrict__ clean_word, unsigned long long clean_sig,
-    bool clear_accum) {
+    bool clear_accum, bool vis_from_grads) {
     griddep_wait();
     // grid-stride over Gaussians (resident blocks): d_view is accumulated per
     // thread over its Gaussians and reduced once per block, so the fixed-order
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
     // parameters and (never touched) accumulator rows are not read at all
     const bool in = i < n;
     const uint32_t nt = in ? tiles[i] : 0u;
-    const bool vis = in && nt != 0u;
+    bool vis = in && nt != 0u;
     float4 v_rgbo = make_float4(0.f, 0.f, 0.f, 0.f), gg = make_float4(0.f, 0.f, 0.f, 0.f);
     float g11 = 0.f;
     float mx = 0.f, my = 0.f, mz = 0.f, s[3] = {1.f, 1.f, 1.f};
@@ -248,6 +248,13 @@ __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
             if (rgbo_in && !PBWD_RGBO_EARLY) orgbo = rgbo_out[i];
         }
     }
+    // tile bands (dist.py): the screen-space gradients were summed over the
+    // ranks' bands, so a Gaussian culled from this rank's band may carry
+    // another band's gradient; only non-zero rows can (a Gaussian culled by
+    // depth has none anywhere, so its undefined projection is never touched)
+    if (vis_from_grads && in && !vis)
+        vis = gg.x != 0.f || gg.y != 0.f || gg.z != 0.f || gg.w != 0.f || g11 != 0.f || v_rgbo.x != 0.f ||
+              v_rgbo.y != 0.f || v_rgbo.z != 0.f || v_rgbo.w != 0.f;
     if (PBWD_RGBO_EARLY && rgbo_in && in && (vis || !accumulate)) {
         if (accumulate) {
             const float4 o = rgbo_out[i];
@@ -462,7 +469,7 @@ __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
 __global__ void __launch_bounds__(384) view_reduce_kernel(const float* __restrict__ partials, int nblocks,
                                                           float* __restrict__ d_view16,
                                                           unsigned long long* __restrict__ clean_word,
-                                                          unsigned long long clean_stamp) {
+                                                          unsigned long long clean_stamp, bool add) {
     griddep_wait();
     if (clean_word && threadIdx.x == 0) *clean_word = clean_stamp;
     const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -470,7 +477,7 @@ __global__ void __launch_bounds__(384) view_reduce_kernel(const float* __restric
     for (int b = lane; b < nblocks; b += 32) v += partials[b * 12 + k];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) d_view16[k] = v;
+    if (lane == 0) d_view16[k] = add ? d_view16[k] + v : v;
     if (threadIdx.x < 4) d_view16[12 + threadIdx.x] = 0.f;
 }
 
@@ -542,7 +549,7 @@ int launch_project_bwd(const float* means3, const float* scales3, const float* q
                        float* d_scales3, float* d_quats4, float* d_view16, float* partials, cudaStream_t s,
                        bool accumulate, int gstride, const float* rgbo_in, float* rgbo_out,
                        unsigned int* done_counter, unsigned long long* clean_word, unsigned long long clean_sig,
-                       bool clear_accum) {
+                       bool clear_accum, bool add_view, bool vis_from_grads) {
     int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
     const int resident = sort_sm_count() * PBWD_MINB;
     if (blocks > resident) blocks = resident;
@@ -550,13 +557,14 @@ int launch_project_bwd(const float* means3, const float* scales3, const float* q
         launch_k(project_bwd_kernel, dim3(blocks), dim3(PBWD_THREADS), 0, s, means3, scales3, (const float4*)quats4,
                  (int)n, k, tiles, (float4*)d_geo4, const_cast<float*>(d_c11), d_means3, d_scales3,
                  (float4*)d_quats4, partials, accumulate, gstride, (float4*)rgbo_in, (float4*)rgbo_out,
-                 PBWD_LASTBLOCK ? done_counter : nullptr, d_view16, clean_word, clean_sig, clear_accum);
+                 PBWD_LASTBLOCK ? done_counter : nullptr, d_view16, clean_word, clean_sig, clear_accum,
+                 vis_from_grads);
         done_counter = PBWD_LASTBLOCK ? done_counter : nullptr;
         if (check_launch("project_bwd_kernel")) return -1;
         if (done_counter) return 0;  // the last block wrote d_view
     }
     launch_k(view_reduce_kernel, dim3(1), dim3(384), 0, s, (const float*)partials, blocks, d_view16, clean_word,
-             clear_accum ? clean_sig : 0ull);
+             clear_accum ? clean_sig : 0ull, add_view);
     return check_launch("view_reduce_kernel");
 }
 
@@ -598,10 +606,10 @@ int gs_project_bwd(const float* means3, const float* scales3, const float* quats
         project_bwd_kernel<<<blocks, PBWD_THREADS, 0, (cudaStream_t)stream>>>(
             means3, scales3, (const float4*)quats4, (int)n, k, tiles, (float4*)d_geo4, const_cast<float*>(d_c11),
             d_means3, d_scales3, (float4*)d_quats4, (float*)ws, false, 1, nullptr, nullptr, nullptr, d_view16,
-            nullptr, 0ull, false);
+            nullptr, 0ull, false, false);
         if (check_launch("project_bwd_kernel")) return -1;
     }
-    view_reduce_kernel<<<1, 384, 0, (cudaStream_t)stream>>>((const float*)ws, blocks, d_view16, nullptr, 0ull);
+    view_reduce_kernel<<<1, 384, 0, (cudaStream_t)stream>>>((const float*)ws, blocks, d_view16, nullptr, 0ull, false);
     return check_launch("view_reduce_kernel");
 }
 

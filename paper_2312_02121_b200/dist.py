@@ -104,3 +104,76 @@ def allreduce_grads(flat, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
     return flat
+
+
+# ------------------------------------------------------------------ device-side reductions
+#
+# View sharding (config 3): every rank accumulates its views' gradients into
+# one flat buffer; the sum over ranks is an all-reduce of the 14 fp32 per
+# Gaussian.  Only the LAST view's projection backward stands between the
+# local sum and that reduction, so it runs in Gaussian buckets and each
+# bucket's all-reduce starts as soon as the bucket is written (NCCL's stream
+# waits for the launching stream at call time), overlapping the following
+# buckets' projection backward.  Tile bands (config 4): the ranks hold
+# disjoint pixel bands of one frame, so the screen-space gradients (9 fp32
+# per Gaussian: d_color 3, d_opacity, d_mean2d 2, d_cov 3) are summed first
+# and every rank then runs the projection backward on the summed rows
+# (sg/proj_backward.py:206-222 is linear in them), ending with identical
+# gradients and d_view on every rank.
+
+def bucket_bounds(n: int, buckets: int, align: int = 256) -> list:
+    """[a, b) Gaussian ranges of about equal size (multiples of `align`)."""
+    buckets = max(1, int(buckets))
+    per = (n + buckets - 1) // buckets
+    step = max(align, (per + align - 1) // align * align)
+    out, a = [], 0
+    while a < n:
+        b = min(n, a + step)
+        out.append((a, b))
+        a = b
+    return out or [(0, 0)]
+
+
+class GradReducer:
+    """Sum the flat gradient buffer (engine.unpack layout) over ranks,
+    overlapped with the last view's projection backward (`buckets` ranges)."""
+
+    def __init__(self, n: int, buckets: int = 4, group=None):
+        self.n = int(n)
+        self.bounds = bucket_bounds(self.n, buckets)
+        self.group = group
+
+    def last_view(self, fr, params, out: dict, d_view, accumulate: bool) -> list:
+        """Projection backward of the last view (after
+        ops.frame_backward(project=False)) bucket by bucket, each bucket's
+        4 gradient slices all-reduced asynchronously.  Returns the works."""
+        import torch.distributed as dist
+        from . import ops
+        m, s, q = params[0], params[1], params[2]
+        works = []
+        for a, b in self.bounds:
+            ops.frame_project_backward(fr, m, s, q, out, d_view, a, b, accumulate=accumulate, add_view=a > 0)
+            for key in ("d_mean", "d_scale", "d_quat", "d_rgbo"):
+                works.append(dist.all_reduce(out[key][a:b], op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+        return works
+
+    @staticmethod
+    def wait(works) -> None:
+        for w in works:
+            w.wait()
+
+
+def band_backward(fr, params, d_image, out: dict, d_view, group=None) -> None:
+    """Tile-band backward of one frame split over ranks: raster backward of
+    this rank's band, sum of the 9 screen-space fp32 per Gaussian over
+    ranks, then the projection backward of the summed rows (identical
+    gradients and d_view on every rank)."""
+    import torch.distributed as dist
+    from . import ops
+    m, s, q, _, c = params
+    ops.frame_backward(fr, m, s, q, c, d_image, project=False)
+    rows, c11 = ops.frame_screen_grads(fr)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(rows, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(c11, op=dist.ReduceOp.SUM, group=group)
+    ops.frame_project_backward(fr, m, s, q, out, d_view, vis_from_grads=True)

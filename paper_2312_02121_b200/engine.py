@@ -96,8 +96,12 @@ def unpack(flat: torch.Tensor, n: int) -> dict:
 
 class RenderStep:
     def __init__(self, n: int, cams, background=(0.0, 0.0, 0.0), early_termination=True, device=None,
-                 headroom: float = 1.05, buffers: int = 2, view_streams: int = 3):
+                 headroom: float = 1.05, buffers: int = 2, view_streams: int = 3, reducer=None):
+        """reducer: a dist.GradReducer -- the step's gradients are summed over
+        the ranks of its process group, the all-reduce overlapped with the
+        last view's projection backward (view-sharded data parallelism)."""
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.reducer = reducer
         self.n = int(n)
         self.cams = [c if isinstance(c, ops.CameraParams) else ops.CameraParams.of(c) for c in cams]
         self.bg = tuple(float(b) for b in background)
@@ -112,6 +116,8 @@ class RenderStep:
                 d_images=[z(c.height, c.width, 3) for c in self.cams],
                 grads=z(14 * n),
                 meta=torch.zeros((len(self.cams), 4), device=self.dev, dtype=torch.int64),
+                d_view=z(len(self.cams), 4, 4),
+                frames=[None] * len(self.cams),
                 graph=None))
         self.caps = None
         self.wss = None
@@ -153,8 +159,15 @@ class RenderStep:
             with torch.cuda.stream(st):
                 fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et, capacity=self.caps[vi],
                                        check_meta=False, ws=self.wss[vi])
-                ops.frame_backward(fr, m, sc, q, c, d, out=out, accumulate=vi > 0, wait_before_accumulate=bwd_done)
+                last = vi == len(self.cams) - 1
+                if last and self.reducer is not None:  # its projection backward runs bucketed in replay()
+                    ops.frame_backward(fr, m, sc, q, c, d, project=False)
+                else:
+                    g = ops.frame_backward(fr, m, sc, q, c, d, out=out, accumulate=vi > 0,
+                                           wait_before_accumulate=bwd_done)
+                    s["d_view"][vi].copy_(g["d_view"])
                 s["meta"][vi].copy_(fr.meta()[:4])
+                s["frames"][vi] = fr
                 if len(sts) > 1:
                     bwd_done = torch.cuda.Event()
                     bwd_done.record(st)
@@ -201,6 +214,19 @@ class RenderStep:
 
     def replay(self, k: int):
         self.sets[k]["graph"].replay()
+        if self.reducer is not None:
+            # the last view's projection backward in Gaussian buckets, each
+            # bucket's all-reduce overlapping the next buckets (dist.py)
+            s = self.sets[k]
+            nv = len(self.cams)
+            works = self.reducer.last_view(s["frames"][nv - 1], s["params"], unpack(s["grads"], self.n),
+                                           s["d_view"][nv - 1], accumulate=nv > 1)
+            self.reducer.wait(works)
+
+    def d_view(self, k: int) -> torch.Tensor:
+        """Per-view d_view (views, 4, 4) of buffer set k's last replay (per
+        camera: not reduced over ranks)."""
+        return self.sets[k]["d_view"]
 
     def grads(self, k: int) -> torch.Tensor:
         return self.sets[k]["grads"]

@@ -517,7 +517,7 @@ def _event_array(events):
 
 
 def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=False, events=None, out=None,
-                   accumulate=False, keep_screen=False, wait_before_accumulate=None):
+                   accumulate=False, keep_screen=False, wait_before_accumulate=None, project=True):
     """gs_frame_backward: the SceneGradients fields (sg/proj_backward.py:25-50).
     out: optional dict of contiguous output tensors d_mean (n,3), d_scale
     (n,3), d_quat (n,4), d_rgbo (n,4) to write (accumulate=False) or add
@@ -528,7 +528,10 @@ def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=F
     wait_before_accumulate: a torch.cuda.Event the stream waits on between
     the raster backward and the projection backward (which adds into `out`):
     views of one step on several streams then overlap their raster backwards
-    and serialise only the accumulation."""
+    and serialise only the accumulation.  project=False: raster backward
+    only -- the screen-space gradients stay in the workspace
+    (frame_screen_grads) for frame_project_backward, e.g. after a reduction
+    across ranks."""
     L = _lib.load()
     H, W = fr.cam.height, fr.cam.width
     if tuple(d_image.shape) != (H, W, 3):
@@ -552,7 +555,7 @@ def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=F
     cnt = torch.zeros((3,), device=dev, dtype=torch.int64) if counts else None
     camc = fr.cam.c()
     bg = (C.c_float * 3)(*fr.background)
-    flags = (1 if accumulate else 0) | (2 if keep_screen else 0)
+    flags = (1 if accumulate else 0) | (2 if keep_screen else 0) | (0 if project else 8)
     if wait_before_accumulate is not None:
         flags |= 4
         events = (list(events) + [None] * 3)[:3] if events else [None, None, None]
@@ -564,6 +567,40 @@ def frame_backward(fr: Frame, means, scales, quats, colors, d_image, *, counts=F
           "gs_frame_backward")
     return dict(d_mean=d_means, d_scale=d_scales, d_quat=d_quats, d_opacity=d_rgbo[:, 3], d_color=d_rgbo[:, :3],
                 d_view=d_view, d_rgbo=d_rgbo, counts=cnt)
+
+
+def frame_screen_grads(fr: Frame):
+    """The screen-space gradient accumulators of a frame (after
+    frame_backward(project=False)): rows (n, 8) = [d_color 3, d_opacity,
+    d_mean2d 2, d_cov00, d_cov01] and d_c11 (n,) -- device views into the
+    workspace, reducible in place across ranks."""
+    v = fr.view()
+    base = fr.ws.data_ptr()
+    off = v.bwd_accum - base
+    rows = fr.ws[off:off + 32 * fr.n].view(torch.float32).view(fr.n, 8)
+    off = v.d_c11 - base
+    return rows, fr.ws[off:off + 4 * fr.n].view(torch.float32)
+
+
+def frame_project_backward(fr: Frame, means, scales, quats, out: dict, d_view: torch.Tensor, begin=0, end=None, *,
+                           accumulate=False, add_view=False, keep_screen=False, vis_from_grads=False):
+    """gs_frame_project_backward: the projection backward of frame `fr`
+    (sg/proj_backward.py:178-223) over Gaussians [begin, end) from the
+    screen-space gradients in its workspace, into `out` (d_mean, d_scale,
+    d_quat, d_rgbo full (n, .) tensors; rows begin..end-1 written or, with
+    accumulate, added to) and d_view (4x4; overwritten or, with add_view,
+    added to).  vis_from_grads: a Gaussian this frame culled but whose rows
+    are non-zero (summed over tile bands) is treated as visible."""
+    L = _lib.load()
+    n = fr.n
+    end = n if end is None else int(end)
+    camc = fr.cam.c()
+    flags = (1 if accumulate else 0) | (2 if keep_screen else 0) | (16 if add_view else 0) | \
+        (32 if vis_from_grads else 0)
+    check(L.gs_frame_project_backward(_ptr(means), _ptr(scales), _ptr(quats), n, C.byref(camc), fr.capacity,
+                                      _ptr(fr.ws), fr.ws.numel(), int(begin), end, _ptr(out["d_mean"]),
+                                      _ptr(out["d_scale"]), _ptr(out["d_quat"]), _ptr(out["d_rgbo"]), _ptr(d_view),
+                                      flags, _stream()), "gs_frame_project_backward")
 
 
 # ------------------------------------------------------ staged (per-stage) path
