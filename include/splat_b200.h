@@ -44,6 +44,7 @@ enum gs_error_code {
     GS_ERR_QUAT = 2,    /* sg/core.py:160-163 "quaternion norm is too small ..." */
     GS_ERR_HOMOG = 3,   /* sg/projection.py:54-55 "degenerate projection ..." */
     GS_ERR_COV2D = 4,   /* sg/projection.py:108-109 "2d covariance must be positive definite" */
+    GS_ERR_BEHIND = 5,  /* sg/projection.py:75-76 "point is behind the camera" */
 };
 
 /* Pinhole camera, the fields of sg/core.py:59-129 Camera (view row-major,
@@ -374,6 +375,27 @@ int gs_project64_bwd(const double* means3, const double* scales3, const double* 
                      const gs_camera64* cam /*[host]*/, const uint32_t* tiles, const double* d9, double* d_means3,
                      double* d_scales3, double* d_quats4, double* d_view16, void* ws, size_t ws_bytes,
                      gs_stream_t stream);
+
+/* ---- Per-splat helpers in float64 (the rest of sg/__init__.py:64-119) ---
+ * gs_op64 runs one helper over n items (one thread each); `in` / `out` are
+ * HOST arrays of device pointers, row-major matrices, items contiguous.
+ * Errors (degenerate inputs) go to *status as index << 8 | gs_error_code.   */
+enum gs_op64_code {
+    GS_OP_QUAT_TO_ROTMAT = 1,      /* sg/core.py:146-171        q4 -> R9 */
+    GS_OP_COMPOSE_COV3D = 2,       /* sg/core.py:174-195        q4, s3 -> R9, S9, M9, sigma9 */
+    GS_OP_FROBENIUS = 3,           /* sg/core.py:198-204        x[cols], y[cols] -> sum x*y */
+    GS_OP_WORLD_TO_CAMERA = 4,     /* sg/projection.py:36-42    mean3 -> t4 (camera) */
+    GS_OP_CAMERA_TO_PIXEL = 5,     /* sg/projection.py:45-61    t4 -> mean2d2 (camera) */
+    GS_OP_PROJECTION_JACOBIAN = 6, /* sg/projection.py:64-82    t4 -> J6 (camera) */
+    GS_OP_PROJECT_COVARIANCE = 7,  /* sg/projection.py:85-96    J6, Rcw9, sigma9 -> cov2d4 */
+    GS_OP_BOUNDING_RADIUS = 8,     /* sg/projection.py:99-112   cov2d4 -> r (integral double) */
+    GS_OP_MEAN2D_BACKWARD = 9,     /* sg/proj_backward.py:53-77  dmean2d2, t4 -> dt4 (camera) */
+    GS_OP_COV2D_BACKWARD = 10,     /* sg/proj_backward.py:88-121 G4, T6, sigma9, J6, Rcw9, t4 -> dsigma9, dt4 */
+    GS_OP_WORLD_BACKWARD = 11,     /* sg/proj_backward.py:124-136 dt4, mean3 -> dmean3, dview16 (camera) */
+    GS_OP_COV3D_BACKWARD = 12,     /* sg/proj_backward.py:151-175 dsigma9, R9, S9, M9, q4 -> dq4, ds3 */
+};
+int gs_op64(int op, int64_t n, const double* const* in /*[host]*/, double* const* out /*[host]*/, int32_t cols,
+            const gs_camera64* cam /*[host], nullable*/, unsigned long long* status, gs_stream_t stream);
 
 #ifdef __cplusplus
 }

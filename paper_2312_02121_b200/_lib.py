@@ -26,7 +26,7 @@ EXPORTS = (
     "gs_activate", "gs_loss_l2", "gs_adam_step",
     "gs_conic_from_cov", "gs_eval_alpha", "gs_composite_pixels", "gs_composite_pixels_bwd",
     "gs_project64", "gs_bin64_workspace_bytes", "gs_bin64_count", "gs_bin64_sort", "gs_raster64_fwd",
-    "gs_raster64_bwd", "gs_project64_bwd_workspace_bytes", "gs_project64_bwd",
+    "gs_raster64_bwd", "gs_project64_bwd_workspace_bytes", "gs_project64_bwd", "gs_op64",
 )
 
 ERR_MESSAGES = {  # include/splat_b200.h gs_error_code -> the reference's ValueError text
@@ -34,6 +34,7 @@ ERR_MESSAGES = {  # include/splat_b200.h gs_error_code -> the reference's ValueE
     2: "quaternion norm is too small to define an orientation",  # sg/core.py:160-163
     3: "degenerate projection: homogeneous component is ~0",     # sg/projection.py:54-55
     4: "2d covariance must be positive definite",                # sg/projection.py:108-109
+    5: "point is behind the camera",                             # sg/projection.py:75-76
 }
 
 
@@ -126,6 +127,7 @@ def load():
         "gs_raster64_bwd": ([P, P, P, P, P, P, f64p, C.c_int32, C.c_int32, P, P, P, P, P], C.c_int),
         "gs_project64_bwd_workspace_bytes": ([i64], C.c_size_t),
         "gs_project64_bwd": ([P, P, P, i64, cam64, P, P, P, P, P, P, P, C.c_size_t, P], C.c_int),
+        "gs_op64": ([C.c_int, i64, P, P, C.c_int32, cam64, P, P], C.c_int),
     })
     for name, (args, res) in sig.items():
         f = getattr(L, name)

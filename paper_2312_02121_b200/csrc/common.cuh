@@ -23,6 +23,8 @@ constexpr float ALPHA_MAX = 0.999f;            // sg/raster_forward.py:22
 constexpr float T_MIN = 1e-4f;                 // sg/raster_forward.py:25
 constexpr float SIGMA_CUT = 4.5f;              // sg/raster_forward.py:30
 constexpr float QUAT_EPS = 1e-12f;             // sg/core.py:13
+constexpr double QUAT_EPS_D = 1e-12;           // (float64 helpers, ops64.cu)
+constexpr double DILATION_D = 0.3;
 constexpr float NEG_LOG2E = -1.4426950408889634f;
 constexpr int MAX_RADIUS = 1 << 24;            // clamp so int math cannot overflow
 

@@ -30,7 +30,7 @@ GRAD_CLASSES = ("d_mean", "d_scale", "d_quat", "d_opacity", "d_color", "d_view")
 def golden_names():
     # frame fixtures (make_golden.py); pixel.npz is the per-pixel API's own
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if os.path.basename(p) not in ("pixel.npz", "audit_scenes.npz"))
+                  if os.path.basename(p) not in ("pixel.npz", "audit_scenes.npz", "helpers.npz"))
 
 
 def load_pixel_golden():

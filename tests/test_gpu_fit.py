@@ -68,7 +68,7 @@ def _oracle_fit(target, camera, config, init, iterations):
 
 
 def test_fit_loss_history_matches_oracle(cuda):
-    from paper_2312_02121_b200 import api, fit as F
+    from paper_2312_02121_b200 import api, fitting as F
     truth, camera = _hidden_scene(api)
     bg = (0.1, 0.1, 0.1)
     target = api.render(truth, camera, np.asarray(bg)).image.channels
@@ -83,7 +83,7 @@ def test_fit_loss_history_matches_oracle(cuda):
 
 
 def test_fit_criterion5_loss_cut(cuda):
-    from paper_2312_02121_b200 import api, fit as F
+    from paper_2312_02121_b200 import api, fitting as F
     truth, camera = _hidden_scene(api)
     bg = (0.1, 0.1, 0.1)
     target = api.render(truth, camera, np.asarray(bg)).image.channels
@@ -104,7 +104,7 @@ def test_fit_criterion5_loss_cut(cuda):
 
 
 def test_fit_rejects_bad_target(cuda):
-    from paper_2312_02121_b200 import api, fit as F
+    from paper_2312_02121_b200 import api, fitting as F
     _, camera = _hidden_scene(api)
     with pytest.raises(ValueError, match="target shape"):
         F.fit(np.zeros((10, 10, 3)), camera, F.FitConfig(iterations=1))

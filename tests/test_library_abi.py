@@ -79,3 +79,23 @@ def test_product_path_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
                 assert "splat_oracle" not in txt, f
+
+
+def test_package_exports_the_reference_api():
+    """Every name of the reference's sg/__init__.py:64-119 __all__ resolves
+    on the package (lazily; device calls need a GPU, resolution does not)."""
+    import paper_2312_02121_b200 as sg
+    ref = ["ALPHA_MAX", "ALPHA_MIN", "AUDIT_CLASSES", "Camera", "ClassCheck", "Cov3DBundle", "DILATION", "FitConfig",
+           "Gaussian3D", "GradReport", "ImageBuffer", "ProjectedGaussian", "RenderAux", "RenderResult", "SIGMA_CUT",
+           "SceneGradients", "Splat2DGrads", "TILE_SIZE", "T_MIN", "TileGrid", "accumulate_image_backward",
+           "assign_tiles", "audit_scene", "bounding_radius", "camera_to_pixel", "compose_covariance_3d",
+           "composite_pixel", "composite_pixel_backward", "cov2d_backward", "covariance3d_backward", "eval_alpha",
+           "finite_difference", "fit", "frobenius_inner", "init_random", "main", "make_audit_scene",
+           "mean2d_backward", "parse_scene", "project_covariance", "project_gaussian", "projection_jacobian",
+           "quat_to_rotmat", "read_image", "render", "render_brute_force", "run_audit", "scene_backward",
+           "serialize_scene", "sort_bins", "transmittance_replay", "world_backward", "world_to_camera",
+           "write_image"]
+    assert sorted(sg.__all__) == sorted(ref)
+    for name in ref:
+        assert getattr(sg, name) is not None, name
+    assert callable(sg.fit) and callable(sg.main) and sg.TILE_SIZE == 16 and sg.SIGMA_CUT == 4.5
