@@ -230,7 +230,7 @@ def run_ours(args):
     # roofline numerators: evaluation-class counts of a counted pass (untimed)
     counts_f = np.zeros(4, np.int64)
     counts_b = np.zeros(3, np.int64)
-    caps, wss, isect = [], [], []
+    caps, wss, isect, binnings = [], [], [], []
     for cam, d_img in zip(cams, d_imgs):
         fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, counts=True)
         g = ops.frame_backward(fr, m, s, q, c, d_img, counts=True)
@@ -242,6 +242,7 @@ def run_ours(args):
         fr = ops.frame_forward(m, s, q, o, c, cam, bg, True)
         cap = int(fr.needed_capacity * 1.05) + 4096
         caps.append(cap)
+        binnings.append(fr.binning)
         wss.append(ops.frame_workspace(n, cap, cam.width, cam.height, dev))
         del fr
 
@@ -281,7 +282,7 @@ def run_ours(args):
             st = sts[vi % ns]
             with torch.cuda.stream(st):
                 fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, capacity=caps[vi], check_meta=False,
-                                       ws=wss[vi], events=ev_f[vi] if staged else None)
+                                       ws=wss[vi], events=ev_f[vi] if staged else None, binning=binnings[vi])
                 # only the views' accumulation into grad_out is ordered: this view's raster
                 # backward overlaps the previous view's projection backward.  N > 1: the
                 # last view's projection backward runs after the graph, bucketed under the

@@ -131,9 +131,10 @@ class RenderStep:
         s = self.sets[k]
         m, sc, q, o, c = s["params"]
         L = _lib.load()
-        self.caps, self.wss = [], []
+        self.caps, self.wss, self.binnings = [], [], []
         for cam, d in zip(self.cams, s["d_images"]):
             fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et)
+            self.binnings.append(fr.binning)
             cap = int(fr.needed_capacity * self.headroom) + 4096
             self.caps.append(cap)
             self.wss.append(ops.frame_workspace(self.n, cap, cam.width, cam.height, self.dev))
@@ -158,7 +159,7 @@ class RenderStep:
             st = sts[vi % len(sts)]
             with torch.cuda.stream(st):
                 fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et, capacity=self.caps[vi],
-                                       check_meta=False, ws=self.wss[vi])
+                                       check_meta=False, ws=self.wss[vi], binning=self.binnings[vi])
                 last = vi == len(self.cams) - 1
                 if last and self.reducer is not None:  # its projection backward runs bucketed in replay()
                     ops.frame_backward(fr, m, sc, q, c, d, project=False)

@@ -356,6 +356,32 @@ def project_bwd(means, scales, quats, cam: CameraParams, tiles, d_geo, d_c11):
 # ValueError on bad input and to re-run when the capacity was too small.
 
 _capacity_hint: dict = {}
+_binning_hint: dict = {}  # (n, W, H) -> the binning a skewed view fell back to
+_BINNING_CODE = {"auto": 0, "depth_first": 1, "scatter": 2, "direct": 3}
+# Direct binning sizes every tile's bin by the longest per-replica segment of
+# any tile (csrc/raster.cu), so a view whose pairs crowd into a few tiles
+# would need tiles x 8 x that many slots (e.g. 80k Gaussians on 4 of 4096
+# tiles: ~82 M slots, ~4 GB); when it needs more than DIRECT_SKEW x the pair
+# count (and over DIRECT_FLOOR slots) the frame re-runs with scatter binning,
+# whose room is the pair count itself.
+DIRECT_SKEW = 4
+DIRECT_FLOOR = 1 << 20
+
+
+class _binning_option:
+    """Select the frame binning for one call (gs_set_option is process-wide)."""
+
+    def __init__(self, binning):
+        self.code = None if binning in (None, "auto") else _BINNING_CODE[binning]
+
+    def __enter__(self):
+        if self.code is not None:
+            self.prev = get_option("binning")
+            set_option("binning", self.code)
+
+    def __exit__(self, *exc):
+        if self.code is not None:
+            set_option("binning", self.prev)
 
 
 def _default_capacity(n: int, key) -> int:
@@ -388,6 +414,7 @@ class Frame:
     counts_fwd: torch.Tensor | None = None
     meta_host: tuple | None = None
     extra: dict = field(default_factory=dict)  # adapters' payload (api.render)
+    binning: str | None = None  # the binning this frame was forced to (None: the library's choice)
 
     def view(self) -> _lib.GsFrameView:
         v = _lib.GsFrameView()
@@ -469,8 +496,11 @@ def frame_workspace(n: int, capacity: int, width: int, height: int, device) -> t
 
 def frame_forward(means, scales, quats, opacities, colors, cam: CameraParams, background=(0.0, 0.0, 0.0),
                   early_termination=True, *, capacity: int | None = None, counts=False, check_meta=True,
-                  ws: torch.Tensor | None = None, events=None) -> Frame:
-    """gs_frame_forward: image, final_T, n_contrib of one view."""
+                  ws: torch.Tensor | None = None, events=None, binning: str | None = None) -> Frame:
+    """gs_frame_forward: image, final_T, n_contrib of one view.  binning:
+    force "depth_first" / "scatter" / "direct" for this call (default: the
+    library's choice, or the scatter fallback a skewed view of this size
+    needed before -- see DIRECT_SKEW)."""
     L = _lib.load()
     means, scales, quats, opacities, colors = check_params(means, scales, quats, opacities, colors)
     n = means.shape[0]
@@ -480,6 +510,7 @@ def frame_forward(means, scales, quats, opacities, colors, cam: CameraParams, ba
     H, W = cam.height, cam.width
     camc = cam.c()
     bg = (C.c_float * 3)(*[float(b) for b in background])
+    bsel = binning or _binning_hint.get(key)
     while True:
         wsb = L.gs_frame_workspace_bytes(n, cap, W, H)
         if ws is None or ws.numel() < wsb:
@@ -488,16 +519,22 @@ def frame_forward(means, scales, quats, opacities, colors, cam: CameraParams, ba
         final_T = torch.empty((H, W), device=dev, dtype=torch.float32)
         n_contrib = torch.empty((H, W), device=dev, dtype=torch.int32)
         cnt = torch.zeros((4,), device=dev, dtype=torch.int64) if counts else None
-        check(L.gs_frame_forward(_ptr(means), _ptr(scales), _ptr(quats), _ptr(opacities), _ptr(colors), n,
-                                 C.byref(camc), bg, 1 if early_termination else 0, cap, _ptr(ws), ws.numel(),
-                                 _ptr(image), _ptr(final_T), _ptr(n_contrib), _ptr(cnt), _event_array(events),
-                                 _stream()), "gs_frame_forward")
+        with _binning_option(bsel):
+            check(L.gs_frame_forward(_ptr(means), _ptr(scales), _ptr(quats), _ptr(opacities), _ptr(colors), n,
+                                     C.byref(camc), bg, 1 if early_termination else 0, cap, _ptr(ws), ws.numel(),
+                                     _ptr(image), _ptr(final_T), _ptr(n_contrib), _ptr(cnt), _event_array(events),
+                                     _stream()), "gs_frame_forward")
         fr = Frame(cam, tuple(float(b) for b in background), bool(early_termination), n, cap, ws, image, final_T,
-                   n_contrib, cnt)
+                   n_contrib, cnt, binning=bsel)
         if not check_meta:
             return fr
         m = fr._meta_host()
         raise_status(m[0])
+        if m[3] > 0 and binning is None and m[2] > max(DIRECT_SKEW * m[1], DIRECT_FLOOR):
+            bsel = _binning_hint[key] = "scatter"  # skewed view: direct binning's room would explode
+            cap = _capacity_hint[key] = max(1 << 16, int(m[1] * 1.25) + 1024)
+            ws = None
+            continue
         need = needed_capacity(m)
         _capacity_hint[key] = max(1 << 16, int(need * 1.25) + 1024)
         if need <= cap:
