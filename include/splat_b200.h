@@ -69,7 +69,12 @@ int gs_version(void);
  * forward sorts each bin).  Both give sg/binning.py:50-65's (depth,
  * source_index) lists bit for bit.  "fuse_sort" (scatter binning): 1
  * (default) sorts each tile's range at the top of the raster forward CTA
- * that composites it, 0 in a separate per-tile sort kernel; same lists. */
+ * that composites it, 0 in a separate per-tile sort kernel; same lists.
+ * "tile_emit" (depth-first binning): 1 (default) writes every pair straight
+ * to its slot in its tile's list (per-tile counts from the projection, one
+ * stable counting pass over the depth-ordered Gaussians) when the tile count
+ * fits its shared-memory tables (<= 10240 tiles), 0 emits the pairs and sorts
+ * them by tile with onesweep passes; same lists. */
 int gs_set_option(const char* name, int value);
 /* Current value of an option of gs_set_option (-1 and gs_last_error for an
  * unknown name). */
@@ -190,7 +195,9 @@ typedef struct gs_frame_view {
     float* conic4;              /* (n,4) as gs_project_fwd out_conic4 */
     uint32_t* tiles;            /* (n)   tiles touched, 0 = culled */
     uint32_t* depth_order;      /* (n)   Gaussian ids by (depth, index) (see depth_order_alt) */
-    uint32_t* sorted_tile_keys; /* (capacity) tile id of each sorted pair */
+    uint32_t* sorted_tile_keys; /* (capacity) tile id of each sorted pair -- written by scatter
+                                   binning and by the depth-first binning with tile_emit 0 only;
+                                   otherwise implied by ranges2 */
     uint32_t* sorted_vals;      /* (capacity) Gaussian id of each sorted pair */
     uint32_t* ranges2;          /* (tiles,2) [start, end) */
     unsigned long long* meta;   /* [0] status word, [1] total intersections, [2] capacity needed,

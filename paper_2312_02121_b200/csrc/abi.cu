@@ -47,6 +47,16 @@ bool fuse_sort() {
     return g_fuse_sort == 1;
 }
 
+static int g_tile_emit = -1;  // -1: not set (env GS_TILE_EMIT, else on)
+
+bool tile_emit() {
+    if (g_tile_emit < 0) {
+        const char* e = getenv("GS_TILE_EMIT");
+        g_tile_emit = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_tile_emit == 1;
+}
+
 int check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error("%s: %s", what, cudaGetErrorString(e));
@@ -73,6 +83,11 @@ int gs_set_option(const char* name, int value) {
         gs::g_fuse_sort = value;
         return 0;
     }
+    if (strcmp(name, "tile_emit") == 0) {
+        if (value < 0 || value > 1) return gs::set_error("gs_set_option: tile_emit must be 0 or 1");
+        gs::g_tile_emit = value;
+        return 0;
+    }
     return gs::set_error("gs_set_option: unknown option %s", name);
 }
 
@@ -80,6 +95,7 @@ int gs_get_option(const char* name) {
     if (!name) return gs::set_error("gs_get_option: null name");
     if (strcmp(name, "binning") == 0) return gs::binning_mode();
     if (strcmp(name, "fuse_sort") == 0) return gs::fuse_sort() ? 1 : 0;
+    if (strcmp(name, "tile_emit") == 0) return gs::tile_emit() ? 1 : 0;
     return gs::set_error("gs_get_option: unknown option %s", name);
 }
 

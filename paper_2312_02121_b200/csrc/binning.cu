@@ -455,6 +455,324 @@ int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* 
     return check_launch("emit_scan_kernel");
 }
 
+// ---------------------------------------------------------------- tile-sorted emission
+// Depth-first binning without a global sort by tile (frame.cu, <= 10240
+// tiles): every (tile, gaussian) pair is written straight to its final slot
+//     start(tile) + #{pairs of the same tile emitted earlier}
+// where "earlier" is the emission order of sg/binning.py:35-46 over the
+// Gaussians in (depth, index) order -- exactly the stable order of
+// sg/binning.py:50-65.  A stable counting sort whose digit is the whole tile
+// id and whose keys are generated from the Gaussians' rects, never stored:
+//   et_count_kernel  chunk c = ET_CHUNK consecutive Gaussians of the depth
+//                    order: its per-tile pair counts -> row c of a (chunks x
+//                    tiles) u16 matrix (shared-memory histogram, coalesced row)
+//   et_scan_kernel   per tile, the exclusive scan of that column over the
+//                    chunks (u32 in place of the counts' matrix) and the tile's
+//                    total -> tcount (the tile scan makes the ranges of them)
+//   et_emit_kernel   chunk c again: per-(warp, tile) counts in shared memory,
+//                    turned into per-warp offsets on top of the tile's start
+//                    and the column prefix; a second walk over the pairs, in
+//                    order, ranks each step's 32 pairs with match_any and
+//                    writes the Gaussian id.
+// Replaces emission (8 B / pair written) + 2 onesweep passes over the pairs
+// (2 x 16 B / pair) + range detection (4 B / pair) by 4 B / pair written and
+// 12 B / (chunk, tile) of prefix tables; no look-back chain (a decoupled
+// look-back over 4346 digits per chunk measured 320 us per config-3 view: the
+// first wave's chunks all look back to chunk 0 at once).  The sorted tile keys
+// are not written (the ranges imply them).
+constexpr int ET_WARPS = 8;
+constexpr int ET_ROUNDS = 8;  // 32-Gaussian rounds per warp (<= 256 Gaussians per warp: u16 counts)
+constexpr int ET_THREADS = ET_WARPS * 32;
+constexpr int ET_CHUNK = ET_THREADS * ET_ROUNDS;  // Gaussians per chunk (2048: u16 chunk counts)
+
+__host__ __device__ inline int et_stride(int n_tiles) { return (n_tiles + 1) & ~1; }  // u16 row stride, even
+size_t emit_tiles_smem(int n_tiles) {
+    return (size_t)ET_WARPS * et_stride(n_tiles) * 2 + (size_t)n_tiles * 4;
+}
+bool emit_tiles_fits(int n_tiles) { return n_tiles >= 1 && emit_tiles_smem(n_tiles) <= 200 * 1024; }  // <= 10240 tiles
+// tables: u32 column prefixes [chunk][tile], then the u16 counts [chunk][tile]
+static size_t et_prefix_bytes(int64_t n, int n_tiles) {
+    const int64_t chunks = (n + ET_CHUNK - 1) / ET_CHUNK;
+    return (size_t)(chunks > 0 ? chunks : 1) * (size_t)et_stride(n_tiles) * 4;
+}
+size_t emit_tiles_table_bytes(int64_t n, int n_tiles) { return et_prefix_bytes(n, n_tiles) * 3 / 2; }
+
+// The chunk's Gaussians (depth-order positions p0 + 32 r, one per lane and
+// round) and their tile rects; rounds past the visible count are empty.
+struct EtRound {
+    uint32_t g;
+    int tx0, ty0, w, h;
+};
+__device__ __forceinline__ void et_load(const uint32_t* __restrict__ order, const float4* __restrict__ xydr, int p0,
+                                        int V, int tiles_x, int tiles_y, EtRound (&rd)[ET_ROUNDS]) {
+#pragma unroll
+    for (int r = 0; r < ET_ROUNDS; ++r) rd[r].g = p0 + 32 * r < V ? order[p0 + 32 * r] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int r = 0; r < ET_ROUNDS; ++r) {
+        int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
+        if (rd[r].g != 0xFFFFFFFFu) {
+            const float4 q = xydr[rd[r].g];
+            tile_rect(q.x, q.y, __float_as_int(q.w), tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+        }
+        rd[r].tx0 = tx0, rd[r].ty0 = ty0, rd[r].w = tx1 - tx0 + 1, rd[r].h = ty1 - ty0 + 1;
+    }
+}
+
+// Walk the pairs of one round's 32 Gaussians in emission order, 32 per step:
+// f(tile or 0xFFFFFFFF, gaussian).  Empty rects may only trail the non-empty
+// ones (the depth order holds visible Gaussians only; rounds past the visible
+// count are empty).  The owner of step lane j is the owner of the step's
+// first pair (the last lane whose segment starts at or before it: one
+// ballot) plus the segments starting inside the step up to j (a bit mask of
+// the in-step start positions, one warp OR-reduction): ~35 instructions per
+// step instead of a 5-level binary search over the lanes' offsets (80).
+template <typename F>
+__device__ __forceinline__ void et_walk(int lane, const EtRound& rd, int tiles_x, F&& f) {
+    const uint32_t cnt = (uint32_t)(rd.w * rd.h);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - cnt, total = __shfl_sync(0xffffffffu, incl, 31);
+    const float rw = rd.w > 0 ? 1.f / (float)rd.w : 0.f;
+    const uint32_t le = lanemask_lt() | (1u << lane);
+    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+        const uint32_t first = __ballot_sync(0xffffffffu, cnt != 0u && excl <= t0);
+        const uint32_t sp = excl - t0;  // start position in the step (when inside)
+        const uint32_t starts = __reduce_or_sync(0xffffffffu, (cnt != 0u && excl > t0 && sp < 32u) ? 1u << sp : 0u);
+        const int L = (31 - __clz((int)first)) + __popc(starts & le);
+        const uint32_t t = t0 + lane;
+        const uint32_t j = t - __shfl_sync(0xffffffffu, excl, L);
+        const int ow = __shfl_sync(0xffffffffu, rd.w, L);
+        const float orw = __shfl_sync(0xffffffffu, rw, L);
+        const int otx0 = __shfl_sync(0xffffffffu, rd.tx0, L), oty0 = __shfl_sync(0xffffffffu, rd.ty0, L);
+        const uint32_t og = __shfl_sync(0xffffffffu, rd.g, L);
+        int row = (int)((float)j * orw);
+        if (row * ow > (int)j) --row;
+        if ((row + 1) * ow <= (int)j) ++row;
+        f(t < total ? (uint32_t)((oty0 + row) * tiles_x + otx0 + ((int)j - row * ow)) : 0xFFFFFFFFu, og);
+    }
+}
+
+// Every tile of the lane's own rect, row-major (order-free uses: counts).
+// Divergent, so a warp runs as long as its largest rect, but ~5 instructions
+// per tile against the walk's ~45 per step of 32.
+template <typename F>
+__device__ __forceinline__ void et_rect_each(const EtRound& rd, int tiles_x, F&& f) {
+    uint32_t t = (uint32_t)(rd.ty0 * tiles_x + rd.tx0);
+    for (int y = 0; y < rd.h; ++y, t += (uint32_t)tiles_x)
+        for (int x = 0; x < rd.w; ++x) f(t + (uint32_t)x);
+}
+
+// depth-first frame: meta[7] visible Gaussians sorted, in order_alt after an odd pass count (meta[8])
+__device__ __forceinline__ const uint32_t* et_order(const uint32_t* order, const uint32_t* order_alt,
+                                                    const unsigned long long* meta) {
+    return (meta[8] & 1ull) ? order_alt : order;
+}
+
+__global__ void __launch_bounds__(ET_THREADS) et_count_kernel(const uint32_t* __restrict__ order,
+                                                              const uint32_t* __restrict__ order_alt,
+                                                              const float4* __restrict__ xydr, int n, int tiles_x,
+                                                              int tiles_y, unsigned short* __restrict__ counts,
+                                                              const unsigned long long* __restrict__ meta) {
+    griddep_wait();
+    const int V = min(n, (int)meta[7]);
+    const int chunk = blockIdx.x;
+    if (chunk * ET_CHUNK >= V) return;
+    order = et_order(order, order_alt, meta);
+    const int n_tiles = tiles_x * tiles_y, hs = et_stride(n_tiles);
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem);  // [tile] (u32: shared atomics)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int t = tid; t < hs; t += ET_THREADS) s_cnt[t] = 0u;
+    EtRound rd[ET_ROUNDS];
+    et_load(order, xydr, chunk * ET_CHUNK + warp * (32 * ET_ROUNDS) + lane, V, tiles_x, tiles_y, rd);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < ET_ROUNDS; ++r) et_rect_each(rd[r], tiles_x, [&](uint32_t tile) { atomicAdd(&s_cnt[tile], 1u); });
+    __syncthreads();
+    uint32_t* row = reinterpret_cast<uint32_t*>(counts + (size_t)chunk * hs);  // two u16 per word
+    for (int k = tid; k < hs / 2; k += ET_THREADS) row[k] = s_cnt[2 * k] | (s_cnt[2 * k + 1] << 16);
+}
+
+// One CTA per 32 tiles (lane = tile), 32 warps over consecutive runs of
+// chunks: pass 1 sums each warp's rows, the warps' sums are scanned in shared
+// memory, pass 2 writes the running exclusive prefix (u32, row stride hs);
+// the last warp's inclusive sums are the tiles' totals.
+constexpr int ES_WARPS = 32;
+__global__ void __launch_bounds__(ES_WARPS * 32) et_scan_kernel(const unsigned short* __restrict__ counts,
+                                                                uint32_t* __restrict__ prefix, int n, int n_tiles,
+                                                                uint32_t* __restrict__ totals,
+                                                                const unsigned long long* __restrict__ meta) {
+    griddep_wait();
+    const int V = min(n, (int)meta[7]);
+    const int chunks = (V + ET_CHUNK - 1) / ET_CHUNK;
+    const int hs = et_stride(n_tiles);
+    __shared__ uint32_t s_sum[ES_WARPS][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
+    const bool in = t < n_tiles;
+    const int per = (chunks + ES_WARPS - 1) / ES_WARPS;
+    const int c0 = min(chunks, warp * per), c1 = min(chunks, c0 + per);
+    uint32_t sum = 0;
+    if (in) {
+        int c = c0;
+        for (; c + 8 <= c1; c += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = counts[(size_t)(c + u) * hs + t];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sum += v[u];
+        }
+        for (; c < c1; ++c) sum += counts[(size_t)c * hs + t];
+    }
+    s_sum[warp][lane] = sum;
+    __syncthreads();
+    uint32_t run = 0;
+    for (int w = 0; w < warp; ++w) run += s_sum[w][lane];
+    if (warp == ES_WARPS - 1 && in) totals[t] = run + sum;
+    if (!in) return;
+    int c = c0;
+    for (; c + 8 <= c1; c += 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = counts[(size_t)(c + u) * hs + t];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            prefix[(size_t)(c + u) * hs + t] = run;
+            run += v[u];
+        }
+    }
+    for (; c < c1; ++c) {
+        const uint32_t v = counts[(size_t)c * hs + t];
+        prefix[(size_t)c * hs + t] = run;
+        run += v;
+    }
+}
+
+__global__ void __launch_bounds__(ET_THREADS, 2) et_emit_kernel(
+    const uint32_t* __restrict__ order, const uint32_t* __restrict__ order_alt, const float4* __restrict__ xydr,
+    int n, int tiles_x, int tiles_y, int64_t capacity, const uint2* __restrict__ ranges,
+    const uint32_t* __restrict__ prefix, uint32_t* __restrict__ vals, const unsigned long long* __restrict__ meta) {
+    griddep_wait();
+    // meta[1]: the intersection total (tile scan); over capacity the ranges
+    // are empty and nothing is written (the host re-runs with more room)
+    if ((int64_t)meta[1] > capacity) return;
+    const int V = min(n, (int)meta[7]);
+    const int chunk = blockIdx.x;
+    if (chunk * ET_CHUNK >= V) return;
+    order = et_order(order, order_alt, meta);
+    const int n_tiles = tiles_x * tiles_y, hs = et_stride(n_tiles);
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned short* s_hist = reinterpret_cast<unsigned short*>(smem);                // [warp][tile]
+    uint32_t* s_base = reinterpret_cast<uint32_t*>(smem + (size_t)ET_WARPS * hs * 2);  // [tile]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    {
+        uint4* z = reinterpret_cast<uint4*>(smem);
+        const int n16 = (ET_WARPS * hs * 2 + 15) / 16;
+        for (int k = tid; k < n16; k += ET_THREADS) z[k] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    // every tile's start + the pairs of all earlier chunks (loads in flight
+    // together with the Gaussians')
+    const uint32_t* pre = prefix + (size_t)chunk * hs;
+#pragma unroll 4
+    for (int t = tid; t < n_tiles; t += ET_THREADS) s_base[t] = ranges[t].x + pre[t];
+    EtRound rd[ET_ROUNDS];
+    et_load(order, xydr, chunk * ET_CHUNK + warp * (32 * ET_ROUNDS) + lane, V, tiles_x, tiles_y, rd);
+    __syncthreads();
+    // 1. per-(warp, tile) pair counts (order-free: shared atomics on u16
+    //    halves; <= 256 per warp and tile, no carry)
+    uint32_t* h32 = reinterpret_cast<uint32_t*>(s_hist + warp * hs);
+#pragma unroll
+    for (int r = 0; r < ET_ROUNDS; ++r)
+        et_walk(lane, rd[r], tiles_x, [&](uint32_t tile, uint32_t) {
+            if (tile != 0xFFFFFFFFu) atomicAdd(&h32[tile >> 1], 1u << ((tile & 1u) * 16));
+        });
+    __syncthreads();
+    // 2. per tile: exclusive offsets over the warps
+    for (int t = tid; t < n_tiles; t += ET_THREADS) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < ET_WARPS; ++w) {
+            const uint32_t c = s_hist[w * hs + t];
+            s_hist[w * hs + t] = (unsigned short)run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    // 3. the same walk again, in order.  Each pair takes its warp's offset of
+    //    its tile with a returning shared atomic; when no two lanes of the
+    //    step share a tile (no lane's increment was followed by another's:
+    //    after - old == 1 everywhere) that offset is its slot.  Otherwise the
+    //    lanes of each shared tile re-rank in lane (= emission) order over
+    //    the group's range [after - k, after) (match_any, ~1 step in 10).
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < ET_ROUNDS; ++r)
+        et_walk(lane, rd[r], tiles_x, [&](uint32_t tile, uint32_t og) {
+            const bool valid = tile != 0xFFFFFFFFu;
+            const uint32_t sh = (tile & 1u) * 16;
+            uint32_t old = 0, base = 0;
+            if (valid) {
+                base = s_base[tile];
+                old = (atomicAdd(&h32[tile >> 1], 1u << sh) >> sh) & 0xFFFFu;
+            }
+            __syncwarp();
+            const uint32_t after = valid ? (h32[tile >> 1] >> sh) & 0xFFFFu : 0u;
+            if (__any_sync(0xffffffffu, after - old > 1u)) {
+                const uint32_t peers = __match_any_sync(0xffffffffu, tile);
+                old = after - (uint32_t)__popc(peers) + (uint32_t)__popc(peers & lt);
+            }
+            if (valid) vals[base + old] = og;
+            __syncwarp();  // the next step's atomics after every lane's read
+        });
+}
+
+static int et_attr(const void* k, size_t smem, size_t& done) {
+    if (smem > 48 * 1024 && smem > done) {
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return check_launch("emit_tiles smem attribute");
+        done = smem;
+    }
+    return 0;
+}
+
+int launch_emit_tiles_count(const uint32_t* order, const uint32_t* order_alt, const float* xydr4, int64_t n,
+                            int tiles_x, int tiles_y, void* table, uint32_t* totals, const unsigned long long* meta,
+                            cudaStream_t s) {
+    const int n_tiles = tiles_x * tiles_y;
+    if (!emit_tiles_fits(n_tiles)) return set_error("emit_tiles: %d tiles do not fit shared memory", n_tiles);
+    if (n <= 0) return 0;
+    const int64_t chunks = (n + ET_CHUNK - 1) / ET_CHUNK;  // capacity-sized grids: fewer visible -> early exit
+    const size_t smem_c = (size_t)et_stride(n_tiles) * 4;
+    static size_t done_c = 0;
+    if (et_attr((const void*)et_count_kernel, smem_c, done_c)) return -1;
+    unsigned short* counts = reinterpret_cast<unsigned short*>((char*)table + et_prefix_bytes(n, n_tiles));
+    launch_k(et_count_kernel, dim3((unsigned)chunks), dim3(ET_THREADS), smem_c, s, order, order_alt,
+             (const float4*)xydr4, (int)n, tiles_x, tiles_y, counts, meta);
+    if (check_launch("et_count_kernel")) return -1;
+    launch_k(et_scan_kernel, dim3((unsigned)((n_tiles + 31) / 32)), dim3(ES_WARPS * 32), 0, s,
+             (const unsigned short*)counts, (uint32_t*)table, (int)n, n_tiles, totals, meta);
+    return check_launch("et_scan_kernel");
+}
+
+int launch_emit_tiles(const uint32_t* order, const uint32_t* order_alt, const float* xydr4, int64_t n, int tiles_x,
+                      int tiles_y, int64_t capacity, const uint2* ranges, const void* table, uint32_t* vals,
+                      const unsigned long long* meta, cudaStream_t s) {
+    const int n_tiles = tiles_x * tiles_y;
+    if (!emit_tiles_fits(n_tiles)) return set_error("emit_tiles: %d tiles do not fit shared memory", n_tiles);
+    if (n <= 0) return 0;
+    const size_t smem = emit_tiles_smem(n_tiles);
+    static size_t done = 0;
+    if (et_attr((const void*)et_emit_kernel, smem, done)) return -1;
+    const int64_t chunks = (n + ET_CHUNK - 1) / ET_CHUNK;
+    launch_k(et_emit_kernel, dim3((unsigned)chunks), dim3(ET_THREADS), smem, s, order, order_alt,
+             (const float4*)xydr4, (int)n, tiles_x, tiles_y, capacity, ranges, (const uint32_t*)table, vals, meta);
+    return check_launch("et_emit_kernel");
+}
+
 // ---------------------------------------------------------------- scatter binning
 // Small scenes (frame.cu): the projection counts every tile's intersections
 // (project_fwd_kernel<2>); one CTA scans those counts into the tile ranges
@@ -472,6 +790,7 @@ int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* 
 // empty and every cursor at capacity (the scatter then writes nothing; the
 // host reruns with more room).  order != nullptr: also the heaviest-first
 // raster launch order (tile_order_kernel's bucketing).
+template <int REPL>
 __global__ void __launch_bounds__(1024) tile_scan_kernel(uint32_t* __restrict__ tcount, int n_tiles,
                                                          int64_t capacity, uint2* __restrict__ ranges,
                                                          unsigned long long* __restrict__ total,
@@ -486,7 +805,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(uint32_t* __restrict__ 
     auto tile_count = [&](int t) {
         uint32_t c = 0;
 #pragma unroll
-        for (int r = 0; r < TCOUNT_REPL; ++r) c += tcount[(size_t)r * n_tiles + t];
+        for (int r = 0; r < REPL; ++r) c += tcount[(size_t)r * n_tiles + t];
         return c;
     };
     uint32_t sum = 0;
@@ -514,9 +833,9 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(uint32_t* __restrict__ 
     for (int tb = c0; tb < c1; tb += 32) {
         const int t = tb + lane;
         const bool in = t < c1;
-        uint32_t cr[TCOUNT_REPL], c = 0;
+        uint32_t cr[REPL], c = 0;
 #pragma unroll
-        for (int r = 0; r < TCOUNT_REPL; ++r) {
+        for (int r = 0; r < REPL; ++r) {
             cr[r] = in ? tcount[(size_t)r * n_tiles + t] : 0u;
             c += cr[r];
         }
@@ -531,7 +850,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(uint32_t* __restrict__ 
         if (in) {
             uint32_t cur = start;
 #pragma unroll
-            for (int r = 0; r < TCOUNT_REPL; ++r) {  // replica r's cursor: the tile start + earlier replicas
+            for (int r = 0; r < REPL; ++r) {  // replica r's cursor: the tile start + earlier replicas
                 tcount[(size_t)r * n_tiles + t] = over ? (uint32_t)capacity : cur;
                 cur += cr[r];
             }
@@ -558,9 +877,13 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(uint32_t* __restrict__ 
 }
 
 int launch_tile_scan(uint32_t* tcount, int n_tiles, int64_t capacity, uint2* ranges, unsigned long long* total,
-                     uint32_t* order, cudaStream_t s) {
+                     uint32_t* order, cudaStream_t s, int replicas) {
     if (n_tiles <= 0 || n_tiles > 65536) return set_error("tile_scan: %d tiles out of range", n_tiles);
-    launch_k(tile_scan_kernel, dim3(1), dim3(1024), 0, s, tcount, n_tiles, capacity, ranges, total, order);
+    if (replicas == 1)
+        launch_k(tile_scan_kernel<1>, dim3(1), dim3(1024), 0, s, tcount, n_tiles, capacity, ranges, total, order);
+    else
+        launch_k(tile_scan_kernel<TCOUNT_REPL>, dim3(1), dim3(1024), 0, s, tcount, n_tiles, capacity, ranges, total,
+                 order);
     return check_launch("tile_scan_kernel");
 }
 

@@ -6,6 +6,10 @@
 //   -> scan of tile counts in depth order -> emission of (tile, gaussian)
 //   pairs in depth order (+ tile-digit histograms) -> 1-2 pass stable sort by
 //   tile id -> per-tile ranges (+ raster order) -> raster forward.
+//   With the tile-sorted emission (option tile_emit, <= 10240 tiles), the
+//   emission and the sort by tile are one stable counting pass instead:
+//   per-(chunk, tile) pair counts -> column prefixes + tile totals -> tile
+//   scan (ranges, raster order) -> every pair written to its final slot.
 // gs_frame_forward, scatter binning (N <= 400k):
 //   project (+ depth keys and per-tile intersection counts) -> tile scan
 //   (ranges, cursors, raster order) -> pair scatter -> per-tile (depth,
@@ -74,6 +78,7 @@ struct Layout {
     // zeroed region
     size_t zero_begin, meta, dhist, thist, counters, scan_ws, dstatus, tstatus, zero_end;
     // backward
+    size_t etable;  // tile-sorted emission: per-(chunk, tile) counts and prefixes
     size_t d_geo, d_c11, pbwd_done, partials;
     size_t total;
 };
@@ -119,6 +124,7 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.dstatus = take(onesweep_status_bytes<uint32_t>(n, 4));
     L.tstatus = take(onesweep_status_bytes<uint32_t>(cap, tp));
     L.zero_end = o;
+    L.etable = take(emit_tiles_fits((int)nt) ? emit_tiles_table_bytes(n, (int)nt) : 0);
     L.d_geo = take(32 * n);  // interleaved screen-space gradients: [d_rgbo 4 | d_geo 4] per Gaussian
     L.d_c11 = take(4 * n);
     L.pbwd_done = take(16);  // last-block counter of the projection backward (zeroed with the accumulators)
@@ -225,16 +231,18 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     // resets meta and the depth histograms, and the projection kernel clears
     // the later stages' counters / look-back status / tile ranges and the
     // backward's screen-space accumulators (zeroed here, once per forward).
+    const int n_tiles = tiles_x * tiles_y;
+    const Binning binning = binning_for(n, n_tiles);
+    // depth-first binning with the tile-sorted emission (no global sort by tile)
+    const bool etiles = binning == DEPTH_FIRST && tile_emit() && emit_tiles_fits(n_tiles);
     ZeroJobs zj;
     zj.p[0] = at<uint4>(ws, L.thist);
-    zj.n16[0] = (L.zero_end - L.thist) / 16;
+    zj.n16[0] = ((etiles ? L.tstatus : L.zero_end) - L.thist) / 16;  // (no tile-pass look-back status)
     zj.p[1] = at<uint4>(ws, L.ranges);
     zj.n16[1] = (8 * (size_t)tiles_x * tiles_y + 15) / 16;
     zj.p[2] = at<uint4>(ws, L.d_geo);  // the backward accumulators: only when not known clean (meta[4])
     zj.n16[2] = (L.partials - L.d_geo) / 16;
     zj.cond2 = meta + 4;
-    const int n_tiles = tiles_x * tiles_y;
-    const Binning binning = binning_for(n, n_tiles);
     const bool scatter = binning == SCATTER;
     const bool direct = binning == DIRECT && counts4 == nullptr;  // the counted pass bins by scatter
     const int64_t kstride = direct_stride(isect_capacity, n_tiles);
@@ -302,6 +310,32 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
         return -1;
     const uint32_t* order = at<uint32_t>(ws, L.order);
     mark(stage_events, 2, s);
+    if (etiles) {
+        // 3. per-(chunk of the depth order, tile) pair counts, their column
+        //    prefixes and the tiles' totals -> ranges (+ total -> meta[1],
+        //    raster order)
+        uint32_t* totals = at<uint32_t>(ws, L.tcount);
+        if (launch_emit_tiles_count(order, at<uint32_t>(ws, L.order_alt), at<float>(ws, L.xydr), n, tiles_x, tiles_y,
+                                    at<char>(ws, L.etable), totals, meta, s))
+            return -1;
+        if (launch_tile_scan(totals, n_tiles, isect_capacity, at<uint2>(ws, L.ranges), meta + 1,
+                             const_cast<uint32_t*>(t_order), s, 1))
+            return -1;
+        mark(stage_events, 3, s);
+        // 4. every pair straight to its slot, tile lists in (depth, index) order
+        if (launch_emit_tiles(order, at<uint32_t>(ws, L.order_alt), at<float>(ws, L.xydr), n, tiles_x, tiles_y,
+                              isect_capacity, at<uint2>(ws, L.ranges), at<char>(ws, L.etable),
+                              at<uint32_t>(ws, L.tvals), meta, s))
+            return -1;
+        mark(stage_events, 4, s);
+        if (launch_raster_fwd(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.tvals), at<float>(ws, L.xydr),
+                              at<float>(ws, L.conic), colors3, bg, W, H, early_termination != 0, out_image,
+                              out_final_T, out_n_contrib, counts4, s, at<uint2>(ws, L.rec),
+                              at<uint32_t>(ws, L.rec_count), t_order))
+            return -1;
+        mark(stage_events, 5, s);
+        return 0;
+    }
     // 3+4. fused: scan of the tile counts (in depth order), total ->
     //      meta[1], emission of the (tile, gaussian) pairs + tile-digit histograms
     // (an odd number of tile passes starts from the alternate buffers, so the

@@ -470,9 +470,11 @@ class Frame:
             end = torch.cumsum(cnt, 0)
             ranges = torch.stack([end - cnt, end], 1).to(torch.int32)
             ranges[cnt == 0] = 0  # empty tiles: (0, 0), as the other binnings write them
-        else:
+        else:  # compact tile-ordered lists; the tile keys follow from the ranges (the
+            # tile-sorted emission writes no keys)
             sorted_vals = sl(v.sorted_vals, m, torch.int32, (m,))
-            sorted_tile_keys = sl(v.sorted_tile_keys, m, torch.int32, (m,))
+            cnt = (ranges[:, 1] - ranges[:, 0]).long()
+            sorted_tile_keys = torch.repeat_interleave(torch.arange(nt, device=cnt.device, dtype=torch.int32), cnt)
         mh = self._meta_host()
         n_sorted = min(mh[7], n)  # depth-first binning: the visible Gaussians by (depth, index)
         dptr = v.depth_order_alt if mh[8] & 1 else v.depth_order

@@ -50,18 +50,26 @@ def test_frame_equals_staged_on_golden(name, cuda):
         assert r["ok"], (name, k, r)
 
 
-@pytest.fixture(params=[(1, 1), (2, 1), (2, 0), (3, 1)],
-                ids=["depth_first", "scatter", "scatter_sort_kernel", "direct"])
+@pytest.fixture(params=[(1, 1, 1), (1, 1, 0), (2, 1, 1), (2, 0, 1), (3, 1, 1)],
+                ids=["depth_first", "depth_first_onesweep", "scatter", "scatter_sort_kernel", "direct"])
 def binning(request, cuda):
-    """Run a test under every frame binning strategy (gs_set_option), the
-    scatter one with its per-tile sort fused into the raster forward and as
-    its own kernel."""
+    """Run a test under every frame binning strategy (gs_set_option): the
+    depth-first one with the tile-sorted emission and with emission + onesweep
+    by tile, the scatter one with its per-tile sort fused into the raster
+    forward and as its own kernel."""
     from paper_2312_02121_b200 import ops
     ops.set_option("binning", request.param[0])
     ops.set_option("fuse_sort", request.param[1])
+    ops.set_option("tile_emit", request.param[2])
     yield request.param[0]
     ops.set_option("binning", 0)
     ops.set_option("fuse_sort", 1)
+    ops.set_option("tile_emit", 1)
+
+
+def _modes():
+    """(binning, tile_emit) of every list-producing path."""
+    return [(1, 1), (1, 0), (2, 1), (3, 1)]
 
 
 @pytest.mark.parametrize("name", golden_names())
@@ -164,6 +172,31 @@ def test_capacity_overflow_reruns(cuda):
     assert int(m[1]) == full.n_isect and int(m[0]) == -1
 
 
+@pytest.mark.parametrize("tile_emit", [1, 0])
+def test_depth_first_capacity_overflow_reruns(tile_emit, cuda):
+    """Depth-first binning over capacity: the tile scan leaves every range
+    empty and the emission writes nothing; the re-run at the reported total
+    equals a frame sized right."""
+    from paper_2312_02121_b200 import ops
+    g = load_golden("cfg0_mini")
+    t = _tensors(g["inputs"], cuda)
+    cp = ops.CameraParams.of(g["camera"])
+    ops.set_option("binning", 1)
+    ops.set_option("tile_emit", tile_emit)
+    try:
+        full = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True)
+        small = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True, capacity=100)
+        raw = ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True, capacity=100, check_meta=False)
+        m = raw.meta().cpu()
+        assert int(m[1]) == full.n_isect and int(m[0]) == -1
+        assert small.capacity >= small.n_isect > 100
+        assert torch.equal(full.image, small.image)
+        assert torch.equal(full.tensors()["sorted_vals"], small.tensors()["sorted_vals"])
+    finally:
+        ops.set_option("binning", 0)
+        ops.set_option("tile_emit", 1)
+
+
 def test_frame_errors_and_empty(cuda):
     from paper_2312_02121_b200 import ops
     cp = ops.CameraParams(np.eye(4).tolist(), 16.0, 16.0, 8.0, 8.0, 16, 16, 0.1, 100.0)
@@ -231,19 +264,21 @@ def test_binning_strategies_agree_on_configs(config, cuda):
     cam = ops.CameraParams.of(spec.cameras[0])
     got = {}
     try:
-        for mode in (1, 2, 3):
-            ops.set_option("binning", mode)
+        for mode in _modes():
+            ops.set_option("binning", mode[0])
+            ops.set_option("tile_emit", mode[1])
             fr = ops.frame_forward(*t, cam, (0.0, 0.0, 0.0), True)
             tv = fr.tensors()
             got[mode] = (tv["ranges"].clone(), tv["sorted_vals"].clone(), fr.image.clone())
             del fr, tv
     finally:
         ops.set_option("binning", 0)
-    lens = (got[1][0][:, 1] - got[1][0][:, 0])
+        ops.set_option("tile_emit", 1)
+    lens = (got[(1, 1)][0][:, 1] - got[(1, 1)][0][:, 0])
     if config == 2:
         assert int(lens.max()) > 512
-    for m in (2, 3):
-        for a, b in zip(got[1], got[m]):
+    for m in _modes()[1:]:
+        for a, b in zip(got[(1, 1)], got[m]):
             assert torch.equal(a, b)
 
 
@@ -274,17 +309,19 @@ def test_scatter_binning_ties_in_long_lists(cuda):
     t = _tensors((means, scales, quats, opac, cols), cuda)
     got = {}
     try:
-        for mode in (1, 2, 3):
-            ops.set_option("binning", mode)
+        for mode in _modes():
+            ops.set_option("binning", mode[0])
+            ops.set_option("tile_emit", mode[1])
             fr = ops.frame_forward(*t, cam, (0.0, 0.0, 0.0), True)
             tv = fr.tensors()
             got[mode] = (tv["ranges"].clone(), tv["sorted_vals"].clone(), fr.image.clone())
     finally:
         ops.set_option("binning", 0)
-    lens = got[1][0][:, 1] - got[1][0][:, 0]
+        ops.set_option("tile_emit", 1)
+    lens = got[(1, 1)][0][:, 1] - got[(1, 1)][0][:, 0]
     assert int(lens.max()) > 512 and bool(((lens > 1) & (lens <= 512)).any())
-    for m in (2, 3):
-        for a, b in zip(got[1], got[m]):
+    for m in _modes()[1:]:
+        for a, b in zip(got[(1, 1)], got[m]):
             assert torch.equal(a, b)
 
 
