@@ -2,6 +2,8 @@
 // tile counts (single-pass decoupled look-back), key emission and per-tile
 // range detection.  Together with sort.cu these replace sg/binning.py:27-65
 // (assign_tiles + sort_bins).  All HBM-bound.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.cuh"
 
@@ -537,6 +539,7 @@ __device__ __forceinline__ void et_walk(int lane, const EtRound& rd, int tiles_x
     }
     const uint32_t excl = incl - cnt, total = __shfl_sync(0xffffffffu, incl, 31);
     const float rw = rd.w > 0 ? 1.f / (float)rd.w : 0.f;
+    const int tb = rd.ty0 * tiles_x + rd.tx0;  // the tile of the lane's first pair
     const uint32_t le = lanemask_lt() | (1u << lane);
     for (uint32_t t0 = 0; t0 < total; t0 += 32) {
         const uint32_t first = __ballot_sync(0xffffffffu, cnt != 0u && excl <= t0);
@@ -544,15 +547,15 @@ __device__ __forceinline__ void et_walk(int lane, const EtRound& rd, int tiles_x
         const uint32_t starts = __reduce_or_sync(0xffffffffu, (cnt != 0u && excl > t0 && sp < 32u) ? 1u << sp : 0u);
         const int L = (31 - __clz((int)first)) + __popc(starts & le);
         const uint32_t t = t0 + lane;
-        const uint32_t j = t - __shfl_sync(0xffffffffu, excl, L);
+        const int j = (int)(t - __shfl_sync(0xffffffffu, excl, L));
         const int ow = __shfl_sync(0xffffffffu, rd.w, L);
         const float orw = __shfl_sync(0xffffffffu, rw, L);
-        const int otx0 = __shfl_sync(0xffffffffu, rd.tx0, L), oty0 = __shfl_sync(0xffffffffu, rd.ty0, L);
+        const int otb = __shfl_sync(0xffffffffu, tb, L);
         const uint32_t og = __shfl_sync(0xffffffffu, rd.g, L);
         int row = (int)((float)j * orw);
-        if (row * ow > (int)j) --row;
-        if ((row + 1) * ow <= (int)j) ++row;
-        f(t < total ? (uint32_t)((oty0 + row) * tiles_x + otx0 + ((int)j - row * ow)) : 0xFFFFFFFFu, og);
+        if (row * ow > j) --row;
+        if ((row + 1) * ow <= j) ++row;
+        f(t < total ? (uint32_t)(otb + row * (tiles_x - ow) + j) : 0xFFFFFFFFu, og);
     }
 }
 
@@ -674,13 +677,12 @@ __global__ void __launch_bounds__(ET_THREADS, 2) et_emit_kernel(
         const int n16 = (ET_WARPS * hs * 2 + 15) / 16;
         for (int k = tid; k < n16; k += ET_THREADS) z[k] = make_uint4(0u, 0u, 0u, 0u);
     }
-    // every tile's start + the pairs of all earlier chunks (loads in flight
-    // together with the Gaussians')
+    EtRound rd[ET_ROUNDS];
+    et_load(order, xydr, chunk * ET_CHUNK + warp * (32 * ET_ROUNDS) + lane, V, tiles_x, tiles_y, rd);
+    // every tile's start + the pairs of all earlier chunks
     const uint32_t* pre = prefix + (size_t)chunk * hs;
 #pragma unroll 4
     for (int t = tid; t < n_tiles; t += ET_THREADS) s_base[t] = ranges[t].x + pre[t];
-    EtRound rd[ET_ROUNDS];
-    et_load(order, xydr, chunk * ET_CHUNK + warp * (32 * ET_ROUNDS) + lane, V, tiles_x, tiles_y, rd);
     __syncthreads();
     // 1. per-(warp, tile) pair counts (order-free: shared atomics on u16
     //    halves; <= 256 per warp and tile, no carry)
@@ -764,10 +766,10 @@ int launch_emit_tiles(const uint32_t* order, const uint32_t* order_alt, const fl
     const int n_tiles = tiles_x * tiles_y;
     if (!emit_tiles_fits(n_tiles)) return set_error("emit_tiles: %d tiles do not fit shared memory", n_tiles);
     if (n <= 0) return 0;
+    const int64_t chunks = (n + ET_CHUNK - 1) / ET_CHUNK;
     const size_t smem = emit_tiles_smem(n_tiles);
     static size_t done = 0;
     if (et_attr((const void*)et_emit_kernel, smem, done)) return -1;
-    const int64_t chunks = (n + ET_CHUNK - 1) / ET_CHUNK;
     launch_k(et_emit_kernel, dim3((unsigned)chunks), dim3(ET_THREADS), smem, s, order, order_alt,
              (const float4*)xydr4, (int)n, tiles_x, tiles_y, capacity, ranges, (const uint32_t*)table, vals, meta);
     return check_launch("et_emit_kernel");

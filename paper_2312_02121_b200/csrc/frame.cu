@@ -6,7 +6,7 @@
 //   -> scan of tile counts in depth order -> emission of (tile, gaussian)
 //   pairs in depth order (+ tile-digit histograms) -> 1-2 pass stable sort by
 //   tile id -> per-tile ranges (+ raster order) -> raster forward.
-//   With the tile-sorted emission (option tile_emit, <= 10240 tiles), the
+//   With the tile-sorted emission (option tile_emit, <= 8500 tiles), the
 //   emission and the sort by tile are one stable counting pass instead:
 //   per-(chunk, tile) pair counts -> column prefixes + tile totals -> tile
 //   scan (ranges, raster order) -> every pair written to its final slot.
