@@ -230,7 +230,7 @@ def run_ours(args):
     # roofline numerators: evaluation-class counts of a counted pass (untimed)
     counts_f = np.zeros(4, np.int64)
     counts_b = np.zeros(3, np.int64)
-    caps, wss, isect, binnings = [], [], [], []
+    caps, wss, isect, binnings, visible = [], [], [], [], []
     for cam, d_img in zip(cams, d_imgs):
         fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, counts=True)
         g = ops.frame_backward(fr, m, s, q, c, d_img, counts=True)
@@ -242,6 +242,7 @@ def run_ours(args):
         fr = ops.frame_forward(m, s, q, o, c, cam, bg, True)
         cap = int(fr.needed_capacity * 1.05) + 4096
         caps.append(cap)
+        visible.append(min(int(fr.meta().cpu()[7]), n))  # depth-first: the depth-sorted (visible) Gaussians
         binnings.append(fr.binning)
         wss.append(ops.frame_workspace(n, cap, cam.width, cam.height, dev))
         del fr
@@ -345,8 +346,13 @@ def run_ours(args):
     if sampler:
         sampler.start()
     step_ms = []
-    stage_names = ("project", "depth_sort", "scan_emit", "tile_sort_ranges", "raster_fwd", "raster_bwd",
-                   "project_bwd")
+    from paper_2312_02121_b200 import ops as _ops
+    tile_emit = _ops.frame_tile_emit(n, cams[0])
+    # depth-first binning with the tile-sorted emission: (per-chunk tile counts, column prefixes,
+    # tile scan) then the emission into the final slots; otherwise fused scan + emission then the
+    # onesweep passes by tile + ranges
+    stage_names = ("project", "depth_sort", "tile_counts" if tile_emit else "scan_emit",
+                   "tile_emit" if tile_emit else "tile_sort_ranges", "raster_fwd", "raster_bwd", "project_bwd")
     stage_ms = np.zeros(len(stage_names))
     timed_bwd_ms = 0.0
     stream = torch.cuda.current_stream()
@@ -427,6 +433,9 @@ def run_ours(args):
     seg = binning != "depth_first"
     direct = binning == "direct"
     fused = fused_sort(n, cams[0])
+    vis = float(sum(visible))  # visible Gaussians over the rank's views (the depth-sorted ones)
+    chunks_x_tiles = float(sum(((v + 2047) // 2048) * ((cm.tiles_x * cm.tiles_y + 1) & ~1)
+                               for v, cm in zip(visible, cams)))
     work = {
         # 72 B per Gaussian (read mean 12 + scale 12 + quat 16; write mean2d 8 +
         # cov/conic 12 + depth 4 + radius 4 + tiles 4).  The kernel itself moves 84 B (+ opacity
@@ -447,6 +456,11 @@ def run_ours(args):
         "tile_sort_ranges": ("none", 0.0) if fused else
                             ("hbm", (12.0 * I + 8.0 * n_tiles) if seg else
                              (tp * 16.0 * I + 4.0 * I + 8.0 * n_tiles)),
+        # tile-sorted emission: order + xydr gather per visible Gaussian, u16 counts out, column
+        # scan (u16 in, u32 prefix out), tile scan (4 B in, 8 B ranges out per tile)
+        "tile_counts": ("hbm", 20.0 * vis + 8.0 * chunks_x_tiles + 12.0 * n_tiles),
+        # order + xydr gather per visible Gaussian, ranges + prefix per (chunk, tile), 4 B per pair out
+        "tile_emit": ("hbm", 20.0 * vis + 8.0 * chunks_x_tiles + 4.0 * I),
         "raster_fwd": ("fp32", float(F_fwd)),
         "raster_bwd": ("fp32", float(F_bwd)),
         # 104 B per Gaussian (read mean, scale, quat 40 + d_mean2d 8 + d_cov 12 +

@@ -21,7 +21,7 @@ EXPORTS = (
     "gs_sort_workspace_bytes", "gs_sort_pairs", "gs_tile_counts", "gs_tile_ranges",
     "gs_raster_fwd", "gs_raster_bwd",
     "gs_project_bwd_workspace_bytes", "gs_project_bwd",
-    "gs_frame_workspace_bytes", "gs_frame_workspace_init", "gs_frame_binning", "gs_frame_view_of",
+    "gs_frame_workspace_bytes", "gs_frame_workspace_init", "gs_frame_binning", "gs_frame_tile_emit", "gs_frame_view_of",
     "gs_frame_forward", "gs_frame_backward", "gs_frame_project_backward",
     "gs_activate", "gs_loss_l2", "gs_adam_step",
     "gs_conic_from_cov", "gs_eval_alpha", "gs_composite_pixels", "gs_composite_pixels_bwd",
@@ -94,6 +94,7 @@ def load():
         "gs_project_bwd": ([P, P, P, i64, cam, P, P, P, P, P, P, P, P, sz, P], C.c_int),
         "gs_frame_workspace_bytes": ([i64, i64, i32, i32], sz),
         "gs_frame_binning": ([i64, i32, i32], C.c_int),
+        "gs_frame_tile_emit": ([i64, i32, i32], C.c_int),
         "gs_frame_view_of": ([i64, i64, i32, i32, P, C.POINTER(GsFrameView)], C.c_int),
         "gs_frame_workspace_init": ([i64, i64, i32, i32, P, P], C.c_int),
         "gs_frame_forward": ([P, P, P, P, P, i64, cam, C.POINTER(C.c_float), C.c_int, i64, P, sz, P, P, P, P, P,

@@ -173,6 +173,11 @@ int gs_frame_binning(int64_t n, int32_t width, int32_t height) {
     return (int)binning_for(n, ((width + TILE - 1) / TILE) * ((height + TILE - 1) / TILE));
 }
 
+int gs_frame_tile_emit(int64_t n, int32_t width, int32_t height) {
+    const int nt = ((width + TILE - 1) / TILE) * ((height + TILE - 1) / TILE);
+    return binning_for(n, nt) == DEPTH_FIRST && tile_emit() && emit_tiles_fits(nt) ? 1 : 0;
+}
+
 size_t gs_frame_workspace_bytes(int64_t n, int64_t isect_capacity, int32_t width, int32_t height) {
     return layout(n, isect_capacity, width, height).total;
 }

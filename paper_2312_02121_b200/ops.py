@@ -85,6 +85,12 @@ def frame_binning(n: int, cam) -> str:
     return {1: "depth_first", 2: "scatter", 3: "direct"}[b]
 
 
+def frame_tile_emit(n: int, cam) -> bool:
+    """Whether gs_frame_forward's depth-first binning uses the tile-sorted
+    emission for n Gaussians on this view (gs_frame_tile_emit)."""
+    return bool(_lib.load().gs_frame_tile_emit(int(n), int(cam.width), int(cam.height)))
+
+
 def get_option(name: str) -> int:
     """Current value of a gs_set_option option (gs_get_option)."""
     v = int(_lib.load().gs_get_option(name.encode()))

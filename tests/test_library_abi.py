@@ -48,12 +48,18 @@ def test_set_option():
     for v in (0, 1):
         ops.set_option("fuse_sort", v)
         assert ops.get_option("fuse_sort") == v
+    for v in (0, 1):
+        ops.set_option("tile_emit", v)
+        assert ops.get_option("tile_emit") == v
     with pytest.raises(_lib.SplatLibError, match="binning"):
         ops.set_option("binning", 7)
     L = _lib.load()
     assert L.gs_frame_binning(100000, 800, 800) == 3  # auto: direct (2500 tiles)
     assert L.gs_frame_binning(100000, 1920, 1080) == 2  # 8160 tiles: scatter
     assert L.gs_frame_binning(1000000, 800, 800) == 1  # large scene: depth-first
+    assert L.gs_frame_tile_emit(1000000, 800, 800) == 1  # ... with the tile-sorted emission (2500 tiles)
+    assert L.gs_frame_tile_emit(1000000, 3840, 2160) == 0  # 32400 tiles: emission + onesweep by tile
+    assert L.gs_frame_tile_emit(100000, 800, 800) == 0  # direct binning
     with pytest.raises(_lib.SplatLibError, match="fuse_sort"):
         ops.set_option("fuse_sort", 2)
     with pytest.raises(_lib.SplatLibError, match="unknown option"):
