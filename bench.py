@@ -260,6 +260,11 @@ def run_ours(args):
     grad_out = E.unpack(grad_flat, n)
 
     ev_t = [mk_events(3) for _ in cams]  # timed graph: only around the dominant kernel (raster bwd)
+    # several views: every view runs its raster backward only, then one batched projection
+    # backward over all views (gs_frame_views_project_backward); GS_BATCHED_PROJ=0: per view
+    batched = len(cams) > 1 and os.environ.get("GS_BATCHED_PROJ", "1") != "0"
+    ev_pb = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]  # recorded inside capture
+    d_views = torch.zeros((len(cams), 4, 4), device=dev, dtype=torch.float32)
 
     def step(staged=False):
         # every view writes (first) or accumulates (others) straight into
@@ -292,13 +297,19 @@ def run_ours(args):
                 ops.frame_backward(fr, m, s, q, c, d_img,
                                    events=ev_b[vi] if staged else [ev_t[vi][0], ev_t[vi][1], None],
                                    out=grad_out, accumulate=vi > 0, wait_before_accumulate=bwd_done,
-                                   project=not tail)
-                if two:
+                                   project=not (tail or batched))
+                if two and not batched:
                     bwd_done = torch.cuda.Event()
                     bwd_done.record(st)
             frames_out[vi] = fr
         for a in sts[1:]:
             main.wait_stream(a)
+        if batched and world == 1:  # N > 1: bucketed under the all-reduce in run_step
+            if staged:
+                ev_pb[0].record()
+            ops.frame_views_project_backward(frames_out, m, s, q, grad_out, d_views)
+            if staged:
+                ev_pb[1].record()
 
     aux = [torch.cuda.Stream() for _ in range(max(args.streams - 1, 0))]
     graph = graph_staged = None
@@ -328,7 +339,9 @@ def run_ours(args):
             step(staged)
         if world > 1:
             fr = frames_out[-1]
-            if band is None:  # view shards: 14 fp32 per Gaussian, all-reduced under the last projection bwd
+            if band is None and batched:  # view shards: all-reduced under the batched projection bwd
+                reducer.wait(reducer.views(frames_out, params, grad_out, d_views))
+            elif band is None:  # view shards: 14 fp32 per Gaussian, all-reduced under the last projection bwd
                 reducer.wait(reducer.last_view(fr, params, grad_out, d_view_tail, accumulate=len(cams) > 1))
             else:  # tile bands: 9 screen-space fp32 per Gaussian, then the projection bwd on every rank
                 rows, c11 = ops.frame_screen_grads(fr)
@@ -386,7 +399,10 @@ def run_ours(args):
             stage_ms[3] += f[3].elapsed_time(f[4])
             stage_ms[4] += f[4].elapsed_time(f[5])
             stage_ms[5] += b[0].elapsed_time(b[1])
-            stage_ms[6] += b[1].elapsed_time(b[2])
+            if not batched:
+                stage_ms[6] += b[1].elapsed_time(b[2])
+        if batched and world == 1:
+            stage_ms[6] += ev_pb[0].elapsed_time(ev_pb[1])
     # the capacity was sized from a checked run; confirm nothing overflowed
     for vi, fr in enumerate(frames_out):
         meta = fr.meta().cpu()
@@ -467,7 +483,11 @@ def run_ours(args):
         # radius/visibility 4; write d_mean, d_scale, d_quat 40).  The kernel also copies the
         # d_color/d_opacity row (16 + 16), clears the rows it read, and views after the first
         # read-modify-write the running sums
-        "project_bwd": ("hbm", 104.0 * n * nv),
+        # batched over the views (one pass): parameters read once (40 B) and the sums written once
+        # (56 B) per Gaussian; per view the screen-space rows read (36 B, every Gaussian) and
+        # cleared (36 B, the visible ones) -- §8(d)'s per-view 104 B would count the parameter
+        # traffic once per view
+        "project_bwd": ("hbm", (96.0 * n + 36.0 * n * nv + 36.0 * vis) if batched else 104.0 * n * nv),
     }
     st = {}
     for name, ms in zip(stage_names, stage_ms):

@@ -277,6 +277,26 @@ int gs_frame_project_backward(const float* means3, const float* scales3, const f
                               const gs_camera* cam /*[host]*/, int64_t isect_capacity, void* ws, size_t ws_bytes,
                               int64_t begin, int64_t end, float* d_means3, float* d_scales3, float* d_quats4,
                               float* d_rgbo4, float* d_view16, int flags, gs_stream_t stream);
+/* The projection backward of all views of a multi-view step at once
+ * (sg/proj_backward.py:178-223 per view, summed over the views): after each
+ * view's gs_frame_backward with flag bit 3 (raster backward only; every view
+ * on its own workspace), one pass over Gaussians [begin, end) reads the
+ * parameters once and every view's screen-space gradient rows, and writes
+ * (flag bit 0: adds to) d_means3 / d_scales3 / d_quats4 / d_rgbo4 the sums
+ * over the views, and d_views16 (n_views x 16, flag bit 4: added) per view.
+ * A Gaussian counts as visible in a view iff its rows there are non-zero (a
+ * culled one's rows are never written; zero rows contribute exactly zero).
+ * The rows read are cleared and each workspace stamped clean unless flag bit
+ * 1 keeps them.  cams / capacities / workspaces / ws_bytes: [host] n_views
+ * entries, as given to each view's gs_frame_forward.  Against
+ * gs_frame_backward per view it moves ~76 instead of ~224 bytes per visible
+ * Gaussian and view (parameters read once, sums written once). */
+int gs_frame_views_project_backward(const float* means3, const float* scales3, const float* quats4, int64_t n,
+                                    int32_t n_views, const gs_camera* cams /*[host]*/,
+                                    const int64_t* capacities /*[host]*/, void* const* workspaces /*[host]*/,
+                                    const size_t* ws_bytes /*[host]*/, int64_t begin, int64_t end,
+                                    float* d_means3, float* d_scales3, float* d_quats4, float* d_rgbo4,
+                                    float* d_views16, int flags, gs_stream_t stream);
 
 /* ---- Training step around the path (sg/optimize.py:96-190 fit) ----------
  * gs_activate : scales = exp(log_scales), opacities = sigmoid(logits)  (:144-145)

@@ -460,4 +460,42 @@ int gs_frame_project_backward(const float* means3, const float* scales3, const f
                               (flags & 16) != 0, (flags & 32) != 0);
 }
 
+int gs_frame_views_project_backward(const float* means3, const float* scales3, const float* quats4, int64_t n,
+                                    int32_t n_views, const gs_camera* cams, const int64_t* capacities,
+                                    void* const* workspaces, const size_t* ws_bytes, int64_t begin, int64_t end,
+                                    float* d_means3, float* d_scales3, float* d_quats4, float* d_rgbo4,
+                                    float* d_views16, int flags, gs_stream_t stream) {
+    if (n_views < 0 || (n_views > 0 && (!cams || !capacities || !workspaces || !ws_bytes)))
+        return set_error("gs_frame_views_project_backward: bad view arrays");
+    if (begin < 0 || end > n || begin > end)
+        return set_error("gs_frame_views_project_backward: range [%lld, %lld) outside [0, %lld)", (long long)begin,
+                         (long long)end, (long long)n);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool keep = (flags & 2) != 0;
+    for (int v0 = 0; v0 < n_views; v0 += MV_MAX) {
+        MvArgs a;
+        a.nv = n_views - v0 < MV_MAX ? n_views - v0 : MV_MAX;
+        for (int j = 0; j < a.nv; ++j) {
+            const gs_camera& c = cams[v0 + j];
+            const Layout L = layout(n, capacities[v0 + j], c.width, c.height);
+            if (ws_bytes[v0 + j] < L.total)
+                return set_error("gs_frame_views_project_backward: workspace %d too small", v0 + j);
+            void* ws = workspaces[v0 + j];
+            MvView& V = a.v[j];
+            V.cam = make_camk(c);
+            V.g8 = at<float4>(ws, L.d_geo) + 2 * begin;
+            V.d_c11 = at<float>(ws, L.d_c11) + begin;
+            V.partials = at<float>(ws, L.partials);
+            V.clean_word = at<unsigned long long>(ws, L.clean);
+            V.clean_stamp = keep ? 0ull : clean_sig(n, capacities[v0 + j], c.width, c.height);
+        }
+        if (launch_views_project_bwd(means3 + 3 * begin, scales3 + 3 * begin, quats4 + 4 * begin, end - begin, a,
+                                     d_means3 + 3 * begin, d_scales3 + 3 * begin, d_quats4 + 4 * begin,
+                                     d_rgbo4 + 4 * begin, d_views16 + 16 * v0, (flags & 1) != 0 || v0 > 0, !keep,
+                                     (flags & 16) != 0, s))
+            return -1;
+    }
+    return 0;
+}
+
 }  // extern "C"

@@ -32,6 +32,25 @@ int launch_project_bwd(const float* means3, const float* scales3, const float* q
 // gstride 2: d_geo4 rows interleaved with d_rgbo rows (g8 layout); with
 // rgbo_in, each Gaussian's d_rgbo row is copied (or added) to rgbo_out.
 constexpr int PBWD_BLOCK = 256;
+// all views of a step at once (project.cu): per view its camera, its
+// workspace's screen-space gradient rows ([d_rgbo4 | d_geo4] per Gaussian,
+// d_c11), its d_view partials (>= blocks x 12 floats) and its clean word
+constexpr int MV_MAX = 32;
+struct MvView {
+    CamK cam;
+    float4* g8;
+    float* d_c11;
+    float* partials;
+    unsigned long long* clean_word;
+    unsigned long long clean_stamp;
+};
+struct MvArgs {
+    int nv;
+    MvView v[MV_MAX];
+};
+int launch_views_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n,
+                             const MvArgs& a, float* d_means3, float* d_scales3, float* d_quats4, float* d_rgbo4,
+                             float* d_views16, bool accumulate, bool clear_rows, bool add_view, cudaStream_t s);
 
 // sort.cu
 int sort_sm_count();

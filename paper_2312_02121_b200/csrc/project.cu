@@ -187,6 +187,134 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
     }
 }
 
+// View-independent part of sg/proj_backward.py:139-175 for one Gaussian:
+// the unit quaternion (and 1/|q|), R, M = R diag(s) and Sigma = M M^T.
+struct BwdPrep {
+    float qw, qx, qy, qz, inv;
+    float R[9], M[9], Sg[9];
+};
+__device__ __forceinline__ BwdPrep proj_bwd_prep(float4 q, const float s[3]) {
+    BwdPrep P;
+    const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+    P.inv = 1.f / qn;
+    P.qw = q.x * P.inv, P.qx = q.y * P.inv, P.qy = q.z * P.inv, P.qz = q.w * P.inv;
+    quat_rot(P.qw, P.qx, P.qy, P.qz, P.R);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) P.M[3 * a + b] = P.R[3 * a + b] * s[b];
+    // Sigma = M M^T
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            P.Sg[3 * a + b] = P.M[3 * a] * P.M[3 * b] + P.M[3 * a + 1] * P.M[3 * b + 1] + P.M[3 * a + 2] * P.M[3 * b + 2];
+    return P;
+}
+
+// Per-view body of sg/proj_backward.py:200-222 for one visible Gaussian and
+// the view's screen-space gradients (gg = d_mean2d x, y, d_cov00, d_cov01;
+// g11 = d_cov11): d_mean, d_scale, d_quat and the 12 d_view terms.
+__device__ __forceinline__ void proj_bwd_view(const CamK& cam, float mx, float my, float mz, const float s[3],
+                                              const BwdPrep& P, float4 gg, float g11, float& dmx, float& dmy,
+                                              float& dmz, float& dsx, float& dsy, float& dsz, float4& dq,
+                                              float dv[12]) {
+    const float qw = P.qw, qx = P.qx, qy = P.qy, qz = P.qz, inv = P.inv;
+    const float* R = P.R;
+    const float* M = P.M;
+    const float* Sg = P.Sg;
+    const float* Rc = cam.R;
+    const float tx = Rc[0] * mx + Rc[1] * my + Rc[2] * mz + cam.t[0];
+    const float ty = Rc[3] * mx + Rc[4] * my + Rc[5] * mz + cam.t[1];
+    const float tz = Rc[6] * mx + Rc[7] * my + Rc[8] * mz + cam.t[2];
+    const float iz = 1.f / tz, iz2 = iz * iz;
+    const float j00 = cam.fx * iz, j02 = -cam.fx * tx * iz2;
+    const float j11 = cam.fy * iz, j12 = -cam.fy * ty * iz2;
+    float T0[3], T1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        T0[k] = j00 * Rc[k] + j02 * Rc[6 + k];
+        T1[k] = j11 * Rc[3 + k] + j12 * Rc[6 + k];
+    }
+    const float gx = gg.x, gy = gg.y, g00 = gg.z, g01 = gg.w;
+    // mean2d_backward (:53-77) == J^T d_mean2d with dt_w = 0
+    float dt0 = cam.fx * gx * iz;
+    float dt1 = cam.fy * gy * iz;
+    float dt2 = -(cam.fx * gx * tx + cam.fy * gy * ty) * iz2;
+    // cov2d_backward (:88-121)
+    float GT0[3], GT1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        GT0[k] = g00 * T0[k] + g01 * T1[k];
+        GT1[k] = g01 * T0[k] + g11 * T1[k];
+    }
+    float dS[9];  // T^T G T
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) dS[3 * a + b] = T0[a] * GT0[b] + T1[a] * GT1[b];
+    // _cov_transform_grad (:80-85): G T Sigma^T + G^T T Sigma = 2 (G T) Sigma
+    float dT0[3], dT1[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        dT0[b] = 2.f * (GT0[0] * Sg[b] + GT0[1] * Sg[3 + b] + GT0[2] * Sg[6 + b]);
+        dT1[b] = 2.f * (GT1[0] * Sg[b] + GT1[1] * Sg[3 + b] + GT1[2] * Sg[6 + b]);
+    }
+    // dJ = dT R_cw^T (only the structurally non-zero entries of J matter)
+    const float dJ00 = dT0[0] * Rc[0] + dT0[1] * Rc[1] + dT0[2] * Rc[2];
+    const float dJ02 = dT0[0] * Rc[6] + dT0[1] * Rc[7] + dT0[2] * Rc[8];
+    const float dJ11 = dT1[0] * Rc[3] + dT1[1] * Rc[4] + dT1[2] * Rc[5];
+    const float dJ12 = dT1[0] * Rc[6] + dT1[1] * Rc[7] + dT1[2] * Rc[8];
+    const float iz3 = iz2 * iz;
+    dt0 += -cam.fx * iz2 * dJ02;
+    dt1 += -cam.fy * iz2 * dJ12;
+    dt2 += -cam.fx * iz2 * dJ00 + 2.f * cam.fx * tx * iz3 * dJ02 - cam.fy * iz2 * dJ11 +
+           2.f * cam.fy * ty * iz3 * dJ12;
+    // world_backward (:124-136)
+    dmx = Rc[0] * dt0 + Rc[3] * dt1 + Rc[6] * dt2;
+    dmy = Rc[1] * dt0 + Rc[4] * dt1 + Rc[7] * dt2;
+    dmz = Rc[2] * dt0 + Rc[5] * dt1 + Rc[8] * dt2;
+    const float dtv[3] = {dt0, dt1, dt2};
+    const float hm[4] = {mx, my, mz, 1.f};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dv[4 * a + b] = dtv[a] * hm[b];
+    // view rotation path (:218-222): d_view[:3,:3] += J^T dT
+    const float J0[3] = {j00, 0.f, j02}, J1[3] = {0.f, j11, j12};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) dv[4 * a + b] += J0[a] * dT0[b] + J1[a] * dT1[b];
+    // covariance3d_backward (:151-175): dM = (dS + dS^T) M = 2 dS M
+    float dM[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            dM[3 * a + b] = 2.f * (dS[3 * a] * M[b] + dS[3 * a + 1] * M[3 + b] + dS[3 * a + 2] * M[6 + b]);
+    float dR[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) dR[3 * a + b] = dM[3 * a + b] * s[b];
+    dsx = R[0] * dM[0] + R[3] * dM[3] + R[6] * dM[6];
+    dsy = R[1] * dM[1] + R[4] * dM[4] + R[7] * dM[7];
+    dsz = R[2] * dM[2] + R[5] * dM[5] + R[8] * dM[8];
+    // <dR, dR/dq_k> with the Jacobians of :139-148
+    const float gw = 2.f * (-qz * dR[1] + qy * dR[2] + qz * dR[3] - qx * dR[5] - qy * dR[6] + qx * dR[7]);
+    const float gxq = 2.f * (qy * dR[1] + qz * dR[2] + qy * dR[3] - 2.f * qx * dR[4] - qw * dR[5] +
+                             qz * dR[6] + qw * dR[7] - 2.f * qx * dR[8]);
+    const float gyq = 2.f * (-2.f * qy * dR[0] + qx * dR[1] + qw * dR[2] + qx * dR[3] + qz * dR[5] -
+                             qw * dR[6] + qz * dR[7] - 2.f * qy * dR[8]);
+    const float gzq = 2.f * (-2.f * qz * dR[0] - qw * dR[1] + qx * dR[2] + qw * dR[3] - 2.f * qz * dR[4] +
+                             qy * dR[5] + qx * dR[6] + qy * dR[7]);
+    // normalisation chain: (dq_hat - q_hat (q_hat . dq_hat)) / |q|
+    const float dot = qw * gw + qx * gxq + qy * gyq + qz * gzq;
+    dq = make_float4((gw - qw * dot) * inv, (gxq - qx * dot) * inv, (gyq - qy * dot) * inv,
+                     (gzq - qz * dot) * inv);
+}
+
 constexpr int PBWD_THREADS = 256;
 
 // Per-Gaussian loop body of sg/proj_backward.py:200-222.
@@ -270,112 +398,8 @@ __global__ void __launch_bounds__(PBWD_THREADS, PBWD_MINB) project_bwd_kernel(
         float dmx = 0.f, dmy = 0.f, dmz = 0.f, dsx = 0.f, dsy = 0.f, dsz = 0.f;
         float4 dq = make_float4(0.f, 0.f, 0.f, 0.f);
         if (vis) {
-            const float* Rc = cam.R;
-            const float tx = Rc[0] * mx + Rc[1] * my + Rc[2] * mz + cam.t[0];
-            const float ty = Rc[3] * mx + Rc[4] * my + Rc[5] * mz + cam.t[1];
-            const float tz = Rc[6] * mx + Rc[7] * my + Rc[8] * mz + cam.t[2];
-            const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
-            const float inv = 1.f / qn;
-            const float qw = q.x * inv, qx = q.y * inv, qy = q.z * inv, qz = q.w * inv;
-            float R[9];
-            quat_rot(qw, qx, qy, qz, R);
-            float M[9];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) M[3 * a + b] = R[3 * a + b] * s[b];
-            float Sg[9];  // Sigma = M M^T
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-                    Sg[3 * a + b] = M[3 * a] * M[3 * b] + M[3 * a + 1] * M[3 * b + 1] + M[3 * a + 2] * M[3 * b + 2];
-            const float iz = 1.f / tz, iz2 = iz * iz;
-            const float j00 = cam.fx * iz, j02 = -cam.fx * tx * iz2;
-            const float j11 = cam.fy * iz, j12 = -cam.fy * ty * iz2;
-            float T0[3], T1[3];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                T0[k] = j00 * Rc[k] + j02 * Rc[6 + k];
-                T1[k] = j11 * Rc[3 + k] + j12 * Rc[6 + k];
-            }
-            const float gx = gg.x, gy = gg.y, g00 = gg.z, g01 = gg.w;
-            // mean2d_backward (:53-77) == J^T d_mean2d with dt_w = 0
-            float dt0 = cam.fx * gx * iz;
-            float dt1 = cam.fy * gy * iz;
-            float dt2 = -(cam.fx * gx * tx + cam.fy * gy * ty) * iz2;
-            // cov2d_backward (:88-121)
-            float GT0[3], GT1[3];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                GT0[k] = g00 * T0[k] + g01 * T1[k];
-                GT1[k] = g01 * T0[k] + g11 * T1[k];
-            }
-            float dS[9];  // T^T G T
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) dS[3 * a + b] = T0[a] * GT0[b] + T1[a] * GT1[b];
-            // _cov_transform_grad (:80-85): G T Sigma^T + G^T T Sigma = 2 (G T) Sigma
-            float dT0[3], dT1[3];
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-                dT0[b] = 2.f * (GT0[0] * Sg[b] + GT0[1] * Sg[3 + b] + GT0[2] * Sg[6 + b]);
-                dT1[b] = 2.f * (GT1[0] * Sg[b] + GT1[1] * Sg[3 + b] + GT1[2] * Sg[6 + b]);
-            }
-            // dJ = dT R_cw^T (only the structurally non-zero entries of J matter)
-            const float dJ00 = dT0[0] * Rc[0] + dT0[1] * Rc[1] + dT0[2] * Rc[2];
-            const float dJ02 = dT0[0] * Rc[6] + dT0[1] * Rc[7] + dT0[2] * Rc[8];
-            const float dJ11 = dT1[0] * Rc[3] + dT1[1] * Rc[4] + dT1[2] * Rc[5];
-            const float dJ12 = dT1[0] * Rc[6] + dT1[1] * Rc[7] + dT1[2] * Rc[8];
-            const float iz3 = iz2 * iz;
-            dt0 += -cam.fx * iz2 * dJ02;
-            dt1 += -cam.fy * iz2 * dJ12;
-            dt2 += -cam.fx * iz2 * dJ00 + 2.f * cam.fx * tx * iz3 * dJ02 - cam.fy * iz2 * dJ11 +
-                   2.f * cam.fy * ty * iz3 * dJ12;
-            // world_backward (:124-136)
-            dmx = Rc[0] * dt0 + Rc[3] * dt1 + Rc[6] * dt2;
-            dmy = Rc[1] * dt0 + Rc[4] * dt1 + Rc[7] * dt2;
-            dmz = Rc[2] * dt0 + Rc[5] * dt1 + Rc[8] * dt2;
-            const float dtv[3] = {dt0, dt1, dt2};
-            const float hm[4] = {mx, my, mz, 1.f};
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) dv[4 * a + b] = dtv[a] * hm[b];
-            // view rotation path (:218-222): d_view[:3,:3] += J^T dT
-            const float J0[3] = {j00, 0.f, j02}, J1[3] = {0.f, j11, j12};
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) dv[4 * a + b] += J0[a] * dT0[b] + J1[a] * dT1[b];
-            // covariance3d_backward (:151-175): dM = (dS + dS^T) M = 2 dS M
-            float dM[9];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-                    dM[3 * a + b] = 2.f * (dS[3 * a] * M[b] + dS[3 * a + 1] * M[3 + b] + dS[3 * a + 2] * M[6 + b]);
-            float dR[9];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) dR[3 * a + b] = dM[3 * a + b] * s[b];
-            dsx = R[0] * dM[0] + R[3] * dM[3] + R[6] * dM[6];
-            dsy = R[1] * dM[1] + R[4] * dM[4] + R[7] * dM[7];
-            dsz = R[2] * dM[2] + R[5] * dM[5] + R[8] * dM[8];
-            // <dR, dR/dq_k> with the Jacobians of :139-148
-            const float gw = 2.f * (-qz * dR[1] + qy * dR[2] + qz * dR[3] - qx * dR[5] - qy * dR[6] + qx * dR[7]);
-            const float gxq = 2.f * (qy * dR[1] + qz * dR[2] + qy * dR[3] - 2.f * qx * dR[4] - qw * dR[5] +
-                                     qz * dR[6] + qw * dR[7] - 2.f * qx * dR[8]);
-            const float gyq = 2.f * (-2.f * qy * dR[0] + qx * dR[1] + qw * dR[2] + qx * dR[3] + qz * dR[5] -
-                                     qw * dR[6] + qz * dR[7] - 2.f * qy * dR[8]);
-            const float gzq = 2.f * (-2.f * qz * dR[0] - qw * dR[1] + qx * dR[2] + qw * dR[3] - 2.f * qz * dR[4] +
-                                     qy * dR[5] + qx * dR[6] + qy * dR[7]);
-            // normalisation chain: (dq_hat - q_hat (q_hat . dq_hat)) / |q|
-            const float dot = qw * gw + qx * gxq + qy * gyq + qz * gzq;
-            dq = make_float4((gw - qw * dot) * inv, (gxq - qx * dot) * inv, (gyq - qy * dot) * inv,
-                             (gzq - qz * dot) * inv);
+            const BwdPrep P = proj_bwd_prep(q, s);
+            proj_bwd_view(cam, mx, my, mz, s, P, gg, g11, dmx, dmy, dmz, dsx, dsy, dsz, dq, dv);
         }
         if (accumulate) {  // sum over views into the caller's gradient (culled: nothing to add)
             if (vis) {
@@ -542,6 +566,161 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
                  (const float4*)quats4, opac, (int)n, k, (float4*)xydr4, (float4*)conic4, tiles, cov3, status, dkeys,
                  dhist, zj, (uint32_t*)nullptr, (uint32_t*)nullptr, 0u);
     return check_launch("project_fwd_kernel<dkey>");
+}
+
+// ---------------------------------------------------------------- all views at once
+// The projection backward of a multi-view step (sg/proj_backward.py:178-223
+// for every view, summed): one pass over the Gaussians, each thread loading
+// its Gaussian's parameters once, deriving the view-independent part (unit
+// quaternion, R, M, Sigma) once, then for every view reading the view's
+// screen-space gradient rows (its own workspace), adding the view's
+// contribution to registers and clearing the rows it read; the parameter
+// gradients are written once.  Against one projection backward per view,
+// which re-reads the parameters and read-modify-writes the running sums for
+// every view (~224 B per visible Gaussian and view), this moves ~76 B per
+// visible Gaussian and view.  A Gaussian is visible in a view iff its rows are
+// non-zero: a culled one's rows are never written, and a visible one with
+// zero rows contributes exactly zero (the backward is linear in them), so the
+// visibility word is not read.  d_view per view: the 12 terms are warp-
+// reduced per view (transposed shuffle tree, fixed order), summed per warp in
+// shared memory, per block into the view's own partials, then by
+// views_reduce_kernel in a fixed order -- deterministic.
+__global__ void __launch_bounds__(PBWD_THREADS, 2) views_project_bwd_kernel(
+    const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats, int n,
+    const MvArgs args, float* __restrict__ d_means, float* __restrict__ d_scales, float4* __restrict__ d_quats,
+    float4* __restrict__ d_rgbo, bool accumulate, bool clear_rows) {
+    griddep_wait();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ float s_dv[PBWD_THREADS / 32][MV_MAX][12];  // per-warp d_view sums (each warp owns its row)
+    for (int k = lane; k < MV_MAX * 12; k += 32) (&s_dv[warp][0][0])[k] = 0.f;
+    __syncwarp();
+    const int nv = args.nv;
+    const int n_round = (n + 31) & ~31;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += gridDim.x * blockDim.x) {
+        const bool in = i < n;
+        float mx = 0.f, my = 0.f, mz = 0.f, s[3] = {1.f, 1.f, 1.f};
+        float4 q = make_float4(1.f, 0.f, 0.f, 0.f);
+        if (in) {
+            mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
+            s[0] = scales[3 * i], s[1] = scales[3 * i + 1], s[2] = scales[3 * i + 2];
+            q = quats[i];
+        }
+        BwdPrep P;
+        bool prepped = false;
+        float am[3] = {0.f, 0.f, 0.f}, as[3] = {0.f, 0.f, 0.f};
+        float4 aq = make_float4(0.f, 0.f, 0.f, 0.f), argbo = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int v = 0; v < nv; ++v) {
+            const MvView& V = args.v[v];
+            float4 rg = make_float4(0.f, 0.f, 0.f, 0.f), gg = rg;
+            float g11 = 0.f;
+            if (in) {
+                rg = V.g8[2 * (size_t)i];
+                gg = V.g8[2 * (size_t)i + 1];
+                g11 = V.d_c11[i];
+            }
+            const bool vis = gg.x != 0.f || gg.y != 0.f || gg.z != 0.f || gg.w != 0.f || g11 != 0.f ||
+                             rg.x != 0.f || rg.y != 0.f || rg.z != 0.f || rg.w != 0.f;
+            float dv[12];
+#pragma unroll
+            for (int k = 0; k < 12; ++k) dv[k] = 0.f;
+            if (vis) {
+                if (!prepped) {
+                    P = proj_bwd_prep(q, s);
+                    prepped = true;
+                }
+                float dmx, dmy, dmz, dsx, dsy, dsz;
+                float4 dq;
+                proj_bwd_view(V.cam, mx, my, mz, s, P, gg, g11, dmx, dmy, dmz, dsx, dsy, dsz, dq, dv);
+                am[0] += dmx, am[1] += dmy, am[2] += dmz;
+                as[0] += dsx, as[1] += dsy, as[2] += dsz;
+                aq.x += dq.x, aq.y += dq.y, aq.z += dq.z, aq.w += dq.w;
+                argbo.x += rg.x, argbo.y += rg.y, argbo.z += rg.z, argbo.w += rg.w;
+                if (clear_rows) {  // the accumulators stay zero for the view's next frame
+                    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                    __stcs(V.g8 + 2 * (size_t)i, z);
+                    __stcs(V.g8 + 2 * (size_t)i + 1, z);
+                    __stcs(V.d_c11 + i, 0.f);
+                }
+            }
+            if (__any_sync(0xffffffffu, vis)) {
+                // transposed warp reduction of the 12 terms (padded to 16)
+                float v16[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) v16[k] = k < 12 ? dv[k] : 0.f;
+#pragma unroll
+                for (int h = 8, m = 16; h >= 1; h >>= 1, m >>= 1) {
+                    const bool up = lane & m;
+#pragma unroll
+                    for (int j = 0; j < h; ++j) {
+                        const float send = up ? v16[j] : v16[j + h];
+                        const float keep = up ? v16[j + h] : v16[j];
+                        v16[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                    }
+                }
+                const float tot = v16[0] + __shfl_xor_sync(0xffffffffu, v16[0], 1);
+                const int k = lane >> 1;
+                if ((lane & 1) == 0 && k < 12) s_dv[warp][v][k] += tot;
+            }
+        }
+        if (in) {
+            if (accumulate) {
+                d_means[3 * i] += am[0], d_means[3 * i + 1] += am[1], d_means[3 * i + 2] += am[2];
+                d_scales[3 * i] += as[0], d_scales[3 * i + 1] += as[1], d_scales[3 * i + 2] += as[2];
+                const float4 o = d_quats[i];
+                d_quats[i] = make_float4(o.x + aq.x, o.y + aq.y, o.z + aq.z, o.w + aq.w);
+                const float4 r = d_rgbo[i];
+                d_rgbo[i] = make_float4(r.x + argbo.x, r.y + argbo.y, r.z + argbo.z, r.w + argbo.w);
+            } else {
+                d_means[3 * i] = am[0], d_means[3 * i + 1] = am[1], d_means[3 * i + 2] = am[2];
+                d_scales[3 * i] = as[0], d_scales[3 * i + 1] = as[1], d_scales[3 * i + 2] = as[2];
+                d_quats[i] = aq;
+                d_rgbo[i] = argbo;
+            }
+        }
+    }
+    __syncthreads();
+    // block partials: per view, the warps' sums in warp order
+    for (int k = threadIdx.x; k < nv * 12; k += blockDim.x) {
+        const int v = k / 12, c = k - 12 * v;
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < PBWD_THREADS / 32; ++w) acc += s_dv[w][v][c];
+        args.v[v].partials[blockIdx.x * 12 + c] = acc;
+    }
+}
+
+// Per view (one CTA each): the fixed-order sum of its block partials ->
+// d_views16[v] (bottom row 0), and its workspace stamped clean (or not).
+__global__ void __launch_bounds__(384) views_reduce_kernel(const MvArgs args, int nblocks, float* __restrict__ d_views16,
+                                                           bool add) {
+    griddep_wait();
+    const int v = blockIdx.x;
+    const MvView& V = args.v[v];
+    if (threadIdx.x == 0 && V.clean_word) *V.clean_word = V.clean_stamp;
+    const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float acc = 0.f;
+    for (int b = lane; b < nblocks; b += 32) acc += V.partials[b * 12 + k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    float* dv = d_views16 + 16 * v;
+    if (lane == 0) dv[k] = add ? dv[k] + acc : acc;
+    if (threadIdx.x < 4) dv[12 + threadIdx.x] = 0.f;
+}
+
+int launch_views_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n,
+                             const MvArgs& a, float* d_means3, float* d_scales3, float* d_quats4, float* d_rgbo4,
+                             float* d_views16, bool accumulate, bool clear_rows, bool add_view, cudaStream_t s) {
+    if (a.nv <= 0) return 0;
+    int blocks = (int)((n + PBWD_THREADS - 1) / PBWD_THREADS);
+    const int resident = sort_sm_count() * 2;
+    if (blocks > resident) blocks = resident;
+    if (blocks < 1) blocks = 1;
+    launch_k(views_project_bwd_kernel, dim3(blocks), dim3(PBWD_THREADS), 0, s, means3, scales3,
+             (const float4*)quats4, (int)n, a, d_means3, d_scales3, (float4*)d_quats4, (float4*)d_rgbo4, accumulate,
+             clear_rows);
+    if (check_launch("views_project_bwd_kernel")) return -1;
+    launch_k(views_reduce_kernel, dim3(a.nv), dim3(384), 0, s, a, blocks, d_views16, add_view);
+    return check_launch("views_reduce_kernel");
 }
 
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,

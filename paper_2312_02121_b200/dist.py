@@ -157,6 +157,22 @@ class GradReducer:
                 works.append(dist.all_reduce(out[key][a:b], op=dist.ReduceOp.SUM, group=self.group, async_op=True))
         return works
 
+    def views(self, frames, params, out: dict, d_views, accumulate: bool = False) -> list:
+        """The batched projection backward of all of this rank's views (each
+        after ops.frame_backward(project=False)) bucket by bucket, each
+        bucket's 4 gradient slices all-reduced asynchronously.  Returns the
+        works."""
+        import torch.distributed as dist
+        from . import ops
+        m, s, q = params[0], params[1], params[2]
+        works = []
+        for a, b in self.bounds:
+            ops.frame_views_project_backward(frames, m, s, q, out, d_views, a, b, accumulate=accumulate,
+                                             add_view=a > 0)
+            for key in ("d_mean", "d_scale", "d_quat", "d_rgbo"):
+                works.append(dist.all_reduce(out[key][a:b], op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+        return works
+
     @staticmethod
     def wait(works) -> None:
         for w in works:

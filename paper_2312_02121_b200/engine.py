@@ -96,10 +96,15 @@ def unpack(flat: torch.Tensor, n: int) -> dict:
 
 class RenderStep:
     def __init__(self, n: int, cams, background=(0.0, 0.0, 0.0), early_termination=True, device=None,
-                 headroom: float = 1.05, buffers: int = 2, view_streams: int = 3, reducer=None):
+                 headroom: float = 1.05, buffers: int = 2, view_streams: int = 3, reducer=None,
+                 batched_projection: bool = True):
         """reducer: a dist.GradReducer -- the step's gradients are summed over
         the ranks of its process group, the all-reduce overlapped with the
-        last view's projection backward (view-sharded data parallelism)."""
+        (last view's, or the batched) projection backward (view-sharded data
+        parallelism).  batched_projection: with several views, every view
+        runs its raster backward only and one gs_frame_views_project_backward
+        pass does all views' projection backward (parameters read once, sums
+        written once) instead of one read-modify-write pass per view."""
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         self.reducer = reducer
         self.n = int(n)
@@ -107,6 +112,7 @@ class RenderStep:
         self.bg = tuple(float(b) for b in background)
         self.et = bool(early_termination)
         self.headroom = headroom
+        self.batched = bool(batched_projection) and len(self.cams) > 1
         self.nbuf = buffers
         z = lambda *shape: torch.zeros(shape, device=self.dev, dtype=torch.float32)
         self.sets = []
@@ -161,7 +167,9 @@ class RenderStep:
                 fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et, capacity=self.caps[vi],
                                        check_meta=False, ws=self.wss[vi], binning=self.binnings[vi])
                 last = vi == len(self.cams) - 1
-                if last and self.reducer is not None:  # its projection backward runs bucketed in replay()
+                if self.batched or (last and self.reducer is not None):
+                    # the projection backward runs afterwards (batched over the views, and/or
+                    # bucketed under the all-reduce in replay())
                     ops.frame_backward(fr, m, sc, q, c, d, project=False)
                 else:
                     g = ops.frame_backward(fr, m, sc, q, c, d, out=out, accumulate=vi > 0,
@@ -174,6 +182,8 @@ class RenderStep:
                     bwd_done.record(st)
         for a in sts[1:]:
             main.wait_stream(a)
+        if self.batched and self.reducer is None:
+            ops.frame_views_project_backward(s["frames"], m, sc, q, out, s["d_view"])
 
     def _capture(self):
         side = torch.cuda.Stream(self.dev)
@@ -220,8 +230,11 @@ class RenderStep:
             # bucket's all-reduce overlapping the next buckets (dist.py)
             s = self.sets[k]
             nv = len(self.cams)
-            works = self.reducer.last_view(s["frames"][nv - 1], s["params"], unpack(s["grads"], self.n),
-                                           s["d_view"][nv - 1], accumulate=nv > 1)
+            if self.batched:
+                works = self.reducer.views(s["frames"], s["params"], unpack(s["grads"], self.n), s["d_view"])
+            else:
+                works = self.reducer.last_view(s["frames"][nv - 1], s["params"], unpack(s["grads"], self.n),
+                                               s["d_view"][nv - 1], accumulate=nv > 1)
             self.reducer.wait(works)
 
     def d_view(self, k: int) -> torch.Tensor:

@@ -648,6 +648,38 @@ def frame_project_backward(fr: Frame, means, scales, quats, out: dict, d_view: t
                                       flags, _stream()), "gs_frame_project_backward")
 
 
+def frame_views_project_backward(frames, means, scales, quats, out: dict, d_views: torch.Tensor, begin=0, end=None,
+                                 *, accumulate=False, add_view=False, keep_screen=False):
+    """gs_frame_views_project_backward: the projection backward of every
+    frame in `frames` (one per view, each after frame_backward(project=False)
+    on its own workspace) in one pass over Gaussians [begin, end):
+    sg/proj_backward.py:178-223 per view, summed over the views, into `out`
+    (d_mean, d_scale, d_quat, d_rgbo full (n, .) tensors; rows written or,
+    with accumulate, added to) and d_views (views, 4, 4; per view,
+    overwritten or, with add_view, added to)."""
+    L = _lib.load()
+    nv = len(frames)
+    if nv == 0:
+        return
+    n = frames[0].n
+    end = n if end is None else int(end)
+    if any(f.n != n for f in frames):
+        raise ValueError("frame_views_project_backward: frames of different scenes")
+    if tuple(d_views.shape) != (nv, 4, 4) or not d_views.is_contiguous():
+        raise ValueError("frame_views_project_backward: d_views must be contiguous (views, 4, 4)")
+    cams = (_lib.GsCamera * nv)(*[f.cam.c() for f in frames])
+    caps = (C.c_int64 * nv)(*[f.capacity for f in frames])
+    wss = (C.c_void_p * nv)(*[f.ws.data_ptr() for f in frames])
+    wsb = (C.c_size_t * nv)(*[f.ws.numel() for f in frames])
+    flags = (1 if accumulate else 0) | (2 if keep_screen else 0) | (16 if add_view else 0)
+    vp = lambda a: C.cast(a, C.c_void_p)
+    check(L.gs_frame_views_project_backward(_ptr(means), _ptr(scales), _ptr(quats), n, nv, cams, vp(caps), vp(wss),
+                                            vp(wsb),
+                                            int(begin), end, _ptr(out["d_mean"]), _ptr(out["d_scale"]),
+                                            _ptr(out["d_quat"]), _ptr(out["d_rgbo"]), _ptr(d_views), flags,
+                                            _stream()), "gs_frame_views_project_backward")
+
+
 # ------------------------------------------------------ staged (per-stage) path
 # The same frame through the individual stage entry points and the 64-bit
 # (tile << 32 | depth) key sort; used by the parity harness (it exposes every

@@ -122,6 +122,95 @@ def test_multi_view_step_sums_views(cuda):
     assert m.shape == (3, 4) and bool((m[:, 0] == -1).all()) and bool((m[:, 1] > 0).all())
 
 
+def _views(ops, cam0, angles):
+    cams = []
+    for ang in angles:
+        c, s_ = np.cos(ang), np.sin(ang)
+        view = np.array(cam0.view, np.float64)
+        view[:3, :3] = np.array([[c, 0.0, s_], [0.0, 1.0, 0.0], [-s_, 0.0, c]]) @ view[:3, :3]
+        cams.append(ops.CameraParams(view.tolist(), cam0.fx, cam0.fy, cam0.cx, cam0.cy, cam0.width, cam0.height,
+                                     cam0.near, cam0.far))
+    return cams
+
+
+def test_views_project_backward_equals_per_view(cuda):
+    """gs_frame_views_project_backward (all views' projection backward in one
+    pass over the Gaussians) equals the per-view projection backward summed
+    over the views, per gradient class and per view's d_view; the screen-
+    space rows are cleared and the workspaces stamped clean (the next frames
+    give the same result again)."""
+    from paper_2312_02121_b200 import engine as E, ops
+    g = load_golden("config0")
+    params = [torch.as_tensor(np.asarray(a, np.float32), device=cuda) for a in g["inputs"]]
+    m, s, q, o, c = params
+    n = len(m)
+    cams = _views(ops, ops.CameraParams.of(g["camera"]), (0.0, 0.1, -0.15, 0.3))
+    rng = np.random.default_rng(5)
+    d_imgs = [torch.as_tensor(rng.normal(size=(cm.height, cm.width, 3)).astype(np.float32), device=cuda)
+              for cm in cams]
+    ref = {k: torch.zeros((n, w), device=cuda) for k, w in (("d_mean", 3), ("d_scale", 3), ("d_quat", 4),
+                                                             ("d_rgbo", 4))}
+    ref_views = []
+    for cm, d in zip(cams, d_imgs):
+        fr = ops.frame_forward(*params, cm, (0.0, 0.0, 0.0), True)
+        gv = ops.frame_backward(fr, m, s, q, c, d)
+        for k in ref:
+            ref[k] += gv[k]
+        ref_views.append(gv["d_view"])
+    for rep in range(2):
+        frames = []
+        for cm, d in zip(cams, d_imgs):
+            fr = ops.frame_forward(*params, cm, (0.0, 0.0, 0.0), True)
+            ops.frame_backward(fr, m, s, q, c, d, project=False)
+            frames.append(fr)
+        out = {k: torch.full_like(v, 7.0) for k, v in ref.items()}
+        d_views = torch.full((len(cams), 4, 4), 3.0, device=cuda)
+        ops.frame_views_project_backward(frames, m, s, q, out, d_views)
+        torch.cuda.synchronize()
+        for k in ref:
+            a, b = out[k].cpu().double().numpy(), ref[k].cpu().double().numpy()
+            assert np.abs(a - b).max() <= 1e-4 * (np.abs(b).max() + 1e-30), (rep, k)
+        for v, dv in enumerate(ref_views):
+            a, b = d_views[v].cpu().double().numpy(), dv.cpu().double().numpy()
+            assert np.abs(a - b).max() <= 1e-4 * (np.abs(b).max() + 1e-30), (rep, v)
+        for fr in frames:
+            tv = fr.tensors()
+            assert not bool(tv["d_geo"].any()) and not bool(tv["d_c11"].any())  # rows cleared
+    # accumulate / add_view add onto the outputs
+    frames = []
+    for cm, d in zip(cams, d_imgs):
+        fr = ops.frame_forward(*params, cm, (0.0, 0.0, 0.0), True)
+        ops.frame_backward(fr, m, s, q, c, d, project=False)
+        frames.append(fr)
+    out = {k: v.clone() for k, v in ref.items()}
+    d_views = torch.stack(ref_views).clone()
+    ops.frame_views_project_backward(frames, m, s, q, out, d_views, accumulate=True, add_view=True)
+    for k in ref:
+        a, b = out[k].cpu().double().numpy(), 2 * ref[k].cpu().double().numpy()
+        assert np.abs(a - b).max() <= 1e-4 * (np.abs(b).max() + 1e-30), k
+
+
+def test_batched_and_per_view_engine_agree(cuda):
+    """RenderStep with the batched projection backward (default for several
+    views) and with one projection backward per view give the same step."""
+    from paper_2312_02121_b200 import engine as E, ops
+    g = load_golden("config0")
+    params = [torch.as_tensor(np.asarray(a, np.float32), device=cuda) for a in g["inputs"]]
+    cams = _views(ops, ops.CameraParams.of(g["camera"]), (0.0, 0.2, -0.1))
+    rng = np.random.default_rng(2)
+    d_imgs = [torch.as_tensor(rng.normal(size=(cm.height, cm.width, 3)).astype(np.float32), device=cuda)
+              for cm in cams]
+    a = E.RenderStep(len(params[0]), cams, device=cuda)
+    b = E.RenderStep(len(params[0]), cams, device=cuda, batched_projection=False)
+    assert a.batched and not b.batched
+    a.prime(params, d_imgs)
+    b.prime(params, d_imgs)
+    ga, gb = a.step(params, d_imgs).clone(), b.step(params, d_imgs).clone()
+    _close(ga, gb)
+    dva, dvb = a.d_view(0).cpu().double().numpy(), b.d_view(0).cpu().double().numpy()
+    assert np.abs(dva - dvb).max() <= 1e-4 * np.abs(dvb).max()
+
+
 def test_pipeline_from_write_combined_staging(cuda):
     """Inputs staged in write-combined pinned memory (engine.host_staging)
     give the same gradients as the per-call path."""
