@@ -609,14 +609,23 @@ __global__ void __launch_bounds__(PBWD_THREADS, 2) views_project_bwd_kernel(
         bool prepped = false;
         float am[3] = {0.f, 0.f, 0.f}, as[3] = {0.f, 0.f, 0.f};
         float4 aq = make_float4(0.f, 0.f, 0.f, 0.f), argbo = make_float4(0.f, 0.f, 0.f, 0.f);
+        // the next view's rows are loaded while this view's are processed
+        float4 nrg = make_float4(0.f, 0.f, 0.f, 0.f), ngg = nrg;
+        float ng11 = 0.f;
+        if (in && nv > 0) {
+            nrg = args.v[0].g8[2 * (size_t)i];
+            ngg = args.v[0].g8[2 * (size_t)i + 1];
+            ng11 = args.v[0].d_c11[i];
+        }
         for (int v = 0; v < nv; ++v) {
             const MvView& V = args.v[v];
-            float4 rg = make_float4(0.f, 0.f, 0.f, 0.f), gg = rg;
-            float g11 = 0.f;
-            if (in) {
-                rg = V.g8[2 * (size_t)i];
-                gg = V.g8[2 * (size_t)i + 1];
-                g11 = V.d_c11[i];
+            const float4 rg = nrg, gg = ngg;
+            const float g11 = ng11;
+            if (in && v + 1 < nv) {
+                const MvView& N = args.v[v + 1];
+                nrg = N.g8[2 * (size_t)i];
+                ngg = N.g8[2 * (size_t)i + 1];
+                ng11 = N.d_c11[i];
             }
             const bool vis = gg.x != 0.f || gg.y != 0.f || gg.z != 0.f || gg.w != 0.f || g11 != 0.f ||
                              rg.x != 0.f || rg.y != 0.f || rg.z != 0.f || rg.w != 0.f;
