@@ -264,6 +264,9 @@ def run_ours(args):
     # backward over all views (gs_frame_views_project_backward); GS_BATCHED_PROJ=0: per view
     batched = len(cams) > 1 and os.environ.get("GS_BATCHED_PROJ", "1") != "0"
     ev_pb = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]  # recorded inside capture
+    # ... and every view's projection in one pass (when all views bin depth-first); GS_BATCHED_FWD=0: per view
+    batched_fwd = batched and os.environ.get("GS_BATCHED_FWD", "1") != "0" and ops.frames_projectable(n, cams)
+    ev_pf = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]
     d_views = torch.zeros((len(cams), 4, 4), device=dev, dtype=torch.float32)
 
     def step(staged=False):
@@ -281,6 +284,12 @@ def run_ours(args):
         two = ns > 1
         main = torch.cuda.current_stream()
         sts = [main] + aux[:ns - 1]
+        if batched_fwd:
+            if staged:
+                ev_pf[0].record()
+            ops.frames_project(m, s, q, o, cams, caps, wss)
+            if staged:
+                ev_pf[1].record()
         for a in sts[1:]:
             a.wait_stream(main)
         bwd_done = None
@@ -288,7 +297,8 @@ def run_ours(args):
             st = sts[vi % ns]
             with torch.cuda.stream(st):
                 fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, capacity=caps[vi], check_meta=False,
-                                       ws=wss[vi], events=ev_f[vi] if staged else None, binning=binnings[vi])
+                                       ws=wss[vi], events=ev_f[vi] if staged else None, binning=binnings[vi],
+                                       projected=batched_fwd)
                 # only the views' accumulation into grad_out is ordered: this view's raster
                 # backward overlaps the previous view's projection backward.  N > 1: the
                 # last view's projection backward runs after the graph, bucketed under the
@@ -393,7 +403,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         for vi in range(len(cams)):
             f, b = ev_f[vi], ev_b[vi]
-            stage_ms[0] += f[0].elapsed_time(f[1])
+            if not batched_fwd:
+                stage_ms[0] += f[0].elapsed_time(f[1])
             stage_ms[1] += f[1].elapsed_time(f[2])
             stage_ms[2] += f[2].elapsed_time(f[3])
             stage_ms[3] += f[3].elapsed_time(f[4])
@@ -403,6 +414,8 @@ def run_ours(args):
                 stage_ms[6] += b[1].elapsed_time(b[2])
         if batched and world == 1:
             stage_ms[6] += ev_pb[0].elapsed_time(ev_pb[1])
+        if batched_fwd:
+            stage_ms[0] += ev_pf[0].elapsed_time(ev_pf[1])
     # the capacity was sized from a checked run; confirm nothing overflowed
     for vi, fr in enumerate(frames_out):
         meta = fr.meta().cpu()
@@ -458,7 +471,9 @@ def run_ours(args):
         # 4 in, the conic's 4th float and the depth sort key out); the backward accumulators are
         # no longer zeroed here (the projection backward clears the rows it reads).  Direct
         # binning: + a slot atomic and the Gaussian id per intersection (8 B)
-        "project": ("hbm", 72.0 * n * nv + (8.0 * I if direct else 0.0)),
+        # batched over the views (one pass): the 44 B of parameters read once, per view the
+        # xydr / conic / tiles / depth key written (40 B)
+        "project": ("hbm", (44.0 * n + 40.0 * n * nv) if batched_fwd else 72.0 * n * nv + (8.0 * I if direct else 0.0)),
         # depth-first: 4 passes x (key+value) x (read+write); scatter / direct: no global depth sort
         "depth_sort": ("none", 0.0) if seg else ("hbm", 4 * 16.0 * n * nv),
         # depth-first: fused scan + emission, (order +) count + xydr gather per Gaussian, pairs out;

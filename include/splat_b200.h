@@ -239,6 +239,22 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
                      const float* background3 /*[host]*/, int early_termination, int64_t isect_capacity,
                      void* ws, size_t ws_bytes, float* out_image, float* out_final_T, int32_t* out_n_contrib,
                      unsigned long long* counts4, void* const* stage_events, gs_stream_t stream);
+/* Multi-view steps: the projection of every view (each on its own
+ * workspace, all using depth-first binning) in one pass that reads each
+ * Gaussian once (40 + 44/n_views instead of 84 bytes per Gaussian and view),
+ * then per view gs_frame_forward_projected = gs_frame_forward without its
+ * projection (same arguments; no counted pass).  cams / capacities /
+ * workspaces / ws_bytes: [host] n_views entries. */
+int gs_frames_project(const float* means3, const float* scales3, const float* quats4, const float* opacities,
+                      int64_t n, int32_t n_views, const gs_camera* cams /*[host]*/,
+                      const int64_t* capacities /*[host]*/, void* const* workspaces /*[host]*/,
+                      const size_t* ws_bytes /*[host]*/, gs_stream_t stream);
+int gs_frame_forward_projected(const float* means3, const float* scales3, const float* quats4,
+                               const float* opacities, const float* colors3, int64_t n,
+                               const gs_camera* cam /*[host]*/, const float* background3 /*[host]*/,
+                               int early_termination, int64_t isect_capacity, void* ws, size_t ws_bytes,
+                               float* out_image, float* out_final_T, int32_t* out_n_contrib,
+                               void* const* stage_events, gs_stream_t stream);
 /* stage_events (nullable; entries nullable): cudaEvent_t handles recorded
  * on `stream` at stage boundaries, for live per-stage timing.
  *   forward : [0] start [1] projected [2] depth-sorted [3] emitted [4] tile-sorted+ranges [5] rastered

@@ -22,7 +22,7 @@ EXPORTS = (
     "gs_raster_fwd", "gs_raster_bwd",
     "gs_project_bwd_workspace_bytes", "gs_project_bwd",
     "gs_frame_workspace_bytes", "gs_frame_workspace_init", "gs_frame_binning", "gs_frame_tile_emit", "gs_frame_view_of",
-    "gs_frame_forward", "gs_frame_backward", "gs_frame_project_backward", "gs_frame_views_project_backward",
+    "gs_frame_forward", "gs_frame_forward_projected", "gs_frames_project", "gs_frame_backward", "gs_frame_project_backward", "gs_frame_views_project_backward",
     "gs_activate", "gs_loss_l2", "gs_adam_step",
     "gs_conic_from_cov", "gs_eval_alpha", "gs_composite_pixels", "gs_composite_pixels_bwd",
     "gs_project64", "gs_bin64_workspace_bytes", "gs_bin64_count", "gs_bin64_sort", "gs_raster64_fwd",
@@ -102,6 +102,9 @@ def load():
         "gs_frame_backward": ([P, P, P, P, i64, cam, C.POINTER(C.c_float), i64, P, sz, P, P, P, P, P, P, P, P,
                                C.c_int, P, P, P], C.c_int),
         "gs_frame_project_backward": ([P, P, P, i64, cam, i64, P, sz, i64, i64, P, P, P, P, P, C.c_int, P], C.c_int),
+        "gs_frame_forward_projected": ([P, P, P, P, P, i64, cam, C.POINTER(C.c_float), C.c_int, i64, P, sz, P, P, P,
+                                        P, P], C.c_int),
+        "gs_frames_project": ([P, P, P, P, i64, i32, cam, P, P, P, P], C.c_int),
         "gs_frame_views_project_backward": ([P, P, P, i64, i32, cam, P, P, P, i64, i64, P, P, P, P, P, C.c_int, P],
                                             C.c_int),
     }

@@ -161,6 +161,32 @@ unsigned long long clean_sig(int64_t n, int64_t cap, int W, int H) {
     return h | 1ull;  // never 0 (0 = "not clean")
 }
 
+// Buffers the frame's projection clears for the later stages (no memset
+// nodes): the zeroed region (minus the tile passes' look-back status under the
+// tile-sorted emission), the tile ranges and -- only when the workspace is not
+// known clean (meta[4]) -- the backward's screen-space accumulators.
+ZeroJobs frame_zero_jobs(const Layout& L, void* ws, int n_tiles, bool etiles) {
+    ZeroJobs zj;
+    zj.p[0] = at<uint4>(ws, L.thist);
+    zj.n16[0] = ((etiles ? L.tstatus : L.zero_end) - L.thist) / 16;
+    zj.p[1] = at<uint4>(ws, L.ranges);
+    zj.n16[1] = (8 * (size_t)n_tiles + 15) / 16;
+    zj.p[2] = at<uint4>(ws, L.d_geo);
+    zj.n16[2] = (L.partials - L.d_geo) / 16;
+    zj.cond2 = at<unsigned long long>(ws, L.meta) + 4;
+    return zj;
+}
+
+bool uses_tile_emit(int64_t n, int n_tiles) {
+    return binning_for(n, n_tiles) == DEPTH_FIRST && tile_emit() && emit_tiles_fits(n_tiles);
+}
+
+int frame_forward_impl(const float* means3, const float* scales3, const float* quats4, const float* opacities,
+                       const float* colors3, int64_t n, const gs_camera* cam, const float* background3,
+                       int early_termination, int64_t isect_capacity, void* ws, size_t ws_bytes, float* out_image,
+                       float* out_final_T, int32_t* out_n_contrib, unsigned long long* counts4,
+                       void* const* stage_events, gs_stream_t stream, bool projected);
+
 }  // namespace
 
 }  // namespace gs
@@ -215,6 +241,72 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
                      int early_termination, int64_t isect_capacity, void* ws, size_t ws_bytes, float* out_image,
                      float* out_final_T, int32_t* out_n_contrib, unsigned long long* counts4, void* const* stage_events,
                      gs_stream_t stream) {
+    return frame_forward_impl(means3, scales3, quats4, opacities, colors3, n, cam, background3, early_termination,
+                              isect_capacity, ws, ws_bytes, out_image, out_final_T, out_n_contrib, counts4,
+                              stage_events, stream, false);
+}
+
+int gs_frame_forward_projected(const float* means3, const float* scales3, const float* quats4,
+                               const float* opacities, const float* colors3, int64_t n, const gs_camera* cam,
+                               const float* background3, int early_termination, int64_t isect_capacity, void* ws,
+                               size_t ws_bytes, float* out_image, float* out_final_T, int32_t* out_n_contrib,
+                               void* const* stage_events, gs_stream_t stream) {
+    if (cam && binning_for(n, ((cam->width + TILE - 1) / TILE) * ((cam->height + TILE - 1) / TILE)) != DEPTH_FIRST)
+        return set_error("gs_frame_forward_projected: the view does not use depth-first binning");
+    return frame_forward_impl(means3, scales3, quats4, opacities, colors3, n, cam, background3, early_termination,
+                              isect_capacity, ws, ws_bytes, out_image, out_final_T, out_n_contrib, nullptr,
+                              stage_events, stream, true);
+}
+
+int gs_frames_project(const float* means3, const float* scales3, const float* quats4, const float* opacities,
+                      int64_t n, int32_t n_views, const gs_camera* cams, const int64_t* capacities,
+                      void* const* workspaces, const size_t* ws_bytes, gs_stream_t stream) {
+    if (n < 0 || n > 0x7fffffff) return set_error("gs_frames_project: n=%lld out of range", (long long)n);
+    if (n_views < 0 || (n_views > 0 && (!cams || !capacities || !workspaces || !ws_bytes)))
+        return set_error("gs_frames_project: bad view arrays");
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int v0 = 0; v0 < n_views; v0 += MV_MAX) {
+        MvFwdArgs a;
+        a.nv = n_views - v0 < MV_MAX ? n_views - v0 : MV_MAX;
+        for (int j = 0; j < a.nv; ++j) {
+            const gs_camera& c = cams[v0 + j];
+            if (c.width < 1 || c.height < 1) return set_error("gs_frames_project: bad image size");
+            const int nt = ((c.width + TILE - 1) / TILE) * ((c.height + TILE - 1) / TILE);
+            if (nt > 65536) return set_error("gs_frames_project: more than 65536 tiles");
+            if (binning_for(n, nt) != DEPTH_FIRST)
+                return set_error("gs_frames_project: view %d does not use depth-first binning", v0 + j);
+            if (capacities[v0 + j] < 0 || capacities[v0 + j] >= (1ll << 30))
+                return set_error("gs_frames_project: capacity out of range");
+            const Layout L = layout(n, capacities[v0 + j], c.width, c.height);
+            if (ws_bytes[v0 + j] < L.total) return set_error("gs_frames_project: workspace %d too small", v0 + j);
+            void* ws = workspaces[v0 + j];
+            MvFwdView& V = a.v[j];
+            V.cam = make_camk(c);
+            V.xydr = at<float4>(ws, L.xydr);
+            V.conic = at<float4>(ws, L.conic);
+            V.tiles = at<uint32_t>(ws, L.tiles);
+            V.dkeys = at<uint32_t>(ws, L.dkeys);
+            V.dhist = at<uint32_t>(ws, L.dhist);
+            V.meta = at<unsigned long long>(ws, L.meta);
+            V.clean_word = at<unsigned long long>(ws, L.clean);
+            V.clean_sig = clean_sig(n, capacities[v0 + j], c.width, c.height);
+            V.zj = frame_zero_jobs(L, ws, nt, uses_tile_emit(n, nt));
+        }
+        if (launch_views_project_fwd(means3, scales3, quats4, opacities, n, a, s)) return -1;
+    }
+    return 0;
+}
+
+}  // extern "C"
+
+namespace gs {
+namespace {
+
+int frame_forward_impl(const float* means3, const float* scales3, const float* quats4, const float* opacities,
+                       const float* colors3, int64_t n, const gs_camera* cam, const float* background3,
+                       int early_termination, int64_t isect_capacity, void* ws, size_t ws_bytes, float* out_image,
+                       float* out_final_T, int32_t* out_n_contrib, unsigned long long* counts4,
+                       void* const* stage_events, gs_stream_t stream, bool projected) {
     if (!cam || !background3) return set_error("gs_frame_forward: null camera/background");
     if (n < 0 || n > 0x7fffffff) return set_error("gs_frame_forward: n=%lld out of range", (long long)n);
     if (isect_capacity < 0 || isect_capacity >= (1ll << 30))
@@ -239,20 +331,15 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     const int n_tiles = tiles_x * tiles_y;
     const Binning binning = binning_for(n, n_tiles);
     // depth-first binning with the tile-sorted emission (no global sort by tile)
-    const bool etiles = binning == DEPTH_FIRST && tile_emit() && emit_tiles_fits(n_tiles);
-    ZeroJobs zj;
-    zj.p[0] = at<uint4>(ws, L.thist);
-    zj.n16[0] = ((etiles ? L.tstatus : L.zero_end) - L.thist) / 16;  // (no tile-pass look-back status)
-    zj.p[1] = at<uint4>(ws, L.ranges);
-    zj.n16[1] = (8 * (size_t)tiles_x * tiles_y + 15) / 16;
-    zj.p[2] = at<uint4>(ws, L.d_geo);  // the backward accumulators: only when not known clean (meta[4])
-    zj.n16[2] = (L.partials - L.d_geo) / 16;
-    zj.cond2 = meta + 4;
+    const bool etiles = uses_tile_emit(n, n_tiles);
+    const ZeroJobs zj = frame_zero_jobs(L, ws, n_tiles, etiles);
     const bool scatter = binning == SCATTER;
     const bool direct = binning == DIRECT && counts4 == nullptr;  // the counted pass bins by scatter
     const int64_t kstride = direct_stride(isect_capacity, n_tiles);
     const uint32_t* t_order = !direct && tile_order_enabled(n_tiles) ? at<uint32_t>(ws, L.tile_order) : nullptr;
-    if (launch_project_fwd_dkey(means3, scales3, quats4, opacities, n, k, at<float>(ws, L.xydr),
+    // projected: gs_frames_project already projected this view (with every other view of the step)
+    if (!projected &&
+        launch_project_fwd_dkey(means3, scales3, quats4, opacities, n, k, at<float>(ws, L.xydr),
                                 at<float>(ws, L.conic), at<uint32_t>(ws, L.tiles), nullptr, meta,
                                 at<uint32_t>(ws, L.dkeys), at<uint32_t>(ws, L.dhist), s, zj,
                                 binning != DEPTH_FIRST ? at<uint32_t>(ws, L.tcount) : nullptr,
@@ -375,6 +462,11 @@ int gs_frame_forward(const float* means3, const float* scales3, const float* qua
     mark(stage_events, 5, s);
     return 0;
 }
+
+}  // namespace
+}  // namespace gs
+
+extern "C" {
 
 int gs_frame_backward(const float* means3, const float* scales3, const float* quats4, const float* colors3,
                       int64_t n, const gs_camera* cam, const float* background3, int64_t isect_capacity, void* ws,

@@ -48,6 +48,27 @@ struct MvArgs {
     int nv;
     MvView v[MV_MAX];
 };
+// the depth-first projection of every view of a step (views_init_kernel +
+// views_project_fwd_kernel, project.cu): per view its camera, its
+// workspace's outputs, meta, depth histograms, clean word and zero jobs
+struct MvFwdView {
+    CamK cam;
+    float4* xydr;
+    float4* conic;
+    uint32_t* tiles;
+    uint32_t* dkeys;
+    uint32_t* dhist;
+    unsigned long long* meta;
+    unsigned long long* clean_word;
+    unsigned long long clean_sig;
+    ZeroJobs zj;
+};
+struct MvFwdArgs {
+    int nv;
+    MvFwdView v[MV_MAX];
+};
+int launch_views_project_fwd(const float* means3, const float* scales3, const float* quats4, const float* opac,
+                             int64_t n, const MvFwdArgs& a, cudaStream_t s);
 int launch_views_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n,
                              const MvArgs& a, float* d_means3, float* d_scales3, float* d_quats4, float* d_rgbo4,
                              float* d_views16, bool accumulate, bool clear_rows, bool add_view, cudaStream_t s);

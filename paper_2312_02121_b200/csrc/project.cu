@@ -7,14 +7,122 @@
 namespace gs {
 
 // sg/core.py:146-171 quat_to_rotmat (normalised, (w,x,y,z) order).
+// Explicit roundings (no contraction left to the compiler): every kernel that
+// forms R -- per view or once for all views -- gets the same bits.
 __device__ __forceinline__ void quat_rot(float w, float x, float y, float z, float R[9]) {
-    R[0] = 1.f - 2.f * (y * y + z * z); R[1] = 2.f * (x * y - w * z); R[2] = 2.f * (x * z + w * y);
-    R[3] = 2.f * (x * y + w * z); R[4] = 1.f - 2.f * (x * x + z * z); R[5] = 2.f * (y * z - w * x);
-    R[6] = 2.f * (x * z - w * y); R[7] = 2.f * (y * z + w * x); R[8] = 1.f - 2.f * (x * x + y * y);
+    const float xx = __fmul_rn(x, x), yy = __fmul_rn(y, y), xy = __fmul_rn(x, y), xz = __fmul_rn(x, z),
+                yz = __fmul_rn(y, z);
+    R[0] = __fsub_rn(1.f, 2.f * __fmaf_rn(z, z, yy));
+    R[1] = 2.f * __fmaf_rn(-w, z, xy);
+    R[2] = 2.f * __fmaf_rn(w, y, xz);
+    R[3] = 2.f * __fmaf_rn(w, z, xy);
+    R[4] = __fsub_rn(1.f, 2.f * __fmaf_rn(z, z, xx));
+    R[5] = 2.f * __fmaf_rn(-w, x, yz);
+    R[6] = 2.f * __fmaf_rn(-w, y, xz);
+    R[7] = 2.f * __fmaf_rn(w, x, yz);
+    R[8] = __fsub_rn(1.f, 2.f * __fmaf_rn(y, y, xx));
+}
+
+// |q| with one fixed rounding sequence
+__device__ __forceinline__ float quat_norm(float4 q) {
+    return sqrtf(__fmaf_rn(q.w, q.w, __fmaf_rn(q.z, q.z, __fmaf_rn(q.y, q.y, __fmul_rn(q.x, q.x)))));
+}
+
+// a0 b0 + a1 b1 + a2 b2 with one fixed rounding sequence (no contraction
+// left to the compiler, so every kernel computing it gets the same bits)
+__device__ __forceinline__ float dot3_rn(float a0, float b0, float a1, float b1, float a2, float b2) {
+    return __fmaf_rn(a2, b2, __fmaf_rn(a1, b1, __fmul_rn(a0, b0)));
 }
 
 __device__ __forceinline__ void report(unsigned long long* status, int i, int code) {
     atomicMin(status, ((unsigned long long)(unsigned)i << 8) | (unsigned long long)code);
+}
+
+// The projection split into its view-independent part and the per-view rest
+// for the multi-view kernel (which reads and prepares a Gaussian once and
+// runs the rest for every view).  project_fwd_kernel keeps the same
+// operations inline (the split costs it register spills at its 32-register
+// budget); the roundings that the compiler could otherwise contract
+// differently in the two contexts are explicit (dot3_rn), so both give the
+// same bits.
+// View-independent part (sg/core.py:146-195): the scale / quaternion validity
+// and M = R(q / |q|) diag(s).
+struct FwdPrep {
+    int err;  // 0, GS_ERR_SCALE or GS_ERR_QUAT
+    float M[9];
+};
+__device__ __forceinline__ FwdPrep proj_fwd_prep(float4 q, float sx, float sy, float sz) {
+    FwdPrep P;
+    const float qn = quat_norm(q);
+    P.err = (sx <= 0.f || sy <= 0.f || sz <= 0.f) ? GS_ERR_SCALE : (qn <= QUAT_EPS ? GS_ERR_QUAT : 0);
+    if (P.err == 0) {
+        const float inv = 1.f / qn;
+        float R[9];
+        quat_rot(q.x * inv, q.y * inv, q.z * inv, q.w * inv, R);
+        // M = R diag(s)
+        P.M[0] = R[0] * sx, P.M[1] = R[1] * sy, P.M[2] = R[2] * sz;
+        P.M[3] = R[3] * sx, P.M[4] = R[4] * sy, P.M[5] = R[5] * sz;
+        P.M[6] = R[6] * sx, P.M[7] = R[7] * sy, P.M[8] = R[8] * sz;
+    }
+    return P;
+}
+
+// The rest of sg/projection.py:115-145 for a Gaussian not culled by depth
+// (camera-space mean t): errors -> Sigma' + 0.3 I -> pixel -> radius ->
+// off-screen cull, plus the conic and the tile rect.
+__device__ __forceinline__ void proj_fwd_core(const CamK& cam, int i, float tx, float ty, float tz, const FwdPrep& P,
+                                              float op, unsigned long long* status, float4& o_xydr, float4& o_con,
+                                              uint32_t& nt, float& ca, float& cb, float& cc, int& tx0, int& tx1,
+                                              int& ty0, int& ty1) {
+    if (P.err) {
+        report(status, i, P.err);
+        return;
+    }
+    const float* Rc = cam.R;
+    const float* M = P.M;
+    // T = J R_cw, J = [[fx/tz, 0, -fx tx/tz^2], [0, fy/tz, -fy ty/tz^2]]
+    const float iz = 1.f / tz;
+    const float j00 = cam.fx * iz, j02 = -cam.fx * tx * iz * iz;
+    const float j11 = cam.fy * iz, j12 = -cam.fy * ty * iz * iz;
+    float T0[3], T1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        T0[k] = __fmaf_rn(j02, Rc[6 + k], __fmul_rn(j00, Rc[k]));
+        T1[k] = __fmaf_rn(j12, Rc[6 + k], __fmul_rn(j11, Rc[3 + k]));
+    }
+    // V = T M; Sigma' = V V^T + 0.3 I  (T Sigma T^T with Sigma = M M^T)
+    float V0[3], V1[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        V0[c] = dot3_rn(T0[0], M[c], T0[1], M[3 + c], T0[2], M[6 + c]);
+        V1[c] = dot3_rn(T1[0], M[c], T1[1], M[3 + c], T1[2], M[6 + c]);
+    }
+    ca = __fadd_rn(dot3_rn(V0[0], V0[0], V0[1], V0[1], V0[2], V0[2]), DILATION);
+    cb = dot3_rn(V0[0], V1[0], V0[1], V1[1], V0[2], V1[2]);
+    cc = __fadd_rn(dot3_rn(V1[0], V1[0], V1[1], V1[1], V1[2], V1[2]), DILATION);
+    if (fabsf(tz) < 1e-12f) {
+        report(status, i, GS_ERR_HOMOG);
+        return;
+    }
+    const float px = (cam.fx * (tx / tz) + 0.5f) + cam.cx;
+    const float py = (cam.fy * (ty / tz) + 0.5f) + cam.cy;
+    const float det = cov2d_det(ca, cb, cc);
+    if (!(det > 0.f && ca + cc > 0.f)) {
+        report(status, i, GS_ERR_COV2D);
+        return;
+    }
+    const float mid = 0.5f * (ca + cc);
+    const float lam = __fadd_rn(mid, sqrtf(__fmaf_rn(cb, cb, __fmul_rn(__fmul_rn(0.25f, ca - cc), ca - cc))));
+    const float rf = ceilf(3.f * sqrtf(lam));
+    const int r = rf < (float)MAX_RADIUS ? (int)rf : MAX_RADIUS;
+    const float fr = (float)r;
+    const bool off = (px + fr < 0.f) || (px - fr >= (float)cam.W) || (py + fr < 0.f) || (py - fr >= (float)cam.H);
+    o_xydr = make_float4(px, py, tz, __int_as_float(off ? 0 : r));
+    if (!off) {
+        o_con = conic_of(ca, cb, cc, det, op);
+        tile_rect(px, py, r, cam.tiles_x, cam.tiles_y, tx0, tx1, ty0, ty1);
+        nt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+    }
 }
 
 // sg/projection.py:115-145 project_gaussian for every Gaussian, in the
@@ -76,7 +184,7 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
     uint32_t nt = 0;
     const bool depth_culled = (tz <= cam.near_plane) || (tz >= cam.far_plane);
     if (!depth_culled) {
-        const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+        const float qn = quat_norm(q);
         if (sx <= 0.f || sy <= 0.f || sz <= 0.f) {
             report(status, i, GS_ERR_SCALE);
         } else if (qn <= QUAT_EPS) {
@@ -95,19 +203,19 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
             float T0[3], T1[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                T0[k] = j00 * Rc[k] + j02 * Rc[6 + k];
-                T1[k] = j11 * Rc[3 + k] + j12 * Rc[6 + k];
+                T0[k] = __fmaf_rn(j02, Rc[6 + k], __fmul_rn(j00, Rc[k]));
+                T1[k] = __fmaf_rn(j12, Rc[6 + k], __fmul_rn(j11, Rc[3 + k]));
             }
             // V = T M; Sigma' = V V^T + 0.3 I  (T Sigma T^T with Sigma = M M^T)
             float V0[3], V1[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                V0[c] = T0[0] * M[c] + T0[1] * M[3 + c] + T0[2] * M[6 + c];
-                V1[c] = T1[0] * M[c] + T1[1] * M[3 + c] + T1[2] * M[6 + c];
+                V0[c] = dot3_rn(T0[0], M[c], T0[1], M[3 + c], T0[2], M[6 + c]);
+                V1[c] = dot3_rn(T1[0], M[c], T1[1], M[3 + c], T1[2], M[6 + c]);
             }
-            ca = V0[0] * V0[0] + V0[1] * V0[1] + V0[2] * V0[2] + DILATION;
-            cb = V0[0] * V1[0] + V0[1] * V1[1] + V0[2] * V1[2];
-            cc = V1[0] * V1[0] + V1[1] * V1[1] + V1[2] * V1[2] + DILATION;
+            ca = __fadd_rn(dot3_rn(V0[0], V0[0], V0[1], V0[1], V0[2], V0[2]), DILATION);
+            cb = dot3_rn(V0[0], V1[0], V0[1], V1[1], V0[2], V1[2]);
+            cc = __fadd_rn(dot3_rn(V1[0], V1[0], V1[1], V1[1], V1[2], V1[2]), DILATION);
             if (fabsf(tz) < 1e-12f) {
                 report(status, i, GS_ERR_HOMOG);
             } else {
@@ -118,7 +226,7 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
                     report(status, i, GS_ERR_COV2D);
                 } else {
                     const float mid = 0.5f * (ca + cc);
-                    const float lam = mid + sqrtf(0.25f * (ca - cc) * (ca - cc) + cb * cb);
+                    const float lam = __fadd_rn(mid, sqrtf(__fmaf_rn(cb, cb, __fmul_rn(__fmul_rn(0.25f, ca - cc), ca - cc))));
                     const float rf = ceilf(3.f * sqrtf(lam));
                     const int r = rf < (float)MAX_RADIUS ? (int)rf : MAX_RADIUS;
                     const float fr = (float)r;
@@ -195,7 +303,7 @@ struct BwdPrep {
 };
 __device__ __forceinline__ BwdPrep proj_bwd_prep(float4 q, const float s[3]) {
     BwdPrep P;
-    const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+    const float qn = quat_norm(q);
     P.inv = 1.f / qn;
     P.qw = q.x * P.inv, P.qx = q.y * P.inv, P.qy = q.z * P.inv, P.qz = q.w * P.inv;
     quat_rot(P.qw, P.qx, P.qy, P.qz, P.R);
@@ -730,6 +838,110 @@ int launch_views_project_bwd(const float* means3, const float* scales3, const fl
     if (check_launch("views_project_bwd_kernel")) return -1;
     launch_k(views_reduce_kernel, dim3(a.nv), dim3(384), 0, s, a, blocks, d_views16, add_view);
     return check_launch("views_reduce_kernel");
+}
+
+// ---------------------------------------------------------------- all views at once (forward)
+// The depth-first frame's projection (project_fwd_kernel<1>) for every view
+// of a multi-view step in one pass: each Gaussian's parameters are read once
+// (44 B) and its M = R diag(s) formed once; per view the camera-space mean,
+// the depth cull and the rest of sg/projection.py:115-145 write the view's
+// xydr / conic / tiles / depth key (40 B) into its own workspace.  Each
+// view's visible depth-key range is reduced per warp, per block in shared
+// memory and once per block into the view's meta[5] / meta[6].  Against one
+// projection per view: 40 + 44/views instead of 84 B per Gaussian and view.
+__global__ void __launch_bounds__(256) views_init_kernel(const MvFwdArgs a) {
+    griddep_wait();
+    const MvFwdView& V = a.v[blockIdx.x];
+    if (threadIdx.x == 0) {
+        unsigned long long* meta = V.meta;
+        meta[0] = ~0ull;
+        meta[1] = 0ull;
+        meta[2] = 0ull;
+        meta[3] = 0ull;
+        meta[4] = *V.clean_word != V.clean_sig ? 1ull : 0ull;
+        *V.clean_word = V.clean_sig;
+        meta[5] = 0xFFFFFFFFull;
+        meta[6] = 0ull;
+        meta[7] = 0ull;
+        meta[8] = 4ull;
+    }
+    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) V.dhist[k] = 0u;
+}
+
+__global__ void __launch_bounds__(256, 4) views_project_fwd_kernel(const float* __restrict__ means,
+                                                                   const float* __restrict__ scales,
+                                                                   const float4* __restrict__ quats,
+                                                                   const float* __restrict__ opac, int n,
+                                                                   const MvFwdArgs a) {
+    griddep_wait();
+    const int nv = a.nv;
+    for (int v = 0; v < nv; ++v) run_zero_jobs(a.v[v].zj);
+    __shared__ uint32_t s_kmin[MV_MAX], s_kmax[MV_MAX];
+    for (int v = threadIdx.x; v < MV_MAX; v += blockDim.x) s_kmin[v] = 0xFFFFFFFFu, s_kmax[v] = 0u;
+    __syncthreads();
+    const int n_round = (n + 31) & ~31;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += gridDim.x * blockDim.x) {
+        const bool in = i < n;
+        float mx = 0.f, my = 0.f, mz = 0.f, sx = 1.f, sy = 1.f, sz = 1.f, op = 0.f;
+        float4 q = make_float4(1.f, 0.f, 0.f, 0.f);
+        if (in) {
+            mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
+            sx = scales[3 * i], sy = scales[3 * i + 1], sz = scales[3 * i + 2];
+            q = quats[i];
+            op = opac[i];
+        }
+        const FwdPrep P = proj_fwd_prep(q, sx, sy, sz);
+        for (int v = 0; v < nv; ++v) {
+            const MvFwdView& V = a.v[v];
+            const CamK& cam = V.cam;
+            uint32_t dkey = 0xFFFFFFFFu;
+            if (in) {
+                const float* Rc = cam.R;
+                const float tx = Rc[0] * mx + Rc[1] * my + Rc[2] * mz + cam.t[0];
+                const float ty = Rc[3] * mx + Rc[4] * my + Rc[5] * mz + cam.t[1];
+                const float tz = Rc[6] * mx + Rc[7] * my + Rc[8] * mz + cam.t[2];
+                float4 o_xydr = make_float4(0.f, 0.f, tz, __int_as_float(0));
+                float4 o_con = make_float4(0.f, 0.f, 0.f, 0.f);
+                float ca = 0.f, cb = 0.f, cc = 0.f;
+                int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
+                uint32_t nt = 0;
+                if (!((tz <= cam.near_plane) || (tz >= cam.far_plane)))
+                    proj_fwd_core(cam, i, tx, ty, tz, P, op, V.meta, o_xydr, o_con, nt, ca, cb, cc, tx0, tx1, ty0,
+                                  ty1);
+                V.xydr[i] = o_xydr;
+                V.conic[i] = o_con;
+                V.tiles[i] = nt;
+                dkey = nt ? __float_as_uint(tz) : 0xFFFFFFFFu;
+                V.dkeys[i] = dkey;
+            }
+            const uint32_t kmin = __reduce_min_sync(0xffffffffu, dkey);
+            const uint32_t kmax = __reduce_max_sync(0xffffffffu, dkey != 0xFFFFFFFFu ? dkey : 0u);
+            if ((threadIdx.x & 31) == 0 && kmin != 0xFFFFFFFFu) {
+                atomicMin(&s_kmin[v], kmin);
+                atomicMax(&s_kmax[v], kmax);
+            }
+        }
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < nv; v += blockDim.x)
+        if (s_kmin[v] <= s_kmax[v]) {
+            atomicMin(a.v[v].meta + 5, (unsigned long long)s_kmin[v]);
+            atomicMax(a.v[v].meta + 6, (unsigned long long)s_kmax[v]);
+        }
+}
+
+int launch_views_project_fwd(const float* means3, const float* scales3, const float* quats4, const float* opac,
+                             int64_t n, const MvFwdArgs& a, cudaStream_t s) {
+    if (a.nv <= 0) return 0;
+    launch_k(views_init_kernel, dim3(a.nv), dim3(256), 0, s, a);
+    if (check_launch("views_init_kernel")) return -1;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks < 1) blocks = 1;  // the zero jobs run even for an empty scene
+    const int64_t cap = (int64_t)sort_sm_count() * 4;
+    if (blocks > cap) blocks = cap;
+    launch_k(views_project_fwd_kernel, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
+             (const float4*)quats4, opac, (int)n, a);
+    return check_launch("views_project_fwd_kernel");
 }
 
 int launch_project_bwd(const float* means3, const float* scales3, const float* quats4, int64_t n, const CamK& k,

@@ -113,6 +113,8 @@ class RenderStep:
         self.et = bool(early_termination)
         self.headroom = headroom
         self.batched = bool(batched_projection) and len(self.cams) > 1
+        # batched forward projection too, when every view bins depth-first (large scenes)
+        self.batched_fwd = self.batched and ops.frames_projectable(self.n, self.cams)
         self.nbuf = buffers
         z = lambda *shape: torch.zeros(shape, device=self.dev, dtype=torch.float32)
         self.sets = []
@@ -158,6 +160,8 @@ class RenderStep:
         out = unpack(s["grads"], self.n)
         main = torch.cuda.current_stream(self.dev)
         sts = [main] + self.aux
+        if self.batched_fwd:  # every view's projection in one pass over the Gaussians
+            ops.frames_project(m, sc, q, o, self.cams, self.caps, self.wss)
         for a in sts[1:]:
             a.wait_stream(main)
         bwd_done = None
@@ -165,7 +169,8 @@ class RenderStep:
             st = sts[vi % len(sts)]
             with torch.cuda.stream(st):
                 fr = ops.frame_forward(m, sc, q, o, c, cam, self.bg, self.et, capacity=self.caps[vi],
-                                       check_meta=False, ws=self.wss[vi], binning=self.binnings[vi])
+                                       check_meta=False, ws=self.wss[vi], binning=self.binnings[vi],
+                                       projected=self.batched_fwd)
                 last = vi == len(self.cams) - 1
                 if self.batched or (last and self.reducer is not None):
                     # the projection backward runs afterwards (batched over the views, and/or

@@ -504,12 +504,31 @@ def frame_workspace(n: int, capacity: int, width: int, height: int, device) -> t
 
 def frame_forward(means, scales, quats, opacities, colors, cam: CameraParams, background=(0.0, 0.0, 0.0),
                   early_termination=True, *, capacity: int | None = None, counts=False, check_meta=True,
-                  ws: torch.Tensor | None = None, events=None, binning: str | None = None) -> Frame:
+                  ws: torch.Tensor | None = None, events=None, binning: str | None = None,
+                  projected: bool = False) -> Frame:
     """gs_frame_forward: image, final_T, n_contrib of one view.  binning:
     force "depth_first" / "scatter" / "direct" for this call (default: the
     library's choice, or the scatter fallback a skewed view of this size
-    needed before -- see DIRECT_SKEW)."""
+    needed before -- see DIRECT_SKEW).  projected: frames_project already
+    projected this view into `ws` (gs_frame_forward_projected; needs the
+    capacity and workspace given, check_meta=False, no counts)."""
     L = _lib.load()
+    if projected:
+        if ws is None or capacity is None or check_meta or counts:
+            raise ValueError("frame_forward(projected=True) needs ws and capacity, check_meta=False, no counts")
+        means, scales, quats, opacities, colors = check_params(means, scales, quats, opacities, colors)
+        n, dev, H, W = means.shape[0], means.device, cam.height, cam.width
+        image = torch.empty((H, W, 3), device=dev, dtype=torch.float32)
+        final_T = torch.empty((H, W), device=dev, dtype=torch.float32)
+        n_contrib = torch.empty((H, W), device=dev, dtype=torch.int32)
+        camc = cam.c()
+        bg = (C.c_float * 3)(*[float(b) for b in background])
+        check(L.gs_frame_forward_projected(_ptr(means), _ptr(scales), _ptr(quats), _ptr(opacities), _ptr(colors), n,
+                                           C.byref(camc), bg, 1 if early_termination else 0, int(capacity),
+                                           _ptr(ws), ws.numel(), _ptr(image), _ptr(final_T), _ptr(n_contrib),
+                                           _event_array(events), _stream()), "gs_frame_forward_projected")
+        return Frame(cam, tuple(float(b) for b in background), bool(early_termination), n, int(capacity), ws, image,
+                     final_T, n_contrib, None, binning="depth_first")
     means, scales, quats, opacities, colors = check_params(means, scales, quats, opacities, colors)
     n = means.shape[0]
     dev = means.device
@@ -549,6 +568,30 @@ def frame_forward(means, scales, quats, opacities, colors, cam: CameraParams, ba
             return fr
         cap = _capacity_hint[key]
         ws = None
+
+
+def frames_project(means, scales, quats, opacities, cams, capacities, workspaces) -> None:
+    """gs_frames_project: the depth-first projection of every view of a step
+    (each into its own workspace, sized for its capacity) in one pass over
+    the Gaussians; each view then continues with
+    frame_forward(..., projected=True)."""
+    L = _lib.load()
+    nv = len(cams)
+    if nv == 0:
+        return
+    n = means.shape[0]
+    camc = (_lib.GsCamera * nv)(*[c.c() for c in cams])
+    caps = (C.c_int64 * nv)(*[int(c) for c in capacities])
+    wss = (C.c_void_p * nv)(*[w.data_ptr() for w in workspaces])
+    wsb = (C.c_size_t * nv)(*[w.numel() for w in workspaces])
+    vp = lambda a: C.cast(a, C.c_void_p)
+    check(L.gs_frames_project(_ptr(means), _ptr(scales), _ptr(quats), _ptr(opacities), n, nv, camc, vp(caps),
+                              vp(wss), vp(wsb), _stream()), "gs_frames_project")
+
+
+def frames_projectable(n: int, cams) -> bool:
+    """Whether every view would use depth-first binning (gs_frames_project)."""
+    return all(frame_binning(n, c) == "depth_first" for c in cams)
 
 
 def _event_array(events):

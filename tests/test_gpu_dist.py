@@ -19,7 +19,7 @@ import pytest
 import torch
 import torch.multiprocessing as mp
 
-from parity import grad_gate
+from parity import grad_gate, runs_gate
 
 pytestmark = pytest.mark.gpu
 
@@ -97,13 +97,9 @@ def _gate(a, b, n, what):
     from paper_2312_02121_b200 import engine as E
     ua, ub = E.unpack(torch.as_tensor(a), n), E.unpack(torch.as_tensor(b), n)
     for k in KEYS:
-        r = grad_gate(ua[k].numpy(), ub[k].numpy(), rel=1e-3, floor=1e-2)
+        r = runs_gate(ua[k].numpy(), ub[k].numpy())
         print(what, k, r)
-        # the sums over views / ranks associate differently on the two sides and the raster
-        # backward's fp32 atomics land in a different order: an element whose per-view terms
-        # nearly cancel (d_quat) can miss the per-element bound by a small factor -- a handful
-        # of such elements out of millions is allowed, the class as a whole must agree
-        assert r["rel_l2"] <= 1e-4 and (r["ok"] or (r["n_viol"] <= 4 and r["worst_ratio"] < 10.0)), (what, k, r)
+        assert r["ok"], (what, k, r)
 
 
 def test_view_sharded_two_ranks(cuda, tmp_path):

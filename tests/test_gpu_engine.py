@@ -190,6 +190,49 @@ def test_views_project_backward_equals_per_view(cuda):
         assert np.abs(a - b).max() <= 1e-4 * (np.abs(b).max() + 1e-30), k
 
 
+def test_frames_project_equals_per_view_projection(cuda):
+    """gs_frames_project (every view's depth-first projection in one pass)
+    then gs_frame_forward_projected per view give the per-view
+    gs_frame_forward's frames bit for bit (same operations, same order),
+    including the error a bad Gaussian raises in a view that sees it."""
+    from paper_2312_02121_b200 import ops
+    from paper_2312_02121_b200.scenes import make_config
+    spec = make_config(3, n_override=450_000, n_views=3)  # > 400k: depth-first binning
+    params = [torch.as_tensor(a, device=cuda) for a in (spec.means, spec.scales, spec.quats, spec.opacities,
+                                                        spec.colors)]
+    n = spec.n
+    cams = [ops.CameraParams.of(c) for c in spec.cameras]
+    assert ops.frames_projectable(n, cams)
+    refs = [ops.frame_forward(*params, cm, (0.0, 0.0, 0.0), True) for cm in cams]
+    caps = [r.capacity for r in refs]
+    wss = [ops.frame_workspace(n, cap, cm.width, cm.height, cuda) for cap, cm in zip(caps, cams)]
+    ops.frames_project(*params[:4], cams, caps, wss)
+    for r, cm, cap, ws in zip(refs, cams, caps, wss):
+        fr = ops.frame_forward(*params, cm, (0.0, 0.0, 0.0), True, capacity=cap, ws=ws, check_meta=False,
+                               projected=True)
+        assert torch.equal(fr.image, r.image) and torch.equal(fr.final_T, r.final_T)
+        assert torch.equal(fr.n_contrib, r.n_contrib)
+        ta, tb = fr.tensors(), r.tensors()
+        for k in ("xydr", "conic", "tiles", "ranges", "sorted_vals", "depth_order"):
+            assert torch.equal(ta[k], tb[k]), k
+        assert torch.equal(fr.meta().cpu()[:9], r.meta().cpu()[:9])
+    bad = [p.clone() for p in params]
+    bad[1][123] = -1.0  # a non-positive scale (sg/core.py:189-191): the error of every view that sees it
+    ops.frames_project(*bad[:4], cams, caps, wss)
+    errs = 0
+    for cm, cap, ws in zip(cams, caps, wss):
+        fr = ops.frame_forward(*bad, cm, (0.0, 0.0, 0.0), True, capacity=cap, ws=ws, check_meta=False,
+                               projected=True)
+        ref = ops.frame_forward(*bad, cm, (0.0, 0.0, 0.0), True, check_meta=False)
+        st = int(fr.meta().cpu()[0])
+        assert st == int(ref.meta().cpu()[0])
+        if st != -1:
+            errs += 1
+            with pytest.raises(ValueError, match="scale"):
+                ops.raise_status(st)
+    assert errs > 0
+
+
 def test_batched_and_per_view_engine_agree(cuda):
     """RenderStep with the batched projection backward (default for several
     views) and with one projection backward per view give the same step."""

@@ -7,7 +7,7 @@ import pytest
 import torch
 
 import oracle as O
-from parity import GRAD_CLASSES, classify_image, golden_names, grad_gate, load_golden
+from parity import GRAD_CLASSES, classify_image, golden_names, grad_gate, load_golden, runs_gate
 
 pytestmark = pytest.mark.gpu
 
@@ -46,7 +46,7 @@ def test_frame_equals_staged_on_golden(name, cuda):
     assert torch.equal(tv["sorted_tile_keys"].long(), (st.bins.sorted_keys >> 32))
     for k in GRAD_CLASSES:
         a, b = g_f[k].cpu().numpy(), g_s[k].cpu().numpy()
-        r = grad_gate(a, b, rel=1e-3, floor=1e-2)  # only the fp32 summation order differs (atomics, reduction tree)
+        r = runs_gate(a, b)  # only the fp32 summation order differs (atomics, reduction tree)
         assert r["ok"], (name, k, r)
 
 
@@ -370,7 +370,7 @@ def test_option_change_between_forward_and_backward(cuda):
             ops.set_option("binning", bwd_mode)
             g = ops.frame_backward(fr, t[0], t[1], t[2], t[4], d)
             for k in GRAD_CLASSES:
-                r = grad_gate(g[k].cpu().numpy(), ref[k].cpu().numpy(), rel=1e-3, floor=1e-2)
+                r = runs_gate(g[k].cpu().numpy(), ref[k].cpu().numpy())
                 assert r["ok"], (fwd_mode, bwd_mode, k, r)
     finally:
         ops.set_option("binning", 0)
@@ -397,7 +397,7 @@ def test_backward_accumulators_stay_clean(cuda):
     def same(a, b):
         for k in a:
             # only the fp32 atomic order differs (a dirty accumulator would be off by O(1))
-            r = grad_gate(a[k].cpu().numpy(), b[k].cpu().numpy(), rel=1e-4, floor=1e-2)
+            r = runs_gate(a[k].cpu().numpy(), b[k].cpu().numpy(), rel=1e-4)
             assert r["ok"], (k, r)
 
     ref = grads(ops.frame_forward(*t, cp, (0.0, 0.0, 0.0), True))
@@ -448,5 +448,5 @@ def test_skewed_view_falls_back_from_direct_binning(cuda):
     ga = ops.frame_backward(fr, t[0], t[1], t[2], t[4], d)
     gb = ops.frame_backward(ref, t[0], t[1], t[2], t[4], d)
     for k in ("d_mean", "d_rgbo"):
-        r = grad_gate(ga[k].cpu().numpy(), gb[k].cpu().numpy(), rel=1e-3, floor=1e-2)
+        r = runs_gate(ga[k].cpu().numpy(), gb[k].cpu().numpy())
         assert r["ok"], (k, r)

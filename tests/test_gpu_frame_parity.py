@@ -23,7 +23,7 @@ import numpy as np
 import pytest
 import torch
 
-from parity import GRAD_CLASSES, compare_grads, frame_ok, frame_parity
+from parity import GRAD_CLASSES, compare_grads, frame_ok, frame_parity, runs_gate
 
 pytestmark = pytest.mark.gpu
 
@@ -125,10 +125,10 @@ def test_full_frame_record_backward_equals_stage_backward(config, cuda):
     torch.cuda.synchronize()
     for name, a, b in (("d_rgbo", gf["d_rgbo"], gs["d_rgbo"]), ("d_geo", tv["d_geo"], gs["d_geo"]),
                        ("d_c11", tv["d_c11"], gs["d_c11"])):
-        r = grad_gate(a.cpu().numpy(), b.cpu().numpy(), rel=1e-3, floor=1e-2)
+        r = runs_gate(a.cpu().numpy(), b.cpu().numpy())
         print(config, name, r)
         assert r["ok"], (config, name, r)
     for k in GRAD_CLASSES:
-        r = grad_gate(gf[k].cpu().numpy(), gs[k].cpu().numpy(), rel=1e-3, floor=1e-2)
+        r = runs_gate(gf[k].cpu().numpy(), gs[k].cpu().numpy())
         print(config, k, r)
         assert r["rel_l2"] <= 1e-5, (config, k, r)
