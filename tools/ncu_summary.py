@@ -21,14 +21,16 @@ import sys
 from collections import defaultdict
 
 STAGE_OF = [  # kernel-name regex -> bench stage name (the last capture of each kernel wins)
-    (r"project_fwd_kernel", "project"),
+    (r"views_project_fwd_kernel|project_fwd_kernel", "project"),
     (r"onesweep_kernel<unsigned int, (16|4)", "sort_u32"),
     (r"emit_scan_kernel", "scan_emit"),
+    (r"et_count_kernel", "tile_counts"),
+    (r"et_emit_kernel", "tile_emit"),
     (r"segsort_small_kernel", "segsort"),
     (r"ranges_u32_kernel", "tile_sort_ranges"),
     (r"raster_fwd_kernel", "raster_fwd"),
     (r"raster_bwd_rec_kernel", "raster_bwd"),
-    (r"project_bwd_kernel", "project_bwd"),
+    (r"views_project_bwd_kernel|project_bwd_kernel", "project_bwd"),
 ]
 
 

@@ -14,8 +14,8 @@ for r in rows:
         hdr = r
         stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
         continue
-    if not hdr or len(r) < 6 or not r[0].strip().isdigit():
-        continue
+    if not hdr or len(r) != len(hdr) or not r[0].strip().isdigit():
+        continue  # (lines whose source text ncu did not quote cleanly are skipped)
     line = int(r[0])
     num = lambda i: float(r[i].replace(",", "") or 0) if i < len(r) and r[i] not in ("", "-") else 0.0
     a = agg[line]
