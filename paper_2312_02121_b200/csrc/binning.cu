@@ -482,7 +482,13 @@ int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* 
 // look-back over 4346 digits per chunk measured 320 us per config-3 view: the
 // first wave's chunks all look back to chunk 0 at once).  The sorted tile keys
 // are not written (the ranges imply them).
-constexpr int ET_WARPS = 8;
+#ifndef GS_ET_WARPS
+#define GS_ET_WARPS 8  // warps per chunk (A/B knob)
+#endif
+#ifndef GS_ET_MINB
+#define GS_ET_MINB 2  // resident emission CTAs per SM the registers are budgeted for
+#endif
+constexpr int ET_WARPS = GS_ET_WARPS;
 constexpr int ET_ROUNDS = 8;  // 32-Gaussian rounds per warp (<= 256 Gaussians per warp: u16 counts)
 constexpr int ET_THREADS = ET_WARPS * 32;
 constexpr int ET_CHUNK = ET_THREADS * ET_ROUNDS;  // Gaussians per chunk (2048: u16 chunk counts)
@@ -491,7 +497,7 @@ __host__ __device__ inline int et_stride(int n_tiles) { return (n_tiles + 1) & ~
 size_t emit_tiles_smem(int n_tiles) {
     return (size_t)ET_WARPS * et_stride(n_tiles) * 2 + (size_t)n_tiles * 4;
 }
-bool emit_tiles_fits(int n_tiles) { return n_tiles >= 1 && emit_tiles_smem(n_tiles) <= 200 * 1024; }  // <= 10240 tiles
+bool emit_tiles_fits(int n_tiles) { return n_tiles >= 1 && emit_tiles_smem(n_tiles) <= 200 * 1024; }  // <= 10240 tiles (8 warps)
 // tables: u32 column prefixes [chunk][tile], then the u16 counts [chunk][tile]
 static size_t et_prefix_bytes(int64_t n, int n_tiles) {
     const int64_t chunks = (n + ET_CHUNK - 1) / ET_CHUNK;
@@ -655,7 +661,7 @@ __global__ void __launch_bounds__(ES_WARPS * 32) et_scan_kernel(const unsigned s
     }
 }
 
-__global__ void __launch_bounds__(ET_THREADS, 2) et_emit_kernel(
+__global__ void __launch_bounds__(ET_THREADS, GS_ET_MINB) et_emit_kernel(
     const uint32_t* __restrict__ order, const uint32_t* __restrict__ order_alt, const float4* __restrict__ xydr,
     int n, int tiles_x, int tiles_y, int64_t capacity, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ prefix, uint32_t* __restrict__ vals, const unsigned long long* __restrict__ meta) {
