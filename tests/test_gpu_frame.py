@@ -214,6 +214,43 @@ def test_frame_errors_and_empty(cuda):
     assert g["d_view"].abs().max().item() == 0.0
 
 
+@pytest.mark.parametrize("tile_emit", [1, 0])
+def test_depth_first_all_culled_and_errors(tile_emit, cuda):
+    """Depth-first binning (both variants) on a scene with nothing visible
+    (every Gaussian behind the camera or off screen): background image, no
+    intersections, zero gradients; and the reference's error for a bad
+    Gaussian that the view sees."""
+    from paper_2312_02121_b200 import ops
+    cp = ops.CameraParams(np.eye(4).tolist(), 16.0, 16.0, 8.0, 8.0, 16, 16, 0.1, 100.0)
+    n = 3000
+    means = torch.zeros((n, 3), device=cuda)
+    means[:, 2] = -5.0  # behind the camera
+    means[::2, 0], means[::2, 2] = 1e4, 5.0  # off screen
+    scales = torch.full((n, 3), 0.1, device=cuda)
+    quats = torch.zeros((n, 4), device=cuda)
+    quats[:, 0] = 1.0
+    opac = torch.full((n,), 0.5, device=cuda)
+    cols = torch.rand((n, 3), device=cuda)
+    ops.set_option("binning", 1)
+    ops.set_option("tile_emit", tile_emit)
+    try:
+        fr = ops.frame_forward(means, scales, quats, opac, cols, cp, (0.2, 0.4, 0.6))
+        assert fr.n_isect == 0 and int(fr.meta().cpu()[7]) == 0
+        assert np.allclose(fr.image.cpu().numpy(), np.array([0.2, 0.4, 0.6], np.float32)[None, None, :])
+        g = ops.frame_backward(fr, means, scales, quats, cols, torch.ones(16, 16, 3, device=cuda))
+        for k in ("d_mean", "d_scale", "d_quat", "d_rgbo", "d_view"):
+            assert g[k].abs().max().item() == 0.0, k
+        bad = scales.clone()
+        means2 = means.clone()
+        means2[7] = torch.tensor([0.0, 0.0, 4.0], device=cuda)  # visible
+        bad[7, 1] = -1.0
+        with pytest.raises(ValueError, match="gaussian 7: scale"):
+            ops.frame_forward(means2, bad, quats, opac, cols, cp)
+    finally:
+        ops.set_option("binning", 0)
+        ops.set_option("tile_emit", 1)
+
+
 def test_autograd_matches_frame(cuda):
     from paper_2312_02121_b200 import ops
     g = load_golden("rot_ragged")
