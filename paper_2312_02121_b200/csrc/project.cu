@@ -158,6 +158,13 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
     constexpr bool DKEY = MODE != 0;
     griddep_wait();
     run_zero_jobs(zj);  // frame path: clear the later stages' counters / accumulators
+    // MODE 1: the histogram of the visible depth keys' low byte (the depth
+    // sort's first pass rotates it by the minimum's low byte: sort.cu)
+    __shared__ uint32_t s_lo[MODE == 1 ? 256 : 1];
+    if (MODE == 1) {
+        for (int k = threadIdx.x; k < 256; k += blockDim.x) s_lo[k] = 0u;
+        __syncthreads();
+    }
     // MODE 1: the range [kmin, kmax] of the visible depth keys, so the depth
     // sort ranks keys relative to kmin and skips the passes above its width
     uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
@@ -284,6 +291,7 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
         kmin = min(kmin, dkey);
         kmax = max(kmax, dkey);
     }
+    if (MODE == 1) warp_hist_add(s_lo, dkey & 255u, dkey != 0xFFFFFFFFu);
     }  // grid-stride
     if (MODE == 1) {  // one atomic pair per warp (meta[5] / meta[6], reset by frame_init_kernel)
         kmin = __reduce_min_sync(0xffffffffu, kmin);
@@ -292,6 +300,9 @@ __global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
             atomicMin(reinterpret_cast<unsigned long long*>(status) + 5, (unsigned long long)kmin);
             atomicMax(reinterpret_cast<unsigned long long*>(status) + 6, (unsigned long long)kmax);
         }
+        __syncthreads();
+        for (int k = threadIdx.x; k < 256; k += blockDim.x)
+            if (s_lo[k]) atomicAdd(&dhist[k], s_lo[k]);
     }
 }
 
@@ -638,7 +649,7 @@ __global__ void __launch_bounds__(256) frame_init_kernel(unsigned long long* __r
             }
             meta[5] = 0xFFFFFFFFull;  // visible depth-key range (depth-first binning)
             meta[6] = 0ull;
-            meta[7] = 0ull;           // visible Gaussians (depth_hist_kernel)
+            meta[7] = 0ull;           // visible Gaussians (the depth sort's first pass)
             meta[8] = 4ull;           // depth-sort passes
         }
         for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) dhist[k] = 0u;
@@ -877,7 +888,9 @@ __global__ void __launch_bounds__(256, 4) views_project_fwd_kernel(const float* 
     const int nv = a.nv;
     for (int v = 0; v < nv; ++v) run_zero_jobs(a.v[v].zj);
     __shared__ uint32_t s_kmin[MV_MAX], s_kmax[MV_MAX];
+    __shared__ uint32_t s_lo[MV_MAX][256];  // per view: the visible keys' low-byte histogram (sort.cu)
     for (int v = threadIdx.x; v < MV_MAX; v += blockDim.x) s_kmin[v] = 0xFFFFFFFFu, s_kmax[v] = 0u;
+    for (int k = threadIdx.x; k < MV_MAX * 256; k += blockDim.x) (&s_lo[0][0])[k] = 0u;
     __syncthreads();
     const int n_round = (n + 31) & ~31;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += gridDim.x * blockDim.x) {
@@ -914,6 +927,7 @@ __global__ void __launch_bounds__(256, 4) views_project_fwd_kernel(const float* 
                 dkey = nt ? __float_as_uint(tz) : 0xFFFFFFFFu;
                 V.dkeys[i] = dkey;
             }
+            warp_hist_add(s_lo[v], dkey & 255u, dkey != 0xFFFFFFFFu);
             const uint32_t kmin = __reduce_min_sync(0xffffffffu, dkey);
             const uint32_t kmax = __reduce_max_sync(0xffffffffu, dkey != 0xFFFFFFFFu ? dkey : 0u);
             if ((threadIdx.x & 31) == 0 && kmin != 0xFFFFFFFFu) {
@@ -928,6 +942,10 @@ __global__ void __launch_bounds__(256, 4) views_project_fwd_kernel(const float* 
             atomicMin(a.v[v].meta + 5, (unsigned long long)s_kmin[v]);
             atomicMax(a.v[v].meta + 6, (unsigned long long)s_kmax[v]);
         }
+    for (int k = threadIdx.x; k < nv * 256; k += blockDim.x) {
+        const uint32_t c = (&s_lo[0][0])[k];
+        if (c) atomicAdd(&a.v[k >> 8].dhist[k & 255], c);
+    }
 }
 
 int launch_views_project_fwd(const float* means3, const float* scales3, const float* quats4, const float* opac,

@@ -52,7 +52,8 @@ constexpr int sort_tile() { return SORT_THREADS * ITEMS; }
 template <typename K, int ITEMS>
 constexpr size_t sort_smem() {
     return (size_t)sort_tile<K, ITEMS>() * (sizeof(K) + 4) + (size_t)SORT_WARPS * RADIX * 4 + 2 * RADIX * 4 +
-           (size_t)SORT_WARPS * 2 * RADIX * 4;  // peer-mask banks (RANK_OR)
+           (size_t)SORT_WARPS * 2 * RADIX * 4 +  // peer-mask banks (RANK_OR)
+           RADIX * 4;                            // the next digit's histogram (depth sort)
 }
 
 // look-back status words: GPU-scope relaxed accesses (flag and value share
@@ -124,12 +125,21 @@ constexpr int sort_minb() {
 // *rel_min and 0xFFFFFFFF keys (culled Gaussians) are dropped -- the output
 // holds only the valid items, in order.  npass_dev: the pass is skipped
 // entirely when `pass` >= *npass_dev (the relative keys are narrower).
+// The depth sort has no histogram kernel: pass 0's digit histogram is the
+// projection's histogram of the visible keys' ABSOLUTE low byte, rotated by
+// the minimum's low byte ((key - min) mod 256 = (key mod 256 - min mod 256)
+// mod 256); pass 0 also writes the pass count (meta[8], from the key range
+// meta[5..6] = rel_min[0..1]) and the visible count (meta[7] = the
+// histogram's total), and every pass adds the next digit's histogram of its
+// keys into next_hist (the passes are latency-bound: the extra shared
+// atomics are nearly free).
 template <typename K, int ITEMS, bool RANK_OR>
 __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) onesweep_kernel(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_cap, const unsigned long long* __restrict__ n_dev, int shift,
     const uint32_t* __restrict__ hist, uint32_t* __restrict__ status, uint32_t* __restrict__ counter,
-    const unsigned long long* __restrict__ rel_min, const unsigned long long* __restrict__ npass_dev, int pass) {
+    const unsigned long long* __restrict__ rel_min, const unsigned long long* __restrict__ npass_dev, int pass,
+    uint32_t* __restrict__ next_hist, unsigned long long* __restrict__ meta_out) {
     griddep_wait();
     if (npass_dev && pass >= (int)*npass_dev) return;
     constexpr int TILE_N = sort_tile<K, ITEMS>();
@@ -140,6 +150,7 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
     uint32_t* s_gbase = s_whist + SORT_WARPS * RADIX;  // global dst of local slot 0 per digit
     uint32_t* s_lstart = s_gbase + RADIX;              // local start of each digit in the tile
     uint32_t* s_peers = s_lstart + RADIX;              // [warp][2][digit] peer masks (RANK_OR)
+    uint32_t* s_next = s_peers + SORT_WARPS * 2 * RADIX;  // [digit] next digit's counts (next_hist)
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_tmp[SORT_WARPS];
     __shared__ uint32_t s_total;
@@ -153,6 +164,7 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
 #pragma unroll
         for (int k = 0; k < 2 * SORT_WARPS; ++k) s_peers[k * RADIX + tid] = 0;
     }
+    if (next_hist) s_next[tid] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
     if ((int64_t)tile * TILE_N >= n) return;  // capacity-sized grid, fewer items this frame
@@ -174,6 +186,11 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
             key[i] -= kmin;
         }
         okm |= ok ? (1u << i) : 0u;
+    }
+    if (next_hist) {  // the next pass's digit of this tile's keys
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+            warp_hist_add(s_next, (uint32_t)(key[i] >> (shift + 8)) & 255u, (okm >> i) & 1u);
     }
     // warp-local stable ranking: items in (i, lane) order = input order
     const uint32_t lt = lanemask_lt();
@@ -250,9 +267,16 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
         }
         stv(st, ST_PRE | (excl + run));
     }
-    const uint32_t h = hist[d];
+    // depth sort pass 0: the projection's absolute low-byte histogram, rotated
+    const uint32_t h = rel_min ? hist[(d + (uint32_t)*rel_min) & 255u] : hist[d];
     const uint32_t lincl = block_incl_scan256(run, s_tmp);
     const uint32_t hincl = block_incl_scan256(h, s_tmp);
+    if (meta_out && tile == 0 && d == RADIX - 1) {  // visible count and pass count (read by the later kernels)
+        const uint32_t kmin = (uint32_t)rel_min[0], kmax = (uint32_t)rel_min[1];
+        const uint32_t range = kmin <= kmax ? kmax - kmin : 0u;
+        meta_out[7] = (unsigned long long)hincl;
+        meta_out[8] = (unsigned long long)(range == 0u ? 1 : (32 - __clz((int)range) + 7) / 8);
+    }
     const uint32_t lstart = lincl - run;
     if (d == RADIX - 1) s_total = lincl;  // valid items of the tile
     s_lstart[d] = lstart;
@@ -275,6 +299,10 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
         const uint32_t dst = s_gbase[dd] + (uint32_t)j;
         kout[dst] = k;
         vout[dst] = s_vals[j];
+    }
+    if (next_hist) {
+        const uint32_t c = s_next[tid];  // (the scatter loop's barrier ordered the counts)
+        if (c) atomicAdd(&next_hist[tid], c);
     }
 }
 
@@ -329,6 +357,8 @@ struct PassOpts {  // depth sort: pass 0 relative + compacting, later passes on 
     const unsigned long long* n_dev_rest = nullptr;
     const unsigned long long* rel_min0 = nullptr;
     const unsigned long long* npass_dev = nullptr;
+    bool next_hist = false;             // every pass but the last adds the next digit's histogram
+    unsigned long long* meta = nullptr;  // pass 0 writes meta[7] (visible) and meta[8] (passes)
 };
 
 template <typename K, int ITEMS, bool RANK_OR>
@@ -346,7 +376,9 @@ static int run_passes_t(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap,
                  sort_smem<K, ITEMS>(), s, (const K*)kin, (const uint32_t*)((p == 0 && identity_vals) ? nullptr : vin),
                  kout, vout, n_cap, (p > 0 && po.n_dev_rest) ? po.n_dev_rest : n_dev, 8 * p,
                  (const uint32_t*)(hist + p * RADIX), status + (size_t)p * tiles * RADIX, counters + p,
-                 p == 0 ? po.rel_min0 : nullptr, po.npass_dev, p);
+                 p == 0 ? po.rel_min0 : nullptr, po.npass_dev, p,
+                 po.next_hist && p + 1 < passes ? const_cast<uint32_t*>(hist) + (p + 1) * RADIX : nullptr,
+                 p == 0 ? po.meta : nullptr);
         if (check_launch("onesweep_kernel")) return -1;
         K* tk = kin; kin = kout; kout = tk;
         uint32_t* tv = vin; vin = vout; vout = tv;
@@ -405,75 +437,18 @@ template int run_onesweep<unsigned long long>(unsigned long long*, uint32_t*, un
                                               int64_t, const unsigned long long*, int, const uint32_t*,
                                               uint32_t*, uint32_t*, cudaStream_t, bool);
 
-// Digit histograms of the visible Gaussians' depth keys relative to the
-// visible minimum (meta[5]; culled keys are 0xFFFFFFFF), their count V
-// (meta[7], reset by frame_init_kernel) and the number of 8-bit passes the
-// relative keys need (meta[8]: the width of meta[6] - meta[5]).
-__global__ void __launch_bounds__(256) depth_hist_kernel(const uint32_t* __restrict__ keys, int64_t n,
-                                                         unsigned long long* __restrict__ meta,
-                                                         uint32_t* __restrict__ hist) {
-    griddep_wait();
-    __shared__ uint32_t sh[4 * RADIX];
-    __shared__ uint32_t s_cnt;
-    for (int k = threadIdx.x; k < 4 * RADIX; k += blockDim.x) sh[k] = 0;
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    const uint32_t kmin = (uint32_t)meta[5], kmax = (uint32_t)meta[6];
-    const uint32_t range = kmin <= kmax ? kmax - kmin : 0u;
-    const int npass = range == 0u ? 1 : (32 - __clz((int)range) + 7) / 8;
-    // 8 keys per thread per round (two 16-byte loads in flight): the loop is
-    // latency-bound with one key per load (33 us at config 3 -> ~10 us)
-    constexpr int KPT = 8;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * KPT;
-    const int64_t n_round = (n + 32 * KPT - 1) / (32 * KPT) * (32 * KPT);
-    uint32_t cnt = 0;
-    for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * KPT; base < n_round; base += stride) {
-        uint32_t kk[KPT];
-        if (base + KPT <= n) {
-            const uint4 a = *reinterpret_cast<const uint4*>(keys + base);
-            const uint4 b = *reinterpret_cast<const uint4*>(keys + base + 4);
-            kk[0] = a.x; kk[1] = a.y; kk[2] = a.z; kk[3] = a.w; kk[4] = b.x; kk[5] = b.y; kk[6] = b.z; kk[7] = b.w;
-        } else {
-#pragma unroll
-            for (int j = 0; j < KPT; ++j) kk[j] = base + j < n ? keys[base + j] : 0xFFFFFFFFu;
-        }
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) {
-            const uint32_t key = kk[j];
-            const bool valid = key != 0xFFFFFFFFu;
-            const uint32_t rel = key - kmin;
-            cnt += valid;
-            warp_hist_add(sh, rel & 255u, valid);
-            warp_hist_add(sh + RADIX, (rel >> 8) & 255u, valid);
-            if (npass > 2) warp_hist_add(sh + 2 * RADIX, (rel >> 16) & 255u, valid);
-            if (npass > 3) warp_hist_add(sh + 3 * RADIX, rel >> 24, valid);
-        }
-    }
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_cnt, cnt);
-    __syncthreads();
-    for (int k = threadIdx.x; k < 4 * RADIX; k += blockDim.x) {
-        const uint32_t v = sh[k];
-        if (v) atomicAdd(&hist[k], v);
-    }
-    if (threadIdx.x == 0) {
-        if (s_cnt) atomicAdd(&meta[7], (unsigned long long)s_cnt);
-        if (blockIdx.x == 0) meta[8] = (unsigned long long)npass;
-    }
-}
-
+// Stable sort of the visible Gaussians by depth (frame.cu): hist holds the
+// projection's histogram of the visible keys' absolute low byte (rows 1-3
+// zeroed; the passes fill them in turn), meta[5..6] the key range.
 int run_depth_sort(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t n_cap,
                    unsigned long long* meta, uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s) {
     if (n_cap <= 0) return 0;
-    int64_t hb = (n_cap + 256 * 8 - 1) / (256 * 8);
-    const int64_t lim = (int64_t)sort_sm_count() * 4;
-    if (hb > lim) hb = lim;
-    launch_k(depth_hist_kernel, dim3((unsigned)hb), dim3(256), 0, s, (const uint32_t*)k0, n_cap, meta, hist);
-    if (check_launch("depth_hist_kernel")) return -1;
     PassOpts po;
     po.n_dev_rest = meta + 7;
     po.rel_min0 = meta + 5;
     po.npass_dev = meta + 8;
+    po.next_hist = true;
+    po.meta = meta;
     constexpr int BIG = SortCfg<uint32_t>::ITEMS;
     const int64_t big_tiles = (n_cap + sort_tile<uint32_t, BIG>() - 1) / sort_tile<uint32_t, BIG>();
     if (big_tiles < 64)
