@@ -49,10 +49,16 @@ constexpr int SMALL_ITEMS = 4;
 template <typename K, int ITEMS>
 constexpr int sort_tile() { return SORT_THREADS * ITEMS; }
 
+// The peer-mask banks (ranking) and the key / value staging (scatter) are
+// live at different times: they share memory when the staging is the larger.
+template <typename K, int ITEMS>
+constexpr bool sort_peers_alias() {
+    return (size_t)sort_tile<K, ITEMS>() * (sizeof(K) + 4) >= (size_t)SORT_WARPS * 2 * RADIX * 4;
+}
 template <typename K, int ITEMS>
 constexpr size_t sort_smem() {
     return (size_t)sort_tile<K, ITEMS>() * (sizeof(K) + 4) + (size_t)SORT_WARPS * RADIX * 4 + 2 * RADIX * 4 +
-           (size_t)SORT_WARPS * 2 * RADIX * 4 +  // peer-mask banks (RANK_OR)
+           (sort_peers_alias<K, ITEMS>() ? 0 : (size_t)SORT_WARPS * 2 * RADIX * 4) +  // peer-mask banks (RANK_OR)
            RADIX * 4;                            // the next digit's histogram (depth sort)
 }
 
@@ -118,6 +124,11 @@ __device__ __forceinline__ uint32_t block_incl_scan256(uint32_t v, uint32_t* s_t
 // One 8-bit pass.  vin == nullptr means value = input index (identity).
 template <typename K, int ITEMS>
 constexpr int sort_minb() {
+#ifndef GS_SORT_MINB16
+#define GS_SORT_MINB16 4  // 64 registers (a 12-byte spill): with the peer masks over the staging (43 KB of
+                          // shared memory) 4 CTAs per SM -- config 3 depth sort 4.16 -> 3.75 ms per step
+#endif
+    if (sizeof(K) == 4 && ITEMS == 16) return GS_SORT_MINB16;
     return sizeof(K) == 4 ? (ITEMS <= 8 ? 5 : (ITEMS <= 12 ? 4 : (ITEMS <= 16 ? 3 : 2))) : 2;
 }
 
@@ -149,8 +160,10 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
     uint32_t* s_whist = s_vals + TILE_N;               // [warp][digit]
     uint32_t* s_gbase = s_whist + SORT_WARPS * RADIX;  // global dst of local slot 0 per digit
     uint32_t* s_lstart = s_gbase + RADIX;              // local start of each digit in the tile
-    uint32_t* s_peers = s_lstart + RADIX;              // [warp][2][digit] peer masks (RANK_OR)
-    uint32_t* s_next = s_peers + SORT_WARPS * 2 * RADIX;  // [digit] next digit's counts (next_hist)
+    constexpr bool ALIAS = sort_peers_alias<K, ITEMS>();
+    // [warp][2][digit] peer masks (RANK_OR), over the staging when it is the larger
+    uint32_t* s_peers = ALIAS ? reinterpret_cast<uint32_t*>(smem) : s_lstart + RADIX;
+    uint32_t* s_next = ALIAS ? s_lstart + RADIX : s_peers + SORT_WARPS * 2 * RADIX;  // [digit] next digit's counts
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_tmp[SORT_WARPS];
     __shared__ uint32_t s_total;
