@@ -302,8 +302,9 @@ int gs_frame_project_backward(const float* means3, const float* scales3, const f
  * over the views, and d_views16 (n_views x 16, flag bit 4: added) per view.
  * A Gaussian counts as visible in a view iff its rows there are non-zero (a
  * culled one's rows are never written; zero rows contribute exactly zero).
- * The rows read are cleared and each workspace stamped clean unless flag bit
- * 1 keeps them.  cams / capacities / workspaces / ws_bytes: [host] n_views
+ * The rows read are cleared unless flag bit 1 keeps them; the call whose
+ * range ends at n stamps each workspace clean (its rows all cleared: calls
+ * over earlier ranges must not keep theirs) or, keeping, not clean.  cams / capacities / workspaces / ws_bytes: [host] n_views
  * entries, as given to each view's gs_frame_forward.  Against
  * gs_frame_backward per view it moves ~76 instead of ~224 bytes per visible
  * Gaussian and view (parameters read once, sums written once). */

@@ -489,7 +489,10 @@ int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* 
 #define GS_ET_MINB 2  // resident emission CTAs per SM the registers are budgeted for
 #endif
 constexpr int ET_WARPS = GS_ET_WARPS;
-constexpr int ET_ROUNDS = 8;  // 32-Gaussian rounds per warp (<= 256 Gaussians per warp: u16 counts)
+#ifndef GS_ET_ROUNDS
+#define GS_ET_ROUNDS 8
+#endif
+constexpr int ET_ROUNDS = GS_ET_ROUNDS;  // 32-Gaussian rounds per warp (u16 counts and offsets)
 constexpr int ET_THREADS = ET_WARPS * 32;
 constexpr int ET_CHUNK = ET_THREADS * ET_ROUNDS;  // Gaussians per chunk (2048: u16 chunk counts)
 

@@ -578,7 +578,9 @@ int gs_frame_views_project_backward(const float* means3, const float* scales3, c
             V.g8 = at<float4>(ws, L.d_geo) + 2 * begin;
             V.d_c11 = at<float>(ws, L.d_c11) + begin;
             V.partials = at<float>(ws, L.partials);
-            V.clean_word = at<unsigned long long>(ws, L.clean);
+            // the call whose range ends at n declares the workspace's rows clear (the
+            // earlier ranges' calls cleared theirs) or, keeping its rows, dirty
+            V.clean_word = end == n ? at<unsigned long long>(ws, L.clean) : nullptr;
             V.clean_stamp = keep ? 0ull : clean_sig(n, capacities[v0 + j], c.width, c.height);
         }
         if (launch_views_project_bwd(means3 + 3 * begin, scales3 + 3 * begin, quats4 + 4 * begin, end - begin, a,

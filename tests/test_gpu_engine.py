@@ -233,6 +233,56 @@ def test_frames_project_equals_per_view_projection(cuda):
     assert errs > 0
 
 
+def test_batched_projections_over_32_views(cuda):
+    """More views than one batched launch takes (MV_MAX = 32): both batched
+    projections loop over groups of views -- forward bit for bit the per-view
+    frames, backward the per-view sums; Gaussian ranges (the bucketed
+    multi-GPU path) add up to the whole."""
+    from paper_2312_02121_b200 import ops
+    from paper_2312_02121_b200.scenes import make_config
+    spec = make_config(3, n_override=420_000, n_views=32)  # > 400k Gaussians: depth-first views
+    params = [torch.as_tensor(a, device=cuda) for a in (spec.means, spec.scales, spec.quats, spec.opacities,
+                                                        spec.colors)]
+    m, s, q, o, c = params
+    n = spec.n
+    # small views (1/4 scale) keep the 36 workspaces cheap; 4 more views turned off the ring's first
+    cams = []
+    for cs in spec.cameras:
+        cp = ops.CameraParams.of(cs)
+        cams.append(ops.CameraParams(cp.view, cp.fx / 4, cp.fy / 4, cp.cx / 4, cp.cy / 4, cp.width // 4,
+                                     cp.height // 4, cp.near, cp.far))
+    cams += _views(ops, cams[0], (0.05, 0.1, -0.05, -0.1))
+    assert ops.frames_projectable(n, cams)
+    rng = np.random.default_rng(9)
+    d_imgs = [torch.as_tensor(rng.normal(size=(cm.height, cm.width, 3)).astype(np.float32), device=cuda)
+              for cm in cams]
+    refs = [ops.frame_forward(*params, cm, (0.0, 0.0, 0.0), True) for cm in cams]
+    caps = [r.capacity for r in refs]
+    wss = [ops.frame_workspace(n, cap, cm.width, cm.height, cuda) for cap, cm in zip(caps, cams)]
+    ops.frames_project(m, s, q, o, cams, caps, wss)
+    frames = []
+    for r, cm, cap, ws, d in zip(refs, cams, caps, wss, d_imgs):
+        fr = ops.frame_forward(*params, cm, (0.0, 0.0, 0.0), True, capacity=cap, ws=ws, check_meta=False,
+                               projected=True)
+        assert torch.equal(fr.image, r.image)
+        ops.frame_backward(fr, m, s, q, c, d, project=False)
+        frames.append(fr)
+    ref = {k: torch.zeros((n, w), device=cuda) for k, w in (("d_mean", 3), ("d_scale", 3), ("d_quat", 4),
+                                                             ("d_rgbo", 4))}
+    for r, d in zip(refs, d_imgs):
+        gv = ops.frame_backward(r, m, s, q, c, d)
+        for k in ref:
+            ref[k] += gv[k]
+    out = {k: torch.zeros_like(v) for k, v in ref.items()}
+    d_views = torch.zeros((len(cams), 4, 4), device=cuda)
+    half = n // 2 // 256 * 256
+    ops.frame_views_project_backward(frames, m, s, q, out, d_views, 0, half)
+    ops.frame_views_project_backward(frames, m, s, q, out, d_views, half, n, add_view=True)
+    for k in ref:
+        a, b = out[k].cpu().double().numpy(), ref[k].cpu().double().numpy()
+        assert np.abs(a - b).max() <= 1e-4 * (np.abs(b).max() + 1e-30), k
+
+
 def test_batched_and_per_view_engine_agree(cuda):
     """RenderStep with the batched projection backward (default for several
     views) and with one projection backward per view give the same step."""
