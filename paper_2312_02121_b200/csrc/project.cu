@@ -145,11 +145,14 @@ __device__ __forceinline__ void proj_fwd_core(const CamK& cam, int i, float tx, 
 #ifndef DIRECT_UNROLL
 #define DIRECT_UNROLL 4  // slot atomics in flight per lane (direct binning)
 #endif
-template <int MODE>
 #ifndef PFWD_MINB
 #define PFWD_MINB 8  // 32 registers, 8 resident CTAs per SM (config 4 projection 165 -> 160 us)
 #endif
-__global__ void __launch_bounds__(256, PFWD_MINB) project_fwd_kernel(
+// MODE 1 also histograms the depth keys' low byte: 40 registers (6 CTAs per
+// SM) instead of a spill at 32
+constexpr int pfwd_minb(int mode) { return mode == 1 ? 6 : PFWD_MINB; }
+template <int MODE>
+__global__ void __launch_bounds__(256, pfwd_minb(MODE)) project_fwd_kernel(
     const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats,
     const float* __restrict__ opac, int n, CamK cam, float4* __restrict__ xydr, float4* __restrict__ conic,
     uint32_t* __restrict__ tiles, float* __restrict__ cov_out, unsigned long long* __restrict__ status,
@@ -670,7 +673,7 @@ int launch_project_fwd_dkey(const float* means3, const float* scales3, const flo
     if (check_launch("frame_init_kernel")) return -1;
     int64_t blocks = (n + 255) / 256;
     if (blocks < 1) blocks = 1;  // the zero jobs run even for an empty scene
-    const int64_t cap = (int64_t)sort_sm_count() * PFWD_MINB;  // resident CTAs of 256 threads
+    const int64_t cap = (int64_t)sort_sm_count() * (tcount ? PFWD_MINB : pfwd_minb(1));  // resident CTAs
     if (blocks > cap) blocks = cap;
     if (tcount && bins)
         launch_k(project_fwd_kernel<3>, dim3((unsigned)blocks), dim3(256), 0, s, means3, scales3,
