@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true")
-    p.add_argument("--streams", type=int, default=4, help="streams the views of a multi-view step alternate on")
+    p.add_argument("--streams", type=int, default=16, help="streams the views of a multi-view step alternate on")
     return p.parse_args()
 
 

@@ -96,7 +96,7 @@ def unpack(flat: torch.Tensor, n: int) -> dict:
 
 class RenderStep:
     def __init__(self, n: int, cams, background=(0.0, 0.0, 0.0), early_termination=True, device=None,
-                 headroom: float = 1.05, buffers: int = 2, view_streams: int = 4, reducer=None,
+                 headroom: float = 1.05, buffers: int = 2, view_streams: int = 16, reducer=None,
                  batched_projection: bool = True):
         """reducer: a dist.GradReducer -- the step's gradients are summed over
         the ranks of its process group, the all-reduce overlapped with the
@@ -129,8 +129,9 @@ class RenderStep:
                 graph=None))
         self.caps = None
         self.wss = None
-        # further view streams (multi-view steps): with the batched projections, config 3 measured
-        # 2: 1236, 3: 1256, 4: 1275, 6: 1280 frames/s (bench.py --streams); 4 by default
+        # further view streams (multi-view steps): with the batched projections the views are
+        # independent; config 3 measured 2: 1236, 3: 1256, 4: 1274, 6: 1298, 8: 1306, 16: 1313,
+        # 32: 1306 frames/s (bench.py --streams); 16 by default
         self.aux = [torch.cuda.Stream(self.dev) for _ in range(max(0, min(view_streams, len(self.cams)) - 1))]
 
     # -------------------------------------------------------------- set-up
