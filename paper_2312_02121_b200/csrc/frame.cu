@@ -108,7 +108,6 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.tkeys_alt = take(4 * cap);
     L.tvals = take(4 * cap);
     L.tvals_alt = take(4 * cap);
-    L.ranges = take(8 * nt);
     L.rec = take(8 * 4 * cap);    // forward commit records, 4 warp regions per tile list
     L.rec_count = take(16 * nt);  // records per (tile, warp)
     L.tile_order = take(4 * nt);  // raster launch order (heaviest lists first)
@@ -121,9 +120,10 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.thist = take(4 * 256 * 2);
     L.counters = take(64);
     L.scan_ws = take(emit_scan_ws_bytes(n));
-    L.dstatus = take(onesweep_status_bytes<uint32_t>(n, 4));
-    L.tstatus = take(onesweep_status_bytes<uint32_t>(cap, tp));
+    L.ranges = take(8 * nt);
+    L.dstatus = take(onesweep_status_bytes<uint32_t>(n, 4));  // sized for either pass variant; the used part is zeroed
     L.zero_end = o;
+    L.tstatus = take(onesweep_status_bytes<uint32_t>(cap, tp));  // tile passes (depth-first without the tile emission)
     L.etable = take(emit_tiles_fits((int)nt) ? emit_tiles_table_bytes(n, (int)nt) : 0);
     L.d_geo = take(32 * n);  // interleaved screen-space gradients: [d_rgbo 4 | d_geo 4] per Gaussian
     L.d_c11 = take(4 * n);
@@ -162,15 +162,17 @@ unsigned long long clean_sig(int64_t n, int64_t cap, int W, int H) {
 }
 
 // Buffers the frame's projection clears for the later stages (no memset
-// nodes): the zeroed region (minus the tile passes' look-back status under the
-// tile-sorted emission), the tile ranges and -- only when the workspace is not
-// known clean (meta[4]) -- the backward's screen-space accumulators.
-ZeroJobs frame_zero_jobs(const Layout& L, void* ws, int n_tiles, bool etiles) {
+// nodes): the counters, tile ranges and the part of the depth sort's
+// look-back status its pass variant uses; the tile passes' status only for
+// the depth-first binning without the tile-sorted emission; and -- only when
+// the workspace is not known clean (meta[4]) -- the backward's screen-space
+// accumulators.
+ZeroJobs frame_zero_jobs(const Layout& L, void* ws, int64_t n, int n_tiles, bool tile_passes) {
     ZeroJobs zj;
     zj.p[0] = at<uint4>(ws, L.thist);
-    zj.n16[0] = ((etiles ? L.tstatus : L.zero_end) - L.thist) / 16;
-    zj.p[1] = at<uint4>(ws, L.ranges);
-    zj.n16[1] = (8 * (size_t)n_tiles + 15) / 16;
+    zj.n16[0] = (L.dstatus + depth_sort_status_bytes(n) - L.thist + 15) / 16;
+    zj.p[1] = at<uint4>(ws, L.tstatus);
+    zj.n16[1] = tile_passes ? (L.etable - L.tstatus) / 16 : 0;
     zj.p[2] = at<uint4>(ws, L.d_geo);
     zj.n16[2] = (L.partials - L.d_geo) / 16;
     zj.cond2 = at<unsigned long long>(ws, L.meta) + 4;
@@ -290,7 +292,7 @@ int gs_frames_project(const float* means3, const float* scales3, const float* qu
             V.meta = at<unsigned long long>(ws, L.meta);
             V.clean_word = at<unsigned long long>(ws, L.clean);
             V.clean_sig = clean_sig(n, capacities[v0 + j], c.width, c.height);
-            V.zj = frame_zero_jobs(L, ws, nt, uses_tile_emit(n, nt));
+            V.zj = frame_zero_jobs(L, ws, n, nt, !uses_tile_emit(n, nt));
         }
         if (launch_views_project_fwd(means3, scales3, quats4, opacities, n, a, s)) return -1;
     }
@@ -332,7 +334,7 @@ int frame_forward_impl(const float* means3, const float* scales3, const float* q
     const Binning binning = binning_for(n, n_tiles);
     // depth-first binning with the tile-sorted emission (no global sort by tile)
     const bool etiles = uses_tile_emit(n, n_tiles);
-    const ZeroJobs zj = frame_zero_jobs(L, ws, n_tiles, etiles);
+    const ZeroJobs zj = frame_zero_jobs(L, ws, n, n_tiles, binning == DEPTH_FIRST && !etiles);
     const bool scatter = binning == SCATTER;
     const bool direct = binning == DIRECT && counts4 == nullptr;  // the counted pass bins by scatter
     const int64_t kstride = direct_stride(isect_capacity, n_tiles);

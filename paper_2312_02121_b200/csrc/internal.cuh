@@ -77,6 +77,7 @@ int launch_views_project_bwd(const float* means3, const float* scales3, const fl
 int sort_sm_count();
 template <typename K>
 size_t onesweep_status_bytes(int64_t n_cap, int passes);
+size_t depth_sort_status_bytes(int64_t n);  // the part of onesweep_status_bytes(n, 4) the depth sort uses
 template <typename K>
 int run_onesweep(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n_cap, const unsigned long long* n_dev,
                  int passes, const uint32_t* hist, uint32_t* status, uint32_t* counters, cudaStream_t s,

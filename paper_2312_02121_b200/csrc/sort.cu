@@ -450,6 +450,15 @@ template int run_onesweep<unsigned long long>(unsigned long long*, uint32_t*, un
                                               int64_t, const unsigned long long*, int, const uint32_t*,
                                               uint32_t*, uint32_t*, cudaStream_t, bool);
 
+// Look-back status the depth sort of n keys uses (its pass variant, 4 passes).
+size_t depth_sort_status_bytes(int64_t n) {
+    constexpr int BIG = SortCfg<uint32_t>::ITEMS;
+    const int64_t big_tiles = (n + sort_tile<uint32_t, BIG>() - 1) / sort_tile<uint32_t, BIG>();
+    const int items = big_tiles < 64 ? SMALL_ITEMS : BIG;
+    const int64_t tiles = (n + (int64_t)SORT_THREADS * items - 1) / ((int64_t)SORT_THREADS * items);
+    return (size_t)4 * (size_t)(tiles > 0 ? tiles : 1) * RADIX * 4;
+}
+
 // Stable sort of the visible Gaussians by depth (frame.cu): hist holds the
 // projection's histogram of the visible keys' absolute low byte (rows 1-3
 // zeroed; the passes fill them in turn), meta[5..6] the key range.
