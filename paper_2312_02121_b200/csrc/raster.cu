@@ -980,6 +980,10 @@ static int fwd_regions() {
     return v;
 }
 
+#ifndef GS_FWD_FRAME_MINB
+#define GS_FWD_FRAME_MINB 9  // resident forward CTAs per SM the frame path's registers are budgeted for
+#endif
+
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
                       unsigned long long* counts, cudaStream_t s, uint2* rec, uint32_t* rec_count,
@@ -999,7 +1003,7 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
     // frame path: 8x8 quadrants with commit records, 9 CTAs/SM (measured best
     // against 8 and 10), optionally with the per-tile sort fused in front
 #define GS_FWD_M(ET, SORT)                                                                                     \
-    launch_k(raster_fwd_kernel<4, ET, false, true, 9, SORT>, dim3(nt), dim3(128), 0, s, ranges, vals, g, q,   \
+    launch_k(raster_fwd_kernel<4, ET, false, true, GS_FWD_FRAME_MINB, SORT>, dim3(nt), dim3(128), 0, s, ranges, vals, g, q,   \
              colors3, bg, W, H, tiles_x, img, T, nc, counts, rec, rec_count, tile_order, dkeys, sort_alt,        \
              direct_counts, kstride, meta)
     if (dkeys && !(rec && !cnt)) return set_error("raster_fwd: the fused tile sort needs the frame path");
