@@ -196,10 +196,18 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    # GS_BENCH_SHARED_GPU=1: a functional test of the N-rank path on fewer GPUs (ranks share
+    # devices, gloo reductions on the host; the numbers mean nothing)
+    shared = os.environ.get("GS_BENCH_SHARED_GPU") == "1" and world > torch.cuda.device_count()
+    if shared:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = args.config
     spec = make_config(cfg)
     views = views_for(cfg, spec, world, rank)
