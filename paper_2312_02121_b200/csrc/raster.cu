@@ -24,6 +24,7 @@
 // Retired pixels (forward: out of the image or early-terminated) get
 // py = +inf, so sigma is inf/NaN and fails the cut.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.cuh"
@@ -32,7 +33,12 @@
 namespace gs {
 
 constexpr int NW = 4;    // warps (quadrants, forward)
-constexpr int RB = 128;  // splats per staged batch
+#ifndef GS_RB
+#define GS_RB 128
+#endif
+constexpr int RB = GS_RB;  // splats per staged batch (A/B knob: 128 or 256)
+// compacted-list entry index (the sentinel is RB)
+using ListIdx = std::conditional_t<(RB < 255), uint8_t, uint16_t>;
 
 // Warp regions: NWR = 4 -> four 8x8 quadrants (one pixel pair per lane);
 // NWR = 2 -> two 8-column x 16-row halves (two pixel pairs per lane).
@@ -45,7 +51,7 @@ struct BatchT {
         float4 a, b, c;
     } e[RB + 1];
     uint32_t mask[NWR][RB / 32];  // region reach bits per group of 32 entries
-    __align__(4) uint8_t list[NWR][RB + 2];  // compacted entry indices per region (+ sentinel pad)
+    __align__(4) ListIdx list[NWR][RB + 2];  // compacted entry indices per region (+ sentinel pad)
     uint8_t rbuf[NWR][RB];                   // forward records of this batch (entry indices, per region)
 };
 using Batch = BatchT<NW>;
@@ -155,10 +161,10 @@ __device__ __forceinline__ int stage_batch(BatchT<NWR>& s, int tile, int tiles_x
 #pragma unroll
     for (int j = 0; j < RB / 32; ++j) {
         const uint32_t m = s.mask[warp][j];
-        if ((m >> lane) & 1u) s.list[warp][n + __popc(m & lt)] = (uint8_t)(32 * j + lane);
+        if ((m >> lane) & 1u) s.list[warp][n + __popc(m & lt)] = (ListIdx)(32 * j + lane);
         n += __popc(m);
     }
-    if (lane == 0) s.list[warp][n] = (uint8_t)RB;  // pad odd lists with the sentinel
+    if (lane == 0) s.list[warp][n] = (ListIdx)RB;  // pad odd lists with the sentinel
     __syncwarp();
     return n;
 }
@@ -321,11 +327,13 @@ __device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uin
         if (__all_sync(0xffffffffu, all_done())) continue;  // whole warp finished: only help staging
         const int pos_base = b0 - start + 1;
         if constexpr (NPR == 1) {
-            const uint16_t* lst2 = reinterpret_cast<const uint16_t*>(s.list[warp]);
+            using Pair = std::conditional_t<sizeof(ListIdx) == 1, uint16_t, uint32_t>;
+            constexpr int IB = 8 * sizeof(ListIdx);
+            const Pair* lst2 = reinterpret_cast<const Pair*>(s.list[warp]);
 #pragma unroll 1
             for (int i = 0; i < n; i += 2) {
                 const uint32_t kk = lst2[i >> 1];
-                const int k0 = kk & 0xffu, k1 = kk >> 8;  // k1 may be the sentinel
+                const int k0 = kk & ((1u << IB) - 1u), k1 = kk >> IB;  // k1 may be the sentinel
                 const float4 a0 = s.e[k0].a, a1 = s.e[k1].a;
                 const float hC0 = s.e[k0].b.x, hC1 = s.e[k1].b.x;
                 const float dx0 = __fsub_rn(px, a0.x), dx1 = __fsub_rn(px, a1.x);
@@ -351,7 +359,7 @@ __device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uin
             }
             if (REC) fwd_record_flush(s, warp, lane, rcur, rbuf_w, rp, pos_base - 1);
         } else {
-            const uint8_t* lst = s.list[warp];
+            const ListIdx* lst = s.list[warp];
 #pragma unroll 1
             for (int i = 0; i < n; ++i) {
                 const int k = lst[i];
@@ -701,7 +709,7 @@ __global__ void __launch_bounds__(32 * NWR, NWR == 4 ? 8 : 4) raster_bwd_kernel(
         const int bstart = max(0, bend - RB);
         __syncthreads();
         int n = stage_batch<NWR>(s, tile, tiles_x, sorted_vals, start + bstart, bend - bstart, xydr, conic, colors);
-        const uint8_t* lst = s.list[warp];
+        const ListIdx* lst = s.list[warp];
         const int kmax = min(bend, warp_max) - bstart;  // positions >= warp_max are inactive for this warp
         while (n > 0 && (int)lst[n - 1] >= kmax) --n;
         // two entries per iteration (independent sigma chains), committed
