@@ -73,7 +73,7 @@ int gs_version(void);
  * "tile_emit" (depth-first binning): 1 (default) writes every pair straight
  * to its slot in its tile's list (per-tile counts from the projection, one
  * stable counting pass over the depth-ordered Gaussians) when the tile count
- * fits its shared-memory tables (<= 8500 tiles), 0 emits the pairs and sorts
+ * fits its shared-memory tables (<= 9800 tiles), 0 emits the pairs and sorts
  * them by tile with onesweep passes; same lists. */
 int gs_set_option(const char* name, int value);
 /* Current value of an option of gs_set_option (-1 and gs_last_error for an
@@ -230,7 +230,7 @@ int gs_frame_workspace_init(int64_t n, int64_t isect_capacity, int32_t width, in
  * view under the current options: 1 depth-first, 2 scatter, 3 direct. */
 int gs_frame_binning(int64_t n, int32_t width, int32_t height);
 /* 1 when such a frame's depth-first binning writes its pairs with the
- * tile-sorted emission (option "tile_emit", <= 8500 tiles), else 0. */
+ * tile-sorted emission (option "tile_emit", <= 9800 tiles), else 0. */
 int gs_frame_tile_emit(int64_t n, int32_t width, int32_t height);
 int gs_frame_view_of(int64_t n, int64_t isect_capacity, int32_t width, int32_t height, void* ws,
                      gs_frame_view* out /*[host]*/);

@@ -464,29 +464,37 @@ int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* 
 // where "earlier" is the emission order of sg/binning.py:35-46 over the
 // Gaussians in (depth, index) order -- exactly the stable order of
 // sg/binning.py:50-65.  A stable counting sort whose digit is the whole tile
-// id and whose keys are generated from the Gaussians' rects, never stored:
-//   et_count_kernel  chunk c = ET_CHUNK consecutive Gaussians of the depth
-//                    order: its per-tile pair counts -> row c of a (chunks x
-//                    tiles) u16 matrix (shared-memory histogram, coalesced row)
-//   et_scan_kernel   per tile, the exclusive scan of that column over the
-//                    chunks (u32 in place of the counts' matrix) and the tile's
-//                    total -> tcount (the tile scan makes the ranges of them)
-//   et_emit_kernel   chunk c again: per-(warp, tile) counts in shared memory,
-//                    turned into per-warp offsets on top of the tile's start
-//                    and the column prefix; a second walk over the pairs, in
-//                    order, ranks each step's 32 pairs with match_any and
-//                    writes the Gaussian id.
+// id, over chunks of ET_CHUNK consecutive Gaussians of the depth order:
+//   et_expand_kernel   walks each chunk's pairs once, in emission order,
+//                      writing them as (chunk-local Gaussian << 16 | tile)
+//                      words (every warp's run contiguous, placed by a
+//                      decoupled look-back over the chunks' pair totals) and
+//                      the chunk's per-tile counts (one u16 row)
+//   et_colsum_kernel   per tile, the column sums of those counts over 32
+//                      segments of chunks and the tile's total -> tcount
+//   (tile_scan_kernel  the totals -> ranges, raster order, starts)
+//   et_colscan_kernel  per (chunk, tile): start(tile) + the pairs of all
+//                      earlier chunks (u32 rows)
+//   et_place_kernel    per chunk: its row of bases and its Gaussian ids bulk-
+//                      copied (TMA) into shared memory; its pair words
+//                      streamed twice -- per-(warp, tile) counts, then, with
+//                      the per-warp offsets, each step's 32 pairs ranked in
+//                      lane (= emission) order and the Gaussian ids written.
 // Replaces emission (8 B / pair written) + 2 onesweep passes over the pairs
-// (2 x 16 B / pair) + range detection (4 B / pair) by 4 B / pair written and
-// 12 B / (chunk, tile) of prefix tables; no look-back chain (a decoupled
-// look-back over 4346 digits per chunk measured 320 us per config-3 view: the
-// first wave's chunks all look back to chunk 0 at once).  The sorted tile keys
-// are not written (the ranges imply them).
+// (2 x 16 B / pair) + range detection (4 B / pair) by 4 B / pair written
+// and read twice, 4 B / pair of output and 12 B / (chunk, tile) of tables.
+// What did not work: a decoupled look-back over the 4346 tile digits per
+// chunk in one kernel (320 us per config-3 view: the first wave's chunks all
+// look back to chunk 0 together); walking the rects in the placement kernel
+// itself, twice (154 us against 116 + 28 for the expansion; the placement is
+// latency-bound on its loads, hence the bulk copies and the 8-step batches of
+// pair words); 4-, 6-, 12- and 16-warp chunks (per-chunk overheads or
+// occupancy).  The sorted tile keys are not written (the ranges imply them).
 #ifndef GS_ET_WARPS
 #define GS_ET_WARPS 8  // warps per chunk (A/B knob)
 #endif
 #ifndef GS_ET_MINB
-#define GS_ET_MINB 2  // resident emission CTAs per SM the registers are budgeted for
+#define GS_ET_MINB 2  // resident placement CTAs per SM the registers are budgeted for
 #endif
 constexpr int ET_WARPS = GS_ET_WARPS;
 #ifndef GS_ET_ROUNDS
@@ -494,19 +502,42 @@ constexpr int ET_WARPS = GS_ET_WARPS;
 #endif
 constexpr int ET_ROUNDS = GS_ET_ROUNDS;  // 32-Gaussian rounds per warp (u16 counts and offsets)
 constexpr int ET_THREADS = ET_WARPS * 32;
-constexpr int ET_CHUNK = ET_THREADS * ET_ROUNDS;  // Gaussians per chunk (2048: u16 chunk counts)
+constexpr int ET_CHUNK = ET_THREADS * ET_ROUNDS;  // Gaussians per chunk (2048: u16 chunk counts, 11-bit locals)
+constexpr int ES_WARPS = 32;                      // chunk segments of the column sums
 
-__host__ __device__ inline int et_stride(int n_tiles) { return (n_tiles + 1) & ~1; }  // u16 row stride, even
+// row stride (tiles) of the per-(chunk, tile) tables and the shared tables: a
+// multiple of 8, so every u16 and u32 row starts 16-byte aligned (bulk copies)
+__host__ __device__ inline int et_stride(int n_tiles) { return (n_tiles + 7) & ~7; }
+// placement shared memory: per-warp u16 offsets + the bases + the chunk's Gaussian ids
 size_t emit_tiles_smem(int n_tiles) {
-    return (size_t)ET_WARPS * et_stride(n_tiles) * 2 + (size_t)n_tiles * 4;
+    return (size_t)ET_WARPS * et_stride(n_tiles) * 2 + (size_t)et_stride(n_tiles) * 4 + (size_t)ET_CHUNK * 4;
 }
-bool emit_tiles_fits(int n_tiles) { return n_tiles >= 1 && emit_tiles_smem(n_tiles) <= 200 * 1024; }  // <= 10240 tiles (8 warps)
-// tables: u32 column prefixes [chunk][tile], then the u16 counts [chunk][tile]
-static size_t et_prefix_bytes(int64_t n, int n_tiles) {
-    const int64_t chunks = (n + ET_CHUNK - 1) / ET_CHUNK;
-    return (size_t)(chunks > 0 ? chunks : 1) * (size_t)et_stride(n_tiles) * 4;
+bool emit_tiles_fits(int n_tiles) { return n_tiles >= 1 && emit_tiles_smem(n_tiles) <= 200 * 1024; }  // <= 9856 tiles
+// tables: u32 bases [chunk][tile], u16 counts [chunk][tile], u32 segment sums
+// [32][tile], u32 per-(chunk, warp) pair offsets
+struct EtTables {
+    uint32_t* bases;
+    unsigned short* counts;
+    uint32_t* segs;
+    uint32_t* wbases;
+};
+static size_t et_chunks(int64_t n) {
+    const int64_t c = (n + ET_CHUNK - 1) / ET_CHUNK;
+    return (size_t)(c > 0 ? c : 1);
 }
-size_t emit_tiles_table_bytes(int64_t n, int n_tiles) { return et_prefix_bytes(n, n_tiles) * 3 / 2; }
+static size_t et_layout(int64_t n, int n_tiles, char* table, EtTables* t) {
+    const size_t hs = (size_t)et_stride(n_tiles), C = et_chunks(n);
+    const size_t o_counts = C * hs * 4, o_segs = o_counts + C * hs * 2, o_wb = o_segs + ES_WARPS * hs * 4;
+    const size_t total = o_wb + (C * (ET_WARPS + 1) * 4 + 15) / 16 * 16;
+    if (t) {
+        t->bases = reinterpret_cast<uint32_t*>(table);
+        t->counts = reinterpret_cast<unsigned short*>(table + o_counts);
+        t->segs = reinterpret_cast<uint32_t*>(table + o_segs);
+        t->wbases = reinterpret_cast<uint32_t*>(table + o_wb);
+    }
+    return total;
+}
+size_t emit_tiles_table_bytes(int64_t n, int n_tiles) { return et_layout(n, n_tiles, nullptr, nullptr); }
 
 // The chunk's Gaussians (depth-order positions p0 + 32 r, one per lane and
 // round) and their tile rects; rounds past the visible count are empty.
@@ -564,60 +595,107 @@ __device__ __forceinline__ void et_walk(int lane, const EtRound& rd, int tiles_x
         int row = (int)((float)j * orw);
         if (row * ow > j) --row;
         if ((row + 1) * ow <= j) ++row;
-        f(t < total ? (uint32_t)(otb + row * (tiles_x - ow) + j) : 0xFFFFFFFFu, og);
+        f(t < total ? (uint32_t)(otb + row * (tiles_x - ow) + j) : 0xFFFFFFFFu, og, t, L);
     }
 }
 
 // Every tile of the lane's own rect, row-major (order-free uses: counts).
 // Divergent, so a warp runs as long as its largest rect, but ~5 instructions
 // per tile against the walk's ~45 per step of 32.
-template <typename F>
-__device__ __forceinline__ void et_rect_each(const EtRound& rd, int tiles_x, F&& f) {
-    uint32_t t = (uint32_t)(rd.ty0 * tiles_x + rd.tx0);
-    for (int y = 0; y < rd.h; ++y, t += (uint32_t)tiles_x)
-        for (int x = 0; x < rd.w; ++x) f(t + (uint32_t)x);
-}
-
 // depth-first frame: meta[7] visible Gaussians sorted, in order_alt after an odd pass count (meta[8])
 __device__ __forceinline__ const uint32_t* et_order(const uint32_t* order, const uint32_t* order_alt,
                                                     const unsigned long long* meta) {
     return (meta[8] & 1ull) ? order_alt : order;
 }
 
-__global__ void __launch_bounds__(ET_THREADS) et_count_kernel(const uint32_t* __restrict__ order,
-                                                              const uint32_t* __restrict__ order_alt,
-                                                              const float4* __restrict__ xydr, int n, int tiles_x,
-                                                              int tiles_y, unsigned short* __restrict__ counts,
-                                                              const unsigned long long* __restrict__ meta) {
+// Expansion: the chunk's pairs walked once, in emission order, and written
+// out as (chunk-local Gaussian index << 16 | tile) words -- every warp's
+// pairs contiguous at a global offset obtained by a decoupled look-back over
+// the chunks' pair totals (one status word per chunk, chunks taken in order
+// from a counter) -- together with the chunk's per-tile counts.
+__global__ void __launch_bounds__(ET_THREADS) et_expand_kernel(
+    const uint32_t* __restrict__ order, const uint32_t* __restrict__ order_alt, const float4* __restrict__ xydr,
+    int n, int tiles_x, int tiles_y, int64_t capacity, unsigned short* __restrict__ counts,
+    uint32_t* __restrict__ pairs, uint32_t* __restrict__ wbases, unsigned int* __restrict__ chunk_counter,
+    unsigned long long* __restrict__ status, const unsigned long long* __restrict__ meta) {
     griddep_wait();
     const int V = min(n, (int)meta[7]);
-    const int chunk = blockIdx.x;
-    if (chunk * ET_CHUNK >= V) return;
     order = et_order(order, order_alt, meta);
     const int n_tiles = tiles_x * tiles_y, hs = et_stride(n_tiles);
+    const int n_chunks = (V + ET_CHUNK - 1) / ET_CHUNK;
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem);  // [tile] (u32: shared atomics)
+    __shared__ unsigned int s_chunk;
+    __shared__ uint32_t s_wt[ET_WARPS];
+    __shared__ unsigned long long s_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_chunk = atomicAdd(chunk_counter, 1u);  // chunks in launch order: look-back progress
     for (int t = tid; t < hs; t += ET_THREADS) s_cnt[t] = 0u;
+    __syncthreads();
+    const int chunk = (int)s_chunk;
+    if (chunk >= n_chunks) return;
     EtRound rd[ET_ROUNDS];
     et_load(order, xydr, chunk * ET_CHUNK + warp * (32 * ET_ROUNDS) + lane, V, tiles_x, tiles_y, rd);
-    __syncthreads();
+    uint32_t rtot[ET_ROUNDS], wsum = 0;  // pairs per round of this warp, and in all
 #pragma unroll
-    for (int r = 0; r < ET_ROUNDS; ++r) et_rect_each(rd[r], tiles_x, [&](uint32_t tile) { atomicAdd(&s_cnt[tile], 1u); });
+    for (int r = 0; r < ET_ROUNDS; ++r) {
+        rtot[r] = __reduce_add_sync(0xffffffffu, (uint32_t)(rd[r].w * rd[r].h));
+        wsum += rtot[r];
+    }
+    if (lane == 0) s_wt[warp] = wsum;
+    __syncthreads();
+    if (tid == 0) {  // the chunk's global pair offset: decoupled look-back over the chunks' totals
+        unsigned long long agg = 0;
+        for (int w = 0; w < ET_WARPS; ++w) agg += s_wt[w];
+        unsigned long long prefix = 0;
+        if (chunk == 0) {
+            st_volatile(&status[0], FLAG_PRE | agg);
+        } else {
+            st_volatile(&status[chunk], FLAG_AGG | agg);
+            int q = chunk - 1;
+            while (true) {
+                unsigned long long sv = ld_volatile(&status[q]);
+                while ((sv & ~VAL_MASK) == 0) sv = ld_volatile(&status[q]);
+                prefix += sv & VAL_MASK;
+                if ((sv & ~VAL_MASK) == FLAG_PRE) break;
+                --q;
+            }
+            st_volatile(&status[chunk], FLAG_PRE | (prefix + agg));
+        }
+        s_base = prefix;
+        unsigned long long b = prefix;
+        for (int w = 0; w < ET_WARPS; ++w) {
+            wbases[(size_t)chunk * (ET_WARPS + 1) + w] = (uint32_t)b;
+            b += s_wt[w];
+        }
+        wbases[(size_t)chunk * (ET_WARPS + 1) + ET_WARPS] = (uint32_t)b;
+    }
+    __syncthreads();
+    unsigned long long out = s_base;
+    for (int w = 0; w < warp; ++w) out += s_wt[w];
+#pragma unroll
+    for (int r = 0; r < ET_ROUNDS; ++r) {
+        const uint32_t loc0 = (uint32_t)(warp * (32 * ET_ROUNDS) + 32 * r) << 16;  // the round's first local index
+        et_walk(lane, rd[r], tiles_x, [&](uint32_t tile, uint32_t, uint32_t t, int L) {
+            if (tile != 0xFFFFFFFFu) {
+                atomicAdd(&s_cnt[tile], 1u);
+                const unsigned long long pos = out + t;
+                if ((int64_t)pos < capacity) pairs[pos] = (loc0 + ((uint32_t)L << 16)) | tile;
+            }
+        });
+        out += rtot[r];
+    }
     __syncthreads();
     uint32_t* row = reinterpret_cast<uint32_t*>(counts + (size_t)chunk * hs);  // two u16 per word
     for (int k = tid; k < hs / 2; k += ET_THREADS) row[k] = s_cnt[2 * k] | (s_cnt[2 * k + 1] << 16);
 }
 
 // One CTA per 32 tiles (lane = tile), 32 warps over consecutive runs of
-// chunks: pass 1 sums each warp's rows, the warps' sums are scanned in shared
-// memory, pass 2 writes the running exclusive prefix (u32, row stride hs);
-// the last warp's inclusive sums are the tiles' totals.
-constexpr int ES_WARPS = 32;
-__global__ void __launch_bounds__(ES_WARPS * 32) et_scan_kernel(const unsigned short* __restrict__ counts,
-                                                                uint32_t* __restrict__ prefix, int n, int n_tiles,
-                                                                uint32_t* __restrict__ totals,
-                                                                const unsigned long long* __restrict__ meta) {
+// chunks: each warp's column sums (segs) and the tiles' totals (tcount).
+__global__ void __launch_bounds__(ES_WARPS * 32) et_colsum_kernel(const unsigned short* __restrict__ counts,
+                                                                  uint32_t* __restrict__ segs, int n, int n_tiles,
+                                                                  uint32_t* __restrict__ totals,
+                                                                  const unsigned long long* __restrict__ meta) {
     griddep_wait();
     const int V = min(n, (int)meta[7]);
     const int chunks = (V + ET_CHUNK - 1) / ET_CHUNK;
@@ -639,13 +717,38 @@ __global__ void __launch_bounds__(ES_WARPS * 32) et_scan_kernel(const unsigned s
             for (int u = 0; u < 8; ++u) sum += v[u];
         }
         for (; c < c1; ++c) sum += counts[(size_t)c * hs + t];
+        segs[(size_t)warp * hs + t] = sum;
     }
     s_sum[warp][lane] = sum;
     __syncthreads();
-    uint32_t run = 0;
-    for (int w = 0; w < warp; ++w) run += s_sum[w][lane];
-    if (warp == ES_WARPS - 1 && in) totals[t] = run + sum;
-    if (!in) return;
+    if (warp == 0 && in) {
+        uint32_t tot = 0;
+        for (int w = 0; w < ES_WARPS; ++w) tot += s_sum[w][lane];
+        totals[t] = tot;
+    }
+}
+
+// The same CTAs after the tile scan (tcount = every tile's start): per
+// (chunk, tile) the absolute slot of the chunk's first pair of the tile,
+// start + the column sums of the earlier segments + the running sum.
+__global__ void __launch_bounds__(ES_WARPS * 32) et_colscan_kernel(const unsigned short* __restrict__ counts,
+                                                                   const uint32_t* __restrict__ segs,
+                                                                   const uint32_t* __restrict__ starts,
+                                                                   uint32_t* __restrict__ bases, int n, int n_tiles,
+                                                                   int64_t capacity,
+                                                                   const unsigned long long* __restrict__ meta) {
+    griddep_wait();
+    if ((int64_t)meta[1] > capacity) return;  // over capacity: nothing is placed
+    const int V = min(n, (int)meta[7]);
+    const int chunks = (V + ET_CHUNK - 1) / ET_CHUNK;
+    const int hs = et_stride(n_tiles);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
+    if (t >= n_tiles) return;
+    const int per = (chunks + ES_WARPS - 1) / ES_WARPS;
+    const int c0 = min(chunks, warp * per), c1 = min(chunks, c0 + per);
+    uint32_t run = starts[t];
+    for (int w = 0; w < warp; ++w) run += segs[(size_t)w * hs + t];
     int c = c0;
     for (; c + 8 <= c1; c += 8) {
         uint32_t v[8];
@@ -653,54 +756,95 @@ __global__ void __launch_bounds__(ES_WARPS * 32) et_scan_kernel(const unsigned s
         for (int u = 0; u < 8; ++u) v[u] = counts[(size_t)(c + u) * hs + t];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            prefix[(size_t)(c + u) * hs + t] = run;
+            bases[(size_t)(c + u) * hs + t] = run;
             run += v[u];
         }
     }
     for (; c < c1; ++c) {
         const uint32_t v = counts[(size_t)c * hs + t];
-        prefix[(size_t)c * hs + t] = run;
+        bases[(size_t)c * hs + t] = run;
         run += v;
     }
 }
 
-__global__ void __launch_bounds__(ET_THREADS, GS_ET_MINB) et_emit_kernel(
-    const uint32_t* __restrict__ order, const uint32_t* __restrict__ order_alt, const float4* __restrict__ xydr,
-    int n, int tiles_x, int tiles_y, int64_t capacity, const uint2* __restrict__ ranges,
-    const uint32_t* __restrict__ prefix, uint32_t* __restrict__ vals, const unsigned long long* __restrict__ meta) {
+// 1D bulk (TMA) copy global -> shared completing on an mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// Placement (see the section head).  Over capacity (meta[1]) nothing is
+// written and the host re-runs with more room.
+__global__ void __launch_bounds__(ET_THREADS, GS_ET_MINB) et_place_kernel(
+    const uint32_t* __restrict__ order, const uint32_t* __restrict__ order_alt, int n, int n_tiles,
+    int64_t capacity, const uint32_t* __restrict__ bases, const uint32_t* __restrict__ pairs,
+    const uint32_t* __restrict__ wbases, uint32_t* __restrict__ vals, const unsigned long long* __restrict__ meta) {
     griddep_wait();
-    // meta[1]: the intersection total (tile scan); over capacity the ranges
-    // are empty and nothing is written (the host re-runs with more room)
     if ((int64_t)meta[1] > capacity) return;
     const int V = min(n, (int)meta[7]);
     const int chunk = blockIdx.x;
     if (chunk * ET_CHUNK >= V) return;
     order = et_order(order, order_alt, meta);
-    const int n_tiles = tiles_x * tiles_y, hs = et_stride(n_tiles);
+    const int hs = et_stride(n_tiles);
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned short* s_hist = reinterpret_cast<unsigned short*>(smem);                // [warp][tile]
     uint32_t* s_base = reinterpret_cast<uint32_t*>(smem + (size_t)ET_WARPS * hs * 2);  // [tile]
+    uint32_t* s_gid = s_base + hs;                                                    // [local Gaussian]
+    __shared__ __align__(8) uint64_t s_bar;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {  // the chunk's row of bases and its Gaussian ids, by the bulk-copy engine
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t row = (uint32_t)hs * 4, ids = (uint32_t)ET_CHUNK * 4;
+        mbar_expect_tx(&s_bar, row + ids);
+        bulk_g2s(s_base, bases + (size_t)chunk * hs, row, &s_bar);
+        bulk_g2s(s_gid, order + (size_t)chunk * ET_CHUNK, ids, &s_bar);  // (ids past V are never referenced)
+    }
     {
         uint4* z = reinterpret_cast<uint4*>(smem);
         const int n16 = (ET_WARPS * hs * 2 + 15) / 16;
         for (int k = tid; k < n16; k += ET_THREADS) z[k] = make_uint4(0u, 0u, 0u, 0u);
     }
-    EtRound rd[ET_ROUNDS];
-    et_load(order, xydr, chunk * ET_CHUNK + warp * (32 * ET_ROUNDS) + lane, V, tiles_x, tiles_y, rd);
-    // every tile's start + the pairs of all earlier chunks
-    const uint32_t* pre = prefix + (size_t)chunk * hs;
-#pragma unroll 4
-    for (int t = tid; t < n_tiles; t += ET_THREADS) s_base[t] = ranges[t].x + pre[t];
+    const uint32_t wb = wbases[(size_t)chunk * (ET_WARPS + 1) + warp];
+    const uint32_t we = min(wbases[(size_t)chunk * (ET_WARPS + 1) + warp + 1], (uint32_t)capacity);
     __syncthreads();
-    // 1. per-(warp, tile) pair counts (order-free: shared atomics on u16
-    //    halves; <= 256 per warp and tile, no carry)
+    // 1. per-(warp, tile) pair counts (PF steps of 32 pair words in flight)
+    constexpr int PF = 8;
     uint32_t* h32 = reinterpret_cast<uint32_t*>(s_hist + warp * hs);
+    for (uint32_t p0 = wb; p0 < we; p0 += 32 * PF) {
+        uint32_t wv[PF];
 #pragma unroll
-    for (int r = 0; r < ET_ROUNDS; ++r)
-        et_walk(lane, rd[r], tiles_x, [&](uint32_t tile, uint32_t) {
-            if (tile != 0xFFFFFFFFu) atomicAdd(&h32[tile >> 1], 1u << ((tile & 1u) * 16));
-        });
+        for (int u = 0; u < PF; ++u) {
+            const uint32_t p = p0 + 32 * u + lane;
+            wv[u] = p < we ? pairs[p] : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const uint32_t tile = wv[u] & 0xFFFFu;
+            if (wv[u] != 0xFFFFFFFFu) atomicAdd(&h32[tile >> 1], 1u << ((tile & 1u) * 16));
+        }
+    }
     __syncthreads();
     // 2. per tile: exclusive offsets over the warps
     for (int t = tid; t < n_tiles; t += ET_THREADS) {
@@ -712,21 +856,30 @@ __global__ void __launch_bounds__(ET_THREADS, GS_ET_MINB) et_emit_kernel(
             run += c;
         }
     }
+    mbar_wait(&s_bar, 0);
     __syncthreads();
-    // 3. the same walk again, in order.  Each pair takes its warp's offset of
-    //    its tile with a returning shared atomic; when no two lanes of the
-    //    step share a tile (no lane's increment was followed by another's:
-    //    after - old == 1 everywhere) that offset is its slot.  Otherwise the
-    //    lanes of each shared tile re-rank in lane (= emission) order over
-    //    the group's range [after - k, after) (match_any, ~1 step in 10).
+    // 3. the pairs again, in order (PF steps at a time).  Each pair takes its
+    //    warp's offset of its tile with a returning shared atomic; when no two
+    //    lanes of the step share a tile (after - old == 1 everywhere) that is
+    //    its slot, otherwise the lanes of each shared tile re-rank in lane
+    //    order over the group's range [after - k, after) (match_any)
     const uint32_t lt = lanemask_lt();
+    for (uint32_t q0 = wb; q0 < we; q0 += 32 * PF) {
+        uint32_t wv[PF];
 #pragma unroll
-    for (int r = 0; r < ET_ROUNDS; ++r)
-        et_walk(lane, rd[r], tiles_x, [&](uint32_t tile, uint32_t og) {
-            const bool valid = tile != 0xFFFFFFFFu;
-            const uint32_t sh = (tile & 1u) * 16;
-            uint32_t old = 0, base = 0;
+        for (int u = 0; u < PF; ++u) {
+            const uint32_t p = q0 + 32 * u + lane;
+            wv[u] = p < we ? pairs[p] : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            if (q0 + 32 * u >= we) break;  // (warp-uniform)
+            const bool valid = wv[u] != 0xFFFFFFFFu;
+            uint32_t tile = 0xFFFFFFFFu, og = 0u, sh = 0u, old = 0u, base = 0u;
             if (valid) {
+                tile = wv[u] & 0xFFFFu;
+                og = s_gid[wv[u] >> 16];
+                sh = (tile & 1u) * 16;
                 base = s_base[tile];
                 old = (atomicAdd(&h32[tile >> 1], 1u << sh) >> sh) & 0xFFFFu;
             }
@@ -738,7 +891,8 @@ __global__ void __launch_bounds__(ET_THREADS, GS_ET_MINB) et_emit_kernel(
             }
             if (valid) vals[base + old] = og;
             __syncwarp();  // the next step's atomics after every lane's read
-        });
+        }
+    }
 }
 
 static int et_attr(const void* k, size_t smem, size_t& done) {
@@ -751,37 +905,45 @@ static int et_attr(const void* k, size_t smem, size_t& done) {
 }
 
 int launch_emit_tiles_count(const uint32_t* order, const uint32_t* order_alt, const float* xydr4, int64_t n,
-                            int tiles_x, int tiles_y, void* table, uint32_t* totals, const unsigned long long* meta,
-                            cudaStream_t s) {
+                            int tiles_x, int tiles_y, int64_t capacity, void* table, uint32_t* totals,
+                            uint32_t* pairs, void* scan_ws, const unsigned long long* meta, cudaStream_t s) {
     const int n_tiles = tiles_x * tiles_y;
     if (!emit_tiles_fits(n_tiles)) return set_error("emit_tiles: %d tiles do not fit shared memory", n_tiles);
     if (n <= 0) return 0;
+    EtTables tb;
+    et_layout(n, n_tiles, static_cast<char*>(table), &tb);
     const int64_t chunks = (n + ET_CHUNK - 1) / ET_CHUNK;  // capacity-sized grids: fewer visible -> early exit
-    const size_t smem_c = (size_t)et_stride(n_tiles) * 4;
-    static size_t done_c = 0;
-    if (et_attr((const void*)et_count_kernel, smem_c, done_c)) return -1;
-    unsigned short* counts = reinterpret_cast<unsigned short*>((char*)table + et_prefix_bytes(n, n_tiles));
-    launch_k(et_count_kernel, dim3((unsigned)chunks), dim3(ET_THREADS), smem_c, s, order, order_alt,
-             (const float4*)xydr4, (int)n, tiles_x, tiles_y, counts, meta);
-    if (check_launch("et_count_kernel")) return -1;
-    launch_k(et_scan_kernel, dim3((unsigned)((n_tiles + 31) / 32)), dim3(ES_WARPS * 32), 0, s,
-             (const unsigned short*)counts, (uint32_t*)table, (int)n, n_tiles, totals, meta);
-    return check_launch("et_scan_kernel");
+    const size_t smem_x = (size_t)et_stride(n_tiles) * 4;
+    static size_t done_x = 0;
+    if (et_attr((const void*)et_expand_kernel, smem_x, done_x)) return -1;
+    launch_k(et_expand_kernel, dim3((unsigned)chunks), dim3(ET_THREADS), smem_x, s, order, order_alt,
+             (const float4*)xydr4, (int)n, tiles_x, tiles_y, capacity, tb.counts, pairs, tb.wbases,
+             (unsigned int*)scan_ws, (unsigned long long*)((char*)scan_ws + 16), meta);
+    if (check_launch("et_expand_kernel")) return -1;
+    launch_k(et_colsum_kernel, dim3((unsigned)((n_tiles + 31) / 32)), dim3(ES_WARPS * 32), 0, s,
+             (const unsigned short*)tb.counts, tb.segs, (int)n, n_tiles, totals, meta);
+    return check_launch("et_colsum_kernel");
 }
 
-int launch_emit_tiles(const uint32_t* order, const uint32_t* order_alt, const float* xydr4, int64_t n, int tiles_x,
-                      int tiles_y, int64_t capacity, const uint2* ranges, const void* table, uint32_t* vals,
+int launch_emit_tiles(const uint32_t* order, const uint32_t* order_alt, int64_t n, int tiles_x, int tiles_y,
+                      int64_t capacity, const uint32_t* starts, void* table, const uint32_t* pairs, uint32_t* vals,
                       const unsigned long long* meta, cudaStream_t s) {
     const int n_tiles = tiles_x * tiles_y;
     if (!emit_tiles_fits(n_tiles)) return set_error("emit_tiles: %d tiles do not fit shared memory", n_tiles);
     if (n <= 0) return 0;
+    EtTables tb;
+    et_layout(n, n_tiles, static_cast<char*>(table), &tb);
+    launch_k(et_colscan_kernel, dim3((unsigned)((n_tiles + 31) / 32)), dim3(ES_WARPS * 32), 0, s,
+             (const unsigned short*)tb.counts, (const uint32_t*)tb.segs, starts, tb.bases, (int)n, n_tiles, capacity,
+             meta);
+    if (check_launch("et_colscan_kernel")) return -1;
     const int64_t chunks = (n + ET_CHUNK - 1) / ET_CHUNK;
-    const size_t smem = emit_tiles_smem(n_tiles);
-    static size_t done = 0;
-    if (et_attr((const void*)et_emit_kernel, smem, done)) return -1;
-    launch_k(et_emit_kernel, dim3((unsigned)chunks), dim3(ET_THREADS), smem, s, order, order_alt,
-             (const float4*)xydr4, (int)n, tiles_x, tiles_y, capacity, ranges, (const uint32_t*)table, vals, meta);
-    return check_launch("et_emit_kernel");
+    const size_t smem_p = emit_tiles_smem(n_tiles);
+    static size_t done_p = 0;
+    if (et_attr((const void*)et_place_kernel, smem_p, done_p)) return -1;
+    launch_k(et_place_kernel, dim3((unsigned)chunks), dim3(ET_THREADS), smem_p, s, order, order_alt, (int)n, n_tiles,
+             capacity, (const uint32_t*)tb.bases, pairs, (const uint32_t*)tb.wbases, vals, meta);
+    return check_launch("et_place_kernel");
 }
 
 // ---------------------------------------------------------------- scatter binning

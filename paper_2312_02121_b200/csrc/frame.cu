@@ -6,7 +6,7 @@
 //   -> scan of tile counts in depth order -> emission of (tile, gaussian)
 //   pairs in depth order (+ tile-digit histograms) -> 1-2 pass stable sort by
 //   tile id -> per-tile ranges (+ raster order) -> raster forward.
-//   With the tile-sorted emission (option tile_emit, <= 8500 tiles), the
+//   With the tile-sorted emission (option tile_emit, <= 9800 tiles), the
 //   emission and the sort by tile are one stable counting pass instead:
 //   per-(chunk, tile) pair counts -> column prefixes + tile totals -> tile
 //   scan (ranges, raster order) -> every pair written to its final slot.
@@ -410,16 +410,16 @@ int frame_forward_impl(const float* means3, const float* scales3, const float* q
         //    raster order)
         uint32_t* totals = at<uint32_t>(ws, L.tcount);
         if (launch_emit_tiles_count(order, at<uint32_t>(ws, L.order_alt), at<float>(ws, L.xydr), n, tiles_x, tiles_y,
-                                    at<char>(ws, L.etable), totals, meta, s))
+                                    isect_capacity, at<char>(ws, L.etable), totals, at<uint32_t>(ws, L.tkeys),
+                                    at<char>(ws, L.scan_ws), meta, s))
             return -1;
         if (launch_tile_scan(totals, n_tiles, isect_capacity, at<uint2>(ws, L.ranges), meta + 1,
                              const_cast<uint32_t*>(t_order), s, 1))
             return -1;
         mark(stage_events, 3, s);
         // 4. every pair straight to its slot, tile lists in (depth, index) order
-        if (launch_emit_tiles(order, at<uint32_t>(ws, L.order_alt), at<float>(ws, L.xydr), n, tiles_x, tiles_y,
-                              isect_capacity, at<uint2>(ws, L.ranges), at<char>(ws, L.etable),
-                              at<uint32_t>(ws, L.tvals), meta, s))
+        if (launch_emit_tiles(order, at<uint32_t>(ws, L.order_alt), n, tiles_x, tiles_y, isect_capacity, totals,
+                              at<char>(ws, L.etable), at<uint32_t>(ws, L.tkeys), at<uint32_t>(ws, L.tvals), meta, s))
             return -1;
         mark(stage_events, 4, s);
         if (launch_raster_fwd(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.tvals), at<float>(ws, L.xydr),

@@ -108,19 +108,20 @@ int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* 
                      const uint32_t* order_alt = nullptr, const unsigned long long* sort_meta = nullptr);
 // sort_meta (depth-first frame, = meta + 7): [0] the number of sorted (visible)
 // Gaussians, [1] the depth-sort pass count (odd: the order is in order_alt)
-// depth-first binning, tile-sorted emission (binning.cu): per-(chunk, tile)
-// counts of the depth-ordered Gaussians' pairs and their column prefixes
-// (table: emit_tiles_table_bytes, no zeroing needed) + every tile's total into
-// totals (then launch_tile_scan(totals, ..., replicas 1) makes the ranges);
-// then every pair written to its final slot
+// depth-first binning, tile-sorted emission (binning.cu): the expanded pairs
+// (pairs: capacity u32 scratch), the per-(chunk, tile) counts and their
+// column sums (table: emit_tiles_table_bytes, no zeroing needed; scan_ws:
+// emit_scan_ws_bytes, zeroed) and every tile's total into totals; then
+// (launch_tile_scan(totals, ..., replicas 1) makes the ranges and leaves the
+// starts in totals) the bases of every (chunk, tile) and the placement
 size_t emit_tiles_smem(int n_tiles);
 bool emit_tiles_fits(int n_tiles);
 size_t emit_tiles_table_bytes(int64_t n, int n_tiles);
 int launch_emit_tiles_count(const uint32_t* order, const uint32_t* order_alt, const float* xydr4, int64_t n,
-                            int tiles_x, int tiles_y, void* table, uint32_t* totals, const unsigned long long* meta,
-                            cudaStream_t s);
-int launch_emit_tiles(const uint32_t* order, const uint32_t* order_alt, const float* xydr4, int64_t n, int tiles_x,
-                      int tiles_y, int64_t capacity, const uint2* ranges, const void* table, uint32_t* vals,
+                            int tiles_x, int tiles_y, int64_t capacity, void* table, uint32_t* totals,
+                            uint32_t* pairs, void* scan_ws, const unsigned long long* meta, cudaStream_t s);
+int launch_emit_tiles(const uint32_t* order, const uint32_t* order_alt, int64_t n, int tiles_x, int tiles_y,
+                      int64_t capacity, const uint32_t* starts, void* table, const uint32_t* pairs, uint32_t* vals,
                       const unsigned long long* meta, cudaStream_t s);
 // option "tile_emit" (abi.cu): 1 (default) tile-sorted emission where it fits, 0 emission + onesweep by tile
 bool tile_emit();
