@@ -644,31 +644,43 @@ __global__ void __launch_bounds__(ET_THREADS) et_expand_kernel(
     }
     if (lane == 0) s_wt[warp] = wsum;
     __syncthreads();
-    if (tid == 0) {  // the chunk's global pair offset: decoupled look-back over the chunks' totals
+    if (warp == 0) {  // the chunk's global pair offset: decoupled look-back over the chunks' totals
         unsigned long long agg = 0;
         for (int w = 0; w < ET_WARPS; ++w) agg += s_wt[w];
         unsigned long long prefix = 0;
         if (chunk == 0) {
-            st_volatile(&status[0], FLAG_PRE | agg);
+            if (lane == 0) st_volatile(&status[0], FLAG_PRE | agg);
         } else {
-            st_volatile(&status[chunk], FLAG_AGG | agg);
+            if (lane == 0) st_volatile(&status[chunk], FLAG_AGG | agg);
+            // warp-wide: lane l reads predecessor q - l; the nearest inclusive
+            // prefix (PRE) ends the window, the aggregates up to it are summed
             int q = chunk - 1;
             while (true) {
-                unsigned long long sv = ld_volatile(&status[q]);
-                while ((sv & ~VAL_MASK) == 0) sv = ld_volatile(&status[q]);
-                prefix += sv & VAL_MASK;
-                if ((sv & ~VAL_MASK) == FLAG_PRE) break;
-                --q;
+                const int pq = q - lane;
+                unsigned long long sv = pq >= 0 ? ld_volatile(&status[pq]) : FLAG_PRE;
+                while (__any_sync(0xffffffffu, (sv & ~VAL_MASK) == 0)) {
+                    if ((sv & ~VAL_MASK) == 0) sv = ld_volatile(&status[pq]);
+                }
+                const uint32_t pre = __ballot_sync(0xffffffffu, (sv & ~VAL_MASK) == FLAG_PRE);
+                const int stop = pre ? __ffs(pre) - 1 : 32;  // lanes [0, stop] count
+                unsigned long long v = lane <= stop ? (sv & VAL_MASK) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                prefix += v;
+                if (pre) break;
+                q -= 32;
             }
-            st_volatile(&status[chunk], FLAG_PRE | (prefix + agg));
+            if (lane == 0) st_volatile(&status[chunk], FLAG_PRE | (prefix + agg));
         }
-        s_base = prefix;
-        unsigned long long b = prefix;
-        for (int w = 0; w < ET_WARPS; ++w) {
-            wbases[(size_t)chunk * (ET_WARPS + 1) + w] = (uint32_t)b;
-            b += s_wt[w];
+        if (lane == 0) s_base = prefix;
+        if (lane == 0) {
+            unsigned long long b = prefix;
+            for (int w = 0; w < ET_WARPS; ++w) {
+                wbases[(size_t)chunk * (ET_WARPS + 1) + w] = (uint32_t)b;
+                b += s_wt[w];
+            }
+            wbases[(size_t)chunk * (ET_WARPS + 1) + ET_WARPS] = (uint32_t)b;
         }
-        wbases[(size_t)chunk * (ET_WARPS + 1) + ET_WARPS] = (uint32_t)b;
     }
     __syncthreads();
     unsigned long long out = s_base;
