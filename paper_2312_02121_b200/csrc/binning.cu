@@ -489,7 +489,9 @@ int launch_emit_scan(const uint32_t* order, const float* xydr4, const uint32_t* 
 // itself, twice (154 us against 116 + 28 for the expansion; the placement is
 // latency-bound on its loads, hence the bulk copies and the 8-step batches of
 // pair words); 4-, 6-, 12- and 16-warp chunks (per-chunk overheads or
-// occupancy).  The sorted tile keys are not written (the ranges imply them).
+// occupancy); match_any on every step, even with the 8 steps' matches
+// issued together (3.70 -> 4.43 ms per config-3 step: match_any is slow on
+// sm_100a, the returning atomic + duplicate check needs it on ~1 step in 4).  The sorted tile keys are not written (the ranges imply them).
 #ifndef GS_ET_WARPS
 #define GS_ET_WARPS 8  // warps per chunk (A/B knob)
 #endif
