@@ -300,6 +300,8 @@ int gs_frame_project_backward(const float* means3, const float* scales3, const f
  * parameters once and every view's screen-space gradient rows, and writes
  * (flag bit 0: adds to) d_means3 / d_scales3 / d_quats4 / d_rgbo4 the sums
  * over the views, and d_views16 (n_views x 16, flag bit 4: added) per view.
+ * Adding continues each row's running sum in view order (the row's current
+ * value first), so views split over several calls give bit-identical sums.
  * A Gaussian counts as visible in a view iff its rows there are non-zero (a
  * culled one's rows are never written; zero rows contribute exactly zero).
  * The rows read are cleared unless flag bit 1 keeps them; the call whose

@@ -1,6 +1,8 @@
 // project.cu -- stage 1 (projection forward) and stage 5 (projection
 // backward).  One thread per Gaussian; both kernels are HBM-bound
 // (80 B/Gaussian forward, 104 B/Gaussian backward).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.cuh"
 
@@ -315,12 +317,8 @@ struct BwdPrep {
     float qw, qx, qy, qz, inv;
     float R[9], M[9], Sg[9];
 };
-__device__ __forceinline__ BwdPrep proj_bwd_prep(float4 q, const float s[3]) {
-    BwdPrep P;
-    const float qn = quat_norm(q);
-    P.inv = 1.f / qn;
-    P.qw = q.x * P.inv, P.qx = q.y * P.inv, P.qy = q.z * P.inv, P.qz = q.w * P.inv;
-    quat_rot(P.qw, P.qx, P.qy, P.qz, P.R);
+// M = R diag(s) and Sigma = M M^T of a prepared Gaussian (P.R set)
+__device__ __forceinline__ void bwd_prep_ms(BwdPrep& P, const float s[3]) {
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -331,6 +329,14 @@ __device__ __forceinline__ BwdPrep proj_bwd_prep(float4 q, const float s[3]) {
 #pragma unroll
         for (int b = 0; b < 3; ++b)
             P.Sg[3 * a + b] = P.M[3 * a] * P.M[3 * b] + P.M[3 * a + 1] * P.M[3 * b + 1] + P.M[3 * a + 2] * P.M[3 * b + 2];
+}
+__device__ __forceinline__ BwdPrep proj_bwd_prep(float4 q, const float s[3]) {
+    BwdPrep P;
+    const float qn = quat_norm(q);
+    P.inv = 1.f / qn;
+    P.qw = q.x * P.inv, P.qx = q.y * P.inv, P.qy = q.z * P.inv, P.qz = q.w * P.inv;
+    quat_rot(P.qw, P.qx, P.qy, P.qz, P.R);
+    bwd_prep_ms(P, s);
     return P;
 }
 
@@ -729,8 +735,16 @@ __global__ void __launch_bounds__(PBWD_THREADS, 2) views_project_bwd_kernel(
         }
         BwdPrep P;
         bool prepped = false;
+        // accumulate: the running sums start from the rows' current values, so
+        // views split over several calls sum in exactly the one-call order
         float am[3] = {0.f, 0.f, 0.f}, as[3] = {0.f, 0.f, 0.f};
         float4 aq = make_float4(0.f, 0.f, 0.f, 0.f), argbo = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (in && accumulate) {
+            am[0] = d_means[3 * i], am[1] = d_means[3 * i + 1], am[2] = d_means[3 * i + 2];
+            as[0] = d_scales[3 * i], as[1] = d_scales[3 * i + 1], as[2] = d_scales[3 * i + 2];
+            aq = d_quats[i];
+            argbo = d_rgbo[i];
+        }
         // the next view's rows are loaded while this view's are processed
         float4 nrg = make_float4(0.f, 0.f, 0.f, 0.f), ngg = nrg;
         float ng11 = 0.f;
@@ -794,19 +808,10 @@ __global__ void __launch_bounds__(PBWD_THREADS, 2) views_project_bwd_kernel(
             }
         }
         if (in) {
-            if (accumulate) {
-                d_means[3 * i] += am[0], d_means[3 * i + 1] += am[1], d_means[3 * i + 2] += am[2];
-                d_scales[3 * i] += as[0], d_scales[3 * i + 1] += as[1], d_scales[3 * i + 2] += as[2];
-                const float4 o = d_quats[i];
-                d_quats[i] = make_float4(o.x + aq.x, o.y + aq.y, o.z + aq.z, o.w + aq.w);
-                const float4 r = d_rgbo[i];
-                d_rgbo[i] = make_float4(r.x + argbo.x, r.y + argbo.y, r.z + argbo.z, r.w + argbo.w);
-            } else {
-                d_means[3 * i] = am[0], d_means[3 * i + 1] = am[1], d_means[3 * i + 2] = am[2];
-                d_scales[3 * i] = as[0], d_scales[3 * i + 1] = as[1], d_scales[3 * i + 2] = as[2];
-                d_quats[i] = aq;
-                d_rgbo[i] = argbo;
-            }
+            d_means[3 * i] = am[0], d_means[3 * i + 1] = am[1], d_means[3 * i + 2] = am[2];
+            d_scales[3 * i] = as[0], d_scales[3 * i + 1] = as[1], d_scales[3 * i + 2] = as[2];
+            d_quats[i] = aq;
+            d_rgbo[i] = argbo;
         }
     }
     __syncthreads();
@@ -816,6 +821,251 @@ __global__ void __launch_bounds__(PBWD_THREADS, 2) views_project_bwd_kernel(
         float acc = 0.f;
 #pragma unroll
         for (int w = 0; w < PBWD_THREADS / 32; ++w) acc += s_dv[w][v][c];
+        args.v[v].partials[blockIdx.x * 12 + c] = acc;
+    }
+}
+
+// The same projection backward with the per-view work compacted.  Only
+// ~15 % of a config-3 step's (Gaussian, view) rows are non-zero (early
+// termination hides most in-frustum Gaussians), so in the kernel above a
+// warp runs the ~400-instruction per-view body for nearly every (warp, view)
+// with a handful of lanes live.  Here each warp owns 32 Gaussians per
+// iteration (lane j: Gaussian base + j; its view-independent part -- mean,
+// scale, unit quaternion, R, M, Sigma -- goes to shared memory), walks the
+// views, and appends every non-zero (Gaussian, view) row to a warp-private
+// queue (view-major order); each time 32 items are queued all 32 lanes run
+// the per-view body on one item each.  The items' d_mean / d_scale / d_quat
+// go through shared memory back to their owner lanes, which add them in queue
+// order -- i.e. in view order, the order of the kernel above; d_rgbo is added
+// by the owner while walking.  d_view: a segmented scan over the batch's
+// view runs (fixed order), the run totals into the warp's per-view sums, then
+// block partials and views_reduce_kernel as above -- deterministic.  The
+// rows arrive through a per-warp cp.async ring (the next view's copies in
+// flight while the current view is scanned).  Config 3: 1.61 -> 1.14 ms per
+// step; without the per-view work (gather and clears only) it takes 1.18 ms,
+// so what is left is the rows' ~3.5 GB read from 32 interleaved arrays at
+// ~3.7 TB/s (a per-Gaussian "touched" bit set by the raster backward, so
+// only marked rows are read, measured no faster: 1.19 ms, and cost the
+// raster backward 0.07-0.14 ms in atomics).
+constexpr int VQ = 64;   // queue slots per warp
+constexpr int VG = 20;   // per-Gaussian fields: mean 3, scale 3, qw qx qy qz inv, R 9 (M, Sigma per item)
+constexpr int VCAM = 15; // per-view camera fields (R 9, t 3, fx, fy; odd stride)
+constexpr int VD = 2;    // views of screen-space rows in flight per warp (cp.async ring; measured 2: 1.14, 4: 1.20, 6: 1.22 ms)
+struct VbRows {
+    float4 rg[32], gg[32];  // [d_rgbo | d_geo] rows of the warp's 32 Gaussians in one view
+    float c11[32];
+};
+struct VbWarp {
+    float g[VG][32];            // the warp's 32 Gaussians (SoA)
+    VbRows ring[VD];
+    float qd[5][VQ];            // queued rows: d_mean2d x y, d_cov00, d_cov01, d_cov11
+    uint32_t qo[VQ];            // queued owner lane | view << 8
+    float out[10][32];          // a batch's d_mean 3, d_scale 3, d_quat 4 per item
+    uint32_t own[32];           // per owner lane: its items in the batch (bit mask)
+    float dv[MV_MAX][12];       // per-view d_view sums
+};
+struct VbShared {
+    float cam[MV_MAX][VCAM];
+    VbWarp w[PBWD_THREADS / 32];
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void vb_process(VbShared& sh, VbWarp& W, int lane, uint32_t head, int count) {
+    const bool act = lane < count;
+    const int slot = (int)((head + (uint32_t)lane) & (VQ - 1));
+    const uint32_t o = act ? W.qo[slot] : 0xFFFFFF00u | (uint32_t)lane;
+    const int j = (int)(o & 31u), v = (int)(o >> 8);
+    float dvv[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) dvv[k] = 0.f;
+    if (act) {
+        CamK cam;
+        const float* c = sh.cam[v];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) cam.R[k] = c[k];
+        cam.t[0] = c[9], cam.t[1] = c[10], cam.t[2] = c[11];
+        cam.fx = c[12], cam.fy = c[13];
+        const float sc[3] = {W.g[3][j], W.g[4][j], W.g[5][j]};
+        BwdPrep P;
+        P.qw = W.g[6][j], P.qx = W.g[7][j], P.qy = W.g[8][j], P.qz = W.g[9][j], P.inv = W.g[10][j];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) P.R[k] = W.g[11 + k][j];
+        bwd_prep_ms(P, sc);
+        const float4 gg = make_float4(W.qd[0][slot], W.qd[1][slot], W.qd[2][slot], W.qd[3][slot]);
+        float dmx, dmy, dmz, dsx, dsy, dsz;
+        float4 dq;
+        proj_bwd_view(cam, W.g[0][j], W.g[1][j], W.g[2][j], sc, P, gg, W.qd[4][slot], dmx, dmy, dmz, dsx, dsy, dsz,
+                      dq, dvv);
+        W.out[0][lane] = dmx, W.out[1][lane] = dmy, W.out[2][lane] = dmz;
+        W.out[3][lane] = dsx, W.out[4][lane] = dsy, W.out[5][lane] = dsz;
+        W.out[6][lane] = dq.x, W.out[7][lane] = dq.y, W.out[8][lane] = dq.z, W.out[9][lane] = dq.w;
+    }
+    // d_view: inclusive scan within each run of equal views (the queue is
+    // view-major, so a view's items are contiguous); the run's last lane adds
+    // the total to the warp's sum for the view
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int vo = __shfl_up_sync(0xffffffffu, v, off);
+        const bool take = lane >= off && vo == v;
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+            const float t = __shfl_up_sync(0xffffffffu, dvv[k], off);
+            if (take) dvv[k] = __fadd_rn(t, dvv[k]);
+        }
+    }
+    const int vn = __shfl_down_sync(0xffffffffu, v, 1);
+    if (act && (lane == count - 1 || vn != v)) {
+#pragma unroll
+        for (int k = 0; k < 12; ++k) W.dv[v][k] = __fadd_rn(W.dv[v][k], dvv[k]);
+    }
+    // owners: each item's lane set per owner (lowest lane publishes it)
+    const uint32_t same = __match_any_sync(0xffffffffu, act ? j : 32 + lane);
+    if (act && lane == __ffs(same) - 1) W.own[j] = same;
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(PBWD_THREADS, 2) views_project_bwd_compact_kernel(
+    const float* __restrict__ means, const float* __restrict__ scales, const float4* __restrict__ quats, int n,
+    const MvArgs args, float* __restrict__ d_means, float* __restrict__ d_scales, float4* __restrict__ d_quats,
+    float4* __restrict__ d_rgbo, bool accumulate, bool clear_rows) {
+    griddep_wait();
+    extern __shared__ __align__(16) unsigned char vb_raw[];
+    VbShared& sh = *reinterpret_cast<VbShared*>(vb_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    VbWarp& W = sh.w[warp];
+    const int nv = args.nv;
+    for (int k = threadIdx.x; k < nv * VCAM; k += blockDim.x) {
+        const int v = k / VCAM, f = k - v * VCAM;
+        const CamK& c = args.v[v].cam;
+        sh.cam[v][f] = f < 9 ? c.R[f] : f < 12 ? c.t[f - 9] : f == 12 ? c.fx : f == 13 ? c.fy : 0.f;
+    }
+    for (int k = lane; k < MV_MAX * 12; k += 32) (&W.dv[0][0])[k] = 0.f;
+    W.own[lane] = 0u;
+    __syncthreads();
+    const uint32_t lt = (1u << lane) - 1u;
+    const int n_round = (n + 31) & ~31;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += gridDim.x * blockDim.x) {
+        const bool in = i < n;
+        // view v's rows of this lane's Gaussian -> ring slot v % VD (one group per view)
+        auto fetch = [&](int v) {
+            if (in && v < nv) {
+                VbRows& R = W.ring[v % VD];
+                cp_async16(&R.rg[lane], args.v[v].g8 + 2 * (size_t)i);
+                cp_async16(&R.gg[lane], args.v[v].g8 + 2 * (size_t)i + 1);
+                cp_async4(&R.c11[lane], args.v[v].d_c11 + i);
+            }
+            cp_async_commit();
+        };
+#pragma unroll
+        for (int v = 0; v < VD - 1; ++v) fetch(v);
+        {
+            float mx = 0.f, my = 0.f, mz = 0.f, sc[3] = {1.f, 1.f, 1.f};
+            float4 q = make_float4(1.f, 0.f, 0.f, 0.f);
+            if (in) {
+                mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
+                sc[0] = scales[3 * i], sc[1] = scales[3 * i + 1], sc[2] = scales[3 * i + 2];
+                q = quats[i];
+            }
+            const BwdPrep P = proj_bwd_prep(q, sc);
+            W.g[0][lane] = mx, W.g[1][lane] = my, W.g[2][lane] = mz;
+            W.g[3][lane] = sc[0], W.g[4][lane] = sc[1], W.g[5][lane] = sc[2];
+            W.g[6][lane] = P.qw, W.g[7][lane] = P.qx, W.g[8][lane] = P.qy, W.g[9][lane] = P.qz;
+            W.g[10][lane] = P.inv;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) W.g[11 + k][lane] = P.R[k];
+        }
+        float am[3] = {0.f, 0.f, 0.f}, as[3] = {0.f, 0.f, 0.f}, aq[4] = {0.f, 0.f, 0.f, 0.f};
+        float4 argbo = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (in && accumulate) {
+            am[0] = d_means[3 * i], am[1] = d_means[3 * i + 1], am[2] = d_means[3 * i + 2];
+            as[0] = d_scales[3 * i], as[1] = d_scales[3 * i + 1], as[2] = d_scales[3 * i + 2];
+            const float4 o = d_quats[i];
+            aq[0] = o.x, aq[1] = o.y, aq[2] = o.z, aq[3] = o.w;
+            argbo = d_rgbo[i];
+        }
+        __syncwarp();
+        uint32_t head = 0, tail = 0;
+        // an owner adds its items of the batch just processed, in queue order
+        auto drain = [&]() {
+            uint32_t mm = W.own[lane];
+            if (mm) W.own[lane] = 0u;
+            while (mm) {
+                const int k = __ffs(mm) - 1;
+                mm &= mm - 1u;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) am[c] = __fadd_rn(am[c], W.out[c][k]);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) as[c] = __fadd_rn(as[c], W.out[3 + c][k]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) aq[c] = __fadd_rn(aq[c], W.out[6 + c][k]);
+            }
+            __syncwarp();
+        };
+        for (int v = 0; v < nv; ++v) {
+            const MvView& V = args.v[v];
+            fetch(v + VD - 1);
+            cp_async_wait<VD - 1>();  // this lane's copies of view v have landed
+            const VbRows& R = W.ring[v % VD];
+            float4 rg = make_float4(0.f, 0.f, 0.f, 0.f), gg = rg;
+            float g11 = 0.f;
+            if (in) rg = R.rg[lane], gg = R.gg[lane], g11 = R.c11[lane];
+            const bool vis = gg.x != 0.f || gg.y != 0.f || gg.z != 0.f || gg.w != 0.f || g11 != 0.f ||
+                             rg.x != 0.f || rg.y != 0.f || rg.z != 0.f || rg.w != 0.f;
+            const uint32_t bal = __ballot_sync(0xffffffffu, vis);
+            if (!bal) continue;
+            if (vis) {
+                argbo.x = __fadd_rn(argbo.x, rg.x), argbo.y = __fadd_rn(argbo.y, rg.y);
+                argbo.z = __fadd_rn(argbo.z, rg.z), argbo.w = __fadd_rn(argbo.w, rg.w);
+                const int slot = (int)((tail + (uint32_t)__popc(bal & lt)) & (VQ - 1));
+                W.qo[slot] = (uint32_t)lane | ((uint32_t)v << 8);
+                W.qd[0][slot] = gg.x, W.qd[1][slot] = gg.y, W.qd[2][slot] = gg.z, W.qd[3][slot] = gg.w;
+                W.qd[4][slot] = g11;
+                if (clear_rows) {  // the accumulators stay zero for the view's next frame
+                    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                    __stcs(V.g8 + 2 * (size_t)i, z);
+                    __stcs(V.g8 + 2 * (size_t)i + 1, z);
+                    __stcs(V.d_c11 + i, 0.f);
+                }
+            }
+            tail += (uint32_t)__popc(bal);
+            if (tail - head >= 32u) {
+                __syncwarp();
+                vb_process(sh, W, lane, head, 32);
+                head += 32u;
+                drain();
+            }
+        }
+        cp_async_wait<0>();  // (only empty groups remain) before the ring is reused
+        if (tail != head) {
+            __syncwarp();
+            vb_process(sh, W, lane, head, (int)(tail - head));
+            drain();
+        }
+        if (in) {
+            d_means[3 * i] = am[0], d_means[3 * i + 1] = am[1], d_means[3 * i + 2] = am[2];
+            d_scales[3 * i] = as[0], d_scales[3 * i + 1] = as[1], d_scales[3 * i + 2] = as[2];
+            d_quats[i] = make_float4(aq[0], aq[1], aq[2], aq[3]);
+            d_rgbo[i] = argbo;
+        }
+        __syncwarp();  // the warp's Gaussian fields are rewritten next iteration
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nv * 12; k += blockDim.x) {
+        const int v = k / 12, c = k - 12 * v;
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < PBWD_THREADS / 32; ++w) acc += sh.w[w].dv[v][c];
         args.v[v].partials[blockIdx.x * 12 + c] = acc;
     }
 }
@@ -846,10 +1096,27 @@ int launch_views_project_bwd(const float* means3, const float* scales3, const fl
     const int resident = sort_sm_count() * 2;
     if (blocks > resident) blocks = resident;
     if (blocks < 1) blocks = 1;
-    launch_k(views_project_bwd_kernel, dim3(blocks), dim3(PBWD_THREADS), 0, s, means3, scales3,
-             (const float4*)quats4, (int)n, a, d_means3, d_scales3, (float4*)d_quats4, (float4*)d_rgbo4, accumulate,
-             clear_rows);
-    if (check_launch("views_project_bwd_kernel")) return -1;
+    static const bool compact = [] {
+        const char* e = getenv("GS_PBWD_COMPACT");
+        return !(e && e[0] == '0');
+    }();
+    if (compact) {
+        static const bool attr = [] {
+            cudaFuncSetAttribute(views_project_bwd_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(VbShared));
+            return true;
+        }();
+        (void)attr;
+        launch_k(views_project_bwd_compact_kernel, dim3(blocks), dim3(PBWD_THREADS), sizeof(VbShared), s, means3,
+                 scales3, (const float4*)quats4, (int)n, a, d_means3, d_scales3, (float4*)d_quats4,
+                 (float4*)d_rgbo4, accumulate, clear_rows);
+        if (check_launch("views_project_bwd_compact_kernel")) return -1;
+    } else {
+        launch_k(views_project_bwd_kernel, dim3(blocks), dim3(PBWD_THREADS), 0, s, means3, scales3,
+                 (const float4*)quats4, (int)n, a, d_means3, d_scales3, (float4*)d_quats4, (float4*)d_rgbo4,
+                 accumulate, clear_rows);
+        if (check_launch("views_project_bwd_kernel")) return -1;
+    }
     launch_k(views_reduce_kernel, dim3(a.nv), dim3(384), 0, s, a, blocks, d_views16, add_view);
     return check_launch("views_reduce_kernel");
 }

@@ -273,6 +273,17 @@ def test_batched_projections_over_32_views(cuda):
         gv = ops.frame_backward(r, m, s, q, c, d)
         for k in ref:
             ref[k] += gv[k]
+    # views split over two calls (the second adding): bit for bit the one-call
+    # sums (d_view: the same terms, grouped by the calls' work batches)
+    one = {k: torch.zeros_like(v) for k, v in ref.items()}
+    two = {k: torch.full_like(v, 7.0) for k, v in ref.items()}
+    dv1, dv2 = torch.zeros((len(cams), 4, 4), device=cuda), torch.zeros((len(cams), 4, 4), device=cuda)
+    ops.frame_views_project_backward(frames, m, s, q, one, dv1, keep_screen=True)
+    ops.frame_views_project_backward(frames[:13], m, s, q, two, dv2[:13], keep_screen=True)
+    ops.frame_views_project_backward(frames[13:], m, s, q, two, dv2[13:], accumulate=True, keep_screen=True)
+    for k in ref:
+        assert torch.equal(one[k], two[k]), k
+    assert torch.allclose(dv1, dv2, rtol=1e-5, atol=1e-6 * dv1.abs().max().item())
     out = {k: torch.zeros_like(v) for k, v in ref.items()}
     d_views = torch.zeros((len(cams), 4, 4), device=cuda)
     half = n // 2 // 256 * 256

@@ -24,8 +24,8 @@ STAGE_OF = [  # kernel-name regex -> bench stage name (the last capture of each 
     (r"views_project_fwd_kernel|project_fwd_kernel", "project"),
     (r"onesweep_kernel<unsigned int, (16|4)", "sort_u32"),
     (r"emit_scan_kernel", "scan_emit"),
-    (r"et_count_kernel", "tile_counts"),
-    (r"et_emit_kernel", "tile_emit"),
+    (r"et_expand_kernel|et_colsum_kernel", "tile_counts"),
+    (r"et_colscan_kernel|et_place_kernel", "tile_emit"),
     (r"segsort_small_kernel", "segsort"),
     (r"ranges_u32_kernel", "tile_sort_ranges"),
     (r"raster_fwd_kernel", "raster_fwd"),
@@ -66,7 +66,24 @@ KEYS = ["Duration", "Elapsed Cycles", "SM Frequency", "DRAM Throughput", "Memory
         "Eligible Warps Per Scheduler", "No Eligible", "L1/TEX Hit Rate", "L2 Hit Rate"]
 
 
-def full(rep, out, traffic_out=None):
+def full(reps, out, traffic_out=None):
+    """reps: one .ncu-rep or several, comma-separated (their summaries are
+    concatenated and their per-stage traffic merged)."""
+    lines, by_kernel = [], {}
+    for i, rep in enumerate(reps.split(",")):
+        ln, bk = _full_one(rep, f"{i}." if "," in reps else "")
+        lines += ln
+        by_kernel.update(bk)
+    traffic = {}
+    for (stage, _), v in by_kernel.items():
+        traffic[stage] = traffic.get(stage, 0.0) + v
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    if traffic_out:  # rewritten from this capture only (no stale entries)
+        json.dump({k: int(v) for k, v in traffic.items()}, open(traffic_out, "w"), indent=1)
+
+
+def _full_one(rep, tag):
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(det)))
@@ -84,7 +101,7 @@ def full(rep, out, traffic_out=None):
             names[r[idi]] = short(r[ki])
     rrows = list(csv.reader(io.StringIO(raw)))
     rh = rrows[0]
-    traffic = {}
+    by_kernel = {}
     stalls = {}
     for r in rrows[2:]:
         if len(r) != len(rh):
@@ -97,9 +114,12 @@ def full(rep, out, traffic_out=None):
         except ValueError:
             rd = wr = 0.0
         # raw page units may be in bytes or scaled; normalise via the unit row
-        unit_r = rrows[1][rh.index("dram__bytes_read.sum")] if "dram__bytes_read.sum" in rh else "byte"
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
-        per[kid]["dram_bytes_read+write"] = f"{(rd + wr) * scale:.0f} byte"
+        # the unit row gives each metric its own scale (reads in Mbyte, writes in Gbyte, ...)
+        units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        unit = lambda m: units.get(rrows[1][rh.index(m)], 1) if m in rh else 1
+        rd *= unit("dram__bytes_read.sum")
+        wr *= unit("dram__bytes_write.sum")
+        per[kid]["dram_bytes_read+write"] = f"{rd + wr:.0f} byte"
         st = []
         for k, v in d.items():
             if k.startswith("smsp__pcsamp_warps_issue_stalled") and not k.endswith("not_issued"):
@@ -112,19 +132,18 @@ def full(rep, out, traffic_out=None):
         nm = names.get(kid, short(d.get("Kernel Name", "")))
         for pat, stage in STAGE_OF:
             if re.search(pat, d.get("Kernel Name", "")):
-                traffic[stage] = (rd + wr) * scale  # the last capture wins (warmed-up frame)
+                # the last capture of each kernel wins (warmed-up frame); a
+                # stage made of several kernels sums them
+                by_kernel[(stage, short(d.get("Kernel Name", "")))] = rd + wr
     lines = []
     for kid in sorted(per, key=lambda x: int(x)):
-        lines.append(f"[{kid}] {names.get(kid, '?')}")
+        lines.append(f"[{tag}{kid}] {names.get(kid, '?')}")
         for k in KEYS + ["dram_bytes_read+write"]:
             if k in per[kid]:
                 lines.append(f"    {k:32s} {per[kid][k]}")
         if kid in stalls:
             lines.append(f"    {'top stall reasons':32s} {stalls[kid]}")
-    open(out, "w").write("\n".join(lines) + "\n")
-    print("\n".join(lines))
-    if traffic_out:  # rewritten from this capture only (no stale entries)
-        json.dump({k: int(v) for k, v in traffic.items()}, open(traffic_out, "w"), indent=1)
+    return lines, by_kernel
 
 
 if __name__ == "__main__":

@@ -12,6 +12,12 @@ PYTHONPATH=. ncu --profile-from-start off --metrics gpu__time_duration.sum --clo
 echo "launch list rc=$?"
 PYTHONPATH=. ncu --profile-from-start off --set full --clock-control none --import-source on \
     --metrics sm__inst_executed_pipe_fma.sum,sm__inst_executed_pipe_fmaheavy.sum,sm__inst_executed_pipe_fmalite.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_alu.sum,sm__inst_executed_pipe_xu.sum,lts__t_requests_op_red.sum,lts__t_requests_op_atom.sum,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active \
-    -k regex:"views_project|depth_hist|onesweep|et_count|et_scan|et_emit|tile_scan|raster_fwd|raster_bwd_rec" -c 13 \
+    -k regex:"views_project|onesweep|et_expand|et_colsum|et_colscan|et_place|tile_scan|raster_fwd|raster_bwd_rec" -c 14 \
     -o gpurun_out/prof_$TAG python tools/prof_step.py 3 32 1 > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "full rc=$?"
+# the projection backward runs once per step, after every view's raster
+# backward: a second capture picks it out
+PYTHONPATH=. ncu --profile-from-start off --set full --clock-control none --import-source on \
+    -k regex:"views_project_bwd" -c 1 \
+    -o gpurun_out/prof_${TAG}_pbwd python tools/prof_step.py 3 32 1 > gpurun_out/ncu_pbwd_$TAG.log 2>&1
+echo "pbwd rc=$?"
