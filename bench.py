@@ -238,7 +238,7 @@ def run_ours(args):
     # roofline numerators: evaluation-class counts of a counted pass (untimed)
     counts_f = np.zeros(4, np.int64)
     counts_b = np.zeros(3, np.int64)
-    caps, wss, isect, binnings, visible = [], [], [], [], []
+    caps, wss, isect, binnings, visible, touched = [], [], [], [], [], []
     for cam, d_img in zip(cams, d_imgs):
         fr = ops.frame_forward(m, s, q, o, c, cam, bg, True, counts=True)
         g = ops.frame_backward(fr, m, s, q, c, d_img, counts=True)
@@ -251,6 +251,10 @@ def run_ours(args):
         cap = int(fr.needed_capacity * 1.05) + 4096
         caps.append(cap)
         visible.append(min(int(fr.meta().cpu()[7]), n))  # depth-first: the depth-sorted (visible) Gaussians
+        # the Gaussians with non-zero screen-space rows (the ones the projection backward clears)
+        ops.frame_backward(fr, m, s, q, c, d_img, project=False)
+        rows, c11 = ops.frame_screen_grads(fr)
+        touched.append(int(((rows != 0).any(1) | (c11 != 0)).sum()))
         binnings.append(fr.binning)
         wss.append(ops.frame_workspace(n, cap, cam.width, cam.height, dev))
         del fr
@@ -471,6 +475,7 @@ def run_ours(args):
     direct = binning == "direct"
     fused = fused_sort(n, cams[0])
     vis = float(sum(visible))  # visible Gaussians over the rank's views (the depth-sorted ones)
+    nz = float(sum(touched))  # (Gaussian, view) pairs with non-zero screen-space gradient rows
     chunks_x_tiles = float(sum(((v + 2047) // 2048) * ((cm.tiles_x * cm.tiles_y + 1) & ~1)
                                for v, cm in zip(visible, cams)))
     work = {
@@ -508,9 +513,9 @@ def run_ours(args):
         # read-modify-write the running sums
         # batched over the views (one pass): parameters read once (40 B) and the sums written once
         # (56 B) per Gaussian; per view the screen-space rows read (36 B, every Gaussian) and
-        # cleared (36 B, the visible ones) -- §8(d)'s per-view 104 B would count the parameter
+        # cleared (36 B, the non-zero ones) -- §8(d)'s per-view 104 B would count the parameter
         # traffic once per view
-        "project_bwd": ("hbm", (96.0 * n + 36.0 * n * nv + 36.0 * vis) if batched else 104.0 * n * nv),
+        "project_bwd": ("hbm", (96.0 * n + 36.0 * n * nv + 36.0 * nz) if batched else 104.0 * n * nv),
     }
     st = {}
     for name, ms in zip(stage_names, stage_ms):
@@ -578,6 +583,7 @@ def run_ours(args):
                                l2="flushed between timed steps (192 MiB write, untimed)"),
         "evals_per_s": round(evals_per_s, 1), "evals_per_step": evals_step,
         "intersections_per_step_rank": int(I),
+        "visible_per_step_rank": int(vis), "nonzero_grad_rows_per_step_rank": int(nz),
         "e2e": e2e,
         # per view (csrc/frame.cu): direct binning: init, project (+ pairs into the tile bins),
         # raster fwd (+ the per-tile sort) | raster bwd, project bwd, view reduce; scatter binning:

@@ -30,7 +30,7 @@ STAGE_OF = [  # kernel-name regex -> bench stage name (the last capture of each 
     (r"ranges_u32_kernel", "tile_sort_ranges"),
     (r"raster_fwd_kernel", "raster_fwd"),
     (r"raster_bwd_rec_kernel", "raster_bwd"),
-    (r"views_project_bwd_kernel|project_bwd_kernel", "project_bwd"),
+    (r"views_project_bwd|project_bwd_kernel", "project_bwd"),
 ]
 
 
