@@ -512,10 +512,10 @@ def run_ours(args):
         # d_color/d_opacity row (16 + 16), clears the rows it read, and views after the first
         # read-modify-write the running sums
         # batched over the views (one pass): parameters read once (40 B) and the sums written once
-        # (56 B) per Gaussian; per view the screen-space rows read (36 B, every Gaussian) and
-        # cleared (36 B, the non-zero ones) -- §8(d)'s per-view 104 B would count the parameter
-        # traffic once per view
-        "project_bwd": ("hbm", (96.0 * n + 36.0 * n * nv + 36.0 * nz) if batched else 104.0 * n * nv),
+        # (56 B) per Gaussian; per view the raster backward's marks (1 bit per Gaussian) and the
+        # marked rows read (36 B) and cleared (36 B) -- §8(d)'s per-view 104 B would count the
+        # parameter traffic once per view
+        "project_bwd": ("hbm", (96.0 * n + n * nv / 8.0 + 72.0 * nz) if batched else 104.0 * n * nv),
     }
     st = {}
     for name, ms in zip(stage_names, stage_ms):

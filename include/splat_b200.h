@@ -217,6 +217,11 @@ typedef struct gs_frame_view {
     uint32_t* depth_order_alt;  /* depth-first binning: the visible Gaussians (meta[7] of them) by
                                    (depth, index) are in depth_order_alt when meta[8] (the depth-sort
                                    pass count) is odd, else in depth_order */
+    uint32_t* touched;          /* (ceil(n/32)) bit i: the frame's raster backward added to Gaussian
+                                   i's rows (cleared by every gs_frame_forward);
+                                   gs_frame_views_project_backward reads only the marked rows.  A
+                                   caller that writes the rows itself (e.g. sums them over ranks)
+                                   sets every bit first */
 } gs_frame_view;
 
 size_t gs_frame_workspace_bytes(int64_t n, int64_t isect_capacity, int32_t width, int32_t height);
@@ -297,13 +302,14 @@ int gs_frame_project_backward(const float* means3, const float* scales3, const f
  * (sg/proj_backward.py:178-223 per view, summed over the views): after each
  * view's gs_frame_backward with flag bit 3 (raster backward only; every view
  * on its own workspace), one pass over Gaussians [begin, end) reads the
- * parameters once and every view's screen-space gradient rows, and writes
+ * parameters once and every view's screen-space gradient rows that view's
+ * raster backward marked (gs_frame_view.touched; unmarked rows are zero), and writes
  * (flag bit 0: adds to) d_means3 / d_scales3 / d_quats4 / d_rgbo4 the sums
  * over the views, and d_views16 (n_views x 16, flag bit 4: added) per view.
  * Adding continues each row's running sum in view order (the row's current
  * value first), so views split over several calls give bit-identical sums.
- * A Gaussian counts as visible in a view iff its rows there are non-zero (a
- * culled one's rows are never written; zero rows contribute exactly zero).
+ * A Gaussian counts as visible in a view iff it is marked there (a culled
+ * one is never marked; marked zero rows contribute exactly zero).
  * The rows read are cleared unless flag bit 1 keeps them; the call whose
  * range ends at n stamps each workspace clean (its rows all cleared: calls
  * over earlier ranges must not keep theirs) or, keeping, not clean.  cams / capacities / workspaces / ws_bytes: [host] n_views

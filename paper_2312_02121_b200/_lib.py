@@ -54,7 +54,8 @@ class GsFrameView(C.Structure):
     _fields_ = [(name, C.c_void_p) for name in (
         "xydr4", "conic4", "tiles", "depth_order", "sorted_tile_keys", "sorted_vals", "ranges2", "meta",
         "d_geo4", "d_c11", "bwd_accum")] + [("bwd_accum_bytes", C.c_size_t), ("rec_count", C.c_void_p),
-                                                       ("depth_order_alt", C.c_void_p)]
+                                                       ("depth_order_alt", C.c_void_p),
+                                                       ("touched", C.c_void_p)]
 
 
 class SplatLibError(RuntimeError):

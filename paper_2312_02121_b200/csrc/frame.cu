@@ -76,7 +76,7 @@ struct Layout {
     size_t xydr, conic, tiles, dkeys, dkeys_alt, order, order_alt, offsets;
     size_t tkeys, tkeys_alt, tvals, tvals_alt, ranges, rec, rec_count, tile_order, tcount, clean;
     // zeroed region
-    size_t zero_begin, meta, dhist, thist, counters, scan_ws, dstatus, tstatus, zero_end;
+    size_t zero_begin, meta, dhist, thist, counters, scan_ws, touched, dstatus, tstatus, zero_end;
     // backward
     size_t etable;  // tile-sorted emission: per-(chunk, tile) counts and prefixes
     size_t d_geo, d_c11, pbwd_done, partials;
@@ -121,6 +121,7 @@ Layout layout(int64_t n, int64_t cap, int W, int H) {
     L.counters = take(64);
     L.scan_ws = take(emit_scan_ws_bytes(n));
     L.ranges = take(8 * nt);
+    L.touched = take(4 * ((n + 31) / 32));  // Gaussians the raster backward added to (bit per Gaussian)
     L.dstatus = take(onesweep_status_bytes<uint32_t>(n, 4));  // sized for either pass variant; the used part is zeroed
     L.zero_end = o;
     L.tstatus = take(onesweep_status_bytes<uint32_t>(cap, tp));  // tile passes (depth-first without the tile emission)
@@ -235,6 +236,7 @@ int gs_frame_view_of(int64_t n, int64_t isect_capacity, int32_t width, int32_t h
     out->bwd_accum = at<char>(ws, L.d_geo);
     out->bwd_accum_bytes = L.partials - L.d_geo;
     out->rec_count = at<uint32_t>(ws, L.rec_count);
+    out->touched = at<uint32_t>(ws, L.touched);
     return 0;
 }
 
@@ -494,11 +496,14 @@ int gs_frame_backward(const float* means3, const float* scales3, const float* qu
                               colors3, bg, W, H, final_T, n_contrib, d_image, g8, g8 + 4, at<float>(ws, L.d_c11),
                               counts3, s, 2))
             return -1;
+        // the list-walking backward does not mark the Gaussians it adds to: all count as touched
+        if (cudaMemsetAsync(at<uint32_t>(ws, L.touched), 0xFF, 4 * ((n + 31) / 32), s) != cudaSuccess)
+            return set_error("gs_frame_backward: memset failed");
     } else if (launch_raster_bwd_rec(at<uint2>(ws, L.ranges), at<uint2>(ws, L.rec), at<uint32_t>(ws, L.rec_count),
                                      at<float>(ws, L.xydr), at<float>(ws, L.conic), colors3, bg, W, H, final_T,
                                      n_contrib, d_image, g8, at<float>(ws, L.d_c11), s,
                                      tile_order_enabled(tiles_x * tiles_y) ? at<uint32_t>(ws, L.tile_order) : nullptr,
-                                     at<unsigned long long>(ws, L.meta))) {
+                                     at<unsigned long long>(ws, L.meta), at<uint32_t>(ws, L.touched))) {
         return -1;
     }
     mark(stage_events, 1, s);
@@ -579,6 +584,8 @@ int gs_frame_views_project_backward(const float* means3, const float* scales3, c
             V.cam = make_camk(c);
             V.g8 = at<float4>(ws, L.d_geo) + 2 * begin;
             V.d_c11 = at<float>(ws, L.d_c11) + begin;
+            V.touched = at<uint32_t>(ws, L.touched);
+            V.tbase = (int)begin;
             V.partials = at<float>(ws, L.partials);
             // the call whose range ends at n declares the workspace's rows clear (the
             // earlier ranges' calls cleared theirs) or, keeping its rows, dirty

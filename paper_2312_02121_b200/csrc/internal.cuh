@@ -40,6 +40,10 @@ struct MvView {
     CamK cam;
     float4* g8;
     float* d_c11;
+    // bit (tbase + i) of touched clear: Gaussian i's rows are zero (the raster
+    // backward marks every Gaussian it adds to; nullptr: read every row)
+    const uint32_t* touched;
+    int tbase;
     float* partials;
     unsigned long long* clean_word;
     unsigned long long clean_stamp;
@@ -158,7 +162,8 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
 int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
                           const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s,
-                          const uint32_t* tile_order = nullptr, const unsigned long long* meta = nullptr);
+                          const uint32_t* tile_order = nullptr, const unsigned long long* meta = nullptr,
+                          uint32_t* touched = nullptr);
 int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, const float* fT, const int* nc,
                       const float* dimg, float* d_rgbo4, float* d_geo4, float* d_c11, unsigned long long* counts,

@@ -826,70 +826,80 @@ __global__ void __launch_bounds__(PBWD_THREADS, 2) views_project_bwd_kernel(
 }
 
 // The same projection backward with the per-view work compacted.  Only
-// ~15 % of a config-3 step's (Gaussian, view) rows are non-zero (early
+// ~9 % of a config-3 step's (Gaussian, view) rows are non-zero (early
 // termination hides most in-frustum Gaussians), so in the kernel above a
 // warp runs the ~400-instruction per-view body for nearly every (warp, view)
-// with a handful of lanes live.  Here each warp owns 32 Gaussians per
-// iteration (lane j: Gaussian base + j; its view-independent part -- mean,
-// scale, unit quaternion, R, M, Sigma -- goes to shared memory), walks the
-// views, and appends every non-zero (Gaussian, view) row to a warp-private
-// queue (view-major order); each time 32 items are queued all 32 lanes run
-// the per-view body on one item each.  The items' d_mean / d_scale / d_quat
-// go through shared memory back to their owner lanes, which add them in queue
-// order -- i.e. in view order, the order of the kernel above; d_rgbo is added
-// by the owner while walking.  d_view: a segmented scan over the batch's
-// view runs (fixed order), the run totals into the warp's per-view sums, then
-// block partials and views_reduce_kernel as above -- deterministic.  The
-// rows arrive through a per-warp cp.async ring (the next view's copies in
-// flight while the current view is scanned).  Config 3: 1.61 -> 1.14 ms per
-// step; without the per-view work (gather and clears only) it takes 1.18 ms,
-// so what is left is the rows' ~3.5 GB read from 32 interleaved arrays at
-// ~3.7 TB/s (a per-Gaussian "touched" bit set by the raster backward, so
-// only marked rows are read, measured no faster: 1.19 ms, and cost the
-// raster backward 0.07-0.14 ms in atomics).
-constexpr int VQ = 64;   // queue slots per warp
-constexpr int VG = 20;   // per-Gaussian fields: mean 3, scale 3, qw qx qy qz inv, R 9 (M, Sigma per item)
-constexpr int VCAM = 15; // per-view camera fields (R 9, t 3, fx, fy; odd stride)
-constexpr int VD = 2;    // views of screen-space rows in flight per warp (cp.async ring; measured 2: 1.14, 4: 1.20, 6: 1.22 ms)
-struct VbRows {
-    float4 rg[32], gg[32];  // [d_rgbo | d_geo] rows of the warp's 32 Gaussians in one view
-    float c11[32];
-};
+// with a few lanes live, and reads every row to find the non-zero ones.
+// Here the raster backward marks every Gaussian it adds to (one bit per
+// Gaussian and view, gs_frame_view.touched, cleared by the forward), and each
+// warp owns 32 Gaussians per iteration: lane v reads view v's 32 marks, the
+// marked (view, Gaussian) pairs become a view-major item list in shared
+// memory (a warp prefix sum over the lanes' counts), the view-independent
+// part of each Gaussian (mean, scale, unit quaternion, R) goes to shared
+// memory, and the per-view body runs on 32 items at a time, one per lane --
+// its rows loaded a batch ahead and cleared after use.  The items' d_mean /
+// d_scale / d_quat / d_rgbo go through shared memory back to their owner
+// lanes, which add them in item order, i.e. in view order (the order of the
+// kernel above).  d_view: a segmented scan over the batch's view runs (fixed
+// order), the run totals into the warp's per-view sums, then block partials
+// and views_reduce_kernel as above -- deterministic.  Config 3: 1.61 ->
+// 0.57 ms per step; reading every row and queueing the non-zero ones instead
+// took 1.14 ms (bound by the 3.5 GB of rows), a per-view walk with the marks
+// 0.86 ms (~100 instructions per (warp, view)); clearing a row right after
+// loading it (store behind the load of the same address) took 4.7 ms.
+constexpr int VG = 20;    // per-Gaussian fields: mean 3, scale 3, qw qx qy qz inv, R 9 (M, Sigma per item)
+constexpr int VCAM = 15;  // per-view camera fields (R 9, t 3, fx, fy; odd stride)
 struct VbWarp {
-    float g[VG][32];            // the warp's 32 Gaussians (SoA)
-    VbRows ring[VD];
-    float qd[5][VQ];            // queued rows: d_mean2d x y, d_cov00, d_cov01, d_cov11
-    uint32_t qo[VQ];            // queued owner lane | view << 8
-    float out[10][32];          // a batch's d_mean 3, d_scale 3, d_quat 4 per item
-    uint32_t own[32];           // per owner lane: its items in the batch (bit mask)
-    float dv[MV_MAX][12];       // per-view d_view sums
+    float g[VG][32];              // the warp's 32 Gaussians (SoA)
+    uint16_t items[MV_MAX * 32];  // the marked (view, Gaussian) pairs, view-major: view << 5 | lane
+    float out[14][32];            // a batch's d_mean 3, d_scale 3, d_quat 4, d_rgbo 4 per item
+    uint32_t own[32];             // per owner lane: its items in the batch (bit mask)
+    float dv[MV_MAX][12];         // per-view d_view sums
 };
 struct VbShared {
     float cam[MV_MAX][VCAM];
+    float4* g8[MV_MAX];
+    float* c11[MV_MAX];
     VbWarp w[PBWD_THREADS / 32];
 };
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+// One batch of up to 32 items, one per lane: the item's rows (cleared after
+// reading), the per-view body, the results to shared memory for their
+// owners, d_view by a segmented scan over the batch's view runs.
+// An item's rows (loaded a batch ahead).
+struct VbRow {
+    float4 rg, gg;
+    float g11;
+};
+__device__ __forceinline__ VbRow vb_load(const VbShared& sh, const VbWarp& W, int lane, int i0, int b0, int total) {
+    VbRow r;
+    r.rg = r.gg = make_float4(0.f, 0.f, 0.f, 0.f);
+    r.g11 = 0.f;
+    if (b0 + lane < total) {
+        const uint32_t it = W.items[b0 + lane];
+        const size_t gi = (size_t)(i0 + (int)(it & 31u));
+        const float4* g8 = sh.g8[it >> 5] + 2 * gi;
+        r.rg = g8[0], r.gg = g8[1];
+        r.g11 = sh.c11[it >> 5][gi];
+    }
+    return r;
 }
 
-__device__ __forceinline__ void vb_process(VbShared& sh, VbWarp& W, int lane, uint32_t head, int count) {
+__device__ __forceinline__ void vb_process(VbShared& sh, VbWarp& W, int lane, int i0, int b0, int count,
+                                           bool clear_rows, const VbRow& row) {
     const bool act = lane < count;
-    const int slot = (int)((head + (uint32_t)lane) & (VQ - 1));
-    const uint32_t o = act ? W.qo[slot] : 0xFFFFFF00u | (uint32_t)lane;
-    const int j = (int)(o & 31u), v = (int)(o >> 8);
+    const uint32_t it = act ? W.items[b0 + lane] : 0u;
+    const int j = (int)(it & 31u);
+    const int v = act ? (int)(it >> 5) : 0x10000 + lane;  // (inactive lanes: runs of their own)
     float dvv[12];
 #pragma unroll
     for (int k = 0; k < 12; ++k) dvv[k] = 0.f;
     if (act) {
+        const size_t gi = (size_t)(i0 + j);
+        float4* g8 = sh.g8[v] + 2 * gi;
+        float* c11 = sh.c11[v] + gi;
+        const float4 rg = row.rg, gg = row.gg;
+        const float g11 = row.g11;
         CamK cam;
         const float* c = sh.cam[v];
 #pragma unroll
@@ -902,16 +912,24 @@ __device__ __forceinline__ void vb_process(VbShared& sh, VbWarp& W, int lane, ui
 #pragma unroll
         for (int k = 0; k < 9; ++k) P.R[k] = W.g[11 + k][j];
         bwd_prep_ms(P, sc);
-        const float4 gg = make_float4(W.qd[0][slot], W.qd[1][slot], W.qd[2][slot], W.qd[3][slot]);
         float dmx, dmy, dmz, dsx, dsy, dsz;
         float4 dq;
-        proj_bwd_view(cam, W.g[0][j], W.g[1][j], W.g[2][j], sc, P, gg, W.qd[4][slot], dmx, dmy, dmz, dsx, dsy, dsz,
-                      dq, dvv);
+        proj_bwd_view(cam, W.g[0][j], W.g[1][j], W.g[2][j], sc, P, gg, g11, dmx, dmy, dmz, dsx, dsy, dsz, dq, dvv);
         W.out[0][lane] = dmx, W.out[1][lane] = dmy, W.out[2][lane] = dmz;
         W.out[3][lane] = dsx, W.out[4][lane] = dsy, W.out[5][lane] = dsz;
         W.out[6][lane] = dq.x, W.out[7][lane] = dq.y, W.out[8][lane] = dq.z, W.out[9][lane] = dq.w;
+        W.out[10][lane] = rg.x, W.out[11][lane] = rg.y, W.out[12][lane] = rg.z, W.out[13][lane] = rg.w;
+        // the accumulators stay zero for the view's next frame (cleared well
+        // after the loads: a store right behind the load of the same row stalls
+        // the warp for tens of microseconds)
+        if (clear_rows) {
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            __stcs(g8, z);
+            __stcs(g8 + 1, z);
+            __stcs(c11, 0.f);
+        }
     }
-    // d_view: inclusive scan within each run of equal views (the queue is
+    // d_view: inclusive scan within each run of equal views (the items are
     // view-major, so a view's items are contiguous); the run's last lane adds
     // the total to the warp's sum for the view
 #pragma unroll
@@ -950,6 +968,7 @@ __global__ void __launch_bounds__(PBWD_THREADS, 2) views_project_bwd_compact_ker
         const CamK& c = args.v[v].cam;
         sh.cam[v][f] = f < 9 ? c.R[f] : f < 12 ? c.t[f - 9] : f == 12 ? c.fx : f == 13 ? c.fy : 0.f;
     }
+    if (threadIdx.x < nv) sh.g8[threadIdx.x] = args.v[threadIdx.x].g8, sh.c11[threadIdx.x] = args.v[threadIdx.x].d_c11;
     for (int k = lane; k < MV_MAX * 12; k += 32) (&W.dv[0][0])[k] = 0.f;
     W.own[lane] = 0u;
     __syncthreads();
@@ -957,18 +976,38 @@ __global__ void __launch_bounds__(PBWD_THREADS, 2) views_project_bwd_compact_ker
     const int n_round = (n + 31) & ~31;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += gridDim.x * blockDim.x) {
         const bool in = i < n;
-        // view v's rows of this lane's Gaussian -> ring slot v % VD (one group per view)
-        auto fetch = [&](int v) {
-            if (in && v < nv) {
-                VbRows& R = W.ring[v % VD];
-                cp_async16(&R.rg[lane], args.v[v].g8 + 2 * (size_t)i);
-                cp_async16(&R.gg[lane], args.v[v].g8 + 2 * (size_t)i + 1);
-                cp_async4(&R.c11[lane], args.v[v].d_c11 + i);
+        const int i0 = i - lane;  // the warp's first Gaussian
+        // lane v: view v's marks of the warp's 32 Gaussians (the raster backward
+        // marked every Gaussian it added to; unmarked rows are zero)
+        uint32_t vmark = 0u;
+        if (lane < nv) {
+            vmark = 0xFFFFFFFFu;
+            if (args.v[lane].touched) {
+                const uint32_t a = (uint32_t)(args.v[lane].tbase + i0);
+                const uint32_t* t = args.v[lane].touched + (a >> 5);
+                const uint32_t sh5 = a & 31u;
+                vmark = t[0] >> sh5;
+                if (sh5 && i0 + 32 - (int)sh5 < n) vmark |= t[1] << (32u - sh5);
             }
-            cp_async_commit();
-        };
+            if (n - i0 < 32) vmark &= (1u << (n - i0)) - 1u;
+        }
+        // the items, view-major: lane v writes its marked Gaussians after the lower views'
+        const uint32_t cnt = (uint32_t)__popc(vmark);
+        uint32_t incl = cnt;
 #pragma unroll
-        for (int v = 0; v < VD - 1; ++v) fetch(v);
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = (int)__shfl_sync(0xffffffffu, incl, 31);
+        {
+            uint32_t m = vmark, k = incl - cnt;
+            while (m) {
+                const uint32_t jj = (uint32_t)(__ffs(m) - 1);
+                m &= m - 1u;
+                W.items[k++] = (uint16_t)(((uint32_t)lane << 5) | jj);
+            }
+        }
         {
             float mx = 0.f, my = 0.f, mz = 0.f, sc[3] = {1.f, 1.f, 1.f};
             float4 q = make_float4(1.f, 0.f, 0.f, 0.f);
@@ -985,81 +1024,42 @@ __global__ void __launch_bounds__(PBWD_THREADS, 2) views_project_bwd_compact_ker
 #pragma unroll
             for (int k = 0; k < 9; ++k) W.g[11 + k][lane] = P.R[k];
         }
-        float am[3] = {0.f, 0.f, 0.f}, as[3] = {0.f, 0.f, 0.f}, aq[4] = {0.f, 0.f, 0.f, 0.f};
-        float4 argbo = make_float4(0.f, 0.f, 0.f, 0.f);
+        float acc[14];  // d_mean 3, d_scale 3, d_quat 4, d_rgbo 4
+#pragma unroll
+        for (int c = 0; c < 14; ++c) acc[c] = 0.f;
         if (in && accumulate) {
-            am[0] = d_means[3 * i], am[1] = d_means[3 * i + 1], am[2] = d_means[3 * i + 2];
-            as[0] = d_scales[3 * i], as[1] = d_scales[3 * i + 1], as[2] = d_scales[3 * i + 2];
-            const float4 o = d_quats[i];
-            aq[0] = o.x, aq[1] = o.y, aq[2] = o.z, aq[3] = o.w;
-            argbo = d_rgbo[i];
+            acc[0] = d_means[3 * i], acc[1] = d_means[3 * i + 1], acc[2] = d_means[3 * i + 2];
+            acc[3] = d_scales[3 * i], acc[4] = d_scales[3 * i + 1], acc[5] = d_scales[3 * i + 2];
+            const float4 o = d_quats[i], r = d_rgbo[i];
+            acc[6] = o.x, acc[7] = o.y, acc[8] = o.z, acc[9] = o.w;
+            acc[10] = r.x, acc[11] = r.y, acc[12] = r.z, acc[13] = r.w;
         }
         __syncwarp();
-        uint32_t head = 0, tail = 0;
-        // an owner adds its items of the batch just processed, in queue order
-        auto drain = [&]() {
+        VbRow row = vb_load(sh, W, lane, i0, 0, total);
+        for (int b0 = 0; b0 < total; b0 += 32) {
+            const VbRow cur = row;
+            if (b0 + 32 < total) row = vb_load(sh, W, lane, i0, b0 + 32, total);  // the next batch's rows in flight
+            vb_process(sh, W, lane, i0, b0, min(32, total - b0), clear_rows, cur);
+            // an owner adds its items of the batch in item (= view) order
             uint32_t mm = W.own[lane];
             if (mm) W.own[lane] = 0u;
             while (mm) {
                 const int k = __ffs(mm) - 1;
                 mm &= mm - 1u;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) am[c] = __fadd_rn(am[c], W.out[c][k]);
-#pragma unroll
-                for (int c = 0; c < 3; ++c) as[c] = __fadd_rn(as[c], W.out[3 + c][k]);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) aq[c] = __fadd_rn(aq[c], W.out[6 + c][k]);
+                for (int c = 0; c < 14; ++c) acc[c] = __fadd_rn(acc[c], W.out[c][k]);
             }
             __syncwarp();
-        };
-        for (int v = 0; v < nv; ++v) {
-            const MvView& V = args.v[v];
-            fetch(v + VD - 1);
-            cp_async_wait<VD - 1>();  // this lane's copies of view v have landed
-            const VbRows& R = W.ring[v % VD];
-            float4 rg = make_float4(0.f, 0.f, 0.f, 0.f), gg = rg;
-            float g11 = 0.f;
-            if (in) rg = R.rg[lane], gg = R.gg[lane], g11 = R.c11[lane];
-            const bool vis = gg.x != 0.f || gg.y != 0.f || gg.z != 0.f || gg.w != 0.f || g11 != 0.f ||
-                             rg.x != 0.f || rg.y != 0.f || rg.z != 0.f || rg.w != 0.f;
-            const uint32_t bal = __ballot_sync(0xffffffffu, vis);
-            if (!bal) continue;
-            if (vis) {
-                argbo.x = __fadd_rn(argbo.x, rg.x), argbo.y = __fadd_rn(argbo.y, rg.y);
-                argbo.z = __fadd_rn(argbo.z, rg.z), argbo.w = __fadd_rn(argbo.w, rg.w);
-                const int slot = (int)((tail + (uint32_t)__popc(bal & lt)) & (VQ - 1));
-                W.qo[slot] = (uint32_t)lane | ((uint32_t)v << 8);
-                W.qd[0][slot] = gg.x, W.qd[1][slot] = gg.y, W.qd[2][slot] = gg.z, W.qd[3][slot] = gg.w;
-                W.qd[4][slot] = g11;
-                if (clear_rows) {  // the accumulators stay zero for the view's next frame
-                    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-                    __stcs(V.g8 + 2 * (size_t)i, z);
-                    __stcs(V.g8 + 2 * (size_t)i + 1, z);
-                    __stcs(V.d_c11 + i, 0.f);
-                }
-            }
-            tail += (uint32_t)__popc(bal);
-            if (tail - head >= 32u) {
-                __syncwarp();
-                vb_process(sh, W, lane, head, 32);
-                head += 32u;
-                drain();
-            }
-        }
-        cp_async_wait<0>();  // (only empty groups remain) before the ring is reused
-        if (tail != head) {
-            __syncwarp();
-            vb_process(sh, W, lane, head, (int)(tail - head));
-            drain();
         }
         if (in) {
-            d_means[3 * i] = am[0], d_means[3 * i + 1] = am[1], d_means[3 * i + 2] = am[2];
-            d_scales[3 * i] = as[0], d_scales[3 * i + 1] = as[1], d_scales[3 * i + 2] = as[2];
-            d_quats[i] = make_float4(aq[0], aq[1], aq[2], aq[3]);
-            d_rgbo[i] = argbo;
+            d_means[3 * i] = acc[0], d_means[3 * i + 1] = acc[1], d_means[3 * i + 2] = acc[2];
+            d_scales[3 * i] = acc[3], d_scales[3 * i + 1] = acc[4], d_scales[3 * i + 2] = acc[5];
+            d_quats[i] = make_float4(acc[6], acc[7], acc[8], acc[9]);
+            d_rgbo[i] = make_float4(acc[10], acc[11], acc[12], acc[13]);
         }
-        __syncwarp();  // the warp's Gaussian fields are rewritten next iteration
+        __syncwarp();  // the warp's Gaussian fields and items are rewritten next iteration
     }
+    (void)lt;
     __syncthreads();
     for (int k = threadIdx.x; k < nv * 12; k += blockDim.x) {
         const int v = k / 12, c = k - 12 * v;

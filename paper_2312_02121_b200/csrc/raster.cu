@@ -850,7 +850,8 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
     const float4* __restrict__ xydr, const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg,
     int W, int H, int tiles_x, const float* __restrict__ final_T, const int* __restrict__ n_contrib,
     const float* __restrict__ d_img, float* __restrict__ g8, float* __restrict__ d_c11,
-    const uint32_t* __restrict__ tile_order, const unsigned long long* __restrict__ meta) {
+    const uint32_t* __restrict__ tile_order, const unsigned long long* __restrict__ meta,
+    uint32_t* __restrict__ touched) {
     griddep_wait();
     // BWD_WPC warps per CTA: 4 (one CTA per tile) or 1 (one CTA per 8x8
     // quadrant: a warp that finishes frees its slot without waiting for
@@ -899,6 +900,8 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
         const int nb = hi - lo;
         if (lane < nb) {  // stage up to 32 records and their splats (independent gathers)
             const uint2 r = rec[rb + lo + lane];
+            // the splat's screen-space rows get added to: mark it for the projection backward
+            if (touched) atomicOr(touched + (r.x >> 5), 1u << (r.x & 31u));
             const float4 g = xydr[r.x];
             const float4 q = conic[r.x];
             RecStage& st = s_rec[wslot][lane];
@@ -1058,13 +1061,13 @@ int launch_raster_bwd(const uint2* ranges, const uint32_t* vals, const float* xy
 int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t* rec_count, const float* xydr4,
                           const float* conic4, const float* colors3, float3 bg, int W, int H, const float* fT,
                           const int* nc, const float* dimg, float* g8, float* d_c11, cudaStream_t s,
-                          const uint32_t* tile_order, const unsigned long long* meta) {
+                          const uint32_t* tile_order, const unsigned long long* meta, uint32_t* touched) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     if (tile_order && !meta) return set_error("raster_bwd_rec: a raster order needs the frame meta");
     launch_k(raster_bwd_rec_kernel, dim3((unsigned)(tiles_x * tiles_y * (4 / BWD_WPC))), dim3(32 * BWD_WPC), 0, s,
              ranges, rec, rec_count,
              (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H, tiles_x, fT, nc, dimg, g8, d_c11,
-             tile_order, meta);
+             tile_order, meta, touched);
     return check_launch("raster_bwd_rec_kernel");
 }
 

@@ -661,9 +661,13 @@ def frame_screen_grads(fr: Frame):
     """The screen-space gradient accumulators of a frame (after
     frame_backward(project=False)): rows (n, 8) = [d_color 3, d_opacity,
     d_mean2d 2, d_cov00, d_cov01] and d_c11 (n,) -- device views into the
-    workspace, reducible in place across ranks."""
+    workspace, reducible in place across ranks.  Every Gaussian is marked
+    touched (gs_frame_view.touched): rows changed by the caller are then all
+    read by the projection backward."""
     v = fr.view()
     base = fr.ws.data_ptr()
+    off = v.touched - base
+    fr.ws[off:off + 4 * ((fr.n + 31) // 32)].fill_(255)
     off = v.bwd_accum - base
     rows = fr.ws[off:off + 32 * fr.n].view(torch.float32).view(fr.n, 8)
     off = v.d_c11 - base

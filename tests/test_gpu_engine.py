@@ -190,6 +190,62 @@ def test_views_project_backward_equals_per_view(cuda):
         assert np.abs(a - b).max() <= 1e-4 * (np.abs(b).max() + 1e-30), k
 
 
+def test_views_project_backward_reads_caller_written_rows(cuda):
+    """The batched projection backward reads only the rows the raster
+    backward marked (gs_frame_view.touched); frame_screen_grads hands the rows
+    out for in-place changes (e.g. a sum over ranks) and marks every Gaussian,
+    so rows the caller changed or wrote -- here doubled, plus a row for an
+    off-screen Gaussian no raster backward touched -- are all read: the result
+    equals the per-view projection backward over the same rows (which treats
+    a culled Gaussian with non-zero rows as visible)."""
+    from paper_2312_02121_b200 import ops
+    g = load_golden("config0")
+    params = [torch.as_tensor(np.asarray(a, np.float32), device=cuda) for a in g["inputs"]]
+    m, s, q, o, c = params
+    n = len(m)
+    cams = []
+    for dx in (2.5, -2.5):  # the scene shifted sideways: part of it off screen
+        c0 = ops.CameraParams.of(g["camera"])
+        view = np.array(c0.view, np.float64)
+        view[0, 3] += dx
+        cams.append(ops.CameraParams(view.tolist(), c0.fx, c0.fy, c0.cx, c0.cy, c0.width, c0.height, c0.near,
+                                     c0.far))
+    rng = np.random.default_rng(7)
+    frames, saved, injected = [], [], 0
+    for cm in cams:
+        d = torch.as_tensor(rng.normal(size=(cm.height, cm.width, 3)).astype(np.float32), device=cuda)
+        fr = ops.frame_forward(*params, cm, (0.0, 0.0, 0.0), True)
+        ops.frame_backward(fr, m, s, q, c, d, project=False)
+        rows, c11 = ops.frame_screen_grads(fr)
+        # a Gaussian in front of the camera but off screen: never marked, rows zero
+        tv = fr.tensors()
+        zero = torch.nonzero((rows == 0).all(1) & (c11 == 0) & (tv["tiles"] == 0) & (tv["xydr"][:, 2] > 1.0)).flatten()
+        rows.mul_(2.0)
+        if len(zero):
+            rows[zero[0]] = torch.tensor([0.1, -0.2, 0.3, 0.05, 0.5, -0.4, 0.02, 0.01], device=cuda)
+            c11[zero[0]] = 0.03
+            injected += 1
+        frames.append(fr)
+        saved.append((rows.clone(), c11.clone()))
+    assert injected > 0
+    shape = (("d_mean", 3), ("d_scale", 3), ("d_quat", 4), ("d_rgbo", 4))
+    out = {k: torch.zeros((n, w), device=cuda) for k, w in shape}
+    d_views = torch.zeros((len(cams), 4, 4), device=cuda)
+    ops.frame_views_project_backward(frames, m, s, q, out, d_views)
+    ref = {k: torch.zeros((n, w), device=cuda) for k, w in shape}
+    for vi, (fr, (rows, c11)) in enumerate(zip(frames, saved)):
+        r2, c2 = ops.frame_screen_grads(fr)  # (the batched pass cleared them)
+        r2.copy_(rows)
+        c2.copy_(c11)
+        dv = torch.zeros((4, 4), device=cuda)
+        ops.frame_project_backward(fr, m, s, q, ref, dv, accumulate=vi > 0, vis_from_grads=True)
+        a, b = d_views[vi].cpu().double().numpy(), dv.cpu().double().numpy()
+        assert np.abs(a - b).max() <= 1e-4 * (np.abs(b).max() + 1e-30), vi
+    for k in ref:
+        a, b = out[k].cpu().double().numpy(), ref[k].cpu().double().numpy()
+        assert np.abs(a - b).max() <= 1e-4 * (np.abs(b).max() + 1e-30), k
+
+
 def test_frames_project_equals_per_view_projection(cuda):
     """gs_frames_project (every view's depth-first projection in one pass)
     then gs_frame_forward_projected per view give the per-view
