@@ -1159,6 +1159,22 @@ __global__ void __launch_bounds__(256, 4) views_project_fwd_kernel(const float* 
     for (int v = 0; v < nv; ++v) run_zero_jobs(a.v[v].zj);
     __shared__ uint32_t s_kmin[MV_MAX], s_kmax[MV_MAX];
     __shared__ uint32_t s_lo[MV_MAX][256];  // per view: the visible keys' low-byte histogram (sort.cu)
+    // per view: the camera and the output pointers in shared memory (the view
+    // loop's reads are then shared loads, not register-indexed constant loads)
+    struct Hot {
+        CamK cam;
+        float4* xydr;
+        float4* conic;
+        uint32_t* tiles;
+        uint32_t* dkeys;
+        unsigned long long* meta;
+    };
+    __shared__ Hot s_v[MV_MAX];
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        s_v[v].cam = a.v[v].cam;
+        s_v[v].xydr = a.v[v].xydr, s_v[v].conic = a.v[v].conic, s_v[v].tiles = a.v[v].tiles;
+        s_v[v].dkeys = a.v[v].dkeys, s_v[v].meta = a.v[v].meta;
+    }
     for (int v = threadIdx.x; v < MV_MAX; v += blockDim.x) s_kmin[v] = 0xFFFFFFFFu, s_kmax[v] = 0u;
     for (int k = threadIdx.x; k < MV_MAX * 256; k += blockDim.x) (&s_lo[0][0])[k] = 0u;
     __syncthreads();
@@ -1175,7 +1191,7 @@ __global__ void __launch_bounds__(256, 4) views_project_fwd_kernel(const float* 
         }
         const FwdPrep P = proj_fwd_prep(q, sx, sy, sz);
         for (int v = 0; v < nv; ++v) {
-            const MvFwdView& V = a.v[v];
+            const Hot& V = s_v[v];
             const CamK& cam = V.cam;
             uint32_t dkey = 0xFFFFFFFFu;
             if (in) {
