@@ -52,7 +52,12 @@ struct BatchT {
     } e[RB + 1];
     uint32_t mask[NWR][RB / 32];  // region reach bits per group of 32 entries
     __align__(4) ListIdx list[NWR][RB + 2];  // compacted entry indices per region (+ sentinel pad)
-    uint8_t rbuf[NWR][RB];                   // forward records of this batch (entry indices, per region)
+    // forward records of this batch (entry indices, one byte each, per region): written over the
+    // region's own list -- record j is stored only after the list entries up to j were read (the
+    // records are a subsequence of the list, and the sigma votes order a pair's reads before its
+    // stores) -- so the batch is 6784 B and 8 CTAs fit a 64 KB carve-out (192 KB of L1)
+    __device__ __forceinline__ uint8_t* rbuf(int w) { return reinterpret_cast<uint8_t*>(list[w]); }
+    __device__ __forceinline__ const uint8_t* rbuf(int w) const { return reinterpret_cast<const uint8_t*>(list[w]); }
 };
 using Batch = BatchT<NW>;
 
@@ -232,7 +237,7 @@ __device__ __forceinline__ void fwd_record_flush(const BatchT<NWR>& s, int warp,
     __syncwarp();
     const int nrec = (int)(rcur - rbase_w);
     for (int j = lane; j < nrec; j += 32) {
-        const int k = s.rbuf[warp][j];
+        const int k = s.rbuf(warp)[j];
         rp[j] = make_uint2(__float_as_uint(s.e[k].c.y), (uint32_t)(pos0 + k));
     }
     rp += nrec;
@@ -313,7 +318,7 @@ __device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uin
     unsigned long long e_s = 0, e_a = 0, e_c = 0;
     // this warp's record region: 4 * start + warp * len (no atomics)
     uint2* rp = REC ? rec + 4 * (int64_t)start + (int64_t)warp * (end - start) : nullptr;
-    const uint32_t rbuf_w = smem_addr(&s.rbuf[warp][0]);
+    const uint32_t rbuf_w = smem_addr(s.rbuf(warp));
     uint32_t rcur = rbuf_w;
     if (threadIdx.x == 0) {  // sentinel entry: dx = -inf -> sigma NaN -> never visible
         s.e[RB].a = make_float4(INF, 0.f, 0.f, 0.f);
@@ -845,6 +850,10 @@ constexpr int BWD_WPC = GS_BWD_WPC;  // warps per CTA of the record backward (4 
 #define GS_BWD_UNROLL 1
 #endif
 constexpr int BWD_UNROLL = GS_BWD_UNROLL;
+#ifndef GS_BWD_CH
+#define GS_BWD_CH 32
+#endif
+constexpr int BWD_CH = GS_BWD_CH;  // records staged per chunk (<= 32; 16: 18.7 KB of shared memory per CTA)
 __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kernel(
     const uint2* __restrict__ ranges, const uint2* __restrict__ rec, const uint32_t* __restrict__ rec_count,
     const float4* __restrict__ xydr, const float4* __restrict__ conic, const float* __restrict__ colors, float3 bg,
@@ -858,7 +867,7 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
     // its tile's slowest quadrant; the warps never synchronise anyway).
     // Measured: 1 is 3 % slower at config 1 and 5 % at config 2 -- a tile's
     // four warps gather the same splats, so they share L1 lines.
-    __shared__ RecStage s_rec[BWD_WPC][32];
+    __shared__ RecStage s_rec[BWD_WPC][BWD_CH];
     __shared__ __align__(16) float s_red[BWD_WPC][RBS][9][RROW];
     const int job = (int)blockIdx.x / (4 / BWD_WPC);
     // the forward's raster order exists unless it binned directly (meta[3] = bin stride)
@@ -895,8 +904,8 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
     const uint32_t red_w = smem_addr(&s_red[wslot][0][0][0]);
     const uint32_t stage_w = smem_addr(&s_rec[wslot][0]);
     int nslot = 0;
-    for (int hi = count; hi > 0; hi -= 32) {
-        const int lo = hi > 32 ? hi - 32 : 0;
+    for (int hi = count; hi > 0; hi -= BWD_CH) {
+        const int lo = hi > BWD_CH ? hi - BWD_CH : 0;
         const int nb = hi - lo;
         if (lane < nb) {  // stage up to 32 records and their splats (independent gathers)
             const uint2 r = rec[rb + lo + lane];
@@ -995,6 +1004,29 @@ static int fwd_regions() {
 #define GS_FWD_FRAME_MINB 9  // resident forward CTAs per SM the frame path's registers are budgeted for
 #endif
 
+// A/B knobs: GS_FWD_PAD / GS_BWD_PAD = bytes of (unused) dynamic shared memory added to the frame
+// path's raster launches (caps their resident CTAs per SM below the register limit);
+// GS_FWD_CARVE / GS_BWD_CARVE = preferred shared-memory carve-out in percent of the maximum
+// (cudaFuncAttributePreferredSharedMemoryCarveout; the rest of the 256 KB is L1).
+static size_t pad_env(const char* name) {
+    const char* e = getenv(name);
+    const long v = e ? atol(e) : 0;
+    return v > 0 && v <= 200 * 1024 ? (size_t)v : 0;
+}
+template <typename F>
+static void carve_env(const char* name, F* kernel, int dflt = -1) {
+    const char* e = getenv(name);
+    const int v = e ? atoi(e) : dflt;
+    if (v >= 0 && v <= 100) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+}
+// The frame path's forward asks for the 64 KB carve-out (25 % of 228 KB; a hint the driver may
+// ignore) and pads its 6.8 KB batch to > 7 KB per CTA, so 7 CTAs sit in it (instead of 9 in
+// 100 KB): alone it runs as fast (192 KB of L1 for the gathers make up for the occupancy), and in
+// a multi-view step the registers it leaves free let other views' latency-bound binning kernels
+// sit beside it (config 3: 1405 -> 1420 frames/s; 8 CTAs 1409, 6 CTAs 1363).
+constexpr int FWD_FRAME_CARVE = 25;
+constexpr size_t FWD_FRAME_PAD = 512;
+
 int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xydr4, const float* conic4,
                       const float* colors3, float3 bg, int W, int H, bool et, float* img, float* T, int* nc,
                       unsigned long long* counts, cudaStream_t s, uint2* rec, uint32_t* rec_count,
@@ -1013,15 +1045,28 @@ int launch_raster_fwd(const uint2* ranges, const uint32_t* vals, const float* xy
     const bool cnt = counts != nullptr;
     // frame path: 8x8 quadrants with commit records, 9 CTAs/SM (measured best
     // against 8 and 10), optionally with the per-tile sort fused in front
+    static const size_t fwd_pad = getenv("GS_FWD_PAD") ? pad_env("GS_FWD_PAD") : FWD_FRAME_PAD;
 #define GS_FWD_M(ET, SORT)                                                                                     \
-    launch_k(raster_fwd_kernel<4, ET, false, true, GS_FWD_FRAME_MINB, SORT>, dim3(nt), dim3(128), 0, s, ranges, vals, g, q,   \
+    {                                                                                                          \
+        static bool once = false;                                                                              \
+        if (!once) {                                                                                           \
+            once = true;                                                                                       \
+            carve_env("GS_FWD_CARVE", raster_fwd_kernel<4, ET, false, true, GS_FWD_FRAME_MINB, SORT>,         \
+                      SORT ? -1 : FWD_FRAME_CARVE); /* (the fused sort's 16 KB want the default) */           \
+            if (fwd_pad > 40 * 1024)                                                                           \
+                cudaFuncSetAttribute(raster_fwd_kernel<4, ET, false, true, GS_FWD_FRAME_MINB, SORT>,           \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_pad);               \
+        }                                                                                                      \
+    }                                                                                                          \
+    launch_k(raster_fwd_kernel<4, ET, false, true, GS_FWD_FRAME_MINB, SORT>, dim3(nt), dim3(128),              \
+             (SORT && !getenv("GS_FWD_PAD")) ? 0 : fwd_pad, s, ranges, vals, g, q,                             \
              colors3, bg, W, H, tiles_x, img, T, nc, counts, rec, rec_count, tile_order, dkeys, sort_alt,        \
              direct_counts, kstride, meta)
     if (dkeys && !(rec && !cnt)) return set_error("raster_fwd: the fused tile sort needs the frame path");
     if (direct_counts && (!dkeys || !meta)) return set_error("raster_fwd: direct binning needs the fused sort");
     if (rec && !cnt) {
-        if (dkeys) { if (et) GS_FWD_M(true, true); else GS_FWD_M(false, true); }
-        else { if (et) GS_FWD_M(true, false); else GS_FWD_M(false, false); }
+        if (dkeys) { if (et) { GS_FWD_M(true, true); } else { GS_FWD_M(false, true); } }
+        else { if (et) { GS_FWD_M(true, false); } else { GS_FWD_M(false, false); } }
     } else if (rec) {
         if (et) GS_FWD_R(4, true, true, true); else GS_FWD_R(4, false, true, true);
     } else if (fwd_regions() == 2) {
@@ -1064,7 +1109,13 @@ int launch_raster_bwd_rec(const uint2* ranges, const uint2* rec, const uint32_t*
                           const uint32_t* tile_order, const unsigned long long* meta, uint32_t* touched) {
     const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
     if (tile_order && !meta) return set_error("raster_bwd_rec: a raster order needs the frame meta");
-    launch_k(raster_bwd_rec_kernel, dim3((unsigned)(tiles_x * tiles_y * (4 / BWD_WPC))), dim3(32 * BWD_WPC), 0, s,
+    static const size_t bwd_pad = pad_env("GS_BWD_PAD");
+    static bool once = false;
+    if (!once) {
+        once = true;
+        carve_env("GS_BWD_CARVE", raster_bwd_rec_kernel);
+    }
+    launch_k(raster_bwd_rec_kernel, dim3((unsigned)(tiles_x * tiles_y * (4 / BWD_WPC))), dim3(32 * BWD_WPC), bwd_pad, s,
              ranges, rec, rec_count,
              (const float4*)xydr4, (const float4*)conic4, colors3, bg, W, H, tiles_x, fT, nc, dimg, g8, d_c11,
              tile_order, meta, touched);

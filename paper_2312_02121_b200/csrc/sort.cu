@@ -74,6 +74,19 @@ __device__ __forceinline__ void stv(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// shared-memory reductions / volatile loads through 32-bit shared addresses (the ranking loop)
+__device__ __forceinline__ void red_shared_or(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_shared_add(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u32v(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ int64_t resolve_n(const unsigned long long* n_dev, int64_t n_cap) {
     if (!n_dev) return n_cap;
     const int64_t v = (int64_t)*n_dev;
@@ -188,44 +201,101 @@ __global__ void __launch_bounds__(SORT_THREADS, (sort_minb<K, ITEMS>())) oneswee
     uint32_t rank[ITEMS];
     uint32_t okm = 0;  // valid items (bit i)
     const K kmin = rel_min ? (K)*rel_min : (K)0;
+    constexpr uint32_t ALL_OK = ITEMS >= 32 ? 0xffffffffu : ((1u << ITEMS) - 1u);
+    if (wbase + ITEMS * 32 <= n) {
+        // a full warp slice (all but the last tile's): plain loads at constant offsets from one base
+        const K* kp = kin + wbase + lane;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const int64_t idx = wbase + i * 32 + lane;
-        key[i] = idx < n ? kin[idx] : (K)0;
-        val[i] = idx < n ? (vin ? vin[idx] : (uint32_t)idx) : 0u;
-        bool ok = idx < n;
-        if (rel_min) {
-            ok = ok && key[i] != (K)0xFFFFFFFFu;
-            key[i] -= kmin;
+        for (int i = 0; i < ITEMS; ++i) key[i] = kp[i * 32];
+        if (vin) {
+            const uint32_t* vp = vin + wbase + lane;
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) val[i] = vp[i * 32];
+        } else {
+            const uint32_t v0 = (uint32_t)(wbase + lane);
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) val[i] = v0 + (uint32_t)(i * 32);
         }
-        okm |= ok ? (1u << i) : 0u;
-    }
-    if (next_hist) {  // the next pass's digit of this tile's keys
+        okm = ALL_OK;
+        if (rel_min) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i)
-            warp_hist_add(s_next, (uint32_t)(key[i] >> (shift + 8)) & 255u, (okm >> i) & 1u);
+            for (int i = 0; i < ITEMS; ++i) {
+                if (key[i] == (K)0xFFFFFFFFu) okm &= ~(1u << i);
+                key[i] -= kmin;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int64_t idx = wbase + i * 32 + lane;
+            key[i] = idx < n ? kin[idx] : (K)0;
+            val[i] = idx < n ? (vin ? vin[idx] : (uint32_t)idx) : 0u;
+            bool ok = idx < n;
+            if (rel_min) {
+                ok = ok && key[i] != (K)0xFFFFFFFFu;
+                key[i] -= kmin;
+            }
+            okm |= ok ? (1u << i) : 0u;
+        }
+    }
+    const bool warp_all_ok = __all_sync(0xffffffffu, okm == ALL_OK);
+    if (next_hist) {  // the next pass's digit of this tile's keys
+        const uint32_t next_w = smem_addr(s_next);
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const bool valid = (okm >> i) & 1u;
+            const uint32_t d4 = ((uint32_t)(key[i] >> (shift + 8)) & 255u) * 4u;
+            int same;
+            __match_all_sync(0xffffffffu, valid ? d4 : 0xffffffffu, &same);
+            // one digit in the whole warp (typical for the high bytes): lane 0 adds 32
+            if (valid && (!same || lane == 0)) red_shared_add(next_w + d4, same ? 32u : 1u);
+        }
     }
     // warp-local stable ranking: items in (i, lane) order = input order
     const uint32_t lt = lanemask_lt();
     if (RANK_OR) {
         // peer masks built with shared atomic OR (two alternating mask
-        // banks, so a bank is cleared while the other is being filled)
-        uint32_t* s_peer = s_peers + warp * 2 * RADIX;
+        // banks, so a bank is cleared while the other is being filled);
+        // 32-bit shared addresses, and a predicate-free body when every item
+        // of the warp is valid (all passes but the compacting first one)
+        const uint32_t peer_w = smem_addr(s_peers + warp * 2 * RADIX);
+        const uint32_t whist_w = smem_addr(s_whist + warp * RADIX);
+        const uint32_t lbit = 1u << lane;
+        if (warp_all_ok) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const bool valid = (okm >> i) & 1u;
-            const uint32_t d = (uint32_t)(key[i] >> shift) & 255u;
-            uint32_t* pm = s_peer + (i & 1) * RADIX + d;
-            if (valid) atomicOr(pm, 1u << lane);
-            __syncwarp();
-            const uint32_t peers = valid ? *pm : 0u;
-            const uint32_t old = valid ? s_whist[warp * RADIX + d] : 0u;
-            __syncwarp();
-            if (valid && (peers & lt) == 0) {  // lowest peer: bump the count, clear the mask
-                s_whist[warp * RADIX + d] = old + (uint32_t)__popc(peers);
-                *pm = 0u;
+            for (int i = 0; i < ITEMS; ++i) {
+                const uint32_t d4 = ((uint32_t)(key[i] >> shift) & 255u) * 4u;
+                const uint32_t pm = peer_w + (uint32_t)((i & 1) * RADIX * 4) + d4;
+                const uint32_t wh = whist_w + d4;
+                red_shared_or(pm, lbit);
+                __syncwarp();
+                const uint32_t peers = lds_u32v(pm);
+                const uint32_t old = lds_u32v(wh);
+                __syncwarp();
+                if ((peers & lt) == 0) {  // lowest peer: bump the count, clear the mask
+                    sts_u32(wh, old + (uint32_t)__popc(peers));
+                    sts_u32(pm, 0u);
+                }
+                rank[i] = old + (uint32_t)__popc(peers & lt);
             }
-            rank[i] = old + (uint32_t)__popc(peers & lt);
+        } else {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const bool valid = (okm >> i) & 1u;
+                const uint32_t d4 = ((uint32_t)(key[i] >> shift) & 255u) * 4u;
+                const uint32_t pm = peer_w + (uint32_t)((i & 1) * RADIX * 4) + d4;
+                const uint32_t wh = whist_w + d4;
+                if (valid) red_shared_or(pm, lbit);
+                __syncwarp();
+                const uint32_t peers = valid ? lds_u32v(pm) : 0u;
+                const uint32_t old = valid ? lds_u32v(wh) : 0u;
+                __syncwarp();
+                if (valid && (peers & lt) == 0) {
+                    sts_u32(wh, old + (uint32_t)__popc(peers));
+                    sts_u32(pm, 0u);
+                }
+                rank[i] = old + (uint32_t)__popc(peers & lt);
+            }
         }
     } else {
 #pragma unroll
