@@ -1,6 +1,5 @@
 #!/bin/bash
-# Round-2g A/B (config 3): shared-memory carve-out preferences of the raster kernels; the backward with
-# 16-record staging chunks (_ab/ch16: 18.6 KB per CTA, 8 CTAs in a 164 KB carve-out).
+# Round-2g A/B (config 3): forward register budget (7 / 8 CTAs per SM: 72 / 64 registers) and entry-pair loop unrolled by 2.
 mkdir -p gpurun_out
 run() {  # name, env...
   n=$1; shift
@@ -10,13 +9,6 @@ run() {  # name, env...
 }
 rm -f gpurun_out/g_*.json gpurun_out/g_*.err
 run cur A=1
-run fc25 GS_FWD_CARVE=25
-run fc25_7 GS_FWD_CARVE=25 GS_FWD_PAD=512
-run fc25_6 GS_FWD_CARVE=25 GS_FWD_PAD=2000
-run fc25_5 GS_FWD_CARVE=25 GS_FWD_PAD=4400
-run ch16 GS_LIB_PATH=_ab/ch16/libsplat_b200.so
-run ch16_bc72 GS_LIB_PATH=_ab/ch16/libsplat_b200.so GS_BWD_CARVE=72
-run ch16_bc58 GS_LIB_PATH=_ab/ch16/libsplat_b200.so GS_BWD_CARVE=58
-run ch16_bc72_fc25_7 GS_LIB_PATH=_ab/ch16/libsplat_b200.so GS_BWD_CARVE=72 GS_FWD_CARVE=25 GS_FWD_PAD=512
-run bc58 GS_BWD_CARVE=58
+for v in fm7 fm8 fu2 fm7u2; do run $v GS_LIB_PATH=_ab/$v/libsplat_b200.so; done
+run fm7_nopad GS_LIB_PATH=_ab/fm7/libsplat_b200.so GS_FWD_PAD=0
 python tools/show_bench.py gpurun_out/g_*.json
