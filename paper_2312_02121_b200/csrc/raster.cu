@@ -37,6 +37,14 @@ constexpr int NW = 4;    // warps (quadrants, forward)
 #define GS_FWD_UNROLL 1  // unrolling of the forward's entry-pair loop (A/B knob)
 #endif
 constexpr int FWD_UNROLL = GS_FWD_UNROLL;
+#ifndef GS_FWD_DONE_EVERY
+// Entry pairs between the forward's "whole warp retired" votes (a power of two).  1 = after every
+// pair, unconditionally: measured best at config 3 (raster forward 6.57 ms per step; every 2nd /
+// 4th / 8th pair 6.67 / 6.70 / 6.72 -- most warps leave their list early, and late exits cost more
+// than the votes; the earlier vote guarded by "some pixel passed the sigma cut" 6.78).
+#define GS_FWD_DONE_EVERY 1
+#endif
+constexpr int FWD_DONE_EVERY = GS_FWD_DONE_EVERY;
 #ifndef GS_RB
 #define GS_RB 128
 #endif
@@ -364,7 +372,11 @@ __device__ __noinline__ void raster_fwd_body(BatchT<NWR>& s, int tile, const uin
                     fwd_commit<ET, COUNT>(p[0], SG1, v10, v11, s.e[k1].b, s.e[k1].c.x, pos_base + k1, e_a, e_c);
                     if (REC) fwd_record(rcur, k1);
                 }
-                if (ET && (b0m | b1m) && __all_sync(0xffffffffu, p[0].done == 3u)) break;
+                // all pixels retired: leave the batch.  Voted on every FWD_DONE_EVERY-th pair only -- a
+                // retired pixel's PY is +inf, so the pairs evaluated before the vote fires commit nothing
+                if (ET && (i & (2 * FWD_DONE_EVERY - 2)) == (2 * FWD_DONE_EVERY - 2) &&
+                    __all_sync(0xffffffffu, p[0].done == 3u))
+                    break;
             }
             if (REC) fwd_record_flush(s, warp, lane, rcur, rbuf_w, rp, pos_base - 1);
         } else {

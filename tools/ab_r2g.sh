@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2g A/B (config 3): forward register budget (7 / 8 CTAs per SM: 72 / 64 registers) and entry-pair loop unrolled by 2.
+# Round-2g A/B (config 3): pairs between the forward's "whole warp retired" votes (_ab/de1, de2, de4, de8).
 mkdir -p gpurun_out
 run() {  # name, env...
   n=$1; shift
@@ -8,7 +8,7 @@ run() {  # name, env...
   done
 }
 rm -f gpurun_out/g_*.json gpurun_out/g_*.err
-run cur A=1
-for v in fm7 fm8 fu2 fm7u2; do run $v GS_LIB_PATH=_ab/$v/libsplat_b200.so; done
-run fm7_nopad GS_LIB_PATH=_ab/fm7/libsplat_b200.so GS_FWD_PAD=0
+GS_LIB_PATH=_ab/de4/libsplat_b200.so python -m pytest tests/test_gpu_frame.py tests/test_gpu_frame_parity.py tests/test_gpu_golden.py -m gpu -x -q 2>&1 | tail -2
+run base GS_LIB_PATH=_ab/base2/libsplat_b200.so
+for v in de1 de2 de4 de8; do run $v GS_LIB_PATH=_ab/$v/libsplat_b200.so; done
 python tools/show_bench.py gpurun_out/g_*.json
