@@ -859,8 +859,11 @@ __device__ __forceinline__ void bwd_flush(uint32_t red, int nslot, int lane, flo
 #define GS_BWD_WPC 4
 #endif
 constexpr int BWD_WPC = GS_BWD_WPC;  // warps per CTA of the record backward (4 or 1)
+// resident record-backward CTAs per SM the registers are budgeted for: 7 (68 registers, nothing
+// spilled or rematerialised) measured a little faster than 8 (64) -- config 3 raster backward
+// 8.69 -> 8.63 ms per step and 1453 -> 1457 frames/s, config 1 +0.6 %, configs 2 / 4 +-0.2 %
 #ifndef GS_BWD_MINB
-#define GS_BWD_MINB (32 / GS_BWD_WPC)
+#define GS_BWD_MINB (GS_BWD_WPC == 4 ? 7 : 32)
 #endif
 #ifndef GS_BWD_UNROLL
 #define GS_BWD_UNROLL 1
