@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2g A/B (config 3): forward with a producer warp and a two-batch ring (GS_FWD_WS=1).
+# Round-2g A/B (config 3): record backward with each record's staged loads issued a record ahead (_ab/pre1).
 mkdir -p gpurun_out
 run() {  # name, env...
   n=$1; shift
@@ -8,8 +8,7 @@ run() {  # name, env...
   done
 }
 rm -f gpurun_out/g_*.json gpurun_out/g_*.err
-GS_FWD_WS=1 timeout 900 python -m pytest tests/test_gpu_frame.py tests/test_gpu_frame_parity.py tests/test_gpu_engine.py tests/test_gpu_configs.py -m gpu -x -q 2>&1 | tail -5
+GS_LIB_PATH=_ab/pre1/libsplat_b200.so timeout 900 python -m pytest tests/test_gpu_frame.py tests/test_gpu_frame_parity.py -m gpu -x -q 2>&1 | tail -2
 run cur A=1
-run ws GS_FWD_WS=1
-run ws_nopad GS_FWD_WS=1 GS_FWD_CARVE=-1
+run pre1 GS_LIB_PATH=_ab/pre1/libsplat_b200.so
 python tools/show_bench.py gpurun_out/g_*.json
