@@ -566,6 +566,15 @@ def run_ours(args):
         roof["duration_source"] = ("single-stream instrumented replay of the step (CUDA events on the launching "
                                    "stream); in-step interval: the timed region's events around each view's launch")
     roof["traffic"] = traffic.get(dom)
+    # per-stage DRAM bytes of ONE launch from the committed ncu --set full capture of a config-3 engine
+    # step (profiles/ncu_traffic.json; depth_sort: one onesweep pass; tile_counts / tile_emit: their
+    # kernels of one view): a stage whose traffic is far below its byte model runs out of L2
+    if cfg == 3:
+        for name, key in (("project", "project"), ("depth_sort", "sort_u32"), ("tile_counts", "tile_counts"),
+                          ("tile_emit", "tile_emit"), ("raster_fwd", "raster_fwd"), ("raster_bwd", "raster_bwd"),
+                          ("project_bwd", "project_bwd")):
+            if name in st and key in traffic:
+                st[name]["ncu_dram_bytes_per_launch"] = traffic[key]
     roof["algorithmic_work_per_launch"] = work[dom][1] / nv
     roof["duration_ms_per_launch"] = round(float(stage_ms[stage_names.index(dom)]) / nv, 4)
 
