@@ -609,9 +609,20 @@ def run_ours(args):
         # over one raster wave), raster fwd | raster bwd, project bwd, view reduce
         # (depth-first: + the depth histogram, the view reduce; depth passes skipped on the
         # device beyond the key width still launch)
-        "gpu_launches": int(args.steps * (len(cams) * (6 if direct else (8 if fused else 9) if seg else
-                                                       13 + tp + tile_order_launches(cams[0])) +
-                                          (0 if world == 1 else 2 if band else 2 * len(reducer.bounds)))),
+        # depth-first, per view: init + project (none when the projections are batched: views_init +
+        # views_project_fwd once per step), 4 depth passes, then either the tile-sorted emission
+        # (expansion, column sums, tile scan incl. the raster order, column scan, placement) or
+        # fused scan + emission, tp tile passes, ranges (+ tile order); raster fwd, raster bwd;
+        # project bwd + view reduce (batched: views_project_bwd + views_reduce once per step).
+        # Config 3 (batched, tile-sorted emission): 11 per view + 4 per step = 356, the launch
+        # list of profiles/*_config3_launches.txt
+        "gpu_launches": int(args.steps * (
+            len(cams) * (6 if direct else (8 if fused else 9) if seg else
+                         (0 if batched_fwd else 2) + 4 +
+                         (5 if tile_emit else 2 + tp + tile_order_launches(cams[0])) + 2 +
+                         (0 if batched else 2)) +
+            (0 if direct or seg else (2 if batched_fwd else 0) + (2 if batched else 0)) +
+            (0 if world == 1 else 2 if band else 2 * len(reducer.bounds)))),
         "binning": binning,
         "roofline": roof,
         "stages": st,
