@@ -933,7 +933,7 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
     for (int hi = count; hi > 0; hi -= BWD_CH) {
         const int lo = hi > BWD_CH ? hi - BWD_CH : 0;
         const int nb = hi - lo;
-        if (lane < nb) {  // stage up to 32 records and their splats (independent gathers)
+        if (lane < nb) {  // stage up to BWD_CH records and their splats (independent gathers)
             const uint2 r = rec[rb + lo + lane];
             // the splat's screen-space rows get added to: mark it for the projection backward
             if (touched) atomicOr(touched + (r.x >> 5), 1u << (r.x & 31u));
