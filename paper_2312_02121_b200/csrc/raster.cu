@@ -814,8 +814,10 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
 #ifndef GS_BWD_V4
 #define GS_BWD_V4 0
 #endif
+// ids: 0 = each slot's splat id rides in the padding word of its first row; otherwise the shared
+// address of slot 0's staged record id, slot k's one record (REC_BYTES) below it (GS_BWD_IDS).
 __device__ __forceinline__ void bwd_flush(uint32_t red, int nslot, int lane, float* __restrict__ g8,
-                                          float* __restrict__ d_c11) {
+                                          float* __restrict__ d_c11, uint32_t ids = 0u) {
     const int k = lane / 9, t = lane - 9 * k;
     float sum = 0.f;
     if (lane < 9 * nslot) {
@@ -841,7 +843,7 @@ __device__ __forceinline__ void bwd_flush(uint32_t red, int nslot, int lane, flo
     const float s2v = __shfl_down_sync(0xffffffffu, sum, 2);
     const float s3 = __shfl_down_sync(0xffffffffu, sum, 3);
     if (lane < 9 * nslot && (t == 0 || t == 4 || t == 8)) {
-        const uint32_t id = lds_u32(red + (uint32_t)k * (9 * RROW * 4) + 32 * 4);
+        const uint32_t id = lds_u32(ids ? ids - (uint32_t)k * REC_BYTES : red + (uint32_t)k * (9 * RROW * 4) + 32 * 4);
         if (t == 8)
             atomicAdd(d_c11 + id, sum);
         else
@@ -849,7 +851,7 @@ __device__ __forceinline__ void bwd_flush(uint32_t red, int nslot, int lane, flo
     }
 #else
     if (lane < 9 * nslot) {
-        const uint32_t id = lds_u32(red + (uint32_t)k * (9 * RROW * 4) + 32 * 4);
+        const uint32_t id = lds_u32(ids ? ids - (uint32_t)k * REC_BYTES : red + (uint32_t)k * (9 * RROW * 4) + 32 * 4);
         atomicAdd(t < 8 ? g8 + 8 * (size_t)id + t : d_c11 + id, sum);
     }
 #endif
@@ -875,6 +877,12 @@ constexpr int BWD_WPC = GS_BWD_WPC;  // warps per CTA of the record backward (4 
 // (0 restores the counted loop, whose 2x / 4x unrolling gave 9.00).
 #ifndef GS_BWD_G3
 #define GS_BWD_G3 1
+#endif
+// Grouped loop: the flush takes each slot's splat id from the staged record (a group never leaves its
+// chunk) instead of a copy lane 0 parks in the row padding per record: config 3 raster backward
+// 8.63 -> 8.42 ms per step, 1457 -> 1472 frames/s (0: the parked copy, which the counted loop needs).
+#ifndef GS_BWD_IDS
+#define GS_BWD_IDS 1
 #endif
 #ifndef GS_BWD_CH
 #define GS_BWD_CH (GS_BWD_G3 ? 30 : 32)
@@ -930,6 +938,7 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
     const uint32_t red_w = smem_addr(&s_red[wslot][0][0][0]);
     const uint32_t stage_w = smem_addr(&s_rec[wslot][0]);
     int nslot = 0;
+    [[maybe_unused]] uint32_t tail_ids = 0u;
     for (int hi = count; hi > 0; hi -= BWD_CH) {
         const int lo = hi > BWD_CH ? hi - BWD_CH : 0;
         const int nb = hi - lo;
@@ -987,7 +996,9 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
                                 MY1,          mul2(MY0, Y0), mul2(MY0, Y1), mul2(MY1, Y1)};
 #pragma unroll
             for (int u = 0; u < 9; ++u) sts_f32(slot + u * (RROW * 4), lo2(D[u]) + hi2(D[u]));
+#if !(GS_BWD_G3 && GS_BWD_IDS)
             if (lane == 0) sts_u32(slot + 32 * 4, __float_as_uint(cq.z));  // splat id -> row padding
+#endif
             SDOT = fma2(WC, CDOT, SDOT);
             T = sel2(c0, c1, TH, T);
         };
@@ -999,9 +1010,11 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
 #pragma unroll
             for (int j = 0; j < RBS; ++j) record(k - j, red_w + (uint32_t)j * (9 * RROW * 4) + 4 * lane);
             __syncwarp();
-            bwd_flush(red_w, RBS, lane, g8, d_c11);
+            // (a group never leaves its chunk: the flush reads the ids from the staged records)
+            bwd_flush(red_w, RBS, lane, g8, d_c11, GS_BWD_IDS ? stage_w + (uint32_t)k * REC_BYTES + 40u : 0u);
             __syncwarp();
         }
+        if (k >= 0) tail_ids = stage_w + (uint32_t)k * REC_BYTES + 40u;  // (last chunk: stays staged)
         for (; k >= 0; --k) {
             record(k, red_w + (uint32_t)nslot * (9 * RROW * 4) + 4 * lane);
             ++nslot;
@@ -1022,7 +1035,7 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
     }
     if (nslot) {
         __syncwarp();
-        bwd_flush(red_w, nslot, lane, g8, d_c11);
+        bwd_flush(red_w, nslot, lane, g8, d_c11, (GS_BWD_G3 && GS_BWD_IDS) ? tail_ids : 0u);
     }
 }
 
