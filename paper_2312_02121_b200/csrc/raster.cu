@@ -884,6 +884,12 @@ constexpr int BWD_WPC = GS_BWD_WPC;  // warps per CTA of the record backward (4 
 #ifndef GS_BWD_IDS
 #define GS_BWD_IDS 1
 #endif
+// Alpha zeroed for the pixels a record does not contribute to, instead of selects on the weight and on
+// T (rcp.approx.ftz(1.0) is exactly 1.0 -- checked on the device, tools/ab_r2g.sh -- so T * 1 keeps T
+// bit for bit): config 3 raster backward 8.42 -> 8.17 ms per step, 1472 -> 1488 frames/s.
+#ifndef GS_BWD_AZ
+#define GS_BWD_AZ 1
+#endif
 #ifndef GS_BWD_CH
 #define GS_BWD_CH (GS_BWD_G3 ? 30 : 32)
 #endif
@@ -977,12 +983,22 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
             const bool c1 = pos < nc[1] && hi2(SG) <= SIGMA_CUT && al1 >= ALPHA_MIN;
             // no vote: ~98 % of records contribute to some pixel of the warp;
             // a record that does not adds zero rows (WC = DAL = 0, T kept)
+#if GS_BWD_AZ
+            // a pixel the record does not contribute to gets alpha 0: 1 - alpha = 1, its reciprocal
+            // (rcp.approx of 1.0) is exactly 1, so TH = T, the weight is 0 and neither needs a select
+            const f32x2 AL = pk2(c0 ? al0 : 0.f, c1 ? al1 : 0.f);
+            const f32x2 OM = sub2(bc2(1.f), AL);
+            const f32x2 INV = pk2(rcp_approx(lo2(OM)), rcp_approx(hi2(OM)));
+            const f32x2 TH = mul2(T, INV);
+            const f32x2 WC = mul2(AL, TH);
+#else
             const f32x2 AL = pk2(al0, al1);
             const f32x2 OM = sub2(bc2(1.f), AL);
             const f32x2 INV = pk2(rcp_approx(lo2(OM)), rcp_approx(hi2(OM)));
             const f32x2 TH = mul2(T, INV);
             const f32x2 Wt = mul2(AL, TH);
             const f32x2 WC = pk2(c0 ? lo2(Wt) : 0.f, c1 ? hi2(Wt) : 0.f);
+#endif
             const f32x2 CDOT = fma2(bc2(blue), G2, fma2(bc2(bq.w), G1, mul2(bc2(bq.z), G0)));
             const f32x2 DA = sub2(mul2(TH, CDOT), mul2(INV, SDOT));
             const bool l0 = c0 && lo2(ARAW) < ALPHA_MAX, l1 = c1 && hi2(ARAW) < ALPHA_MAX;
@@ -1000,7 +1016,11 @@ __global__ void __launch_bounds__(32 * BWD_WPC, GS_BWD_MINB) raster_bwd_rec_kern
             if (lane == 0) sts_u32(slot + 32 * 4, __float_as_uint(cq.z));  // splat id -> row padding
 #endif
             SDOT = fma2(WC, CDOT, SDOT);
+#if GS_BWD_AZ
+            T = TH;
+#else
             T = sel2(c0, c1, TH, T);
+#endif
         };
 #if GS_BWD_G3
         // groups of RBS records with compile-time slots and an unconditional flush (a chunk

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2g A/B (config 3): the grouped record backward's flush reading the splat ids from the staged records (_ab/ids1).
+# Round-2g A/B (config 3): record backward with alpha zeroed for non-contributing pixels (_ab/az1; needs rcp.approx(1.0) == 1.0).
 mkdir -p gpurun_out
 run() {  # name, env...
   n=$1; shift
@@ -8,7 +8,8 @@ run() {  # name, env...
   done
 }
 rm -f gpurun_out/g_*.json gpurun_out/g_*.err
-GS_LIB_PATH=_ab/ids1/libsplat_b200.so timeout 900 python -m pytest tests/test_gpu_frame.py tests/test_gpu_frame_parity.py tests/test_gpu_engine.py -m gpu -x -q 2>&1 | tail -2
+[ -x tools/bin/rcp1 ] && tools/bin/rcp1  # nvcc -gencode arch=compute_100a,code=sm_100a -o tools/bin/rcp1 tools/src/rcp1.cu
+GS_LIB_PATH=_ab/az1/libsplat_b200.so timeout 900 python -m pytest tests/test_gpu_frame.py tests/test_gpu_frame_parity.py tests/test_gpu_engine.py tests/test_gpu_golden.py -m gpu -x -q 2>&1 | tail -2
 run cur A=1
-run ids1 GS_LIB_PATH=_ab/ids1/libsplat_b200.so
+run az1 GS_LIB_PATH=_ab/az1/libsplat_b200.so
 python tools/show_bench.py gpurun_out/g_*.json
